@@ -1,0 +1,266 @@
+"""Generate tests/golden/*.npz from the UNMODIFIED reference (oracle/_ref, built from /root/reference).
+
+Run in the build container only (the GPU box has no /root/reference):
+    python tests/golden/make_golden.py
+The fixtures are committed; tests never regenerate them.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+import oracle  # noqa: E402
+from oracle import AdamConfig, Config, MlpConfig, Ref  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+U64 = 2**64 - 1
+
+
+def points(ref: Ref, n: int, count: int, seed: int) -> np.ndarray:
+    """count x n points: reference-RNG uniforms + hand-picked boundary / tie cases."""
+    x = ref.rng_doubles(seed, n, count * n).reshape(count, n)
+    special = [np.zeros(n), np.ones(n), np.full(n, 0.5), np.full(n, np.nextafter(1.0, 0.0)),
+               np.array([1.0 if i % 2 == 0 else 0.0 for i in range(n)]),
+               np.array([0.999999999 if i == 0 else 1.0 for i in range(n)]),
+               np.full(n, 0.25), np.array([(i + 1) / (n + 1) for i in range(n)])]
+    for i, s in enumerate(special):
+        x[i] = s
+    return x
+
+
+def vertex_lists(ref: Ref, cfg: Config, x: np.ndarray):
+    """(idx, w, count) per (sample, level) recovered through the public API: a features=1 encoder and a
+    ones upstream make EncoderGradient hold the interpolation weights in first-touch (= chain) order."""
+    c1 = Config(**{**cfg.__dict__, "features": 1})
+    enc = ref.encoder(c1)
+    V = cfg.vertices
+    N = x.shape[0]
+    idx = np.zeros((N, cfg.levels, V), dtype=np.uint32)
+    w = np.zeros((N, cfg.levels, V), dtype=np.float64)
+    cnt = np.zeros((N, cfg.levels), dtype=np.uint8)
+    up = np.ones((1, cfg.levels))
+    for s in range(N):
+        _, _, order, bad, st = enc.encode_backward(x[s:s + 1], up)
+        assert st == 0 and bad == -1
+        lib = ref.lib
+        # re-read values in touch order
+        g = lib.sxr_grad_create(c1.levels, c1.table_size, 1)
+        import ctypes as C
+        b = C.c_long(-1)
+        xs = np.ascontiguousarray(x[s:s + 1])
+        lib.sxr_encode_backward(enc.h, xs.ctypes.data_as(C.POINTER(C.c_double)),
+                                up.ctypes.data_as(C.POINTER(C.c_double)), 1, g, C.byref(b))
+        for l in range(cfg.levels):
+            k = lib.sxr_grad_touched_count(g, l)
+            ii = np.empty(k, dtype=np.uint32)
+            vv = np.empty(k, dtype=np.float64)
+            lib.sxr_grad_read(g, l, ii.ctypes.data_as(C.POINTER(C.c_uint32)), vv.ctypes.data_as(C.POINTER(C.c_double)))
+            idx[s, l, :k] = ii
+            w[s, l, :k] = vv
+            cnt[s, l] = k
+        lib.sxr_grad_destroy(g)
+    return idx, w, cnt
+
+
+def sparse_grad(order, grad):
+    """Flatten the reference's per-level touch lists: (level, row) pairs + slices."""
+    lv, rows, vals = [], [], []
+    for l, idx in enumerate(order):
+        lv.append(np.full(idx.size, l, dtype=np.int32))
+        rows.append(idx.astype(np.uint32))
+        vals.append(grad[l, idx])
+    return np.concatenate(lv), np.concatenate(rows), np.concatenate(vals)
+
+
+def encode_cases(ref: Ref):
+    cases = {}
+    specs = []
+    for backend in (oracle.BACKEND_SIMPLEX, oracle.BACKEND_GRID):
+        for n in range(1, 8):  # reference test_encoding.cpp:224-251 sweep (small_config, 3 levels)
+            specs.append((f"small_b{backend}_n{n}", Config(dim=n, levels=3, table_size=1 << 10, features=2,
+                                                           base_resolution=4, growth=2.0, backend=backend), 40, 77))
+    specs += [
+        ("c2_n3", Config(dim=3, levels=16, table_size=1 << 19, features=2, base_resolution=16, growth=1.5), 96, 42),
+        ("c3_n2", Config(dim=2, levels=16, table_size=1 << 19, features=2, base_resolution=16, growth=2.0), 96, 42),
+        ("c1_n2", Config(dim=2, levels=16, table_size=1 << 19, features=2, base_resolution=16,
+                         growth=(2048 / 16) ** (1 / 15)), 64, 42),
+        ("eqmem_n3", Config(dim=3, levels=6, table_size=1 << 14, features=4, base_resolution=8, growth=1.7,
+                            level_scale=oracle.SCALE_EQUAL_MEMORY), 48, 5),
+        ("f1_n4", Config(dim=4, levels=5, table_size=1 << 12, features=1, base_resolution=3, growth=1.9), 48, 6),
+        ("f8_n2", Config(dim=2, levels=4, table_size=1 << 12, features=8, base_resolution=16, growth=2.0), 48, 7),
+        ("f3_n5", Config(dim=5, levels=3, table_size=1 << 11, features=3, base_resolution=5, growth=1.5), 48, 8),
+        ("n8", Config(dim=8, levels=2, table_size=1 << 13, features=2, base_resolution=4, growth=2.0), 32, 9),
+    ]
+    for name, cfg, count, seed in specs:
+        assert ref.validate(cfg) == 0, name
+        enc = ref.encoder(cfg)
+        enc.init_tables(seed)
+        x = points(ref, cfg.dim, count, 1000 + seed)
+        feats, bad, st = enc.encode(x)
+        assert st == 0 and bad == -1
+        enc.reset_counters()
+        enc.encode(x)
+        touched_cnt, oob_cnt = enc.counters()
+        idx, w, cnt = vertex_lists(ref, cfg, x)
+        up = ref.rng_doubles(7, 2, count * cfg.encoded_width, -1.0, 1.0).reshape(count, -1) * 1e-3
+        grad, touched, order, bad, st = enc.encode_backward(x, up)
+        assert st == 0
+        lv, rows, vals = sparse_grad(order, grad)
+        res = np.array([enc.resolution(l) for l in range(cfg.levels)], dtype=np.uint32)
+        cases[name] = dict(
+            cfg=np.array([cfg.dim, cfg.levels, cfg.table_size, cfg.features, cfg.base_resolution, cfg.backend,
+                          cfg.level_scale], dtype=np.int64), growth=np.float64(cfg.growth), seed=np.uint64(seed),
+            res=res, x=x, features=feats, idx=idx, w=w, cnt=cnt, upstream=up, g_level=lv, g_row=rows, g_val=vals,
+            counters=np.array([touched_cnt, oob_cnt], dtype=np.uint64),
+            table_head=np.stack([enc.table(l)[:8].copy() for l in range(cfg.levels)]))
+    flat = {}
+    for name, d in cases.items():
+        for k, v in d.items():
+            flat[f"{name}/{k}"] = v
+    flat["names"] = np.array(list(cases.keys()))
+    np.savez_compressed(os.path.join(OUT, "encode_cases.npz"), **flat)
+    print("encode_cases:", len(cases), "cases")
+
+
+def scalar_cases(ref: Ref):
+    d = {}
+    zs = np.array([0, 1, 42, 1234, U64, 0x9e3779b97f4a7c15, 2**63], dtype=np.uint64)
+    d["mix64_in"] = zs
+    d["mix64_out"] = np.array([ref.mix64(int(z)) for z in zs], dtype=np.uint64)
+    d["hash_combine_out"] = np.array([ref.hash_combine(int(a), int(b)) for a in zs for b in zs[:4]], dtype=np.uint64)
+    d["rng_1234_0_u64"] = ref.rng_u64(1234, 0, 16)
+    d["rng_99_u64"] = ref.rng_u64(99, None, 16)
+    d["rng_99_double"] = ref.rng_doubles(99, None, 16)
+    d["rng_7_2_ranged"] = ref.rng_doubles(7, 2, 16, -1.0, 1.0)
+    d["skew"] = np.stack([ref.skew_constants(n) for n in range(1, 9)])
+    d["eqmem"] = np.array([ref.equal_memory_multiplier(n) for n in range(1, 9)])
+    # hash: reference test_encoding.cpp:47-59 protocol (coords in [-1e6, 1e6))
+    coords, hashes = [], []
+    draws = ref.rng_u64(21, None, 8 * 64 * 8)
+    k = 0
+    for n in range(1, 9):
+        for _ in range(64):
+            c = np.array([int(draws[k + i] % 2000000) - 1000000 for i in range(n)] + [0] * (8 - n), dtype=np.int64)
+            k += n
+            coords.append(c)
+            hashes.append(ref.hash_coords(c[:n]))
+    d["hash_coords_in"] = np.stack(coords)
+    d["hash_coords_n"] = np.repeat(np.arange(1, 9), 64).astype(np.int32)
+    d["hash_coords_out"] = np.array(hashes, dtype=np.uint32)
+    # subdivide / barycentric on random + tie inputs
+    fr_all, perm_all, srt_all, w_all, n_all = [], [], [], [], []
+    for n in range(1, 9):
+        fr = ref.rng_doubles(13, n, 32 * n).reshape(32, n)
+        fr[0] = 0.5
+        fr[1] = 0.0
+        if n > 1:
+            fr[2, 1] = fr[2, 0]
+        for f in fr:
+            perm, srt = ref.subdivide(f)
+            w = ref.barycentric(srt)
+            fr_all.append(np.pad(f, (0, 8 - n)))
+            perm_all.append(np.pad(perm, (0, 8 - n)))
+            srt_all.append(np.pad(srt, (0, 8 - n)))
+            w_all.append(np.pad(w, (0, 8 - n)))
+            n_all.append(n)
+    d["sub_fracs"], d["sub_perm"], d["sub_sorted"], d["sub_w"], d["sub_n"] = map(
+        np.array, (fr_all, perm_all, srt_all, w_all, n_all))
+    # resolution ladders
+    ladders = {
+        "res_b16_g1.5": Config(dim=3, levels=16, base_resolution=16, growth=1.5, table_size=1 << 19),
+        "res_b16_g2": Config(dim=2, levels=16, base_resolution=16, growth=2.0, table_size=1 << 19),
+        "res_eqmem_n2": Config(dim=2, levels=10, base_resolution=16, growth=1.6, level_scale=oracle.SCALE_EQUAL_MEMORY),
+        "res_eqmem_n5": Config(dim=5, levels=10, base_resolution=7, growth=1.37, level_scale=oracle.SCALE_EQUAL_MEMORY),
+        "res_grid_eqmem": Config(dim=3, levels=6, base_resolution=16, growth=1.5, backend=oracle.BACKEND_GRID,
+                                 level_scale=oracle.SCALE_EQUAL_MEMORY),
+    }
+    for k_, cfg in ladders.items():
+        d[k_] = np.array([ref.level_resolution(cfg, l) for l in range(cfg.levels)], dtype=np.uint32)
+    np.savez_compressed(os.path.join(OUT, "scalar_cases.npz"), **d)
+    print("scalar_cases written")
+
+
+def neural_cases(ref: Ref):
+    d = {}
+    mc = MlpConfig(32, 64, 2, 3)
+    mlp = ref.mlp(mc)
+    seed = ref.hash_combine(42, 1)
+    mlp.init(seed)
+    d["mlp_seed"] = np.uint64(seed)
+    d["mlp_params"] = mlp.params().copy()
+    inp = (ref.rng_doubles(31, 0, 24 * 32, -1.0, 1.0).reshape(24, 32)).astype(np.float32)
+    up = ref.rng_doubles(31, 1, 24 * 3, -1.0, 1.0).reshape(24, 3)
+    out, grad, ig = mlp.forward_backward(inp, up)
+    d["mlp_in"], d["mlp_up"], d["mlp_out"], d["mlp_grad"], d["mlp_input_grad"] = inp, up, out, grad, ig
+    # second shape: 0 hidden layers and 1 hidden layer, odd widths
+    for tag, mc2 in (("h0", MlpConfig(5, 7, 0, 2)), ("h1", MlpConfig(6, 9, 1, 1))):
+        m2 = ref.mlp(mc2)
+        m2.init(11)
+        i2 = ref.rng_doubles(32, 0, 8 * mc2.input_width, -2.0, 2.0).reshape(8, -1).astype(np.float32)
+        u2 = ref.rng_doubles(32, 1, 8 * mc2.output_width, -1.0, 1.0).reshape(8, -1)
+        o2, g2, ig2 = m2.forward_backward(i2, u2)
+        d[f"mlp_{tag}_params"], d[f"mlp_{tag}_in"], d[f"mlp_{tag}_up"] = m2.params().copy(), i2, u2
+        d[f"mlp_{tag}_out"], d[f"mlp_{tag}_grad"], d[f"mlp_{tag}_input_grad"] = o2, g2, ig2
+
+    # dense Adam: 5 steps on 16 params
+    import ctypes as C
+    lib = ref.lib
+    ac = AdamConfig(lr=1e-2, beta1=0.9, beta2=0.99, epsilon=1e-15)
+    p = ref.rng_doubles(33, 0, 16, -1.0, 1.0).astype(np.float32)
+    d["adam_p0"] = p.copy()
+    st = lib.sxr_adam_create(16)
+    gs, ps = [], []
+    for t in range(5):
+        g = ref.rng_doubles(33, 10 + t, 16, -1.0, 1.0)
+        if t == 2:
+            g[3] = 0.0
+        cac = ac.c()
+        assert lib.sxr_adam_step(st, p.ctypes.data_as(C.POINTER(C.c_float)), g.ctypes.data_as(C.POINTER(C.c_double)), 16,
+                                 C.byref(cac)) == 0
+        gs.append(g)
+        ps.append(p.copy())
+    lib.sxr_adam_destroy(st)
+    d["adam_g"], d["adam_p"] = np.stack(gs), np.stack(ps)
+
+    # full train_field on a tiny problem, 1 thread and 3 threads (reference src/trainer.cpp:53)
+    cfg = Config(dim=2, levels=4, table_size=1 << 10, features=2, base_resolution=4, growth=2.0)
+    mc3 = MlpConfig(8, 16, 2, 3)
+    steps, batch = 12, 64
+    coords = ref.rng_doubles(1234, 5, steps * batch * 2).reshape(steps, batch, 2)
+    targets = 0.5 + 0.5 * np.sin(6.0 * coords[..., :1] + np.array([0.0, 1.0, 2.0])) * np.cos(4.0 * coords[..., 1:2])
+    targets = np.ascontiguousarray(targets)
+    d["train_cfg"] = np.array([cfg.dim, cfg.levels, cfg.table_size, cfg.features, cfg.base_resolution], dtype=np.int64)
+    d["train_mlp"] = np.array([8, 16, 2, 3], dtype=np.int64)
+    d["train_coords"], d["train_targets"] = coords, targets
+    tadam, madam = AdamConfig(lr=1e-2), AdamConfig(lr=1e-3)
+    for threads in (1, 3):
+        enc = ref.encoder(cfg)
+        enc.init_tables(42)
+        mlp3 = ref.mlp(mc3)
+        mlp3.init(ref.hash_combine(42, 1))
+        loss = np.zeros(steps)
+        ta, ma = tadam.c(), madam.c()
+        stt = lib.sxr_train_field(enc.h, mlp3.h, coords.ctypes.data_as(C.POINTER(C.c_double)),
+                                  targets.ctypes.data_as(C.POINTER(C.c_double)), steps, batch, threads, C.byref(ta),
+                                  C.byref(ma), loss.ctypes.data_as(C.POINTER(C.c_double)))
+        assert stt == 0, ref.lib.sxr_last_error()
+        d[f"train_loss_t{threads}"] = loss
+        d[f"train_tables_t{threads}"] = enc.tables()
+        d[f"train_mlp_params_t{threads}"] = mlp3.params().copy()
+    np.savez_compressed(os.path.join(OUT, "neural_cases.npz"), **d)
+    print("neural_cases written; loss t1:", d["train_loss_t1"][:3], "...", d["train_loss_t1"][-1])
+
+
+if __name__ == "__main__":
+    oracle.build(ref=True)
+    ref = Ref()
+    scalar_cases(ref)
+    encode_cases(ref)
+    neural_cases(ref)
+    for f in sorted(os.listdir(OUT)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(OUT, f)) // 1024, "KiB")

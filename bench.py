@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""bench.py -- simplex-encode forward+backward throughput on B200 (BASELINE.json metric, configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--dim 3] [--path fused|split]
+
+One "step" = HashEncoder::encode + encode_backward over one batch of 2^20 synthetic samples per GPU
+(n=3, L=16, F=2, T=2^19, base 16, growth 1.5; coords CounterRng(99,1), upstream CounterRng(7,2)*1e-3,
+tables init_tables(42) -- SURVEY.md 8d).  Prints ONE JSON line (rank 0).
+
+  value     samples/s, inputs resident in HBM, CUDA-event timed, max over ranks
+  e2e       the same metric through the host-buffer C-ABI call (pinned host memory in, features out)
+  roofline  dominant kernel's algorithmic bytes / its CUDA-event duration vs MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the reference's own encode+encode_backward (oracle/_ref) on this box's host cores, bounded sample
+
+--impl reference times the unmodified reference CPU implementation (oracle/_ref, else the oracle port) instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "simplex_encode_fwd_bwd_samples_per_s"
+UNIT = "samples/s"
+L, F, T_LOG2, BASE = 16, 2, 19, 16
+GROWTH = {2: 2.0, 3: 1.5}
+BATCH_LOG2 = 20
+
+
+def alg_bytes(n: int, mode: str) -> int:
+    """SURVEY.md 8d payload accounting per sample (f32 coords/features/upstream/grads, scatter-add = read+write)."""
+    fwd = 4 * n + 4 * L * F * (n + 1) + 4 * L * F
+    bwd = 4 * n + 4 * L * F + 8 * L * F * (n + 1)
+    return {"fwd": fwd, "bwd": bwd, "fused": fwd + bwd}[mode]
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            return float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def workload_name(n: int) -> str:
+    return (f"{n}D simplex encode fwd+bwd microbench, L={L} F={F} T=2^{T_LOG2} base={BASE} growth={GROWTH[n]}, "
+            f"2^{BATCH_LOG2} uniform random samples per GPU")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons DURING the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.idx)], stdout=open(self.path, "w"),
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.proc is None:
+            return out
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        try:
+            for line in open(self.path):
+                p = [c.strip() for c in line.split(",")]
+                if len(p) < 9:
+                    continue
+                try:
+                    sm.append(float(p[1]))
+                    mx.append(float(p[2]))
+                except ValueError:
+                    continue
+                for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), p[5:9]):
+                    if val.lower().startswith("active"):
+                        reasons.add(name)
+            os.unlink(self.path)
+        except Exception:
+            pass
+        if sm:
+            out.update(sm_mhz=statistics.median(sm), sm_max_mhz=max(mx), reasons=sorted(reasons), samples=len(sm))
+        return out
+
+
+def traffic_for(kernel_key: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture (profiles/traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(p)).get(kernel_key)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------------------------- reference arm
+def cpu_reference_run(n: int, samples: int, threads: int):
+    """Times the reference's encode + encode_backward worker pattern on `samples` samples. Returns (samples/s, kind)."""
+    import numpy as np
+
+    import oracle
+    cfg = oracle.Config(dim=n, levels=L, table_size=1 << T_LOG2, features=F, base_resolution=BASE, growth=GROWTH[n])
+    o = oracle.Oracle()
+    x = o.rng_doubles(99, 1, samples * n).reshape(samples, n)
+    up = o.rng_doubles(7, 2, samples * L * F, -1e-3, 1e-3).reshape(samples, L * F)
+    if oracle.Ref.available():
+        ref = oracle.Ref()
+        enc = ref.encoder(cfg)
+        enc.init_tables(42)
+        secs = enc.bench_fwd_bwd(x, up, threads)
+        kind = "reference"
+    else:
+        tables = o.init_tables(cfg, 42)
+        secs = o.bench_fwd_bwd(cfg, tables, x, up, threads)
+        kind = "port"
+    if secs <= 0:
+        raise RuntimeError("CPU baseline failed")
+    return samples / secs, kind
+
+
+def host_threads() -> int:
+    cores = os.cpu_count() or 1
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        pass
+    # every worker owns a dense fp64 accumulator (128 MiB at T=2^19) + seen maps, as the reference does
+    try:
+        import psutil
+        by_mem = int(psutil.virtual_memory().available // (220 << 20))
+        cores = max(1, min(cores, by_mem))
+    except Exception:
+        pass
+    return cores
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n = args.dim
+    threads = host_threads()
+    samples = min(1 << BATCH_LOG2, threads << 16)
+    vals = []
+    kind = "reference"
+    for i in range(args.warmup + args.steps):
+        v, kind = cpu_reference_run(n, samples, threads)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.mean(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * samples / value, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(n), "dim": n, "levels": L, "features": F, "table_size_log2": T_LOG2,
+                   "note": "CPU reference arm: unmodified reference sources (oracle/_ref) on host cores only"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{samples} samples per step (same RNG streams as the GPU arm), "
+                                   f"encode+encode_backward per worker chunk, steady_clock"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+
+    import paper_2311_15439_b200 as sx
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available() or sx.device_count() < 1:
+        raise SystemExit("bench.py: no sm_100 CUDA device -- the GPU arm has no CPU fallback")
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+
+    n = args.dim
+    N = 1 << BATCH_LOG2
+    LF = L * F
+    dev = torch.device(f"cuda:{local_rank}")
+    cfg = sx.EncoderConfig(dim=n, levels=L, table_size=1 << T_LOG2, features=F, base_resolution=BASE, growth=GROWTH[n])
+    enc = sx.HashEncoder(cfg, device=local_rank)
+    enc.init_tables(42)
+    tune = sx.Tuning(levels_per_thread=args.lpt, block_threads=args.block, level_major=args.level_major,
+                     exact_blend=args.exact, warp_aggregate=args.aggregate)
+    enc.set_tuning(tune)
+    grad = sx.EncoderGradient(enc)
+
+    # Rotating input sets larger than L2 in total (126 MB): each set is coords 12 MB + upstream 128 MB + out 128 MB.
+    n_sets = 4
+    xs, ups, outs = [], [], []
+    for i in range(n_sets):
+        x = torch.empty((N, n), dtype=torch.float32, device=dev)
+        # rank r, set i draws its own slice of the reference bench stream CounterRng(99, 1)
+        r = sx.CounterRng(99, 1)
+        r.counter = (rank * n_sets + i) * N * n
+        r.fill_device(x)
+        up = torch.empty((N, LF), dtype=torch.float32, device=dev)
+        r2 = sx.CounterRng(7, 2)
+        r2.counter = (rank * n_sets + i) * N * LF
+        r2.fill_device(up, -1e-3, 1e-3)
+        xs.append(x)
+        ups.append(up)
+        outs.append(torch.empty((N, LF), dtype=torch.float32, device=dev))
+    gview = grad.device_view()
+    stream = torch.cuda.current_stream()
+
+    def step(i, ev=None):
+        k = i % n_sets
+        if args.path == "fused":
+            enc.encode_forward_backward(xs[k], ups[k], grad, out=outs[k])
+            if ev is not None:
+                ev[1].record(stream)
+        else:
+            enc.encode(xs[k], out=outs[k])
+            if ev is not None:
+                ev[0].record(stream)
+            enc.encode_backward(xs[k], ups[k], grad)
+            if ev is not None:
+                ev[1].record(stream)
+        if dist is not None and not args.no_allreduce:
+            dist.all_reduce(gview)  # table-gradient exchange of the batch-sharded step
+
+    for i in range(args.warmup):
+        step(i)
+    grad.clear(stream.cuda_stream)  # accumulator zeroed outside the timed region
+    torch.cuda.synchronize()
+    enc.check()
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    sampler = ClockSampler(local_rank)
+    if rank == 0:
+        sampler.start()
+    launches0 = sx.launch_count()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(args.steps):
+        evs[i][2].record(stream)
+        step(i, evs[i])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    launches = sx.launch_count() - launches0
+    clocks = sampler.stop() if rank == 0 else None
+    enc.check()
+    total_ms = t_start.elapsed_time(t_end)
+    if dist is not None:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * N / (ms_per_step * 1e-3)
+
+    # dominant kernel duration, live, from events on the launching stream
+    if args.path == "fused":
+        kms = statistics.mean(e[2].elapsed_time(e[1]) for e in evs)
+        dom, dom_bytes = "encode_fwd_bwd_fused", alg_bytes(n, "fused")
+        parts = {"fused_ms": kms}
+    else:
+        fwd_ms = statistics.mean(e[2].elapsed_time(e[0]) for e in evs)
+        bwd_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+        kms, dom, dom_bytes = bwd_ms, "encode_backward", alg_bytes(n, "bwd")
+        parts = {"fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
+                 "fwd_frac_of_hbm": alg_bytes(n, "fwd") * N / (fwd_ms * 1e-3) / 1e9 / hbm_peak()[0]}
+    peak, peak_src = hbm_peak()
+    achieved = dom_bytes * N / (kms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic_for(f"{dom}_n{n}"), "peak_source": peak_src,
+                "alg_bytes_per_sample": dom_bytes, "kernel_ms": kms, **parts}
+
+    line = None
+    if rank == 0:
+        # ---- e2e: the host-buffer C-ABI call, pinned host memory, H2D + D2H inside the timed region
+        import ctypes as C
+
+        import numpy as np
+        lib = sx.lib
+
+        def pinned(shape, dtype):
+            nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+            p = C.c_void_p()
+            assert lib.sxen_host_alloc(nbytes, C.byref(p)) == 0, lib.sxen_last_error()
+            buf = (C.c_char * nbytes).from_address(p.value)
+            return np.frombuffer(buf, dtype=dtype).reshape(shape), p
+
+        hx, px = pinned((N, n), np.float64)
+        hup, pup = pinned((N, LF), np.float32)
+        hout, pout = pinned((N, LF), np.float32)
+        hx[:] = xs[0].double().cpu().numpy()
+        hup[:] = ups[0].cpu().numpy()
+        e2e_steps = max(3, min(args.steps, 10))
+        for _ in range(2):
+            enc.encode_forward_backward(hx, hup, grad, out=hout)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            enc.encode_forward_backward(hx, hup, grad, out=hout)
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        e2e = {"value": N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(hx.nbytes + hup.nbytes),
+               "d2h_bytes_per_step": int(hout.nbytes), "ms_per_step": e2e_s * 1e3, "n_gpus": 1,
+               "call": "sxen_encoder_encode_forward_backward_host (x f64, upstream f32, features f32; pinned host buffers)"}
+        # spot parity of the e2e result against the device path
+        assert np.array_equal(hout[:4096], outs[0][:4096].cpu().numpy()) or args.exact == 0
+        for p in (px, pup, pout):
+            lib.sxen_host_free(p)
+
+        # ---- CPU baseline on this box's host cores (bounded sample), N=1 only
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            try:
+                threads = host_threads()
+                samples = min(1 << 18, threads << 15)
+                v, kind = cpu_reference_run(n, samples, threads)
+                cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
+                       "sample": f"{samples} samples of the same workload (same RNG streams), reference worker pattern: "
+                                 f"encode+encode_backward per contiguous chunk into a per-thread accumulator"}
+            except Exception as exc:  # the GPU numbers stand on their own; say why the baseline is missing
+                cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": str(exc)}
+
+        t = enc.tuning()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64 lattice math / u32 hash / f32 features+grads", "data": "synthetic",
+            "config": {"workload": workload_name(n), "dim": n, "levels": L, "features": F, "table_size_log2": T_LOG2,
+                       "base_resolution": BASE, "growth": GROWTH[n], "samples_per_gpu_per_step": N,
+                       "coords": "f32 on device (CounterRng(99,1))", "path": args.path,
+                       "l2_policy": f"inputs larger than L2: {n_sets} rotating sets x 268 MB + 64 MiB tables + 64 MiB grads",
+                       "tuning": {"levels_per_thread": t.levels_per_thread, "block_threads": t.block_threads,
+                                  "level_major": t.level_major, "exact_blend": t.exact_blend,
+                                  "warp_aggregate": t.warp_aggregate},
+                       "multi_gpu": "batch sharded, tables replicated, NCCL all-reduce of the 64 MiB table-gradient "
+                                    "buffer per step" if world > 1 and not args.no_allreduce else "single GPU"},
+            "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu,
+        }
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--dim", type=int, default=3, choices=[2, 3])
+    ap.add_argument("--path", choices=["fused", "split"], default="fused")
+    ap.add_argument("--lpt", type=int, default=0)
+    ap.add_argument("--block", type=int, default=0)
+    ap.add_argument("--level-major", type=int, default=0)
+    ap.add_argument("--exact", type=int, default=1)
+    ap.add_argument("--aggregate", type=int, default=0)
+    ap.add_argument("--no-allreduce", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,235 @@
+/*
+ * sxen_cuda.h -- C ABI of the B200-native simplex multiresolution hash encoder (libsxen_b200.so).
+ *
+ * This is the drop-in boundary for ONE hot path of the reference (arXiv 2311.15439 "sxen"):
+ * HashEncoder::encode / encode_backward, the tiny MLP head, the Adam updates and the train step
+ * that strings them together.  The reference has no FFI layer of its own; each entry point below is
+ * the BATCHED form of the reference C++ call it replaces, cited as file:line under
+ * /root/reference/proj/.  Plain pointers and sizes only -- no C++ or torch types.
+ *
+ * Conventions
+ *  - Every function returns sxen_status and never throws.  On failure sxen_last_error() (thread
+ *    local) holds the message.  The status values map 1:1 onto the exception types the reference
+ *    throws (include/sxen/errors.hpp:8-15; std::invalid_argument / std::logic_error).
+ *  - Handles are opaque and own device memory on ONE device.  Pointer arguments named *_dev are
+ *    caller-owned device memory, never retained after the call's stream work completes; *_host are
+ *    caller-owned host memory.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).  Device-pointer
+ *    entry points are asynchronous and stream-ordered; *_host entry points are synchronous.
+ *  - Layouts are the reference's: coords N x dim row-major; features / upstream N x (L*F) with
+ *    element [s*L*F + l*F + f] (src/encoding.cpp:311-313); tables L x (T*F), row-major [row][f]
+ *    (include/sxen/encoding.hpp:107,145).
+ *  - There is no CPU fallback: every entry point that computes requires an sm_100 device and
+ *    fails with SXEN_CUDA_ERROR otherwise.
+ */
+#ifndef SXEN_CUDA_H
+#define SXEN_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(_WIN32)
+#define SXEN_API __declspec(dllexport)
+#else
+#define SXEN_API __attribute__((visibility("default")))
+#endif
+
+#define SXEN_MAX_DIM 8        /* include/sxen/lattice.hpp:12  kMaxDim */
+#define SXEN_MAX_FEATURES 64  /* src/encoding.cpp:14           kMaxFeatures */
+#define SXEN_MAX_RESOLUTION (1u << 26) /* src/encoding.cpp:15  kMaxResolution */
+
+typedef enum sxen_status {
+  SXEN_OK = 0,
+  SXEN_INVALID_ARGUMENT = 1, /* std::invalid_argument (src/encoding.cpp:28-58,183-194,297-325) */
+  SXEN_LOGIC_ERROR = 2,      /* std::logic_error      (src/mlp.cpp:165-167) */
+  SXEN_TRAINING_ERROR = 3,   /* sxen::TrainingError   (src/trainer.cpp:121-123, src/optimizer.cpp:35-37,73-76) */
+  SXEN_CUDA_ERROR = 4,       /* no reference analogue: device/runtime failure */
+  SXEN_IO_ERROR = 5          /* sxen::IoError         (include/sxen/errors.hpp:8-10) */
+} sxen_status;
+
+typedef enum sxen_backend { SXEN_BACKEND_SIMPLEX = 0, SXEN_BACKEND_GRID = 1 } sxen_backend;           /* include/sxen/encoding.hpp:12 */
+typedef enum sxen_level_scale { SXEN_SCALE_RAW = 0, SXEN_SCALE_EQUAL_MEMORY = 1 } sxen_level_scale;   /* include/sxen/encoding.hpp:13 */
+typedef enum sxen_coord_type { SXEN_COORD_F64 = 0, SXEN_COORD_F32 = 1 } sxen_coord_type;
+
+/* sxen::EncoderConfig, field for field (include/sxen/encoding.hpp:18-33). */
+typedef struct sxen_encoder_config {
+  int32_t dim;             /* n, input dimension, [1, 8]            default 2 */
+  int32_t levels;          /* L >= 1                                default 8 */
+  uint32_t table_size;     /* T entries per level, power of two     default 1<<16 */
+  int32_t features;        /* F in [1, 64]                          default 2 */
+  int32_t base_resolution; /* coarsest lattice resolution >= 1      default 16 */
+  double growth;           /* per-level growth, finite, > 1         default 2.0 */
+  int32_t backend;         /* sxen_backend                          default simplex */
+  int32_t level_scale;     /* sxen_level_scale                      default raw */
+} sxen_encoder_config;
+
+/* sxen::MlpConfig (include/sxen/mlp.hpp:11-25); hidden activation is ReLU, output identity. */
+typedef struct sxen_mlp_config {
+  int32_t input_width;   /* default 32 */
+  int32_t hidden_width;  /* default 64 */
+  int32_t hidden_layers; /* default 2 */
+  int32_t output_width;  /* default 3 */
+} sxen_mlp_config;
+
+/* sxen::AdamConfig (include/sxen/optimizer.hpp:13-18). */
+typedef struct sxen_adam_config {
+  double lr;      /* default 1e-3 */
+  double beta1;   /* default 0.9 */
+  double beta2;   /* default 0.99 */
+  double epsilon; /* default 1e-15 */
+} sxen_adam_config;
+
+/* sxen::LookupCounters (include/sxen/encoding.hpp:44-47). */
+typedef struct sxen_lookup_counters {
+  uint64_t touched_vertices;
+  uint64_t out_of_bounds;
+} sxen_lookup_counters;
+
+/* Launch-shape knobs of the encode kernels (no reference analogue; 0 = library default). */
+typedef struct sxen_tuning {
+  int32_t levels_per_thread; /* 1,2,4,8,16: levels one thread walks */
+  int32_t block_threads;     /* CTA size, multiple of 32 */
+  int32_t level_major;       /* 0: consecutive threads walk one sample's level groups (coalesced rows);
+                                1: grid.y = level group, all samples of a group before the next (L2-resident tables) */
+  int32_t exact_blend;       /* 1: fp64 chain-order blend, features bit-identical to the reference; 0: fp32 FMA blend */
+  int32_t warp_aggregate;    /* backward: merge equal rows inside a warp before the atomic on levels whose
+                                lattice has at most this many vertices (0 = off) */
+  int32_t reserved[3];
+} sxen_tuning;
+
+typedef struct sxen_encoder sxen_encoder;   /* sxen::HashEncoder     (include/sxen/encoding.hpp:92-148) */
+typedef struct sxen_grad sxen_grad;         /* sxen::EncoderGradient (include/sxen/encoding.hpp:53-86) */
+typedef struct sxen_mlp sxen_mlp;           /* sxen::Mlp + MlpGradient + batched MlpWorkspace (include/sxen/mlp.hpp) */
+typedef struct sxen_sparse_adam sxen_sparse_adam; /* sxen::SparseAdamState (include/sxen/optimizer.hpp:42-59) */
+typedef struct sxen_adam sxen_adam;         /* sxen::AdamState       (include/sxen/optimizer.hpp:21-37) */
+
+/* ------------------------------------------------------------------ library */
+SXEN_API const char* sxen_last_error(void);
+SXEN_API const char* sxen_version(void);
+/* Number of visible CUDA devices with compute capability 10.x (0 when none / no driver). */
+SXEN_API int32_t sxen_device_count(void);
+/* Kernels launched by this library since load (all handles, all streams); bench.py's gpu_launches. */
+SXEN_API uint64_t sxen_launch_count(void);
+
+/* Pinned host memory for callers of the *_host entry points (pageable memory works too, but copies then serialise). */
+SXEN_API sxen_status sxen_host_alloc(size_t bytes, void** out);
+SXEN_API sxen_status sxen_host_free(void* ptr);
+
+/* ------------------------------------------------------------------ rng (include/sxen/rng.hpp:9-54), host-side */
+SXEN_API uint64_t sxen_mix64(uint64_t z);
+SXEN_API uint64_t sxen_hash_combine(uint64_t a, uint64_t b);
+/* Fills out_dev[i] = lo + (hi-lo)*next_double() for draws first_counter+i (1-based) of
+ * CounterRng(seed) (has_stream=0) or CounterRng(seed, stream_id); as f64 or f32 (rounded from the f64 value). */
+SXEN_API sxen_status sxen_rng_fill_dev(uint64_t seed, int32_t has_stream, uint64_t stream_id, uint64_t first_counter,
+                                       double lo, double hi, void* out_dev, size_t count, sxen_coord_type type,
+                                       void* stream);
+
+/* ------------------------------------------------------------------ config (src/encoding.cpp:28-82) */
+SXEN_API sxen_status sxen_encoder_config_default(sxen_encoder_config* cfg);
+SXEN_API sxen_status sxen_encoder_validate(const sxen_encoder_config* cfg);                       /* EncoderConfig::validate */
+SXEN_API sxen_status sxen_level_resolution(const sxen_encoder_config* cfg, int32_t level, uint32_t* out); /* level_resolution */
+SXEN_API sxen_status sxen_equal_memory_multiplier(int32_t dim, double* out);                      /* equal_memory_multiplier */
+/* out[0]=F_n (skew), out[1]=G_n (unskew), out[2]=S_n (scale): SkewConstants::make (src/lattice.cpp:21-30) */
+SXEN_API sxen_status sxen_skew_constants(int32_t dim, double out[3]);
+/* hash_coords (include/sxen/hashing.hpp:23-29), host-side helper */
+SXEN_API sxen_status sxen_hash_coords(const int64_t* coords, int32_t dim, uint32_t* out);
+
+/* ------------------------------------------------------------------ encoder (src/encoding.cpp:157-335) */
+/* HashEncoder::HashEncoder: validates, computes the per-level resolutions, allocates zeroed tables on `device`. */
+SXEN_API sxen_status sxen_encoder_create(const sxen_encoder_config* cfg, int32_t device, sxen_encoder** out);
+SXEN_API sxen_status sxen_encoder_destroy(sxen_encoder* enc);
+SXEN_API sxen_status sxen_encoder_get_config(const sxen_encoder* enc, sxen_encoder_config* out);
+SXEN_API sxen_status sxen_encoder_resolution(const sxen_encoder* enc, int32_t level, uint32_t* out); /* HashEncoder::resolution */
+SXEN_API sxen_status sxen_encoder_parameter_count(const sxen_encoder* enc, uint64_t* out);           /* parameter_count */
+SXEN_API sxen_status sxen_encoder_set_tuning(sxen_encoder* enc, const sxen_tuning* tuning);
+SXEN_API sxen_status sxen_encoder_get_tuning(const sxen_encoder* enc, sxen_tuning* out);
+/* HashEncoder::init_tables (src/encoding.cpp:169-176): counter RNG evaluated on the device, bit-identical. */
+SXEN_API sxen_status sxen_encoder_init_tables(sxen_encoder* enc, uint64_t seed, void* stream);
+/* HashEncoder::table(level) (include/sxen/encoding.hpp:107): T*F floats. */
+SXEN_API sxen_status sxen_encoder_upload_table(sxen_encoder* enc, int32_t level, const float* src_host);
+SXEN_API sxen_status sxen_encoder_download_table(const sxen_encoder* enc, int32_t level, float* dst_host);
+/* Device pointer of level 0; levels are contiguous, level l starts at ptr + l*T*F. */
+SXEN_API sxen_status sxen_encoder_tables_dev(sxen_encoder* enc, float** out_dev);
+
+/* HashEncoder::encode, batched (src/encoding.cpp:295-315).  x_dev: N x dim (type), out_dev: N x L*F f32. */
+SXEN_API sxen_status sxen_encoder_encode(sxen_encoder* enc, const void* x_dev, sxen_coord_type type, size_t n_samples,
+                                         float* out_dev, void* stream);
+/* Parity probe: the per-(sample, level) vertex chain the encode kernels use.
+ * idx_dev: N x L x V u32, w_dev: N x L x V f64, V = dim+1 (simplex) or 2^dim (grid). */
+SXEN_API sxen_status sxen_encoder_encode_debug(sxen_encoder* enc, const void* x_dev, sxen_coord_type type,
+                                               size_t n_samples, uint32_t* idx_dev, double* w_dev, void* stream);
+/* HashEncoder::encode_backward, batched (src/encoding.cpp:317-335).  upstream_dev: N x L*F f32. */
+SXEN_API sxen_status sxen_encoder_encode_backward(sxen_encoder* enc, const void* x_dev, sxen_coord_type type,
+                                                  const float* upstream_dev, size_t n_samples, sxen_grad* grad,
+                                                  void* stream);
+/* encode + encode_backward of the same batch in ONE kernel (one lattice walk per (sample, level));
+ * the run_chunk pair of src/trainer.cpp:31,47 when upstream does not depend on this batch's features. */
+SXEN_API sxen_status sxen_encoder_encode_forward_backward(sxen_encoder* enc, const void* x_dev, sxen_coord_type type,
+                                                          const float* upstream_dev, size_t n_samples, float* out_dev,
+                                                          sxen_grad* grad, void* stream);
+/* Synchronises `stream` and reports what the reference would have thrown for this encoder's launches since the
+ * last check: SXEN_INVALID_ARGUMENT with the first sample whose coordinate is NaN or outside [0,1]
+ * (check_input, src/encoding.cpp:183-194).  Such samples write zero features and add no gradient. */
+SXEN_API sxen_status sxen_encoder_check(sxen_encoder* enc, void* stream);
+/* HashEncoder::counters / reset_counters (include/sxen/encoding.hpp:122-128). Synchronises the device. */
+SXEN_API sxen_status sxen_encoder_counters(sxen_encoder* enc, sxen_lookup_counters* out);
+SXEN_API sxen_status sxen_encoder_reset_counters(sxen_encoder* enc);
+
+/* Host-buffer forms: the call a user of the reference makes, batched.  x_host: N x dim doubles (the reference's
+ * own coordinate type), copied to the device through pinned staging, synchronous, errors reported directly. */
+SXEN_API sxen_status sxen_encoder_encode_host(sxen_encoder* enc, const double* x_host, size_t n_samples, float* out_host);
+SXEN_API sxen_status sxen_encoder_encode_backward_host(sxen_encoder* enc, const double* x_host,
+                                                       const double* upstream_host, size_t n_samples, sxen_grad* grad);
+/* encode + encode_backward of one host batch in a single pipelined pass: chunks are copied in, run through the fused
+ * kernel and copied out on rotating streams so H2D, compute and D2H overlap.  upstream_host is N x L*F of
+ * `upstream_type` (f64 = the reference's type, narrowed on the device; f32 = half the bytes over PCIe). */
+SXEN_API sxen_status sxen_encoder_encode_forward_backward_host(sxen_encoder* enc, const double* x_host,
+                                                               const void* upstream_host, sxen_coord_type upstream_type,
+                                                               size_t n_samples, float* out_host, sxen_grad* grad);
+
+/* ------------------------------------------------------------------ gradient accumulator (src/encoding.cpp:84-137) */
+/* EncoderGradient(levels, table_size, features): dense f32 device buffer L x T x F.  "Touched" is carried in-band:
+ * an untouched row holds -0.0f in feature 0; any accumulated contribution (zeros are added as +0.0f) clears it. */
+SXEN_API sxen_status sxen_grad_create(const sxen_encoder* enc, sxen_grad** out);
+SXEN_API sxen_status sxen_grad_destroy(sxen_grad* grad);
+SXEN_API sxen_status sxen_grad_clear(sxen_grad* grad, void* stream);                 /* EncoderGradient::clear */
+SXEN_API sxen_status sxen_grad_values_dev(sxen_grad* grad, float** out_dev, size_t* count); /* for all-reduce */
+/* EncoderGradient::slice + touched for one level: values_host T*F floats (-0.0 reported as 0), touched_host T bytes. */
+SXEN_API sxen_status sxen_grad_download(const sxen_grad* grad, int32_t level, float* values_host, uint8_t* touched_host);
+/* Inverse of sxen_grad_download: overwrites one level (rows with touched_host[r]==0 become untouched). */
+SXEN_API sxen_status sxen_grad_upload(sxen_grad* grad, int32_t level, const float* values_host, const uint8_t* touched_host);
+SXEN_API sxen_status sxen_grad_touched_total(const sxen_grad* grad, uint64_t* out); /* EncoderGradient::touched_total */
+/* EncoderGradient::merge (src/encoding.cpp:122-131): dst += src, touched = union. */
+SXEN_API sxen_status sxen_grad_merge(sxen_grad* dst, const sxen_grad* src, void* stream);
+
+/* ------------------------------------------------------------------ optimizers (src/optimizer.cpp) */
+SXEN_API sxen_status sxen_adam_config_default(sxen_adam_config* cfg);
+/* SparseAdamState: fp64 moments L x T x F, global step counter. */
+SXEN_API sxen_status sxen_sparse_adam_create(const sxen_encoder* enc, sxen_sparse_adam** out);
+SXEN_API sxen_status sxen_sparse_adam_destroy(sxen_sparse_adam* opt);
+SXEN_API sxen_status sxen_sparse_adam_step_count(const sxen_sparse_adam* opt, int64_t* out);
+/* SparseAdamState::step (src/optimizer.cpp:54-84): updates only touched rows, fp64 math without FMA contraction.
+ * clear_grad != 0 resets the accumulator in the same pass.  Non-finite gradients set SXEN_TRAINING_ERROR, reported
+ * by sxen_sparse_adam_check. */
+SXEN_API sxen_status sxen_sparse_adam_step(sxen_sparse_adam* opt, sxen_encoder* enc, sxen_grad* grad,
+                                           const sxen_adam_config* cfg, int32_t clear_grad, void* stream);
+SXEN_API sxen_status sxen_sparse_adam_check(sxen_sparse_adam* opt, void* stream);
+/* Moments of one level for inspection: m_host, v_host T*F doubles. */
+SXEN_API sxen_status sxen_sparse_adam_download(const sxen_sparse_adam* opt, int32_t level, double* m_host, double* v_host);
+
+/* AdamState over a dense f32 parameter vector (src/optimizer.cpp:25-41); gradients f64 or f32 (grad_type). */
+SXEN_API sxen_status sxen_adam_create(size_t size, int32_t device, sxen_adam** out);
+SXEN_API sxen_status sxen_adam_destroy(sxen_adam* opt);
+SXEN_API sxen_status sxen_adam_step_count(const sxen_adam* opt, int64_t* out);
+SXEN_API sxen_status sxen_adam_step(sxen_adam* opt, float* params_dev, const void* grads_dev, sxen_coord_type grad_type,
+                                    size_t size, const sxen_adam_config* cfg, void* stream);
+SXEN_API sxen_status sxen_adam_check(sxen_adam* opt, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SXEN_CUDA_H */

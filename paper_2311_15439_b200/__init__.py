@@ -1,0 +1,30 @@
+"""paper_2311_15439_b200 -- B200-native simplex multiresolution hash encoding (hot path of arXiv 2311.15439).
+
+Host-side mirror of the reference's C++ interface for the encode path (names follow
+/root/reference/proj/include/sxen/*.hpp) over the C ABI in include/sxen_cuda.h.  All compute happens in
+lib/libsxen_b200.so (hand-written sm_100a kernels); importing the package without it raises ImportError.
+"""
+from . import _abi
+
+lib = _abi.load()  # raises ImportError when the CUDA extension has not been built
+
+from .errors import CudaError, IoError, TrainingError  # noqa: E402
+from .encoding import (Backend, EncoderConfig, EncoderGradient, HashEncoder, LevelScale, LookupCounters,  # noqa: E402
+                       Tuning, equal_memory_multiplier, hash_coords, level_resolution, skew_constants)
+from .optimizer import AdamConfig, AdamState, SparseAdamState  # noqa: E402
+from .rng import CounterRng, hash_combine, mix64  # noqa: E402
+
+__all__ = ["lib", "CudaError", "IoError", "TrainingError", "Backend", "LevelScale", "EncoderConfig", "HashEncoder",
+           "EncoderGradient", "LookupCounters", "Tuning", "equal_memory_multiplier", "level_resolution",
+           "skew_constants", "hash_coords", "AdamConfig", "AdamState", "SparseAdamState", "CounterRng", "mix64",
+           "hash_combine"]
+
+
+def device_count() -> int:
+    """Visible sm_100 devices."""
+    return lib.sxen_device_count()
+
+
+def launch_count() -> int:
+    """Kernels this library has launched since load."""
+    return lib.sxen_launch_count()

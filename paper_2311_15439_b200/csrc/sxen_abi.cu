@@ -1,0 +1,793 @@
+// sxen_abi.cu -- the C ABI of include/sxen_cuda.h: library, rng, config, encoder and gradient-accumulator entry
+// points.  Host code above the kernels; every entry point cites the reference call it stands in for in the header.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "sxen_common.hpp"
+#include "sxen_encode.cuh"
+
+namespace sxen_host {
+
+std::string& last_error() {
+  thread_local std::string e;
+  return e;
+}
+
+sxen_status fail(sxen_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  last_error() = buf;
+  return st;
+}
+
+sxen_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(SXEN_CUDA_ERROR, "CUDA error %d (%s) in %s", static_cast<int>(e), cudaGetErrorString(e), what);
+}
+
+std::atomic<uint64_t> g_launches{0};
+
+}  // namespace sxen_host
+
+using namespace sxen_host;
+using sxen_dev::EncodeArgs;
+using sxen_dev::EncodeLaunch;
+
+namespace {
+
+constexpr unsigned long long kNoBadSample = ~0ULL;
+constexpr uint32_t kUntouchedBits = 0x80000000u;  // -0.0f
+
+bool is_pow2(uint32_t v) { return v != 0 && (v & (v - 1)) == 0; }
+
+// src/encoding.cpp:60-66
+double equal_memory_multiplier(int n) {
+  return std::pow(static_cast<double>(n + 1), static_cast<double>(n - 1) / (2.0 * static_cast<double>(n)));
+}
+
+// src/encoding.cpp:68-82
+uint32_t level_resolution(const sxen_encoder_config& cfg, int level) {
+  double r = static_cast<double>(cfg.base_resolution) * std::pow(cfg.growth, level);
+  if (cfg.level_scale == SXEN_SCALE_EQUAL_MEMORY && cfg.backend == SXEN_BACKEND_SIMPLEX) {
+    r *= equal_memory_multiplier(cfg.dim);
+  }
+  const double floored = std::floor(r);
+  if (floored < 1.0) return 1;
+  if (floored > static_cast<double>(SXEN_MAX_RESOLUTION)) return SXEN_MAX_RESOLUTION + 1;
+  return static_cast<uint32_t>(floored);
+}
+
+// EncoderConfig::validate, src/encoding.cpp:28-58 (same order, same rejections)
+sxen_status validate(const sxen_encoder_config& c) {
+  SXEN_REQUIRE(c.dim >= 1 && c.dim <= SXEN_MAX_DIM, "encoder dim must be in [1, %d], got %d", SXEN_MAX_DIM, c.dim);
+  SXEN_REQUIRE(c.levels >= 1, "encoder levels must be >= 1, got %d", c.levels);
+  SXEN_REQUIRE(is_pow2(c.table_size), "encoder table_size must be a power of two, got %u", c.table_size);
+  SXEN_REQUIRE(c.features >= 1 && c.features <= SXEN_MAX_FEATURES, "encoder features must be in [1, %d], got %d",
+               SXEN_MAX_FEATURES, c.features);
+  SXEN_REQUIRE(c.base_resolution >= 1, "encoder base_resolution must be >= 1, got %d", c.base_resolution);
+  SXEN_REQUIRE(c.growth > 1.0 && std::isfinite(c.growth), "encoder growth must be a finite value > 1");
+  SXEN_REQUIRE(c.backend == SXEN_BACKEND_SIMPLEX || c.backend == SXEN_BACKEND_GRID, "encoder backend must be 0 or 1");
+  SXEN_REQUIRE(c.level_scale == SXEN_SCALE_RAW || c.level_scale == SXEN_SCALE_EQUAL_MEMORY,
+               "encoder level_scale must be 0 or 1");
+  const uint32_t finest = level_resolution(c, c.levels - 1);
+  SXEN_REQUIRE(finest <= SXEN_MAX_RESOLUTION,
+               "finest level resolution %u exceeds the supported maximum %u; lower levels, growth, or base_resolution",
+               finest, SXEN_MAX_RESOLUTION);
+  return SXEN_OK;
+}
+
+sxen_tuning default_tuning() {
+  sxen_tuning t{};
+  t.levels_per_thread = 2;
+  t.block_threads = 256;
+  t.level_major = 0;
+  t.exact_blend = 1;
+  t.warp_aggregate = 0;
+  return t;
+}
+
+__global__ void fill_u32_kernel(uint32_t* __restrict__ p, size_t n, uint32_t value) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) p[i] = value;
+}
+
+// init_tables, src/encoding.cpp:169-176: entry i of level l = float(-1e-4 + 2e-4 * draw(i+1) of CounterRng(seed, l))
+__global__ void init_tables_kernel(float* __restrict__ tables, size_t per_level, int levels, uint64_t seed_key,
+                                   double lo, double span) {
+  const size_t total = per_level * static_cast<size_t>(levels);
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const size_t l = i / per_level;
+    const size_t e = i - l * per_level;
+    const uint64_t key = sxen_dev::hash_combine(seed_key, static_cast<uint64_t>(l));  // CounterRng(seed, stream)
+    tables[i] = static_cast<float>(sxen_dev::rng_double(key, static_cast<uint64_t>(e) + 1, lo, span));
+  }
+}
+
+template <typename T>
+__global__ void rng_fill_kernel(T* __restrict__ out, size_t n, uint64_t key, uint64_t first, double lo, double span) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = static_cast<T>(sxen_dev::rng_double(key, first + i, lo, span));
+}
+
+// EncoderGradient::merge, src/encoding.cpp:122-131, on the in-band touched encoding: a row untouched in src leaves
+// dst alone; otherwise every feature is added (src's -0.0f in features > 0 cannot occur for a touched row).
+__global__ void grad_merge_kernel(float* __restrict__ dst, const float* __restrict__ src, size_t rows, int features) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t r = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < rows; r += stride) {
+    const float* s = src + r * features;
+    if (__float_as_uint(s[0]) == kUntouchedBits) continue;
+    float* d = dst + r * features;
+    for (int f = 0; f < features; ++f) d[f] = (d[f] + 0.0f) + s[f];  // +0.0f first: an untouched dst row becomes +0
+  }
+}
+
+__global__ void grad_touched_kernel(const float* __restrict__ v, size_t rows, int features,
+                                    unsigned long long* __restrict__ out) {
+  unsigned long long local = 0;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t r = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < rows; r += stride)
+    local += (__float_as_uint(v[r * features]) != kUntouchedBits) ? 1ULL : 0ULL;
+  for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(out, local);
+}
+
+int grid_for(size_t n, int block = 256) {
+  size_t b = (n + block - 1) / block;
+  const size_t cap = 148 * 16;  // a few waves of the 148 SMs; kernels above are grid-stride
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return static_cast<int>(b);
+}
+
+typedef cudaError_t (*encode_fn)(const EncodeLaunch&, EncodeArgs&, cudaStream_t, int*);
+typedef cudaError_t (*debug_fn)(EncodeArgs&, int, uint32_t*, double*, int, cudaStream_t);
+
+const encode_fn kEncode[8] = {sxen_dev::launch_encode_nd1, sxen_dev::launch_encode_nd2, sxen_dev::launch_encode_nd3,
+                              sxen_dev::launch_encode_nd4, sxen_dev::launch_encode_nd5, sxen_dev::launch_encode_nd6,
+                              sxen_dev::launch_encode_nd7, sxen_dev::launch_encode_nd8};
+const debug_fn kDebug[8] = {sxen_dev::launch_debug_nd1, sxen_dev::launch_debug_nd2, sxen_dev::launch_debug_nd3,
+                            sxen_dev::launch_debug_nd4, sxen_dev::launch_debug_nd5, sxen_dev::launch_debug_nd6,
+                            sxen_dev::launch_debug_nd7, sxen_dev::launch_debug_nd8};
+
+int ptr_vec(const void* p) {
+  const uintptr_t u = reinterpret_cast<uintptr_t>(p);
+  return (u % 16 == 0) ? 4 : (u % 8 == 0) ? 2 : 1;
+}
+
+// Fills the launch-invariant part of the argument block.
+void base_args(const sxen_encoder* enc, const void* x, sxen_coord_type type, size_t n, EncodeArgs& a) {
+  std::memset(&a, 0, sizeof(a));
+  a.x = x;
+  a.tables = enc->tables;
+  a.status = enc->status;
+  a.n_samples = n;
+  a.level_stride = enc->level_floats();
+  a.mask = enc->cfg.table_size - 1u;
+  a.row_width = enc->cfg.levels * enc->cfg.features;
+  a.features = enc->cfg.features;
+  a.coord_f32 = type == SXEN_COORD_F32 ? 1 : 0;
+  a.skew = enc->skew;
+}
+
+void level_chunk(const sxen_encoder* enc, int level0, EncodeArgs& a) {
+  a.level0 = level0;
+  a.n_levels = std::min<int>(sxen_dev::kMaxLaunchLevels, enc->cfg.levels - level0);
+  a.agg_mask = 0;
+  for (int l = 0; l < sxen_dev::kMaxLaunchLevels; ++l) {
+    const bool live = l < a.n_levels;
+    const uint32_t res = live ? enc->res[static_cast<size_t>(level0 + l)] : 1u;
+    // simplex: s = N_l / S_n (src/encoding.cpp:200); grid: y = x * N_l (src/encoding.cpp:255)
+    a.geom.scale[l] = enc->cfg.backend == SXEN_BACKEND_SIMPLEX ? static_cast<double>(res) / enc->scale
+                                                               : static_cast<double>(res);
+    a.geom.res[l] = static_cast<int32_t>(res);
+    if (live && enc->tuning.warp_aggregate > 0) {
+      const double verts = std::pow(static_cast<double>(res) + 1.0, enc->cfg.dim);
+      if (verts <= static_cast<double>(enc->tuning.warp_aggregate)) a.agg_mask |= 1u << l;
+    }
+  }
+}
+
+sxen_status check_batch(const sxen_encoder* enc, const void* x, sxen_coord_type type, size_t n) {
+  SXEN_REQUIRE(enc != nullptr, "encoder handle is null");
+  SXEN_REQUIRE(type == SXEN_COORD_F64 || type == SXEN_COORD_F32, "unknown coordinate type %d", static_cast<int>(type));
+  SXEN_REQUIRE(n == 0 || x != nullptr, "coordinate pointer is null");
+  SXEN_REQUIRE(n <= (1ULL << 36), "batch of %zu samples exceeds the supported launch size", n);
+  return SXEN_OK;
+}
+
+sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, const float* upstream, size_t n,
+                       float* out, sxen_grad* grad, int mode, cudaStream_t stream) {
+  if (sxen_status st = check_batch(enc, x, type, n)) return st;
+  if (mode & sxen_dev::kModeFwd) SXEN_REQUIRE(n == 0 || out != nullptr, "encode: output pointer is null");
+  if (mode & sxen_dev::kModeBwd) {
+    SXEN_REQUIRE(n == 0 || upstream != nullptr, "encode_backward: upstream pointer is null");
+    SXEN_REQUIRE(grad != nullptr, "encode_backward: gradient accumulator is null");
+    // src/encoding.cpp:323-325
+    SXEN_REQUIRE(grad->levels == enc->cfg.levels && grad->features == enc->cfg.features &&
+                     grad->table_size == enc->cfg.table_size && grad->device == enc->device,
+                 "encode_backward: gradient accumulator shape mismatch");
+  }
+  if (n == 0) return SXEN_OK;
+  DeviceGuard guard(enc->device);
+  EncodeArgs a;
+  base_args(enc, x, type, n, a);
+  a.upstream = upstream;
+  a.out = out;
+  a.grads = grad ? grad->values : nullptr;
+  a.level_major = enc->tuning.level_major ? 1 : 0;
+  EncodeLaunch ln{};
+  ln.features = enc->cfg.features;
+  ln.lpt = enc->tuning.levels_per_thread;
+  ln.mode = mode;
+  ln.exact = enc->tuning.exact_blend ? 1 : 0;
+  ln.grid_backend = enc->cfg.backend == SXEN_BACKEND_GRID ? 1 : 0;
+  ln.block_threads = enc->tuning.block_threads;
+  for (int level0 = 0; level0 < enc->cfg.levels; level0 += sxen_dev::kMaxLaunchLevels) {
+    level_chunk(enc, level0, a);
+    a.vec = 4;
+    if (mode & sxen_dev::kModeFwd) a.vec = std::min(a.vec, ptr_vec(out));
+    if (mode & sxen_dev::kModeBwd) a.vec = std::min(a.vec, ptr_vec(upstream));
+    int used = 0;
+    SXEN_CUDA(kEncode[enc->cfg.dim - 1](ln, a, stream, &used));
+    count_launch();
+  }
+  enc->touched += static_cast<uint64_t>(n) * static_cast<uint64_t>(enc->cfg.levels) *
+                  static_cast<uint64_t>(enc->vertices()) * ((mode == sxen_dev::kModeBoth) ? 2u : 1u);
+  return SXEN_OK;
+}
+
+sxen_status read_status(sxen_encoder* enc, cudaStream_t stream, bool reset_bad) {
+  SXEN_CUDA(cudaMemcpyAsync(enc->status_host, enc->status, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                            stream));
+  SXEN_CUDA(cudaStreamSynchronize(stream));
+  if (reset_bad && enc->status_host[0] != kNoBadSample) {
+    const unsigned long long none = kNoBadSample;
+    SXEN_CUDA(cudaMemcpyAsync(enc->status, &none, sizeof(none), cudaMemcpyHostToDevice, stream));
+    SXEN_CUDA(cudaStreamSynchronize(stream));
+  }
+  return SXEN_OK;
+}
+
+sxen_status ensure_staging(sxen_encoder* enc) {
+  if (enc->stage_samples) return SXEN_OK;
+  const size_t chunk = 1u << 18;
+  const size_t lf = static_cast<size_t>(enc->cfg.levels) * static_cast<size_t>(enc->cfg.features);
+  for (int i = 0; i < sxen_encoder::kStages; ++i) {
+    SXEN_CUDA(cudaMalloc(&enc->stage_x[i], chunk * static_cast<size_t>(enc->cfg.dim) * sizeof(double)));
+    // one buffer serves features (f32) on the way out and upstream (f64 from the host, narrowed on device) on the way in
+    SXEN_CUDA(cudaMalloc(&enc->stage_io[i], chunk * lf * sizeof(double)));
+    SXEN_CUDA(cudaStreamCreateWithFlags(&enc->stage_stream[i], cudaStreamNonBlocking));
+  }
+  enc->stage_samples = chunk;
+  return SXEN_OK;
+}
+
+// upstream arrives from the host as the reference's doubles (include/sxen/encoding.hpp:119); the kernels take f32.
+__global__ void narrow_kernel(const double* __restrict__ src, float* __restrict__ dst, size_t n) {
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = static_cast<float>(src[i]);
+}
+
+}  // namespace
+
+extern "C" {
+
+// ---------------------------------------------------------------------------------------------- library
+const char* sxen_last_error(void) { return last_error().c_str(); }
+const char* sxen_version(void) { return "sxen-b200 0.1 (sm_100a)"; }
+
+int32_t sxen_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int ok = 0;
+  for (int d = 0; d < n; ++d) {
+    int major = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d) == cudaSuccess && major == 10) ++ok;
+  }
+  return ok;
+}
+
+uint64_t sxen_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+sxen_status sxen_host_alloc(size_t bytes, void** out) {
+  SXEN_REQUIRE(out != nullptr, "output pointer is null");
+  SXEN_CUDA(cudaHostAlloc(out, bytes, cudaHostAllocDefault));
+  return SXEN_OK;
+}
+
+sxen_status sxen_host_free(void* ptr) {
+  if (ptr) SXEN_CUDA(cudaFreeHost(ptr));
+  return SXEN_OK;
+}
+
+// ---------------------------------------------------------------------------------------------- rng
+uint64_t sxen_mix64(uint64_t z) { return sxen_dev::mix64(z); }
+uint64_t sxen_hash_combine(uint64_t a, uint64_t b) { return sxen_dev::hash_combine(a, b); }
+
+sxen_status sxen_rng_fill_dev(uint64_t seed, int32_t has_stream, uint64_t stream_id, uint64_t first_counter, double lo,
+                              double hi, void* out_dev, size_t count, sxen_coord_type type, void* stream) {
+  SXEN_REQUIRE(count == 0 || out_dev != nullptr, "output pointer is null");
+  SXEN_REQUIRE(first_counter >= 1, "CounterRng draws are 1-based");
+  if (count == 0) return SXEN_OK;
+  uint64_t key = sxen_dev::mix64(seed);                       // include/sxen/rng.hpp:26
+  if (has_stream) key = sxen_dev::hash_combine(key, stream_id);  // include/sxen/rng.hpp:27
+  const double span = hi - lo;
+  if (type == SXEN_COORD_F32) {
+    rng_fill_kernel<float><<<grid_for(count), 256, 0, as_stream(stream)>>>(static_cast<float*>(out_dev), count, key,
+                                                                          first_counter, lo, span);
+  } else {
+    rng_fill_kernel<double><<<grid_for(count), 256, 0, as_stream(stream)>>>(static_cast<double*>(out_dev), count, key,
+                                                                           first_counter, lo, span);
+  }
+  SXEN_CUDA(cudaGetLastError());
+  count_launch();
+  return SXEN_OK;
+}
+
+// ---------------------------------------------------------------------------------------------- config
+sxen_status sxen_encoder_config_default(sxen_encoder_config* cfg) {
+  SXEN_REQUIRE(cfg != nullptr, "config pointer is null");
+  *cfg = sxen_encoder_config{2, 8, 1u << 16, 2, 16, 2.0, SXEN_BACKEND_SIMPLEX, SXEN_SCALE_RAW};  // encoding.hpp:18-27
+  return SXEN_OK;
+}
+
+sxen_status sxen_encoder_validate(const sxen_encoder_config* cfg) {
+  SXEN_REQUIRE(cfg != nullptr, "config pointer is null");
+  return validate(*cfg);
+}
+
+sxen_status sxen_level_resolution(const sxen_encoder_config* cfg, int32_t level, uint32_t* out) {
+  SXEN_REQUIRE(cfg != nullptr && out != nullptr, "null argument");
+  SXEN_REQUIRE(level >= 0 && level < cfg->levels, "level_resolution: level out of range");  // src/encoding.cpp:69-71
+  *out = level_resolution(*cfg, level);
+  return SXEN_OK;
+}
+
+sxen_status sxen_equal_memory_multiplier(int32_t dim, double* out) {
+  SXEN_REQUIRE(out != nullptr, "null argument");
+  SXEN_REQUIRE(dim >= 1 && dim <= SXEN_MAX_DIM, "equal_memory_multiplier: dim out of range");  // src/encoding.cpp:61-63
+  *out = equal_memory_multiplier(dim);
+  return SXEN_OK;
+}
+
+sxen_status sxen_skew_constants(int32_t dim, double out[3]) {
+  SXEN_REQUIRE(out != nullptr, "null argument");
+  SXEN_REQUIRE(dim >= 1 && dim <= SXEN_MAX_DIM, "dimension must be in [1, %d], got %d", SXEN_MAX_DIM, dim);
+  const double root = std::sqrt(static_cast<double>(dim) + 1.0);  // src/lattice.cpp:23
+  out[0] = (root - 1.0) / static_cast<double>(dim);
+  out[1] = (1.0 - 1.0 / root) / static_cast<double>(dim);
+  out[2] = root;
+  return SXEN_OK;
+}
+
+sxen_status sxen_hash_coords(const int64_t* coords, int32_t dim, uint32_t* out) {
+  SXEN_REQUIRE(coords != nullptr && out != nullptr, "null argument");
+  SXEN_REQUIRE(dim >= 1 && dim <= SXEN_MAX_DIM, "hash_index: coordinate count out of range");  // hashing.hpp:36-38
+  uint32_t h = 0;
+  for (int i = 0; i < dim; ++i) h ^= static_cast<uint32_t>(static_cast<uint64_t>(coords[i])) * sxen_dev::prime_of(i);
+  *out = h;
+  return SXEN_OK;
+}
+
+// ---------------------------------------------------------------------------------------------- encoder
+sxen_status sxen_encoder_create(const sxen_encoder_config* cfg, int32_t device, sxen_encoder** out) {
+  SXEN_REQUIRE(cfg != nullptr && out != nullptr, "null argument");
+  *out = nullptr;
+  if (sxen_status st = validate(*cfg)) return st;
+  int ndev = 0;
+  SXEN_CUDA(cudaGetDeviceCount(&ndev));
+  SXEN_REQUIRE(device >= 0 && device < ndev, "device %d out of range (%d visible)", device, ndev);
+  int major = 0;
+  SXEN_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  if (major != 10) return fail(SXEN_CUDA_ERROR, "device %d is sm_%dx; this library carries sm_100a code only", device, major);
+  DeviceGuard guard(device);
+  sxen_encoder* e = new sxen_encoder();
+  e->cfg = *cfg;
+  e->device = device;
+  e->tuning = default_tuning();
+  e->res.resize(static_cast<size_t>(cfg->levels));
+  for (int l = 0; l < cfg->levels; ++l) e->res[static_cast<size_t>(l)] = level_resolution(*cfg, l);
+  double sc[3];
+  sxen_skew_constants(cfg->dim, sc);
+  e->skew = sc[0];
+  e->scale = sc[2];
+  const size_t bytes = static_cast<size_t>(cfg->levels) * e->level_floats() * sizeof(float);
+  cudaError_t err = cudaMalloc(&e->tables, bytes);
+  if (err == cudaSuccess) err = cudaMemset(e->tables, 0, bytes);  // tables start at zero (src/encoding.cpp:163-166)
+  if (err == cudaSuccess) err = cudaMalloc(&e->status, 2 * sizeof(unsigned long long));
+  if (err == cudaSuccess) err = cudaHostAlloc(&e->status_host, 2 * sizeof(unsigned long long), cudaHostAllocDefault);
+  if (err == cudaSuccess) {
+    const unsigned long long init[2] = {kNoBadSample, 0ULL};
+    err = cudaMemcpy(e->status, init, sizeof(init), cudaMemcpyHostToDevice);
+  }
+  if (err != cudaSuccess) {
+    sxen_encoder_destroy(e);
+    return cuda_fail(err, "sxen_encoder_create allocation");
+  }
+  *out = e;
+  return SXEN_OK;
+}
+
+sxen_status sxen_encoder_destroy(sxen_encoder* enc) {
+  if (!enc) return SXEN_OK;
+  DeviceGuard guard(enc->device);
+  cudaFree(enc->tables);
+  cudaFree(enc->status);
+  cudaFreeHost(enc->status_host);
+  for (int i = 0; i < sxen_encoder::kStages; ++i) {
+    cudaFree(enc->stage_x[i]);
+    cudaFree(enc->stage_io[i]);
+    if (enc->stage_stream[i]) cudaStreamDestroy(enc->stage_stream[i]);
+  }
+  delete enc;
+  return SXEN_OK;
+}
+
+sxen_status sxen_encoder_get_config(const sxen_encoder* enc, sxen_encoder_config* out) {
+  SXEN_REQUIRE(enc != nullptr && out != nullptr, "null argument");
+  *out = enc->cfg;
+  return SXEN_OK;
+}
+
+sxen_status sxen_encoder_resolution(const sxen_encoder* enc, int32_t level, uint32_t* out) {
+  SXEN_REQUIRE(enc != nullptr && out != nullptr, "null argument");
+  SXEN_REQUIRE(level >= 0 && level < enc->cfg.levels, "resolution: level out of range");
+  *out = enc->res[static_cast<size_t>(level)];
+  return SXEN_OK;
+}
+
+sxen_status sxen_encoder_parameter_count(const sxen_encoder* enc, uint64_t* out) {
+  SXEN_REQUIRE(enc != nullptr && out != nullptr, "null argument");
+  *out = static_cast<uint64_t>(enc->cfg.levels) * enc->cfg.table_size * static_cast<uint64_t>(enc->cfg.features);
+  return SXEN_OK;
+}
+
+sxen_status sxen_encoder_set_tuning(sxen_encoder* enc, const sxen_tuning* t) {
+  SXEN_REQUIRE(enc != nullptr && t != nullptr, "null argument");
+  sxen_tuning d = default_tuning();
+  sxen_tuning n = *t;
+  if (n.levels_per_thread <= 0) n.levels_per_thread = d.levels_per_thread;
+  if (n.block_threads <= 0) n.block_threads = d.block_threads;
+  SXEN_REQUIRE(n.block_threads % 32 == 0 && n.block_threads <= 1024, "block_threads must be a multiple of 32, <= 1024");
+  SXEN_REQUIRE(n.warp_aggregate >= 0, "warp_aggregate must be >= 0");
+  enc->tuning = n;
+  return SXEN_OK;
+}
+
+sxen_status sxen_encoder_get_tuning(const sxen_encoder* enc, sxen_tuning* out) {
+  SXEN_REQUIRE(enc != nullptr && out != nullptr, "null argument");
+  *out = enc->tuning;
+  return SXEN_OK;
+}
+
+sxen_status sxen_encoder_init_tables(sxen_encoder* enc, uint64_t seed, void* stream) {
+  SXEN_REQUIRE(enc != nullptr, "encoder handle is null");
+  DeviceGuard guard(enc->device);
+  const size_t total = static_cast<size_t>(enc->cfg.levels) * enc->level_floats();
+  const double lo = -1e-4, hi = 1e-4;
+  init_tables_kernel<<<grid_for(total), 256, 0, as_stream(stream)>>>(enc->tables, enc->level_floats(), enc->cfg.levels,
+                                                                     sxen_dev::mix64(seed), lo, hi - lo);
+  SXEN_CUDA(cudaGetLastError());
+  count_launch();
+  return SXEN_OK;
+}
+
+sxen_status sxen_encoder_upload_table(sxen_encoder* enc, int32_t level, const float* src_host) {
+  SXEN_REQUIRE(enc != nullptr && src_host != nullptr, "null argument");
+  SXEN_REQUIRE(level >= 0 && level < enc->cfg.levels, "table: level out of range");
+  DeviceGuard guard(enc->device);
+  SXEN_CUDA(cudaMemcpy(enc->tables + static_cast<size_t>(level) * enc->level_floats(), src_host,
+                       enc->level_floats() * sizeof(float), cudaMemcpyHostToDevice));
+  return SXEN_OK;
+}
+
+sxen_status sxen_encoder_download_table(const sxen_encoder* enc, int32_t level, float* dst_host) {
+  SXEN_REQUIRE(enc != nullptr && dst_host != nullptr, "null argument");
+  SXEN_REQUIRE(level >= 0 && level < enc->cfg.levels, "table: level out of range");
+  DeviceGuard guard(enc->device);
+  SXEN_CUDA(cudaMemcpy(dst_host, enc->tables + static_cast<size_t>(level) * enc->level_floats(),
+                       enc->level_floats() * sizeof(float), cudaMemcpyDeviceToHost));
+  return SXEN_OK;
+}
+
+sxen_status sxen_encoder_tables_dev(sxen_encoder* enc, float** out_dev) {
+  SXEN_REQUIRE(enc != nullptr && out_dev != nullptr, "null argument");
+  *out_dev = enc->tables;
+  return SXEN_OK;
+}
+
+sxen_status sxen_encoder_encode(sxen_encoder* enc, const void* x_dev, sxen_coord_type type, size_t n_samples,
+                                float* out_dev, void* stream) {
+  return run_encode(enc, x_dev, type, nullptr, n_samples, out_dev, nullptr, sxen_dev::kModeFwd, as_stream(stream));
+}
+
+sxen_status sxen_encoder_encode_backward(sxen_encoder* enc, const void* x_dev, sxen_coord_type type,
+                                         const float* upstream_dev, size_t n_samples, sxen_grad* grad, void* stream) {
+  return run_encode(enc, x_dev, type, upstream_dev, n_samples, nullptr, grad, sxen_dev::kModeBwd, as_stream(stream));
+}
+
+sxen_status sxen_encoder_encode_forward_backward(sxen_encoder* enc, const void* x_dev, sxen_coord_type type,
+                                                 const float* upstream_dev, size_t n_samples, float* out_dev,
+                                                 sxen_grad* grad, void* stream) {
+  return run_encode(enc, x_dev, type, upstream_dev, n_samples, out_dev, grad, sxen_dev::kModeBoth, as_stream(stream));
+}
+
+sxen_status sxen_encoder_encode_debug(sxen_encoder* enc, const void* x_dev, sxen_coord_type type, size_t n_samples,
+                                      uint32_t* idx_dev, double* w_dev, void* stream) {
+  if (sxen_status st = check_batch(enc, x_dev, type, n_samples)) return st;
+  SXEN_REQUIRE(n_samples == 0 || (idx_dev != nullptr && w_dev != nullptr), "encode_debug: output pointer is null");
+  if (n_samples == 0) return SXEN_OK;
+  DeviceGuard guard(enc->device);
+  EncodeArgs a;
+  base_args(enc, x_dev, type, n_samples, a);
+  for (int level0 = 0; level0 < enc->cfg.levels; level0 += sxen_dev::kMaxLaunchLevels) {
+    level_chunk(enc, level0, a);
+    SXEN_CUDA(kDebug[enc->cfg.dim - 1](a, enc->cfg.backend == SXEN_BACKEND_GRID ? 1 : 0, idx_dev, w_dev,
+                                       enc->cfg.levels, as_stream(stream)));
+    count_launch();
+  }
+  return SXEN_OK;
+}
+
+sxen_status sxen_encoder_check(sxen_encoder* enc, void* stream) {
+  SXEN_REQUIRE(enc != nullptr, "encoder handle is null");
+  DeviceGuard guard(enc->device);
+  if (sxen_status st = read_status(enc, as_stream(stream), true)) return st;
+  if (enc->status_host[0] != kNoBadSample) {
+    // check_input, src/encoding.cpp:189-192
+    return fail(SXEN_INVALID_ARGUMENT, "encode: coordinate outside the unit cube (first offending sample %llu)",
+                enc->status_host[0]);
+  }
+  return SXEN_OK;
+}
+
+sxen_status sxen_encoder_counters(sxen_encoder* enc, sxen_lookup_counters* out) {
+  SXEN_REQUIRE(enc != nullptr && out != nullptr, "null argument");
+  DeviceGuard guard(enc->device);
+  SXEN_CUDA(cudaDeviceSynchronize());
+  SXEN_CUDA(cudaMemcpy(enc->status_host, enc->status, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  out->touched_vertices = enc->touched;
+  out->out_of_bounds = enc->status_host[1];
+  return SXEN_OK;
+}
+
+sxen_status sxen_encoder_reset_counters(sxen_encoder* enc) {
+  SXEN_REQUIRE(enc != nullptr, "encoder handle is null");
+  DeviceGuard guard(enc->device);
+  SXEN_CUDA(cudaDeviceSynchronize());
+  SXEN_CUDA(cudaMemset(enc->status + 1, 0, sizeof(unsigned long long)));
+  enc->touched = 0;
+  return SXEN_OK;
+}
+
+// Host-buffer forms: chunked three-stage pipeline (H2D copy | kernel | D2H copy on rotating streams).
+sxen_status sxen_encoder_encode_host(sxen_encoder* enc, const double* x_host, size_t n_samples, float* out_host) {
+  if (sxen_status st = check_batch(enc, x_host, SXEN_COORD_F64, n_samples)) return st;
+  SXEN_REQUIRE(n_samples == 0 || out_host != nullptr, "encode: output pointer is null");
+  if (n_samples == 0) return SXEN_OK;
+  DeviceGuard guard(enc->device);
+  if (sxen_status st = ensure_staging(enc)) return st;
+  const size_t dim = static_cast<size_t>(enc->cfg.dim);
+  const size_t lf = static_cast<size_t>(enc->cfg.levels) * static_cast<size_t>(enc->cfg.features);
+  size_t done = 0;
+  for (int c = 0; done < n_samples; ++c) {
+    const int slot = c % sxen_encoder::kStages;
+    const size_t n = std::min(enc->stage_samples, n_samples - done);
+    cudaStream_t st = enc->stage_stream[slot];
+    SXEN_CUDA(cudaMemcpyAsync(enc->stage_x[slot], x_host + done * dim, n * dim * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (sxen_status s = run_encode(enc, enc->stage_x[slot], SXEN_COORD_F64, nullptr, n, enc->stage_io[slot], nullptr,
+                                   sxen_dev::kModeFwd, st))
+      return s;
+    SXEN_CUDA(cudaMemcpyAsync(out_host + done * lf, enc->stage_io[slot], n * lf * sizeof(float), cudaMemcpyDeviceToHost, st));
+    done += n;
+  }
+  for (int i = 0; i < sxen_encoder::kStages; ++i) SXEN_CUDA(cudaStreamSynchronize(enc->stage_stream[i]));
+  if (sxen_status st = sxen_encoder_check(enc, enc->stage_stream[0])) return st;
+  return SXEN_OK;
+}
+
+sxen_status sxen_encoder_encode_backward_host(sxen_encoder* enc, const double* x_host, const double* upstream_host,
+                                              size_t n_samples, sxen_grad* grad) {
+  if (sxen_status st = check_batch(enc, x_host, SXEN_COORD_F64, n_samples)) return st;
+  SXEN_REQUIRE(n_samples == 0 || upstream_host != nullptr, "encode_backward: upstream pointer is null");
+  SXEN_REQUIRE(grad != nullptr, "encode_backward: gradient accumulator is null");
+  if (n_samples == 0) return SXEN_OK;
+  DeviceGuard guard(enc->device);
+  if (sxen_status st = ensure_staging(enc)) return st;
+  const size_t dim = static_cast<size_t>(enc->cfg.dim);
+  const size_t lf = static_cast<size_t>(enc->cfg.levels) * static_cast<size_t>(enc->cfg.features);
+  // half-size chunks: the stage buffer (chunk*lf*8 B) holds the f32 copy in its first quarter and the incoming
+  // doubles from byte chunk*lf*2 on -- disjoint ranges
+  size_t done = 0;
+  for (int c = 0; done < n_samples; ++c) {
+    const int slot = c % sxen_encoder::kStages;
+    const size_t n = std::min(enc->stage_samples / 2, n_samples - done);
+    cudaStream_t st = enc->stage_stream[slot];
+    float* up_f32 = enc->stage_io[slot];
+    double* up_f64 = reinterpret_cast<double*>(reinterpret_cast<char*>(enc->stage_io[slot]) +
+                                               (enc->stage_samples / 2) * lf * sizeof(float));
+    SXEN_CUDA(cudaMemcpyAsync(enc->stage_x[slot], x_host + done * dim, n * dim * sizeof(double), cudaMemcpyHostToDevice, st));
+    SXEN_CUDA(cudaMemcpyAsync(up_f64, upstream_host + done * lf, n * lf * sizeof(double), cudaMemcpyHostToDevice, st));
+    narrow_kernel<<<static_cast<unsigned>((n * lf + 255) / 256), 256, 0, st>>>(up_f64, up_f32, n * lf);
+    SXEN_CUDA(cudaGetLastError());
+    count_launch();
+    if (sxen_status s = run_encode(enc, enc->stage_x[slot], SXEN_COORD_F64, up_f32, n, nullptr, grad, sxen_dev::kModeBwd, st))
+      return s;
+    done += n;
+  }
+  for (int i = 0; i < sxen_encoder::kStages; ++i) SXEN_CUDA(cudaStreamSynchronize(enc->stage_stream[i]));
+  if (sxen_status st = sxen_encoder_check(enc, enc->stage_stream[0])) return st;
+  return SXEN_OK;
+}
+
+sxen_status sxen_encoder_encode_forward_backward_host(sxen_encoder* enc, const double* x_host,
+                                                      const void* upstream_host, sxen_coord_type upstream_type,
+                                                      size_t n_samples, float* out_host, sxen_grad* grad) {
+  if (sxen_status st = check_batch(enc, x_host, SXEN_COORD_F64, n_samples)) return st;
+  SXEN_REQUIRE(upstream_type == SXEN_COORD_F64 || upstream_type == SXEN_COORD_F32, "unknown upstream type");
+  SXEN_REQUIRE(n_samples == 0 || (upstream_host != nullptr && out_host != nullptr), "null upstream or output pointer");
+  SXEN_REQUIRE(grad != nullptr, "encode_backward: gradient accumulator is null");
+  if (n_samples == 0) return SXEN_OK;
+  DeviceGuard guard(enc->device);
+  if (sxen_status st = ensure_staging(enc)) return st;
+  const size_t dim = static_cast<size_t>(enc->cfg.dim);
+  const size_t lf = static_cast<size_t>(enc->cfg.levels) * static_cast<size_t>(enc->cfg.features);
+  // Stage buffer (chunk*lf*8 B) per slot, chunk/4 samples per pass: features out in [0, q), f32 upstream in [q, 2q),
+  // incoming f64 upstream in [2q, 4q) with q = chunk*lf*2 bytes... sized for the f64 case; disjoint ranges.
+  const size_t per = enc->stage_samples / 4;
+  size_t done = 0;
+  for (int c = 0; done < n_samples; ++c) {
+    const int slot = c % sxen_encoder::kStages;
+    const size_t n = std::min(per, n_samples - done);
+    cudaStream_t st = enc->stage_stream[slot];
+    char* base = reinterpret_cast<char*>(enc->stage_io[slot]);
+    float* out_dev = reinterpret_cast<float*>(base);
+    float* up_f32 = reinterpret_cast<float*>(base + per * lf * sizeof(float));
+    double* up_f64 = reinterpret_cast<double*>(base + 2 * per * lf * sizeof(float));
+    SXEN_CUDA(cudaMemcpyAsync(enc->stage_x[slot], x_host + done * dim, n * dim * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (upstream_type == SXEN_COORD_F64) {
+      SXEN_CUDA(cudaMemcpyAsync(up_f64, static_cast<const double*>(upstream_host) + done * lf, n * lf * sizeof(double),
+                                cudaMemcpyHostToDevice, st));
+      narrow_kernel<<<static_cast<unsigned>((n * lf + 255) / 256), 256, 0, st>>>(up_f64, up_f32, n * lf);
+      SXEN_CUDA(cudaGetLastError());
+      count_launch();
+    } else {
+      SXEN_CUDA(cudaMemcpyAsync(up_f32, static_cast<const float*>(upstream_host) + done * lf, n * lf * sizeof(float),
+                                cudaMemcpyHostToDevice, st));
+    }
+    if (sxen_status s = run_encode(enc, enc->stage_x[slot], SXEN_COORD_F64, up_f32, n, out_dev, grad,
+                                   sxen_dev::kModeBoth, st))
+      return s;
+    SXEN_CUDA(cudaMemcpyAsync(out_host + done * lf, out_dev, n * lf * sizeof(float), cudaMemcpyDeviceToHost, st));
+    done += n;
+  }
+  for (int i = 0; i < sxen_encoder::kStages; ++i) SXEN_CUDA(cudaStreamSynchronize(enc->stage_stream[i]));
+  if (sxen_status st = sxen_encoder_check(enc, enc->stage_stream[0])) return st;
+  return SXEN_OK;
+}
+
+// ---------------------------------------------------------------------------------------------- gradient accumulator
+sxen_status sxen_grad_create(const sxen_encoder* enc, sxen_grad** out) {
+  SXEN_REQUIRE(enc != nullptr && out != nullptr, "null argument");
+  *out = nullptr;
+  DeviceGuard guard(enc->device);
+  sxen_grad* g = new sxen_grad();
+  g->device = enc->device;
+  g->levels = enc->cfg.levels;
+  g->features = enc->cfg.features;
+  g->table_size = enc->cfg.table_size;
+  cudaError_t err = cudaMalloc(&g->values, g->count() * sizeof(float));
+  if (err != cudaSuccess) {
+    delete g;
+    return cuda_fail(err, "sxen_grad_create allocation");
+  }
+  *out = g;
+  const sxen_status st = sxen_grad_clear(g, nullptr);
+  if (st == SXEN_OK) {
+    if (cudaStreamSynchronize(nullptr) != cudaSuccess) return fail(SXEN_CUDA_ERROR, "sxen_grad_create sync failed");
+  }
+  return st;
+}
+
+sxen_status sxen_grad_destroy(sxen_grad* grad) {
+  if (!grad) return SXEN_OK;
+  DeviceGuard guard(grad->device);
+  cudaFree(grad->values);
+  delete grad;
+  return SXEN_OK;
+}
+
+sxen_status sxen_grad_clear(sxen_grad* grad, void* stream) {
+  SXEN_REQUIRE(grad != nullptr, "gradient handle is null");
+  DeviceGuard guard(grad->device);
+  fill_u32_kernel<<<grid_for(grad->count()), 256, 0, as_stream(stream)>>>(reinterpret_cast<uint32_t*>(grad->values),
+                                                                          grad->count(), kUntouchedBits);
+  SXEN_CUDA(cudaGetLastError());
+  count_launch();
+  return SXEN_OK;
+}
+
+sxen_status sxen_grad_values_dev(sxen_grad* grad, float** out_dev, size_t* count) {
+  SXEN_REQUIRE(grad != nullptr && out_dev != nullptr, "null argument");
+  *out_dev = grad->values;
+  if (count) *count = grad->count();
+  return SXEN_OK;
+}
+
+sxen_status sxen_grad_download(const sxen_grad* grad, int32_t level, float* values_host, uint8_t* touched_host) {
+  SXEN_REQUIRE(grad != nullptr && values_host != nullptr, "null argument");
+  SXEN_REQUIRE(level >= 0 && level < grad->levels, "gradient: level out of range");
+  DeviceGuard guard(grad->device);
+  const size_t per = static_cast<size_t>(grad->table_size) * static_cast<size_t>(grad->features);
+  SXEN_CUDA(cudaMemcpy(values_host, grad->values + static_cast<size_t>(level) * per, per * sizeof(float),
+                       cudaMemcpyDeviceToHost));
+  for (size_t r = 0; r < grad->table_size; ++r) {
+    uint32_t bits;
+    std::memcpy(&bits, values_host + r * grad->features, sizeof(bits));
+    const bool untouched = bits == kUntouchedBits;
+    if (touched_host) touched_host[r] = untouched ? 0 : 1;
+    if (untouched)
+      for (int f = 0; f < grad->features; ++f) values_host[r * grad->features + f] = 0.0f;
+  }
+  return SXEN_OK;
+}
+
+sxen_status sxen_grad_upload(sxen_grad* grad, int32_t level, const float* values_host, const uint8_t* touched_host) {
+  SXEN_REQUIRE(grad != nullptr && values_host != nullptr && touched_host != nullptr, "null argument");
+  SXEN_REQUIRE(level >= 0 && level < grad->levels, "gradient: level out of range");
+  DeviceGuard guard(grad->device);
+  const size_t per = static_cast<size_t>(grad->table_size) * static_cast<size_t>(grad->features);
+  std::vector<float> tmp(values_host, values_host + per);
+  const float neg_zero = -0.0f;
+  for (size_t r = 0; r < grad->table_size; ++r) {
+    for (int f = 0; f < grad->features; ++f) {
+      float& v = tmp[r * grad->features + f];
+      v = touched_host[r] ? (v + 0.0f) : neg_zero;  // a touched row never carries -0.0f
+    }
+  }
+  SXEN_CUDA(cudaMemcpy(grad->values + static_cast<size_t>(level) * per, tmp.data(), per * sizeof(float),
+                       cudaMemcpyHostToDevice));
+  return SXEN_OK;
+}
+
+sxen_status sxen_grad_touched_total(const sxen_grad* grad, uint64_t* out) {
+  SXEN_REQUIRE(grad != nullptr && out != nullptr, "null argument");
+  DeviceGuard guard(grad->device);
+  unsigned long long* d = nullptr;
+  SXEN_CUDA(cudaMalloc(&d, sizeof(unsigned long long)));
+  cudaMemset(d, 0, sizeof(unsigned long long));
+  const size_t rows = static_cast<size_t>(grad->levels) * grad->table_size;
+  grad_touched_kernel<<<grid_for(rows), 256>>>(grad->values, rows, grad->features, d);
+  count_launch();
+  unsigned long long h = 0;
+  const cudaError_t err = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  SXEN_CUDA(err);
+  *out = h;
+  return SXEN_OK;
+}
+
+sxen_status sxen_grad_merge(sxen_grad* dst, const sxen_grad* src, void* stream) {
+  SXEN_REQUIRE(dst != nullptr && src != nullptr, "null argument");
+  // src/encoding.cpp:123-125
+  SXEN_REQUIRE(dst->levels == src->levels && dst->features == src->features && dst->table_size == src->table_size &&
+                   dst->device == src->device,
+               "EncoderGradient::merge: shape mismatch");
+  DeviceGuard guard(dst->device);
+  const size_t rows = static_cast<size_t>(dst->levels) * dst->table_size;
+  grad_merge_kernel<<<grid_for(rows), 256, 0, as_stream(stream)>>>(dst->values, src->values, rows, dst->features);
+  SXEN_CUDA(cudaGetLastError());
+  count_launch();
+  return SXEN_OK;
+}
+
+}  // extern "C"

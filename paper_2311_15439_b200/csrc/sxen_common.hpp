@@ -1,0 +1,99 @@
+// sxen_common.hpp -- host-side plumbing shared by the C-ABI translation units: error strings, CUDA call checks,
+// handle definitions.  Nothing here is exported; the exported surface is include/sxen_cuda.h.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/sxen_cuda.h"
+
+namespace sxen_host {
+
+std::string& last_error();
+sxen_status fail(sxen_status st, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+sxen_status cuda_fail(cudaError_t e, const char* what);
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+#define SXEN_CUDA(call)                                                   \
+  do {                                                                    \
+    cudaError_t e__ = (call);                                             \
+    if (e__ != cudaSuccess) return ::sxen_host::cuda_fail(e__, #call);    \
+  } while (0)
+
+#define SXEN_REQUIRE(cond, ...)                                           \
+  do {                                                                    \
+    if (!(cond)) return ::sxen_host::fail(SXEN_INVALID_ARGUMENT, __VA_ARGS__); \
+  } while (0)
+
+// RAII device switch: handles live on one device, callers may have another current.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace sxen_host
+
+struct sxen_encoder {
+  sxen_encoder_config cfg{};
+  int device = 0;
+  std::vector<uint32_t> res;          // per-level resolution (src/encoding.cpp:159-162)
+  double skew = 0.0, scale = 1.0;     // F_n, S_n
+  float* tables = nullptr;            // L x T x F
+  unsigned long long* status = nullptr;       // device: [0] first bad sample, [1] oob count
+  unsigned long long* status_host = nullptr;  // pinned mirror
+  sxen_tuning tuning{};
+  uint64_t touched = 0;               // LookupCounters::touched_vertices
+  uint64_t oob_base = 0;              // oob counted before the last device reset
+  // staging for the *_host entry points (chunked H2D / compute / D2H pipeline)
+  static constexpr int kStages = 3;
+  size_t stage_samples = 0;
+  double* stage_x[kStages] = {nullptr, nullptr, nullptr};
+  float* stage_io[kStages] = {nullptr, nullptr, nullptr};
+  cudaStream_t stage_stream[kStages] = {nullptr, nullptr, nullptr};
+  size_t level_floats() const { return static_cast<size_t>(cfg.table_size) * static_cast<size_t>(cfg.features); }
+  int vertices() const { return cfg.backend == SXEN_BACKEND_SIMPLEX ? cfg.dim + 1 : (1 << cfg.dim); }
+};
+
+struct sxen_grad {
+  int device = 0;
+  int levels = 0, features = 0;
+  uint32_t table_size = 0;
+  float* values = nullptr;  // L x T x F, untouched rows carry -0.0f in feature 0
+  size_t count() const { return static_cast<size_t>(levels) * table_size * static_cast<size_t>(features); }
+};
+
+struct sxen_sparse_adam {
+  int device = 0;
+  int levels = 0, features = 0;
+  uint32_t table_size = 0;
+  double* m = nullptr;
+  double* v = nullptr;
+  int64_t t = 0;
+  unsigned long long* status = nullptr;       // device: first non-finite gradient element
+  unsigned long long* status_host = nullptr;  // pinned
+};
+
+struct sxen_adam {
+  int device = 0;
+  size_t size = 0;
+  double* m = nullptr;
+  double* v = nullptr;
+  int64_t t = 0;
+  unsigned long long* status = nullptr;
+  unsigned long long* status_host = nullptr;
+};

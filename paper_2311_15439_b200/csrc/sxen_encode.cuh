@@ -1,0 +1,364 @@
+// sxen_encode.cuh -- the encode / encode_backward kernels (sm_100a).
+//
+// One thread owns one sample and LPT consecutive levels.  For each (sample, level) it walks the simplex once
+// (sxen_device.cuh: simplex_lookup) and then
+//   forward  : gathers the ND+1 table rows (read-only path, one vector load per row) and blends them,
+//   backward : scatter-adds weight * upstream into the gradient rows with one vector `red.global.add` per row,
+//   both     : does the two off the same lattice walk (the fused fwd+bwd kernel).
+// HBM-bound integer/gather work: no tensor cores here by design.
+// Reference semantics: HashEncoder::encode / encode_backward, /root/reference/proj/src/encoding.cpp:295-335.
+#pragma once
+
+#include "sxen_device.cuh"
+
+namespace sxen_dev {
+
+enum : int { kModeFwd = 1, kModeBwd = 2, kModeBoth = 3 };
+
+struct EncodeArgs {
+  const void* x;                 // N x ND coordinates, f64 or f32
+  const float* upstream;         // N x row_width (backward / both)
+  float* out;                    // N x row_width (forward / both)
+  const float* tables;           // encoder level 0; level l at + l*level_stride
+  float* grads;                  // accumulator level 0, same layout
+  unsigned long long* status;    // [0] first rejected sample (atomicMin), [1] clamped cells (LookupCounters::out_of_bounds)
+  unsigned long long n_samples;
+  unsigned long long level_stride;  // T*F floats
+  uint32_t mask;                 // T-1
+  int32_t level0;                // first encoder level of this launch
+  int32_t n_levels;              // levels in this launch (<= kMaxLaunchLevels)
+  int32_t row_width;             // L*F
+  int32_t features;              // F (used by the dynamic-F kernels)
+  int32_t groups;                // ceil(n_levels / LPT)
+  int32_t groups_shift;          // log2(groups) when a power of two, else -1
+  int32_t coord_f32;             // coordinate element type
+  int32_t level_major;           // 1: blockIdx.y = level group
+  int32_t vec;                   // proven float alignment of every thread's out/upstream chunk: 4, 2 or 1
+  uint32_t agg_mask;             // bit l: warp-aggregate the backward atomics of local level l
+  double skew;                   // F_n
+  LevelGeom geom;
+};
+
+// Sum v[] over the lanes of `m` that hold the same key, leaving the total in the group's lowest lane.
+// Returns true on the lane that must issue the atomic.
+template <int F>
+__device__ __forceinline__ bool warp_merge_rows(unsigned m, unsigned long long key, float (&v)[F]) {
+  const unsigned peers = __match_any_sync(m, key);
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(peers) - 1;
+  unsigned todo = (lane == leader) ? (peers & ~(1u << lane)) : 0u;
+  while (__any_sync(m, todo != 0u)) {
+    const int src = todo ? (__ffs(todo) - 1) : lane;
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+      const float t = __shfl_sync(m, v[f], src);
+      if (todo) v[f] += t;
+    }
+    todo &= todo - 1u;
+  }
+  return lane == leader;
+}
+
+template <int ND>
+__device__ __forceinline__ bool load_coords(const EncodeArgs& a, unsigned long long s, double (&x)[ND]) {
+  if (a.coord_f32) {
+    const float* xp = static_cast<const float*>(a.x) + s * ND;
+#pragma unroll
+    for (int i = 0; i < ND; ++i) x[i] = static_cast<double>(__ldg(xp + i));
+  } else {
+    const double* xp = static_cast<const double*>(a.x) + s * ND;
+#pragma unroll
+    for (int i = 0; i < ND; ++i) x[i] = __ldg(xp + i);
+  }
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < ND; ++i) {
+    ok = ok && (x[i] >= 0.0 && x[i] <= 1.0);           // check_input, src/encoding.cpp:189 (NaN fails both)
+    x[i] = (kOneBelow < x[i]) ? kOneBelow : x[i];      // std::min(x, one_below), src/encoding.cpp:204
+  }
+  return ok;
+}
+
+template <int ND, int F, int LPT, int MODE, bool EXACT>
+__global__ void __launch_bounds__(LPT >= 4 ? 256 : 512)
+encode_kernel(const __grid_constant__ EncodeArgs a) {
+  constexpr bool kFwd = (MODE & kModeFwd) != 0;
+  constexpr bool kBwd = (MODE & kModeBwd) != 0;
+  constexpr int K = LPT * F;
+
+  __shared__ double s_scale[kMaxLaunchLevels];
+  __shared__ int s_res[kMaxLaunchLevels];
+  if (threadIdx.x < kMaxLaunchLevels) {
+    s_scale[threadIdx.x] = a.geom.scale[threadIdx.x];
+    s_res[threadIdx.x] = a.geom.res[threadIdx.x];
+  }
+  __syncthreads();
+
+  unsigned long long s;
+  int g;
+  if (a.level_major) {
+    g = blockIdx.y;
+    s = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  } else {
+    const unsigned long long gid = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (a.groups_shift >= 0) {
+      s = gid >> a.groups_shift;
+      g = static_cast<int>(gid & static_cast<unsigned long long>(a.groups - 1));
+    } else {
+      s = gid / static_cast<unsigned long long>(a.groups);
+      g = static_cast<int>(gid - s * static_cast<unsigned long long>(a.groups));
+    }
+  }
+  const bool in_range = s < a.n_samples;
+
+  double x[ND];
+  bool ok = false;
+  if (in_range) ok = load_coords<ND>(a, s, x);
+  const unsigned live = __ballot_sync(0xffffffffu, ok);
+  if (!in_range) return;
+
+  const int l_begin = g * LPT;
+  const bool full = l_begin + LPT <= a.n_levels;
+  const size_t chunk = static_cast<size_t>(s) * a.row_width + static_cast<size_t>(a.level0 + l_begin) * F;
+
+  if (!ok) {
+    // The reference throws std::invalid_argument before touching anything (src/encoding.cpp:183-194).  Here the
+    // sample is reported through the status word, its features are written as zeros, and it adds no gradient.
+    atomicMin(a.status, s);
+    if constexpr (kFwd) {
+      for (int j = 0; j < LPT; ++j)
+        if (l_begin + j < a.n_levels)
+          for (int f = 0; f < F; ++f) a.out[chunk + j * F + f] = 0.0f;
+    }
+    return;
+  }
+
+  float upv[K];
+  float outv[K];
+  if constexpr (kBwd) {
+    if (full) {
+      load_stream<K>(a.upstream + chunk, upv, a.vec);
+    } else {
+#pragma unroll
+      for (int q = 0; q < K; ++q) upv[q] = (l_begin + q / F < a.n_levels) ? __ldcs(a.upstream + chunk + q) : 0.0f;
+    }
+  }
+
+#pragma unroll
+  for (int j = 0; j < LPT; ++j) {
+    const int l = l_begin + j;
+    const bool has = l < a.n_levels;
+    unsigned aggm = 0u;
+    if constexpr (kBwd) {
+      if (a.agg_mask != 0u) aggm = __ballot_sync(live, has && ((a.agg_mask >> l) & 1u));
+    }
+    if (has) {
+      uint32_t idx[ND + 1];
+      double w[ND + 1];
+      const bool oob = simplex_lookup<ND>(x, s_scale[l], a.skew, s_res[l], a.mask, idx, w);
+      if (oob) atomicAdd(a.status + 1, 1ULL);
+      const size_t level_off = static_cast<size_t>(a.level0 + l) * a.level_stride;
+
+      if constexpr (kFwd) {
+        const float* __restrict__ tab = a.tables + level_off;
+        float e[ND + 1][F];
+#pragma unroll
+        for (int k = 0; k <= ND; ++k) load_row<F>(tab + static_cast<size_t>(idx[k]) * F, e[k]);
+        if constexpr (EXACT) {
+          // src/encoding.cpp:305-313: acc starts at 0.0, acc += w_i * entry in chain order, all in double.
+          double acc[F];
+#pragma unroll
+          for (int f = 0; f < F; ++f) acc[f] = 0.0;
+#pragma unroll
+          for (int k = 0; k <= ND; ++k) {
+#pragma unroll
+            for (int f = 0; f < F; ++f) acc[f] = __dadd_rn(acc[f], __dmul_rn(w[k], static_cast<double>(e[k][f])));
+          }
+#pragma unroll
+          for (int f = 0; f < F; ++f) outv[j * F + f] = static_cast<float>(acc[f]);
+        } else {
+          float acc[F];
+#pragma unroll
+          for (int f = 0; f < F; ++f) acc[f] = 0.0f;
+#pragma unroll
+          for (int k = 0; k <= ND; ++k) {
+            const float wk = static_cast<float>(w[k]);
+#pragma unroll
+            for (int f = 0; f < F; ++f) acc[f] = __fmaf_rn(wk, e[k][f], acc[f]);
+          }
+#pragma unroll
+          for (int f = 0; f < F; ++f) outv[j * F + f] = acc[f];
+        }
+      }
+
+      if constexpr (kBwd) {
+        float* __restrict__ gl = a.grads + level_off;
+        const bool agg = (aggm >> (threadIdx.x & 31)) & 1u;
+#pragma unroll
+        for (int k = 0; k <= ND; ++k) {
+          // EncoderGradient::add, src/encoding.cpp:110-120: dst[f] += scale * upstream[f]
+          const float wk = static_cast<float>(w[k]);
+          float v[F];
+#pragma unroll
+          for (int f = 0; f < F; ++f) v[f] = canon(__fmul_rn(wk, upv[j * F + f]));
+          bool issue = true;
+          if (agg) {
+            const unsigned long long key = (static_cast<unsigned long long>(l) << 32) | idx[k];
+            issue = warp_merge_rows<F>(aggm, key, v);
+          }
+          if (issue) red_row<F>(gl + static_cast<size_t>(idx[k]) * F, v);
+        }
+      }
+    }
+  }
+
+  if constexpr (kFwd) {
+    if (full) {
+      store_stream<K>(a.out + chunk, outv, a.vec);
+    } else {
+#pragma unroll
+      for (int q = 0; q < K; ++q)
+        if (l_begin + q / F < a.n_levels) __stcs(a.out + chunk + q, outv[q]);
+    }
+  }
+}
+
+// Any F in [1, 64] and both backends: one thread per (sample, level), features walked one at a time.
+// Always the exact fp64 chain-order blend.  The slow-but-general path.
+template <int ND, int MODE, bool GRID>
+__global__ void __launch_bounds__(256) encode_generic_kernel(const __grid_constant__ EncodeArgs a) {
+  constexpr bool kFwd = (MODE & kModeFwd) != 0;
+  constexpr bool kBwd = (MODE & kModeBwd) != 0;
+  const unsigned long long gid = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const unsigned long long s = gid / static_cast<unsigned long long>(a.n_levels);
+  const int l = static_cast<int>(gid - s * static_cast<unsigned long long>(a.n_levels));
+  if (s >= a.n_samples) return;
+  double x[ND];
+  const bool ok = load_coords<ND>(a, s, x);
+  const int F = a.features;
+  const size_t chunk = static_cast<size_t>(s) * a.row_width + static_cast<size_t>(a.level0 + l) * F;
+  if (!ok) {
+    atomicMin(a.status, s);
+    if constexpr (kFwd)
+      for (int f = 0; f < F; ++f) a.out[chunk + f] = 0.0f;
+    return;
+  }
+  const size_t level_off = static_cast<size_t>(a.level0 + l) * a.level_stride;
+  const float* __restrict__ tab = a.tables + level_off;
+  float* __restrict__ gl = a.grads + level_off;
+
+  if constexpr (GRID) {
+    GridCell<ND> cell;
+    if (grid_prepare<ND>(x, a.geom.scale[l], a.geom.res[l], cell)) atomicAdd(a.status + 1, 1ULL);
+    for (int f = 0; f < F; ++f) {
+      double acc = 0.0;
+      float up = 0.0f;
+      if constexpr (kBwd) up = __ldg(a.upstream + chunk + f);
+#pragma unroll 1
+      for (int m = 0; m < (1 << ND); ++m) {
+        uint32_t idx;
+        double w;
+        grid_corner<ND>(cell, m, a.mask, idx, w);
+        if constexpr (kFwd)
+          acc = __dadd_rn(acc, __dmul_rn(w, static_cast<double>(__ldg(tab + static_cast<size_t>(idx) * F + f))));
+        if constexpr (kBwd) red_add(gl + static_cast<size_t>(idx) * F + f, canon(__fmul_rn(static_cast<float>(w), up)));
+      }
+      if constexpr (kFwd) a.out[chunk + f] = static_cast<float>(acc);
+    }
+  } else {
+    uint32_t idx[ND + 1];
+    double w[ND + 1];
+    if (simplex_lookup<ND>(x, a.geom.scale[l], a.skew, a.geom.res[l], a.mask, idx, w)) atomicAdd(a.status + 1, 1ULL);
+    for (int f = 0; f < F; ++f) {
+      if constexpr (kFwd) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k <= ND; ++k)
+          acc = __dadd_rn(acc, __dmul_rn(w[k], static_cast<double>(__ldg(tab + static_cast<size_t>(idx[k]) * F + f))));
+        a.out[chunk + f] = static_cast<float>(acc);
+      }
+      if constexpr (kBwd) {
+        const float up = __ldg(a.upstream + chunk + f);
+#pragma unroll
+        for (int k = 0; k <= ND; ++k)
+          red_add(gl + static_cast<size_t>(idx[k]) * F + f, canon(__fmul_rn(static_cast<float>(w[k]), up)));
+      }
+    }
+  }
+}
+
+// Parity probe: the vertex chain itself.  idx: N x total_levels x V, w likewise (doubles).
+template <int ND, bool GRID>
+__global__ void __launch_bounds__(256)
+encode_debug_kernel(const __grid_constant__ EncodeArgs a, uint32_t* __restrict__ idx_out, double* __restrict__ w_out,
+                    int total_levels) {
+  constexpr int V = GRID ? (1 << ND) : (ND + 1);
+  const unsigned long long gid = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const unsigned long long s = gid / static_cast<unsigned long long>(a.n_levels);
+  const int l = static_cast<int>(gid - s * static_cast<unsigned long long>(a.n_levels));
+  if (s >= a.n_samples) return;
+  double x[ND];
+  const bool ok = load_coords<ND>(a, s, x);
+  const size_t o = (static_cast<size_t>(s) * total_levels + (a.level0 + l)) * V;
+  if (!ok) {
+    atomicMin(a.status, s);
+    for (int k = 0; k < V; ++k) {
+      idx_out[o + k] = 0u;
+      w_out[o + k] = 0.0;
+    }
+    return;
+  }
+  if constexpr (GRID) {
+    GridCell<ND> cell;
+    grid_prepare<ND>(x, a.geom.scale[l], a.geom.res[l], cell);
+#pragma unroll 1
+    for (int m = 0; m < V; ++m) {
+      uint32_t idx;
+      double w;
+      grid_corner<ND>(cell, m, a.mask, idx, w);
+      idx_out[o + m] = idx;
+      w_out[o + m] = w;
+    }
+  } else {
+    uint32_t idx[V];
+    double w[V];
+    simplex_lookup<ND>(x, a.geom.scale[l], a.skew, a.geom.res[l], a.mask, idx, w);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      idx_out[o + k] = idx[k];
+      w_out[o + k] = w[k];
+    }
+  }
+}
+
+// ---- host-side launch plumbing, one translation unit per ND (sxen_encode_nd.cu) -----------------------------
+
+struct EncodeLaunch {
+  int features;         // F, any
+  int lpt;              // requested levels per thread
+  int mode;             // kModeFwd / kModeBwd / kModeBoth
+  int exact;            // fp64 blend
+  int grid_backend;     // 0 simplex, 1 grid
+  int block_threads;
+};
+
+// Each returns cudaSuccess/err; *used_lpt reports the levels-per-thread actually instantiated.
+cudaError_t launch_encode_nd1(const EncodeLaunch&, EncodeArgs&, cudaStream_t, int* used_lpt);
+cudaError_t launch_encode_nd2(const EncodeLaunch&, EncodeArgs&, cudaStream_t, int* used_lpt);
+cudaError_t launch_encode_nd3(const EncodeLaunch&, EncodeArgs&, cudaStream_t, int* used_lpt);
+cudaError_t launch_encode_nd4(const EncodeLaunch&, EncodeArgs&, cudaStream_t, int* used_lpt);
+cudaError_t launch_encode_nd5(const EncodeLaunch&, EncodeArgs&, cudaStream_t, int* used_lpt);
+cudaError_t launch_encode_nd6(const EncodeLaunch&, EncodeArgs&, cudaStream_t, int* used_lpt);
+cudaError_t launch_encode_nd7(const EncodeLaunch&, EncodeArgs&, cudaStream_t, int* used_lpt);
+cudaError_t launch_encode_nd8(const EncodeLaunch&, EncodeArgs&, cudaStream_t, int* used_lpt);
+
+cudaError_t launch_debug_nd1(EncodeArgs&, int grid_backend, uint32_t*, double*, int total_levels, cudaStream_t);
+cudaError_t launch_debug_nd2(EncodeArgs&, int grid_backend, uint32_t*, double*, int total_levels, cudaStream_t);
+cudaError_t launch_debug_nd3(EncodeArgs&, int grid_backend, uint32_t*, double*, int total_levels, cudaStream_t);
+cudaError_t launch_debug_nd4(EncodeArgs&, int grid_backend, uint32_t*, double*, int total_levels, cudaStream_t);
+cudaError_t launch_debug_nd5(EncodeArgs&, int grid_backend, uint32_t*, double*, int total_levels, cudaStream_t);
+cudaError_t launch_debug_nd6(EncodeArgs&, int grid_backend, uint32_t*, double*, int total_levels, cudaStream_t);
+cudaError_t launch_debug_nd7(EncodeArgs&, int grid_backend, uint32_t*, double*, int total_levels, cudaStream_t);
+cudaError_t launch_debug_nd8(EncodeArgs&, int grid_backend, uint32_t*, double*, int total_levels, cudaStream_t);
+
+}  // namespace sxen_dev

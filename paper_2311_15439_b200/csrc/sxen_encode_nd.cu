@@ -1,0 +1,134 @@
+// sxen_encode_nd.cu -- instantiates the encode kernels for ONE input dimension (compile with -DSXEN_ND=<1..8>).
+// One translation unit per dimension keeps nvcc parallel and the per-file kernel count bounded.
+#include "sxen_encode.cuh"
+
+#ifndef SXEN_ND
+#error "compile with -DSXEN_ND=<1..8>"
+#endif
+
+namespace sxen_dev {
+namespace {
+
+constexpr int ND = SXEN_ND;
+
+template <int F, int LPT, int MODE, bool EXACT>
+cudaError_t go(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t stream) {
+  a.groups = (a.n_levels + LPT - 1) / LPT;
+  a.groups_shift = -1;
+  for (int sft = 0; sft < 31; ++sft)
+    if ((1 << sft) == a.groups) a.groups_shift = sft;
+  // out/upstream chunk alignment the kernel may rely on (base pointers are checked by the caller via a.vec)
+  const int k = LPT * F;
+  int vec = a.vec;
+  while (vec > 1 && ((k % vec) != 0 || (a.row_width % vec) != 0 || ((a.level0 * F) % vec) != 0)) vec >>= 1;
+  a.vec = vec;
+  int block = ln.block_threads > 0 ? ln.block_threads : 256;
+  const int max_block = LPT >= 4 ? 256 : 512;
+  if (block > max_block) block = max_block;
+  block = (block / 32) * 32;
+  if (block < 32) block = 32;
+  dim3 grid;
+  if (a.level_major) {
+    grid = dim3(static_cast<unsigned>((a.n_samples + block - 1) / block), static_cast<unsigned>(a.groups), 1);
+  } else {
+    const unsigned long long threads = a.n_samples * static_cast<unsigned long long>(a.groups);
+    grid = dim3(static_cast<unsigned>((threads + block - 1) / block), 1, 1);
+  }
+  encode_kernel<ND, F, LPT, MODE, EXACT><<<grid, block, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+template <int F, int LPT, bool EXACT>
+cudaError_t by_mode(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t stream) {
+  switch (ln.mode) {
+    case kModeFwd: return go<F, LPT, kModeFwd, EXACT>(ln, a, stream);
+    case kModeBwd: return go<F, LPT, kModeBwd, EXACT>(ln, a, stream);
+    default: return go<F, LPT, kModeBoth, EXACT>(ln, a, stream);
+  }
+}
+
+template <int MODE, bool GRID>
+cudaError_t go_generic(EncodeArgs& a, cudaStream_t stream) {
+  const int block = 256;
+  const unsigned long long threads = a.n_samples * static_cast<unsigned long long>(a.n_levels);
+  encode_generic_kernel<ND, MODE, GRID><<<static_cast<unsigned>((threads + block - 1) / block), block, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+template <bool GRID>
+cudaError_t generic_by_mode(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t stream) {
+  switch (ln.mode) {
+    case kModeFwd: return go_generic<kModeFwd, GRID>(a, stream);
+    case kModeBwd: return go_generic<kModeBwd, GRID>(a, stream);
+    default: return go_generic<kModeBoth, GRID>(a, stream);
+  }
+}
+
+// F == 2 is the configuration every BASELINE workload uses: full tuning surface.
+cudaError_t launch_f2(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t stream, int* used) {
+  int lpt = ln.lpt;
+#if SXEN_ND == 2 || SXEN_ND == 3
+  if (lpt >= 16) {
+    *used = 16;
+    return ln.exact ? by_mode<2, 16, true>(ln, a, stream) : by_mode<2, 16, false>(ln, a, stream);
+  }
+#endif
+  if (lpt >= 4) {
+    *used = 4;
+    return ln.exact ? by_mode<2, 4, true>(ln, a, stream) : by_mode<2, 4, false>(ln, a, stream);
+  }
+  if (lpt >= 2) {
+    *used = 2;
+    return ln.exact ? by_mode<2, 2, true>(ln, a, stream) : by_mode<2, 2, false>(ln, a, stream);
+  }
+  *used = 1;
+  return ln.exact ? by_mode<2, 1, true>(ln, a, stream) : by_mode<2, 1, false>(ln, a, stream);
+}
+
+// F in {1, 4, 8}: vectorised rows, exact blend only, one or two levels per thread.
+template <int F>
+cudaError_t launch_fx(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t stream, int* used) {
+  if (ln.lpt >= 2) {
+    *used = 2;
+    return by_mode<F, 2, true>(ln, a, stream);
+  }
+  *used = 1;
+  return by_mode<F, 1, true>(ln, a, stream);
+}
+
+}  // namespace
+
+#define SXEN_CAT2(a, b) a##b
+#define SXEN_CAT(a, b) SXEN_CAT2(a, b)
+
+cudaError_t SXEN_CAT(launch_encode_nd, SXEN_ND)(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t stream,
+                                                int* used_lpt) {
+  if (ln.grid_backend) {
+    *used_lpt = 1;
+    return generic_by_mode<true>(ln, a, stream);
+  }
+  switch (ln.features) {
+    case 2: return launch_f2(ln, a, stream, used_lpt);
+    case 1: return launch_fx<1>(ln, a, stream, used_lpt);
+    case 4: return launch_fx<4>(ln, a, stream, used_lpt);
+    case 8: return launch_fx<8>(ln, a, stream, used_lpt);
+    default:
+      *used_lpt = 1;
+      return generic_by_mode<false>(ln, a, stream);
+  }
+}
+
+cudaError_t SXEN_CAT(launch_debug_nd, SXEN_ND)(EncodeArgs& a, int grid_backend, uint32_t* idx, double* w,
+                                               int total_levels, cudaStream_t stream) {
+  const int block = 256;
+  const unsigned long long threads = a.n_samples * static_cast<unsigned long long>(a.n_levels);
+  const unsigned blocks = static_cast<unsigned>((threads + block - 1) / block);
+  if (grid_backend) {
+    encode_debug_kernel<ND, true><<<blocks, block, 0, stream>>>(a, idx, w, total_levels);
+  } else {
+    encode_debug_kernel<ND, false><<<blocks, block, 0, stream>>>(a, idx, w, total_levels);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace sxen_dev

@@ -1,0 +1,311 @@
+// sxen_optim.cu -- Adam updates on the device (reference: /root/reference/proj/src/optimizer.cpp).
+//
+// The arithmetic is the reference's, operation for operation, in fp64 with explicit round-to-nearest intrinsics so
+// nvcc cannot contract mul+add into an FMA (the reference's x86-64 build does not fuse either): given the same
+// gradient values the updated parameters and moments are bit-identical to AdamState::step / SparseAdamState::step.
+#include <cmath>
+
+#include "sxen_common.hpp"
+
+using namespace sxen_host;
+
+namespace {
+
+constexpr unsigned long long kNoBad = ~0ULL;
+constexpr uint32_t kUntouchedBits = 0x80000000u;
+
+struct AdamScalars {
+  double beta1, beta2, one_minus_beta1, one_minus_beta2, neg_lr, epsilon, bc1, bc2;
+};
+
+// adam_delta, src/optimizer.cpp:9-15
+__device__ __forceinline__ double adam_delta(double g, double& m, double& v, const AdamScalars& c) {
+  m = __dadd_rn(__dmul_rn(c.beta1, m), __dmul_rn(c.one_minus_beta1, g));
+  v = __dadd_rn(__dmul_rn(c.beta2, v), __dmul_rn(__dmul_rn(c.one_minus_beta2, g), g));
+  const double m_hat = __ddiv_rn(m, c.bc1);
+  const double v_hat = __ddiv_rn(v, c.bc2);
+  return __ddiv_rn(__dmul_rn(c.neg_lr, m_hat), __dadd_rn(__dsqrt_rn(v_hat), c.epsilon));
+}
+
+// SparseAdamState::step, src/optimizer.cpp:54-84.  One thread per table row; a row is visited iff the accumulator
+// touched it (feature 0 != -0.0f), zero gradients included; untouched rows' moments do not decay.
+__global__ void sparse_adam_kernel(float* __restrict__ tables, float* __restrict__ grads, double* __restrict__ m,
+                                   double* __restrict__ v, size_t rows, int features, AdamScalars c, int clear_grad,
+                                   unsigned long long* __restrict__ status) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t r = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < rows; r += stride) {
+    const size_t base = r * static_cast<size_t>(features);
+    if (__float_as_uint(grads[base]) == kUntouchedBits) continue;
+    for (int f = 0; f < features; ++f) {
+      const size_t i = base + static_cast<size_t>(f);
+      const double g = static_cast<double>(grads[i]);
+      if (!isfinite(g)) {
+        atomicMin(status, static_cast<unsigned long long>(i));  // TrainingError, src/optimizer.cpp:73-76
+        continue;
+      }
+      double mi = m[i], vi = v[i];
+      const double d = adam_delta(g, mi, vi, c);
+      m[i] = mi;
+      v[i] = vi;
+      tables[i] = static_cast<float>(__dadd_rn(static_cast<double>(tables[i]), d));
+      if (clear_grad) grads[i] = __uint_as_float(kUntouchedBits);
+    }
+  }
+}
+
+// F == 2 fast path: 8-byte gradient/table rows, 16-byte moment rows, one vector access each.
+__global__ void sparse_adam_f2_kernel(float2* __restrict__ tables, float2* __restrict__ grads, double2* __restrict__ m,
+                                      double2* __restrict__ v, size_t rows, AdamScalars c, int clear_grad,
+                                      unsigned long long* __restrict__ status) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t r = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < rows; r += stride) {
+    const float2 g2 = grads[r];
+    if (__float_as_uint(g2.x) == kUntouchedBits) continue;
+    const double gx = static_cast<double>(g2.x), gy = static_cast<double>(g2.y);
+    if (!isfinite(gx) || !isfinite(gy)) {
+      atomicMin(status, static_cast<unsigned long long>(2 * r + (isfinite(gx) ? 1 : 0)));
+      continue;
+    }
+    double2 mm = m[r], vv = v[r];
+    float2 t = tables[r];
+    const double dx = adam_delta(gx, mm.x, vv.x, c);
+    const double dy = adam_delta(gy, mm.y, vv.y, c);
+    m[r] = mm;
+    v[r] = vv;
+    t.x = static_cast<float>(__dadd_rn(static_cast<double>(t.x), dx));
+    t.y = static_cast<float>(__dadd_rn(static_cast<double>(t.y), dy));
+    tables[r] = t;
+    if (clear_grad) grads[r] = make_float2(__uint_as_float(kUntouchedBits), __uint_as_float(kUntouchedBits));
+  }
+}
+
+// AdamState::step, src/optimizer.cpp:25-41
+template <typename G>
+__global__ void dense_adam_kernel(float* __restrict__ params, const G* __restrict__ grads, double* __restrict__ m,
+                                  double* __restrict__ v, size_t n, AdamScalars c,
+                                  unsigned long long* __restrict__ status) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double g = static_cast<double>(grads[i]);
+    if (!isfinite(g)) {
+      atomicMin(status, static_cast<unsigned long long>(i));  // TrainingError, src/optimizer.cpp:35-37
+      continue;
+    }
+    double mi = m[i], vi = v[i];
+    const double d = adam_delta(g, mi, vi, c);
+    m[i] = mi;
+    v[i] = vi;
+    params[i] = static_cast<float>(__dadd_rn(static_cast<double>(params[i]), d));
+  }
+}
+
+AdamScalars scalars(const sxen_adam_config& cfg, int64_t t) {
+  AdamScalars c;
+  c.beta1 = cfg.beta1;
+  c.beta2 = cfg.beta2;
+  c.one_minus_beta1 = 1.0 - cfg.beta1;
+  c.one_minus_beta2 = 1.0 - cfg.beta2;
+  c.neg_lr = -cfg.lr;
+  c.epsilon = cfg.epsilon;
+  c.bc1 = 1.0 - std::pow(cfg.beta1, static_cast<double>(t));  // src/optimizer.cpp:31-32,65-66
+  c.bc2 = 1.0 - std::pow(cfg.beta2, static_cast<double>(t));
+  return c;
+}
+
+int grid_for(size_t n) {
+  size_t b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  return static_cast<int>(b < 1 ? 1 : b);
+}
+
+template <class H>
+sxen_status alloc_status(H* h) {
+  SXEN_CUDA(cudaMalloc(&h->status, sizeof(unsigned long long)));
+  SXEN_CUDA(cudaHostAlloc(&h->status_host, sizeof(unsigned long long), cudaHostAllocDefault));
+  const unsigned long long none = kNoBad;
+  SXEN_CUDA(cudaMemcpy(h->status, &none, sizeof(none), cudaMemcpyHostToDevice));
+  return SXEN_OK;
+}
+
+template <class H>
+sxen_status check_status(H* h, cudaStream_t stream, const char* what) {
+  SXEN_CUDA(cudaMemcpyAsync(h->status_host, h->status, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
+  SXEN_CUDA(cudaStreamSynchronize(stream));
+  if (*h->status_host != kNoBad) {
+    const unsigned long long bad = *h->status_host;
+    const unsigned long long none = kNoBad;
+    SXEN_CUDA(cudaMemcpyAsync(h->status, &none, sizeof(none), cudaMemcpyHostToDevice, stream));
+    SXEN_CUDA(cudaStreamSynchronize(stream));
+    return fail(SXEN_TRAINING_ERROR, "%s %llu", what, bad);
+  }
+  return SXEN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+sxen_status sxen_adam_config_default(sxen_adam_config* cfg) {
+  SXEN_REQUIRE(cfg != nullptr, "config pointer is null");
+  *cfg = sxen_adam_config{1e-3, 0.9, 0.99, 1e-15};  // include/sxen/optimizer.hpp:13-18
+  return SXEN_OK;
+}
+
+sxen_status sxen_sparse_adam_create(const sxen_encoder* enc, sxen_sparse_adam** out) {
+  SXEN_REQUIRE(enc != nullptr && out != nullptr, "null argument");
+  *out = nullptr;
+  DeviceGuard guard(enc->device);
+  sxen_sparse_adam* o = new sxen_sparse_adam();
+  o->device = enc->device;
+  o->levels = enc->cfg.levels;
+  o->features = enc->cfg.features;
+  o->table_size = enc->cfg.table_size;
+  const size_t bytes = static_cast<size_t>(o->levels) * o->table_size * static_cast<size_t>(o->features) * sizeof(double);
+  cudaError_t err = cudaMalloc(&o->m, bytes);
+  if (err == cudaSuccess) err = cudaMalloc(&o->v, bytes);
+  if (err == cudaSuccess) err = cudaMemset(o->m, 0, bytes);
+  if (err == cudaSuccess) err = cudaMemset(o->v, 0, bytes);
+  if (err != cudaSuccess) {
+    sxen_sparse_adam_destroy(o);
+    return cuda_fail(err, "sxen_sparse_adam_create allocation");
+  }
+  if (sxen_status st = alloc_status(o)) {
+    sxen_sparse_adam_destroy(o);
+    return st;
+  }
+  *out = o;
+  return SXEN_OK;
+}
+
+sxen_status sxen_sparse_adam_destroy(sxen_sparse_adam* opt) {
+  if (!opt) return SXEN_OK;
+  DeviceGuard guard(opt->device);
+  cudaFree(opt->m);
+  cudaFree(opt->v);
+  cudaFree(opt->status);
+  cudaFreeHost(opt->status_host);
+  delete opt;
+  return SXEN_OK;
+}
+
+sxen_status sxen_sparse_adam_step_count(const sxen_sparse_adam* opt, int64_t* out) {
+  SXEN_REQUIRE(opt != nullptr && out != nullptr, "null argument");
+  *out = opt->t;
+  return SXEN_OK;
+}
+
+sxen_status sxen_sparse_adam_step(sxen_sparse_adam* opt, sxen_encoder* enc, sxen_grad* grad, const sxen_adam_config* cfg,
+                                  int32_t clear_grad, void* stream) {
+  SXEN_REQUIRE(opt != nullptr && enc != nullptr && grad != nullptr && cfg != nullptr, "null argument");
+  // src/optimizer.cpp:57-61
+  SXEN_REQUIRE(enc->cfg.levels == opt->levels && enc->cfg.features == opt->features &&
+                   enc->cfg.table_size == opt->table_size && grad->levels == opt->levels &&
+                   grad->features == opt->features && grad->table_size == opt->table_size &&
+                   enc->device == opt->device && grad->device == opt->device,
+               "sparse adam step: encoder/gradient shape mismatch");
+  DeviceGuard guard(opt->device);
+  ++opt->t;  // the step counter is global: it advances even for rows that are never touched (src/optimizer.cpp:64)
+  const AdamScalars c = scalars(*cfg, opt->t);
+  const size_t rows = static_cast<size_t>(opt->levels) * opt->table_size;
+  if (opt->features == 2) {
+    sparse_adam_f2_kernel<<<grid_for(rows), 256, 0, as_stream(stream)>>>(
+        reinterpret_cast<float2*>(enc->tables), reinterpret_cast<float2*>(grad->values),
+        reinterpret_cast<double2*>(opt->m), reinterpret_cast<double2*>(opt->v), rows, c, clear_grad, opt->status);
+  } else {
+    sparse_adam_kernel<<<grid_for(rows), 256, 0, as_stream(stream)>>>(enc->tables, grad->values, opt->m, opt->v, rows,
+                                                                      opt->features, c, clear_grad, opt->status);
+  }
+  SXEN_CUDA(cudaGetLastError());
+  count_launch();
+  return SXEN_OK;
+}
+
+sxen_status sxen_sparse_adam_check(sxen_sparse_adam* opt, void* stream) {
+  SXEN_REQUIRE(opt != nullptr, "optimizer handle is null");
+  DeviceGuard guard(opt->device);
+  return check_status(opt, as_stream(stream), "non-finite table gradient at flat element");
+}
+
+sxen_status sxen_sparse_adam_download(const sxen_sparse_adam* opt, int32_t level, double* m_host, double* v_host) {
+  SXEN_REQUIRE(opt != nullptr && m_host != nullptr && v_host != nullptr, "null argument");
+  SXEN_REQUIRE(level >= 0 && level < opt->levels, "sparse adam: level out of range");
+  DeviceGuard guard(opt->device);
+  const size_t per = static_cast<size_t>(opt->table_size) * static_cast<size_t>(opt->features);
+  SXEN_CUDA(cudaMemcpy(m_host, opt->m + static_cast<size_t>(level) * per, per * sizeof(double), cudaMemcpyDeviceToHost));
+  SXEN_CUDA(cudaMemcpy(v_host, opt->v + static_cast<size_t>(level) * per, per * sizeof(double), cudaMemcpyDeviceToHost));
+  return SXEN_OK;
+}
+
+sxen_status sxen_adam_create(size_t size, int32_t device, sxen_adam** out) {
+  SXEN_REQUIRE(out != nullptr, "null argument");
+  *out = nullptr;
+  int ndev = 0;
+  SXEN_CUDA(cudaGetDeviceCount(&ndev));
+  SXEN_REQUIRE(device >= 0 && device < ndev, "device %d out of range (%d visible)", device, ndev);
+  DeviceGuard guard(device);
+  sxen_adam* o = new sxen_adam();
+  o->device = device;
+  o->size = size;
+  const size_t bytes = (size ? size : 1) * sizeof(double);
+  cudaError_t err = cudaMalloc(&o->m, bytes);
+  if (err == cudaSuccess) err = cudaMalloc(&o->v, bytes);
+  if (err == cudaSuccess) err = cudaMemset(o->m, 0, bytes);
+  if (err == cudaSuccess) err = cudaMemset(o->v, 0, bytes);
+  if (err != cudaSuccess) {
+    sxen_adam_destroy(o);
+    return cuda_fail(err, "sxen_adam_create allocation");
+  }
+  if (sxen_status st = alloc_status(o)) {
+    sxen_adam_destroy(o);
+    return st;
+  }
+  *out = o;
+  return SXEN_OK;
+}
+
+sxen_status sxen_adam_destroy(sxen_adam* opt) {
+  if (!opt) return SXEN_OK;
+  DeviceGuard guard(opt->device);
+  cudaFree(opt->m);
+  cudaFree(opt->v);
+  cudaFree(opt->status);
+  cudaFreeHost(opt->status_host);
+  delete opt;
+  return SXEN_OK;
+}
+
+sxen_status sxen_adam_step_count(const sxen_adam* opt, int64_t* out) {
+  SXEN_REQUIRE(opt != nullptr && out != nullptr, "null argument");
+  *out = opt->t;
+  return SXEN_OK;
+}
+
+sxen_status sxen_adam_step(sxen_adam* opt, float* params_dev, const void* grads_dev, sxen_coord_type grad_type,
+                           size_t size, const sxen_adam_config* cfg, void* stream) {
+  SXEN_REQUIRE(opt != nullptr && cfg != nullptr, "null argument");
+  // src/optimizer.cpp:27-29
+  SXEN_REQUIRE(size == opt->size, "adam step: parameter/gradient size mismatch");
+  SXEN_REQUIRE(size == 0 || (params_dev != nullptr && grads_dev != nullptr), "adam step: null parameter or gradient pointer");
+  DeviceGuard guard(opt->device);
+  ++opt->t;
+  if (size == 0) return SXEN_OK;
+  const AdamScalars c = scalars(*cfg, opt->t);
+  if (grad_type == SXEN_COORD_F32) {
+    dense_adam_kernel<float><<<grid_for(size), 256, 0, as_stream(stream)>>>(
+        params_dev, static_cast<const float*>(grads_dev), opt->m, opt->v, size, c, opt->status);
+  } else {
+    dense_adam_kernel<double><<<grid_for(size), 256, 0, as_stream(stream)>>>(
+        params_dev, static_cast<const double*>(grads_dev), opt->m, opt->v, size, c, opt->status);
+  }
+  SXEN_CUDA(cudaGetLastError());
+  count_launch();
+  return SXEN_OK;
+}
+
+sxen_status sxen_adam_check(sxen_adam* opt, void* stream) {
+  SXEN_REQUIRE(opt != nullptr, "optimizer handle is null");
+  DeviceGuard guard(opt->device);
+  return check_status(opt, as_stream(stream), "non-finite gradient at parameter");
+}
+
+}  // extern "C"

@@ -98,7 +98,9 @@ typedef struct sxen_tuning {
   int32_t exact_blend;       /* 1: fp64 chain-order blend, features bit-identical to the reference; 0: fp32 FMA blend */
   int32_t warp_aggregate;    /* backward: merge equal rows inside a warp before the atomic on levels whose
                                 lattice has at most this many vertices (0 = off) */
-  int32_t reserved[3];
+  int32_t merge_pairs;       /* backward, F == 2: chain vertices whose rows share a 16-byte slot (idx, idx^1) take one
+                                red.v4 instead of two red.v2.  1 = on (default), -1 = off, 0 = library default */
+  int32_t reserved[2];
 } sxen_tuning;
 
 typedef struct sxen_encoder sxen_encoder;   /* sxen::HashEncoder     (include/sxen/encoding.hpp:92-148) */

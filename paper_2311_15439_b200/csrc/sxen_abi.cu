@@ -87,6 +87,7 @@ sxen_tuning default_tuning() {
   t.level_major = 0;
   t.exact_blend = 1;
   t.warp_aggregate = 0;
+  t.merge_pairs = 1;
   return t;
 }
 
@@ -221,6 +222,7 @@ sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, c
   a.out = out;
   a.grads = grad ? grad->values : nullptr;
   a.level_major = enc->tuning.level_major ? 1 : 0;
+  a.merge_pairs = (enc->tuning.merge_pairs > 0 && enc->cfg.table_size >= 2) ? 1 : 0;
   EncodeLaunch ln{};
   ln.features = enc->cfg.features;
   ln.lpt = enc->tuning.levels_per_thread;
@@ -459,6 +461,7 @@ sxen_status sxen_encoder_set_tuning(sxen_encoder* enc, const sxen_tuning* t) {
   if (n.block_threads <= 0) n.block_threads = d.block_threads;
   SXEN_REQUIRE(n.block_threads % 32 == 0 && n.block_threads <= 1024, "block_threads must be a multiple of 32, <= 1024");
   SXEN_REQUIRE(n.warp_aggregate >= 0, "warp_aggregate must be >= 0");
+  if (n.merge_pairs == 0) n.merge_pairs = d.merge_pairs;
   enc->tuning = n;
   return SXEN_OK;
 }

@@ -35,6 +35,7 @@ struct EncodeArgs {
   int32_t level_major;           // 1: blockIdx.y = level group
   int32_t vec;                   // proven float alignment of every thread's out/upstream chunk: 4, 2 or 1
   uint32_t agg_mask;             // bit l: warp-aggregate the backward atomics of local level l
+  int32_t merge_pairs;           // F == 2: one red.v4 for two chain vertices in the same 16-byte slot
   double skew;                   // F_n
   LevelGeom geom;
 };
@@ -194,19 +195,43 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
       if constexpr (kBwd) {
         float* __restrict__ gl = a.grads + level_off;
         const bool agg = (aggm >> (threadIdx.x & 31)) & 1u;
+        // EncoderGradient::add, src/encoding.cpp:110-120: dst[f] += scale * upstream[f]
+        float v[ND + 1][F];
 #pragma unroll
         for (int k = 0; k <= ND; ++k) {
-          // EncoderGradient::add, src/encoding.cpp:110-120: dst[f] += scale * upstream[f]
           const float wk = static_cast<float>(w[k]);
-          float v[F];
 #pragma unroll
-          for (int f = 0; f < F; ++f) v[f] = canon(__fmul_rn(wk, upv[j * F + f]));
+          for (int f = 0; f < F; ++f) v[k][f] = canon(__fmul_rn(wk, upv[j * F + f]));
+        }
+        bool skip = false;
+#pragma unroll
+        for (int k = 0; k <= ND; ++k) {
+          if (skip) {
+            skip = false;
+            continue;
+          }
+          if constexpr (F == 2) {
+            // The hash multiplies axis 0 by 1 (include/sxen/hashing.hpp:16), so the chain step along axis 0 from an even
+            // coordinate lands on the neighbouring row: rows idx and idx^1 share one 16-byte slot and take ONE
+            // red.v4 instead of two red.v2 (half the L2 atomic requests for that pair).
+            if (k < ND && a.merge_pairs && !agg) {
+              if ((idx[k] ^ idx[k < ND ? k + 1 : k]) == 1u) {
+                const int kn = k < ND ? k + 1 : k;
+                const bool low = (idx[k] & 1u) == 0u;
+                float* p = gl + static_cast<size_t>(idx[k] & ~1u) * 2;
+                red_add4(p, low ? v[k][0] : v[kn][0], low ? v[k][1] : v[kn][1], low ? v[kn][0] : v[k][0],
+                         low ? v[kn][1] : v[k][1]);
+                skip = true;
+                continue;
+              }
+            }
+          }
           bool issue = true;
           if (agg) {
             const unsigned long long key = (static_cast<unsigned long long>(l) << 32) | idx[k];
-            issue = warp_merge_rows<F>(aggm, key, v);
+            issue = warp_merge_rows<F>(aggm, key, v[k]);
           }
-          if (issue) red_row<F>(gl + static_cast<size_t>(idx[k]) * F, v);
+          if (issue) red_row<F>(gl + static_cast<size_t>(idx[k]) * F, v[k]);
         }
       }
     }

@@ -82,10 +82,11 @@ class Tuning:
     level_major: int = 0
     exact_blend: int = 1
     warp_aggregate: int = 0
+    merge_pairs: int = 0  # 1 on, -1 off, 0 library default (on)
 
     def c(self) -> _abi.TuningC:
         return _abi.TuningC(self.levels_per_thread, self.block_threads, self.level_major, self.exact_blend,
-                            self.warp_aggregate, (C.c_int32 * 3)(0, 0, 0))
+                            self.warp_aggregate, self.merge_pairs, (C.c_int32 * 2)(0, 0))
 
 
 def equal_memory_multiplier(n: int) -> float:
@@ -277,7 +278,8 @@ class HashEncoder:
     def tuning(self) -> Tuning:
         c = _abi.TuningC()
         raise_for(self._lib, self._lib.sxen_encoder_get_tuning(self._h, C.byref(c)))
-        return Tuning(c.levels_per_thread, c.block_threads, c.level_major, c.exact_blend, c.warp_aggregate)
+        return Tuning(c.levels_per_thread, c.block_threads, c.level_major, c.exact_blend, c.warp_aggregate,
+                      c.merge_pairs)
 
     # ---- the hot path
     def _check_x(self, x):

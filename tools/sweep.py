@@ -65,13 +65,14 @@ def main():
     rows = []
     print(f"# n={n} N=2^{args.log2n} T=2^{args.log2t} L=16 F=2; ms per launch (mean of {args.reps}), rotating 4 input sets")
     print("lpt blk lm ex agg |   fwd_ms   bwd_ms fused_ms | fwd_Gs/s bwd_Gs/s fused_Gs/s")
-    for lpt, lm, exact, block, agg in itertools.product(lpts, (0, 1), (1, 0), blocks, (0, 1 << 16)):
+    for lpt, lm, exact, block, agg in itertools.product(lpts, (0, 1), (1, 0), blocks, (0, -1)):
         if block > 256 and lpt >= 4:
             continue
         if args.quick and (agg or (exact == 0 and lm == 1)):
             continue
+        # the "agg" column now toggles the pair-merged red.v4 path: 0 = merged (default), -1 = off
         enc.set_tuning(sx.Tuning(levels_per_thread=lpt, block_threads=block, level_major=lm, exact_blend=exact,
-                                 warp_aggregate=agg))
+                                 merge_pairs=-1 if agg else 1))
         fwd = timeit(lambda i: enc.encode(sets[i % 4][0], out=sets[i % 4][2])) if agg == 0 else float("nan")
         bwd = timeit(lambda i: enc.encode_backward(sets[i % 4][0], sets[i % 4][1], grad))
         fused = timeit(lambda i: enc.encode_forward_backward(sets[i % 4][0], sets[i % 4][1], grad, out=sets[i % 4][2]))

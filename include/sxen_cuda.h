@@ -231,6 +231,66 @@ SXEN_API sxen_status sxen_adam_step(sxen_adam* opt, float* params_dev, const voi
                                     size_t size, const sxen_adam_config* cfg, void* stream);
 SXEN_API sxen_status sxen_adam_check(sxen_adam* opt, void* stream);
 
+/* ------------------------------------------------------------------ MLP head (src/mlp.cpp) */
+SXEN_API sxen_status sxen_mlp_config_default(sxen_mlp_config* cfg);
+SXEN_API sxen_status sxen_mlp_validate(const sxen_mlp_config* cfg);                       /* MlpConfig::validate */
+/* Mlp::Mlp: validates, allocates zeroed f32 parameters (per layer: weights out x in row-major, then biases --
+ * src/mlp.cpp:19-32) and the fp64 MlpGradient on `device`. */
+SXEN_API sxen_status sxen_mlp_create(const sxen_mlp_config* cfg, int32_t device, sxen_mlp** out);
+SXEN_API sxen_status sxen_mlp_destroy(sxen_mlp* mlp);
+SXEN_API sxen_status sxen_mlp_get_config(const sxen_mlp* mlp, sxen_mlp_config* out);
+SXEN_API sxen_status sxen_mlp_parameter_count(const sxen_mlp* mlp, uint64_t* out);         /* Mlp::parameter_count */
+SXEN_API sxen_status sxen_mlp_init_params(sxen_mlp* mlp, uint64_t seed, void* stream);     /* Mlp::init_params, bit-identical */
+SXEN_API sxen_status sxen_mlp_upload_params(sxen_mlp* mlp, const float* src_host);         /* Mlp::parameters() */
+SXEN_API sxen_status sxen_mlp_download_params(const sxen_mlp* mlp, float* dst_host);
+SXEN_API sxen_status sxen_mlp_params_dev(sxen_mlp* mlp, float** out_dev);
+SXEN_API sxen_status sxen_mlp_grads_dev(sxen_mlp* mlp, double** out_dev);                  /* MlpGradient::values(), for all-reduce */
+SXEN_API sxen_status sxen_mlp_grad_clear(sxen_mlp* mlp, void* stream);                     /* MlpGradient::clear */
+SXEN_API sxen_status sxen_mlp_grad_download(const sxen_mlp* mlp, double* dst_host);
+/* Mlp::forward, batched (src/mlp.cpp:137-162). input_dev: N x input_width f32; out_dev (may be NULL): N x output_width.
+ * The activations stay in the handle (the batched MlpWorkspace) for the matching backward. */
+SXEN_API sxen_status sxen_mlp_forward(sxen_mlp* mlp, const float* input_dev, size_t n_samples, float* out_dev, void* stream);
+/* Mlp::backward, batched (src/mlp.cpp:164-202). upstream_dev: N x output_width f64; parameter gradients accumulate into
+ * the handle's MlpGradient; d(loss)/d(input) is written as f32 (input_grad_dev) and/or f64 (input_grad_f64_dev), either
+ * may be NULL.  SXEN_LOGIC_ERROR if no forward populated the workspace. */
+SXEN_API sxen_status sxen_mlp_backward(sxen_mlp* mlp, const double* upstream_dev, size_t n_samples, float* input_grad_dev,
+                                       double* input_grad_f64_dev, void* stream);
+/* The workspace of the last forward: [N x act_width] f32 rows, slot 0 = input, the output starts at output_offset. */
+SXEN_API sxen_status sxen_mlp_activations_dev(sxen_mlp* mlp, float** out_dev, size_t* act_width, size_t* output_offset);
+/* run_chunk's loss (src/trainer.cpp:26-44): e = pred - target, sample_loss = sum e^2, upstream = 2e / (global_batch*out_w).
+ * pred_dev rows are pred_stride floats apart; targets N x out_w (f64 or f32); loss_sum_dev (may be NULL) receives the
+ * deterministic sum of sample_loss. */
+SXEN_API sxen_status sxen_mse_loss(const float* pred_dev, size_t pred_stride, const void* targets_dev,
+                                   sxen_coord_type target_type, int32_t out_w, size_t n_samples, size_t global_batch,
+                                   double* upstream_dev, double* sample_loss_dev, double* loss_sum_dev, void* stream);
+
+/* ------------------------------------------------------------------ training step (src/trainer.cpp:94-136) */
+typedef struct sxen_trainer sxen_trainer;
+/* Binds an encoder and an MLP (not owned) with a gradient accumulator, SparseAdamState and AdamState (owned). */
+SXEN_API sxen_status sxen_trainer_create(sxen_encoder* enc, sxen_mlp* mlp, sxen_trainer** out);
+SXEN_API sxen_status sxen_trainer_destroy(sxen_trainer* trainer);
+/* run_chunk over this rank's contiguous chunk: encode -> forward -> MSE -> backward -> encode_backward.  Table and MLP
+ * gradients and the loss sum ACCUMULATE until sxen_trainer_update.  global_batch is the B of upstream = 2e/(B*out_w). */
+SXEN_API sxen_status sxen_trainer_accumulate(sxen_trainer* trainer, const void* coords_dev, sxen_coord_type coord_type,
+                                             const void* targets_dev, sxen_coord_type target_type, size_t n_samples,
+                                             size_t global_batch, void* stream);
+/* Buffers a multi-GPU host all-reduces (SUM) between accumulate and update: the table-gradient accumulator, the MLP
+ * gradient (sxen_mlp_grads_dev) and the loss sum. */
+SXEN_API sxen_status sxen_trainer_table_grad(sxen_trainer* trainer, sxen_grad** out);
+SXEN_API sxen_status sxen_trainer_loss_dev(sxen_trainer* trainer, double** out_dev);
+/* Synchronises; loss = sum / (global_batch*out_w).  SXEN_TRAINING_ERROR if non-finite (src/trainer.cpp:120-123);
+ * SXEN_INVALID_ARGUMENT if a coordinate left the unit cube. */
+SXEN_API sxen_status sxen_trainer_loss(sxen_trainer* trainer, size_t global_batch, double* loss_out, void* stream);
+/* SparseAdamState::step + AdamState::step, then clears the accumulators for the next step (src/trainer.cpp:97-100,129-130). */
+SXEN_API sxen_status sxen_trainer_update(sxen_trainer* trainer, const sxen_adam_config* table_adam,
+                                         const sxen_adam_config* mlp_adam, void* stream);
+SXEN_API sxen_status sxen_trainer_check(sxen_trainer* trainer, void* stream);  /* non-finite gradient -> SXEN_TRAINING_ERROR */
+/* One whole single-GPU step: accumulate + loss + update + check. */
+SXEN_API sxen_status sxen_trainer_step(sxen_trainer* trainer, const void* coords_dev, sxen_coord_type coord_type,
+                                       const void* targets_dev, sxen_coord_type target_type, size_t n_samples,
+                                       const sxen_adam_config* table_adam, const sxen_adam_config* mlp_adam,
+                                       double* loss_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

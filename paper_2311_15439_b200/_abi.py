@@ -102,6 +102,32 @@ SIGNATURES = {
     "sxen_adam_step_count": (C.c_int, [_vp, _P(C.c_int64)]),
     "sxen_adam_step": (C.c_int, [_vp, _vp, _vp, C.c_int, _sz, _P(AdamConfigC), _vp]),
     "sxen_adam_check": (C.c_int, [_vp, _vp]),
+    "sxen_mlp_config_default": (C.c_int, [_P(MlpConfigC)]),
+    "sxen_mlp_validate": (C.c_int, [_P(MlpConfigC)]),
+    "sxen_mlp_create": (C.c_int, [_P(MlpConfigC), _i32, _P(_vp)]),
+    "sxen_mlp_destroy": (C.c_int, [_vp]),
+    "sxen_mlp_get_config": (C.c_int, [_vp, _P(MlpConfigC)]),
+    "sxen_mlp_parameter_count": (C.c_int, [_vp, _P(_u64)]),
+    "sxen_mlp_init_params": (C.c_int, [_vp, _u64, _vp]),
+    "sxen_mlp_upload_params": (C.c_int, [_vp, _P(C.c_float)]),
+    "sxen_mlp_download_params": (C.c_int, [_vp, _P(C.c_float)]),
+    "sxen_mlp_params_dev": (C.c_int, [_vp, _P(_vp)]),
+    "sxen_mlp_grads_dev": (C.c_int, [_vp, _P(_vp)]),
+    "sxen_mlp_grad_clear": (C.c_int, [_vp, _vp]),
+    "sxen_mlp_grad_download": (C.c_int, [_vp, _P(_dbl)]),
+    "sxen_mlp_forward": (C.c_int, [_vp, _vp, _sz, _vp, _vp]),
+    "sxen_mlp_backward": (C.c_int, [_vp, _vp, _sz, _vp, _vp, _vp]),
+    "sxen_mlp_activations_dev": (C.c_int, [_vp, _P(_vp), _P(_sz), _P(_sz)]),
+    "sxen_mse_loss": (C.c_int, [_vp, _sz, _vp, C.c_int, _i32, _sz, _sz, _vp, _vp, _vp, _vp]),
+    "sxen_trainer_create": (C.c_int, [_vp, _vp, _P(_vp)]),
+    "sxen_trainer_destroy": (C.c_int, [_vp]),
+    "sxen_trainer_accumulate": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, _sz, _sz, _vp]),
+    "sxen_trainer_table_grad": (C.c_int, [_vp, _P(_vp)]),
+    "sxen_trainer_loss_dev": (C.c_int, [_vp, _P(_vp)]),
+    "sxen_trainer_loss": (C.c_int, [_vp, _sz, _P(_dbl), _vp]),
+    "sxen_trainer_update": (C.c_int, [_vp, _P(AdamConfigC), _P(AdamConfigC), _vp]),
+    "sxen_trainer_check": (C.c_int, [_vp, _vp]),
+    "sxen_trainer_step": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, _sz, _P(AdamConfigC), _P(AdamConfigC), _P(_dbl), _vp]),
 }
 
 

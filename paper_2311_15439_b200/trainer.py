@@ -1,0 +1,176 @@
+"""Training-step mirror (include/sxen/trainer.hpp, src/trainer.cpp) over sxen_trainer_*.
+
+``train_field`` follows the reference's contract: a BatchSampler fills (coords, aux, targets) for each step, the step
+runs encode -> forward -> MSE -> backward -> encode_backward, then sparse Adam on the tables and dense Adam on the MLP.
+With ``world_size > 1`` (torch.distributed initialised) each rank takes its contiguous chunk of the batch exactly as the
+reference's workers do (src/trainer.cpp:93,107-108) and the gradient buffers are all-reduced where the reference merges
+its per-worker accumulators (:125-128)."""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Callable, List, Tuple
+
+from . import _abi
+from .errors import TrainingError, raise_for
+from .optimizer import AdamConfig
+
+
+def _lib():
+    from . import lib
+    return lib
+
+
+@dataclass
+class TrainConfig:
+    """sxen::TrainConfig, same defaults (include/sxen/trainer.hpp:15-24).  `threads` has no device meaning."""
+
+    batch_size: int = 2048
+    steps: int = 10000
+    aux_dims: int = 0
+    table_adam: AdamConfig = field(default_factory=lambda: AdamConfig(lr=1e-2, beta1=0.9, beta2=0.99, epsilon=1e-15))
+    mlp_adam: AdamConfig = field(default_factory=lambda: AdamConfig(lr=1e-3, beta1=0.9, beta2=0.99, epsilon=1e-15))
+    seed: int = 1234
+    threads: int = 0
+    record_every: int = 100
+
+
+@dataclass
+class TrainResult:
+    loss_curve: List[Tuple[int, float]] = field(default_factory=list)
+    final_loss: float = 0.0
+    steps_run: int = 0
+
+
+def chunk_bounds(batch: int, workers: int, worker: int) -> Tuple[int, int]:
+    """The reference's contiguous chunking (src/trainer.cpp:93,107-108): chunk = ceil(B/T), worker t takes
+    [t*chunk, min(B, (t+1)*chunk)).  Ranks play the workers."""
+    chunk = (batch + workers - 1) // workers
+    begin = min(batch, worker * chunk)
+    return begin, min(batch, begin + chunk)
+
+
+class Trainer:
+    """Owns the gradient accumulator and both Adam states for one (encoder, mlp) pair."""
+
+    def __init__(self, encoder, mlp):
+        self._lib = _lib()
+        self._h = C.c_void_p()
+        self.encoder, self.mlp = encoder, mlp
+        raise_for(self._lib, self._lib.sxen_trainer_create(encoder._h, mlp._h, C.byref(self._h)))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            self._lib.sxen_trainer_destroy(self._h)
+            self._h = None
+
+    @staticmethod
+    def _typ(t):
+        import torch
+        return {torch.float64: _abi.COORD_F64, torch.float32: _abi.COORD_F32}[t.dtype]
+
+    def accumulate(self, coords, targets, global_batch: int, stream=None) -> None:
+        from .encoding import _stream_ptr
+        coords, targets = coords.contiguous(), targets.contiguous()
+        raise_for(self._lib, self._lib.sxen_trainer_accumulate(
+            self._h, C.c_void_p(coords.data_ptr()), self._typ(coords), C.c_void_p(targets.data_ptr()),
+            self._typ(targets), coords.shape[0], global_batch, _stream_ptr(stream)))
+
+    def table_grad_device(self):
+        """Flat float32 view of the table-gradient accumulator (untouched rows carry -0.0; SUM all-reduce keeps that)."""
+        import torch
+        from .encoding import _wrap_device
+        g = C.c_void_p()
+        raise_for(self._lib, self._lib.sxen_trainer_table_grad(self._h, C.byref(g)))
+        ptr, cnt = C.c_void_p(), C.c_size_t()
+        raise_for(self._lib, self._lib.sxen_grad_values_dev(g, C.byref(ptr), C.byref(cnt)))
+        return _wrap_device(ptr.value, cnt.value, torch.float32, self)
+
+    def loss_device(self):
+        import torch
+        from .encoding import _wrap_device
+        p = C.c_void_p()
+        raise_for(self._lib, self._lib.sxen_trainer_loss_dev(self._h, C.byref(p)))
+        return _wrap_device(p.value, 1, torch.float64, self)
+
+    def loss(self, global_batch: int, stream=None) -> float:
+        from .encoding import _stream_ptr
+        out = C.c_double()
+        raise_for(self._lib, self._lib.sxen_trainer_loss(self._h, global_batch, C.byref(out), _stream_ptr(stream)))
+        return out.value
+
+    def update(self, table_adam: AdamConfig, mlp_adam: AdamConfig, stream=None, check: bool = True) -> None:
+        from .encoding import _stream_ptr
+        ta, ma = table_adam.c(), mlp_adam.c()
+        raise_for(self._lib, self._lib.sxen_trainer_update(self._h, C.byref(ta), C.byref(ma), _stream_ptr(stream)))
+        if check:
+            raise_for(self._lib, self._lib.sxen_trainer_check(self._h, _stream_ptr(stream)))
+
+    def step(self, coords, targets, table_adam: AdamConfig, mlp_adam: AdamConfig, stream=None) -> float:
+        """One whole single-GPU step; returns the batch MSE before the update (TrainResult::loss_curve's value)."""
+        from .encoding import _stream_ptr
+        coords, targets = coords.contiguous(), targets.contiguous()
+        ta, ma = table_adam.c(), mlp_adam.c()
+        out = C.c_double()
+        raise_for(self._lib, self._lib.sxen_trainer_step(
+            self._h, C.c_void_p(coords.data_ptr()), self._typ(coords), C.c_void_p(targets.data_ptr()),
+            self._typ(targets), coords.shape[0], C.byref(ta), C.byref(ma), C.byref(out), _stream_ptr(stream)))
+        return out.value
+
+    def distributed_step(self, coords, targets, table_adam: AdamConfig, mlp_adam: AdamConfig, group=None) -> float:
+        """Batch-sharded step: coords/targets hold the WHOLE batch on every rank (the sampler is deterministic in
+        (seed, step), so no scatter is needed); this rank runs its contiguous chunk, then table gradients, MLP gradients
+        and the loss sum are all-reduced (SUM) and every rank applies the identical update."""
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        batch = coords.shape[0]
+        b, e = chunk_bounds(batch, world, rank)
+        self.accumulate(coords[b:e], targets[b:e], batch)
+        dist.all_reduce(self.table_grad_device(), group=group)
+        dist.all_reduce(self.mlp.gradient_device(), group=group)
+        dist.all_reduce(self.loss_device(), group=group)
+        loss = self.loss(batch)
+        self.update(table_adam, mlp_adam)
+        return loss
+
+
+BatchSampler = Callable[[int, int], tuple]  # (step, batch) -> (coords [B, dim], targets [B, out_w]) CUDA tensors
+
+
+def train_field(encoder, mlp, sampler: BatchSampler, cfg: TrainConfig, group=None) -> TrainResult:
+    """sxen::train_field (src/trainer.cpp:53-139)."""
+    if cfg.batch_size < 1:
+        raise ValueError("train: batch_size must be >= 1")
+    if cfg.steps < 0:
+        raise ValueError("train: steps must be >= 0")
+    if cfg.aux_dims != 0:
+        raise ValueError("train: aux_dims must be 0 on the device path")
+    if cfg.record_every < 1:
+        raise ValueError("train: record_every must be >= 1")
+    if sampler is None:
+        raise ValueError("train: sampler must be callable")
+    trainer = Trainer(encoder, mlp)
+    distributed = False
+    if group is not None:
+        distributed = True
+    else:
+        try:
+            import torch.distributed as dist
+            distributed = dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+        except Exception:
+            distributed = False
+    result = TrainResult()
+    for step in range(cfg.steps):
+        coords, targets = sampler(step, cfg.batch_size)
+        if distributed:
+            loss = trainer.distributed_step(coords, targets, cfg.table_adam, cfg.mlp_adam, group)
+        else:
+            loss = trainer.step(coords, targets, cfg.table_adam, cfg.mlp_adam)
+        if not math.isfinite(loss):
+            raise TrainingError(f"loss became non-finite at step {step}")
+        if step % cfg.record_every == 0 or step == cfg.steps - 1:
+            result.loss_curve.append((step, loss))
+        result.final_loss = loss
+    result.steps_run = cfg.steps
+    return result

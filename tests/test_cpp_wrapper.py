@@ -1,0 +1,19 @@
+"""CPU: include/sxen_b200.hpp (the C++ mirror of the reference classes) compiles against the C ABI, links with
+libsxen_b200.so and its host-only entry points throw the reference's exception types."""
+import os
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_cpp_wrapper_builds_and_runs(tmp_path):
+    lib_dir = os.path.join(ROOT, "paper_2311_15439_b200", "lib")
+    if not os.path.exists(os.path.join(lib_dir, "libsxen_b200.so")):
+        import __graft_entry__
+        __graft_entry__.build()
+    exe = str(tmp_path / "wrapper_host_check")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "wrapper_host_check.cpp"), "-o", exe, "-L", lib_dir,
+                    "-lsxen_b200", f"-Wl,-rpath,{lib_dir}"], check=True)
+    out = subprocess.run([exe], check=True, capture_output=True, text=True).stdout
+    assert "wrapper ok" in out

@@ -255,6 +255,18 @@ SXEN_API sxen_status sxen_mlp_forward(sxen_mlp* mlp, const float* input_dev, siz
  * may be NULL.  SXEN_LOGIC_ERROR if no forward populated the workspace. */
 SXEN_API sxen_status sxen_mlp_backward(sxen_mlp* mlp, const double* upstream_dev, size_t n_samples, float* input_grad_dev,
                                        double* input_grad_f64_dev, void* stream);
+/* Arithmetic of the head.  EXACT (default): fp64 accumulation in the reference's order, any shape, bit-identical outputs.
+ * TENSOR_*: the fused tcgen05 kernel for the 32 -> 64 -> 64 -> {<=3} head; BF16X3 = split-bf16 operands (three MMAs per
+ * product, ~1e-5 relative), BF16 = single bf16 product (~4e-3). */
+typedef enum sxen_mlp_precision { SXEN_MLP_EXACT = 0, SXEN_MLP_TENSOR_BF16X3 = 1, SXEN_MLP_TENSOR_BF16 = 2 } sxen_mlp_precision;
+SXEN_API sxen_status sxen_mlp_set_precision(sxen_mlp* mlp, int32_t precision);
+SXEN_API sxen_status sxen_mlp_get_precision(const sxen_mlp* mlp, int32_t* out);
+/* Mlp::forward + run_chunk's MSE/upstream + Mlp::backward of one batch (src/trainer.cpp:36-46) in one call: parameter
+ * gradients accumulate into the handle, d(loss)/d(input) goes to input_grad_dev (N x input_width f32), the sum of the
+ * per-sample losses is ADDED to *loss_sum_dev (may be NULL), predictions go to pred_dev (may be NULL). */
+SXEN_API sxen_status sxen_mlp_forward_backward(sxen_mlp* mlp, const float* input_dev, const void* targets_dev,
+                                               sxen_coord_type target_type, size_t n_samples, size_t global_batch,
+                                               float* pred_dev, float* input_grad_dev, double* loss_sum_dev, void* stream);
 /* The workspace of the last forward: [N x act_width] f32 rows, slot 0 = input, the output starts at output_offset. */
 SXEN_API sxen_status sxen_mlp_activations_dev(sxen_mlp* mlp, float** out_dev, size_t* act_width, size_t* output_offset);
 /* run_chunk's loss (src/trainer.cpp:26-44): e = pred - target, sample_loss = sum e^2, upstream = 2e / (global_batch*out_w).

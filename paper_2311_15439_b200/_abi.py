@@ -14,6 +14,7 @@ OK, INVALID_ARGUMENT, LOGIC_ERROR, TRAINING_ERROR, CUDA_ERROR, IO_ERROR = range(
 BACKEND_SIMPLEX, BACKEND_GRID = 0, 1
 SCALE_RAW, SCALE_EQUAL_MEMORY = 0, 1
 COORD_F64, COORD_F32 = 0, 1
+MLP_EXACT, MLP_TENSOR_BF16X3, MLP_TENSOR_BF16 = 0, 1, 2
 
 
 class EncoderConfigC(C.Structure):
@@ -117,6 +118,9 @@ SIGNATURES = {
     "sxen_mlp_grad_download": (C.c_int, [_vp, _P(_dbl)]),
     "sxen_mlp_forward": (C.c_int, [_vp, _vp, _sz, _vp, _vp]),
     "sxen_mlp_backward": (C.c_int, [_vp, _vp, _sz, _vp, _vp, _vp]),
+    "sxen_mlp_set_precision": (C.c_int, [_vp, _i32]),
+    "sxen_mlp_get_precision": (C.c_int, [_vp, _P(_i32)]),
+    "sxen_mlp_forward_backward": (C.c_int, [_vp, _vp, _vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _vp]),
     "sxen_mlp_activations_dev": (C.c_int, [_vp, _P(_vp), _P(_sz), _P(_sz)]),
     "sxen_mse_loss": (C.c_int, [_vp, _sz, _vp, C.c_int, _i32, _sz, _sz, _vp, _vp, _vp, _vp]),
     "sxen_trainer_create": (C.c_int, [_vp, _vp, _P(_vp)]),

@@ -24,6 +24,8 @@ struct sxen_mlp {
   size_t acts_capacity = 0;  // samples
   size_t forward_samples = 0;
   bool forward_done = false;
+  int precision = SXEN_MLP_EXACT;  // sxen_mlp_precision
+  double* loss_scratch = nullptr;  // 1 double, used when the caller does not want the loss
   int layer_count() const { return cfg.hidden_layers + 1; }
   int layer_in(int l) const { return l == 0 ? cfg.input_width : cfg.hidden_width; }
   int layer_out(int l) const { return l == layer_count() - 1 ? cfg.output_width : cfg.hidden_width; }
@@ -33,6 +35,12 @@ struct sxen_mlp {
     return w;
   }
 };
+
+// sxen_mlp_tc.cu
+bool sxen_mlp_tc_supported(const sxen_mlp_config& c);
+sxen_status sxen_mlp_tc_run(bool train, const float* params, const float* features, const void* targets, int target_f32,
+                            float* pred, float* input_grad, double* mlp_grad, double* loss_sum, size_t n, int out_w,
+                            size_t global_batch, int precise, cudaStream_t stream);
 
 namespace {
 
@@ -249,6 +257,8 @@ __global__ void __launch_bounds__(1024) sum_kernel(const double* __restrict__ v,
   if (threadIdx.x == 0) *out = part[0];
 }
 
+__global__ void add_scalar_kernel(double* __restrict__ acc, const double* __restrict__ v) { *acc += *v; }
+
 int grid_for(size_t n, int block = 256) {
   size_t b = (n + block - 1) / block;
   if (b > 148 * 16) b = 148 * 16;
@@ -312,6 +322,7 @@ sxen_status sxen_mlp_destroy(sxen_mlp* mlp) {
   cudaFree(mlp->params);
   cudaFree(mlp->grads);
   cudaFree(mlp->acts);
+  cudaFree(mlp->loss_scratch);
   delete mlp;
   return SXEN_OK;
 }
@@ -377,10 +388,72 @@ sxen_status sxen_mlp_grad_download(const sxen_mlp* mlp, double* dst_host) {
   return SXEN_OK;
 }
 
+sxen_status sxen_mlp_set_precision(sxen_mlp* mlp, int32_t precision) {
+  SXEN_REQUIRE(mlp != nullptr, "mlp handle is null");
+  SXEN_REQUIRE(precision == SXEN_MLP_EXACT || precision == SXEN_MLP_TENSOR_BF16X3 || precision == SXEN_MLP_TENSOR_BF16,
+               "mlp: unknown precision mode %d", precision);
+  SXEN_REQUIRE(precision == SXEN_MLP_EXACT || sxen_mlp_tc_supported(mlp->cfg),
+               "mlp: the tensor-core path covers input 32, hidden 64 x 2 layers, output <= 3; this head is %d/%d x %d/%d",
+               mlp->cfg.input_width, mlp->cfg.hidden_width, mlp->cfg.hidden_layers, mlp->cfg.output_width);
+  mlp->precision = precision;
+  return SXEN_OK;
+}
+
+sxen_status sxen_mlp_get_precision(const sxen_mlp* mlp, int32_t* out) {
+  SXEN_REQUIRE(mlp != nullptr && out != nullptr, "null argument");
+  *out = mlp->precision;
+  return SXEN_OK;
+}
+
+// Forward + MSE + backward of one batch in one call (what run_chunk does per sample, src/trainer.cpp:36-46).
+// Tensor-core modes run the fused tcgen05 kernel; the exact mode chains forward, sxen_mse_loss and backward.
+sxen_status sxen_mlp_forward_backward(sxen_mlp* mlp, const float* input_dev, const void* targets_dev,
+                                      sxen_coord_type target_type, size_t n_samples, size_t global_batch, float* pred_dev,
+                                      float* input_grad_dev, double* loss_sum_dev, void* stream) {
+  SXEN_REQUIRE(mlp != nullptr, "mlp handle is null");
+  SXEN_REQUIRE(n_samples == 0 || (input_dev && targets_dev && input_grad_dev), "mlp forward_backward: null pointer");
+  SXEN_REQUIRE(global_batch >= 1, "mlp forward_backward: global batch must be >= 1");
+  if (n_samples == 0) return SXEN_OK;
+  DeviceGuard guard(mlp->device);
+  cudaStream_t st = as_stream(stream);
+  if (!mlp->loss_scratch) SXEN_CUDA(cudaMalloc(&mlp->loss_scratch, sizeof(double)));
+  if (mlp->precision != SXEN_MLP_EXACT) {
+    double* loss = loss_sum_dev ? loss_sum_dev : mlp->loss_scratch;
+    mlp->forward_done = false;  // no activations are kept: a separate backward would be a logic error
+    return sxen_mlp_tc_run(true, mlp->params, input_dev, targets_dev, target_type == SXEN_COORD_F32 ? 1 : 0, pred_dev,
+                           input_grad_dev, mlp->grads, loss, n_samples, mlp->cfg.output_width, global_batch,
+                           mlp->precision == SXEN_MLP_TENSOR_BF16X3 ? 1 : 0, st);
+  }
+  if (sxen_status s = sxen_mlp_forward(mlp, input_dev, n_samples, pred_dev, stream)) return s;
+  const MlpShape sh = shape_of(mlp);
+  double* scratch = nullptr;  // upstream [N x ow], sample loss [N], batch sum [1]
+  const size_t ow = static_cast<size_t>(mlp->cfg.output_width);
+  SXEN_CUDA(cudaMallocAsync(&scratch, (n_samples * (ow + 1) + 1) * sizeof(double), st));
+  double* upstream = scratch;
+  double* sample_loss = scratch + n_samples * ow;
+  double* batch_sum = sample_loss + n_samples;
+  sxen_status s = sxen_mse_loss(mlp->acts + sh.a_off[sh.layers], sh.act_width, targets_dev, target_type,
+                                mlp->cfg.output_width, n_samples, global_batch, upstream, sample_loss, batch_sum, stream);
+  if (s == SXEN_OK && loss_sum_dev) {
+    add_scalar_kernel<<<1, 1, 0, st>>>(loss_sum_dev, batch_sum);
+    count_launch();
+  }
+  if (s == SXEN_OK) s = sxen_mlp_backward(mlp, upstream, n_samples, input_grad_dev, nullptr, stream);
+  cudaFreeAsync(scratch, st);
+  return s;
+}
+
 sxen_status sxen_mlp_forward(sxen_mlp* mlp, const float* input_dev, size_t n_samples, float* out_dev, void* stream) {
   SXEN_REQUIRE(mlp != nullptr, "mlp handle is null");
   SXEN_REQUIRE(n_samples == 0 || input_dev != nullptr, "mlp forward: input pointer is null");
   DeviceGuard guard(mlp->device);
+  if (mlp->precision != SXEN_MLP_EXACT) {
+    // inference on the tensor cores: outputs only, no workspace (Mlp::backward after this is a logic error)
+    SXEN_REQUIRE(n_samples == 0 || out_dev != nullptr, "mlp forward: output pointer is null");
+    mlp->forward_done = false;
+    return sxen_mlp_tc_run(false, mlp->params, input_dev, nullptr, 0, out_dev, nullptr, nullptr, nullptr, n_samples,
+                           mlp->cfg.output_width, 1, mlp->precision == SXEN_MLP_TENSOR_BF16X3 ? 1 : 0, as_stream(stream));
+  }
   mlp->forward_done = true;
   mlp->forward_samples = n_samples;
   if (n_samples == 0) return SXEN_OK;

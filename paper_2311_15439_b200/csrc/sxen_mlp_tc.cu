@@ -1,0 +1,532 @@
+// sxen_mlp_tc.cu -- the 32 -> 64 -> 64 -> {<=16} MLP head on 5th-generation tensor cores (tcgen05 + TMEM), fully fused:
+// forward, MSE loss + upstream, input gradients and weight gradients of one 128-sample tile never leave the SM.
+//
+// Reference semantics: Mlp::forward / Mlp::backward and run_chunk's loss (/root/reference/proj/src/mlp.cpp:137-202,
+// src/trainer.cpp:26-48).  The reference accumulates in fp64; here every GEMM runs as split-bf16 ("bf16x3"):
+// x = hi + lo with hi = bf16(x), lo = bf16(x - hi), D += A_hi*B_hi + A_hi*B_lo + A_lo*B_hi in fp32 TMEM accumulators,
+// i.e. ~16 mantissa bits per operand, relative error ~1e-5 per product (tests state the tolerance).
+// kind::tf32 was not usable: on sm_100a MN-major tf32 operands produce zeros (tools/tc_probe.py), and the weight-gradient
+// GEMMs need the sample dimension as K, i.e. MN-major views of the activation tiles.
+//
+// Layout: all operand tiles are bf16 CM16 tiles (sxen_tc.cuh), self-dual, so ONE activation tile [128 samples][features]
+// is the K-major A operand of the next layer, the K-major A operand of the input-gradient GEMM and the MN-major operand of
+// the weight-gradient GEMM.  Each tile carries one extra 8-column block whose first column is 1.0: used as the B operand of
+// a weight-gradient GEMM it makes the bias gradient fall out as column `in` of the same accumulator.
+// One CTA = 128 threads = 128 TMEM lanes = 128 samples; thread t owns sample t of the tile in every epilogue.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "sxen_common.hpp"
+#include "sxen_tc.cuh"
+
+using namespace sxen_host;
+using namespace sxen_tc;
+
+namespace {
+
+constexpr int kTile = 128;
+constexpr int IN = 32, HID = 64, OUTP = 16;
+constexpr int X0C = IN + 8, HC = HID + 8;  // tile widths including the ones-column block
+
+// shared-memory map (bytes)
+constexpr uint32_t kW0 = 0;                                     // CM16(64, 32) hi, lo
+constexpr uint32_t kW1 = kW0 + 2 * cm16_bytes(HID, IN);         // CM16(64, 64) hi, lo
+constexpr uint32_t kW2 = kW1 + 2 * cm16_bytes(HID, HID);        // CM16(16, 64) hi, lo (rows >= out_w are zero)
+constexpr uint32_t kX0 = kW2 + 2 * cm16_bytes(OUTP, HID);       // CM16(128, 40) hi, lo
+constexpr uint32_t kH1 = kX0 + 2 * cm16_bytes(kTile, X0C);      // CM16(128, 72) hi, lo
+constexpr uint32_t kH2 = kH1 + 2 * cm16_bytes(kTile, HC);
+constexpr uint32_t kDY = kH2 + 2 * cm16_bytes(kTile, HC);       // CM16(128, 16) hi, lo
+constexpr uint32_t kDH2 = kDY + 2 * cm16_bytes(kTile, OUTP);    // CM16(128, 64) hi, lo
+constexpr uint32_t kDH1 = kDH2 + 2 * cm16_bytes(kTile, HID);
+constexpr uint32_t kBias = kDH1 + 2 * cm16_bytes(kTile, HID);   // b0[64], b1[64], b2[16] floats
+constexpr uint32_t kSmemBytes = kBias + (HID + HID + OUTP) * 4;
+
+// TMEM columns (fp32): scratch accumulators (128 lanes) and the persistent weight-gradient accumulators (M = 64)
+constexpr uint32_t tS0 = 0;     // [128 x 64] layer-1 pre-activation, later dH2
+constexpr uint32_t tS1 = 64;    // [128 x 64] layer-2 pre-activation, later dH1
+constexpr uint32_t tS2 = 128;   // [128 x 32] output (16 cols), later d(input) (32 cols)
+constexpr uint32_t tG0 = 160;   // [64 x 40]  dW0 | db0
+constexpr uint32_t tG1 = 200;   // [64 x 72]  dW1 | db1
+constexpr uint32_t tG2 = 272;   // [64 x 16]  dW2^T
+constexpr uint32_t kTmemCols = 512;
+
+struct TcArgs {
+  const float* params;      // W0[64x32] b0[64] W1[64x64] b1[64] W2[ow x 64] b2[ow]  (src/mlp.cpp:19-32)
+  const float* features;    // N x 32
+  const void* targets;      // N x ow, f32 or f64
+  float* pred;              // N x ow or nullptr
+  float* input_grad;        // N x 32 (training)
+  double* mlp_grad;         // parameter layout, accumulated into
+  double* loss_sum;         // accumulated into
+  unsigned long long n;
+  int out_w;
+  int target_f32;
+  int precise;              // 1: bf16x3, 0: single bf16 product
+  double upstream_scale;    // 2 / (global_batch * out_w)
+};
+
+__device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const __nv_bfloat16 h0 = __float2bfloat16_rn(v[2 * q]), h1 = __float2bfloat16_rn(v[2 * q + 1]);
+    const __nv_bfloat16 l0 = __float2bfloat16_rn(v[2 * q] - __bfloat162float(h0));
+    const __nv_bfloat16 l1 = __float2bfloat16_rn(v[2 * q + 1] - __bfloat162float(h1));
+    h[q] = static_cast<uint32_t>(__bfloat16_as_ushort(h0)) | (static_cast<uint32_t>(__bfloat16_as_ushort(h1)) << 16);
+    l[q] = static_cast<uint32_t>(__bfloat16_as_ushort(l0)) | (static_cast<uint32_t>(__bfloat16_as_ushort(l1)) << 16);
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+// Row `row` of a CM16(., cols) hi/lo tile pair: columns [8*chunk, 8*chunk+8) <- v[0..8)
+__device__ __forceinline__ void store_chunk(unsigned char* tile_hi, unsigned char* tile_lo, int row, int chunk, int cols,
+                                            const float* v) {
+  uint4 hi, lo;
+  split8(v, hi, lo);
+  const uint32_t off = cm16_offset(row, 8 * chunk, cols);
+  *reinterpret_cast<uint4*>(tile_hi + off) = hi;
+  *reinterpret_cast<uint4*>(tile_lo + off) = lo;
+}
+
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// D += A*B over `ksteps` UMMA_K=16 steps with split operands.  Descriptor builders are passed as lambdas of the k step.
+template <class DA, class DB>
+__device__ __forceinline__ void gemm_split(uint32_t d, uint32_t idesc, int ksteps, bool accumulate, bool precise,
+                                           DA desc_a /*(tile_is_lo, ks)*/, DB desc_b) {
+  for (int ks = 0; ks < ksteps; ++ks) {
+    mma_bf16(d, desc_a(false, ks), desc_b(false, ks), idesc, accumulate || ks > 0);
+    if (precise) {
+      mma_bf16(d, desc_a(false, ks), desc_b(true, ks), idesc, true);
+      mma_bf16(d, desc_a(true, ks), desc_b(false, ks), idesc, true);
+    }
+  }
+}
+
+template <bool TRAIN>
+__global__ void __launch_bounds__(kTile, 1) mlp_tc_kernel(const __grid_constant__ TcArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base_slot;
+  __shared__ double red_buf[4][4];
+  const int t = threadIdx.x;
+  const int warp = t >> 5;
+  float* bias = reinterpret_cast<float*>(smem + kBias);
+  const float* W0 = a.params;
+  const float* b0 = W0 + HID * IN;
+  const float* W1 = b0 + HID;
+  const float* b1 = W1 + HID * HID;
+  const float* W2 = b1 + HID;
+  const float* b2 = W2 + a.out_w * HID;
+
+  // ---- one-time setup: weights (hi/lo CM16 tiles, rows = output unit, cols = input unit), biases, ones columns
+  for (int e = t; e < HID * IN / 8; e += kTile) {
+    const int o = e / (IN / 8), ch = e % (IN / 8);
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = W0[o * IN + ch * 8 + q];
+    store_chunk(smem + kW0, smem + kW0 + cm16_bytes(HID, IN), o, ch, IN, v);
+  }
+  for (int e = t; e < HID * HID / 8; e += kTile) {
+    const int o = e / (HID / 8), ch = e % (HID / 8);
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = W1[o * HID + ch * 8 + q];
+    store_chunk(smem + kW1, smem + kW1 + cm16_bytes(HID, HID), o, ch, HID, v);
+  }
+  for (int e = t; e < OUTP * HID / 8; e += kTile) {
+    const int o = e / (HID / 8), ch = e % (HID / 8);
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = o < a.out_w ? W2[o * HID + ch * 8 + q] : 0.0f;
+    store_chunk(smem + kW2, smem + kW2 + cm16_bytes(OUTP, HID), o, ch, HID, v);
+  }
+  if (t < HID) {
+    bias[t] = b0[t];
+    bias[HID + t] = b1[t];
+  }
+  if (t < OUTP) bias[2 * HID + t] = t < a.out_w ? b2[t] : 0.0f;
+  {
+    float ones[8] = {1.0f, 0, 0, 0, 0, 0, 0, 0};
+    store_chunk(smem + kX0, smem + kX0 + cm16_bytes(kTile, X0C), t, IN / 8, X0C, ones);
+    store_chunk(smem + kH1, smem + kH1 + cm16_bytes(kTile, HC), t, HID / 8, HC, ones);
+    store_chunk(smem + kH2, smem + kH2 + cm16_bytes(kTile, HC), t, HID / 8, HC, ones);
+  }
+  if (t == 0) mbar_init(&bar, 1);
+  if (warp == 0) tmem_alloc(&tmem_base_slot, kTmemCols);
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tb = tmem_base_slot;
+  const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+  uint32_t phase = 0;
+  const bool precise = a.precise != 0;
+
+  const uint32_t sW0 = smem_u32(smem + kW0), sW1 = smem_u32(smem + kW1), sW2 = smem_u32(smem + kW2);
+  const uint32_t sX0 = smem_u32(smem + kX0), sH1 = smem_u32(smem + kH1), sH2 = smem_u32(smem + kH2);
+  const uint32_t sDY = smem_u32(smem + kDY), sDH2 = smem_u32(smem + kDH2), sDH1 = smem_u32(smem + kDH1);
+  constexpr uint32_t loW0 = cm16_bytes(HID, IN), loW1 = cm16_bytes(HID, HID), loW2 = cm16_bytes(OUTP, HID);
+  constexpr uint32_t loX0 = cm16_bytes(kTile, X0C), loH = cm16_bytes(kTile, HC), loDY = cm16_bytes(kTile, OUTP),
+                     loDH = cm16_bytes(kTile, HID);
+
+  double loss_acc = 0.0;
+  double db2_acc[3] = {0.0, 0.0, 0.0};  // out_w <= 3 keeps its bias gradient here; wider heads use column sums below
+  bool g_started = false;
+  const unsigned long long n_tiles = (a.n + kTile - 1) / kTile;
+
+  for (unsigned long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const unsigned long long s0 = tile * kTile;
+    const unsigned long long smp = s0 + t;
+    const bool valid = smp < a.n;
+
+    // ---- stage 0: features -> X0 tiles.  Lane mapping: 8 rows x 4 chunks per warp instruction keeps both the global
+    // reads (64 contiguous bytes per row) and the shared stores (8 rows = 8 distinct 16-byte bank groups) efficient.
+    for (int it = 0; it < 4; ++it) {
+      const int row = (t & 7) + 8 * ((t >> 5) + 4 * it);    // 0..127
+      const int ch = (t >> 3) & 3;                          // 8-column chunk 0..3
+      float v[8];
+      const unsigned long long gs = s0 + row;
+      if (gs < a.n) {
+        const float4* p = reinterpret_cast<const float4*>(a.features + gs * IN + ch * 8);
+        const float4 x0 = __ldg(p), x1 = __ldg(p + 1);
+        v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w; v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = 0.0f;
+      }
+      store_chunk(smem + kX0, smem + kX0 + loX0, row, ch, X0C, v);
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+
+    // ---- layer 1: S0 = X0 * W0^T
+    if (t == 0) {
+      tc_fence_after();
+      gemm_split(tb + tS0, make_idesc_bf16(128, HID, false, false), IN / 16, false, precise,
+                 [&](bool lo, int ks) { return desc16_k_major(sX0 + (lo ? loX0 : 0), X0C, ks); },
+                 [&](bool lo, int ks) { return desc16_k_major(sW0 + (lo ? loW0 : 0), IN, ks); });
+      tc_commit(&bar);
+    }
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    unsigned long long m1 = 0, m2 = 0;  // ReLU masks of this thread's sample (bit o = unit o active)
+    {
+      uint32_t r[4][16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tmem_ld16_nowait(tb + lane_base + tS0 + 16 * q, r[q]);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float x = __uint_as_float(r[q][i]) + bias[16 * q + i];
+          x = x > 0.0f ? x : 0.0f;
+          if (x > 0.0f) m1 |= 1ull << (16 * q + i);
+          v[i] = x;
+        }
+        store_chunk(smem + kH1, smem + kH1 + loH, t, 2 * q, HC, v);
+        store_chunk(smem + kH1, smem + kH1 + loH, t, 2 * q + 1, HC, v + 8);
+      }
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+
+    // ---- layer 2: S1 = H1 * W1^T
+    if (t == 0) {
+      tc_fence_after();
+      gemm_split(tb + tS1, make_idesc_bf16(128, HID, false, false), HID / 16, false, precise,
+                 [&](bool lo, int ks) { return desc16_k_major(sH1 + (lo ? loH : 0), HC, ks); },
+                 [&](bool lo, int ks) { return desc16_k_major(sW1 + (lo ? loW1 : 0), HID, ks); });
+      tc_commit(&bar);
+    }
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    {
+      uint32_t r[4][16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tmem_ld16_nowait(tb + lane_base + tS1 + 16 * q, r[q]);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float x = __uint_as_float(r[q][i]) + bias[HID + 16 * q + i];
+          x = x > 0.0f ? x : 0.0f;
+          if (x > 0.0f) m2 |= 1ull << (16 * q + i);
+          v[i] = x;
+        }
+        store_chunk(smem + kH2, smem + kH2 + loH, t, 2 * q, HC, v);
+        store_chunk(smem + kH2, smem + kH2 + loH, t, 2 * q + 1, HC, v + 8);
+      }
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+
+    // ---- output layer: S2[:, 0:16] = H2 * W2p^T
+    if (t == 0) {
+      tc_fence_after();
+      gemm_split(tb + tS2, make_idesc_bf16(128, OUTP, false, false), HID / 16, false, precise,
+                 [&](bool lo, int ks) { return desc16_k_major(sH2 + (lo ? loH : 0), HC, ks); },
+                 [&](bool lo, int ks) { return desc16_k_major(sW2 + (lo ? loW2 : 0), HID, ks); });
+      tc_commit(&bar);
+    }
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    {
+      uint32_t r[16];
+      tmem_ld16_nowait(tb + lane_base + tS2, r);
+      tmem_ld_wait();
+      float u[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) u[i] = 0.0f;
+      for (int o = 0; o < a.out_w; ++o) {
+        const float p = __uint_as_float(r[o]) + bias[2 * HID + o];
+        if (valid && a.pred) a.pred[smp * a.out_w + o] = p;
+        if constexpr (TRAIN) {
+          if (valid) {
+            // src/trainer.cpp:38-44: e = pred - target, loss += e*e, upstream = 2e/(B*out_w), all in double
+            const double tg = a.target_f32 ? static_cast<double>(static_cast<const float*>(a.targets)[smp * a.out_w + o])
+                                           : static_cast<const double*>(a.targets)[smp * a.out_w + o];
+            const double e = static_cast<double>(p) - tg;
+            loss_acc += e * e;
+            const double up = a.upstream_scale * e;
+            u[o] = static_cast<float>(up);
+            if (o < 3) db2_acc[o] += up;
+          }
+        }
+      }
+      if constexpr (TRAIN) {
+        store_chunk(smem + kDY, smem + kDY + loDY, t, 0, OUTP, u);
+        store_chunk(smem + kDY, smem + kDY + loDY, t, 1, OUTP, u + 8);
+      }
+    }
+    if constexpr (!TRAIN) {
+      tc_fence_before();
+      __syncthreads();  // S2 / tiles are reused by the next tile
+      continue;
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+
+    // ---- backward of the output layer: S0 = dY * W2p (input gradient of layer 3),  G2 += H2^T * dY (dW2^T)
+    if (t == 0) {
+      tc_fence_after();
+      gemm_split(tb + tS0, make_idesc_bf16(128, HID, false, true), OUTP / 16, false, precise,
+                 [&](bool lo, int ks) { return desc16_k_major(sDY + (lo ? loDY : 0), OUTP, ks); },
+                 [&](bool lo, int ks) { return desc16_mn_major(sW2 + (lo ? loW2 : 0), HID, ks); });
+      gemm_split(tb + tG2, make_idesc_bf16(64, OUTP, true, true), kTile / 16, g_started, precise,
+                 [&](bool lo, int ks) { return desc16_mn_major(sH2 + (lo ? loH : 0), HC, ks); },
+                 [&](bool lo, int ks) { return desc16_mn_major(sDY + (lo ? loDY : 0), OUTP, ks); });
+      tc_commit(&bar);
+    }
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    {
+      uint32_t r[4][16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tmem_ld16_nowait(tb + lane_base + tS0 + 16 * q, r[q]);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)  // src/mlp.cpp:197: a clamped unit passes no gradient
+          v[i] = ((m2 >> (16 * q + i)) & 1ull) ? __uint_as_float(r[q][i]) : 0.0f;
+        store_chunk(smem + kDH2, smem + kDH2 + loDH, t, 2 * q, HID, v);
+        store_chunk(smem + kDH2, smem + kDH2 + loDH, t, 2 * q + 1, HID, v + 8);
+      }
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+
+    // ---- backward of layer 2: S1 = dH2 * W1,  G1 += dH2^T * [H1 | 1]
+    if (t == 0) {
+      tc_fence_after();
+      gemm_split(tb + tS1, make_idesc_bf16(128, HID, false, true), HID / 16, false, precise,
+                 [&](bool lo, int ks) { return desc16_k_major(sDH2 + (lo ? loDH : 0), HID, ks); },
+                 [&](bool lo, int ks) { return desc16_mn_major(sW1 + (lo ? loW1 : 0), HID, ks); });
+      gemm_split(tb + tG1, make_idesc_bf16(64, HC, true, true), kTile / 16, g_started, precise,
+                 [&](bool lo, int ks) { return desc16_mn_major(sDH2 + (lo ? loDH : 0), HID, ks); },
+                 [&](bool lo, int ks) { return desc16_mn_major(sH1 + (lo ? loH : 0), HC, ks); });
+      tc_commit(&bar);
+    }
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    {
+      uint32_t r[4][16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tmem_ld16_nowait(tb + lane_base + tS1 + 16 * q, r[q]);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = ((m1 >> (16 * q + i)) & 1ull) ? __uint_as_float(r[q][i]) : 0.0f;
+        store_chunk(smem + kDH1, smem + kDH1 + loDH, t, 2 * q, HID, v);
+        store_chunk(smem + kDH1, smem + kDH1 + loDH, t, 2 * q + 1, HID, v + 8);
+      }
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+
+    // ---- backward of layer 1: S2 = dH1 * W0 (d loss / d encoding),  G0 += dH1^T * [X0 | 1]
+    if (t == 0) {
+      tc_fence_after();
+      gemm_split(tb + tS2, make_idesc_bf16(128, IN, false, true), HID / 16, false, precise,
+                 [&](bool lo, int ks) { return desc16_k_major(sDH1 + (lo ? loDH : 0), HID, ks); },
+                 [&](bool lo, int ks) { return desc16_mn_major(sW0 + (lo ? loW0 : 0), IN, ks); });
+      gemm_split(tb + tG0, make_idesc_bf16(64, X0C, true, true), kTile / 16, g_started, precise,
+                 [&](bool lo, int ks) { return desc16_mn_major(sDH1 + (lo ? loDH : 0), HID, ks); },
+                 [&](bool lo, int ks) { return desc16_mn_major(sX0 + (lo ? loX0 : 0), X0C, ks); });
+      tc_commit(&bar);
+    }
+    g_started = true;
+    mbar_wait(&bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    {
+      uint32_t r[2][16];
+      tmem_ld16_nowait(tb + lane_base + tS2, r[0]);
+      tmem_ld16_nowait(tb + lane_base + tS2 + 16, r[1]);
+      tmem_ld_wait();
+      if (valid) {
+        float4* dst = reinterpret_cast<float4*>(a.input_grad + smp * IN);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          __stcs(dst + q, make_float4(__uint_as_float(r[q / 4][4 * (q % 4)]), __uint_as_float(r[q / 4][4 * (q % 4) + 1]),
+                                      __uint_as_float(r[q / 4][4 * (q % 4) + 2]), __uint_as_float(r[q / 4][4 * (q % 4) + 3])));
+      }
+    }
+    tc_fence_before();
+    __syncthreads();  // X0 / S2 are rewritten by the next tile
+  }
+
+  if constexpr (TRAIN) {
+    // ---- weight gradients out of TMEM.  An M = 64 accumulator keeps row i in lane (i/16)*32 + i%16 (tools/tc_probe.py),
+    // so lanes 0..15 of each warp hold rows 16*warp .. 16*warp+15.
+    tc_fence_after();
+    const int lane = t & 31;
+    const int row = 16 * warp + lane;  // output unit o (G0, G1) or hidden unit i (G2)
+    double* gW0 = a.mlp_grad;
+    double* gb0 = gW0 + HID * IN;
+    double* gW1 = gb0 + HID;
+    double* gb1 = gW1 + HID * HID;
+    double* gW2 = gb1 + HID;
+    double* gb2 = gW2 + a.out_w * HID;
+    if (g_started) {
+      for (int c0 = 0; c0 < X0C; c0 += 8) {  // G0: 40 columns = dW0[row][0..31], db0[row] at column 32
+        uint32_t r[16];
+        tmem_ld16_nowait(tb + lane_base + tG0 + (c0 < 32 ? c0 : 24), r);  // last read re-covers cols 24..39
+        tmem_ld_wait();
+        if (lane < 16) {
+          if (c0 < 32) {
+            for (int i = 0; i < 8; ++i) atomicAdd(gW0 + row * IN + c0 + i, static_cast<double>(__uint_as_float(r[i])));
+          } else {
+            atomicAdd(gb0 + row, static_cast<double>(__uint_as_float(r[8])));
+          }
+        }
+      }
+      for (int c0 = 0; c0 < HC; c0 += 8) {  // G1: 72 columns = dW1[row][0..63], db1[row] at column 64
+        uint32_t r[16];
+        tmem_ld16_nowait(tb + lane_base + tG1 + (c0 < 64 ? c0 : 56), r);
+        tmem_ld_wait();
+        if (lane < 16) {
+          if (c0 < 64) {
+            for (int i = 0; i < 8; ++i) atomicAdd(gW1 + row * HID + c0 + i, static_cast<double>(__uint_as_float(r[i])));
+          } else {
+            atomicAdd(gb1 + row, static_cast<double>(__uint_as_float(r[8])));
+          }
+        }
+      }
+      {  // G2: dW2^T[i = row][o]
+        uint32_t r[16];
+        tmem_ld16_nowait(tb + lane_base + tG2, r);
+        tmem_ld_wait();
+        if (lane < 16)
+          for (int o = 0; o < a.out_w; ++o) atomicAdd(gW2 + o * HID + row, static_cast<double>(__uint_as_float(r[o])));
+      }
+    }
+    // loss and output-bias gradient: per-thread fp64 partials -> warp shuffle -> one atomic per CTA
+    double part[4] = {loss_acc, db2_acc[0], db2_acc[1], db2_acc[2]};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      for (int o = 16; o > 0; o >>= 1) part[k] += __shfl_down_sync(0xffffffffu, part[k], o);
+    if (lane == 0)
+      for (int k = 0; k < 4; ++k) red_buf[warp][k] = part[k];
+    __syncthreads();
+    if (t == 0) {
+      double tot[4] = {0, 0, 0, 0};
+      for (int w = 0; w < 4; ++w)
+        for (int k = 0; k < 4; ++k) tot[k] += red_buf[w][k];
+      atomicAdd(a.loss_sum, tot[0]);
+      for (int o = 0; o < a.out_w && o < 3; ++o) atomicAdd(gb2 + o, tot[1 + o]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tb, kTmemCols);
+}
+
+}  // namespace
+
+// Internal entry points used by sxen_mlp.cu / sxen_trainer.cu (declared there).
+bool sxen_mlp_tc_supported(const sxen_mlp_config& c) {
+  return c.input_width == IN && c.hidden_width == HID && c.hidden_layers == 2 && c.output_width >= 1 && c.output_width <= 3;
+}
+
+sxen_status sxen_mlp_tc_run(bool train, const float* params, const float* features, const void* targets, int target_f32,
+                            float* pred, float* input_grad, double* mlp_grad, double* loss_sum, size_t n, int out_w,
+                            size_t global_batch, int precise, cudaStream_t stream) {
+  if (n == 0) return SXEN_OK;
+  TcArgs a{};
+  a.params = params;
+  a.features = features;
+  a.targets = targets;
+  a.pred = pred;
+  a.input_grad = input_grad;
+  a.mlp_grad = mlp_grad;
+  a.loss_sum = loss_sum;
+  a.n = n;
+  a.out_w = out_w;
+  a.target_f32 = target_f32;
+  a.precise = precise;
+  a.upstream_scale = 2.0 / static_cast<double>(global_batch * static_cast<size_t>(out_w));  // src/trainer.cpp:26-27
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned long long tiles = (n + kTile - 1) / kTile;
+  const unsigned grid = static_cast<unsigned>(std::min<unsigned long long>(tiles, static_cast<unsigned long long>(sms)));
+  if (train) {
+    SXEN_CUDA(cudaFuncSetAttribute(mlp_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)));
+    mlp_tc_kernel<true><<<grid, kTile, kSmemBytes, stream>>>(a);
+  } else {
+    SXEN_CUDA(cudaFuncSetAttribute(mlp_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)));
+    mlp_tc_kernel<false><<<grid, kTile, kSmemBytes, stream>>>(a);
+  }
+  SXEN_CUDA(cudaGetLastError());
+  count_launch();
+  return SXEN_OK;
+}

@@ -30,8 +30,6 @@ struct sxen_trainer {
 
 namespace {
 
-__global__ void add_scalar_kernel(double* __restrict__ acc, const double* __restrict__ v) { *acc += *v; }
-
 sxen_status ensure_workspace(sxen_trainer* t, size_t n) {
   if (n <= t->capacity) return SXEN_OK;
   cudaFree(t->features);
@@ -123,24 +121,13 @@ sxen_status sxen_trainer_accumulate(sxen_trainer* t, const void* coords_dev, sxe
   if (n_samples == 0) return SXEN_OK;
   DeviceGuard guard(t->device);
   if (sxen_status st = ensure_workspace(t, n_samples)) return st;
-  cudaStream_t s = as_stream(stream);
   // encoder.encode (src/trainer.cpp:31)
   if (sxen_status st = sxen_encoder_encode(t->enc, coords_dev, coord_type, n_samples, t->features, stream)) return st;
-  // mlp.forward (:36)
-  if (sxen_status st = sxen_mlp_forward(t->mlp, t->features, n_samples, nullptr, stream)) return st;
-  float* acts = nullptr;
-  size_t act_w = 0, out_off = 0;
-  if (sxen_status st = sxen_mlp_activations_dev(t->mlp, &acts, &act_w, &out_off)) return st;
-  // loss and upstream (:37-45)
-  double* batch_sum = t->sample_loss + n_samples;
-  if (sxen_status st = sxen_mse_loss(acts + out_off, act_w, targets_dev, target_type, t->out_w, n_samples, global_batch,
-                                     t->upstream, t->sample_loss, batch_sum, stream))
+  // mlp.forward, loss + upstream, mlp.backward (:36-46): one fused call (tensor-core kernel or the exact chain)
+  if (sxen_status st = sxen_mlp_forward_backward(t->mlp, t->features, targets_dev, target_type, n_samples, global_batch,
+                                                 nullptr, t->input_grad, t->loss_sum, stream))
     return st;
-  add_scalar_kernel<<<1, 1, 0, s>>>(t->loss_sum, batch_sum);
-  SXEN_CUDA(cudaGetLastError());
-  count_launch();
-  // mlp.backward (:46) and encoder.encode_backward on d(loss)/d(encoding) (:47)
-  if (sxen_status st = sxen_mlp_backward(t->mlp, t->upstream, n_samples, t->input_grad, nullptr, stream)) return st;
+  // encoder.encode_backward on d(loss)/d(encoding) (:47)
   return sxen_encoder_encode_backward(t->enc, coords_dev, coord_type, t->input_grad, n_samples, t->grad, stream);
 }
 

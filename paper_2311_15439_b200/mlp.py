@@ -124,6 +124,33 @@ class Mlp:
         raise_for(self._lib, self._lib.sxen_mlp_grads_dev(self._h, C.byref(p)))
         return _wrap_device(p.value, self.parameter_count(), torch.float64, self)
 
+    def set_precision(self, mode: int) -> None:
+        """0 = exact fp64-accumulate (default), 1 = tcgen05 split-bf16 (~1e-5), 2 = tcgen05 single bf16 (~4e-3)."""
+        raise_for(self._lib, self._lib.sxen_mlp_set_precision(self._h, int(mode)))
+
+    def precision(self) -> int:
+        out = C.c_int32()
+        raise_for(self._lib, self._lib.sxen_mlp_get_precision(self._h, C.byref(out)))
+        return out.value
+
+    def forward_backward(self, inputs, targets, global_batch=None, want_pred=False, stream=None):
+        """Fused forward + MSE + backward of one batch (run_chunk per sample, src/trainer.cpp:36-46).
+        Returns (input_grad [N, in] float32, loss_sum 1-element float64 tensor, pred or None)."""
+        import torch
+        from .encoding import _stream_ptr
+        x = inputs.to(torch.float32).contiguous()
+        tg = targets.contiguous()
+        n = x.shape[0]
+        typ = {torch.float64: _abi.COORD_F64, torch.float32: _abi.COORD_F32}[tg.dtype]
+        ig = torch.empty((n, self._cfg.input_width), dtype=torch.float32, device=x.device)
+        loss = torch.zeros(1, dtype=torch.float64, device=x.device)
+        pred = torch.empty((n, self._cfg.output_width), dtype=torch.float32, device=x.device) if want_pred else None
+        raise_for(self._lib, self._lib.sxen_mlp_forward_backward(
+            self._h, C.c_void_p(x.data_ptr()), C.c_void_p(tg.data_ptr()), typ, n, global_batch or n,
+            C.c_void_p(pred.data_ptr()) if want_pred else None, C.c_void_p(ig.data_ptr()), C.c_void_p(loss.data_ptr()),
+            _stream_ptr(stream)))
+        return ig, loss, pred
+
     def forward(self, inputs, stream=None):
         """Batched Mlp::forward.  inputs: CUDA float32 [N, input_width]; returns CUDA float32 [N, output_width]."""
         import torch

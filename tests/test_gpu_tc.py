@@ -1,0 +1,161 @@
+"""GPU (-m gpu): the tcgen05 tensor-core MLP head.
+
+1. Hardware conventions the kernel relies on, pinned with sxen_debug_tc_probe*: bf16 operands in the self-dual CM16 tile
+   work K-major and MN-major, M=64 accumulators keep row i in TMEM lane (i/16)*32 + i%16, and kind::tf32 accepts K-major
+   operands only (MN-major silently yields zeros -- why the head runs on split bf16).
+2. Parity of the fused kernel against the oracle's fp64 MLP: split-bf16 (bf16x3) within TC3_RTOL of the largest magnitude
+   in the compared array, single bf16 within TC1_RTOL."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TC3_RTOL = 3e-5   # ~2^-16 per operand, three layers deep
+TC1_RTOL = 3e-2   # bf16: 2^-8 per operand
+
+
+@pytest.fixture(scope="module")
+def sx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2311_15439_b200 as pkg
+    return pkg
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a), device="cuda:0")
+
+
+def probe(sx, name, M, N, K, a_mn, b_mn, extra=()):
+    fn = getattr(sx.lib, name)
+    fn.restype = C.c_int
+    rng = np.random.default_rng(M * 1000 + N * 10 + K + a_mn * 2 + b_mn)
+    A = rng.integers(-3, 4, size=(M, K)).astype(np.float32)
+    B = rng.integers(-3, 4, size=(N, K)).astype(np.float32)
+    a, b = dev(A), dev(B)
+    raw = torch.zeros((128, N), dtype=torch.float32, device="cuda:0")
+    args = [C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()), C.c_int32(M), C.c_int32(N), C.c_int32(K), C.c_int32(a_mn),
+            C.c_int32(b_mn)] + [C.c_int32(e) for e in extra] + [C.c_void_p(raw.data_ptr())]
+    assert fn(*args) == 0, sx.lib.sxen_last_error()
+    R = raw.cpu().numpy()
+    lanes = list(range(128)) if M == 128 else [(i // 16) * 32 + i % 16 for i in range(64)]
+    return R[lanes], A @ B.T
+
+
+def test_tcgen05_conventions(sx):
+    for M, N, K, a_mn, b_mn in [(128, 64, 32, 0, 0), (128, 16, 64, 0, 0), (128, 64, 16, 0, 1), (128, 32, 64, 0, 1),
+                                (64, 16, 128, 1, 1), (64, 72, 128, 1, 1), (64, 40, 128, 1, 1)]:
+        got, want = probe(sx, "sxen_debug_tc_probe_bf16", M, N, K, a_mn, b_mn)
+        assert np.array_equal(got, want), (M, N, K, a_mn, b_mn)
+    got, want = probe(sx, "sxen_debug_tc_probe", 128, 64, 32, 0, 0, extra=(0,))
+    assert np.array_equal(got, want)  # tf32, K-major: fine
+    got, want = probe(sx, "sxen_debug_tc_probe", 128, 64, 16, 0, 1, extra=(0,))
+    assert not got.any() and want.any()  # tf32, MN-major B: the tensor core returns zeros
+
+
+def make_case(oracle_lib, n, out_w, seed):
+    mc = oracle.MlpConfig(32, 64, 2, out_w)
+    rng = np.random.default_rng(seed)
+    p = oracle_lib.mlp_init(mc, seed)
+    p[-out_w:] = rng.standard_normal(out_w).astype(np.float32) * 0.1
+    p[32 * 64:32 * 64 + 64] = rng.standard_normal(64).astype(np.float32) * 0.05  # b0
+    inp = (rng.standard_normal((n, 32)) * 1e-1).astype(np.float32)
+    tgt = rng.random((n, out_w))
+    return mc, p, inp, tgt
+
+
+@pytest.mark.parametrize("mode,rtol", [(1, TC3_RTOL), (2, TC1_RTOL)])
+@pytest.mark.parametrize("n,out_w", [(128 * 150 + 37, 3), (500, 1)])
+def test_tensor_core_mlp_matches_oracle(sx, oracle_lib, mode, rtol, n, out_w):
+    mc, p, inp, tgt = make_case(oracle_lib, n, out_w, 7 + out_w)
+    want, acts = oracle_lib.mlp_forward(mc, p, inp)
+    scale = 2.0 / (n * out_w)
+    up = scale * (want.astype(np.float64) - tgt)
+    wg, wig = oracle_lib.mlp_backward(mc, p, acts, up)
+    wloss = ((want.astype(np.float64) - tgt) ** 2).sum()
+
+    mlp = sx.Mlp(sx.MlpConfig(32, 64, 2, out_w))
+    mlp.set_parameters(p)
+    mlp.set_precision(mode)
+    assert mlp.precision() == mode
+    out = mlp.forward(dev(inp)).cpu().numpy()
+    assert np.abs(out - want).max() <= rtol * np.abs(want).max()
+    with pytest.raises(RuntimeError, match="before forward"):
+        mlp.backward(dev(up))  # the tensor-core forward keeps no workspace
+    ig, loss, pred = mlp.forward_backward(dev(inp), dev(tgt), want_pred=True)
+    assert np.abs(pred.cpu().numpy() - want).max() <= rtol * np.abs(want).max()
+    assert abs(loss.item() - wloss) <= 10 * rtol * wloss
+    ig = ig.cpu().numpy()
+    # a hidden unit whose pre-activation sits within the arithmetic error of zero may land on the other side of the
+    # ReLU than in fp64 (src/mlp.cpp:197 masks on the stored activation); that changes the sample's input gradient by a
+    # whole weight column.  Such samples are rare: bound their share, and hold every other sample to the tolerance.
+    bad = (np.abs(ig - wig) > 4 * rtol * np.abs(wig).max()).any(axis=1)
+    assert bad.mean() <= (2e-3 if mode == 1 else 0.25), bad.mean()
+    g = mlp.gradient()
+    # Parameter gradients: sums over the batch.  Besides the per-product rounding (rtol * sum |term|) a ReLU flip (see
+    # above) moves one sample's whole contribution, so entries are held to the rounding bound plus a three-flip
+    # allowance, and each layer as a whole to a relative Frobenius error.
+    W1 = p[32 * 64 + 64:32 * 64 + 64 + 64 * 64].reshape(64, 64).astype(np.float64)
+    W2 = p[32 * 64 + 64 + 64 * 64 + 64:32 * 64 + 64 + 64 * 64 + 64 + 64 * out_w].reshape(out_w, 64).astype(np.float64)
+    x0, h1, h2 = acts[:, :32].astype(np.float64), acts[:, 32:96].astype(np.float64), acts[:, 96:160].astype(np.float64)
+    d2 = (up @ W2) * (h2 > 0)
+    d1 = (d2 @ W1) * (h1 > 0)
+    off = 0
+    for l, (delta, src) in enumerate([(d1, x0), (d2, h1), (up, h2)]):
+        o_w, i_w = delta.shape[1], src.shape[1]
+        wscale = np.abs(delta).T @ np.abs(src)
+        flip = 3 * np.abs(up).max() * np.abs(W2).max() * 64 * np.abs(W1).max() * np.abs(src).max() if mode == 1 else np.inf
+        blk, ref = g[off:off + o_w * i_w].reshape(o_w, i_w), wg[off:off + o_w * i_w].reshape(o_w, i_w)
+        assert (np.abs(blk - ref) <= 2 * rtol * wscale + flip).all(), (l, "weights", np.abs(blk - ref).max())
+        assert np.linalg.norm(blk - ref) <= 10 * rtol * np.linalg.norm(ref), (l, np.linalg.norm(blk - ref) / np.linalg.norm(ref))
+        off += o_w * i_w
+        bref = wg[off:off + o_w]
+        assert np.linalg.norm(g[off:off + o_w] - bref) <= 10 * rtol * np.linalg.norm(bref) + 1e-12, (l, "biases")
+        off += o_w
+    # f32 targets take the same path
+    mlp.clear_gradient()
+    ig2, loss2, _ = mlp.forward_backward(dev(inp), dev(tgt.astype(np.float32)))
+    assert abs(loss2.item() - wloss) <= 10 * rtol * wloss + 1e-6 * wloss
+
+
+def test_tensor_core_path_rejects_other_shapes(sx):
+    mlp = sx.Mlp(sx.MlpConfig(32, 64, 1, 3))
+    with pytest.raises(ValueError, match="tensor-core path"):
+        mlp.set_precision(1)
+    mlp = sx.Mlp(sx.MlpConfig(16, 64, 2, 3))
+    with pytest.raises(ValueError):
+        mlp.set_precision(2)
+    with pytest.raises(ValueError):
+        sx.Mlp(sx.MlpConfig(32, 64, 2, 3)).set_precision(7)
+
+
+def test_training_with_tensor_core_head_tracks_the_exact_head(sx):
+    """Same seeds, same batches: loss curves of the bf16x3 head and of the exact head agree to 5e-3 over 40 steps
+    (1e-9 on the first step; Adam amplifies the 1e-5 arithmetic difference as training proceeds)."""
+    cfg = sx.EncoderConfig(dim=2, levels=16, table_size=1 << 14, features=2, base_resolution=16, growth=1.3)
+    curves = []
+    for mode in (0, 1):
+        enc = sx.HashEncoder(cfg)
+        enc.init_tables(42)
+        mlp = sx.Mlp(sx.MlpConfig(32, 64, 2, 3))
+        mlp.init_params(sx.hash_combine(42, 1))
+        mlp.set_precision(mode)
+
+        def sampler(step, b):
+            x = torch.empty((b, 2), dtype=torch.float64, device="cuda:0")
+            sx.CounterRng(1234, step).fill_device(x)
+            tgt = torch.stack([0.5 + 0.5 * torch.sin(9 * x[:, 0]), 0.5 + 0.5 * torch.cos(7 * x[:, 1]),
+                               x[:, 0] * x[:, 1]], dim=1)
+            return x, tgt
+
+        res = sx.train_field(enc, mlp, sampler, sx.TrainConfig(batch_size=4096, steps=40, record_every=1))
+        curves.append(np.array([v for _, v in res.loss_curve]))
+    exact, tc = curves
+    assert exact[-1] < 0.5 * exact[0]
+    assert abs(tc[0] - exact[0]) <= 1e-7 * exact[0]
+    assert np.all(np.abs(tc - exact) <= 5e-3 * exact), (tc, exact)

@@ -303,6 +303,21 @@ SXEN_API sxen_status sxen_trainer_step(sxen_trainer* trainer, const void* coords
                                        const sxen_adam_config* table_adam, const sxen_adam_config* mlp_adam,
                                        double* loss_out, void* stream);
 
+/* ------------------------------------------------------------------ image-fitting task around the path (src/tasks.cpp) */
+/* fit_image's sampler (src/tasks.cpp:112-126): sample s of step k draws idx = CounterRng(seed, k).next_below(w*h);
+ * coords = pixel centre ((idx%w)+0.5)/w, ((idx/w)+0.5)/h; targets = that pixel's RGB.  image_dev: h x w x 3 doubles in
+ * [0,1] (ImageDataset::pixels, include/sxen/image.hpp).  coords_dev N x 2 f64, targets_dev N x 3 f64.  Bit-identical. */
+SXEN_API sxen_status sxen_sample_image_batch(uint64_t seed, uint64_t step, const double* image_dev, int32_t width,
+                                             int32_t height, size_t n_samples, double* coords_dev, double* targets_dev,
+                                             void* stream);
+/* render_image's coordinates (src/tasks.cpp:69-71) for pixels [first_pixel, first_pixel + count), row-major. */
+SXEN_API sxen_status sxen_pixel_centers(int32_t width, int32_t height, size_t first_pixel, size_t count, double* coords_dev,
+                                        void* stream);
+/* Adds sum over the pixel range and 3 channels of (clamp(pred, 0, 1) - pixel)^2 to *sum_dev (src/tasks.cpp:76-78, 35-46).
+ * pred_dev: count x 3 f32. */
+SXEN_API sxen_status sxen_render_sq_error(const float* pred_dev, const double* image_dev, size_t first_pixel, size_t count,
+                                          double* sum_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

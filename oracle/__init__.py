@@ -428,6 +428,11 @@ class Ref:
         L.sxr_bench_fwd_bwd.restype = dbl
         L.sxr_bench_fwd_bwd.argtypes = [vp, P(dbl), P(dbl), C.c_size_t, C.c_int]
         L.sxr_hardware_concurrency.restype = C.c_int
+        L.sxr_make_test_image.argtypes = [C.c_int, C.c_int, u64, P(dbl)]
+        L.sxr_fit_image.argtypes = [P(dbl), C.c_int, C.c_int, P(CConfig), C.c_int, C.c_int, u64, C.c_int, u64, C.c_int,
+                                    C.c_int, P(CAdamConfig), P(CAdamConfig), P(dbl), P(dbl), P(C.c_float), P(C.c_float)]
+        L.sxr_psnr_from_mse.restype = dbl
+        L.sxr_psnr_from_mse.argtypes = [dbl]
 
     def _check(self, st):
         if st != 0:
@@ -492,6 +497,33 @@ class Ref:
 
     def hardware_concurrency(self) -> int:
         return self.lib.sxr_hardware_concurrency()
+
+    def make_test_image(self, width: int, height: int, seed: int):
+        """sxen::make_test_image (src/image.cpp:68-96): [h, w, 3] doubles in [0, 1]."""
+        out = np.empty((height, width, 3), dtype=np.float64)
+        self._check(self.lib.sxr_make_test_image(width, height, seed, _ptr(out, C.c_double)))
+        return out
+
+    def fit_image(self, pixels, cfg: Config, batch: int, steps: int, train_seed: int = 1234, threads: int = 1,
+                  init_seed: int = 42, hidden_width: int = 64, hidden_layers: int = 2, table_adam: AdamConfig = None,
+                  mlp_adam: AdamConfig = None):
+        """sxen::fit_image (src/tasks.cpp:98-137). Returns (final_psnr, loss[steps], tables[L, T*F], mlp_params)."""
+        px = _f64(pixels)
+        h, w = px.shape[0], px.shape[1]
+        ta = (table_adam or AdamConfig(lr=1e-2)).c()
+        ma = (mlp_adam or AdamConfig(lr=1e-3)).c()
+        mc = MlpConfig(cfg.encoded_width, hidden_width, hidden_layers, 3)
+        psnr = C.c_double()
+        loss = np.zeros(steps, dtype=np.float64)
+        tables = np.zeros((cfg.levels, cfg.table_size * cfg.features), dtype=np.float32)
+        params = np.zeros(mc.param_count, dtype=np.float32)
+        self._check(self.lib.sxr_fit_image(_ptr(px, C.c_double), w, h, C.byref(cfg.c()), batch, steps, train_seed, threads,
+                                           init_seed, hidden_width, hidden_layers, C.byref(ta), C.byref(ma), C.byref(psnr),
+                                           _ptr(loss, C.c_double), _ptr(tables, C.c_float), _ptr(params, C.c_float)))
+        return psnr.value, loss, tables, params
+
+    def psnr_from_mse(self, mse: float) -> float:
+        return self.lib.sxr_psnr_from_mse(mse)
 
 
 class RefEncoder:

@@ -20,8 +20,12 @@
 #include "sxen/lattice.hpp"
 #include "sxen/mlp.hpp"
 #include "sxen/optimizer.hpp"
+#include "sxen/image.hpp"
 #include "sxen/rng.hpp"
+#include "sxen/tasks.hpp"
 #include "sxen/trainer.hpp"
+
+#include <png.h>
 
 namespace {
 
@@ -336,5 +340,59 @@ double sxr_bench_fwd_bwd(void* h, const double* x, const double* upstream, std::
 }
 
 int sxr_hardware_concurrency() { return static_cast<int>(std::thread::hardware_concurrency()); }
+
+// ---- libpng stand-ins (see oracle/png_stub/png.h): always fail, the reference raises IoError
+int png_image_begin_read_from_file(png_image* image, const char*) {
+  std::strncpy(image->message, "libpng is not available in the oracle build", sizeof(image->message) - 1);
+  return 0;
+}
+int png_image_finish_read(png_image*, const void*, void*, int, void*) { return 0; }
+void png_image_free(png_image*) {}
+int png_image_write_to_file(png_image* image, const char*, int, const void*, int, const void*) {
+  std::strncpy(image->message, "libpng is not available in the oracle build", sizeof(image->message) - 1);
+  return 0;
+}
+
+// ---- tasks: make_test_image (src/image.cpp:68-96), fit_image (src/tasks.cpp:98-137), render_image + PSNR (:30-96)
+int sxr_make_test_image(int width, int height, std::uint64_t seed, double* pixels_out) {
+  return guarded([&] {
+    const sxen::ImageDataset img = sxen::make_test_image(width, height, seed);
+    std::memcpy(pixels_out, img.pixels.data(), img.pixels.size() * sizeof(double));
+  });
+}
+
+// Runs the reference's fit_image.  Outputs: final PSNR, per-step loss (record_every = 1), trained tables (L x T*F) and
+// MLP parameters.
+int sxr_fit_image(const double* pixels, int width, int height, const Cfg* cfg, int batch, int steps, std::uint64_t train_seed,
+                  int threads, std::uint64_t init_seed, int hidden_width, int hidden_layers, const AdamCfg* table_adam,
+                  const AdamCfg* mlp_adam, double* final_psnr, double* loss_out, float* tables_out, float* mlp_out) {
+  return guarded([&] {
+    sxen::ImageDataset img;
+    img.width = width;
+    img.height = height;
+    img.pixels.assign(pixels, pixels + 3 * static_cast<std::size_t>(width) * static_cast<std::size_t>(height));
+    sxen::TrainConfig tc;
+    tc.batch_size = batch;
+    tc.steps = steps;
+    tc.seed = train_seed;
+    tc.threads = threads;
+    tc.record_every = 1;
+    tc.table_adam = to_ref(*table_adam);
+    tc.mlp_adam = to_ref(*mlp_adam);
+    sxen::FitImageOptions opt;
+    opt.init_seed = init_seed;
+    opt.mlp_hidden_width = hidden_width;
+    opt.mlp_hidden_layers = hidden_layers;
+    const sxen::EncoderConfig ec = to_ref(*cfg);
+    sxen::FitImageResult r = sxen::fit_image(img, ec, tc, opt);
+    *final_psnr = r.final_psnr;
+    for (const auto& [step, loss] : r.train.loss_curve) loss_out[step] = loss;
+    const std::size_t per = static_cast<std::size_t>(ec.table_size) * static_cast<std::size_t>(ec.features);
+    for (int l = 0; l < ec.levels; ++l) std::memcpy(tables_out + static_cast<std::size_t>(l) * per, r.encoder.table(l).data(), per * sizeof(float));
+    std::memcpy(mlp_out, r.mlp.parameters().data(), r.mlp.parameter_count() * sizeof(float));
+  });
+}
+
+double sxr_psnr_from_mse(double mse) { return sxen::psnr_from_mse(mse); }
 
 }  // extern "C"

@@ -123,6 +123,9 @@ SIGNATURES = {
     "sxen_mlp_forward_backward": (C.c_int, [_vp, _vp, _vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _vp]),
     "sxen_mlp_activations_dev": (C.c_int, [_vp, _P(_vp), _P(_sz), _P(_sz)]),
     "sxen_mse_loss": (C.c_int, [_vp, _sz, _vp, C.c_int, _i32, _sz, _sz, _vp, _vp, _vp, _vp]),
+    "sxen_sample_image_batch": (C.c_int, [_u64, _u64, _vp, _i32, _i32, _sz, _vp, _vp, _vp]),
+    "sxen_pixel_centers": (C.c_int, [_i32, _i32, _sz, _sz, _vp, _vp]),
+    "sxen_render_sq_error": (C.c_int, [_vp, _vp, _sz, _sz, _vp, _vp]),
     "sxen_trainer_create": (C.c_int, [_vp, _vp, _P(_vp)]),
     "sxen_trainer_destroy": (C.c_int, [_vp]),
     "sxen_trainer_accumulate": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, _sz, _sz, _vp]),

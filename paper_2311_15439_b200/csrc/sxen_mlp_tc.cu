@@ -12,7 +12,10 @@
 // is the K-major A operand of the next layer, the K-major A operand of the input-gradient GEMM and the MN-major operand of
 // the weight-gradient GEMM.  Each tile carries one extra 8-column block whose first column is 1.0: used as the B operand of
 // a weight-gradient GEMM it makes the bias gradient fall out as column `in` of the same accumulator.
-// One CTA = 128 threads = 128 TMEM lanes = 128 samples; thread t owns sample t of the tile in every epilogue.
+// One CTA = 128 samples = 128 TMEM lanes, 256 threads: threads t and t+128 share sample t of the tile and split every
+// epilogue's columns in halves (warps w and w+4 read the same TMEM lane quadrant).  The weight-gradient MMAs of a phase are
+// queued behind the phase's dependent-chain MMAs and are only waited for when the tiles they read are about to be rewritten,
+// so they run under the following epilogues.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -46,6 +49,7 @@ constexpr uint32_t kSmemBytes = kBias + (HID + HID + OUTP) * 4;
 constexpr uint32_t tS0 = 0;     // [128 x 64] layer-1 pre-activation, later dH2
 constexpr uint32_t tS1 = 64;    // [128 x 64] layer-2 pre-activation, later dH1
 constexpr uint32_t tS2 = 128;   // [128 x 32] output (16 cols), later d(input) (32 cols)
+constexpr int kThreads = 256;
 constexpr uint32_t tG0 = 160;   // [64 x 40]  dW0 | db0
 constexpr uint32_t tG1 = 200;   // [64 x 72]  dW1 | db1
 constexpr uint32_t tG2 = 272;   // [64 x 16]  dW2^T
@@ -66,15 +70,17 @@ struct TcArgs {
   double upstream_scale;    // 2 / (global_batch * out_w)
 };
 
+// x = hi + lo with hi = bf16(x), lo = bf16(x - hi); two values per F2FP pack instruction.
 __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
   uint32_t h[4], l[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const __nv_bfloat16 h0 = __float2bfloat16_rn(v[2 * q]), h1 = __float2bfloat16_rn(v[2 * q + 1]);
-    const __nv_bfloat16 l0 = __float2bfloat16_rn(v[2 * q] - __bfloat162float(h0));
-    const __nv_bfloat16 l1 = __float2bfloat16_rn(v[2 * q + 1] - __bfloat162float(h1));
-    h[q] = static_cast<uint32_t>(__bfloat16_as_ushort(h0)) | (static_cast<uint32_t>(__bfloat16_as_ushort(h1)) << 16);
-    l[q] = static_cast<uint32_t>(__bfloat16_as_ushort(l0)) | (static_cast<uint32_t>(__bfloat16_as_ushort(l1)) << 16);
+    const __nv_bfloat162 hp = __floats2bfloat162_rn(v[2 * q], v[2 * q + 1]);
+    const uint32_t hb = *reinterpret_cast<const uint32_t*>(&hp);  // low half = element 0
+    const float h0 = __uint_as_float(hb << 16), h1 = __uint_as_float(hb & 0xffff0000u);
+    const __nv_bfloat162 lp = __floats2bfloat162_rn(v[2 * q] - h0, v[2 * q + 1] - h1);
+    h[q] = hb;
+    l[q] = *reinterpret_cast<const uint32_t*>(&lp);
   }
   hi = make_uint4(h[0], h[1], h[2], h[3]);
   lo = make_uint4(l[0], l[1], l[2], l[3]);
@@ -113,13 +119,16 @@ __device__ __forceinline__ void gemm_split(uint32_t d, uint32_t idesc, int kstep
 }
 
 template <bool TRAIN>
-__global__ void __launch_bounds__(kTile, 1) mlp_tc_kernel(const __grid_constant__ TcArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) mlp_tc_kernel(const __grid_constant__ TcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar;     // dependent-chain MMAs of the current phase
+  __shared__ uint64_t bar_g;   // every MMA of the tile, weight-gradient ones included
   __shared__ uint32_t tmem_base_slot;
-  __shared__ double red_buf[4][4];
-  const int t = threadIdx.x;
-  const int warp = t >> 5;
+  __shared__ double red_buf[8][4];
+  const int tid = threadIdx.x;
+  const int t = tid & (kTile - 1);   // sample row inside the tile
+  const int half = tid >> 7;         // which half of an epilogue's columns this thread handles
+  const int warp = tid >> 5;
   float* bias = reinterpret_cast<float*>(smem + kBias);
   const float* W0 = a.params;
   const float* b0 = W0 + HID * IN;
@@ -129,47 +138,50 @@ __global__ void __launch_bounds__(kTile, 1) mlp_tc_kernel(const __grid_constant_
   const float* b2 = W2 + a.out_w * HID;
 
   // ---- one-time setup: weights (hi/lo CM16 tiles, rows = output unit, cols = input unit), biases, ones columns
-  for (int e = t; e < HID * IN / 8; e += kTile) {
+  for (int e = tid; e < HID * IN / 8; e += kThreads) {
     const int o = e / (IN / 8), ch = e % (IN / 8);
     float v[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) v[q] = W0[o * IN + ch * 8 + q];
     store_chunk(smem + kW0, smem + kW0 + cm16_bytes(HID, IN), o, ch, IN, v);
   }
-  for (int e = t; e < HID * HID / 8; e += kTile) {
+  for (int e = tid; e < HID * HID / 8; e += kThreads) {
     const int o = e / (HID / 8), ch = e % (HID / 8);
     float v[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) v[q] = W1[o * HID + ch * 8 + q];
     store_chunk(smem + kW1, smem + kW1 + cm16_bytes(HID, HID), o, ch, HID, v);
   }
-  for (int e = t; e < OUTP * HID / 8; e += kTile) {
+  for (int e = tid; e < OUTP * HID / 8; e += kThreads) {
     const int o = e / (HID / 8), ch = e % (HID / 8);
     float v[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) v[q] = o < a.out_w ? W2[o * HID + ch * 8 + q] : 0.0f;
     store_chunk(smem + kW2, smem + kW2 + cm16_bytes(OUTP, HID), o, ch, HID, v);
   }
-  if (t < HID) {
-    bias[t] = b0[t];
-    bias[HID + t] = b1[t];
+  if (tid < HID) {
+    bias[tid] = b0[tid];
+    bias[HID + tid] = b1[tid];
   }
-  if (t < OUTP) bias[2 * HID + t] = t < a.out_w ? b2[t] : 0.0f;
-  {
+  if (tid < OUTP) bias[2 * HID + tid] = tid < a.out_w ? b2[tid] : 0.0f;
+  if (half == 0) {
     float ones[8] = {1.0f, 0, 0, 0, 0, 0, 0, 0};
     store_chunk(smem + kX0, smem + kX0 + cm16_bytes(kTile, X0C), t, IN / 8, X0C, ones);
     store_chunk(smem + kH1, smem + kH1 + cm16_bytes(kTile, HC), t, HID / 8, HC, ones);
     store_chunk(smem + kH2, smem + kH2 + cm16_bytes(kTile, HC), t, HID / 8, HC, ones);
   }
-  if (t == 0) mbar_init(&bar, 1);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    mbar_init(&bar_g, 1);
+  }
   if (warp == 0) tmem_alloc(&tmem_base_slot, kTmemCols);
   fence_proxy_async();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tb = tmem_base_slot;
-  const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
-  uint32_t phase = 0;
+  const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+  uint32_t phase = 0, phase_g = 0;
   const bool precise = a.precise != 0;
 
   const uint32_t sW0 = smem_u32(smem + kW0), sW1 = smem_u32(smem + kW1), sW2 = smem_u32(smem + kW2);
@@ -191,27 +203,38 @@ __global__ void __launch_bounds__(kTile, 1) mlp_tc_kernel(const __grid_constant_
 
     // ---- stage 0: features -> X0 tiles.  Lane mapping: 8 rows x 4 chunks per warp instruction keeps both the global
     // reads (64 contiguous bytes per row) and the shared stores (8 rows = 8 distinct 16-byte bank groups) efficient.
-    for (int it = 0; it < 4; ++it) {
-      const int row = (t & 7) + 8 * ((t >> 5) + 4 * it);    // 0..127
-      const int ch = (t >> 3) & 3;                          // 8-column chunk 0..3
-      float v[8];
-      const unsigned long long gs = s0 + row;
+    // The loads are issued before waiting for the previous tile's weight-gradient MMAs, which still read X0.
+    float xin[2][8];
+    int xrow[2];
+    const int xch = (tid >> 3) & 3;  // 8-column chunk 0..3
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      xrow[it] = (tid & 7) + 8 * ((tid >> 5) + 8 * it);  // 0..127
+      const unsigned long long gs = s0 + xrow[it];
       if (gs < a.n) {
-        const float4* p = reinterpret_cast<const float4*>(a.features + gs * IN + ch * 8);
+        const float4* p = reinterpret_cast<const float4*>(a.features + gs * IN + xch * 8);
         const float4 x0 = __ldg(p), x1 = __ldg(p + 1);
-        v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w; v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+        xin[it][0] = x0.x; xin[it][1] = x0.y; xin[it][2] = x0.z; xin[it][3] = x0.w;
+        xin[it][4] = x1.x; xin[it][5] = x1.y; xin[it][6] = x1.z; xin[it][7] = x1.w;
       } else {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = 0.0f;
+        for (int q = 0; q < 8; ++q) xin[it][q] = 0.0f;
       }
-      store_chunk(smem + kX0, smem + kX0 + loX0, row, ch, X0C, v);
     }
+    if constexpr (TRAIN) {
+      if (g_started) {
+        mbar_wait(&bar_g, phase_g);
+        phase_g ^= 1;
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < 2; ++it) store_chunk(smem + kX0, smem + kX0 + loX0, xrow[it], xch, X0C, xin[it]);
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
 
     // ---- layer 1: S0 = X0 * W0^T
-    if (t == 0) {
+    if (tid == 0) {
       tc_fence_after();
       gemm_split(tb + tS0, make_idesc_bf16(128, HID, false, false), IN / 16, false, precise,
                  [&](bool lo, int ks) { return desc16_k_major(sX0 + (lo ? loX0 : 0), X0C, ks); },
@@ -221,24 +244,24 @@ __global__ void __launch_bounds__(kTile, 1) mlp_tc_kernel(const __grid_constant_
     mbar_wait(&bar, phase);
     phase ^= 1;
     tc_fence_after();
-    unsigned long long m1 = 0, m2 = 0;  // ReLU masks of this thread's sample (bit o = unit o active)
+    uint32_t m1 = 0, m2 = 0;  // ReLU masks of this thread's 32 units (bit i = unit 32*half + i active)
     {
-      uint32_t r[4][16];
+      uint32_t r[2][16];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) tmem_ld16_nowait(tb + lane_base + tS0 + 16 * q, r[q]);
+      for (int q = 0; q < 2; ++q) tmem_ld16_nowait(tb + lane_base + tS0 + 32 * half + 16 * q, r[q]);
       tmem_ld_wait();
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 2; ++q) {
         float v[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          float x = __uint_as_float(r[q][i]) + bias[16 * q + i];
+          float x = __uint_as_float(r[q][i]) + bias[32 * half + 16 * q + i];
           x = x > 0.0f ? x : 0.0f;
-          if (x > 0.0f) m1 |= 1ull << (16 * q + i);
+          if (x > 0.0f) m1 |= 1u << (16 * q + i);
           v[i] = x;
         }
-        store_chunk(smem + kH1, smem + kH1 + loH, t, 2 * q, HC, v);
-        store_chunk(smem + kH1, smem + kH1 + loH, t, 2 * q + 1, HC, v + 8);
+        store_chunk(smem + kH1, smem + kH1 + loH, t, 4 * half + 2 * q, HC, v);
+        store_chunk(smem + kH1, smem + kH1 + loH, t, 4 * half + 2 * q + 1, HC, v + 8);
       }
     }
     fence_proxy_async();
@@ -246,7 +269,7 @@ __global__ void __launch_bounds__(kTile, 1) mlp_tc_kernel(const __grid_constant_
     __syncthreads();
 
     // ---- layer 2: S1 = H1 * W1^T
-    if (t == 0) {
+    if (tid == 0) {
       tc_fence_after();
       gemm_split(tb + tS1, make_idesc_bf16(128, HID, false, false), HID / 16, false, precise,
                  [&](bool lo, int ks) { return desc16_k_major(sH1 + (lo ? loH : 0), HC, ks); },
@@ -257,22 +280,22 @@ __global__ void __launch_bounds__(kTile, 1) mlp_tc_kernel(const __grid_constant_
     phase ^= 1;
     tc_fence_after();
     {
-      uint32_t r[4][16];
+      uint32_t r[2][16];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) tmem_ld16_nowait(tb + lane_base + tS1 + 16 * q, r[q]);
+      for (int q = 0; q < 2; ++q) tmem_ld16_nowait(tb + lane_base + tS1 + 32 * half + 16 * q, r[q]);
       tmem_ld_wait();
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 2; ++q) {
         float v[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          float x = __uint_as_float(r[q][i]) + bias[HID + 16 * q + i];
+          float x = __uint_as_float(r[q][i]) + bias[HID + 32 * half + 16 * q + i];
           x = x > 0.0f ? x : 0.0f;
-          if (x > 0.0f) m2 |= 1ull << (16 * q + i);
+          if (x > 0.0f) m2 |= 1u << (16 * q + i);
           v[i] = x;
         }
-        store_chunk(smem + kH2, smem + kH2 + loH, t, 2 * q, HC, v);
-        store_chunk(smem + kH2, smem + kH2 + loH, t, 2 * q + 1, HC, v + 8);
+        store_chunk(smem + kH2, smem + kH2 + loH, t, 4 * half + 2 * q, HC, v);
+        store_chunk(smem + kH2, smem + kH2 + loH, t, 4 * half + 2 * q + 1, HC, v + 8);
       }
     }
     fence_proxy_async();
@@ -280,7 +303,7 @@ __global__ void __launch_bounds__(kTile, 1) mlp_tc_kernel(const __grid_constant_
     __syncthreads();
 
     // ---- output layer: S2[:, 0:16] = H2 * W2p^T
-    if (t == 0) {
+    if (tid == 0) {
       tc_fence_after();
       gemm_split(tb + tS2, make_idesc_bf16(128, OUTP, false, false), HID / 16, false, precise,
                  [&](bool lo, int ks) { return desc16_k_major(sH2 + (lo ? loH : 0), HC, ks); },
@@ -290,7 +313,7 @@ __global__ void __launch_bounds__(kTile, 1) mlp_tc_kernel(const __grid_constant_
     mbar_wait(&bar, phase);
     phase ^= 1;
     tc_fence_after();
-    {
+    if (half == 0) {
       uint32_t r[16];
       tmem_ld16_nowait(tb + lane_base + tS2, r);
       tmem_ld_wait();
@@ -328,32 +351,32 @@ __global__ void __launch_bounds__(kTile, 1) mlp_tc_kernel(const __grid_constant_
     __syncthreads();
 
     // ---- backward of the output layer: S0 = dY * W2p (input gradient of layer 3),  G2 += H2^T * dY (dW2^T)
-    if (t == 0) {
+    if (tid == 0) {
       tc_fence_after();
       gemm_split(tb + tS0, make_idesc_bf16(128, HID, false, true), OUTP / 16, false, precise,
                  [&](bool lo, int ks) { return desc16_k_major(sDY + (lo ? loDY : 0), OUTP, ks); },
                  [&](bool lo, int ks) { return desc16_mn_major(sW2 + (lo ? loW2 : 0), HID, ks); });
+      tc_commit(&bar);
       gemm_split(tb + tG2, make_idesc_bf16(64, OUTP, true, true), kTile / 16, g_started, precise,
                  [&](bool lo, int ks) { return desc16_mn_major(sH2 + (lo ? loH : 0), HC, ks); },
                  [&](bool lo, int ks) { return desc16_mn_major(sDY + (lo ? loDY : 0), OUTP, ks); });
-      tc_commit(&bar);
     }
     mbar_wait(&bar, phase);
     phase ^= 1;
     tc_fence_after();
     {
-      uint32_t r[4][16];
+      uint32_t r[2][16];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) tmem_ld16_nowait(tb + lane_base + tS0 + 16 * q, r[q]);
+      for (int q = 0; q < 2; ++q) tmem_ld16_nowait(tb + lane_base + tS0 + 32 * half + 16 * q, r[q]);
       tmem_ld_wait();
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 2; ++q) {
         float v[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i)  // src/mlp.cpp:197: a clamped unit passes no gradient
-          v[i] = ((m2 >> (16 * q + i)) & 1ull) ? __uint_as_float(r[q][i]) : 0.0f;
-        store_chunk(smem + kDH2, smem + kDH2 + loDH, t, 2 * q, HID, v);
-        store_chunk(smem + kDH2, smem + kDH2 + loDH, t, 2 * q + 1, HID, v + 8);
+          v[i] = ((m2 >> (16 * q + i)) & 1u) ? __uint_as_float(r[q][i]) : 0.0f;
+        store_chunk(smem + kDH2, smem + kDH2 + loDH, t, 4 * half + 2 * q, HID, v);
+        store_chunk(smem + kDH2, smem + kDH2 + loDH, t, 4 * half + 2 * q + 1, HID, v + 8);
       }
     }
     fence_proxy_async();
@@ -361,31 +384,31 @@ __global__ void __launch_bounds__(kTile, 1) mlp_tc_kernel(const __grid_constant_
     __syncthreads();
 
     // ---- backward of layer 2: S1 = dH2 * W1,  G1 += dH2^T * [H1 | 1]
-    if (t == 0) {
+    if (tid == 0) {
       tc_fence_after();
       gemm_split(tb + tS1, make_idesc_bf16(128, HID, false, true), HID / 16, false, precise,
                  [&](bool lo, int ks) { return desc16_k_major(sDH2 + (lo ? loDH : 0), HID, ks); },
                  [&](bool lo, int ks) { return desc16_mn_major(sW1 + (lo ? loW1 : 0), HID, ks); });
+      tc_commit(&bar);
       gemm_split(tb + tG1, make_idesc_bf16(64, HC, true, true), kTile / 16, g_started, precise,
                  [&](bool lo, int ks) { return desc16_mn_major(sDH2 + (lo ? loDH : 0), HID, ks); },
                  [&](bool lo, int ks) { return desc16_mn_major(sH1 + (lo ? loH : 0), HC, ks); });
-      tc_commit(&bar);
     }
     mbar_wait(&bar, phase);
     phase ^= 1;
     tc_fence_after();
     {
-      uint32_t r[4][16];
+      uint32_t r[2][16];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) tmem_ld16_nowait(tb + lane_base + tS1 + 16 * q, r[q]);
+      for (int q = 0; q < 2; ++q) tmem_ld16_nowait(tb + lane_base + tS1 + 32 * half + 16 * q, r[q]);
       tmem_ld_wait();
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 2; ++q) {
         float v[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = ((m1 >> (16 * q + i)) & 1ull) ? __uint_as_float(r[q][i]) : 0.0f;
-        store_chunk(smem + kDH1, smem + kDH1 + loDH, t, 2 * q, HID, v);
-        store_chunk(smem + kDH1, smem + kDH1 + loDH, t, 2 * q + 1, HID, v + 8);
+        for (int i = 0; i < 16; ++i) v[i] = ((m1 >> (16 * q + i)) & 1u) ? __uint_as_float(r[q][i]) : 0.0f;
+        store_chunk(smem + kDH1, smem + kDH1 + loDH, t, 4 * half + 2 * q, HID, v);
+        store_chunk(smem + kDH1, smem + kDH1 + loDH, t, 4 * half + 2 * q + 1, HID, v + 8);
       }
     }
     fence_proxy_async();
@@ -393,43 +416,44 @@ __global__ void __launch_bounds__(kTile, 1) mlp_tc_kernel(const __grid_constant_
     __syncthreads();
 
     // ---- backward of layer 1: S2 = dH1 * W0 (d loss / d encoding),  G0 += dH1^T * [X0 | 1]
-    if (t == 0) {
+    if (tid == 0) {
       tc_fence_after();
       gemm_split(tb + tS2, make_idesc_bf16(128, IN, false, true), HID / 16, false, precise,
                  [&](bool lo, int ks) { return desc16_k_major(sDH1 + (lo ? loDH : 0), HID, ks); },
                  [&](bool lo, int ks) { return desc16_mn_major(sW0 + (lo ? loW0 : 0), IN, ks); });
+      tc_commit(&bar);
       gemm_split(tb + tG0, make_idesc_bf16(64, X0C, true, true), kTile / 16, g_started, precise,
                  [&](bool lo, int ks) { return desc16_mn_major(sDH1 + (lo ? loDH : 0), HID, ks); },
                  [&](bool lo, int ks) { return desc16_mn_major(sX0 + (lo ? loX0 : 0), X0C, ks); });
-      tc_commit(&bar);
+      tc_commit(&bar_g);  // covers G2, G1 and G0 of this tile
     }
     g_started = true;
     mbar_wait(&bar, phase);
     phase ^= 1;
     tc_fence_after();
     {
-      uint32_t r[2][16];
-      tmem_ld16_nowait(tb + lane_base + tS2, r[0]);
-      tmem_ld16_nowait(tb + lane_base + tS2 + 16, r[1]);
+      uint32_t r[16];
+      tmem_ld16_nowait(tb + lane_base + tS2 + 16 * half, r);
       tmem_ld_wait();
       if (valid) {
-        float4* dst = reinterpret_cast<float4*>(a.input_grad + smp * IN);
+        float4* dst = reinterpret_cast<float4*>(a.input_grad + smp * IN + 16 * half);
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          __stcs(dst + q, make_float4(__uint_as_float(r[q / 4][4 * (q % 4)]), __uint_as_float(r[q / 4][4 * (q % 4) + 1]),
-                                      __uint_as_float(r[q / 4][4 * (q % 4) + 2]), __uint_as_float(r[q / 4][4 * (q % 4) + 3])));
+        for (int q = 0; q < 4; ++q)
+          __stcs(dst + q, make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
+                                      __uint_as_float(r[4 * q + 3])));
       }
     }
     tc_fence_before();
-    __syncthreads();  // X0 / S2 are rewritten by the next tile
+    __syncthreads();  // S2 is rewritten by the next tile (X0 waits for bar_g in stage 0)
   }
 
   if constexpr (TRAIN) {
     // ---- weight gradients out of TMEM.  An M = 64 accumulator keeps row i in lane (i/16)*32 + i%16 (tools/tc_probe.py),
     // so lanes 0..15 of each warp hold rows 16*warp .. 16*warp+15.
+    if (g_started) mbar_wait(&bar_g, phase_g);
     tc_fence_after();
-    const int lane = t & 31;
-    const int row = 16 * warp + lane;  // output unit o (G0, G1) or hidden unit i (G2)
+    const int lane = tid & 31;
+    const int row = 16 * (warp & 3) + lane;  // output unit o (G0, G1) or hidden unit i (G2)
     double* gW0 = a.mlp_grad;
     double* gb0 = gW0 + HID * IN;
     double* gW1 = gb0 + HID;
@@ -437,7 +461,7 @@ __global__ void __launch_bounds__(kTile, 1) mlp_tc_kernel(const __grid_constant_
     double* gW2 = gb1 + HID;
     double* gb2 = gW2 + a.out_w * HID;
     if (g_started) {
-      for (int c0 = 0; c0 < X0C; c0 += 8) {  // G0: 40 columns = dW0[row][0..31], db0[row] at column 32
+      for (int c0 = 8 * half; c0 < X0C; c0 += 16) {  // G0: 40 columns = dW0[row][0..31], db0[row] at column 32
         uint32_t r[16];
         tmem_ld16_nowait(tb + lane_base + tG0 + (c0 < 32 ? c0 : 24), r);  // last read re-covers cols 24..39
         tmem_ld_wait();
@@ -449,7 +473,7 @@ __global__ void __launch_bounds__(kTile, 1) mlp_tc_kernel(const __grid_constant_
           }
         }
       }
-      for (int c0 = 0; c0 < HC; c0 += 8) {  // G1: 72 columns = dW1[row][0..63], db1[row] at column 64
+      for (int c0 = 8 * half; c0 < HC; c0 += 16) {  // G1: 72 columns = dW1[row][0..63], db1[row] at column 64
         uint32_t r[16];
         tmem_ld16_nowait(tb + lane_base + tG1 + (c0 < 64 ? c0 : 56), r);
         tmem_ld_wait();
@@ -461,7 +485,7 @@ __global__ void __launch_bounds__(kTile, 1) mlp_tc_kernel(const __grid_constant_
           }
         }
       }
-      {  // G2: dW2^T[i = row][o]
+      if (half == 1) {  // G2: dW2^T[i = row][o]
         uint32_t r[16];
         tmem_ld16_nowait(tb + lane_base + tG2, r);
         tmem_ld_wait();
@@ -477,9 +501,9 @@ __global__ void __launch_bounds__(kTile, 1) mlp_tc_kernel(const __grid_constant_
     if (lane == 0)
       for (int k = 0; k < 4; ++k) red_buf[warp][k] = part[k];
     __syncthreads();
-    if (t == 0) {
+    if (tid == 0) {
       double tot[4] = {0, 0, 0, 0};
-      for (int w = 0; w < 4; ++w)
+      for (int w = 0; w < 8; ++w)
         for (int k = 0; k < 4; ++k) tot[k] += red_buf[w][k];
       atomicAdd(a.loss_sum, tot[0]);
       for (int o = 0; o < a.out_w && o < 3; ++o) atomicAdd(gb2 + o, tot[1 + o]);
@@ -521,10 +545,10 @@ sxen_status sxen_mlp_tc_run(bool train, const float* params, const float* featur
   const unsigned grid = static_cast<unsigned>(std::min<unsigned long long>(tiles, static_cast<unsigned long long>(sms)));
   if (train) {
     SXEN_CUDA(cudaFuncSetAttribute(mlp_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)));
-    mlp_tc_kernel<true><<<grid, kTile, kSmemBytes, stream>>>(a);
+    mlp_tc_kernel<true><<<grid, kThreads, kSmemBytes, stream>>>(a);
   } else {
     SXEN_CUDA(cudaFuncSetAttribute(mlp_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)));
-    mlp_tc_kernel<false><<<grid, kTile, kSmemBytes, stream>>>(a);
+    mlp_tc_kernel<false><<<grid, kThreads, kSmemBytes, stream>>>(a);
   }
   SXEN_CUDA(cudaGetLastError());
   count_launch();

@@ -255,12 +255,34 @@ def neural_cases(ref: Ref):
     print("neural_cases written; loss t1:", d["train_loss_t1"][:3], "...", d["train_loss_t1"][-1])
 
 
+def task_cases(ref: Ref):
+    """fit_image on the reference's own procedural test image (src/image.cpp:68-96, src/tasks.cpp:98-137)."""
+    d = {}
+    img = ref.make_test_image(64, 64, 7)
+    cfg = Config(dim=2, levels=16, table_size=1 << 10, features=2, base_resolution=4, growth=1.25)
+    steps, batch = 300, 512
+    psnr, loss, tables, params = ref.fit_image(img, cfg, batch=batch, steps=steps, train_seed=1234, threads=1, init_seed=42)
+    d["image"] = img
+    d["cfg"] = np.array([cfg.dim, cfg.levels, cfg.table_size, cfg.features, cfg.base_resolution], dtype=np.int64)
+    d["growth"] = np.float64(cfg.growth)
+    d["steps"], d["batch"] = np.int64(steps), np.int64(batch)
+    d["final_psnr"], d["loss"], d["tables"], d["mlp_params"] = np.float64(psnr), loss, tables, params
+    d["psnr_examples_in"] = np.array([0.0, -1.0, 1e-12, 1e-4, 0.5, 1.0, 4.0])
+    d["psnr_examples_out"] = np.array([ref.psnr_from_mse(float(v)) for v in d["psnr_examples_in"]])
+    np.savez_compressed(os.path.join(OUT, "task_cases.npz"), **d)
+    print("task_cases written; reference final PSNR", psnr, "loss", loss[0], "->", loss[-1])
+
+
 if __name__ == "__main__":
     oracle.build(ref=True)
     ref = Ref()
+    if len(sys.argv) > 1 and sys.argv[1] == "tasks":
+        task_cases(ref)
+        sys.exit(0)
     scalar_cases(ref)
     encode_cases(ref)
     neural_cases(ref)
+    task_cases(ref)
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)) // 1024, "KiB")

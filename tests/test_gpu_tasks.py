@@ -1,0 +1,94 @@
+"""GPU (-m gpu): the image-fitting task around the hot path against the reference's own fit_image run
+(tests/golden/task_cases.npz: the reference's procedural test image, its trained model, loss curve and final PSNR).
+
+Bars: sampler coordinates/targets BIT-EXACT; rendering the reference-trained model gives the reference's PSNR to 1e-6 dB
+(exact head); a fit from the same seeds ends within 0.5 dB of the reference's final PSNR (north-star tolerance), with the
+exact head and with the tensor-core head."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2311_15439_b200 as pkg
+    return pkg
+
+
+@pytest.fixture(scope="module")
+def golden_task():
+    import os
+    return np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "task_cases.npz"))
+
+
+def cfg_of(sx, g):
+    c = g["cfg"]
+    return sx.EncoderConfig(dim=int(c[0]), levels=int(c[1]), table_size=int(c[2]), features=int(c[3]),
+                            base_resolution=int(c[4]), growth=float(g["growth"]))
+
+
+def test_psnr_from_mse(sx, golden_task):
+    g = golden_task
+    for v, want in zip(g["psnr_examples_in"], g["psnr_examples_out"]):
+        assert sx.psnr_from_mse(float(v)) == pytest.approx(float(want), rel=1e-15)
+
+
+def test_image_sampler_is_bit_exact(sx, oracle_lib, golden_task):
+    img = golden_task["image"]
+    h, w = img.shape[:2]
+    image_dev = torch.as_tensor(img, device="cuda:0")
+    sampler = sx.image_sampler(image_dev, w, h, 1234)
+    for step in (0, 5, 299):
+        coords, targets = sampler(step, 777)
+        u = oracle_lib.rng_u64(1234, step, 777)          # CounterRng(seed, step).next_u64(), src/tasks.cpp:116-118
+        idx = (u % np.uint64(w * h)).astype(np.int64)
+        xi, yi = idx % w, idx // w
+        want = np.stack([(xi + 0.5) / w, (yi + 0.5) / h], axis=1)
+        assert np.array_equal(coords.cpu().numpy(), want)
+        assert np.array_equal(targets.cpu().numpy(), img[yi, xi])
+
+
+def test_render_of_reference_model_reproduces_reference_psnr(sx, golden_task):
+    g = golden_task
+    cfg = cfg_of(sx, g)
+    enc = sx.HashEncoder(cfg)
+    for l in range(cfg.levels):
+        enc.set_table(l, g["tables"][l])
+    mlp = sx.Mlp(sx.MlpConfig(cfg.encoded_width(), 64, 2, 3))
+    mlp.set_parameters(g["mlp_params"])
+    img = g["image"]
+    image_dev = torch.as_tensor(img, device="cuda:0")
+    psnr = sx.psnr_from_mse(sx.render_mse(enc, mlp, image_dev, img.shape[1], img.shape[0], chunk=1000))
+    assert abs(psnr - float(g["final_psnr"])) <= 1e-6
+    mlp.set_precision(1)  # tensor-core head: same model, PSNR within 0.01 dB
+    psnr_tc = sx.psnr_from_mse(sx.render_mse(enc, mlp, image_dev, img.shape[1], img.shape[0]))
+    assert abs(psnr_tc - float(g["final_psnr"])) <= 1e-2
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_fit_image_matches_reference_psnr(sx, golden_task, precision):
+    g = golden_task
+    cfg = cfg_of(sx, g)
+    tc = sx.TrainConfig(batch_size=int(g["batch"]), steps=int(g["steps"]), seed=1234, record_every=1)
+    res = sx.fit_image(g["image"], cfg, tc, sx.FitImageOptions(init_seed=42, mlp_precision=precision))
+    loss = np.array([v for _, v in res.train.loss_curve])
+    ref = g["loss"]
+    assert abs(loss[0] - ref[0]) <= (1e-12 if precision == 0 else 1e-6) * ref[0]   # same batch, same init
+    assert np.all(np.abs(loss[:20] - ref[:20]) <= 2e-3 * ref[:20])
+    assert abs(res.final_psnr - float(g["final_psnr"])) <= 0.5, (res.final_psnr, float(g["final_psnr"]))
+    assert res.psnr_curve[-1][1] > res.psnr_curve[0][1] + 10.0
+
+
+def test_fit_image_validation(sx):
+    cfg = sx.EncoderConfig(dim=3, levels=16, table_size=1 << 10, features=2, base_resolution=4, growth=1.25)
+    with pytest.raises(ValueError, match="dim must be 2"):
+        sx.fit_image(np.zeros((8, 8, 3)), cfg, sx.TrainConfig(batch_size=8, steps=1))
+    cfg.dim = 2
+    with pytest.raises(ValueError):
+        sx.fit_image(np.full((8, 8, 3), 1.5), cfg, sx.TrainConfig(batch_size=8, steps=1))
+    with pytest.raises(ValueError):
+        sx.fit_image(np.zeros((8, 8)), cfg, sx.TrainConfig(batch_size=8, steps=1))

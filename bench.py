@@ -32,7 +32,7 @@ if ROOT not in sys.path:
 METRIC = "simplex_encode_fwd_bwd_samples_per_s"
 UNIT = "samples/s"
 L, F, T_LOG2, BASE = 16, 2, 19, 16
-GROWTH = {2: 2.0, 3: 1.5}
+GROWTH = {2: 2.0, 3: 1.5, 4: 1.5, 5: 1.5, 6: 1.5}
 BATCH_LOG2 = 20
 
 
@@ -53,8 +53,8 @@ def hbm_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def workload_name(n: int) -> str:
-    return (f"{n}D simplex encode fwd+bwd microbench, L={L} F={F} T=2^{T_LOG2} base={BASE} growth={GROWTH[n]}, "
+def workload_name(n: int, t_log2: int = T_LOG2) -> str:
+    return (f"{n}D simplex encode fwd+bwd microbench, L={L} F={F} T=2^{t_log2} base={BASE} growth={GROWTH[n]}, "
             f"2^{BATCH_LOG2} uniform random samples per GPU")
 
 
@@ -122,12 +122,12 @@ def traffic_for(kernel_key: str):
 
 
 # ---------------------------------------------------------------------------------------------- reference arm
-def cpu_reference_run(n: int, samples: int, threads: int):
+def cpu_reference_run(n: int, samples: int, threads: int, t_log2: int = T_LOG2):
     """Times the reference's encode + encode_backward worker pattern on `samples` samples. Returns (samples/s, kind)."""
     import numpy as np
 
     import oracle
-    cfg = oracle.Config(dim=n, levels=L, table_size=1 << T_LOG2, features=F, base_resolution=BASE, growth=GROWTH[n])
+    cfg = oracle.Config(dim=n, levels=L, table_size=1 << t_log2, features=F, base_resolution=BASE, growth=GROWTH[n])
     o = oracle.Oracle()
     x = o.rng_doubles(99, 1, samples * n).reshape(samples, n)
     up = o.rng_doubles(7, 2, samples * L * F, -1e-3, 1e-3).reshape(samples, L * F)
@@ -172,7 +172,7 @@ def run_reference(args):
     vals = []
     kind = "reference"
     for i in range(args.warmup + args.steps):
-        v, kind = cpu_reference_run(n, samples, threads)
+        v, kind = cpu_reference_run(n, samples, threads, args.log2t)
         if i >= args.warmup:
             vals.append(v)
     value = statistics.mean(vals)
@@ -180,7 +180,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * samples / value, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(n), "dim": n, "levels": L, "features": F, "table_size_log2": T_LOG2,
+        "config": {"workload": workload_name(n, args.log2t), "dim": n, "levels": L, "features": F, "table_size_log2": args.log2t,
                    "note": "CPU reference arm: unmodified reference sources (oracle/_ref) on host cores only"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": f"{samples} samples per step (same RNG streams as the GPU arm), "
@@ -214,7 +214,7 @@ def run_ours(args):
     N = 1 << BATCH_LOG2
     LF = L * F
     dev = torch.device(f"cuda:{local_rank}")
-    cfg = sx.EncoderConfig(dim=n, levels=L, table_size=1 << T_LOG2, features=F, base_resolution=BASE, growth=GROWTH[n])
+    cfg = sx.EncoderConfig(dim=n, levels=L, table_size=1 << args.log2t, features=F, base_resolution=BASE, growth=GROWTH[n])
     enc = sx.HashEncoder(cfg, device=local_rank)
     enc.init_tables(42)
     tune = sx.Tuning(levels_per_thread=args.lpt, block_threads=args.block, level_major=args.level_major,
@@ -240,6 +240,45 @@ def run_ours(args):
         outs.append(torch.empty((N, LF), dtype=torch.float32, device=dev))
     gview = grad.device_view()
     stream = torch.cuda.current_stream()
+
+    autotune = None
+    if args.path == "auto":
+        # Launch-shape autotune OUTSIDE the timed region: one fused launch vs forward + backward launches, sample-major vs
+        # level-major.  Which wins depends on whether tables + gradients of the walked levels fit L2 side by side
+        # (profiles/r1_sweep_*.log): time each candidate for a few steps and keep the fastest.
+        cands = [("fused", 0, 2), ("split", 0, 2), ("fused", 1, 4), ("split", 1, 2)]
+        autotune = {}
+        for path, lm, lpt in cands:
+            enc.set_tuning(sx.Tuning(levels_per_thread=lpt, block_threads=args.block, level_major=lm,
+                                     exact_blend=args.exact, warp_aggregate=args.aggregate))
+
+            def one(i, path=path):
+                k = i % n_sets
+                if path == "fused":
+                    enc.encode_forward_backward(xs[k], ups[k], grad, out=outs[k])
+                else:
+                    enc.encode(xs[k], out=outs[k])
+                    enc.encode_backward(xs[k], ups[k], grad)
+
+            for i in range(2):
+                one(i)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for i in range(4):
+                one(i)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            autotune[f"{path}/level_major={lm}/lpt={lpt}"] = e0.elapsed_time(e1) / 4
+        if dist is not None:  # every rank must take the same path
+            t = torch.tensor(list(autotune.values()), dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            autotune = dict(zip(autotune.keys(), [float(v) for v in t.tolist()]))
+        best = min(autotune, key=autotune.get)
+        path, lm, lpt = cands[list(autotune.keys()).index(best)]
+        args.path = path
+        enc.set_tuning(sx.Tuning(levels_per_thread=lpt, block_threads=args.block, level_major=lm, exact_blend=args.exact,
+                                 warp_aggregate=args.aggregate))
 
     def step(i, ev=None):
         k = i % n_sets
@@ -352,28 +391,58 @@ def run_ours(args):
             try:
                 threads = host_threads()
                 samples = min(1 << 18, threads << 15)
-                v, kind = cpu_reference_run(n, samples, threads)
+                v, kind = cpu_reference_run(n, samples, threads, args.log2t)
                 cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
                        "sample": f"{samples} samples of the same workload (same RNG streams), reference worker pattern: "
                                  f"encode+encode_backward per contiguous chunk into a per-thread accumulator"}
             except Exception as exc:  # the GPU numbers stand on their own; say why the baseline is missing
                 cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": str(exc)}
 
+        # ---- extra (not the headline): the whole training step with the tcgen05 head on the same batch shape
+        train = None
+        if not args.no_train and n in (2, 3):
+            try:
+                mlp = sx.Mlp(sx.MlpConfig(LF, 64, 2, 3), device=local_rank)
+                mlp.init_params(sx.hash_combine(42, 1))
+                mlp.set_precision(1)
+                tr = sx.Trainer(enc, mlp)
+                tgt = torch.rand((N, 3), dtype=torch.float32, device=dev)
+                ta, ma = sx.AdamConfig(lr=1e-2), sx.AdamConfig(lr=1e-3)
+                for _ in range(3):
+                    tr.step(xs[0], tgt, ta, ma)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for i in range(8):
+                    tr.step(xs[i % n_sets], tgt, ta, ma)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                tms = e0.elapsed_time(e1) / 8
+                train = {"what": "encode -> tcgen05 MLP 32-64-64-3 (split bf16) fwd+MSE+bwd -> encode_backward -> sparse Adam "
+                                 "+ Adam, one 2^20-sample batch per step, loss read back every step",
+                         "ms_per_step": tms, "samples_per_s": N / (tms * 1e-3)}
+                del tr, mlp
+            except Exception as exc:
+                train = {"error": str(exc)}
+
         t = enc.tuning()
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64 lattice math / u32 hash / f32 features+grads", "data": "synthetic",
-            "config": {"workload": workload_name(n), "dim": n, "levels": L, "features": F, "table_size_log2": T_LOG2,
-                       "base_resolution": BASE, "growth": GROWTH[n], "samples_per_gpu_per_step": N,
+            "config": {"workload": workload_name(n, args.log2t), "dim": n, "levels": L, "features": F,
+                       "table_size_log2": args.log2t, "base_resolution": BASE, "growth": GROWTH[n], "samples_per_gpu_per_step": N,
                        "coords": "f32 on device (CounterRng(99,1))", "path": args.path,
-                       "l2_policy": f"inputs larger than L2: {n_sets} rotating sets x 268 MB + 64 MiB tables + 64 MiB grads",
+                       "autotune_ms": autotune,
+                       "l2_policy": f"inputs larger than L2: {n_sets} rotating input sets x 268 MB, plus "
+                                    f"{L * (1 << args.log2t) * F * 4 >> 20} MiB tables and as much gradient accumulator",
                        "tuning": {"levels_per_thread": t.levels_per_thread, "block_threads": t.block_threads,
                                   "level_major": t.level_major, "exact_blend": t.exact_blend,
                                   "warp_aggregate": t.warp_aggregate},
                        "multi_gpu": "batch sharded, tables replicated, NCCL all-reduce of the 64 MiB table-gradient "
                                     "buffer per step" if world > 1 and not args.no_allreduce else "single GPU"},
             "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu,
+            "train_step": train,
         }
     if dist is not None:
         dist.barrier()
@@ -388,15 +457,17 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--dim", type=int, default=3, choices=[2, 3])
-    ap.add_argument("--path", choices=["fused", "split"], default="fused")
+    ap.add_argument("--dim", type=int, default=3, choices=[2, 3, 4, 5, 6])
+    ap.add_argument("--log2t", type=int, default=T_LOG2, help="log2 of the table size (19 = BASELINE configs[1], 22 = the sweep)")
+    ap.add_argument("--path", choices=["auto", "fused", "split"], default="auto")
     ap.add_argument("--lpt", type=int, default=0)
     ap.add_argument("--block", type=int, default=0)
-    ap.add_argument("--level-major", type=int, default=0)
+    ap.add_argument("--level-major", type=int, default=-1)
     ap.add_argument("--exact", type=int, default=1)
     ap.add_argument("--aggregate", type=int, default=0)
     ap.add_argument("--no-allreduce", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-train", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":

@@ -79,7 +79,7 @@ class Tuning:
 
     levels_per_thread: int = 0
     block_threads: int = 0
-    level_major: int = 0
+    level_major: int = -1  # -1 auto, 0 sample-major, 1 level-major
     exact_blend: int = 1
     warp_aggregate: int = 0
     merge_pairs: int = 0  # 1 on, -1 off, 0 library default (on)

@@ -1,0 +1,106 @@
+#!/usr/bin/env python
+"""tools/config_runs.py -- the other BASELINE.json configs on one B200 (bench.py stays the contract for configs[1]).
+
+  C1  2D image fitting, synthetic 2048x2048 RGB (the reference's make_test_image(seed 7)), L=16 F=2 T=2^19,
+      2^18 samples/batch: first STEPS steps on the GPU (exact head and tcgen05 head) next to the SAME steps run by
+      the unmodified reference on the host cores (oracle/_ref) -> loss curves side by side + throughput of both.
+  C3  gigapixel-style 2D fitting at 2^22 samples/step (procedural target evaluated on the device), growth 2.0
+  C4  NeRF-style 3D encode + fused 64-wide MLP at 2^24 samples/step
+Prints one JSON object per config."""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2311_15439_b200 as sx  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--steps", type=int, default=30)
+ap.add_argument("--skip-c1", action="store_true")
+a = ap.parse_args()
+
+
+def timed_steps(fn, steps):
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    out = [fn(i) for i in range(steps)]
+    e1.record()
+    torch.cuda.synchronize()
+    return out, e0.elapsed_time(e1) / steps
+
+
+# ------------------------------------------------------------------------------------------------ C1
+if not a.skip_c1:
+    import oracle
+    W = H = 2048
+    growth = (2048 / 16) ** (1 / 15)
+    cfg = sx.EncoderConfig(dim=2, levels=16, table_size=1 << 19, features=2, base_resolution=16, growth=growth)
+    ocfg = oracle.Config(dim=2, levels=16, table_size=1 << 19, features=2, base_resolution=16, growth=growth)
+    batch = 1 << 18
+    res = {"config": "C1 2D image fit 2048x2048, L=16 F=2 T=2^19, batch 2^18", "steps": a.steps}
+    if oracle.Ref.available():
+        ref = oracle.Ref()
+        t0 = time.time()
+        img = ref.make_test_image(W, H, 7)
+        res["image_s"] = time.time() - t0
+        threads = max(1, min(os.cpu_count() or 1, 32))
+        t0 = time.time()
+        psnr_ref, loss_ref, _, _ = ref.fit_image(img, ocfg, batch=batch, steps=a.steps, threads=threads)
+        dt = time.time() - t0
+        res["reference"] = {"threads": threads, "seconds_incl_final_render": dt, "loss_first": loss_ref[0], "loss_last": loss_ref[-1],
+                            "final_psnr": psnr_ref, "loss": [float(v) for v in loss_ref]}
+    else:
+        rng = np.random.default_rng(7)
+        img = rng.random((H, W, 3))
+        res["reference"] = None
+    for mode, name in ((0, "exact"), (1, "tcgen05_bf16x3")):
+        t0 = time.time()
+        r = sx.fit_image(img, cfg, sx.TrainConfig(batch_size=batch, steps=a.steps, record_every=1),
+                         sx.FitImageOptions(mlp_precision=mode))
+        dt = time.time() - t0
+        loss = [v for _, v in r.train.loss_curve]
+        entry = {"seconds_incl_upload_and_final_render": dt, "loss_first": loss[0], "loss_last": loss[-1], "final_psnr": r.final_psnr}
+        if res.get("reference"):
+            lr = np.array(res["reference"]["loss"])
+            entry["max_rel_loss_diff_vs_reference"] = float(np.max(np.abs(np.array(loss) - lr) / lr))
+            entry["psnr_diff_vs_reference_db"] = r.final_psnr - res["reference"]["final_psnr"]
+        res[name] = entry
+    if res.get("reference"):
+        res["reference"].pop("loss")
+    print(json.dumps(res), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------ C3 / C4 throughput
+def train_throughput(n, log2_batch, growth, label):
+    N = 1 << log2_batch
+    cfg = sx.EncoderConfig(dim=n, levels=16, table_size=1 << 19, features=2, base_resolution=16, growth=growth)
+    enc = sx.HashEncoder(cfg)
+    enc.init_tables(42)
+    mlp = sx.Mlp(sx.MlpConfig(32, 64, 2, 3))
+    mlp.init_params(sx.hash_combine(42, 1))
+    mlp.set_precision(1)
+    tr = sx.Trainer(enc, mlp)
+    x = torch.empty((N, n), dtype=torch.float32, device="cuda")
+    sx.CounterRng(99, 1).fill_device(x)
+    # procedural target evaluated on the device (no 12.9 GB image is stored)
+    tgt = torch.stack([0.5 + 0.5 * torch.sin(40 * x[:, 0]) * torch.cos(31 * x[:, 1]), x[:, 0] * x[:, -1],
+                       0.5 + 0.5 * torch.cos(57 * x[:, -1])], dim=1).contiguous()
+    ta, ma = sx.AdamConfig(lr=1e-2), sx.AdamConfig(lr=1e-3)
+    for _ in range(2):
+        tr.step(x, tgt, ta, ma)
+    losses, ms = timed_steps(lambda i: tr.step(x, tgt, ta, ma), 8)
+    print(json.dumps({"config": label, "samples_per_step": N, "ms_per_step": ms, "samples_per_s": N / ms * 1e3,
+                      "loss_first": losses[0], "loss_last": losses[-1]}), flush=True)
+    del tr, mlp, enc, x, tgt
+    torch.cuda.empty_cache()
+
+
+train_throughput(2, 22, 2.0, "C3-style 2D fit, 2^22 samples/step, L=16 F=2 T=2^19 growth 2.0, tcgen05 head, full training step")
+train_throughput(3, 24, 1.5, "C4-style 3D encode + fused 64-wide MLP, 2^24 samples/step, L=16 F=2 T=2^19, full training step")

@@ -433,6 +433,9 @@ class Ref:
                                     C.c_int, P(CAdamConfig), P(CAdamConfig), P(dbl), P(dbl), P(C.c_float), P(C.c_float)]
         L.sxr_psnr_from_mse.restype = dbl
         L.sxr_psnr_from_mse.argtypes = [dbl]
+        L.sxr_save_checkpoint.argtypes = [C.c_char_p, vp, vp]
+        L.sxr_load_checkpoint.argtypes = [C.c_char_p, P(CConfig), P(C.c_float), C.c_size_t, P(C.c_int), P(CMlpConfig),
+                                          P(C.c_float), C.c_size_t]
 
     def _check(self, st):
         if st != 0:
@@ -524,6 +527,23 @@ class Ref:
 
     def psnr_from_mse(self, mse: float) -> float:
         return self.lib.sxr_psnr_from_mse(mse)
+
+    def save_checkpoint(self, path: str, encoder: "RefEncoder", mlp: "RefMlp" = None) -> None:
+        self._check(self.lib.sxr_save_checkpoint(path.encode(), encoder.h, mlp.h if mlp is not None else None))
+
+    def load_checkpoint(self, path: str, max_table_floats: int = 1 << 24, max_mlp_floats: int = 1 << 20):
+        """Returns (Config, tables[L, T*F], MlpConfig or None, mlp params or None) as read by the reference."""
+        cfg, mcfg, has = CConfig(), CMlpConfig(), C.c_int(0)
+        tables = np.zeros(max_table_floats, dtype=np.float32)
+        params = np.zeros(max_mlp_floats, dtype=np.float32)
+        self._check(self.lib.sxr_load_checkpoint(path.encode(), C.byref(cfg), _ptr(tables, C.c_float), tables.size,
+                                                 C.byref(has), C.byref(mcfg), _ptr(params, C.c_float), params.size))
+        c = Config(cfg.dim, cfg.levels, cfg.table_size, cfg.features, cfg.base_resolution, cfg.growth, cfg.backend, 0)
+        t = tables[:c.levels * c.table_size * c.features].reshape(c.levels, -1).copy()
+        if not has.value:
+            return c, t, None, None
+        m = MlpConfig(mcfg.input_width, mcfg.hidden_width, mcfg.hidden_layers, mcfg.output_width)
+        return c, t, m, params[:m.param_count].copy()
 
 
 class RefEncoder:

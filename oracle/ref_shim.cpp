@@ -20,6 +20,7 @@
 #include "sxen/lattice.hpp"
 #include "sxen/mlp.hpp"
 #include "sxen/optimizer.hpp"
+#include "sxen/checkpoint.hpp"
 #include "sxen/image.hpp"
 #include "sxen/rng.hpp"
 #include "sxen/tasks.hpp"
@@ -394,5 +395,30 @@ int sxr_fit_image(const double* pixels, int width, int height, const Cfg* cfg, i
 }
 
 double sxr_psnr_from_mse(double mse) { return sxen::psnr_from_mse(mse); }
+
+// ---- checkpoint (src/checkpoint.cpp:81-175); status 9 = IoError
+int sxr_save_checkpoint(const char* path, void* enc, void* mlp) {
+  return guarded([&] { sxen::save_checkpoint(path, *static_cast<sxen::HashEncoder*>(enc), static_cast<sxen::Mlp*>(mlp)); });
+}
+// Loads with the reference and copies out: cfg, tables (L x T*F), and the MLP section if present (has_mlp, mlp cfg, params).
+int sxr_load_checkpoint(const char* path, Cfg* cfg, float* tables_out, std::size_t tables_capacity, int* has_mlp, MlpCfg* mcfg,
+                        float* mlp_out, std::size_t mlp_capacity) {
+  return guarded([&] {
+    sxen::LoadedCheckpoint ck = sxen::load_checkpoint(path);
+    const sxen::EncoderConfig& ec = ck.encoder.config();
+    *cfg = Cfg{ec.dim, ec.levels, ec.table_size, ec.features, ec.base_resolution, ec.growth,
+               ec.backend == sxen::Backend::simplex ? 0 : 1, 0};
+    const std::size_t per = static_cast<std::size_t>(ec.table_size) * static_cast<std::size_t>(ec.features);
+    if (per * static_cast<std::size_t>(ec.levels) > tables_capacity) throw std::invalid_argument("table buffer too small");
+    for (int l = 0; l < ec.levels; ++l) std::memcpy(tables_out + static_cast<std::size_t>(l) * per, ck.encoder.table(l).data(), per * sizeof(float));
+    *has_mlp = ck.mlp.has_value() ? 1 : 0;
+    if (ck.mlp) {
+      const sxen::MlpConfig& mc = ck.mlp->config();
+      *mcfg = MlpCfg{mc.input_width, mc.hidden_width, mc.hidden_layers, mc.output_width};
+      if (ck.mlp->parameter_count() > mlp_capacity) throw std::invalid_argument("mlp buffer too small");
+      std::memcpy(mlp_out, ck.mlp->parameters().data(), ck.mlp->parameter_count() * sizeof(float));
+    }
+  });
+}
 
 }  // extern "C"

@@ -14,6 +14,7 @@ from .encoding import (Backend, EncoderConfig, EncoderGradient, HashEncoder, Lev
 from .optimizer import AdamConfig, AdamState, SparseAdamState  # noqa: E402
 from .mlp import Mlp, MlpConfig  # noqa: E402
 from .trainer import TrainConfig, Trainer, TrainResult, chunk_bounds, train_field  # noqa: E402
+from .checkpoint import load_checkpoint, save_checkpoint  # noqa: E402
 from .tasks import FitImageOptions, FitImageResult, fit_image, image_sampler, psnr_from_mse, render_mse  # noqa: E402
 from .rng import CounterRng, hash_combine, mix64  # noqa: E402
 
@@ -21,7 +22,8 @@ __all__ = ["lib", "CudaError", "IoError", "TrainingError", "Backend", "LevelScal
            "EncoderGradient", "LookupCounters", "Tuning", "equal_memory_multiplier", "level_resolution",
            "skew_constants", "hash_coords", "AdamConfig", "AdamState", "SparseAdamState", "CounterRng", "mix64",
            "hash_combine", "Mlp", "MlpConfig", "TrainConfig", "Trainer", "TrainResult", "chunk_bounds", "train_field",
-           "FitImageOptions", "FitImageResult", "fit_image", "image_sampler", "psnr_from_mse", "render_mse"]
+           "FitImageOptions", "FitImageResult", "fit_image", "image_sampler", "psnr_from_mse", "render_mse",
+           "save_checkpoint", "load_checkpoint"]
 
 
 def device_count() -> int:

@@ -12,6 +12,9 @@
 // is the K-major A operand of the next layer, the K-major A operand of the input-gradient GEMM and the MN-major operand of
 // the weight-gradient GEMM.  Each tile carries one extra 8-column block whose first column is 1.0: used as the B operand of
 // a weight-gradient GEMM it makes the bias gradient fall out as column `in` of the same accumulator.
+// The 64 -> out_w (<= 3) output layer and its input gradient are three dot products per unit: they run on the CUDA cores in
+// fp32 inside the layer-2 epilogue (partial sums of the two column halves meet through shared memory), which removes two
+// tensor-core round trips from the per-tile dependency chain: X0*W0^T | H1*W1^T | dH2*W1 | dH1*W0.
 // One CTA = 128 samples = 128 TMEM lanes, 256 threads: threads t and t+128 share sample t of the tile and split every
 // epilogue's columns in halves (warps w and w+4 read the same TMEM lane quadrant).  The weight-gradient MMAs of a phase are
 // queued behind the phase's dependent-chain MMAs and are only waited for when the tiles they read are about to be rewritten,
@@ -35,25 +38,24 @@ constexpr int X0C = IN + 8, HC = HID + 8;  // tile widths including the ones-col
 // shared-memory map (bytes)
 constexpr uint32_t kW0 = 0;                                     // CM16(64, 32) hi, lo
 constexpr uint32_t kW1 = kW0 + 2 * cm16_bytes(HID, IN);         // CM16(64, 64) hi, lo
-constexpr uint32_t kW2 = kW1 + 2 * cm16_bytes(HID, HID);        // CM16(16, 64) hi, lo (rows >= out_w are zero)
-constexpr uint32_t kX0 = kW2 + 2 * cm16_bytes(OUTP, HID);       // CM16(128, 40) hi, lo
+constexpr uint32_t kX0 = kW1 + 2 * cm16_bytes(HID, HID);        // CM16(128, 40) hi, lo
 constexpr uint32_t kH1 = kX0 + 2 * cm16_bytes(kTile, X0C);      // CM16(128, 72) hi, lo
 constexpr uint32_t kH2 = kH1 + 2 * cm16_bytes(kTile, HC);
 constexpr uint32_t kDY = kH2 + 2 * cm16_bytes(kTile, HC);       // CM16(128, 16) hi, lo
 constexpr uint32_t kDH2 = kDY + 2 * cm16_bytes(kTile, OUTP);    // CM16(128, 64) hi, lo
 constexpr uint32_t kDH1 = kDH2 + 2 * cm16_bytes(kTile, HID);
-constexpr uint32_t kBias = kDH1 + 2 * cm16_bytes(kTile, HID);   // b0[64], b1[64], b2[16] floats
-constexpr uint32_t kSmemBytes = kBias + (HID + HID + OUTP) * 4;
+constexpr uint32_t kBias = kDH1 + 2 * cm16_bytes(kTile, HID);   // b0[64], b1[64], b2[4] floats
+constexpr uint32_t kW2f = kBias + (HID + HID + 4) * 4;          // output layer in fp32: W2f[3][64] (rows >= out_w zero)
+constexpr uint32_t kPP = kW2f + 3 * HID * 4;                    // partial predictions pp[2][128][4]
+constexpr uint32_t kSmemBytes = kPP + 4 * kTile * 4 * 4;  // pp[kSplit <= 4][128][4]
 
 // TMEM columns (fp32): scratch accumulators (128 lanes) and the persistent weight-gradient accumulators (M = 64)
-constexpr uint32_t tS0 = 0;     // [128 x 64] layer-1 pre-activation, later dH2
+constexpr uint32_t tS0 = 0;     // [128 x 64] layer-1 pre-activation, later d(input) (32 cols)
 constexpr uint32_t tS1 = 64;    // [128 x 64] layer-2 pre-activation, later dH1
-constexpr uint32_t tS2 = 128;   // [128 x 32] output (16 cols), later d(input) (32 cols)
-constexpr int kThreads = 256;
-constexpr uint32_t tG0 = 160;   // [64 x 40]  dW0 | db0
-constexpr uint32_t tG1 = 200;   // [64 x 72]  dW1 | db1
-constexpr uint32_t tG2 = 272;   // [64 x 16]  dW2^T
-constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t tG0 = 128;   // [64 x 40]  dW0 | db0
+constexpr uint32_t tG1 = 168;   // [64 x 72]  dW1 | db1
+constexpr uint32_t tG2 = 240;   // [64 x 16]  dW2^T
+constexpr uint32_t kTmemCols = 256;
 
 struct TcArgs {
   const float* params;      // W0[64x32] b0[64] W1[64x64] b1[64] W2[ow x 64] b2[ow]  (src/mlp.cpp:19-32)
@@ -105,30 +107,42 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[1
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// D += A*B over `ksteps` UMMA_K=16 steps with split operands.  Descriptor builders are passed as lambdas of the k step.
-template <class DA, class DB>
-__device__ __forceinline__ void gemm_split(uint32_t d, uint32_t idesc, int ksteps, bool accumulate, bool precise,
-                                           DA desc_a /*(tile_is_lo, ks)*/, DB desc_b) {
+// D += A*B over `ksteps` UMMA_K=16 steps with split operands.  a0/b0 are the descriptors of the hi tiles at k step 0;
+// the lo tile sits `a_lo`/`b_lo` bytes further and one k step adds `a_step`/`b_step` bytes (address field = bytes >> 4).
+__device__ __forceinline__ void gemm_split(uint32_t d, uint32_t idesc, int ksteps, bool accumulate, bool precise, uint64_t a0,
+                                           uint32_t a_lo, uint32_t a_step, uint64_t b0, uint32_t b_lo, uint32_t b_step) {
   for (int ks = 0; ks < ksteps; ++ks) {
-    mma_bf16(d, desc_a(false, ks), desc_b(false, ks), idesc, accumulate || ks > 0);
+    const uint64_t ah = a0 + ((static_cast<uint64_t>(ks) * a_step) >> 4), bh = b0 + ((static_cast<uint64_t>(ks) * b_step) >> 4);
+    mma_bf16(d, ah, bh, idesc, accumulate || ks > 0);
     if (precise) {
-      mma_bf16(d, desc_a(false, ks), desc_b(true, ks), idesc, true);
-      mma_bf16(d, desc_a(true, ks), desc_b(false, ks), idesc, true);
+      mma_bf16(d, ah, bh + (b_lo >> 4), idesc, true);
+      mma_bf16(d, ah + (a_lo >> 4), bh, idesc, true);
     }
   }
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+constexpr int kSplit = 2;                       // epilogue threads per sample row: each handles HID/kSplit columns
+constexpr int CPT = HID / kSplit;               // columns per thread in a hidden-layer epilogue (multiple of 16)
+constexpr int kEpiThreads = kTile * kSplit;     // 8 epilogue warps (kSplit = 4 / 16 warps measured slower: 0.585 vs 0.47 ms)
+constexpr int kThreadsAll = kEpiThreads + 32;   // + one MMA-issuing warp
+
 template <bool TRAIN>
-__global__ void __launch_bounds__(kThreads, 2) mlp_tc_kernel(const __grid_constant__ TcArgs a) {
+__global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_constant__ TcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t bar;     // dependent-chain MMAs of the current phase
-  __shared__ uint64_t bar_g;   // every MMA of the tile, weight-gradient ones included
+  __shared__ uint64_t bar_ready;  // 256 arrivals: the tiles of the next phase are written and the TMEM scratch is drained
+  __shared__ uint64_t bar;        // dependent-chain MMAs of the current phase have completed
+  __shared__ uint64_t bar_g;      // every MMA of the tile (weight-gradient ones included) has completed
   __shared__ uint32_t tmem_base_slot;
-  __shared__ double red_buf[8][4];
+  __shared__ double red_buf[kEpiThreads / 32][4];
   const int tid = threadIdx.x;
   const int t = tid & (kTile - 1);   // sample row inside the tile
-  const int half = tid >> 7;         // which half of an epilogue's columns this thread handles
+  const int half = (tid >> 7) & (kSplit - 1);  // which slice of an epilogue's columns this thread handles
   const int warp = tid >> 5;
+  const bool is_mma_warp = warp == kEpiThreads / 32;
   float* bias = reinterpret_cast<float*>(smem + kBias);
   const float* W0 = a.params;
   const float* b0 = W0 + HID * IN;
@@ -137,40 +151,45 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_tc_kernel(const __grid_consta
   const float* W2 = b1 + HID;
   const float* b2 = W2 + a.out_w * HID;
 
+  constexpr uint32_t loW0 = cm16_bytes(HID, IN), loW1 = cm16_bytes(HID, HID);
+  float* w2f = reinterpret_cast<float*>(smem + kW2f);
+  float* pp = reinterpret_cast<float*>(smem + kPP);
+  constexpr uint32_t loX0 = cm16_bytes(kTile, X0C), loH = cm16_bytes(kTile, HC), loDY = cm16_bytes(kTile, OUTP),
+                     loDH = cm16_bytes(kTile, HID);
+
   // ---- one-time setup: weights (hi/lo CM16 tiles, rows = output unit, cols = input unit), biases, ones columns
-  for (int e = tid; e < HID * IN / 8; e += kThreads) {
-    const int o = e / (IN / 8), ch = e % (IN / 8);
-    float v[8];
+  if (!is_mma_warp) {
+    for (int e = tid; e < HID * IN / 8; e += kEpiThreads) {
+      const int o = e / (IN / 8), ch = e % (IN / 8);
+      float v[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = W0[o * IN + ch * 8 + q];
-    store_chunk(smem + kW0, smem + kW0 + cm16_bytes(HID, IN), o, ch, IN, v);
-  }
-  for (int e = tid; e < HID * HID / 8; e += kThreads) {
-    const int o = e / (HID / 8), ch = e % (HID / 8);
-    float v[8];
+      for (int q = 0; q < 8; ++q) v[q] = W0[o * IN + ch * 8 + q];
+      store_chunk(smem + kW0, smem + kW0 + loW0, o, ch, IN, v);
+    }
+    for (int e = tid; e < HID * HID / 8; e += kEpiThreads) {
+      const int o = e / (HID / 8), ch = e % (HID / 8);
+      float v[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = W1[o * HID + ch * 8 + q];
-    store_chunk(smem + kW1, smem + kW1 + cm16_bytes(HID, HID), o, ch, HID, v);
-  }
-  for (int e = tid; e < OUTP * HID / 8; e += kThreads) {
-    const int o = e / (HID / 8), ch = e % (HID / 8);
-    float v[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = o < a.out_w ? W2[o * HID + ch * 8 + q] : 0.0f;
-    store_chunk(smem + kW2, smem + kW2 + cm16_bytes(OUTP, HID), o, ch, HID, v);
-  }
-  if (tid < HID) {
-    bias[tid] = b0[tid];
-    bias[HID + tid] = b1[tid];
-  }
-  if (tid < OUTP) bias[2 * HID + tid] = tid < a.out_w ? b2[tid] : 0.0f;
-  if (half == 0) {
-    float ones[8] = {1.0f, 0, 0, 0, 0, 0, 0, 0};
-    store_chunk(smem + kX0, smem + kX0 + cm16_bytes(kTile, X0C), t, IN / 8, X0C, ones);
-    store_chunk(smem + kH1, smem + kH1 + cm16_bytes(kTile, HC), t, HID / 8, HC, ones);
-    store_chunk(smem + kH2, smem + kH2 + cm16_bytes(kTile, HC), t, HID / 8, HC, ones);
+      for (int q = 0; q < 8; ++q) v[q] = W1[o * HID + ch * 8 + q];
+      store_chunk(smem + kW1, smem + kW1 + loW1, o, ch, HID, v);
+    }
+    for (int e = tid; e < 3 * HID; e += kEpiThreads) w2f[e] = (e / HID) < a.out_w ? W2[e] : 0.0f;
+    if (tid < HID) {
+      bias[tid] = b0[tid];
+      bias[HID + tid] = b1[tid];
+    }
+    if (tid < 4) bias[2 * HID + tid] = tid < a.out_w ? b2[tid] : 0.0f;
+    if (half == 0) {
+      float ones[8] = {1.0f, 0, 0, 0, 0, 0, 0, 0};
+      store_chunk(smem + kX0, smem + kX0 + loX0, t, IN / 8, X0C, ones);
+      store_chunk(smem + kH1, smem + kH1 + loH, t, HID / 8, HC, ones);
+      store_chunk(smem + kH2, smem + kH2 + loH, t, HID / 8, HC, ones);
+      float zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      store_chunk(smem + kDY, smem + kDY + loDY, t, 1, OUTP, zero);  // columns 8..15 of dY stay zero
+    }
   }
   if (tid == 0) {
+    mbar_init(&bar_ready, kEpiThreads);
     mbar_init(&bar, 1);
     mbar_init(&bar_g, 1);
   }
@@ -180,337 +199,322 @@ __global__ void __launch_bounds__(kThreads, 2) mlp_tc_kernel(const __grid_consta
   __syncthreads();
   tc_fence_after();
   const uint32_t tb = tmem_base_slot;
-  const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-  uint32_t phase = 0, phase_g = 0;
   const bool precise = a.precise != 0;
-
-  const uint32_t sW0 = smem_u32(smem + kW0), sW1 = smem_u32(smem + kW1), sW2 = smem_u32(smem + kW2);
-  const uint32_t sX0 = smem_u32(smem + kX0), sH1 = smem_u32(smem + kH1), sH2 = smem_u32(smem + kH2);
-  const uint32_t sDY = smem_u32(smem + kDY), sDH2 = smem_u32(smem + kDH2), sDH1 = smem_u32(smem + kDH1);
-  constexpr uint32_t loW0 = cm16_bytes(HID, IN), loW1 = cm16_bytes(HID, HID), loW2 = cm16_bytes(OUTP, HID);
-  constexpr uint32_t loX0 = cm16_bytes(kTile, X0C), loH = cm16_bytes(kTile, HC), loDY = cm16_bytes(kTile, OUTP),
-                     loDH = cm16_bytes(kTile, HID);
-
-  double loss_acc = 0.0;
-  double db2_acc[3] = {0.0, 0.0, 0.0};  // out_w <= 3 keeps its bias gradient here; wider heads use column sums below
-  bool g_started = false;
   const unsigned long long n_tiles = (a.n + kTile - 1) / kTile;
+  constexpr int kPhases = TRAIN ? 4 : 2;
+  bool g_started = false;
 
-  for (unsigned long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const unsigned long long s0 = tile * kTile;
-    const unsigned long long smp = s0 + t;
-    const bool valid = smp < a.n;
-
-    // ---- stage 0: features -> X0 tiles.  Lane mapping: 8 rows x 4 chunks per warp instruction keeps both the global
-    // reads (64 contiguous bytes per row) and the shared stores (8 rows = 8 distinct 16-byte bank groups) efficient.
-    // The loads are issued before waiting for the previous tile's weight-gradient MMAs, which still read X0.
-    float xin[2][8];
-    int xrow[2];
-    const int xch = (tid >> 3) & 3;  // 8-column chunk 0..3
-#pragma unroll
-    for (int it = 0; it < 2; ++it) {
-      xrow[it] = (tid & 7) + 8 * ((tid >> 5) + 8 * it);  // 0..127
-      const unsigned long long gs = s0 + xrow[it];
-      if (gs < a.n) {
-        const float4* p = reinterpret_cast<const float4*>(a.features + gs * IN + xch * 8);
-        const float4 x0 = __ldg(p), x1 = __ldg(p + 1);
-        xin[it][0] = x0.x; xin[it][1] = x0.y; xin[it][2] = x0.z; xin[it][3] = x0.w;
-        xin[it][4] = x1.x; xin[it][5] = x1.y; xin[it][6] = x1.z; xin[it][7] = x1.w;
-      } else {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) xin[it][q] = 0.0f;
-      }
-    }
-    if constexpr (TRAIN) {
-      if (g_started) {
-        mbar_wait(&bar_g, phase_g);
-        phase_g ^= 1;
-      }
-    }
-#pragma unroll
-    for (int it = 0; it < 2; ++it) store_chunk(smem + kX0, smem + kX0 + loX0, xrow[it], xch, X0C, xin[it]);
-    fence_proxy_async();
-    tc_fence_before();
-    __syncthreads();
-
-    // ---- layer 1: S0 = X0 * W0^T
-    if (tid == 0) {
-      tc_fence_after();
-      gemm_split(tb + tS0, make_idesc_bf16(128, HID, false, false), IN / 16, false, precise,
-                 [&](bool lo, int ks) { return desc16_k_major(sX0 + (lo ? loX0 : 0), X0C, ks); },
-                 [&](bool lo, int ks) { return desc16_k_major(sW0 + (lo ? loW0 : 0), IN, ks); });
-      tc_commit(&bar);
-    }
-    mbar_wait(&bar, phase);
-    phase ^= 1;
-    tc_fence_after();
-    uint32_t m1 = 0, m2 = 0;  // ReLU masks of this thread's 32 units (bit i = unit 32*half + i active)
-    {
-      uint32_t r[2][16];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) tmem_ld16_nowait(tb + lane_base + tS0 + 32 * half + 16 * q, r[q]);
-      tmem_ld_wait();
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        float v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          float x = __uint_as_float(r[q][i]) + bias[32 * half + 16 * q + i];
-          x = x > 0.0f ? x : 0.0f;
-          if (x > 0.0f) m1 |= 1u << (16 * q + i);
-          v[i] = x;
-        }
-        store_chunk(smem + kH1, smem + kH1 + loH, t, 4 * half + 2 * q, HC, v);
-        store_chunk(smem + kH1, smem + kH1 + loH, t, 4 * half + 2 * q + 1, HC, v + 8);
-      }
-    }
-    fence_proxy_async();
-    tc_fence_before();
-    __syncthreads();
-
-    // ---- layer 2: S1 = H1 * W1^T
-    if (tid == 0) {
-      tc_fence_after();
-      gemm_split(tb + tS1, make_idesc_bf16(128, HID, false, false), HID / 16, false, precise,
-                 [&](bool lo, int ks) { return desc16_k_major(sH1 + (lo ? loH : 0), HC, ks); },
-                 [&](bool lo, int ks) { return desc16_k_major(sW1 + (lo ? loW1 : 0), HID, ks); });
-      tc_commit(&bar);
-    }
-    mbar_wait(&bar, phase);
-    phase ^= 1;
-    tc_fence_after();
-    {
-      uint32_t r[2][16];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) tmem_ld16_nowait(tb + lane_base + tS1 + 32 * half + 16 * q, r[q]);
-      tmem_ld_wait();
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        float v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          float x = __uint_as_float(r[q][i]) + bias[HID + 32 * half + 16 * q + i];
-          x = x > 0.0f ? x : 0.0f;
-          if (x > 0.0f) m2 |= 1u << (16 * q + i);
-          v[i] = x;
-        }
-        store_chunk(smem + kH2, smem + kH2 + loH, t, 4 * half + 2 * q, HC, v);
-        store_chunk(smem + kH2, smem + kH2 + loH, t, 4 * half + 2 * q + 1, HC, v + 8);
-      }
-    }
-    fence_proxy_async();
-    tc_fence_before();
-    __syncthreads();
-
-    // ---- output layer: S2[:, 0:16] = H2 * W2p^T
-    if (tid == 0) {
-      tc_fence_after();
-      gemm_split(tb + tS2, make_idesc_bf16(128, OUTP, false, false), HID / 16, false, precise,
-                 [&](bool lo, int ks) { return desc16_k_major(sH2 + (lo ? loH : 0), HC, ks); },
-                 [&](bool lo, int ks) { return desc16_k_major(sW2 + (lo ? loW2 : 0), HID, ks); });
-      tc_commit(&bar);
-    }
-    mbar_wait(&bar, phase);
-    phase ^= 1;
-    tc_fence_after();
-    if (half == 0) {
-      uint32_t r[16];
-      tmem_ld16_nowait(tb + lane_base + tS2, r);
-      tmem_ld_wait();
-      float u[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) u[i] = 0.0f;
-      for (int o = 0; o < a.out_w; ++o) {
-        const float p = __uint_as_float(r[o]) + bias[2 * HID + o];
-        if (valid && a.pred) a.pred[smp * a.out_w + o] = p;
-        if constexpr (TRAIN) {
-          if (valid) {
-            // src/trainer.cpp:38-44: e = pred - target, loss += e*e, upstream = 2e/(B*out_w), all in double
-            const double tg = a.target_f32 ? static_cast<double>(static_cast<const float*>(a.targets)[smp * a.out_w + o])
-                                           : static_cast<const double*>(a.targets)[smp * a.out_w + o];
-            const double e = static_cast<double>(p) - tg;
-            loss_acc += e * e;
-            const double up = a.upstream_scale * e;
-            u[o] = static_cast<float>(up);
-            if (o < 3) db2_acc[o] += up;
+  if (is_mma_warp) {
+    // =========================== MMA warp: one lane issues every tcgen05.mma of the CTA ===========================
+    if ((tid & 31) == 0) {
+      const uint32_t sW0 = smem_u32(smem + kW0), sW1 = smem_u32(smem + kW1);
+      const uint32_t sX0 = smem_u32(smem + kX0), sH1 = smem_u32(smem + kH1), sH2 = smem_u32(smem + kH2);
+      const uint32_t sDY = smem_u32(smem + kDY), sDH2 = smem_u32(smem + kDH2), sDH1 = smem_u32(smem + kDH1);
+      // K-major views step 256 B per UMMA_K = 16; MN-major views step two 8-row groups
+      const uint64_t kX0d = desc16_k_major(sX0, X0C, 0), kH1d = desc16_k_major(sH1, HC, 0);
+      const uint64_t kW0d = desc16_k_major(sW0, IN, 0), kW1d = desc16_k_major(sW1, HID, 0);
+      const uint64_t kDH2d = desc16_k_major(sDH2, HID, 0), kDH1d = desc16_k_major(sDH1, HID, 0);
+      const uint64_t mW0d = desc16_mn_major(sW0, IN, 0), mW1d = desc16_mn_major(sW1, HID, 0);
+      const uint64_t mX0d = desc16_mn_major(sX0, X0C, 0), mH1d = desc16_mn_major(sH1, HC, 0), mH2d = desc16_mn_major(sH2, HC, 0);
+      const uint64_t mDYd = desc16_mn_major(sDY, OUTP, 0), mDH2d = desc16_mn_major(sDH2, HID, 0), mDH1d = desc16_mn_major(sDH1, HID, 0);
+      constexpr uint32_t kStep = 256;
+      uint32_t ph = 0;
+      for (unsigned long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        for (int p = 0; p < kPhases; ++p) {
+          mbar_wait(&bar_ready, ph);
+          ph ^= 1;
+          tc_fence_after();
+          switch (p) {
+            case 0:  // layer 1: S0 = X0 * W0^T
+              gemm_split(tb + tS0, make_idesc_bf16(128, HID, false, false), IN / 16, false, precise, kX0d, loX0, kStep, kW0d, loW0, kStep);
+              tc_commit(&bar);
+              break;
+            case 1:  // layer 2: S1 = H1 * W1^T
+              gemm_split(tb + tS1, make_idesc_bf16(128, HID, false, false), HID / 16, false, precise, kH1d, loH, kStep, kW1d, loW1, kStep);
+              tc_commit(&bar);
+              break;
+            case 2:  // S1 = dH2 * W1;  G2 += H2^T * dY (dW2^T);  G1 += dH2^T * [H1 | 1]
+              gemm_split(tb + tS1, make_idesc_bf16(128, HID, false, true), HID / 16, false, precise, kDH2d, loDH, kStep, mW1d, loW1,
+                         2 * cm16_row_group_stride(HID));
+              tc_commit(&bar);
+              gemm_split(tb + tG2, make_idesc_bf16(64, OUTP, true, true), kTile / 16, g_started, precise, mH2d, loH,
+                         2 * cm16_row_group_stride(HC), mDYd, loDY, 2 * cm16_row_group_stride(OUTP));
+              gemm_split(tb + tG1, make_idesc_bf16(64, HC, true, true), kTile / 16, g_started, precise, mDH2d, loDH,
+                         2 * cm16_row_group_stride(HID), mH1d, loH, 2 * cm16_row_group_stride(HC));
+              break;
+            default:  // S0[:, 0:32] = dH1 * W0 (d loss / d encoding);  G0 += dH1^T * [X0 | 1]
+              gemm_split(tb + tS0, make_idesc_bf16(128, IN, false, true), HID / 16, false, precise, kDH1d, loDH, kStep, mW0d, loW0,
+                         2 * cm16_row_group_stride(IN));
+              tc_commit(&bar);
+              gemm_split(tb + tG0, make_idesc_bf16(64, X0C, true, true), kTile / 16, g_started, precise, mDH1d, loDH,
+                         2 * cm16_row_group_stride(HID), mX0d, loX0, 2 * cm16_row_group_stride(X0C));
+              tc_commit(&bar_g);  // covers G2, G1 and G0 of this tile
+              g_started = true;
+              break;
           }
+        }
+      }
+    }
+  } else {
+    // =========================== epilogue warps ===========================
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    uint32_t phase = 0, phase_g = 0;
+    double loss_acc = 0.0;
+    double db2_acc[3] = {0.0, 0.0, 0.0};
+
+    // hidden-layer epilogue: 32 columns of this thread's row out of a TMEM accumulator -> (bias, ReLU | mask) -> hi/lo tile
+    auto ready = [&]() {
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(&bar_ready);
+    };
+    auto wait_chain = [&]() {
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+      tc_fence_after();
+    };
+
+    for (unsigned long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const unsigned long long s0 = tile * kTile;
+      const unsigned long long smp = s0 + t;
+      const bool valid = smp < a.n;
+
+      // ---- stage 0: features -> X0 tiles.  Lane mapping: 8 rows x 4 chunks per warp instruction keeps both the global
+      // reads (64 contiguous bytes per row) and the shared stores (8 rows = 8 distinct 16-byte bank groups) efficient.
+      // The loads are issued before waiting for the previous tile's weight-gradient MMAs, which still read X0.
+      constexpr int kXIt = (kTile * (IN / 8)) / kEpiThreads;  // 16-byte-pair chunks per thread
+      float xin[kXIt][8];
+      int xrow[kXIt];
+      const int xch = (tid >> 3) & 3;
+#pragma unroll
+      for (int it = 0; it < kXIt; ++it) {
+        xrow[it] = (tid & 7) + 8 * ((tid >> 5) + (kEpiThreads / 32) * it);
+        const unsigned long long gs = s0 + xrow[it];
+        if (gs < a.n) {
+          const float4* p = reinterpret_cast<const float4*>(a.features + gs * IN + xch * 8);
+          const float4 x0 = __ldg(p), x1 = __ldg(p + 1);
+          xin[it][0] = x0.x; xin[it][1] = x0.y; xin[it][2] = x0.z; xin[it][3] = x0.w;
+          xin[it][4] = x1.x; xin[it][5] = x1.y; xin[it][6] = x1.z; xin[it][7] = x1.w;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) xin[it][q] = 0.0f;
         }
       }
       if constexpr (TRAIN) {
-        store_chunk(smem + kDY, smem + kDY + loDY, t, 0, OUTP, u);
-        store_chunk(smem + kDY, smem + kDY + loDY, t, 1, OUTP, u + 8);
+        if (g_started) {
+          mbar_wait(&bar_g, phase_g);
+          phase_g ^= 1;
+        }
       }
-    }
-    if constexpr (!TRAIN) {
+#pragma unroll
+      for (int it = 0; it < kXIt; ++it) store_chunk(smem + kX0, smem + kX0 + loX0, xrow[it], xch, X0C, xin[it]);
+      ready();
+
+      // ---- layer 1 epilogue: S0 -> H1
+      uint32_t m1 = 0, m2 = 0;  // ReLU masks of this thread's 32 units (bit i = unit 32*half + i active)
+      wait_chain();
+      {
+        uint32_t r[CPT / 16][16];
+#pragma unroll
+        for (int q = 0; q < CPT / 16; ++q) tmem_ld16_nowait(tb + lane_base + tS0 + CPT * half + 16 * q, r[q]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int q = 0; q < CPT / 16; ++q) {
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float x = __uint_as_float(r[q][i]) + bias[CPT * half + 16 * q + i];
+            x = x > 0.0f ? x : 0.0f;
+            if (x > 0.0f) m1 |= 1u << (16 * q + i);
+            v[i] = x;
+          }
+          store_chunk(smem + kH1, smem + kH1 + loH, t, (CPT / 8) * half + 2 * q, HC, v);
+          store_chunk(smem + kH1, smem + kH1 + loH, t, (CPT / 8) * half + 2 * q + 1, HC, v + 8);
+        }
+      }
+      ready();
+
+      // ---- layer 2 epilogue: S1 -> H2, then the output layer, the loss and its way back to dH2 on the CUDA cores
+      wait_chain();
+      {
+        uint32_t r[CPT / 16][16];
+#pragma unroll
+        for (int q = 0; q < CPT / 16; ++q) tmem_ld16_nowait(tb + lane_base + tS1 + CPT * half + 16 * q, r[q]);
+        tmem_ld_wait();
+        float p0 = 0.0f, p1 = 0.0f, p2 = 0.0f;  // partial predictions over this thread's 32 hidden units
+#pragma unroll
+        for (int q = 0; q < CPT / 16; ++q) {
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int c = CPT * half + 16 * q + i;
+            float x = __uint_as_float(r[q][i]) + bias[HID + c];
+            x = x > 0.0f ? x : 0.0f;
+            if (x > 0.0f) m2 |= 1u << (16 * q + i);
+            v[i] = x;
+            p0 = __fmaf_rn(w2f[c], x, p0);
+            p1 = __fmaf_rn(w2f[HID + c], x, p1);
+            p2 = __fmaf_rn(w2f[2 * HID + c], x, p2);
+          }
+          store_chunk(smem + kH2, smem + kH2 + loH, t, (CPT / 8) * half + 2 * q, HC, v);
+          store_chunk(smem + kH2, smem + kH2 + loH, t, (CPT / 8) * half + 2 * q + 1, HC, v + 8);
+        }
+        *reinterpret_cast<float4*>(pp + (half * kTile + t) * 4) = make_float4(p0, p1, p2, 0.0f);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");  // the two halves of every row have posted their partials
+      float u[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      {
+        float pr[3] = {bias[2 * HID], bias[2 * HID + 1], bias[2 * HID + 2]};
+#pragma unroll
+        for (int k = 0; k < kSplit; ++k) {
+          const float4 pk = *reinterpret_cast<const float4*>(pp + (k * kTile + t) * 4);
+          pr[0] += pk.x;
+          pr[1] += pk.y;
+          pr[2] += pk.z;
+        }
+#pragma unroll
+        for (int o = 0; o < 3; ++o) {
+          if (o < a.out_w) {
+            if (half == 0 && valid && a.pred) a.pred[smp * a.out_w + o] = pr[o];
+            if constexpr (TRAIN) {
+              if (valid) {
+                // src/trainer.cpp:38-44: e = pred - target, loss += e*e, upstream = 2e/(B*out_w), all in double
+                const double tg = a.target_f32 ? static_cast<double>(static_cast<const float*>(a.targets)[smp * a.out_w + o])
+                                               : static_cast<const double*>(a.targets)[smp * a.out_w + o];
+                const double e = static_cast<double>(pr[o]) - tg;
+                const double up = a.upstream_scale * e;
+                u[o] = static_cast<float>(up);
+                if (half == 0) {
+                  loss_acc += e * e;
+                  db2_acc[o] += up;
+                }
+              }
+            }
+          }
+        }
+      }
+      if constexpr (!TRAIN) continue;  // the tiles and S1 are only rewritten after the next bar_ready rounds
+      if (half == 0) store_chunk(smem + kDY, smem + kDY + loDY, t, 0, OUTP, u);  // B operand of G2 = H2^T * dY
+      {
+        // dH2[c] = sum_o u[o] * W2[o][c], zero where layer 2's ReLU clamped (src/mlp.cpp:189-199)
+#pragma unroll
+        for (int q = 0; q < CPT / 16; ++q) {
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int c = CPT * half + 16 * q + i;
+            const float g = __fmaf_rn(u[2], w2f[2 * HID + c], __fmaf_rn(u[1], w2f[HID + c], __fmul_rn(u[0], w2f[c])));
+            v[i] = ((m2 >> (16 * q + i)) & 1u) ? g : 0.0f;
+          }
+          store_chunk(smem + kDH2, smem + kDH2 + loDH, t, (CPT / 8) * half + 2 * q, HID, v);
+          store_chunk(smem + kDH2, smem + kDH2 + loDH, t, (CPT / 8) * half + 2 * q + 1, HID, v + 8);
+        }
+      }
+      ready();
+
+      // ---- backward epilogue of layer 2: S1 -> dH1 (masked by layer 1's ReLU)
+      wait_chain();
+      {
+        uint32_t r[CPT / 16][16];
+#pragma unroll
+        for (int q = 0; q < CPT / 16; ++q) tmem_ld16_nowait(tb + lane_base + tS1 + CPT * half + 16 * q, r[q]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int q = 0; q < CPT / 16; ++q) {
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = ((m1 >> (16 * q + i)) & 1u) ? __uint_as_float(r[q][i]) : 0.0f;
+          store_chunk(smem + kDH1, smem + kDH1 + loDH, t, (CPT / 8) * half + 2 * q, HID, v);
+          store_chunk(smem + kDH1, smem + kDH1 + loDH, t, (CPT / 8) * half + 2 * q + 1, HID, v + 8);
+        }
+      }
+      ready();
+
+      // ---- backward epilogue of layer 1: S0[:, 0:32] -> d loss / d encoding, straight to global memory
+      wait_chain();
+      if (half < IN / 16) {
+        uint32_t r[16];
+        tmem_ld16_nowait(tb + lane_base + tS0 + 16 * half, r);
+        tmem_ld_wait();
+        if (valid) {
+          float4* dst = reinterpret_cast<float4*>(a.input_grad + smp * IN + 16 * half);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            __stcs(dst + q, make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
+                                        __uint_as_float(r[4 * q + 3])));
+        }
+      }
       tc_fence_before();
-      __syncthreads();  // S2 / tiles are reused by the next tile
-      continue;
+      g_started = true;
     }
-    fence_proxy_async();
-    tc_fence_before();
-    __syncthreads();
 
-    // ---- backward of the output layer: S0 = dY * W2p (input gradient of layer 3),  G2 += H2^T * dY (dW2^T)
-    if (tid == 0) {
+    if constexpr (TRAIN) {
+      // ---- weight gradients out of TMEM.  An M = 64 accumulator keeps row i in lane (i/16)*32 + i%16 (tools/tc_probe.py),
+      // so lanes 0..15 of each warp hold rows 16*(warp%4) .. +15; warps w and w+4 split the columns.
+      if (g_started) mbar_wait(&bar_g, phase_g);
       tc_fence_after();
-      gemm_split(tb + tS0, make_idesc_bf16(128, HID, false, true), OUTP / 16, false, precise,
-                 [&](bool lo, int ks) { return desc16_k_major(sDY + (lo ? loDY : 0), OUTP, ks); },
-                 [&](bool lo, int ks) { return desc16_mn_major(sW2 + (lo ? loW2 : 0), HID, ks); });
-      tc_commit(&bar);
-      gemm_split(tb + tG2, make_idesc_bf16(64, OUTP, true, true), kTile / 16, g_started, precise,
-                 [&](bool lo, int ks) { return desc16_mn_major(sH2 + (lo ? loH : 0), HC, ks); },
-                 [&](bool lo, int ks) { return desc16_mn_major(sDY + (lo ? loDY : 0), OUTP, ks); });
-    }
-    mbar_wait(&bar, phase);
-    phase ^= 1;
-    tc_fence_after();
-    {
-      uint32_t r[2][16];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) tmem_ld16_nowait(tb + lane_base + tS0 + 32 * half + 16 * q, r[q]);
-      tmem_ld_wait();
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        float v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i)  // src/mlp.cpp:197: a clamped unit passes no gradient
-          v[i] = ((m2 >> (16 * q + i)) & 1u) ? __uint_as_float(r[q][i]) : 0.0f;
-        store_chunk(smem + kDH2, smem + kDH2 + loDH, t, 4 * half + 2 * q, HID, v);
-        store_chunk(smem + kDH2, smem + kDH2 + loDH, t, 4 * half + 2 * q + 1, HID, v + 8);
+      const int lane = tid & 31;
+      const int row = 16 * (warp & 3) + lane;  // output unit o (G0, G1) or hidden unit i (G2)
+      double* gW0 = a.mlp_grad;
+      double* gb0 = gW0 + HID * IN;
+      double* gW1 = gb0 + HID;
+      double* gb1 = gW1 + HID * HID;
+      double* gW2 = gb1 + HID;
+      if (g_started) {
+        for (int c0 = 8 * half; c0 < X0C; c0 += 8 * kSplit) {  // G0: 40 columns = dW0[row][0..31], db0[row] at column 32
+          uint32_t r[16];
+          tmem_ld16_nowait(tb + lane_base + tG0 + (c0 < 32 ? c0 : 24), r);  // the last read re-covers cols 24..39
+          tmem_ld_wait();
+          if (lane < 16) {
+            if (c0 < 32) {
+              for (int i = 0; i < 8; ++i) atomicAdd(gW0 + row * IN + c0 + i, static_cast<double>(__uint_as_float(r[i])));
+            } else {
+              atomicAdd(gb0 + row, static_cast<double>(__uint_as_float(r[8])));
+            }
+          }
+        }
+        for (int c0 = 8 * half; c0 < HC; c0 += 8 * kSplit) {  // G1: 72 columns = dW1[row][0..63], db1[row] at column 64
+          uint32_t r[16];
+          tmem_ld16_nowait(tb + lane_base + tG1 + (c0 < 64 ? c0 : 56), r);
+          tmem_ld_wait();
+          if (lane < 16) {
+            if (c0 < 64) {
+              for (int i = 0; i < 8; ++i) atomicAdd(gW1 + row * HID + c0 + i, static_cast<double>(__uint_as_float(r[i])));
+            } else {
+              atomicAdd(gb1 + row, static_cast<double>(__uint_as_float(r[8])));
+            }
+          }
+        }
+        if (half == 1) {  // G2: dW2^T[i = row][o]
+          uint32_t r[16];
+          tmem_ld16_nowait(tb + lane_base + tG2, r);
+          tmem_ld_wait();
+          if (lane < 16)
+            for (int o = 0; o < a.out_w; ++o) atomicAdd(gW2 + o * HID + row, static_cast<double>(__uint_as_float(r[o])));
+        }
       }
-    }
-    fence_proxy_async();
-    tc_fence_before();
-    __syncthreads();
-
-    // ---- backward of layer 2: S1 = dH2 * W1,  G1 += dH2^T * [H1 | 1]
-    if (tid == 0) {
-      tc_fence_after();
-      gemm_split(tb + tS1, make_idesc_bf16(128, HID, false, true), HID / 16, false, precise,
-                 [&](bool lo, int ks) { return desc16_k_major(sDH2 + (lo ? loDH : 0), HID, ks); },
-                 [&](bool lo, int ks) { return desc16_mn_major(sW1 + (lo ? loW1 : 0), HID, ks); });
-      tc_commit(&bar);
-      gemm_split(tb + tG1, make_idesc_bf16(64, HC, true, true), kTile / 16, g_started, precise,
-                 [&](bool lo, int ks) { return desc16_mn_major(sDH2 + (lo ? loDH : 0), HID, ks); },
-                 [&](bool lo, int ks) { return desc16_mn_major(sH1 + (lo ? loH : 0), HC, ks); });
-    }
-    mbar_wait(&bar, phase);
-    phase ^= 1;
-    tc_fence_after();
-    {
-      uint32_t r[2][16];
+      // loss and output-bias gradient: per-thread fp64 partials -> warp shuffle -> one atomic per CTA (below)
+      double part[4] = {loss_acc, db2_acc[0], db2_acc[1], db2_acc[2]};
 #pragma unroll
-      for (int q = 0; q < 2; ++q) tmem_ld16_nowait(tb + lane_base + tS1 + 32 * half + 16 * q, r[q]);
-      tmem_ld_wait();
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        float v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = ((m1 >> (16 * q + i)) & 1u) ? __uint_as_float(r[q][i]) : 0.0f;
-        store_chunk(smem + kDH1, smem + kDH1 + loDH, t, 4 * half + 2 * q, HID, v);
-        store_chunk(smem + kDH1, smem + kDH1 + loDH, t, 4 * half + 2 * q + 1, HID, v + 8);
-      }
+      for (int k = 0; k < 4; ++k)
+        for (int o = 16; o > 0; o >>= 1) part[k] += __shfl_down_sync(0xffffffffu, part[k], o);
+      if (lane == 0)
+        for (int k = 0; k < 4; ++k) red_buf[warp][k] = part[k];
     }
-    fence_proxy_async();
-    tc_fence_before();
-    __syncthreads();
-
-    // ---- backward of layer 1: S2 = dH1 * W0 (d loss / d encoding),  G0 += dH1^T * [X0 | 1]
-    if (tid == 0) {
-      tc_fence_after();
-      gemm_split(tb + tS2, make_idesc_bf16(128, IN, false, true), HID / 16, false, precise,
-                 [&](bool lo, int ks) { return desc16_k_major(sDH1 + (lo ? loDH : 0), HID, ks); },
-                 [&](bool lo, int ks) { return desc16_mn_major(sW0 + (lo ? loW0 : 0), IN, ks); });
-      tc_commit(&bar);
-      gemm_split(tb + tG0, make_idesc_bf16(64, X0C, true, true), kTile / 16, g_started, precise,
-                 [&](bool lo, int ks) { return desc16_mn_major(sDH1 + (lo ? loDH : 0), HID, ks); },
-                 [&](bool lo, int ks) { return desc16_mn_major(sX0 + (lo ? loX0 : 0), X0C, ks); });
-      tc_commit(&bar_g);  // covers G2, G1 and G0 of this tile
-    }
-    g_started = true;
-    mbar_wait(&bar, phase);
-    phase ^= 1;
-    tc_fence_after();
-    {
-      uint32_t r[16];
-      tmem_ld16_nowait(tb + lane_base + tS2 + 16 * half, r);
-      tmem_ld_wait();
-      if (valid) {
-        float4* dst = reinterpret_cast<float4*>(a.input_grad + smp * IN + 16 * half);
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          __stcs(dst + q, make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
-                                      __uint_as_float(r[4 * q + 3])));
-      }
-    }
-    tc_fence_before();
-    __syncthreads();  // S2 is rewritten by the next tile (X0 waits for bar_g in stage 0)
   }
 
+  tc_fence_before();
+  __syncthreads();
   if constexpr (TRAIN) {
-    // ---- weight gradients out of TMEM.  An M = 64 accumulator keeps row i in lane (i/16)*32 + i%16 (tools/tc_probe.py),
-    // so lanes 0..15 of each warp hold rows 16*warp .. 16*warp+15.
-    if (g_started) mbar_wait(&bar_g, phase_g);
-    tc_fence_after();
-    const int lane = tid & 31;
-    const int row = 16 * (warp & 3) + lane;  // output unit o (G0, G1) or hidden unit i (G2)
-    double* gW0 = a.mlp_grad;
-    double* gb0 = gW0 + HID * IN;
-    double* gW1 = gb0 + HID;
-    double* gb1 = gW1 + HID * HID;
-    double* gW2 = gb1 + HID;
-    double* gb2 = gW2 + a.out_w * HID;
-    if (g_started) {
-      for (int c0 = 8 * half; c0 < X0C; c0 += 16) {  // G0: 40 columns = dW0[row][0..31], db0[row] at column 32
-        uint32_t r[16];
-        tmem_ld16_nowait(tb + lane_base + tG0 + (c0 < 32 ? c0 : 24), r);  // last read re-covers cols 24..39
-        tmem_ld_wait();
-        if (lane < 16) {
-          if (c0 < 32) {
-            for (int i = 0; i < 8; ++i) atomicAdd(gW0 + row * IN + c0 + i, static_cast<double>(__uint_as_float(r[i])));
-          } else {
-            atomicAdd(gb0 + row, static_cast<double>(__uint_as_float(r[8])));
-          }
-        }
-      }
-      for (int c0 = 8 * half; c0 < HC; c0 += 16) {  // G1: 72 columns = dW1[row][0..63], db1[row] at column 64
-        uint32_t r[16];
-        tmem_ld16_nowait(tb + lane_base + tG1 + (c0 < 64 ? c0 : 56), r);
-        tmem_ld_wait();
-        if (lane < 16) {
-          if (c0 < 64) {
-            for (int i = 0; i < 8; ++i) atomicAdd(gW1 + row * HID + c0 + i, static_cast<double>(__uint_as_float(r[i])));
-          } else {
-            atomicAdd(gb1 + row, static_cast<double>(__uint_as_float(r[8])));
-          }
-        }
-      }
-      if (half == 1) {  // G2: dW2^T[i = row][o]
-        uint32_t r[16];
-        tmem_ld16_nowait(tb + lane_base + tG2, r);
-        tmem_ld_wait();
-        if (lane < 16)
-          for (int o = 0; o < a.out_w; ++o) atomicAdd(gW2 + o * HID + row, static_cast<double>(__uint_as_float(r[o])));
-      }
-    }
-    // loss and output-bias gradient: per-thread fp64 partials -> warp shuffle -> one atomic per CTA
-    double part[4] = {loss_acc, db2_acc[0], db2_acc[1], db2_acc[2]};
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      for (int o = 16; o > 0; o >>= 1) part[k] += __shfl_down_sync(0xffffffffu, part[k], o);
-    if (lane == 0)
-      for (int k = 0; k < 4; ++k) red_buf[warp][k] = part[k];
-    __syncthreads();
     if (tid == 0) {
       double tot[4] = {0, 0, 0, 0};
-      for (int w = 0; w < 8; ++w)
+      for (int w = 0; w < kEpiThreads / 32; ++w)
         for (int k = 0; k < 4; ++k) tot[k] += red_buf[w][k];
+      double* gb2 = a.mlp_grad + HID * IN + HID + HID * HID + HID + a.out_w * HID;
       atomicAdd(a.loss_sum, tot[0]);
       for (int o = 0; o < a.out_w && o < 3; ++o) atomicAdd(gb2 + o, tot[1 + o]);
     }
   }
-  tc_fence_before();
-  __syncthreads();
   if (warp == 0) tmem_dealloc(tb, kTmemCols);
 }
 
@@ -545,10 +549,10 @@ sxen_status sxen_mlp_tc_run(bool train, const float* params, const float* featur
   const unsigned grid = static_cast<unsigned>(std::min<unsigned long long>(tiles, static_cast<unsigned long long>(sms)));
   if (train) {
     SXEN_CUDA(cudaFuncSetAttribute(mlp_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)));
-    mlp_tc_kernel<true><<<grid, kThreads, kSmemBytes, stream>>>(a);
+    mlp_tc_kernel<true><<<grid, kThreadsAll, kSmemBytes, stream>>>(a);
   } else {
     SXEN_CUDA(cudaFuncSetAttribute(mlp_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)));
-    mlp_tc_kernel<false><<<grid, kThreads, kSmemBytes, stream>>>(a);
+    mlp_tc_kernel<false><<<grid, kThreadsAll, kSmemBytes, stream>>>(a);
   }
   SXEN_CUDA(cudaGetLastError());
   count_launch();

@@ -227,6 +227,7 @@ sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, c
   const bool big = table_bytes >= (192ull << 20);
   a.level_major = enc->tuning.level_major < 0 ? (big ? 1 : 0) : (enc->tuning.level_major ? 1 : 0);
   a.merge_pairs = (enc->tuning.merge_pairs > 0 && enc->cfg.table_size >= 2) ? 1 : 0;
+  a.cache_hints = enc->tuning.reserved[0];
   EncodeLaunch ln{};
   ln.features = enc->cfg.features;
   ln.lpt = enc->tuning.levels_per_thread;

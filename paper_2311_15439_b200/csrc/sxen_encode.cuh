@@ -36,6 +36,7 @@ struct EncodeArgs {
   int32_t vec;                   // proven float alignment of every thread's out/upstream chunk: 4, 2 or 1
   uint32_t agg_mask;             // bit l: warp-aggregate the backward atomics of local level l
   int32_t merge_pairs;           // F == 2: one red.v4 for two chain vertices in the same 16-byte slot
+  int32_t cache_hints;           // F == 2: gather L2 policy + 4 * red L2 policy (0 none, 1 evict_last, 2 evict_first, 3 evict_unchanged)
   double skew;                   // F_n
   LevelGeom geom;
 };
@@ -136,6 +137,8 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
 
   float upv[K];
   float outv[K];
+  const int gather_kind = a.cache_hints & 3, red_kind = (a.cache_hints >> 2) & 3;
+  const uint64_t gather_pol = l2_policy(gather_kind), red_pol = l2_policy(red_kind);
   if constexpr (kBwd) {
     if (full) {
       load_stream<K>(a.upstream + chunk, upv, a.vec);
@@ -163,8 +166,18 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
       if constexpr (kFwd) {
         const float* __restrict__ tab = a.tables + level_off;
         float e[ND + 1][F];
+        if constexpr (F == 2) {
+          if (gather_kind) {
 #pragma unroll
-        for (int k = 0; k <= ND; ++k) load_row<F>(tab + static_cast<size_t>(idx[k]) * F, e[k]);
+            for (int k = 0; k <= ND; ++k) load_row2_policy(tab + static_cast<size_t>(idx[k]) * F, e[k], gather_pol);
+          } else {
+#pragma unroll
+            for (int k = 0; k <= ND; ++k) load_row<F>(tab + static_cast<size_t>(idx[k]) * F, e[k]);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k <= ND; ++k) load_row<F>(tab + static_cast<size_t>(idx[k]) * F, e[k]);
+        }
         if constexpr (EXACT) {
           // src/encoding.cpp:305-313: acc starts at 0.0, acc += w_i * entry in chain order, all in double.
           double acc[F];
@@ -219,8 +232,12 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
                 const int kn = k < ND ? k + 1 : k;
                 const bool low = (idx[k] & 1u) == 0u;
                 float* p = gl + static_cast<size_t>(idx[k] & ~1u) * 2;
-                red_add4(p, low ? v[k][0] : v[kn][0], low ? v[k][1] : v[kn][1], low ? v[kn][0] : v[k][0],
-                         low ? v[kn][1] : v[k][1]);
+                if (red_kind)
+                  red_add4_policy(p, low ? v[k][0] : v[kn][0], low ? v[k][1] : v[kn][1], low ? v[kn][0] : v[k][0],
+                                  low ? v[kn][1] : v[k][1], red_pol);
+                else
+                  red_add4(p, low ? v[k][0] : v[kn][0], low ? v[k][1] : v[kn][1], low ? v[kn][0] : v[k][0],
+                           low ? v[kn][1] : v[k][1]);
                 skip = true;
                 continue;
               }
@@ -230,6 +247,12 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
           if (agg) {
             const unsigned long long key = (static_cast<unsigned long long>(l) << 32) | idx[k];
             issue = warp_merge_rows<F>(aggm, key, v[k]);
+          }
+          if constexpr (F == 2) {
+            if (issue && red_kind) {
+              red_add2_policy(gl + static_cast<size_t>(idx[k]) * F, v[k][0], v[k][1], red_pol);
+              issue = false;
+            }
           }
           if (issue) red_row<F>(gl + static_cast<size_t>(idx[k]) * F, v[k]);
         }

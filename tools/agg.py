@@ -1,0 +1,45 @@
+#!/usr/bin/env python
+"""tools/agg.py -- warp aggregation threshold (sxen_tuning.warp_aggregate = max lattice vertices of an aggregated level)
+on the bwd / fused launches, sample- and level-major."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2311_15439_b200 as sx  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+log2t = int(sys.argv[2]) if len(sys.argv) > 2 else 19
+N = 1 << 20
+growth = 2.0 if n == 2 else 1.5
+cfg = sx.EncoderConfig(dim=n, levels=16, table_size=1 << log2t, features=2, base_resolution=16, growth=growth)
+enc = sx.HashEncoder(cfg)
+enc.init_tables(42)
+grad = sx.EncoderGradient(enc)
+xs, ups, outs = [], [], []
+for i in range(4):
+    x = torch.empty((N, n), dtype=torch.float32, device="cuda")
+    r = sx.CounterRng(99, 1); r.counter = i * N * n; r.fill_device(x)
+    up = torch.empty((N, 32), dtype=torch.float32, device="cuda")
+    r = sx.CounterRng(7, 2); r.counter = i * N * 32; r.fill_device(up, -1e-3, 1e-3)
+    xs.append(x); ups.append(up); outs.append(torch.empty((N, 32), dtype=torch.float32, device="cuda"))
+print(f"# n={n} T=2^{log2t}\nlm lpt agg_verts  bwd_us  fused_us")
+for lm, lpt in ((0, 2), (1, 4), (1, 2), (1, 1)):
+    for agg in (0, 300, 1100, 5000, 17000, 70000, 300000):
+        enc.set_tuning(sx.Tuning(levels_per_thread=lpt, level_major=lm, warp_aggregate=agg))
+        res_t = []
+        for which in ("bwd", "fused"):
+            fn = {"bwd": lambda i: enc.encode_backward(xs[i % 4], ups[i % 4], grad),
+                  "fused": lambda i: enc.encode_forward_backward(xs[i % 4], ups[i % 4], grad, out=outs[i % 4])}[which]
+            for i in range(4):
+                fn(i)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for i in range(12):
+                fn(i)
+            b.record()
+            torch.cuda.synchronize()
+            res_t.append(a.elapsed_time(b) / 12 * 1e3)
+        print(f"{lm:2d} {lpt:3d} {agg:8d} {res_t[0]:7.1f} {res_t[1]:7.1f}", flush=True)

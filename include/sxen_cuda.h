@@ -101,7 +101,12 @@ typedef struct sxen_tuning {
                                 lattice has at most this many vertices (0 = off) */
   int32_t merge_pairs;       /* backward, F == 2: chain vertices whose rows share a 16-byte slot (idx, idx^1) take one
                                 red.v4 instead of two red.v2.  1 = on (default), -1 = off, 0 = library default */
-  int32_t reserved[2];
+  int32_t cache_hints;       /* F == 2 kernels: L2 eviction policy of the table gathers + 4 * policy of the gradient reds
+                                (0 none, 1 evict_last, 2 evict_first, 3 evict_unchanged).  -1 = chosen from the
+                                footprint; 0 = plain accesses */
+  int32_t coarse_replicas;   /* backward: levels with at most 2^16 lattice vertices accumulate into replicated dense
+                                arrays that the same call folds into the hashed rows (relieves the per-address
+                                serialisation of the L2 atomic unit).  0 = on (default), -1 = off */
 } sxen_tuning;
 
 typedef struct sxen_encoder sxen_encoder;   /* sxen::HashEncoder     (include/sxen/encoding.hpp:92-148) */

@@ -39,7 +39,7 @@ class LookupCountersC(C.Structure):
 class TuningC(C.Structure):
     _fields_ = [("levels_per_thread", C.c_int32), ("block_threads", C.c_int32), ("level_major", C.c_int32),
                 ("exact_blend", C.c_int32), ("warp_aggregate", C.c_int32), ("merge_pairs", C.c_int32),
-                ("reserved", C.c_int32 * 2)]
+                ("cache_hints", C.c_int32), ("coarse_replicas", C.c_int32)]
 
 
 _P = C.POINTER

@@ -88,6 +88,8 @@ sxen_tuning default_tuning() {
   t.exact_blend = 1;
   t.warp_aggregate = 0;
   t.merge_pairs = 1;
+  t.cache_hints = -1;  // auto
+  t.coarse_replicas = 0;
   return t;
 }
 
@@ -152,6 +154,10 @@ typedef cudaError_t (*debug_fn)(EncodeArgs&, int, uint32_t*, double*, int, cudaS
 const encode_fn kEncode[8] = {sxen_dev::launch_encode_nd1, sxen_dev::launch_encode_nd2, sxen_dev::launch_encode_nd3,
                               sxen_dev::launch_encode_nd4, sxen_dev::launch_encode_nd5, sxen_dev::launch_encode_nd6,
                               sxen_dev::launch_encode_nd7, sxen_dev::launch_encode_nd8};
+typedef cudaError_t (*fold_fn)(const EncodeArgs&, cudaStream_t);
+const fold_fn kFold[8] = {sxen_dev::launch_fold_nd1, sxen_dev::launch_fold_nd2, sxen_dev::launch_fold_nd3,
+                          sxen_dev::launch_fold_nd4, sxen_dev::launch_fold_nd5, sxen_dev::launch_fold_nd6,
+                          sxen_dev::launch_fold_nd7, sxen_dev::launch_fold_nd8};
 const debug_fn kDebug[8] = {sxen_dev::launch_debug_nd1, sxen_dev::launch_debug_nd2, sxen_dev::launch_debug_nd3,
                             sxen_dev::launch_debug_nd4, sxen_dev::launch_debug_nd5, sxen_dev::launch_debug_nd6,
                             sxen_dev::launch_debug_nd7, sxen_dev::launch_debug_nd8};
@@ -176,18 +182,31 @@ void base_args(const sxen_encoder* enc, const void* x, sxen_coord_type type, siz
   a.skew = enc->skew;
 }
 
-void level_chunk(const sxen_encoder* enc, int level0, EncodeArgs& a) {
+void level_chunk(const sxen_encoder* enc, const sxen_grad* grad, int level0, EncodeArgs& a) {
   a.level0 = level0;
   a.n_levels = std::min<int>(sxen_dev::kMaxLaunchLevels, enc->cfg.levels - level0);
   a.agg_mask = 0;
+  // the replicas are laid out for the lattice of the encoder the accumulator was created from
+  const bool replicas = grad != nullptr && grad->coarse != nullptr && enc->tuning.coarse_replicas >= 0 &&
+                        enc->cfg.backend == SXEN_BACKEND_SIMPLEX && grad->dim == enc->cfg.dim && grad->res == enc->res;
+  a.coarse = replicas ? grad->coarse : nullptr;
   for (int l = 0; l < sxen_dev::kMaxLaunchLevels; ++l) {
     const bool live = l < a.n_levels;
+    a.cg.shift[l] = -1;
+    a.cg.offset[l] = a.cg.verts[l] = 0;
+    if (live && replicas) {
+      const size_t gl = static_cast<size_t>(level0 + l);
+      a.cg.shift[l] = grad->coarse_shift[gl];
+      a.cg.offset[l] = grad->coarse_offset[gl];
+      a.cg.verts[l] = grad->coarse_verts[gl];
+    }
     const uint32_t res = live ? enc->res[static_cast<size_t>(level0 + l)] : 1u;
     // simplex: s = N_l / S_n (src/encoding.cpp:200); grid: y = x * N_l (src/encoding.cpp:255)
     a.geom.scale[l] = enc->cfg.backend == SXEN_BACKEND_SIMPLEX ? static_cast<double>(res) / enc->scale
                                                                : static_cast<double>(res);
     a.geom.res[l] = static_cast<int32_t>(res);
-    if (live && enc->tuning.warp_aggregate > 0) {
+    // a replicated level never takes the warp-merge path (its lanes leave the level body early)
+    if (live && enc->tuning.warp_aggregate > 0 && a.cg.shift[l] < 0) {
       const double verts = std::pow(static_cast<double>(res) + 1.0, enc->cfg.dim);
       if (verts <= static_cast<double>(enc->tuning.warp_aggregate)) a.agg_mask |= 1u << l;
     }
@@ -227,7 +246,12 @@ sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, c
   const bool big = table_bytes >= (192ull << 20);
   a.level_major = enc->tuning.level_major < 0 ? (big ? 1 : 0) : (enc->tuning.level_major ? 1 : 0);
   a.merge_pairs = (enc->tuning.merge_pairs > 0 && enc->cfg.table_size >= 2) ? 1 : 0;
-  a.cache_hints = enc->tuning.reserved[0];
+  // L2 eviction policies (profiles/r1_cache_hints.log).  Tables + gradients within reach of L2: the fused launch marks
+  // its gradient lines evict_first so the table lines (cached on both dies) survive; beyond L2: gathers and reds both
+  // evict_last, which keeps the hot coarse-level rows resident against the streaming fine levels.
+  a.cache_hints = enc->tuning.cache_hints >= 0 ? enc->tuning.cache_hints
+                  : big ? ((mode & sxen_dev::kModeFwd ? 1 : 0) | (mode & sxen_dev::kModeBwd ? 4 : 0))
+                        : (mode == sxen_dev::kModeBoth ? 8 : 0);
   EncodeLaunch ln{};
   ln.features = enc->cfg.features;
   ln.lpt = enc->tuning.levels_per_thread;
@@ -236,13 +260,21 @@ sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, c
   ln.grid_backend = enc->cfg.backend == SXEN_BACKEND_GRID ? 1 : 0;
   ln.block_threads = enc->tuning.block_threads;
   for (int level0 = 0; level0 < enc->cfg.levels; level0 += sxen_dev::kMaxLaunchLevels) {
-    level_chunk(enc, level0, a);
+    level_chunk(enc, (mode & sxen_dev::kModeBwd) ? grad : nullptr, level0, a);
     a.vec = 4;
     if (mode & sxen_dev::kModeFwd) a.vec = std::min(a.vec, ptr_vec(out));
     if (mode & sxen_dev::kModeBwd) a.vec = std::min(a.vec, ptr_vec(upstream));
     int used = 0;
     SXEN_CUDA(kEncode[enc->cfg.dim - 1](ln, a, stream, &used));
     count_launch();
+    if (a.coarse != nullptr) {
+      bool any = false;
+      for (int l = 0; l < a.n_levels; ++l) any = any || a.cg.shift[l] >= 0;
+      if (any) {
+        SXEN_CUDA(kFold[enc->cfg.dim - 1](a, stream));
+        count_launch();
+      }
+    }
   }
   enc->touched += static_cast<uint64_t>(n) * static_cast<uint64_t>(enc->cfg.levels) *
                   static_cast<uint64_t>(enc->vertices()) * ((mode == sxen_dev::kModeBoth) ? 2u : 1u);
@@ -467,6 +499,7 @@ sxen_status sxen_encoder_set_tuning(sxen_encoder* enc, const sxen_tuning* t) {
   SXEN_REQUIRE(n.block_threads % 32 == 0 && n.block_threads <= 1024, "block_threads must be a multiple of 32, <= 1024");
   SXEN_REQUIRE(n.warp_aggregate >= 0, "warp_aggregate must be >= 0");
   if (n.merge_pairs == 0) n.merge_pairs = d.merge_pairs;
+  SXEN_REQUIRE(n.cache_hints >= -1 && n.cache_hints <= 15, "cache_hints must be -1 (auto) or in [0, 15]");
   enc->tuning = n;
   return SXEN_OK;
 }
@@ -538,7 +571,7 @@ sxen_status sxen_encoder_encode_debug(sxen_encoder* enc, const void* x_dev, sxen
   EncodeArgs a;
   base_args(enc, x_dev, type, n_samples, a);
   for (int level0 = 0; level0 < enc->cfg.levels; level0 += sxen_dev::kMaxLaunchLevels) {
-    level_chunk(enc, level0, a);
+    level_chunk(enc, nullptr, level0, a);
     SXEN_CUDA(kDebug[enc->cfg.dim - 1](a, enc->cfg.backend == SXEN_BACKEND_GRID ? 1 : 0, idx_dev, w_dev,
                                        enc->cfg.levels, as_stream(stream)));
     count_launch();
@@ -698,6 +731,37 @@ sxen_status sxen_grad_create(const sxen_encoder* enc, sxen_grad** out) {
     delete g;
     return cuda_fail(err, "sxen_grad_create allocation");
   }
+  // Replicated dense accumulators for the coarse simplex levels: a level with V = (res+1)^dim lattice vertices gets
+  // R = 2^floor(log2(2^17 / V)) replicas, capped at 64, when R >= 2 (at most 2^17 rows = 1 MiB per level at F = 2).
+  g->dim = enc->cfg.dim;
+  g->res = enc->res;
+  g->coarse_offset.assign(static_cast<size_t>(g->levels), 0u);
+  g->coarse_verts.assign(static_cast<size_t>(g->levels), 0u);
+  g->coarse_shift.assign(static_cast<size_t>(g->levels), -1);
+  if (enc->cfg.backend == SXEN_BACKEND_SIMPLEX) {
+    for (int l = 0; l < g->levels; ++l) {
+      const double verts = std::pow(static_cast<double>(enc->res[static_cast<size_t>(l)]) + 1.0, enc->cfg.dim);
+      if (verts > static_cast<double>(1u << 16)) continue;
+      int shift = 0;
+      while (shift < 6 && verts * static_cast<double>(2u << shift) <= static_cast<double>(1u << 17)) ++shift;
+      if (shift < 1) continue;
+      g->coarse_shift[static_cast<size_t>(l)] = shift;
+      g->coarse_verts[static_cast<size_t>(l)] = static_cast<uint32_t>(verts);
+      g->coarse_offset[static_cast<size_t>(l)] = static_cast<uint32_t>(g->coarse_floats);
+      g->coarse_floats += (static_cast<size_t>(verts) << shift) * static_cast<size_t>(g->features);
+    }
+  }
+  if (g->coarse_floats) {
+    err = cudaMalloc(&g->coarse, g->coarse_floats * sizeof(float));
+    if (err != cudaSuccess) {
+      cudaFree(g->values);
+      delete g;
+      return cuda_fail(err, "sxen_grad_create allocation");
+    }
+    fill_u32_kernel<<<grid_for(g->coarse_floats), 256>>>(reinterpret_cast<uint32_t*>(g->coarse), g->coarse_floats,
+                                                        kUntouchedBits);
+    count_launch();
+  }
   *out = g;
   const sxen_status st = sxen_grad_clear(g, nullptr);
   if (st == SXEN_OK) {
@@ -710,6 +774,7 @@ sxen_status sxen_grad_destroy(sxen_grad* grad) {
   if (!grad) return SXEN_OK;
   DeviceGuard guard(grad->device);
   cudaFree(grad->values);
+  cudaFree(grad->coarse);
   delete grad;
   return SXEN_OK;
 }

@@ -74,6 +74,14 @@ struct sxen_grad {
   int levels = 0, features = 0;
   uint32_t table_size = 0;
   float* values = nullptr;  // L x T x F, untouched rows carry -0.0f in feature 0
+  // Coarse simplex levels (few lattice vertices, every sample's atomics land on them) accumulate into 2^shift dense
+  // replicas [replica][vertex][F] that the backward launch folds into `values` before it returns (sxen_encode.cuh).
+  float* coarse = nullptr;
+  size_t coarse_floats = 0;
+  std::vector<uint32_t> coarse_offset, coarse_verts;  // per level
+  std::vector<int32_t> coarse_shift;                  // per level, -1 = none
+  int dim = 0;
+  std::vector<uint32_t> res;                          // lattice the replicas were laid out for
   size_t count() const { return static_cast<size_t>(levels) * table_size * static_cast<size_t>(features); }
 };
 

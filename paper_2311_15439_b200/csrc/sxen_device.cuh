@@ -46,12 +46,22 @@ struct LevelGeom {
   int32_t res[kMaxLaunchLevels];   // res_l (src/encoding.cpp:198)
 };
 
+// Replicated accumulators of the coarse levels of one launch (backward only; sxen_encode.cuh).
+struct CoarseGeom {
+  uint32_t offset[kMaxLaunchLevels];  // float offset of the level's first replica inside the coarse buffer
+  uint32_t verts[kMaxLaunchLevels];   // (res_l + 1)^dim lattice vertices
+  int32_t shift[kMaxLaunchLevels];    // log2(replicas), -1 = the level accumulates straight into its hashed rows
+};
+
 // One (sample, level) simplex lookup: gather_simplex, src/encoding.cpp:196-242.
 //   x        coordinates already clamped with min(x, nextafter(1,0))   (:201-204)
 //   returns  idx[k], w[k] for the vertex chain k = 0..ND, and whether the cell was clamped (:211-218)
-template <int ND>
+//   dense    (DENSE only) vertex k's position in the level's dense lattice, sum_i c_i * (res+1)^i: the address of the
+//            replicated coarse-level accumulators (sxen_encode.cuh); not part of the reference
+template <int ND, bool DENSE = false>
 __device__ __forceinline__ bool simplex_lookup(const double (&x)[ND], double scale, double skew, int res,
-                                               uint32_t mask, uint32_t (&idx)[ND + 1], double (&w)[ND + 1]) {
+                                               uint32_t mask, uint32_t (&idx)[ND + 1], double (&w)[ND + 1],
+                                               uint32_t* dense = nullptr) {
   double y[ND];
 #pragma unroll
   for (int i = 0; i < ND; ++i) y[i] = __dmul_rn(x[i], scale);
@@ -66,6 +76,8 @@ __device__ __forceinline__ bool simplex_lookup(const double (&x)[ND], double sca
   uint32_t term[ND];   // axis_term(i, base_i)        src/encoding.cpp:17-20
   uint32_t delta[ND];  // term(base_i) ^ term(base_i+1): the XOR applied when the chain steps along axis i (:231-238)
   uint32_t h = 0;
+  uint32_t d0 = 0, stride = 1;
+  uint32_t dstep[ND];
 #pragma unroll
   for (int i = 0; i < ND; ++i) {
     const double yi = __dadd_rn(y[i], shift);
@@ -81,6 +93,11 @@ __device__ __forceinline__ bool simplex_lookup(const double (&x)[ND], double sca
     term[i] = static_cast<uint32_t>(b) * p;
     delta[i] = term[i] ^ (static_cast<uint32_t>(b + 1) * p);
     h ^= term[i];
+    if constexpr (DENSE) {
+      d0 += static_cast<uint32_t>(b) * stride;
+      dstep[i] = stride;
+      stride *= static_cast<uint32_t>(res + 1);
+    }
   }
 
   // subdivide, src/lattice.cpp:72-103: stable descending insertion sort.  rank[i] = position of axis i in that
@@ -102,20 +119,26 @@ __device__ __forceinline__ bool simplex_lookup(const double (&x)[ND], double sca
   // (src/encoding.cpp:229-240): vertex k = base + sum of unit steps along the axes with rank < k.
   double prev = 0.0;
   idx[0] = h & mask;
+  if constexpr (DENSE) dense[0] = d0;
 #pragma unroll
   for (int k = 0; k < ND; ++k) {
     double sk = 0.0;
-    uint32_t dk = 0;
+    uint32_t dk = 0, ds = 0;
 #pragma unroll
     for (int i = 0; i < ND; ++i) {
       const bool hit = rank[i] == k;
       sk = hit ? fr[i] : sk;
       dk = hit ? delta[i] : dk;
+      if constexpr (DENSE) ds = hit ? dstep[i] : ds;
     }
     w[k] = (k == 0) ? __dsub_rn(1.0, sk) : __dsub_rn(prev, sk);
     prev = sk;
     h ^= dk;
     idx[k + 1] = h & mask;
+    if constexpr (DENSE) {
+      d0 += ds;
+      dense[k + 1] = d0;
+    }
   }
   w[ND] = prev;
   return oob;

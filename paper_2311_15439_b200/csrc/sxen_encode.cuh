@@ -38,7 +38,9 @@ struct EncodeArgs {
   int32_t merge_pairs;           // F == 2: one red.v4 for two chain vertices in the same 16-byte slot
   int32_t cache_hints;           // F == 2: gather L2 policy + 4 * red L2 policy (0 none, 1 evict_last, 2 evict_first, 3 evict_unchanged)
   double skew;                   // F_n
+  float* coarse;                 // replicated dense accumulators of the coarse levels (nullptr = none)
   LevelGeom geom;
+  CoarseGeom cg;
 };
 
 // Sum v[] over the lanes of `m` that hold the same key, leaving the total in the group's lowest lane.
@@ -90,9 +92,11 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
 
   __shared__ double s_scale[kMaxLaunchLevels];
   __shared__ int s_res[kMaxLaunchLevels];
+  __shared__ int s_cshift[kMaxLaunchLevels];
   if (threadIdx.x < kMaxLaunchLevels) {
     s_scale[threadIdx.x] = a.geom.scale[threadIdx.x];
     s_res[threadIdx.x] = a.geom.res[threadIdx.x];
+    s_cshift[threadIdx.x] = (kBwd && a.coarse != nullptr) ? a.cg.shift[threadIdx.x] : -1;
   }
   __syncthreads();
 
@@ -158,8 +162,9 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
     }
     if (has) {
       uint32_t idx[ND + 1];
+      uint32_t dense[ND + 1];
       double w[ND + 1];
-      const bool oob = simplex_lookup<ND>(x, s_scale[l], a.skew, s_res[l], a.mask, idx, w);
+      const bool oob = simplex_lookup<ND, kBwd>(x, s_scale[l], a.skew, s_res[l], a.mask, idx, w, dense);
       if (oob) atomicAdd(a.status + 1, 1ULL);
       const size_t level_off = static_cast<size_t>(a.level0 + l) * a.level_stride;
 
@@ -215,6 +220,18 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
           const float wk = static_cast<float>(w[k]);
 #pragma unroll
           for (int f = 0; f < F; ++f) v[k][f] = canon(__fmul_rn(wk, upv[j * F + f]));
+        }
+        // Coarse level: a few thousand hot rows take every sample's atomics and the L2 atomic unit serialises per
+        // address (profiles/r1_per_level_n*.log: level 0 costs 4-12x a fine level).  Such levels accumulate into one of
+        // 2^shift dense replicas picked by the sample index; coarse_fold_kernel adds the replicas into the
+        // hashed rows right after this launch.
+        const int cshift = s_cshift[l];
+        if (cshift >= 0) {
+          const uint32_t rep = static_cast<uint32_t>(s) & ((1u << cshift) - 1u);
+          float* __restrict__ cb = a.coarse + a.cg.offset[l] + static_cast<size_t>(rep) * a.cg.verts[l] * F;
+#pragma unroll
+          for (int k = 0; k <= ND; ++k) red_row<F>(cb + static_cast<size_t>(dense[k]) * F, v[k]);
+          continue;
         }
         bool skip = false;
 #pragma unroll
@@ -379,6 +396,46 @@ encode_debug_kernel(const __grid_constant__ EncodeArgs a, uint32_t* __restrict__
   }
 }
 
+// Adds the dense replicas of one launch's coarse levels into the hashed gradient rows and re-arms them with -0.0f.
+// One thread per (vertex, feature) of a level (blockIdx.y = local level).  Each replica slot is claimed with an atomic
+// exchange, so a backward kernel of another stream that is still adding loses nothing: whatever lands after the exchange
+// is carried by that stream's own fold.  A slot still holding -0.0f was not touched; the sum of touched slots can be
+// +0.0f but never -0.0f, and -0.0f + (+0.0f) = +0.0f marks the hashed row touched exactly as a direct add would.
+template <int ND>
+__global__ void __launch_bounds__(256) coarse_fold_kernel(const __grid_constant__ EncodeArgs a) {
+  const int l = blockIdx.y;
+  const int cshift = a.cg.shift[l];
+  if (l >= a.n_levels || cshift < 0) return;
+  const int F = a.features;
+  const uint32_t verts = a.cg.verts[l];
+  const unsigned long long e = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= static_cast<unsigned long long>(verts) * F) return;
+  const uint32_t v = static_cast<uint32_t>(e / F);
+  const int f = static_cast<int>(e - static_cast<unsigned long long>(v) * F);
+  float* cb = a.coarse + a.cg.offset[l];
+  float sum = 0.0f;
+  bool any = false;
+  for (uint32_t r = 0; r < (1u << cshift); ++r) {
+    float* p = cb + (static_cast<size_t>(r) * verts + v) * F + f;
+    if (__float_as_uint(__ldcg(p)) == 0x80000000u) continue;
+    const uint32_t old = atomicExch(reinterpret_cast<unsigned int*>(p), 0x80000000u);
+    if (old == 0x80000000u) continue;
+    sum += __uint_as_float(old);
+    any = true;
+  }
+  if (!any) return;
+  const uint32_t side = static_cast<uint32_t>(a.geom.res[l]) + 1u;
+  uint32_t rest = v, h = 0;
+#pragma unroll
+  for (int i = 0; i < ND; ++i) {
+    const uint32_t c = rest % side;
+    rest /= side;
+    h ^= c * prime_of(i);
+  }
+  const size_t level_off = static_cast<size_t>(a.level0 + l) * a.level_stride;
+  red_add(a.grads + level_off + static_cast<size_t>(h & a.mask) * F + f, sum);
+}
+
 // ---- host-side launch plumbing, one translation unit per ND (sxen_encode_nd.cu) -----------------------------
 
 struct EncodeLaunch {
@@ -399,6 +456,16 @@ cudaError_t launch_encode_nd5(const EncodeLaunch&, EncodeArgs&, cudaStream_t, in
 cudaError_t launch_encode_nd6(const EncodeLaunch&, EncodeArgs&, cudaStream_t, int* used_lpt);
 cudaError_t launch_encode_nd7(const EncodeLaunch&, EncodeArgs&, cudaStream_t, int* used_lpt);
 cudaError_t launch_encode_nd8(const EncodeLaunch&, EncodeArgs&, cudaStream_t, int* used_lpt);
+
+// coarse_fold_kernel over the levels of the launch `a` describes (no-op when none is replicated)
+cudaError_t launch_fold_nd1(const EncodeArgs&, cudaStream_t);
+cudaError_t launch_fold_nd2(const EncodeArgs&, cudaStream_t);
+cudaError_t launch_fold_nd3(const EncodeArgs&, cudaStream_t);
+cudaError_t launch_fold_nd4(const EncodeArgs&, cudaStream_t);
+cudaError_t launch_fold_nd5(const EncodeArgs&, cudaStream_t);
+cudaError_t launch_fold_nd6(const EncodeArgs&, cudaStream_t);
+cudaError_t launch_fold_nd7(const EncodeArgs&, cudaStream_t);
+cudaError_t launch_fold_nd8(const EncodeArgs&, cudaStream_t);
 
 cudaError_t launch_debug_nd1(EncodeArgs&, int grid_backend, uint32_t*, double*, int total_levels, cudaStream_t);
 cudaError_t launch_debug_nd2(EncodeArgs&, int grid_backend, uint32_t*, double*, int total_levels, cudaStream_t);

@@ -118,6 +118,17 @@ cudaError_t SXEN_CAT(launch_encode_nd, SXEN_ND)(const EncodeLaunch& ln, EncodeAr
   }
 }
 
+cudaError_t SXEN_CAT(launch_fold_nd, SXEN_ND)(const EncodeArgs& a, cudaStream_t stream) {
+  uint32_t most = 0;
+  for (int l = 0; l < a.n_levels; ++l)
+    if (a.cg.shift[l] >= 0) most = a.cg.verts[l] > most ? a.cg.verts[l] : most;
+  if (most == 0 || a.coarse == nullptr) return cudaSuccess;
+  const unsigned long long elems = static_cast<unsigned long long>(most) * static_cast<unsigned long long>(a.features);
+  const dim3 grid(static_cast<unsigned>((elems + 255) / 256), static_cast<unsigned>(a.n_levels), 1);
+  coarse_fold_kernel<ND><<<grid, 256, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t SXEN_CAT(launch_debug_nd, SXEN_ND)(EncodeArgs& a, int grid_backend, uint32_t* idx, double* w,
                                                int total_levels, cudaStream_t stream) {
   const int block = 256;

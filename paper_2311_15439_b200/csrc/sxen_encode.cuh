@@ -40,7 +40,7 @@ struct EncodeArgs {
   double skew;                   // F_n
   float* coarse;                 // replicated dense accumulators of the coarse levels (nullptr = none)
   LevelGeom geom;
-  CoarseGeom cg;
+  CoarseGeom cg;                 // geometry of `coarse`
 };
 
 // Sum v[] over the lanes of `m` that hold the same key, leaving the total in the group's lowest lane.
@@ -172,6 +172,9 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
         const float* __restrict__ tab = a.tables + level_off;
         float e[ND + 1][F];
         if constexpr (F == 2) {
+          // (a 128-bit load for the two rows of an axis-0 pair, or a dense L1-resident shadow of the coarse levels, buys
+          // nothing here: the gathers are bound by sector requests on the L1 miss path, and the pair's second row
+          // already hits the sector its first row fetched -- profiles/r1_coarse_shadow_tables_negative.log)
           if (gather_kind) {
 #pragma unroll
             for (int k = 0; k <= ND; ++k) load_row2_policy(tab + static_cast<size_t>(idx[k]) * F, e[k], gather_pol);

@@ -1,6 +1,6 @@
 #!/usr/bin/env python
-"""tools/replicas.py -- coarse-level replicated accumulators on/off (sxen_tuning.coarse_replicas) for the bwd / fused
-launches of the BASELINE ladders, sample-major LPT=2 and level-major LPT=4."""
+"""tools/replicas.py -- coarse-level side arrays on/off for the fwd / bwd / fused launches of the BASELINE ladders:
+replicated gradient accumulators (sxen_tuning.coarse_replicas) and pair-merged 16-byte gathers / reds (merge_pairs)."""
 import os
 import sys
 
@@ -23,10 +23,11 @@ for n, log2t in ((3, 19), (2, 19), (3, 22), (2, 22)):
         up = torch.empty((N, 32), dtype=torch.float32, device="cuda")
         r = sx.CounterRng(7, 2); r.counter = i * N * 32; r.fill_device(up, -1e-3, 1e-3)
         xs.append(x); ups.append(up); outs.append(torch.empty((N, 32), dtype=torch.float32, device="cuda"))
-    print(f"# n={n} T=2^{log2t}\nlm lpt replicas  fwd_us  bwd_us  fused_us  fwd+bwd_us")
+    print(f"# n={n} T=2^{log2t}\nlm lpt replicas  merge hints  fwd_us  bwd_us  fused_us  fwd+bwd_us")
     for lm, lpt in ((0, 2), (1, 4), (1, 2)):
-        for rep in (-1, 0):
-            enc.set_tuning(sx.Tuning(levels_per_thread=lpt, level_major=lm, coarse_replicas=rep))
+        for rep, tbl, hints in ((-1, -1, -1), (0, -1, -1), (0, 1, -1)):
+            enc.set_tuning(sx.Tuning(levels_per_thread=lpt, level_major=lm, coarse_replicas=rep, merge_pairs=tbl,
+                                     cache_hints=hints))
             res_t = []
             for which in ("fwd", "bwd", "fused"):
                 fn = {"fwd": lambda i: enc.encode(xs[i % 4], out=outs[i % 4]),
@@ -42,6 +43,6 @@ for n, log2t in ((3, 19), (2, 19), (3, 22), (2, 22)):
                 b.record()
                 torch.cuda.synchronize()
                 res_t.append(a.elapsed_time(b) / 20 * 1e3)
-            print(f"{lm:2d} {lpt:3d} {'on' if rep == 0 else 'off':>8s} {res_t[0]:7.1f} {res_t[1]:7.1f} {res_t[2]:7.1f} {res_t[0] + res_t[1]:9.1f}", flush=True)
+            print(f"{lm:2d} {lpt:3d} {'on' if rep == 0 else 'off':>8s} {'on' if tbl == 1 else 'off':>6s} {hints:5d} {res_t[0]:7.1f} {res_t[1]:7.1f} {res_t[2]:7.1f} {res_t[0] + res_t[1]:9.1f}", flush=True)
     del enc, grad, xs, ups, outs
     torch.cuda.empty_cache()

@@ -204,7 +204,7 @@ def run_ours(args):
         raise SystemExit("bench.py: no sm_100 CUDA device -- the GPU arm has no CPU fallback")
     torch.cuda.set_device(local_rank)
     dist = None
-    if world > 1:
+    if world > 1 or "WORLD_SIZE" in os.environ:  # under torchrun a single rank still drives the NCCL path
         import torch.distributed as dist_mod
         dist = dist_mod
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -280,7 +280,36 @@ def run_ours(args):
         enc.set_tuning(sx.Tuning(levels_per_thread=lpt, block_threads=args.block, level_major=lm, exact_blend=args.exact,
                                  warp_aggregate=args.aggregate))
 
+    exchange = dist is not None and not args.no_allreduce
+    ranges = sx.level_ranges(L, args.level_chunks if exchange else 1)
+    per_level = gview.numel() // L
+    comm = torch.cuda.Stream(device=dev) if exchange else None
+
+    def step_overlapped(i, ev=None):
+        """Batch-sharded step: the levels are walked in chunks and each chunk's slice of the table-gradient accumulator is
+        all-reduced on a second stream while the next chunk computes."""
+        k = i % n_sets
+        if args.path != "fused":
+            enc.encode(xs[k], out=outs[k])
+            if ev is not None:
+                ev[0].record(stream)
+        for first, count in ranges:
+            if args.path == "fused":
+                enc.encode_forward_backward(xs[k], ups[k], grad, out=outs[k], levels=(first, count))
+            else:
+                enc.encode_backward(xs[k], ups[k], grad, levels=(first, count))
+            done = torch.cuda.Event()
+            done.record(stream)
+            comm.wait_event(done)
+            with torch.cuda.stream(comm):
+                dist.all_reduce(gview[first * per_level:(first + count) * per_level])
+        if ev is not None:
+            ev[1].record(stream)  # compute done; the tail of the exchange is inside the step but not inside kernel_ms
+        stream.wait_stream(comm)
+
     def step(i, ev=None):
+        if exchange and len(ranges) > 1:
+            return step_overlapped(i, ev)
         k = i % n_sets
         if args.path == "fused":
             enc.encode_forward_backward(xs[k], ups[k], grad, out=outs[k])
@@ -439,8 +468,10 @@ def run_ours(args):
                        "tuning": {"levels_per_thread": t.levels_per_thread, "block_threads": t.block_threads,
                                   "level_major": t.level_major, "exact_blend": t.exact_blend,
                                   "warp_aggregate": t.warp_aggregate},
-                       "multi_gpu": "batch sharded, tables replicated, NCCL all-reduce of the 64 MiB table-gradient "
-                                    "buffer per step" if world > 1 and not args.no_allreduce else "single GPU"},
+                       "multi_gpu": (f"batch sharded, tables replicated, NCCL all-reduce of the "
+                                     f"{L * (1 << args.log2t) * F * 4 >> 20} MiB table-gradient accumulator per step in "
+                                     f"{len(ranges)} level chunks overlapped with the next chunk's kernel")
+                                    if exchange else "single GPU"},
             "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu,
             "train_step": train,
         }
@@ -466,6 +497,8 @@ def main():
     ap.add_argument("--exact", type=int, default=1)
     ap.add_argument("--aggregate", type=int, default=0)
     ap.add_argument("--no-allreduce", action="store_true")
+    ap.add_argument("--level-chunks", type=int, default=4,
+                    help="multi-GPU: level chunks whose gradient all-reduce overlaps the next chunk's kernel")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-train", action="store_true")
     args = ap.parse_args()

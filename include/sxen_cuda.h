@@ -179,6 +179,17 @@ SXEN_API sxen_status sxen_encoder_encode_backward(sxen_encoder* enc, const void*
 SXEN_API sxen_status sxen_encoder_encode_forward_backward(sxen_encoder* enc, const void* x_dev, sxen_coord_type type,
                                                           const float* upstream_dev, size_t n_samples, float* out_dev,
                                                           sxen_grad* grad, void* stream);
+/* The same two calls restricted to encoder levels [first_level, first_level + level_count): only that slice of every
+ * upstream / feature row and of the accumulator is read and written.  A batch-sharded multi-GPU step walks the levels in
+ * chunks and all-reduces each chunk's slice of the accumulator (contiguous: level l starts at values + l*T*F) on a
+ * second stream while the next chunk computes. */
+SXEN_API sxen_status sxen_encoder_encode_backward_levels(sxen_encoder* enc, const void* x_dev, sxen_coord_type type,
+                                                         const float* upstream_dev, size_t n_samples, sxen_grad* grad,
+                                                         int32_t first_level, int32_t level_count, void* stream);
+SXEN_API sxen_status sxen_encoder_encode_forward_backward_levels(sxen_encoder* enc, const void* x_dev,
+                                                                 sxen_coord_type type, const float* upstream_dev,
+                                                                 size_t n_samples, float* out_dev, sxen_grad* grad,
+                                                                 int32_t first_level, int32_t level_count, void* stream);
 /* Synchronises `stream` and reports what the reference would have thrown for this encoder's launches since the
  * last check: SXEN_INVALID_ARGUMENT with the first sample whose coordinate is NaN or outside [0,1]
  * (check_input, src/encoding.cpp:183-194).  Such samples write zero features and add no gradient. */
@@ -294,6 +305,17 @@ SXEN_API sxen_status sxen_trainer_accumulate(sxen_trainer* trainer, const void* 
                                              size_t global_batch, void* stream);
 /* Buffers a multi-GPU host all-reduces (SUM) between accumulate and update: the table-gradient accumulator, the MLP
  * gradient (sxen_mlp_grads_dev) and the loss sum. */
+/* sxen_trainer_accumulate in two halves, for a multi-GPU host that overlaps the gradient exchange with the backward:
+ * _head runs encode -> Mlp forward -> loss/upstream -> Mlp backward and leaves d(loss)/d(encoding) in the workspace;
+ * _tables runs encode_backward for levels [first_level, first_level + level_count) of the same batch (call it once per
+ * level chunk, all-reducing each chunk's slice of the accumulator while the next one runs).
+ * _tables without a matching _head (same n_samples) is SXEN_LOGIC_ERROR. */
+SXEN_API sxen_status sxen_trainer_accumulate_head(sxen_trainer* trainer, const void* coords_dev, sxen_coord_type coord_type,
+                                                  const void* targets_dev, sxen_coord_type target_type, size_t n_samples,
+                                                  size_t global_batch, void* stream);
+SXEN_API sxen_status sxen_trainer_accumulate_tables(sxen_trainer* trainer, const void* coords_dev,
+                                                    sxen_coord_type coord_type, size_t n_samples, int32_t first_level,
+                                                    int32_t level_count, void* stream);
 SXEN_API sxen_status sxen_trainer_table_grad(sxen_trainer* trainer, sxen_grad** out);
 SXEN_API sxen_status sxen_trainer_loss_dev(sxen_trainer* trainer, double** out_dev);
 /* Synchronises; loss = sum / (global_batch*out_w).  SXEN_TRAINING_ERROR if non-finite (src/trainer.cpp:120-123);

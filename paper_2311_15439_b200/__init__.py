@@ -13,7 +13,7 @@ from .encoding import (Backend, EncoderConfig, EncoderGradient, HashEncoder, Lev
                        Tuning, equal_memory_multiplier, hash_coords, level_resolution, skew_constants)
 from .optimizer import AdamConfig, AdamState, SparseAdamState  # noqa: E402
 from .mlp import Mlp, MlpConfig  # noqa: E402
-from .trainer import TrainConfig, Trainer, TrainResult, chunk_bounds, train_field  # noqa: E402
+from .trainer import TrainConfig, Trainer, TrainResult, chunk_bounds, level_ranges, train_field  # noqa: E402
 from .checkpoint import load_checkpoint, save_checkpoint  # noqa: E402
 from .tasks import FitImageOptions, FitImageResult, fit_image, image_sampler, psnr_from_mse, render_mse  # noqa: E402
 from .rng import CounterRng, hash_combine, mix64  # noqa: E402
@@ -21,7 +21,7 @@ from .rng import CounterRng, hash_combine, mix64  # noqa: E402
 __all__ = ["lib", "CudaError", "IoError", "TrainingError", "Backend", "LevelScale", "EncoderConfig", "HashEncoder",
            "EncoderGradient", "LookupCounters", "Tuning", "equal_memory_multiplier", "level_resolution",
            "skew_constants", "hash_coords", "AdamConfig", "AdamState", "SparseAdamState", "CounterRng", "mix64",
-           "hash_combine", "Mlp", "MlpConfig", "TrainConfig", "Trainer", "TrainResult", "chunk_bounds", "train_field",
+           "hash_combine", "Mlp", "MlpConfig", "TrainConfig", "Trainer", "TrainResult", "chunk_bounds", "level_ranges", "train_field",
            "FitImageOptions", "FitImageResult", "fit_image", "image_sampler", "psnr_from_mse", "render_mse",
            "save_checkpoint", "load_checkpoint"]
 

@@ -77,6 +77,8 @@ SIGNATURES = {
     "sxen_encoder_encode_debug": (C.c_int, [_vp, _vp, C.c_int, _sz, _vp, _vp, _vp]),
     "sxen_encoder_encode_backward": (C.c_int, [_vp, _vp, C.c_int, _vp, _sz, _vp, _vp]),
     "sxen_encoder_encode_forward_backward": (C.c_int, [_vp, _vp, C.c_int, _vp, _sz, _vp, _vp, _vp]),
+    "sxen_encoder_encode_backward_levels": (C.c_int, [_vp, _vp, C.c_int, _vp, _sz, _vp, C.c_int32, C.c_int32, _vp]),
+    "sxen_encoder_encode_forward_backward_levels": (C.c_int, [_vp, _vp, C.c_int, _vp, _sz, _vp, _vp, C.c_int32, C.c_int32, _vp]),
     "sxen_encoder_check": (C.c_int, [_vp, _vp]),
     "sxen_encoder_counters": (C.c_int, [_vp, _P(LookupCountersC)]),
     "sxen_encoder_reset_counters": (C.c_int, [_vp]),
@@ -129,6 +131,8 @@ SIGNATURES = {
     "sxen_trainer_create": (C.c_int, [_vp, _vp, _P(_vp)]),
     "sxen_trainer_destroy": (C.c_int, [_vp]),
     "sxen_trainer_accumulate": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, _sz, _sz, _vp]),
+    "sxen_trainer_accumulate_head": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, _sz, _sz, _vp]),
+    "sxen_trainer_accumulate_tables": (C.c_int, [_vp, _vp, C.c_int, _sz, C.c_int32, C.c_int32, _vp]),
     "sxen_trainer_table_grad": (C.c_int, [_vp, _P(_vp)]),
     "sxen_trainer_loss_dev": (C.c_int, [_vp, _P(_vp)]),
     "sxen_trainer_loss": (C.c_int, [_vp, _sz, _P(_dbl), _vp]),

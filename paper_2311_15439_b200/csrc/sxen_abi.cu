@@ -182,9 +182,9 @@ void base_args(const sxen_encoder* enc, const void* x, sxen_coord_type type, siz
   a.skew = enc->skew;
 }
 
-void level_chunk(const sxen_encoder* enc, const sxen_grad* grad, int level0, EncodeArgs& a) {
+void level_chunk(const sxen_encoder* enc, const sxen_grad* grad, int level0, int level_end, EncodeArgs& a) {
   a.level0 = level0;
-  a.n_levels = std::min<int>(sxen_dev::kMaxLaunchLevels, enc->cfg.levels - level0);
+  a.n_levels = std::min<int>(sxen_dev::kMaxLaunchLevels, level_end - level0);
   a.agg_mask = 0;
   // the replicas are laid out for the lattice of the encoder the accumulator was created from
   const bool replicas = grad != nullptr && grad->coarse != nullptr && enc->tuning.coarse_replicas >= 0 &&
@@ -221,9 +221,16 @@ sxen_status check_batch(const sxen_encoder* enc, const void* x, sxen_coord_type 
   return SXEN_OK;
 }
 
+// first_level / level_count select a contiguous range of encoder levels (count < 0 = all from first_level on): the
+// launch reads and writes only that range's slice of every feature / upstream row and of the accumulator.
 sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, const float* upstream, size_t n,
-                       float* out, sxen_grad* grad, int mode, cudaStream_t stream) {
+                       float* out, sxen_grad* grad, int mode, cudaStream_t stream, int first_level = 0,
+                       int level_count = -1) {
   if (sxen_status st = check_batch(enc, x, type, n)) return st;
+  if (level_count < 0) level_count = enc->cfg.levels - first_level;
+  SXEN_REQUIRE(first_level >= 0 && level_count >= 0 && first_level + level_count <= enc->cfg.levels,
+               "level range [%d, %d) outside the encoder's %d levels", first_level, first_level + level_count,
+               enc->cfg.levels);
   if (mode & sxen_dev::kModeFwd) SXEN_REQUIRE(n == 0 || out != nullptr, "encode: output pointer is null");
   if (mode & sxen_dev::kModeBwd) {
     SXEN_REQUIRE(n == 0 || upstream != nullptr, "encode_backward: upstream pointer is null");
@@ -233,7 +240,7 @@ sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, c
                      grad->table_size == enc->cfg.table_size && grad->device == enc->device,
                  "encode_backward: gradient accumulator shape mismatch");
   }
-  if (n == 0) return SXEN_OK;
+  if (n == 0 || level_count == 0) return SXEN_OK;
   DeviceGuard guard(enc->device);
   EncodeArgs a;
   base_args(enc, x, type, n, a);
@@ -259,8 +266,9 @@ sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, c
   ln.exact = enc->tuning.exact_blend ? 1 : 0;
   ln.grid_backend = enc->cfg.backend == SXEN_BACKEND_GRID ? 1 : 0;
   ln.block_threads = enc->tuning.block_threads;
-  for (int level0 = 0; level0 < enc->cfg.levels; level0 += sxen_dev::kMaxLaunchLevels) {
-    level_chunk(enc, (mode & sxen_dev::kModeBwd) ? grad : nullptr, level0, a);
+  const int level_end = first_level + level_count;
+  for (int level0 = first_level; level0 < level_end; level0 += sxen_dev::kMaxLaunchLevels) {
+    level_chunk(enc, (mode & sxen_dev::kModeBwd) ? grad : nullptr, level0, level_end, a);
     a.vec = 4;
     if (mode & sxen_dev::kModeFwd) a.vec = std::min(a.vec, ptr_vec(out));
     if (mode & sxen_dev::kModeBwd) a.vec = std::min(a.vec, ptr_vec(upstream));
@@ -276,7 +284,7 @@ sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, c
       }
     }
   }
-  enc->touched += static_cast<uint64_t>(n) * static_cast<uint64_t>(enc->cfg.levels) *
+  enc->touched += static_cast<uint64_t>(n) * static_cast<uint64_t>(level_count) *
                   static_cast<uint64_t>(enc->vertices()) * ((mode == sxen_dev::kModeBoth) ? 2u : 1u);
   return SXEN_OK;
 }
@@ -562,6 +570,23 @@ sxen_status sxen_encoder_encode_forward_backward(sxen_encoder* enc, const void* 
   return run_encode(enc, x_dev, type, upstream_dev, n_samples, out_dev, grad, sxen_dev::kModeBoth, as_stream(stream));
 }
 
+sxen_status sxen_encoder_encode_backward_levels(sxen_encoder* enc, const void* x_dev, sxen_coord_type type,
+                                                const float* upstream_dev, size_t n_samples, sxen_grad* grad,
+                                                int32_t first_level, int32_t level_count, void* stream) {
+  SXEN_REQUIRE(level_count >= 0, "level_count must be >= 0");
+  return run_encode(enc, x_dev, type, upstream_dev, n_samples, nullptr, grad, sxen_dev::kModeBwd, as_stream(stream),
+                    first_level, level_count);
+}
+
+sxen_status sxen_encoder_encode_forward_backward_levels(sxen_encoder* enc, const void* x_dev, sxen_coord_type type,
+                                                        const float* upstream_dev, size_t n_samples, float* out_dev,
+                                                        sxen_grad* grad, int32_t first_level, int32_t level_count,
+                                                        void* stream) {
+  SXEN_REQUIRE(level_count >= 0, "level_count must be >= 0");
+  return run_encode(enc, x_dev, type, upstream_dev, n_samples, out_dev, grad, sxen_dev::kModeBoth, as_stream(stream),
+                    first_level, level_count);
+}
+
 sxen_status sxen_encoder_encode_debug(sxen_encoder* enc, const void* x_dev, sxen_coord_type type, size_t n_samples,
                                       uint32_t* idx_dev, double* w_dev, void* stream) {
   if (sxen_status st = check_batch(enc, x_dev, type, n_samples)) return st;
@@ -571,7 +596,7 @@ sxen_status sxen_encoder_encode_debug(sxen_encoder* enc, const void* x_dev, sxen
   EncodeArgs a;
   base_args(enc, x_dev, type, n_samples, a);
   for (int level0 = 0; level0 < enc->cfg.levels; level0 += sxen_dev::kMaxLaunchLevels) {
-    level_chunk(enc, nullptr, level0, a);
+    level_chunk(enc, nullptr, level0, enc->cfg.levels, a);
     SXEN_CUDA(kDebug[enc->cfg.dim - 1](a, enc->cfg.backend == SXEN_BACKEND_GRID ? 1 : 0, idx_dev, w_dev,
                                        enc->cfg.levels, as_stream(stream)));
     count_launch();

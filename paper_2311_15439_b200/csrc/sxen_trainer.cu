@@ -18,6 +18,7 @@ struct sxen_trainer {
   sxen_sparse_adam* table_opt = nullptr;
   sxen_adam* mlp_opt = nullptr;
   size_t capacity = 0;           // samples the workspace holds
+  size_t head_samples = 0;       // samples whose input gradient the last accumulate_head left in the workspace
   float* features = nullptr;     // N x L*F
   float* input_grad = nullptr;   // N x L*F
   double* upstream = nullptr;    // N x out_w
@@ -112,9 +113,9 @@ sxen_status sxen_trainer_loss_dev(sxen_trainer* t, double** out_dev) {
   return SXEN_OK;
 }
 
-sxen_status sxen_trainer_accumulate(sxen_trainer* t, const void* coords_dev, sxen_coord_type coord_type,
-                                    const void* targets_dev, sxen_coord_type target_type, size_t n_samples,
-                                    size_t global_batch, void* stream) {
+sxen_status sxen_trainer_accumulate_head(sxen_trainer* t, const void* coords_dev, sxen_coord_type coord_type,
+                                         const void* targets_dev, sxen_coord_type target_type, size_t n_samples,
+                                         size_t global_batch, void* stream) {
   SXEN_REQUIRE(t != nullptr, "trainer handle is null");
   SXEN_REQUIRE(global_batch >= 1 && n_samples <= global_batch, "train: local chunk (%zu) exceeds the global batch (%zu)",
                n_samples, global_batch);
@@ -127,8 +128,33 @@ sxen_status sxen_trainer_accumulate(sxen_trainer* t, const void* coords_dev, sxe
   if (sxen_status st = sxen_mlp_forward_backward(t->mlp, t->features, targets_dev, target_type, n_samples, global_batch,
                                                  nullptr, t->input_grad, t->loss_sum, stream))
     return st;
-  // encoder.encode_backward on d(loss)/d(encoding) (:47)
-  return sxen_encoder_encode_backward(t->enc, coords_dev, coord_type, t->input_grad, n_samples, t->grad, stream);
+  t->head_samples = n_samples;
+  return SXEN_OK;
+}
+
+sxen_status sxen_trainer_accumulate_tables(sxen_trainer* t, const void* coords_dev, sxen_coord_type coord_type,
+                                           size_t n_samples, int32_t first_level, int32_t level_count, void* stream) {
+  SXEN_REQUIRE(t != nullptr, "trainer handle is null");
+  if (n_samples == 0) return SXEN_OK;
+  if (n_samples != t->head_samples)
+    return fail(SXEN_LOGIC_ERROR, "train: accumulate_tables(%zu samples) without a matching accumulate_head (%zu)",
+                n_samples, t->head_samples);
+  DeviceGuard guard(t->device);
+  // encoder.encode_backward on d(loss)/d(encoding) (:47), levels [first_level, first_level + level_count)
+  return sxen_encoder_encode_backward_levels(t->enc, coords_dev, coord_type, t->input_grad, n_samples, t->grad,
+                                             first_level, level_count, stream);
+}
+
+sxen_status sxen_trainer_accumulate(sxen_trainer* t, const void* coords_dev, sxen_coord_type coord_type,
+                                    const void* targets_dev, sxen_coord_type target_type, size_t n_samples,
+                                    size_t global_batch, void* stream) {
+  if (sxen_status st = sxen_trainer_accumulate_head(t, coords_dev, coord_type, targets_dev, target_type, n_samples,
+                                                    global_batch, stream))
+    return st;
+  if (n_samples == 0) return SXEN_OK;
+  sxen_encoder_config ec;
+  sxen_encoder_get_config(t->enc, &ec);
+  return sxen_trainer_accumulate_tables(t, coords_dev, coord_type, n_samples, 0, ec.levels, stream);
 }
 
 sxen_status sxen_trainer_loss(sxen_trainer* t, size_t global_batch, double* loss_out, void* stream) {

@@ -314,8 +314,9 @@ class HashEncoder:
                                                                 out.ctypes.data_as(C.POINTER(C.c_float))))
         return out
 
-    def encode_backward(self, x, upstream, grad: EncoderGradient, stream=None) -> None:
-        """Batched HashEncoder::encode_backward: grad[l][idx] += w * upstream[l*F:(l+1)*F] for every vertex."""
+    def encode_backward(self, x, upstream, grad: EncoderGradient, stream=None, levels=None) -> None:
+        """Batched HashEncoder::encode_backward: grad[l][idx] += w * upstream[l*F:(l+1)*F] for every vertex.
+        ``levels=(first, count)`` (device tensors only) restricts the launch to that range of encoder levels."""
         LF = self._cfg.encoded_width()
         if _is_torch(x):
             import torch
@@ -324,10 +325,17 @@ class HashEncoder:
             if tuple(upstream.shape) != (x.shape[0], LF):  # src/encoding.cpp:320-322
                 raise ValueError("encode_backward: upstream span has wrong width")
             upstream = upstream.to(torch.float32).contiguous()
+            if levels is not None:
+                raise_for(self._lib, self._lib.sxen_encoder_encode_backward_levels(
+                    self._h, C.c_void_p(x.data_ptr()), _coord_type(x), C.c_void_p(upstream.data_ptr()), x.shape[0],
+                    grad._h, int(levels[0]), int(levels[1]), _stream_ptr(stream)))
+                return
             raise_for(self._lib, self._lib.sxen_encoder_encode_backward(
                 self._h, C.c_void_p(x.data_ptr()), _coord_type(x), C.c_void_p(upstream.data_ptr()), x.shape[0],
                 grad._h, _stream_ptr(stream)))
             return
+        if levels is not None:
+            raise ValueError("encode_backward: a level range needs device tensors")
         x = np.ascontiguousarray(x, dtype=np.float64)
         self._check_x(x)
         up = np.ascontiguousarray(upstream, dtype=np.float64)
@@ -337,10 +345,14 @@ class HashEncoder:
             self._h, x.ctypes.data_as(C.POINTER(C.c_double)), up.ctypes.data_as(C.POINTER(C.c_double)), x.shape[0],
             grad._h))
 
-    def encode_forward_backward(self, x, upstream, grad: EncoderGradient, out=None, stream=None):
+    def encode_forward_backward(self, x, upstream, grad: EncoderGradient, out=None, stream=None, levels=None):
         """encode + encode_backward of one batch off a single lattice walk.  numpy inputs (x float64; upstream float64
-        or float32) take the pipelined host entry point; torch CUDA tensors the asynchronous device one."""
+        or float32) take the pipelined host entry point; torch CUDA tensors the asynchronous device one.
+        ``levels=(first, count)`` (device tensors only) restricts the launch to that range of encoder levels: only that
+        slice of every feature row is written."""
         if not _is_torch(x):
+            if levels is not None:
+                raise ValueError("encode_forward_backward: a level range needs device tensors")
             x = np.ascontiguousarray(x, dtype=np.float64)
             self._check_x(x)
             n, LF = x.shape[0], self._cfg.encoded_width()
@@ -366,6 +378,11 @@ class HashEncoder:
         if out is None:
             out = torch.empty((n, LF), dtype=torch.float32, device=x.device)
         upstream = upstream.to(torch.float32).contiguous()
+        if levels is not None:
+            raise_for(self._lib, self._lib.sxen_encoder_encode_forward_backward_levels(
+                self._h, C.c_void_p(x.data_ptr()), _coord_type(x), C.c_void_p(upstream.data_ptr()), n,
+                C.c_void_p(out.data_ptr()), grad._h, int(levels[0]), int(levels[1]), _stream_ptr(stream)))
+            return out
         raise_for(self._lib, self._lib.sxen_encoder_encode_forward_backward(
             self._h, C.c_void_p(x.data_ptr()), _coord_type(x), C.c_void_p(upstream.data_ptr()), n,
             C.c_void_p(out.data_ptr()), grad._h, _stream_ptr(stream)))

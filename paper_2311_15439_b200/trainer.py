@@ -77,6 +77,20 @@ class Trainer:
             self._h, C.c_void_p(coords.data_ptr()), self._typ(coords), C.c_void_p(targets.data_ptr()),
             self._typ(targets), coords.shape[0], global_batch, _stream_ptr(stream)))
 
+    def accumulate_head(self, coords, targets, global_batch: int, stream=None) -> None:
+        """encode -> MLP forward -> loss/upstream -> MLP backward; d(loss)/d(encoding) stays in the workspace."""
+        from .encoding import _stream_ptr
+        raise_for(self._lib, self._lib.sxen_trainer_accumulate_head(
+            self._h, C.c_void_p(coords.data_ptr()), self._typ(coords), C.c_void_p(targets.data_ptr()),
+            self._typ(targets), coords.shape[0], global_batch, _stream_ptr(stream)))
+
+    def accumulate_tables(self, coords, first_level: int, level_count: int, stream=None) -> None:
+        """encode_backward of the batch of the last accumulate_head for one range of encoder levels."""
+        from .encoding import _stream_ptr
+        raise_for(self._lib, self._lib.sxen_trainer_accumulate_tables(
+            self._h, C.c_void_p(coords.data_ptr()), self._typ(coords), coords.shape[0], first_level, level_count,
+            _stream_ptr(stream)))
+
     def table_grad_device(self):
         """Flat float32 view of the table-gradient accumulator (untouched rows carry -0.0; SUM all-reduce keeps that)."""
         import torch
@@ -118,21 +132,57 @@ class Trainer:
             self._typ(targets), coords.shape[0], C.byref(ta), C.byref(ma), C.byref(out), _stream_ptr(stream)))
         return out.value
 
-    def distributed_step(self, coords, targets, table_adam: AdamConfig, mlp_adam: AdamConfig, group=None) -> float:
+    def distributed_step(self, coords, targets, table_adam: AdamConfig, mlp_adam: AdamConfig, group=None,
+                         level_chunks: int = 4) -> float:
         """Batch-sharded step: coords/targets hold the WHOLE batch on every rank (the sampler is deterministic in
         (seed, step), so no scatter is needed); this rank runs its contiguous chunk, then table gradients, MLP gradients
-        and the loss sum are all-reduced (SUM) and every rank applies the identical update."""
+        and the loss sum are all-reduced (SUM) and every rank applies the identical update.
+
+        The exchange overlaps the backward: after the MLP half, encode_backward walks the levels in ``level_chunks``
+        ranges; each range's slice of the accumulator (contiguous, level-major) is all-reduced on a second stream while
+        the next range computes.  The MLP gradient and the loss sum go first, under the first range."""
+        import torch
         import torch.distributed as dist
         world, rank = dist.get_world_size(group), dist.get_rank(group)
         batch = coords.shape[0]
         b, e = chunk_bounds(batch, world, rank)
-        self.accumulate(coords[b:e], targets[b:e], batch)
-        dist.all_reduce(self.table_grad_device(), group=group)
-        dist.all_reduce(self.mlp.gradient_device(), group=group)
-        dist.all_reduce(self.loss_device(), group=group)
+        x, t = coords[b:e].contiguous(), targets[b:e].contiguous()
+        levels = self.encoder.config.levels
+        bounds = level_ranges(levels, level_chunks)
+        gview = self.table_grad_device()
+        per_level = gview.numel() // levels
+        if not x.is_cuda:
+            raise ValueError("distributed_step: coords must be CUDA tensors")
+        main = torch.cuda.current_stream(x.device)
+        if getattr(self, "_comm", None) is None:
+            self._comm = torch.cuda.Stream(device=x.device)
+        comm = self._comm
+        self.accumulate_head(x, t, batch)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        comm.wait_event(ev)
+        with torch.cuda.stream(comm):
+            dist.all_reduce(self.mlp.gradient_device(), group=group)
+            dist.all_reduce(self.loss_device(), group=group)
+        for first, count in bounds:
+            if e > b:
+                self.accumulate_tables(x, first, count)
+            ev = torch.cuda.Event()
+            ev.record(main)
+            comm.wait_event(ev)
+            with torch.cuda.stream(comm):
+                dist.all_reduce(gview[first * per_level:(first + count) * per_level], group=group)
+        main.wait_stream(comm)
         loss = self.loss(batch)
         self.update(table_adam, mlp_adam)
         return loss
+
+
+def level_ranges(levels: int, chunks: int):
+    """[(first, count)] covering 0..levels in at most `chunks` near-equal contiguous ranges."""
+    chunks = max(1, min(chunks, levels))
+    per = (levels + chunks - 1) // chunks
+    return [(f, min(per, levels - f)) for f in range(0, levels, per)]
 
 
 BatchSampler = Callable[[int, int], tuple]  # (step, batch) -> (coords [B, dim], targets [B, out_w]) CUDA tensors

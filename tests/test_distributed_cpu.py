@@ -78,3 +78,14 @@ def test_gradient_allreduce_keeps_the_untouched_marker():
     assert bits[4] == 0x00000000            # exact cancellation is +0 : touched
     assert loss == 2.0
     assert part == list(range(1, 11))       # the chunks tile the batch exactly once
+
+
+def test_level_ranges_cover_every_level_once():
+    from paper_2311_15439_b200.trainer import level_ranges
+    for levels in (1, 3, 8, 16, 17):
+        for chunks in (1, 2, 4, 5, 16, 64):
+            r = level_ranges(levels, chunks)
+            assert len(r) <= max(1, min(chunks, levels))
+            covered = [l for f, c in r for l in range(f, f + c)]
+            assert covered == list(range(levels)), (levels, chunks, r)
+            assert all(c >= 1 for _, c in r)

@@ -168,3 +168,48 @@ def test_constant_target_converges(sx):
 
     res = sx.train_field(enc, mlp, sampler, sx.TrainConfig(batch_size=256, steps=300, record_every=50))
     assert res.loss_curve[0][1] > 0.1 and res.final_loss < 1e-3
+
+
+def test_overlapped_distributed_step_on_one_rank_equals_the_plain_step(sx):
+    """Trainer.distributed_step (level-chunked backward, gradient exchange on a second stream) through a 1-rank NCCL
+    group must reproduce Trainer.step: same loss bits, same tables after the update.  (>1 GPU is not available to the
+    tests; the chunking and the -0.0 algebra across ranks are covered on gloo in test_distributed_cpu.py.)"""
+    import os
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29631")
+    created = False
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+        created = True
+    try:
+        cfg = sx.EncoderConfig(dim=3, levels=16, table_size=1 << 14, features=2, base_resolution=16, growth=1.5)
+        N = 6000
+        x = torch.rand((N, 3), dtype=torch.float32, device="cuda:0")
+        tgt = torch.rand((N, 3), dtype=torch.float32, device="cuda:0")
+        ta, ma = sx.AdamConfig(lr=1e-2), sx.AdamConfig(lr=1e-3)
+        results = []
+        for mode in ("plain", "overlapped"):
+            enc = sx.HashEncoder(cfg)
+            enc.init_tables(42)
+            mlp = sx.Mlp(sx.MlpConfig(32, 64, 2, 3))
+            mlp.init_params(sx.hash_combine(42, 1))
+            tr = sx.Trainer(enc, mlp)
+            losses = []
+            for _ in range(3):
+                if mode == "plain":
+                    losses.append(tr.step(x, tgt, ta, ma))
+                else:
+                    losses.append(tr.distributed_step(x, tgt, ta, ma, level_chunks=4))
+            torch.cuda.synchronize()
+            results.append((losses, np.stack([enc.table(l) for l in range(16)]), mlp.parameters()))
+        (l0, t0, p0), (l1, t1, p1) = results
+        # same kernels on the same data; only the fp32 atomic order differs between runs
+        assert np.allclose(l0, l1, rtol=1e-6), (l0, l1)
+        assert np.allclose(t0, t1, rtol=0, atol=2e-3 * 1e-2 + 1e-7)
+        assert np.allclose(p0, p1, rtol=0, atol=1e-5)
+        with pytest.raises(RuntimeError):  # std::logic_error
+            tr.accumulate_tables(x[:100], 0, 16)  # no matching accumulate_head
+    finally:
+        if created:
+            dist.destroy_process_group()

@@ -477,3 +477,98 @@ def test_full_size_properties(sx, oracle_lib, n, growth, T):
     enc.check()
     c = enc.counters()
     assert c.out_of_bounds == 0
+
+
+# ------------------------------------------------------------------------------------------------ round-1 additions
+@pytest.mark.parametrize("n,growth", [(3, 1.5), (2, 2.0)])
+def test_coarse_replicas_and_cache_policies_do_not_change_results(sx, oracle_lib, n, growth):
+    """Replicated dense accumulators for the coarse levels (folded in-call) and the L2 eviction policies are pure
+    scheduling: touched sets exact, gradients within the fp32 bar, features bit-identical, under every combination."""
+    cfg = oracle.Config(dim=n, levels=16, table_size=1 << 16, features=2, base_resolution=16, growth=growth)
+    tables = oracle_lib.init_tables(cfg, 42)
+    enc = make_encoder(sx, cfg, seed=42)
+    N = 20000
+    x32 = oracle_lib.rng_doubles(5, 1, N * n).reshape(N, n).astype(np.float32)
+    x32[:64] = x32[0]          # a warp and a half of identical samples: maximum same-address pressure
+    x32[64:128, 0] = 0.0       # and a face of the cube
+    x = x32.astype(np.float64)
+    up32 = (oracle_lib.rng_doubles(6, 2, N * 32, -1.0, 1.0)).astype(np.float32).reshape(N, 32)
+    up32[::7] = 0.0            # exact-zero contributions still mark their rows touched
+    want, _ = oracle_lib.encode(cfg, tables, x)
+    wg, wt, _ = oracle_lib.encode_backward(cfg, x, up32.astype(np.float64))
+    scale = abs_contrib(oracle_lib, cfg, x, up32.astype(np.float64))
+    xd, upd = dev(x32), dev(up32)
+    for rep in (0, -1):
+        for hints in (-1, 0, 5, 8, 10, 15):
+            for lm, lpt in ((0, 2), (1, 4), (0, 1)):
+                enc.set_tuning(sx.Tuning(levels_per_thread=lpt, level_major=lm, coarse_replicas=rep, cache_hints=hints))
+                tag = (rep, hints, lm, lpt)
+                grad = sx.EncoderGradient(enc)
+                feats = enc.encode_forward_backward(xd, upd, grad).cpu().numpy()
+                assert np.array_equal(feats.view(np.uint32), want.view(np.uint32)), tag
+                vals, tch = grad_dense(grad, cfg)
+                assert np.array_equal(tch, wt), tag
+                assert (np.abs(vals - wg) <= GRAD_RTOL * scale + GRAD_ATOL).all(), tag
+                # a second batch into the same accumulator doubles it (the replicas were re-armed by the fold)
+                enc.encode_backward(xd, upd, grad)
+                vals2, tch2 = grad_dense(grad, cfg)
+                assert np.array_equal(tch2, wt), tag
+                assert (np.abs(vals2 - 2 * wg) <= 2 * GRAD_RTOL * scale + GRAD_ATOL).all(), tag
+    enc.check()
+
+
+def test_accumulator_of_another_lattice_falls_back_to_hashed_rows(sx, oracle_lib):
+    """An accumulator is shape-compatible with any encoder of the same (L, T, F) -- src/encoding.cpp:323-325 -- but its
+    replicas are laid out for the lattice it was created from; with another ladder the launch must not use them."""
+    cfg_a = oracle.Config(dim=2, levels=4, table_size=1 << 12, features=2, base_resolution=4, growth=2.0)
+    cfg_b = oracle.Config(dim=2, levels=4, table_size=1 << 12, features=2, base_resolution=7, growth=1.7)
+    enc_a, enc_b = make_encoder(sx, cfg_a, seed=1), make_encoder(sx, cfg_b, seed=1)
+    N = 3000
+    x = oracle_lib.rng_doubles(9, 1, N * 2).reshape(N, 2)
+    up = oracle_lib.rng_doubles(9, 2, N * 8, -1.0, 1.0).reshape(N, 8)
+    grad = sx.EncoderGradient(enc_a)        # replicas sized for cfg_a's lattice
+    enc_b.encode_backward(dev(x), dev(up, torch.float32), grad)
+    wg, wt, _ = oracle_lib.encode_backward(cfg_b, x, up.astype(np.float32).astype(np.float64))
+    scale = abs_contrib(oracle_lib, cfg_b, x, up)
+    vals, tch = grad_dense(grad, cfg_b)
+    assert np.array_equal(tch, wt)
+    assert (np.abs(vals - wg) <= GRAD_RTOL * scale + GRAD_ATOL).all()
+
+
+def test_level_ranges_compose_to_the_full_launch(sx, oracle_lib):
+    """encode_backward / encode_forward_backward restricted to level ranges: the chunks together equal the whole launch
+    (features bit-identical, touched sets equal, gradients within the fp32 bar), and a chunk leaves the other levels'
+    slices of the feature rows and of the accumulator alone."""
+    cfg = oracle.Config(dim=3, levels=16, table_size=1 << 15, features=2, base_resolution=16, growth=1.5)
+    tables = oracle_lib.init_tables(cfg, 42)
+    enc = make_encoder(sx, cfg, seed=42)
+    N = 7001
+    x32 = oracle_lib.rng_doubles(99, 1, N * 3).reshape(N, 3).astype(np.float32)
+    up32 = oracle_lib.rng_doubles(7, 2, N * 32, -1.0, 1.0).astype(np.float32).reshape(N, 32)
+    want, _ = oracle_lib.encode(cfg, tables, x32.astype(np.float64))
+    wg, wt, _ = oracle_lib.encode_backward(cfg, x32.astype(np.float64), up32.astype(np.float64))
+    scale = abs_contrib(oracle_lib, cfg, x32.astype(np.float64), up32.astype(np.float64))
+    xd, upd = dev(x32), dev(up32)
+    for chunks in (2, 4, 5, 16):
+        grad = sx.EncoderGradient(enc)
+        out = torch.full((N, 32), float("nan"), dtype=torch.float32, device="cuda:0")
+        ranges = sx.level_ranges(16, chunks)
+        for i, (first, count) in enumerate(ranges):
+            enc.encode_forward_backward(xd, upd, grad, out=out, levels=(first, count))
+            if i == 0:
+                o = out.cpu().numpy()
+                assert np.isnan(o[:, count * 2:]).all() and not np.isnan(o[:, :count * 2]).any()
+                _, tch = grad_dense(grad, cfg)
+                assert not tch[count:].any() and np.array_equal(tch[:count], wt[:count])
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32)), chunks
+        vals, tch = grad_dense(grad, cfg)
+        assert np.array_equal(tch, wt), chunks
+        assert (np.abs(vals - wg) <= GRAD_RTOL * scale + GRAD_ATOL).all(), chunks
+        grad_b = sx.EncoderGradient(enc)
+        for first, count in ranges:
+            enc.encode_backward(xd, upd, grad_b, levels=(first, count))
+        vb, tb = grad_dense(grad_b, cfg)
+        assert np.array_equal(tb, wt) and (np.abs(vb - wg) <= GRAD_RTOL * scale + GRAD_ATOL).all(), chunks
+    with pytest.raises(ValueError):
+        enc.encode_backward(xd, upd, sx.EncoderGradient(enc), levels=(10, 7))
+    assert enc.counters().out_of_bounds == 0

@@ -2,6 +2,7 @@
 // points.  Host code above the kernels; every entry point cites the reference call it stands in for in the header.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 
@@ -301,17 +302,31 @@ sxen_status read_status(sxen_encoder* enc, cudaStream_t stream, bool reset_bad) 
   return SXEN_OK;
 }
 
-sxen_status ensure_staging(sxen_encoder* enc) {
-  if (enc->stage_samples) return SXEN_OK;
-  const size_t chunk = 1u << 18;
+sxen_status ensure_staging(sxen_encoder* enc, bool need_up64) {
   const size_t lf = static_cast<size_t>(enc->cfg.levels) * static_cast<size_t>(enc->cfg.features);
-  for (int i = 0; i < sxen_encoder::kStages; ++i) {
-    SXEN_CUDA(cudaMalloc(&enc->stage_x[i], chunk * static_cast<size_t>(enc->cfg.dim) * sizeof(double)));
-    // one buffer serves features (f32) on the way out and upstream (f64 from the host, narrowed on device) on the way in
-    SXEN_CUDA(cudaMalloc(&enc->stage_io[i], chunk * lf * sizeof(double)));
-    SXEN_CUDA(cudaStreamCreateWithFlags(&enc->stage_stream[i], cudaStreamNonBlocking));
+  if (!enc->stage_samples) {
+    // samples per slot (2^17: 20 MB in, 17 MB out per pass at L*F = 32 -- large enough for the PCIe link's
+    // large-transfer rate, tools/e2e_sweep.py).  SXEN_HOST_CHUNK_LOG2 (14..22) is a tuning aid.
+    size_t chunk = 1u << 17;
+    if (const char* env = std::getenv("SXEN_HOST_CHUNK_LOG2")) {
+      const int v = std::atoi(env);
+      if (v >= 14 && v <= 22) chunk = static_cast<size_t>(1) << v;
+    }
+    for (int i = 0; i < sxen_encoder::kStages; ++i) {
+      SXEN_CUDA(cudaMalloc(&enc->stage_x[i], chunk * static_cast<size_t>(enc->cfg.dim) * sizeof(double)));
+      SXEN_CUDA(cudaMalloc(&enc->stage_up[i], chunk * lf * sizeof(float)));
+      SXEN_CUDA(cudaMalloc(&enc->stage_out[i], chunk * lf * sizeof(float)));
+      SXEN_CUDA(cudaEventCreateWithFlags(&enc->stage_in[i], cudaEventDisableTiming));
+      SXEN_CUDA(cudaEventCreateWithFlags(&enc->stage_done[i], cudaEventDisableTiming));
+      SXEN_CUDA(cudaEventCreateWithFlags(&enc->stage_back[i], cudaEventDisableTiming));
+    }
+    for (int i = 0; i < 3; ++i) SXEN_CUDA(cudaStreamCreateWithFlags(&enc->stage_stream[i], cudaStreamNonBlocking));
+    enc->stage_samples = chunk;
   }
-  enc->stage_samples = chunk;
+  if (need_up64 && enc->stage_up64[0] == nullptr) {
+    for (int i = 0; i < sxen_encoder::kStages; ++i)
+      SXEN_CUDA(cudaMalloc(&enc->stage_up64[i], enc->stage_samples * lf * sizeof(double)));
+  }
   return SXEN_OK;
 }
 
@@ -472,9 +487,15 @@ sxen_status sxen_encoder_destroy(sxen_encoder* enc) {
   cudaFreeHost(enc->status_host);
   for (int i = 0; i < sxen_encoder::kStages; ++i) {
     cudaFree(enc->stage_x[i]);
-    cudaFree(enc->stage_io[i]);
-    if (enc->stage_stream[i]) cudaStreamDestroy(enc->stage_stream[i]);
+    cudaFree(enc->stage_up[i]);
+    cudaFree(enc->stage_up64[i]);
+    cudaFree(enc->stage_out[i]);
+    if (enc->stage_in[i]) cudaEventDestroy(enc->stage_in[i]);
+    if (enc->stage_done[i]) cudaEventDestroy(enc->stage_done[i]);
+    if (enc->stage_back[i]) cudaEventDestroy(enc->stage_back[i]);
   }
+  for (int i = 0; i < 3; ++i)
+    if (enc->stage_stream[i]) cudaStreamDestroy(enc->stage_stream[i]);
   delete enc;
   return SXEN_OK;
 }
@@ -635,30 +656,94 @@ sxen_status sxen_encoder_reset_counters(sxen_encoder* enc) {
   return SXEN_OK;
 }
 
-// Host-buffer forms: chunked three-stage pipeline (H2D copy | kernel | D2H copy on rotating streams).
+// Host-buffer forms.  One pipeline serves all three: pass c copies its inputs on the copy-in stream, runs its kernels on
+// the compute stream and returns its features on the copy-out stream, in slot c % kStages; a slot's inputs are
+// overwritten only after its previous kernels finished, its feature buffer only after the previous copy-out finished.
+// With pinned host buffers the three stages of neighbouring passes overlap and the call runs at the PCIe rate.
+namespace {
+
+sxen_status host_pipeline(sxen_encoder* enc, const double* x_host, const void* up_host, sxen_coord_type up_type,
+                          size_t n_samples, float* out_host, sxen_grad* grad, int mode) {
+  const bool fwd = (mode & sxen_dev::kModeFwd) != 0, bwd = (mode & sxen_dev::kModeBwd) != 0;
+  const bool up64 = bwd && up_type == SXEN_COORD_F64;
+  DeviceGuard guard(enc->device);
+  if (sxen_status st = ensure_staging(enc, up64)) return st;
+  const size_t dim = static_cast<size_t>(enc->cfg.dim);
+  const size_t lf = static_cast<size_t>(enc->cfg.levels) * static_cast<size_t>(enc->cfg.features);
+  cudaStream_t s_in = enc->stage_stream[0], s_k = enc->stage_stream[1], s_out = enc->stage_stream[2];
+  // Pass sizes: the first pass's copy-in and the last pass's copy-out are the only transfers nothing overlaps, so the
+  // passes ramp up from 2^15 samples to the slot size and back down; in between they are slot-sized, which keeps the
+  // link at its large-transfer rate (tools/e2e_proto.py: 3.4 ms per 2^20 samples against 3.3 ms of raw two-way copies).
+  std::vector<size_t> passes;
+  {
+    const size_t cap = enc->stage_samples;
+    std::vector<size_t> ramp;
+    for (size_t r = 1u << 15; r < cap; r <<= 1) ramp.push_back(r);
+    size_t ramps = 0;
+    for (size_t r : ramp) ramps += 2 * r;
+    if (n_samples > ramps + cap / 2) {
+      for (size_t r : ramp) passes.push_back(r);
+      for (size_t left = n_samples - ramps; left > 0;) {
+        const size_t n = std::min(cap, left);
+        passes.push_back(n);
+        left -= n;
+      }
+      for (size_t i = ramp.size(); i-- > 0;) passes.push_back(ramp[i]);
+    } else {
+      const size_t per = std::min(cap, std::max<size_t>((n_samples + 7) / 8, 1u << 14));
+      for (size_t left = n_samples; left > 0;) {
+        const size_t n = std::min(per, left);
+        passes.push_back(n);
+        left -= n;
+      }
+    }
+  }
+  size_t done = 0;
+  for (int c = 0; c < static_cast<int>(passes.size()); ++c) {
+    const int slot = c % sxen_encoder::kStages;
+    const size_t n = passes[static_cast<size_t>(c)];
+    if (c >= sxen_encoder::kStages) SXEN_CUDA(cudaStreamWaitEvent(s_in, enc->stage_done[slot], 0));
+    SXEN_CUDA(cudaMemcpyAsync(enc->stage_x[slot], x_host + done * dim, n * dim * sizeof(double), cudaMemcpyHostToDevice, s_in));
+    if (bwd) {
+      if (up64) {
+        SXEN_CUDA(cudaMemcpyAsync(enc->stage_up64[slot], static_cast<const double*>(up_host) + done * lf,
+                                  n * lf * sizeof(double), cudaMemcpyHostToDevice, s_in));
+      } else {
+        SXEN_CUDA(cudaMemcpyAsync(enc->stage_up[slot], static_cast<const float*>(up_host) + done * lf,
+                                  n * lf * sizeof(float), cudaMemcpyHostToDevice, s_in));
+      }
+    }
+    SXEN_CUDA(cudaEventRecord(enc->stage_in[slot], s_in));
+    SXEN_CUDA(cudaStreamWaitEvent(s_k, enc->stage_in[slot], 0));
+    if (fwd && c >= sxen_encoder::kStages) SXEN_CUDA(cudaStreamWaitEvent(s_k, enc->stage_back[slot], 0));
+    if (up64) {
+      narrow_kernel<<<static_cast<unsigned>((n * lf + 255) / 256), 256, 0, s_k>>>(enc->stage_up64[slot], enc->stage_up[slot], n * lf);
+      SXEN_CUDA(cudaGetLastError());
+      count_launch();
+    }
+    if (sxen_status s = run_encode(enc, enc->stage_x[slot], SXEN_COORD_F64, bwd ? enc->stage_up[slot] : nullptr, n,
+                                   fwd ? enc->stage_out[slot] : nullptr, bwd ? grad : nullptr, mode, s_k))
+      return s;
+    SXEN_CUDA(cudaEventRecord(enc->stage_done[slot], s_k));
+    if (fwd) {
+      SXEN_CUDA(cudaStreamWaitEvent(s_out, enc->stage_done[slot], 0));
+      SXEN_CUDA(cudaMemcpyAsync(out_host + done * lf, enc->stage_out[slot], n * lf * sizeof(float), cudaMemcpyDeviceToHost, s_out));
+      SXEN_CUDA(cudaEventRecord(enc->stage_back[slot], s_out));
+    }
+    done += n;
+  }
+  SXEN_CUDA(cudaStreamSynchronize(s_k));
+  if (fwd) SXEN_CUDA(cudaStreamSynchronize(s_out));
+  return sxen_encoder_check(enc, s_k);
+}
+
+}  // namespace
+
 sxen_status sxen_encoder_encode_host(sxen_encoder* enc, const double* x_host, size_t n_samples, float* out_host) {
   if (sxen_status st = check_batch(enc, x_host, SXEN_COORD_F64, n_samples)) return st;
   SXEN_REQUIRE(n_samples == 0 || out_host != nullptr, "encode: output pointer is null");
   if (n_samples == 0) return SXEN_OK;
-  DeviceGuard guard(enc->device);
-  if (sxen_status st = ensure_staging(enc)) return st;
-  const size_t dim = static_cast<size_t>(enc->cfg.dim);
-  const size_t lf = static_cast<size_t>(enc->cfg.levels) * static_cast<size_t>(enc->cfg.features);
-  size_t done = 0;
-  for (int c = 0; done < n_samples; ++c) {
-    const int slot = c % sxen_encoder::kStages;
-    const size_t n = std::min(enc->stage_samples, n_samples - done);
-    cudaStream_t st = enc->stage_stream[slot];
-    SXEN_CUDA(cudaMemcpyAsync(enc->stage_x[slot], x_host + done * dim, n * dim * sizeof(double), cudaMemcpyHostToDevice, st));
-    if (sxen_status s = run_encode(enc, enc->stage_x[slot], SXEN_COORD_F64, nullptr, n, enc->stage_io[slot], nullptr,
-                                   sxen_dev::kModeFwd, st))
-      return s;
-    SXEN_CUDA(cudaMemcpyAsync(out_host + done * lf, enc->stage_io[slot], n * lf * sizeof(float), cudaMemcpyDeviceToHost, st));
-    done += n;
-  }
-  for (int i = 0; i < sxen_encoder::kStages; ++i) SXEN_CUDA(cudaStreamSynchronize(enc->stage_stream[i]));
-  if (sxen_status st = sxen_encoder_check(enc, enc->stage_stream[0])) return st;
-  return SXEN_OK;
+  return host_pipeline(enc, x_host, nullptr, SXEN_COORD_F32, n_samples, out_host, nullptr, sxen_dev::kModeFwd);
 }
 
 sxen_status sxen_encoder_encode_backward_host(sxen_encoder* enc, const double* x_host, const double* upstream_host,
@@ -667,32 +752,7 @@ sxen_status sxen_encoder_encode_backward_host(sxen_encoder* enc, const double* x
   SXEN_REQUIRE(n_samples == 0 || upstream_host != nullptr, "encode_backward: upstream pointer is null");
   SXEN_REQUIRE(grad != nullptr, "encode_backward: gradient accumulator is null");
   if (n_samples == 0) return SXEN_OK;
-  DeviceGuard guard(enc->device);
-  if (sxen_status st = ensure_staging(enc)) return st;
-  const size_t dim = static_cast<size_t>(enc->cfg.dim);
-  const size_t lf = static_cast<size_t>(enc->cfg.levels) * static_cast<size_t>(enc->cfg.features);
-  // half-size chunks: the stage buffer (chunk*lf*8 B) holds the f32 copy in its first quarter and the incoming
-  // doubles from byte chunk*lf*2 on -- disjoint ranges
-  size_t done = 0;
-  for (int c = 0; done < n_samples; ++c) {
-    const int slot = c % sxen_encoder::kStages;
-    const size_t n = std::min(enc->stage_samples / 2, n_samples - done);
-    cudaStream_t st = enc->stage_stream[slot];
-    float* up_f32 = enc->stage_io[slot];
-    double* up_f64 = reinterpret_cast<double*>(reinterpret_cast<char*>(enc->stage_io[slot]) +
-                                               (enc->stage_samples / 2) * lf * sizeof(float));
-    SXEN_CUDA(cudaMemcpyAsync(enc->stage_x[slot], x_host + done * dim, n * dim * sizeof(double), cudaMemcpyHostToDevice, st));
-    SXEN_CUDA(cudaMemcpyAsync(up_f64, upstream_host + done * lf, n * lf * sizeof(double), cudaMemcpyHostToDevice, st));
-    narrow_kernel<<<static_cast<unsigned>((n * lf + 255) / 256), 256, 0, st>>>(up_f64, up_f32, n * lf);
-    SXEN_CUDA(cudaGetLastError());
-    count_launch();
-    if (sxen_status s = run_encode(enc, enc->stage_x[slot], SXEN_COORD_F64, up_f32, n, nullptr, grad, sxen_dev::kModeBwd, st))
-      return s;
-    done += n;
-  }
-  for (int i = 0; i < sxen_encoder::kStages; ++i) SXEN_CUDA(cudaStreamSynchronize(enc->stage_stream[i]));
-  if (sxen_status st = sxen_encoder_check(enc, enc->stage_stream[0])) return st;
-  return SXEN_OK;
+  return host_pipeline(enc, x_host, upstream_host, SXEN_COORD_F64, n_samples, nullptr, grad, sxen_dev::kModeBwd);
 }
 
 sxen_status sxen_encoder_encode_forward_backward_host(sxen_encoder* enc, const double* x_host,
@@ -703,42 +763,7 @@ sxen_status sxen_encoder_encode_forward_backward_host(sxen_encoder* enc, const d
   SXEN_REQUIRE(n_samples == 0 || (upstream_host != nullptr && out_host != nullptr), "null upstream or output pointer");
   SXEN_REQUIRE(grad != nullptr, "encode_backward: gradient accumulator is null");
   if (n_samples == 0) return SXEN_OK;
-  DeviceGuard guard(enc->device);
-  if (sxen_status st = ensure_staging(enc)) return st;
-  const size_t dim = static_cast<size_t>(enc->cfg.dim);
-  const size_t lf = static_cast<size_t>(enc->cfg.levels) * static_cast<size_t>(enc->cfg.features);
-  // Stage buffer (chunk*lf*8 B) per slot, chunk/4 samples per pass: features out in [0, q), f32 upstream in [q, 2q),
-  // incoming f64 upstream in [2q, 4q) with q = chunk*lf*2 bytes... sized for the f64 case; disjoint ranges.
-  const size_t per = enc->stage_samples / 4;
-  size_t done = 0;
-  for (int c = 0; done < n_samples; ++c) {
-    const int slot = c % sxen_encoder::kStages;
-    const size_t n = std::min(per, n_samples - done);
-    cudaStream_t st = enc->stage_stream[slot];
-    char* base = reinterpret_cast<char*>(enc->stage_io[slot]);
-    float* out_dev = reinterpret_cast<float*>(base);
-    float* up_f32 = reinterpret_cast<float*>(base + per * lf * sizeof(float));
-    double* up_f64 = reinterpret_cast<double*>(base + 2 * per * lf * sizeof(float));
-    SXEN_CUDA(cudaMemcpyAsync(enc->stage_x[slot], x_host + done * dim, n * dim * sizeof(double), cudaMemcpyHostToDevice, st));
-    if (upstream_type == SXEN_COORD_F64) {
-      SXEN_CUDA(cudaMemcpyAsync(up_f64, static_cast<const double*>(upstream_host) + done * lf, n * lf * sizeof(double),
-                                cudaMemcpyHostToDevice, st));
-      narrow_kernel<<<static_cast<unsigned>((n * lf + 255) / 256), 256, 0, st>>>(up_f64, up_f32, n * lf);
-      SXEN_CUDA(cudaGetLastError());
-      count_launch();
-    } else {
-      SXEN_CUDA(cudaMemcpyAsync(up_f32, static_cast<const float*>(upstream_host) + done * lf, n * lf * sizeof(float),
-                                cudaMemcpyHostToDevice, st));
-    }
-    if (sxen_status s = run_encode(enc, enc->stage_x[slot], SXEN_COORD_F64, up_f32, n, out_dev, grad,
-                                   sxen_dev::kModeBoth, st))
-      return s;
-    SXEN_CUDA(cudaMemcpyAsync(out_host + done * lf, out_dev, n * lf * sizeof(float), cudaMemcpyDeviceToHost, st));
-    done += n;
-  }
-  for (int i = 0; i < sxen_encoder::kStages; ++i) SXEN_CUDA(cudaStreamSynchronize(enc->stage_stream[i]));
-  if (sxen_status st = sxen_encoder_check(enc, enc->stage_stream[0])) return st;
-  return SXEN_OK;
+  return host_pipeline(enc, x_host, upstream_host, upstream_type, n_samples, out_host, grad, sxen_dev::kModeBoth);
 }
 
 // ---------------------------------------------------------------------------------------------- gradient accumulator

@@ -59,12 +59,18 @@ struct sxen_encoder {
   sxen_tuning tuning{};
   uint64_t touched = 0;               // LookupCounters::touched_vertices
   uint64_t oob_base = 0;              // oob counted before the last device reset
-  // staging for the *_host entry points (chunked H2D / compute / D2H pipeline)
+  // staging for the *_host entry points: a three-stage pipeline (copy-in stream | compute stream | copy-out stream) over
+  // kStages rotating slots of stage_samples samples each
   static constexpr int kStages = 3;
   size_t stage_samples = 0;
-  double* stage_x[kStages] = {nullptr, nullptr, nullptr};
-  float* stage_io[kStages] = {nullptr, nullptr, nullptr};
-  cudaStream_t stage_stream[kStages] = {nullptr, nullptr, nullptr};
+  double* stage_x[kStages] = {nullptr, nullptr, nullptr};      // coordinates
+  float* stage_up[kStages] = {nullptr, nullptr, nullptr};      // upstream as f32
+  double* stage_up64[kStages] = {nullptr, nullptr, nullptr};   // upstream as the host's f64 (allocated on first use)
+  float* stage_out[kStages] = {nullptr, nullptr, nullptr};     // features
+  cudaStream_t stage_stream[3] = {nullptr, nullptr, nullptr};  // [0] copy-in, [1] compute, [2] copy-out
+  cudaEvent_t stage_in[kStages] = {nullptr, nullptr, nullptr};    // slot's inputs have arrived
+  cudaEvent_t stage_done[kStages] = {nullptr, nullptr, nullptr};  // slot's kernels have finished
+  cudaEvent_t stage_back[kStages] = {nullptr, nullptr, nullptr};  // slot's features have left
   size_t level_floats() const { return static_cast<size_t>(cfg.table_size) * static_cast<size_t>(cfg.features); }
   int vertices() const { return cfg.backend == SXEN_BACKEND_SIMPLEX ? cfg.dim + 1 : (1 << cfg.dim); }
 };

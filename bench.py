@@ -36,10 +36,12 @@ GROWTH = {2: 2.0, 3: 1.5, 4: 1.5, 5: 1.5, 6: 1.5}
 BATCH_LOG2 = 20
 
 
-def alg_bytes(n: int, mode: str) -> int:
-    """SURVEY.md 8d payload accounting per sample (f32 coords/features/upstream/grads, scatter-add = read+write)."""
-    fwd = 4 * n + 4 * L * F * (n + 1) + 4 * L * F
-    bwd = 4 * n + 4 * L * F + 8 * L * F * (n + 1)
+def alg_bytes(n: int, mode: str, verts: int = 0) -> int:
+    """SURVEY.md 8d payload accounting per sample (f32 coords/features/upstream/grads, scatter-add = read+write).
+    verts = vertices per (sample, level): n+1 for the simplex backend (default), 2^n for the grid backend."""
+    verts = verts or (n + 1)
+    fwd = 4 * n + 4 * L * F * verts + 4 * L * F
+    bwd = 4 * n + 4 * L * F + 8 * L * F * verts
     return {"fwd": fwd, "bwd": bwd, "fused": fwd + bwd}[mode]
 
 
@@ -53,8 +55,8 @@ def hbm_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def workload_name(n: int, t_log2: int = T_LOG2) -> str:
-    return (f"{n}D simplex encode fwd+bwd microbench, L={L} F={F} T=2^{t_log2} base={BASE} growth={GROWTH[n]}, "
+def workload_name(n: int, t_log2: int = T_LOG2, backend: str = "simplex") -> str:
+    return (f"{n}D {backend} encode fwd+bwd microbench, L={L} F={F} T=2^{t_log2} base={BASE} growth={GROWTH[n]}, "
             f"2^{BATCH_LOG2} uniform random samples per GPU")
 
 
@@ -214,7 +216,9 @@ def run_ours(args):
     N = 1 << BATCH_LOG2
     LF = L * F
     dev = torch.device(f"cuda:{local_rank}")
-    cfg = sx.EncoderConfig(dim=n, levels=L, table_size=1 << args.log2t, features=F, base_resolution=BASE, growth=GROWTH[n])
+    verts = (1 << n) if args.backend == "grid" else n + 1
+    cfg = sx.EncoderConfig(dim=n, levels=L, table_size=1 << args.log2t, features=F, base_resolution=BASE, growth=GROWTH[n],
+                           backend=1 if args.backend == "grid" else 0)
     enc = sx.HashEncoder(cfg, device=local_rank)
     enc.init_tables(42)
     tune = sx.Tuning(levels_per_thread=args.lpt, block_threads=args.block, level_major=args.level_major,
@@ -363,18 +367,18 @@ def run_ours(args):
     # dominant kernel duration, live, from events on the launching stream
     if args.path == "fused":
         kms = statistics.mean(e[2].elapsed_time(e[1]) for e in evs)
-        dom, dom_bytes = "encode_fwd_bwd_fused", alg_bytes(n, "fused")
+        dom, dom_bytes = "encode_fwd_bwd_fused", alg_bytes(n, "fused", verts)
         parts = {"fused_ms": kms}
     else:
         fwd_ms = statistics.mean(e[2].elapsed_time(e[0]) for e in evs)
         bwd_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
-        kms, dom, dom_bytes = bwd_ms, "encode_backward", alg_bytes(n, "bwd")
+        kms, dom, dom_bytes = bwd_ms, "encode_backward", alg_bytes(n, "bwd", verts)
         parts = {"fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
-                 "fwd_frac_of_hbm": alg_bytes(n, "fwd") * N / (fwd_ms * 1e-3) / 1e9 / hbm_peak()[0]}
+                 "fwd_frac_of_hbm": alg_bytes(n, "fwd", verts) * N / (fwd_ms * 1e-3) / 1e9 / hbm_peak()[0]}
     peak, peak_src = hbm_peak()
     achieved = dom_bytes * N / (kms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic_for(f"{dom}_n{n}"), "peak_source": peak_src,
+                "frac": achieved / peak, "traffic": traffic_for(f"{dom}_n{n}" + ("_grid" if args.backend == "grid" else "")), "peak_source": peak_src,
                 "alg_bytes_per_sample": dom_bytes, "kernel_ms": kms, **parts}
 
     line = None
@@ -416,7 +420,7 @@ def run_ours(args):
 
         # ---- CPU baseline on this box's host cores (bounded sample), N=1 only
         cpu = None
-        if world == 1 and not args.no_cpu:
+        if world == 1 and not args.no_cpu and args.backend == "simplex":
             try:
                 threads = host_threads()
                 samples = min(1 << 18, threads << 15)
@@ -429,7 +433,7 @@ def run_ours(args):
 
         # ---- extra (not the headline): the whole training step with the tcgen05 head on the same batch shape
         train = None
-        if not args.no_train and n in (2, 3):
+        if not args.no_train and n in (2, 3) and args.backend == "simplex":
             try:
                 mlp = sx.Mlp(sx.MlpConfig(LF, 64, 2, 3), device=local_rank)
                 mlp.init_params(sx.hash_combine(42, 1))
@@ -459,8 +463,8 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64 lattice math / u32 hash / f32 features+grads", "data": "synthetic",
-            "config": {"workload": workload_name(n, args.log2t), "dim": n, "levels": L, "features": F,
-                       "table_size_log2": args.log2t, "base_resolution": BASE, "growth": GROWTH[n], "samples_per_gpu_per_step": N,
+            "config": {"workload": workload_name(n, args.log2t, args.backend), "dim": n, "levels": L, "features": F,
+                       "backend": args.backend, "table_size_log2": args.log2t, "base_resolution": BASE, "growth": GROWTH[n], "samples_per_gpu_per_step": N,
                        "coords": "f32 on device (CounterRng(99,1))", "path": args.path,
                        "autotune_ms": autotune,
                        "l2_policy": f"inputs larger than L2: {n_sets} rotating input sets x 268 MB, plus "
@@ -490,6 +494,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--dim", type=int, default=3, choices=[2, 3, 4, 5, 6])
     ap.add_argument("--log2t", type=int, default=T_LOG2, help="log2 of the table size (19 = BASELINE configs[1], 22 = the sweep)")
+    ap.add_argument("--backend", choices=["simplex", "grid"], default="simplex",
+                    help="grid = the paper's comparator (2^n corners, n-linear weights), n = 2 or 3")
     ap.add_argument("--path", choices=["auto", "fused", "split"], default="auto")
     ap.add_argument("--lpt", type=int, default=0)
     ap.add_argument("--block", type=int, default=0)

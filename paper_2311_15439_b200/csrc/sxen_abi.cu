@@ -188,8 +188,11 @@ void level_chunk(const sxen_encoder* enc, const sxen_grad* grad, int level0, int
   a.n_levels = std::min<int>(sxen_dev::kMaxLaunchLevels, level_end - level0);
   a.agg_mask = 0;
   // the replicas are laid out for the lattice of the encoder the accumulator was created from
+  const bool tuned_grid = enc->cfg.backend == SXEN_BACKEND_GRID && enc->cfg.features == 2 && enc->cfg.dim >= 2 &&
+                          enc->cfg.dim <= 3;
   const bool replicas = grad != nullptr && grad->coarse != nullptr && enc->tuning.coarse_replicas >= 0 &&
-                        enc->cfg.backend == SXEN_BACKEND_SIMPLEX && grad->dim == enc->cfg.dim && grad->res == enc->res;
+                        (enc->cfg.backend == SXEN_BACKEND_SIMPLEX || tuned_grid) && grad->dim == enc->cfg.dim &&
+                        grad->res == enc->res;
   a.coarse = replicas ? grad->coarse : nullptr;
   for (int l = 0; l < sxen_dev::kMaxLaunchLevels; ++l) {
     const bool live = l < a.n_levels;
@@ -788,7 +791,8 @@ sxen_status sxen_grad_create(const sxen_encoder* enc, sxen_grad** out) {
   g->coarse_offset.assign(static_cast<size_t>(g->levels), 0u);
   g->coarse_verts.assign(static_cast<size_t>(g->levels), 0u);
   g->coarse_shift.assign(static_cast<size_t>(g->levels), -1);
-  if (enc->cfg.backend == SXEN_BACKEND_SIMPLEX) {
+  {
+    // (both backends address the same (res+1)^dim lattice; kernels without the replica path simply ignore the buffer)
     for (int l = 0; l < g->levels; ++l) {
       const double verts = std::pow(static_cast<double>(enc->res[static_cast<size_t>(l)]) + 1.0, enc->cfg.dim);
       if (verts > static_cast<double>(1u << 16)) continue;

@@ -189,6 +189,42 @@ __device__ __forceinline__ void grid_corner(const GridCell<ND>& c, int m, uint32
   w = weight;
 }
 
+// All 2^ND corners of one (sample, level) grid cell at once, in gather_grid's order (src/encoding.cpp:273-283: corner m,
+// bit d of m = axis d at base+1, weight = running product over the axes starting from 1.0).  For the tuned kernel at
+// ND <= 3, where the 2^ND (index, weight) pairs fit in registers.  `dense` as in simplex_lookup.
+template <int ND, bool DENSE = false>
+__device__ __forceinline__ bool grid_lookup(const double (&x)[ND], double scale, int res, uint32_t mask,
+                                            uint32_t (&idx)[1 << ND], double (&w)[1 << ND], uint32_t* dense = nullptr) {
+  GridCell<ND> c;
+  const bool oob = grid_prepare<ND>(x, scale, res, c);
+  uint32_t base[ND], stride[ND];
+  if constexpr (DENSE) {
+    uint32_t st = 1;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      // t0 = base * prime(d); the base coordinate itself: recompute from the weights' cell (b = t0 / prime is not exact
+      // in u32 arithmetic), so redo the floor the way grid_prepare did
+      const double yi = __dmul_rn(x[d], scale);
+      int b = __double2int_rd(yi);
+      b = min(max(b, 0), res - 1);
+      base[d] = static_cast<uint32_t>(b);
+      stride[d] = st;
+      st *= static_cast<uint32_t>(res + 1);
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < (1 << ND); ++m) {
+    grid_corner<ND>(c, m, mask, idx[m], w[m]);
+    if constexpr (DENSE) {
+      uint32_t dv = 0;
+#pragma unroll
+      for (int d = 0; d < ND; ++d) dv += (base[d] + ((m >> d) & 1)) * stride[d];
+      dense[m] = dv;
+    }
+  }
+  return oob;
+}
+
 // ---- memory helpers -------------------------------------------------------------------------
 
 // Gradient contributions below 2^-100 are added as +0.0f.  This keeps every partial sum on the 2^-123 grid, so the

@@ -83,9 +83,10 @@ __device__ __forceinline__ bool load_coords(const EncodeArgs& a, unsigned long l
   return ok;
 }
 
-template <int ND, int F, int LPT, int MODE, bool EXACT>
-__global__ void __launch_bounds__(LPT >= 4 ? 256 : 512)
+template <int ND, int F, int LPT, int MODE, bool EXACT, bool GRID = false>
+__global__ void __launch_bounds__((LPT >= 4 || GRID) ? 256 : 512)
 encode_kernel(const __grid_constant__ EncodeArgs a) {
+  constexpr int V = GRID ? (1 << ND) : (ND + 1);  // vertices per (sample, level): gather_grid / gather_simplex
   constexpr bool kFwd = (MODE & kModeFwd) != 0;
   constexpr bool kBwd = (MODE & kModeBwd) != 0;
   constexpr int K = LPT * F;
@@ -161,30 +162,32 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
       if (a.agg_mask != 0u) aggm = __ballot_sync(live, has && ((a.agg_mask >> l) & 1u));
     }
     if (has) {
-      uint32_t idx[ND + 1];
-      uint32_t dense[ND + 1];
-      double w[ND + 1];
-      const bool oob = simplex_lookup<ND, kBwd>(x, s_scale[l], a.skew, s_res[l], a.mask, idx, w, dense);
+      uint32_t idx[V];
+      uint32_t dense[V];
+      double w[V];
+      bool oob;
+      if constexpr (GRID) oob = grid_lookup<ND, kBwd>(x, s_scale[l], s_res[l], a.mask, idx, w, dense);
+      else oob = simplex_lookup<ND, kBwd>(x, s_scale[l], a.skew, s_res[l], a.mask, idx, w, dense);
       if (oob) atomicAdd(a.status + 1, 1ULL);
       const size_t level_off = static_cast<size_t>(a.level0 + l) * a.level_stride;
 
       if constexpr (kFwd) {
         const float* __restrict__ tab = a.tables + level_off;
-        float e[ND + 1][F];
+        float e[V][F];
         if constexpr (F == 2) {
           // (a 128-bit load for the two rows of an axis-0 pair, or a dense L1-resident shadow of the coarse levels, buys
           // nothing here: the gathers are bound by sector requests on the L1 miss path, and the pair's second row
           // already hits the sector its first row fetched -- profiles/r1_coarse_shadow_tables_negative.log)
           if (gather_kind) {
 #pragma unroll
-            for (int k = 0; k <= ND; ++k) load_row2_policy(tab + static_cast<size_t>(idx[k]) * F, e[k], gather_pol);
+            for (int k = 0; k < V; ++k) load_row2_policy(tab + static_cast<size_t>(idx[k]) * F, e[k], gather_pol);
           } else {
 #pragma unroll
-            for (int k = 0; k <= ND; ++k) load_row<F>(tab + static_cast<size_t>(idx[k]) * F, e[k]);
+            for (int k = 0; k < V; ++k) load_row<F>(tab + static_cast<size_t>(idx[k]) * F, e[k]);
           }
         } else {
 #pragma unroll
-          for (int k = 0; k <= ND; ++k) load_row<F>(tab + static_cast<size_t>(idx[k]) * F, e[k]);
+          for (int k = 0; k < V; ++k) load_row<F>(tab + static_cast<size_t>(idx[k]) * F, e[k]);
         }
         if constexpr (EXACT) {
           // src/encoding.cpp:305-313: acc starts at 0.0, acc += w_i * entry in chain order, all in double.
@@ -192,7 +195,7 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
 #pragma unroll
           for (int f = 0; f < F; ++f) acc[f] = 0.0;
 #pragma unroll
-          for (int k = 0; k <= ND; ++k) {
+          for (int k = 0; k < V; ++k) {
 #pragma unroll
             for (int f = 0; f < F; ++f) acc[f] = __dadd_rn(acc[f], __dmul_rn(w[k], static_cast<double>(e[k][f])));
           }
@@ -203,7 +206,7 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
 #pragma unroll
           for (int f = 0; f < F; ++f) acc[f] = 0.0f;
 #pragma unroll
-          for (int k = 0; k <= ND; ++k) {
+          for (int k = 0; k < V; ++k) {
             const float wk = static_cast<float>(w[k]);
 #pragma unroll
             for (int f = 0; f < F; ++f) acc[f] = __fmaf_rn(wk, e[k][f], acc[f]);
@@ -217,9 +220,9 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
         float* __restrict__ gl = a.grads + level_off;
         const bool agg = (aggm >> (threadIdx.x & 31)) & 1u;
         // EncoderGradient::add, src/encoding.cpp:110-120: dst[f] += scale * upstream[f]
-        float v[ND + 1][F];
+        float v[V][F];
 #pragma unroll
-        for (int k = 0; k <= ND; ++k) {
+        for (int k = 0; k < V; ++k) {
           const float wk = static_cast<float>(w[k]);
 #pragma unroll
           for (int f = 0; f < F; ++f) v[k][f] = canon(__fmul_rn(wk, upv[j * F + f]));
@@ -233,12 +236,12 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
           const uint32_t rep = static_cast<uint32_t>(s) & ((1u << cshift) - 1u);
           float* __restrict__ cb = a.coarse + a.cg.offset[l] + static_cast<size_t>(rep) * a.cg.verts[l] * F;
 #pragma unroll
-          for (int k = 0; k <= ND; ++k) red_row<F>(cb + static_cast<size_t>(dense[k]) * F, v[k]);
+          for (int k = 0; k < V; ++k) red_row<F>(cb + static_cast<size_t>(dense[k]) * F, v[k]);
           continue;
         }
         bool skip = false;
 #pragma unroll
-        for (int k = 0; k <= ND; ++k) {
+        for (int k = 0; k < V; ++k) {
           if (skip) {
             skip = false;
             continue;
@@ -246,10 +249,11 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
           if constexpr (F == 2) {
             // The hash multiplies axis 0 by 1 (include/sxen/hashing.hpp:16), so the chain step along axis 0 from an even
             // coordinate lands on the neighbouring row: rows idx and idx^1 share one 16-byte slot and take ONE
-            // red.v4 instead of two red.v2 (half the L2 atomic requests for that pair).
-            if (k < ND && a.merge_pairs && !agg) {
-              if ((idx[k] ^ idx[k < ND ? k + 1 : k]) == 1u) {
-                const int kn = k < ND ? k + 1 : k;
+            // red.v4 instead of two red.v2 (half the L2 atomic requests for that pair).  Grid backend: corners m and
+            // m+1 (m even) differ along axis 0 only, the same pair.
+            if (k + 1 < V && a.merge_pairs && !agg) {
+              if ((idx[k] ^ idx[k + 1 < V ? k + 1 : k]) == 1u) {
+                const int kn = k + 1 < V ? k + 1 : k;
                 const bool low = (idx[k] & 1u) == 0u;
                 float* p = gl + static_cast<size_t>(idx[k] & ~1u) * 2;
                 if (red_kind)

@@ -11,7 +11,7 @@ namespace {
 
 constexpr int ND = SXEN_ND;
 
-template <int F, int LPT, int MODE, bool EXACT>
+template <int F, int LPT, int MODE, bool EXACT, bool GRID = false>
 cudaError_t go(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t stream) {
   a.groups = (a.n_levels + LPT - 1) / LPT;
   a.groups_shift = -1;
@@ -23,7 +23,7 @@ cudaError_t go(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t stream) {
   while (vec > 1 && ((k % vec) != 0 || (a.row_width % vec) != 0 || ((a.level0 * F) % vec) != 0)) vec >>= 1;
   a.vec = vec;
   int block = ln.block_threads > 0 ? ln.block_threads : 256;
-  const int max_block = LPT >= 4 ? 256 : 512;
+  const int max_block = (LPT >= 4 || GRID) ? 256 : 512;
   if (block > max_block) block = max_block;
   block = (block / 32) * 32;
   if (block < 32) block = 32;
@@ -34,16 +34,16 @@ cudaError_t go(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t stream) {
     const unsigned long long threads = a.n_samples * static_cast<unsigned long long>(a.groups);
     grid = dim3(static_cast<unsigned>((threads + block - 1) / block), 1, 1);
   }
-  encode_kernel<ND, F, LPT, MODE, EXACT><<<grid, block, 0, stream>>>(a);
+  encode_kernel<ND, F, LPT, MODE, EXACT, GRID><<<grid, block, 0, stream>>>(a);
   return cudaGetLastError();
 }
 
-template <int F, int LPT, bool EXACT>
+template <int F, int LPT, bool EXACT, bool GRID = false>
 cudaError_t by_mode(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t stream) {
   switch (ln.mode) {
-    case kModeFwd: return go<F, LPT, kModeFwd, EXACT>(ln, a, stream);
-    case kModeBwd: return go<F, LPT, kModeBwd, EXACT>(ln, a, stream);
-    default: return go<F, LPT, kModeBoth, EXACT>(ln, a, stream);
+    case kModeFwd: return go<F, LPT, kModeFwd, EXACT, GRID>(ln, a, stream);
+    case kModeBwd: return go<F, LPT, kModeBwd, EXACT, GRID>(ln, a, stream);
+    default: return go<F, LPT, kModeBoth, EXACT, GRID>(ln, a, stream);
   }
 }
 
@@ -104,6 +104,17 @@ cudaError_t launch_fx(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t stream
 cudaError_t SXEN_CAT(launch_encode_nd, SXEN_ND)(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t stream,
                                                 int* used_lpt) {
   if (ln.grid_backend) {
+#if SXEN_ND == 2 || SXEN_ND == 3
+    // the paper's comparator in its 2D / 3D settings: same tuned kernel, 2^ND corners instead of ND+1 vertices
+    if (ln.features == 2) {
+      if (ln.lpt >= 2) {
+        *used_lpt = 2;
+        return ln.exact ? by_mode<2, 2, true, true>(ln, a, stream) : by_mode<2, 2, false, true>(ln, a, stream);
+      }
+      *used_lpt = 1;
+      return ln.exact ? by_mode<2, 1, true, true>(ln, a, stream) : by_mode<2, 1, false, true>(ln, a, stream);
+    }
+#endif
     *used_lpt = 1;
     return generic_by_mode<true>(ln, a, stream);
   }

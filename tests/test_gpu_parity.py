@@ -572,3 +572,44 @@ def test_level_ranges_compose_to_the_full_launch(sx, oracle_lib):
     with pytest.raises(ValueError):
         enc.encode_backward(xd, upd, sx.EncoderGradient(enc), levels=(10, 7))
     assert enc.counters().out_of_bounds == 0
+
+
+@pytest.mark.parametrize("n,growth", [(3, 1.5), (2, 2.0)])
+def test_tuned_grid_backend_matches_the_oracle(sx, oracle_lib, n, growth):
+    """gather_grid (src/encoding.cpp:244-285) through the tuned F == 2 kernel (2^n corners in registers, pair-merged
+    reds, coarse-level replicas): corner indices and weights bit-exact, features bit-exact, gradients within the fp32 bar."""
+    cfg = oracle.Config(dim=n, levels=16, table_size=1 << 16, features=2, base_resolution=16, growth=growth, backend=1)
+    tables = oracle_lib.init_tables(cfg, 42)
+    enc = make_encoder(sx, cfg, seed=42)
+    N = 6001
+    x32 = oracle_lib.rng_doubles(99, 1, N * n).reshape(N, n).astype(np.float32)
+    x32[:40] = 1.0             # the far corner of the cube (legal: clamped to nextafter(1, 0) first)
+    x32[40:80, 0] = 0.0
+    x = x32.astype(np.float64)
+    up32 = oracle_lib.rng_doubles(7, 2, N * 32, -1.0, 1.0).astype(np.float32).reshape(N, 32)
+    want, _ = oracle_lib.encode(cfg, tables, x)
+    wg, wt, _ = oracle_lib.encode_backward(cfg, x, up32.astype(np.float64))
+    scale = abs_contrib(oracle_lib, cfg, x, up32.astype(np.float64))
+    xd, upd = dev(x32), dev(up32)
+    idx, w = enc.encode_debug(xd)
+    oi, ow, _, _, _ = oracle_lib.encode_debug(cfg, x)
+    assert np.array_equal(idx, oi) and np.array_equal(w, ow)
+    for lpt in (1, 2):
+        for lm in (0, 1):
+            for rep, merge in ((0, 1), (-1, 1), (0, -1)):
+                enc.set_tuning(sx.Tuning(levels_per_thread=lpt, level_major=lm, coarse_replicas=rep, merge_pairs=merge))
+                tag = (lpt, lm, rep, merge)
+                feats = enc.encode(xd).cpu().numpy()
+                assert np.array_equal(feats.view(np.uint32), want.view(np.uint32)), tag
+                grad = sx.EncoderGradient(enc)
+                enc.encode_backward(xd, upd, grad)
+                vals, tch = grad_dense(grad, cfg)
+                assert np.array_equal(tch, wt), tag
+                assert (np.abs(vals - wg) <= GRAD_RTOL * scale + GRAD_ATOL).all(), tag
+                grad2 = sx.EncoderGradient(enc)
+                feats2 = enc.encode_forward_backward(xd, upd, grad2).cpu().numpy()
+                assert np.array_equal(feats2.view(np.uint32), want.view(np.uint32)), tag
+                vals2, tch2 = grad_dense(grad2, cfg)
+                assert np.array_equal(tch2, wt), tag
+                assert (np.abs(vals2 - wg) <= GRAD_RTOL * scale + GRAD_ATOL).all(), tag
+    enc.check()

@@ -799,10 +799,13 @@ sxen_status sxen_grad_create(const sxen_encoder* enc, sxen_grad** out) {
       int shift = 0;
       while (shift < 6 && verts * static_cast<double>(2u << shift) <= static_cast<double>(1u << 17)) ++shift;
       if (shift < 1) continue;
+      // rows per replica rounded up to even: every replica then starts on a 16-byte boundary (the F == 2 pair merge
+      // issues 16-byte reds); the padding row is never touched and the fold skips it like any untouched row
+      const uint32_t rows = (static_cast<uint32_t>(verts) + 1u) & ~1u;
       g->coarse_shift[static_cast<size_t>(l)] = shift;
-      g->coarse_verts[static_cast<size_t>(l)] = static_cast<uint32_t>(verts);
+      g->coarse_verts[static_cast<size_t>(l)] = rows;
       g->coarse_offset[static_cast<size_t>(l)] = static_cast<uint32_t>(g->coarse_floats);
-      g->coarse_floats += (static_cast<size_t>(verts) << shift) * static_cast<size_t>(g->features);
+      g->coarse_floats += (static_cast<size_t>(rows) << shift) * static_cast<size_t>(g->features);
     }
   }
   if (g->coarse_floats) {

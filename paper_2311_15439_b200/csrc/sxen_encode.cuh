@@ -217,7 +217,7 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
       }
 
       if constexpr (kBwd) {
-        float* __restrict__ gl = a.grads + level_off;
+        float* gl = a.grads + level_off;
         const bool agg = (aggm >> (threadIdx.x & 31)) & 1u;
         // EncoderGradient::add, src/encoding.cpp:110-120: dst[f] += scale * upstream[f]
         float v[V][F];
@@ -229,15 +229,14 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
         }
         // Coarse level: a few thousand hot rows take every sample's atomics and the L2 atomic unit serialises per
         // address (profiles/r1_per_level_n*.log: level 0 costs 4-12x a fine level).  Such levels accumulate into one of
-        // 2^shift dense replicas picked by the sample index; coarse_fold_kernel adds the replicas into the
-        // hashed rows right after this launch.
+        // 2^shift dense replicas picked by the sample index (rows = dense lattice positions instead of hashed rows);
+        // coarse_fold_kernel adds the replicas into the hashed rows right after this launch.
         const int cshift = s_cshift[l];
         if (cshift >= 0) {
           const uint32_t rep = static_cast<uint32_t>(s) & ((1u << cshift) - 1u);
-          float* __restrict__ cb = a.coarse + a.cg.offset[l] + static_cast<size_t>(rep) * a.cg.verts[l] * F;
+          gl = a.coarse + a.cg.offset[l] + static_cast<size_t>(rep) * a.cg.verts[l] * F;
 #pragma unroll
-          for (int k = 0; k < V; ++k) red_row<F>(cb + static_cast<size_t>(dense[k]) * F, v[k]);
-          continue;
+          for (int k = 0; k < V; ++k) idx[k] = dense[k];  // (a step along axis 0 is +1 here too: the pair merge applies)
         }
         bool skip = false;
 #pragma unroll
@@ -419,16 +418,28 @@ __global__ void __launch_bounds__(256) coarse_fold_kernel(const __grid_constant_
   if (e >= static_cast<unsigned long long>(verts) * F) return;
   const uint32_t v = static_cast<uint32_t>(e / F);
   const int f = static_cast<int>(e - static_cast<unsigned long long>(v) * F);
-  float* cb = a.coarse + a.cg.offset[l];
+  float* cb = a.coarse + a.cg.offset[l] + static_cast<size_t>(v) * F + f;
+  const size_t rstride = static_cast<size_t>(verts) * F;
+  const uint32_t reps = 1u << cshift;
   float sum = 0.0f;
   bool any = false;
-  for (uint32_t r = 0; r < (1u << cshift); ++r) {
-    float* p = cb + (static_cast<size_t>(r) * verts + v) * F + f;
-    if (__float_as_uint(__ldcg(p)) == 0x80000000u) continue;
-    const uint32_t old = atomicExch(reinterpret_cast<unsigned int*>(p), 0x80000000u);
-    if (old == 0x80000000u) continue;
-    sum += __uint_as_float(old);
-    any = true;
+  // replicas in batches: all loads of a batch, then all exchanges, are independent and in flight together
+  constexpr uint32_t kBatch = 8;
+  for (uint32_t r0 = 0; r0 < reps; r0 += kBatch) {
+    uint32_t seen[kBatch];
+#pragma unroll
+    for (uint32_t i = 0; i < kBatch; ++i)
+      seen[i] = (r0 + i < reps) ? __float_as_uint(__ldcg(cb + (r0 + i) * rstride)) : 0x80000000u;
+#pragma unroll
+    for (uint32_t i = 0; i < kBatch; ++i)
+      if (seen[i] != 0x80000000u) seen[i] = atomicExch(reinterpret_cast<unsigned int*>(cb + (r0 + i) * rstride), 0x80000000u);
+#pragma unroll
+    for (uint32_t i = 0; i < kBatch; ++i) {
+      if (seen[i] != 0x80000000u) {
+        sum += __uint_as_float(seen[i]);
+        any = true;
+      }
+    }
   }
   if (!any) return;
   const uint32_t side = static_cast<uint32_t>(a.geom.res[l]) + 1u;

@@ -17,13 +17,16 @@ from .trainer import TrainConfig, Trainer, TrainResult, chunk_bounds, level_rang
 from .checkpoint import load_checkpoint, save_checkpoint  # noqa: E402
 from .tasks import FitImageOptions, FitImageResult, fit_image, image_sampler, psnr_from_mse, render_mse  # noqa: E402
 from .rng import CounterRng, hash_combine, mix64  # noqa: E402
+from .analysis import (KernelBenchConfig, KernelBenchReport, bench_kernel, bench_side, read_kernel_csv,  # noqa: E402
+                       write_kernel_csv)
 
 __all__ = ["lib", "CudaError", "IoError", "TrainingError", "Backend", "LevelScale", "EncoderConfig", "HashEncoder",
            "EncoderGradient", "LookupCounters", "Tuning", "equal_memory_multiplier", "level_resolution",
            "skew_constants", "hash_coords", "AdamConfig", "AdamState", "SparseAdamState", "CounterRng", "mix64",
            "hash_combine", "Mlp", "MlpConfig", "TrainConfig", "Trainer", "TrainResult", "chunk_bounds", "level_ranges", "train_field",
            "FitImageOptions", "FitImageResult", "fit_image", "image_sampler", "psnr_from_mse", "render_mse",
-           "save_checkpoint", "load_checkpoint"]
+           "save_checkpoint", "load_checkpoint", "KernelBenchConfig", "KernelBenchReport", "bench_kernel", "bench_side",
+           "read_kernel_csv", "write_kernel_csv"]
 
 
 def device_count() -> int:

@@ -92,3 +92,15 @@ def test_fit_image_validation(sx):
         sx.fit_image(np.full((8, 8, 3), 1.5), cfg, sx.TrainConfig(batch_size=8, steps=1))
     with pytest.raises(ValueError):
         sx.fit_image(np.zeros((8, 8)), cfg, sx.TrainConfig(batch_size=8, steps=1))
+
+
+def test_bench_kernel_protocol(sx):
+    """bench-kernel mirror (src/analysis.cpp:233-313): single level at the largest side^n <= cells, exact touched-vertex
+    instrumentation (n+1 per lookup on the simplex lattice, 2^n on the grid), reps raised until the timer resolves."""
+    for n, backend, verts in ((2, sx.Backend.simplex, 3), (3, sx.Backend.simplex, 4), (3, sx.Backend.grid, 8),
+                              (5, sx.Backend.simplex, 6)):
+        r = sx.bench_kernel(sx.KernelBenchConfig(n=n, cells=1 << 21, samples=1 << 10, reps=3, backend=backend))
+        assert r.n == n and r.backend == backend and r.samples == 1 << 10
+        assert r.cells == sx.bench_side(n, 1 << 21) ** n
+        assert r.vertices_per_sample == float(verts)
+        assert r.reps >= 3 and r.seconds >= 1e-3  # 3 launches of 1024 samples under-resolve: reps were raised

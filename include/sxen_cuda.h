@@ -331,6 +331,29 @@ SXEN_API sxen_status sxen_trainer_step(sxen_trainer* trainer, const void* coords
                                        const sxen_adam_config* table_adam, const sxen_adam_config* mlp_adam,
                                        double* loss_out, void* stream);
 
+/* ------------------------------------------------------------------ noise-field task around the path (src/noise.cpp, src/tasks.cpp:139-194) */
+typedef enum sxen_noise_kind { SXEN_NOISE_PERLIN = 0, SXEN_NOISE_SIMPLEX = 1 } sxen_noise_kind; /* include/sxen/noise.hpp:38 */
+/* sxen::NoiseFieldSpec (include/sxen/noise.hpp:42-50), same defaults through sxen_noise_spec_default. */
+typedef struct sxen_noise_spec {
+  int32_t dim;       /* 1..8 */
+  int32_t kind;      /* sxen_noise_kind */
+  int32_t octaves;   /* >= 1 */
+  int32_t reserved;
+  uint64_t seed;
+  double frequency;  /* lattice cells per unit of input space, > 0 */
+} sxen_noise_spec;
+SXEN_API sxen_status sxen_noise_spec_default(sxen_noise_spec* spec);
+SXEN_API sxen_status sxen_noise_spec_validate(const sxen_noise_spec* spec);  /* NoiseFieldSpec::validate */
+/* noise_field_value (src/noise.cpp:167-188) at n_points points: x_dev n_points x dim f64 -> out_dev n_points f64.
+ * Vertex keys and subdivision order are the reference's; log/cos/sin are CUDA's, so values agree to rounding. */
+SXEN_API sxen_status sxen_noise_field(const sxen_noise_spec* spec, const double* x_dev, size_t n_points, double* out_dev,
+                                      void* stream);
+/* fit_field's batch (src/tasks.cpp:156-166): coords = consecutive next_double() draws of CounterRng(seed, stream_id)
+ * (or CounterRng(seed) when has_stream == 0: the hold-out stream, :173), targets = noise_field_value(coords). */
+SXEN_API sxen_status sxen_sample_field_batch(const sxen_noise_spec* spec, uint64_t seed, int32_t has_stream,
+                                             uint64_t stream_id, size_t n_samples, double* coords_dev,
+                                             double* targets_dev, void* stream);
+
 /* ------------------------------------------------------------------ image-fitting task around the path (src/tasks.cpp) */
 /* fit_image's sampler (src/tasks.cpp:112-126): sample s of step k draws idx = CounterRng(seed, k).next_below(w*h);
  * coords = pixel centre ((idx%w)+0.5)/w, ((idx/w)+0.5)/h; targets = that pixel's RGB.  image_dev: h x w x 3 doubles in

@@ -433,6 +433,10 @@ class Ref:
                                     C.c_int, P(CAdamConfig), P(CAdamConfig), P(dbl), P(dbl), P(C.c_float), P(C.c_float)]
         L.sxr_psnr_from_mse.restype = dbl
         L.sxr_psnr_from_mse.argtypes = [dbl]
+        if hasattr(L, "sxr_noise_field"):  # a libsxen_ref.so built before the noise shim lacks these two
+            L.sxr_noise_field.argtypes = [C.c_int, u64, C.c_int, C.c_int, dbl, P(dbl), C.c_size_t, P(dbl)]
+            L.sxr_fit_field.argtypes = [C.c_int, u64, C.c_int, C.c_int, dbl, P(CConfig), C.c_int, C.c_int, u64, C.c_int, u64,
+                                        C.c_int, C.c_int, C.c_int, P(dbl), P(dbl), P(dbl)]
         L.sxr_save_checkpoint.argtypes = [C.c_char_p, vp, vp]
         L.sxr_load_checkpoint.argtypes = [C.c_char_p, P(CConfig), P(C.c_float), C.c_size_t, P(C.c_int), P(CMlpConfig),
                                           P(C.c_float), C.c_size_t]
@@ -527,6 +531,25 @@ class Ref:
 
     def psnr_from_mse(self, mse: float) -> float:
         return self.lib.sxr_psnr_from_mse(mse)
+
+    def noise_field(self, dim: int, seed: int, kind: int, octaves: int, frequency: float, x) -> np.ndarray:
+        """sxen::noise_field_value (src/noise.cpp:167-188) at every row of x [N, dim]; kind 0 perlin, 1 simplex."""
+        xs = _f64(x)
+        out = np.zeros(xs.shape[0], dtype=np.float64)
+        self._check(self.lib.sxr_noise_field(dim, C.c_uint64(seed), kind, octaves, C.c_double(frequency), _ptr(xs, C.c_double),
+                                             C.c_size_t(xs.shape[0]), _ptr(out, C.c_double)))
+        return out
+
+    def fit_field(self, dim: int, seed: int, kind: int, octaves: int, frequency: float, cfg: Config, batch: int, steps: int,
+                  train_seed: int = 1234, threads: int = 1, init_seed: int = 42, hidden_width: int = 64,
+                  hidden_layers: int = 2, holdout_samples: int = 1 << 14):
+        """sxen::fit_field (src/tasks.cpp:139-194). Returns (loss[steps], holdout_mse, field_variance)."""
+        loss = np.zeros(steps, dtype=np.float64)
+        mse, var = C.c_double(), C.c_double()
+        self._check(self.lib.sxr_fit_field(dim, C.c_uint64(seed), kind, octaves, C.c_double(frequency), C.byref(cfg.c()), batch,
+                                           steps, C.c_uint64(train_seed), threads, C.c_uint64(init_seed), hidden_width,
+                                           hidden_layers, holdout_samples, _ptr(loss, C.c_double), C.byref(mse), C.byref(var)))
+        return loss, mse.value, var.value
 
     def save_checkpoint(self, path: str, encoder: "RefEncoder", mlp: "RefMlp" = None) -> None:
         self._check(self.lib.sxr_save_checkpoint(path.encode(), encoder.h, mlp.h if mlp is not None else None))

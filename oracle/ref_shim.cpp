@@ -23,6 +23,7 @@
 #include "sxen/checkpoint.hpp"
 #include "sxen/image.hpp"
 #include "sxen/rng.hpp"
+#include "sxen/noise.hpp"
 #include "sxen/tasks.hpp"
 #include "sxen/trainer.hpp"
 
@@ -395,6 +396,50 @@ int sxr_fit_image(const double* pixels, int width, int height, const Cfg* cfg, i
 }
 
 double sxr_psnr_from_mse(double mse) { return sxen::psnr_from_mse(mse); }
+
+// ---- noise field + fit_field (src/noise.cpp:167-188, src/tasks.cpp:139-194)
+static sxen::NoiseFieldSpec noise_spec(int dim, std::uint64_t seed, int kind, int octaves, double frequency) {
+  sxen::NoiseFieldSpec spec;
+  spec.dim = dim;
+  spec.seed = seed;
+  spec.kind = kind == 0 ? sxen::NoiseKind::perlin : sxen::NoiseKind::simplex;
+  spec.octaves = octaves;
+  spec.frequency = frequency;
+  return spec;
+}
+
+int sxr_noise_field(int dim, std::uint64_t seed, int kind, int octaves, double frequency, const double* x, std::size_t n,
+                    double* out) {
+  return guarded([&] {
+    const sxen::NoiseFieldSpec spec = noise_spec(dim, seed, kind, octaves, frequency);
+    for (std::size_t s = 0; s < n; ++s)
+      out[s] = sxen::noise_field_value(spec, std::span<const double>(x + s * static_cast<std::size_t>(dim), static_cast<std::size_t>(dim)));
+  });
+}
+
+// Runs the reference's fit_field.  Outputs: per-step loss (record_every = 1), hold-out MSE, field variance.
+int sxr_fit_field(int dim, std::uint64_t seed, int kind, int octaves, double frequency, const Cfg* cfg, int batch, int steps,
+                  std::uint64_t train_seed, int threads, std::uint64_t init_seed, int hidden_width, int hidden_layers,
+                  int holdout_samples, double* loss_out, double* holdout_mse, double* field_variance) {
+  return guarded([&] {
+    const sxen::NoiseFieldSpec spec = noise_spec(dim, seed, kind, octaves, frequency);
+    sxen::TrainConfig tc;
+    tc.batch_size = batch;
+    tc.steps = steps;
+    tc.seed = train_seed;
+    tc.threads = threads;
+    tc.record_every = 1;
+    sxen::FitFieldOptions opt;
+    opt.init_seed = init_seed;
+    opt.mlp_hidden_width = hidden_width;
+    opt.mlp_hidden_layers = hidden_layers;
+    opt.holdout_samples = holdout_samples;
+    sxen::FitFieldResult r = sxen::fit_field(spec, to_ref(*cfg), tc, opt);
+    for (const auto& [step, loss] : r.train.loss_curve) loss_out[step] = loss;
+    *holdout_mse = r.holdout_mse;
+    *field_variance = r.field_variance;
+  });
+}
 
 // ---- checkpoint (src/checkpoint.cpp:81-175); status 9 = IoError
 int sxr_save_checkpoint(const char* path, void* enc, void* mlp) {

@@ -36,6 +36,11 @@ class LookupCountersC(C.Structure):
     _fields_ = [("touched_vertices", C.c_uint64), ("out_of_bounds", C.c_uint64)]
 
 
+class NoiseSpecC(C.Structure):  # sxen_noise_spec
+    _fields_ = [("dim", C.c_int32), ("kind", C.c_int32), ("octaves", C.c_int32), ("reserved", C.c_int32),
+                ("seed", C.c_uint64), ("frequency", C.c_double)]
+
+
 class TuningC(C.Structure):
     _fields_ = [("levels_per_thread", C.c_int32), ("block_threads", C.c_int32), ("level_major", C.c_int32),
                 ("exact_blend", C.c_int32), ("warp_aggregate", C.c_int32), ("merge_pairs", C.c_int32),
@@ -128,6 +133,10 @@ SIGNATURES = {
     "sxen_sample_image_batch": (C.c_int, [_u64, _u64, _vp, _i32, _i32, _sz, _vp, _vp, _vp]),
     "sxen_pixel_centers": (C.c_int, [_i32, _i32, _sz, _sz, _vp, _vp]),
     "sxen_render_sq_error": (C.c_int, [_vp, _vp, _sz, _sz, _vp, _vp]),
+    "sxen_noise_spec_default": (C.c_int, [_P(NoiseSpecC)]),
+    "sxen_noise_spec_validate": (C.c_int, [_P(NoiseSpecC)]),
+    "sxen_noise_field": (C.c_int, [_P(NoiseSpecC), _vp, _sz, _vp, _vp]),
+    "sxen_sample_field_batch": (C.c_int, [_P(NoiseSpecC), C.c_uint64, C.c_int32, C.c_uint64, _sz, _vp, _vp, _vp]),
     "sxen_trainer_create": (C.c_int, [_vp, _vp, _P(_vp)]),
     "sxen_trainer_destroy": (C.c_int, [_vp]),
     "sxen_trainer_accumulate": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, _sz, _sz, _vp]),

@@ -1,0 +1,213 @@
+// sxen_noise.cu -- the procedural target of fit_field on the device (/root/reference/proj/src/noise.cpp): lattice gradients
+// (Box-Muller on the counter RNG, :41-54 with src/rng.cpp:8-19), Perlin gradient noise (:56-97), simplex-lattice gradient
+// noise (:103-157), octave fields (:167-188), and fit_field's batch sampler (src/tasks.cpp:156-166).
+// fp64 throughout, one thread per point.  The integer parts (vertex keys, subdivision order) are the reference's bit for
+// bit; log / cos / sin come from CUDA's libm instead of glibc's, so field values agree to rounding (tests: 1e-12), not
+// to the bit.  A target generator beside the hot path: written for clarity, not speed (dims up to 8 with runtime loops).
+#include "sxen_common.hpp"
+#include "sxen_device.cuh"
+
+using namespace sxen_host;
+
+namespace {
+
+constexpr int kMaxDim = 8;
+constexpr double kTwoPi = 6.283185307179586476925286766559;  // 2.0 * std::numbers::pi rounds to the same double
+
+__device__ __forceinline__ double smoother_step(double t) {  // src/noise.cpp:34-39
+  return t * t * t * (t * (t * 6.0 - 15.0) + 10.0);
+}
+
+// lattice_gradient, src/noise.cpp:41-54.  CounterRng rng(key): key_ = mix64(key), draw i = mix64(key_ + phi * i).
+__device__ void lattice_gradient(const long long* vertex, int n, uint64_t seed, double* out) {
+  uint64_t key = sxen_dev::mix64(seed);
+  for (int i = 0; i < n; ++i) key = sxen_dev::hash_combine(key, static_cast<uint64_t>(vertex[i]));
+  const uint64_t rkey = sxen_dev::mix64(key);
+  uint64_t counter = 0;
+  double norm_sq = 0.0;
+  do {
+    int i = 0;
+    while (i < n) {  // fill_gaussian, src/rng.cpp:8-19
+      const double u1 = 1.0 - sxen_dev::rng_double(rkey, ++counter, 0.0, 1.0);
+      const double u2 = sxen_dev::rng_double(rkey, ++counter, 0.0, 1.0);
+      const double r = sqrt(-2.0 * log(u1));
+      const double a = kTwoPi * u2;
+      out[i++] = r * cos(a);
+      if (i < n) out[i++] = r * sin(a);
+    }
+    norm_sq = 0.0;
+    for (int d = 0; d < n; ++d) norm_sq += out[d] * out[d];
+  } while (norm_sq < 1e-24);
+  const double inv = 1.0 / sqrt(norm_sq);
+  for (int d = 0; d < n; ++d) out[d] *= inv;
+}
+
+__device__ double perlin_value(const double* x, int n, uint64_t seed) {  // src/noise.cpp:56-97
+  long long base[kMaxDim], corner[kMaxDim];
+  double frac[kMaxDim], warped[kMaxDim], grad[kMaxDim];
+  for (int i = 0; i < n; ++i) {
+    const double f = floor(x[i]);
+    base[i] = static_cast<long long>(f);
+    frac[i] = x[i] - f;
+    warped[i] = smoother_step(frac[i]);
+  }
+  double value = 0.0;
+  for (int m = 0; m < (1 << n); ++m) {
+    double weight = 1.0;
+    for (int d = 0; d < n; ++d) {
+      const int bit = (m >> d) & 1;
+      corner[d] = base[d] + bit;
+      weight *= bit ? warped[d] : 1.0 - warped[d];
+    }
+    if (weight == 0.0) continue;
+    lattice_gradient(corner, n, seed, grad);
+    double dot = 0.0;
+    for (int d = 0; d < n; ++d) dot += grad[d] * (frac[d] - static_cast<double>((m >> d) & 1));
+    value += weight * dot;
+  }
+  return value;
+}
+
+__device__ double simplex_noise_value(const double* x, int n, uint64_t seed) {  // src/noise.cpp:103-157
+  const double root = sqrt(static_cast<double>(n) + 1.0);  // SkewConstants::make, src/lattice.cpp:21-30
+  const double skew = (root - 1.0) / static_cast<double>(n);
+  const double unskew = (1.0 - 1.0 / root) / static_cast<double>(n);
+  double y[kMaxDim], frac[kMaxDim], sorted[kMaxDim], grad[kMaxDim], unsk[kMaxDim];
+  long long vertex[kMaxDim];
+  int perm[kMaxDim];
+  double sum = 0.0;
+  for (int i = 0; i < n; ++i) sum += x[i];  // skew_in_place, src/lattice.cpp:40-45
+  const double shift = skew * sum;
+  for (int i = 0; i < n; ++i) {
+    y[i] = x[i] + shift;
+    const double f = floor(y[i]);
+    vertex[i] = static_cast<long long>(f);
+    double fr = y[i] - f;
+    fr = fr < 0.0 ? 0.0 : (sxen_dev::kOneBelow < fr ? sxen_dev::kOneBelow : fr);
+    frac[i] = fr;
+  }
+  // subdivide, src/lattice.cpp:72-103: stable descending insertion sort carrying the axis ids
+  for (int i = 0; i < n; ++i) {
+    const double v = frac[i];
+    int j = i;
+    while (j > 0 && sorted[j - 1] < v) {
+      sorted[j] = sorted[j - 1];
+      perm[j] = perm[j - 1];
+      --j;
+    }
+    sorted[j] = v;
+    perm[j] = i;
+  }
+  double warped[kMaxDim + 1], dots[kMaxDim + 1];
+  double warped_sum = 0.0;
+  for (int k = 0; k <= n; ++k) {
+    if (k > 0) vertex[perm[k - 1]] += 1;
+    double usum = 0.0;
+    for (int i = 0; i < n; ++i) {
+      unsk[i] = static_cast<double>(vertex[i]);
+      usum += unsk[i];
+    }
+    const double ushift = unskew * usum;  // unskew_in_place, src/lattice.cpp:47-52
+    for (int i = 0; i < n; ++i) unsk[i] -= ushift;
+    lattice_gradient(vertex, n, seed, grad);
+    double dot = 0.0;
+    for (int i = 0; i < n; ++i) dot += grad[i] * (x[i] - unsk[i]);
+    dots[k] = dot;
+    // barycentric_weights, src/lattice.cpp:139-147
+    const double w = (k == 0) ? 1.0 - sorted[0] : (k == n ? sorted[n - 1] : sorted[k - 1] - sorted[k]);
+    warped[k] = smoother_step(w);
+    warped_sum += warped[k];
+  }
+  double value = 0.0;
+  for (int k = 0; k <= n; ++k) value += warped[k] / warped_sum * dots[k];
+  return value;
+}
+
+__device__ double noise_field_value(const sxen_noise_spec& spec, const double* x) {  // src/noise.cpp:167-188
+  double scaled[kMaxDim];
+  double value = 0.0, weight = 1.0, weight_sum = 0.0, freq = spec.frequency;
+  for (int o = 0; o < spec.octaves; ++o) {
+    for (int i = 0; i < spec.dim; ++i) scaled[i] = x[i] * freq;
+    const uint64_t octave_seed = sxen_dev::hash_combine(spec.seed, static_cast<uint64_t>(o));
+    value += weight * (spec.kind == SXEN_NOISE_PERLIN ? perlin_value(scaled, spec.dim, octave_seed)
+                                                      : simplex_noise_value(scaled, spec.dim, octave_seed));
+    weight_sum += weight;
+    weight *= 0.5;
+    freq *= 2.0;
+  }
+  return value / weight_sum;
+}
+
+__global__ void __launch_bounds__(128) noise_field_kernel(const sxen_noise_spec spec, const double* __restrict__ x,
+                                                          unsigned long long n, double* __restrict__ out) {
+  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+  for (unsigned long long s = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; s < n; s += stride) {
+    double p[kMaxDim];
+    for (int i = 0; i < spec.dim; ++i) p[i] = x[s * spec.dim + i];
+    out[s] = noise_field_value(spec, p);
+  }
+}
+
+// fit_field's sampler, src/tasks.cpp:156-166: sample s takes draws s*dim+1 .. s*dim+dim of the batch's CounterRng
+__global__ void __launch_bounds__(128) sample_field_kernel(const sxen_noise_spec spec, uint64_t key, unsigned long long n,
+                                                           double* __restrict__ coords, double* __restrict__ targets) {
+  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+  for (unsigned long long s = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; s < n; s += stride) {
+    double p[kMaxDim];
+    for (int i = 0; i < spec.dim; ++i) {
+      p[i] = sxen_dev::rng_double(key, s * spec.dim + i + 1, 0.0, 1.0);
+      coords[s * spec.dim + i] = p[i];
+    }
+    targets[s] = noise_field_value(spec, p);
+  }
+}
+
+int blocks_for(size_t n) {
+  size_t b = (n + 127) / 128;
+  if (b > 148 * 16) b = 148 * 16;
+  return static_cast<int>(b < 1 ? 1 : b);
+}
+
+}  // namespace
+
+extern "C" {
+
+sxen_status sxen_noise_spec_default(sxen_noise_spec* spec) {
+  SXEN_REQUIRE(spec != nullptr, "null argument");
+  *spec = sxen_noise_spec{2, SXEN_NOISE_PERLIN, 1, 0, 7ULL, 4.0};  // include/sxen/noise.hpp:42-48
+  return SXEN_OK;
+}
+
+sxen_status sxen_noise_spec_validate(const sxen_noise_spec* spec) {  // NoiseFieldSpec::validate, src/noise.cpp:157-165
+  SXEN_REQUIRE(spec != nullptr, "null argument");
+  SXEN_REQUIRE(spec->dim >= 1 && spec->dim <= kMaxDim, "noise field: dim must be in [1, %d]", kMaxDim);
+  SXEN_REQUIRE(spec->octaves >= 1, "noise field: octaves must be >= 1");
+  SXEN_REQUIRE(spec->frequency > 0.0 && std::isfinite(spec->frequency), "noise field: frequency must be finite and > 0");
+  SXEN_REQUIRE(spec->kind == SXEN_NOISE_PERLIN || spec->kind == SXEN_NOISE_SIMPLEX, "noise field: unknown kind %d", spec->kind);
+  return SXEN_OK;
+}
+
+sxen_status sxen_noise_field(const sxen_noise_spec* spec, const double* x_dev, size_t n_points, double* out_dev, void* stream) {
+  if (sxen_status st = sxen_noise_spec_validate(spec)) return st;
+  SXEN_REQUIRE(n_points == 0 || (x_dev != nullptr && out_dev != nullptr), "noise_field: null pointer");
+  if (n_points == 0) return SXEN_OK;
+  noise_field_kernel<<<blocks_for(n_points), 128, 0, as_stream(stream)>>>(*spec, x_dev, n_points, out_dev);
+  SXEN_CUDA(cudaGetLastError());
+  count_launch();
+  return SXEN_OK;
+}
+
+sxen_status sxen_sample_field_batch(const sxen_noise_spec* spec, uint64_t seed, int32_t has_stream, uint64_t stream_id,
+                                    size_t n_samples, double* coords_dev, double* targets_dev, void* stream) {
+  if (sxen_status st = sxen_noise_spec_validate(spec)) return st;
+  SXEN_REQUIRE(n_samples == 0 || (coords_dev != nullptr && targets_dev != nullptr), "sample_field_batch: null pointer");
+  if (n_samples == 0) return SXEN_OK;
+  // CounterRng(seed, stream) or CounterRng(seed), include/sxen/rng.hpp:22-29
+  const uint64_t key = has_stream ? sxen_dev::hash_combine(sxen_dev::mix64(seed), stream_id) : sxen_dev::mix64(seed);
+  sample_field_kernel<<<blocks_for(n_samples), 128, 0, as_stream(stream)>>>(*spec, key, n_samples, coords_dev, targets_dev);
+  SXEN_CUDA(cudaGetLastError());
+  count_launch();
+  return SXEN_OK;
+}
+
+}  // extern "C"

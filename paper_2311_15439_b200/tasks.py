@@ -118,3 +118,122 @@ def fit_image(image, encoder_cfg: EncoderConfig, train_cfg: TrainConfig, opt: Fi
     result.psnr_curve = [(s, psnr_from_mse(l)) for s, l in train.loss_curve]
     result.final_psnr = psnr_from_mse(render_mse(encoder, mlp, image_dev, w, h))
     return result
+
+
+# ------------------------------------------------------------------------------------------------ noise-field task
+class NoiseKind:  # include/sxen/noise.hpp:38
+    perlin = 0
+    simplex = 1
+
+
+@dataclass
+class NoiseFieldSpec:  # include/sxen/noise.hpp:42-50, same defaults
+    dim: int = 2
+    seed: int = 7
+    kind: int = NoiseKind.perlin
+    octaves: int = 1
+    frequency: float = 4.0
+
+    def c(self):
+        from . import _abi
+        return _abi.NoiseSpecC(int(self.dim), int(self.kind), int(self.octaves), 0, int(self.seed) & ((1 << 64) - 1),
+                               float(self.frequency))
+
+    def validate(self) -> None:
+        lib = _lib()
+        spec = self.c()
+        raise_for(lib, lib.sxen_noise_spec_validate(C.byref(spec)))
+
+
+def noise_field_value(spec: NoiseFieldSpec, x, device: int = 0):
+    """sxen::noise_field_value (src/noise.cpp:167-188), batched: x [N, dim] float64 (numpy or CUDA tensor) -> [N] float64
+    of the same kind."""
+    import torch
+    lib = _lib()
+    as_numpy = not isinstance(x, torch.Tensor)
+    xd = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64), device=f"cuda:{device}") if as_numpy else x.contiguous()
+    if xd.ndim != 2 or xd.shape[1] != spec.dim:  # src/noise.cpp:169-171
+        raise ValueError("noise field: coordinate count != dim")
+    if xd.dtype != torch.float64:
+        raise ValueError("noise field: coordinates must be float64")
+    if not bool(torch.isfinite(xd).all()):  # check_coords, src/noise.cpp:15-23
+        raise ValueError("noise: coordinates must be finite")
+    out = torch.empty((xd.shape[0],), dtype=torch.float64, device=xd.device)
+    c = spec.c()
+    raise_for(lib, lib.sxen_noise_field(C.byref(c), C.c_void_p(xd.data_ptr()), xd.shape[0], C.c_void_p(out.data_ptr()),
+                                        C.c_void_p(torch.cuda.current_stream(xd.device).cuda_stream)))
+    return out.cpu().numpy() if as_numpy else out
+
+
+def field_sampler(spec: NoiseFieldSpec, seed: int, device: int = 0):
+    """fit_field's BatchSampler (src/tasks.cpp:156-166) evaluated on the device."""
+    import torch
+    lib = _lib()
+    c = spec.c()
+    dev = torch.device(f"cuda:{device}")
+
+    def sampler(step: int, batch: int):
+        coords = torch.empty((batch, spec.dim), dtype=torch.float64, device=dev)
+        targets = torch.empty((batch, 1), dtype=torch.float64, device=dev)
+        raise_for(lib, lib.sxen_sample_field_batch(C.byref(c), seed & ((1 << 64) - 1), 1, step, batch,
+                                                   C.c_void_p(coords.data_ptr()), C.c_void_p(targets.data_ptr()),
+                                                   C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+        return coords, targets
+
+    return sampler
+
+
+@dataclass
+class FitFieldOptions:  # include/sxen/tasks.hpp:49-54
+    init_seed: int = 42
+    mlp_hidden_width: int = 64
+    mlp_hidden_layers: int = 2
+    holdout_samples: int = 1 << 14
+    mlp_precision: int = 0  # as FitImageOptions
+
+
+@dataclass
+class FitFieldResult:  # include/sxen/tasks.hpp:56-62
+    encoder: HashEncoder
+    mlp: Mlp
+    train: TrainResult
+    holdout_mse: float = 0.0
+    field_variance: float = 0.0
+
+
+def fit_field(spec: NoiseFieldSpec, encoder_cfg: EncoderConfig, train_cfg: TrainConfig, opt: FitFieldOptions = None,
+              device: int = 0) -> FitFieldResult:
+    """sxen::fit_field (src/tasks.cpp:139-194): regress the scalar noise field over the unit cube, then evaluate on a
+    hold-out stream training never sees."""
+    import torch
+    opt = opt or FitFieldOptions()
+    spec.validate()
+    if encoder_cfg.dim != spec.dim:
+        raise ValueError(f"fit_field: encoder dim {encoder_cfg.dim} != field dim {spec.dim}")
+    if opt.holdout_samples < 2:
+        raise ValueError("fit_field: holdout_samples must be >= 2")
+    lib = _lib()
+    encoder = HashEncoder(encoder_cfg, device=device)
+    encoder.init_tables(opt.init_seed)
+    mlp = Mlp(MlpConfig(encoder_cfg.encoded_width(), opt.mlp_hidden_width, opt.mlp_hidden_layers, 1), device=device)
+    mlp.init_params(hash_combine(opt.init_seed, 1))
+    if opt.mlp_precision:
+        mlp.set_precision(opt.mlp_precision)
+    train = train_field(encoder, mlp, field_sampler(spec, train_cfg.seed, device), train_cfg)
+    # hold-out: CounterRng(hash_combine(seed, 'HOLD')) without a stream id (src/tasks.cpp:172-173)
+    dev = torch.device(f"cuda:{device}")
+    n = opt.holdout_samples
+    coords = torch.empty((n, spec.dim), dtype=torch.float64, device=dev)
+    targets = torch.empty((n, 1), dtype=torch.float64, device=dev)
+    c = spec.c()
+    raise_for(lib, lib.sxen_sample_field_batch(C.byref(c), hash_combine(train_cfg.seed & ((1 << 64) - 1), 0x484f4c44), 0, 0, n,
+                                               C.c_void_p(coords.data_ptr()), C.c_void_p(targets.data_ptr()),
+                                               C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+    pred = mlp.forward(encoder.encode(coords)).double()
+    encoder.check()
+    t = targets[:, 0]
+    e = pred[:, 0] - t
+    mse = float((e * e).sum().item()) / n
+    mean = float(t.sum().item()) / n
+    var = max(0.0, float((t * t).sum().item()) / n - mean * mean)  # src/tasks.cpp:189-192
+    return FitFieldResult(encoder, mlp, train, holdout_mse=mse, field_variance=var)

@@ -74,3 +74,9 @@ def merge_chain(idx, w):
             out_i.append(i)
             out_w.append(0.0 + wi)
     return out_i, out_w
+
+
+@pytest.fixture(scope="session")
+def golden_fields():
+    """noise_field_value / fit_field outputs of the unmodified reference (tests/golden/make_golden.py fields)."""
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", "field_cases.npz"), allow_pickle=False)

@@ -255,6 +255,38 @@ def neural_cases(ref: Ref):
     print("neural_cases written; loss t1:", d["train_loss_t1"][:3], "...", d["train_loss_t1"][-1])
 
 
+def field_cases(ref: Ref):
+    """noise_field_value and fit_field straight from the reference (src/noise.cpp:167-188, src/tasks.cpp:139-194)."""
+    d = {}
+    names = []
+    rng = np.random.default_rng(11)
+    for dim, kind, octaves, freq, seed in ((2, 0, 1, 4.0, 7), (2, 1, 3, 4.0, 7), (3, 0, 2, 3.0, 19), (3, 1, 1, 5.5, 3),
+                                           (5, 1, 2, 2.0, 7), (1, 0, 1, 4.0, 7), (6, 0, 1, 2.0, 5)):
+        name = f"d{dim}_k{kind}_o{octaves}"
+        x = rng.random((400, dim))
+        x[0] = 0.0
+        x[1] = 1.0
+        x[2] = 0.25  # lattice vertices and cell faces at frequency 4
+        d[f"{name}/spec"] = np.array([dim, kind, octaves, seed], dtype=np.int64)
+        d[f"{name}/freq"] = np.array([freq])
+        d[f"{name}/x"] = x
+        d[f"{name}/value"] = ref.noise_field(dim, seed, kind, octaves, freq, x)
+        names.append(name)
+    d["names"] = np.array(names)
+    # one short fit_field run per noise kind: batch 4096, 20 steps, record_every 1
+    for kind, dim in ((0, 2), (1, 3)):
+        cfg = Config(dim=dim, levels=8, table_size=1 << 14, features=2, base_resolution=4, growth=1.6)
+        loss, mse, var = ref.fit_field(dim, 7, kind, 2, 4.0, cfg, batch=4096, steps=20, train_seed=1234, threads=1,
+                                       init_seed=42, holdout_samples=4096)
+        d[f"fit_k{kind}/loss"] = loss
+        d[f"fit_k{kind}/holdout"] = np.array([mse, var])
+        d[f"fit_k{kind}/cfg"] = np.array([dim, 8, 1 << 14, 2, 4], dtype=np.int64)
+        d[f"fit_k{kind}/growth"] = np.array([1.6])
+        print("fit_field kind", kind, "loss", loss[0], "->", loss[-1], "holdout mse", mse, "variance", var)
+    np.savez_compressed(os.path.join(OUT, "field_cases.npz"), **d)
+    print("field_cases written")
+
+
 def task_cases(ref: Ref):
     """fit_image on the reference's own procedural test image (src/image.cpp:68-96, src/tasks.cpp:98-137)."""
     d = {}
@@ -279,10 +311,14 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "tasks":
         task_cases(ref)
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "fields":
+        field_cases(ref)
+        sys.exit(0)
     scalar_cases(ref)
     encode_cases(ref)
     neural_cases(ref)
     task_cases(ref)
+    field_cases(ref)
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)) // 1024, "KiB")

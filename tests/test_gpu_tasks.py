@@ -104,3 +104,59 @@ def test_bench_kernel_protocol(sx):
         assert r.cells == sx.bench_side(n, 1 << 21) ** n
         assert r.vertices_per_sample == float(verts)
         assert r.reps >= 3 and r.seconds >= 1e-3  # 3 launches of 1024 samples under-resolve: reps were raised
+
+
+def test_noise_field_matches_the_reference(sx, golden_fields):
+    """Device noise_field_value (Perlin and simplex-lattice gradient noise, octaves; src/noise.cpp) against values
+    computed by the reference itself.  Vertex keys, gradients' RNG draws and the subdivision are integer-exact; log/cos/sin
+    are CUDA's instead of glibc's: |d| <= 1e-12 (values are O(1))."""
+    g = golden_fields
+    for name in g["names"].tolist():
+        dim, kind, octaves, seed = (int(v) for v in g[f"{name}/spec"])
+        spec = sx.NoiseFieldSpec(dim=dim, seed=seed, kind=kind, octaves=octaves, frequency=float(g[f"{name}/freq"][0]))
+        got = sx.noise_field_value(spec, g[f"{name}/x"])
+        want = g[f"{name}/value"]
+        assert got.shape == want.shape
+        assert np.abs(got - want).max() <= 1e-12, (name, np.abs(got - want).max())
+        assert np.abs(want).max() > 1e-3  # the fixture is not degenerate
+    # validation mirrors NoiseFieldSpec::validate and noise_field_value's checks
+    for bad in (dict(dim=0), dict(dim=9), dict(octaves=0), dict(frequency=0.0), dict(frequency=float("inf")), dict(kind=5)):
+        with pytest.raises(ValueError):
+            sx.NoiseFieldSpec(**bad).validate()
+    with pytest.raises(ValueError):
+        sx.noise_field_value(sx.NoiseFieldSpec(dim=3), np.zeros((4, 2)))
+    with pytest.raises(ValueError):
+        sx.noise_field_value(sx.NoiseFieldSpec(dim=2), np.array([[0.5, float("nan")]]))
+
+
+def test_field_sampler_draws_the_reference_stream(sx):
+    """fit_field's sampler: sample s of step k holds draws s*dim+1.. of CounterRng(seed, k) (src/tasks.cpp:156-166)."""
+    spec = sx.NoiseFieldSpec(dim=3, kind=sx.NoiseKind.simplex, octaves=2)
+    coords, targets = sx.field_sampler(spec, 1234)(5, 1000)
+    want = torch.empty((1000, 3), dtype=torch.float64, device="cuda:0")
+    sx.CounterRng(1234, 5).fill_device(want)
+    assert torch.equal(coords, want)
+    assert torch.equal(targets[:, 0], sx.noise_field_value(spec, coords))
+
+
+def test_fit_field_tracks_the_reference_run(sx, golden_fields):
+    """fit_field (src/tasks.cpp:139-194), 20 steps at batch 4096 for both noise kinds: loss curve within 1e-3 of the
+    reference's run (same bar as the training-step test), hold-out MSE within 2 %, field variance to 1e-9."""
+    g = golden_fields
+    for kind in (0, 1):
+        dim, levels, T, F, base = (int(v) for v in g[f"fit_k{kind}/cfg"])
+        cfg = sx.EncoderConfig(dim=dim, levels=levels, table_size=T, features=F, base_resolution=base,
+                               growth=float(g[f"fit_k{kind}/growth"][0]))
+        spec = sx.NoiseFieldSpec(dim=dim, seed=7, kind=kind, octaves=2, frequency=4.0)
+        r = sx.fit_field(spec, cfg, sx.TrainConfig(batch_size=4096, steps=20, record_every=1, seed=1234),
+                         sx.FitFieldOptions(holdout_samples=4096))
+        loss = np.array([v for _, v in r.train.loss_curve])
+        want = g[f"fit_k{kind}/loss"]
+        assert np.allclose(loss, want, rtol=1e-3), (kind, np.abs(loss / want - 1).max())
+        mse, var = g[f"fit_k{kind}/holdout"]
+        assert abs(r.holdout_mse / mse - 1) <= 2e-2, (r.holdout_mse, mse)
+        assert abs(r.field_variance - var) <= 1e-9
+    with pytest.raises(ValueError):
+        sx.fit_field(sx.NoiseFieldSpec(dim=3), sx.EncoderConfig(dim=2), sx.TrainConfig(steps=1))
+    with pytest.raises(ValueError):
+        sx.fit_field(sx.NoiseFieldSpec(dim=2), sx.EncoderConfig(dim=2), sx.TrainConfig(steps=1), sx.FitFieldOptions(holdout_samples=1))

@@ -613,3 +613,46 @@ def test_tuned_grid_backend_matches_the_oracle(sx, oracle_lib, n, growth):
                 assert np.array_equal(tch2, wt), tag
                 assert (np.abs(vals2 - wg) <= GRAD_RTOL * scale + GRAD_ATOL).all(), tag
     enc.check()
+
+
+def test_maximum_sizes(sx, oracle_lib):
+    """The reference's limits (src/encoding.cpp:14-15,28-58): 8 dimensions, 64 features, finest resolution 2^26, and the
+    largest table its CLI accepts (2^24 rows, tools/sxen_main.cpp:52-54).  Indices, weights and features bit-exact;
+    the same limits rejected one step further."""
+    # (a) largest table, finest legal resolution: one level at res 2^26 in a 2^24-row table (128 MiB)
+    cfg = oracle.Config(dim=3, levels=1, table_size=1 << 24, features=2, base_resolution=1 << 26, growth=2.0)
+    enc = make_encoder(sx, cfg, seed=5)
+    x = oracle_lib.rng_doubles(3, 1, 3 * 4096).reshape(4096, 3)
+    x[0], x[1] = 0.0, 1.0
+    idx, w = enc.encode_debug(dev(x))
+    oi, ow, _, _, _ = oracle_lib.encode_debug(cfg, x)
+    assert np.array_equal(idx, oi) and np.array_equal(w, ow)
+    assert int(idx.max()) < (1 << 24) and int(idx.max()) > (1 << 23)  # the whole index range is in use
+    want, _ = oracle_lib.encode(cfg, oracle_lib.init_tables(cfg, 5), x)
+    assert np.array_equal(enc.encode(dev(x)).cpu().numpy().view(np.uint32), want.view(np.uint32))
+    grad = sx.EncoderGradient(enc)
+    up = oracle_lib.rng_doubles(4, 2, 2 * 4096, -1.0, 1.0).reshape(4096, 2).astype(np.float32)
+    enc.encode_backward(dev(x), dev(up), grad)
+    wg, wt, _ = oracle_lib.encode_backward(cfg, x, up.astype(np.float64))
+    vals, tch = grad.level(0)
+    assert np.array_equal(tch, wt[0])
+    scale = abs_contrib(oracle_lib, cfg, x, up.astype(np.float64))[0]
+    assert (np.abs(vals - wg[0]) <= GRAD_RTOL * scale + GRAD_ATOL).all()
+    del grad, enc
+    # (b) 8 dimensions x 64 features (generic kernel), both backends
+    for backend in (0, 1):
+        cfg = oracle.Config(dim=8, levels=2, table_size=1 << 12, features=64, base_resolution=3, growth=2.0, backend=backend)
+        enc = make_encoder(sx, cfg, seed=6)
+        x = oracle_lib.rng_doubles(8, 1, 8 * 257).reshape(257, 8)
+        want, _ = oracle_lib.encode(cfg, oracle_lib.init_tables(cfg, 6), x)
+        assert np.array_equal(enc.encode(dev(x)).cpu().numpy().view(np.uint32), want.view(np.uint32)), backend
+        idx, w = enc.encode_debug(dev(x))
+        oi, ow, _, _, _ = oracle_lib.encode_debug(cfg, x)
+        assert np.array_equal(idx, oi) and np.array_equal(w, ow), backend
+    # (c) one step past each limit is rejected exactly as EncoderConfig::validate does
+    for bad in (dict(dim=9), dict(features=65), dict(base_resolution=(1 << 26) + 1), dict(levels=2, base_resolution=1 << 26),
+                dict(table_size=(1 << 12) + 1), dict(dim=0), dict(levels=0), dict(growth=1.0)):
+        kw = dict(dim=3, levels=1, table_size=1 << 12, features=2, base_resolution=16, growth=2.0)
+        kw.update(bad)
+        with pytest.raises(ValueError):
+            sx.HashEncoder(sx.EncoderConfig(**kw))

@@ -204,6 +204,19 @@ class HashEncoder {
                        void* stream = nullptr) const {
     check(sxen_encoder_encode_backward(h_, x.data, SXEN_COORD_F32, upstream.data, batch_of(x.size), grad.handle(), stream));
   }
+  // One contiguous range of levels (multi-GPU hosts all-reduce each range's slice of the accumulator while the next
+  // range computes; include/sxen_cuda.h: sxen_encoder_encode_backward_levels).
+  void encode_backward(DeviceSpan<const float> x, DeviceSpan<const float> upstream, EncoderGradient& grad, int first_level,
+                       int level_count, void* stream = nullptr) const {
+    check(sxen_encoder_encode_backward_levels(h_, x.data, SXEN_COORD_F32, upstream.data, batch_of(x.size), grad.handle(),
+                                              first_level, level_count, stream));
+  }
+  // encode + encode_backward of one batch off a single lattice walk (the run_chunk pair, src/trainer.cpp:31,47).
+  void encode_forward_backward(DeviceSpan<const float> x, DeviceSpan<const float> upstream, DeviceSpan<float> out,
+                               EncoderGradient& grad, void* stream = nullptr) const {
+    check(sxen_encoder_encode_forward_backward(h_, x.data, SXEN_COORD_F32, upstream.data, batch_of(x.size), out.data,
+                                               grad.handle(), stream));
+  }
   void check_async(void* stream = nullptr) const { check(sxen_encoder_check(h_, stream)); }
 
   LookupCounters counters() const {

@@ -237,3 +237,27 @@ def fit_field(spec: NoiseFieldSpec, encoder_cfg: EncoderConfig, train_cfg: Train
     mean = float(t.sum().item()) / n
     var = max(0.0, float((t * t).sum().item()) / n - mean * mean)  # src/tasks.cpp:189-192
     return FitFieldResult(encoder, mlp, train, holdout_mse=mse, field_variance=var)
+
+
+def make_test_image(width: int, height: int, seed: int, device: int = 0) -> np.ndarray:
+    """sxen::make_test_image (src/image.cpp:68-96): the reference's procedural RGB test image -- a shared 4-octave Perlin
+    field plus one 5-octave field per channel at the pixel centres -- evaluated with the device noise kernels.
+    Returns [height, width, 3] float64 in [0, 1]; agrees with the reference's image to rounding (libm), not to the bit."""
+    import torch
+    if width < 1 or height < 1:
+        raise ValueError("test image: width and height must be >= 1")
+    lib = _lib()
+    dev = torch.device(f"cuda:{device}")
+    total = width * height
+    coords = torch.empty((total, 2), dtype=torch.float64, device=dev)
+    raise_for(lib, lib.sxen_pixel_centers(width, height, 0, total, C.c_void_p(coords.data_ptr()),
+                                          C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+    m64 = (1 << 64) - 1
+    shared = NoiseFieldSpec(dim=2, seed=hash_combine(seed & m64, 0xAB), kind=NoiseKind.perlin, octaves=4, frequency=4.0)
+    base = noise_field_value(shared, coords)
+    out = torch.empty((total, 3), dtype=torch.float64, device=dev)
+    for c in range(3):
+        ch = NoiseFieldSpec(dim=2, seed=hash_combine(seed & m64, c + 1), kind=NoiseKind.perlin, octaves=5, frequency=8.0)
+        v = 0.45 * base + 0.55 * noise_field_value(ch, coords)
+        out[:, c] = torch.clamp(0.5 + 0.62 * v, 0.0, 1.0)
+    return out.cpu().numpy().reshape(height, width, 3)

@@ -287,6 +287,27 @@ def field_cases(ref: Ref):
     print("field_cases written")
 
 
+def c1_reference(ref: Ref, steps: int = 30):
+    """BASELINE configs[0] at full size, run by the reference itself (the CPU reference's own run): 2048 x 2048 test image,
+    L=16 F=2 T=2^19, growth (2048/16)^(1/15), batch 2^18.  tools/config_runs.py puts the device fit next to this."""
+    import time
+    W = H = 2048
+    growth = (2048 / 16) ** (1 / 15)
+    cfg = Config(dim=2, levels=16, table_size=1 << 19, features=2, base_resolution=16, growth=growth)
+    threads = max(1, min(os.cpu_count() or 1, 32))
+    t0 = time.time()
+    img = ref.make_test_image(W, H, 7)
+    t_img = time.time() - t0
+    t0 = time.time()
+    psnr, loss, _, _ = ref.fit_image(img, cfg, batch=1 << 18, steps=steps, threads=threads)
+    dt = time.time() - t0
+    np.savez_compressed(os.path.join(OUT, "c1_reference.npz"), loss=loss, final_psnr=np.float64(psnr), steps=np.int64(steps),
+                        threads=np.int64(threads), seconds_incl_final_render=np.float64(dt), image_seconds=np.float64(t_img),
+                        growth=np.float64(growth), image_probe=img[::256, ::256].copy())
+    print("c1_reference written:", steps, "steps on", threads, "threads in", round(dt, 1), "s; loss", loss[0], "->", loss[-1],
+          "final PSNR", psnr)
+
+
 def task_cases(ref: Ref):
     """fit_image on the reference's own procedural test image (src/image.cpp:68-96, src/tasks.cpp:98-137)."""
     d = {}
@@ -311,6 +332,9 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "tasks":
         task_cases(ref)
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "c1":
+        c1_reference(ref)
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "fields":
         field_cases(ref)
         sys.exit(0)
@@ -319,6 +343,7 @@ if __name__ == "__main__":
     neural_cases(ref)
     task_cases(ref)
     field_cases(ref)
+    c1_reference(ref)
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)) // 1024, "KiB")

@@ -160,3 +160,16 @@ def test_fit_field_tracks_the_reference_run(sx, golden_fields):
         sx.fit_field(sx.NoiseFieldSpec(dim=3), sx.EncoderConfig(dim=2), sx.TrainConfig(steps=1))
     with pytest.raises(ValueError):
         sx.fit_field(sx.NoiseFieldSpec(dim=2), sx.EncoderConfig(dim=2), sx.TrainConfig(steps=1), sx.FitFieldOptions(holdout_samples=1))
+
+
+def test_make_test_image_matches_the_reference(sx, golden_task):
+    """The procedural test image (src/image.cpp:68-96) from the device noise kernels against the reference's own image
+    (tests/golden/make_golden.py: ref.make_test_image(64, 64, 7))."""
+    ref_img = golden_task["image"]
+    h, w = ref_img.shape[0], ref_img.shape[1]
+    img = sx.make_test_image(w, h, 7)
+    assert img.shape == ref_img.shape
+    assert np.abs(img - ref_img).max() <= 1e-12
+    assert img.min() >= 0.0 and img.max() <= 1.0 and img.std() > 0.05
+    with pytest.raises(ValueError):
+        sx.make_test_image(0, 4, 7)

@@ -1,9 +1,10 @@
 #!/usr/bin/env python
 """tools/config_runs.py -- the other BASELINE.json configs on one B200 (bench.py stays the contract for configs[1]).
 
-  C1  2D image fitting, synthetic 2048x2048 RGB (the reference's make_test_image(seed 7)), L=16 F=2 T=2^19,
-      2^18 samples/batch: first STEPS steps on the GPU (exact head and tcgen05 head) next to the SAME steps run by
-      the unmodified reference on the host cores (oracle/_ref) -> loss curves side by side + throughput of both.
+  C1  2D image fitting, synthetic 2048x2048 RGB (the reference's make_test_image(seed 7), from the device noise
+      kernels), L=16 F=2 T=2^19, 2^18 samples/batch: first STEPS steps on the GPU (exact head and tcgen05 head) next to
+      the SAME steps as run by the unmodified reference (committed fixture tests/golden/c1_reference.npz)
+      -> loss curves side by side + time of both.
   C3  gigapixel-style 2D fitting at 2^22 samples/step (procedural target evaluated on the device), growth 2.0
   C4  NeRF-style 3D encode + fused 64-wide MLP at 2^24 samples/step
 Prints one JSON object per config."""
@@ -38,42 +39,38 @@ def timed_steps(fn, steps):
 
 # ------------------------------------------------------------------------------------------------ C1
 if not a.skip_c1:
-    import oracle
     W = H = 2048
     growth = (2048 / 16) ** (1 / 15)
     cfg = sx.EncoderConfig(dim=2, levels=16, table_size=1 << 19, features=2, base_resolution=16, growth=growth)
-    ocfg = oracle.Config(dim=2, levels=16, table_size=1 << 19, features=2, base_resolution=16, growth=growth)
     batch = 1 << 18
     res = {"config": "C1 2D image fit 2048x2048, L=16 F=2 T=2^19, batch 2^18", "steps": a.steps}
-    if oracle.Ref.available():
-        ref = oracle.Ref()
-        t0 = time.time()
-        img = ref.make_test_image(W, H, 7)
-        res["image_s"] = time.time() - t0
-        threads = max(1, min(os.cpu_count() or 1, 32))
-        t0 = time.time()
-        psnr_ref, loss_ref, _, _ = ref.fit_image(img, ocfg, batch=batch, steps=a.steps, threads=threads)
-        dt = time.time() - t0
-        res["reference"] = {"threads": threads, "seconds_incl_final_render": dt, "loss_first": loss_ref[0], "loss_last": loss_ref[-1],
-                            "final_psnr": psnr_ref, "loss": [float(v) for v in loss_ref]}
+    t0 = time.time()
+    img = sx.make_test_image(W, H, 7)  # the reference's make_test_image(seed 7) from the device noise kernels
+    res["image_s"] = time.time() - t0
+    # The reference's own run of the same fit is a committed fixture (tests/golden/make_golden.py c1: the unmodified
+    # reference on the host cores of the build container); this tool never executes oracle/.
+    fx = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden", "c1_reference.npz")
+    ref = np.load(fx) if os.path.exists(fx) and a.steps == int(np.load(fx)["steps"]) else None
+    if ref is not None:
+        res["reference"] = {"threads": int(ref["threads"]), "seconds_incl_final_render": float(ref["seconds_incl_final_render"]),
+                            "where": "build container, fixture tests/golden/c1_reference.npz", "loss_first": float(ref["loss"][0]),
+                            "loss_last": float(ref["loss"][-1]), "final_psnr": float(ref["final_psnr"]),
+                            "image_max_abs_diff_on_probe": float(np.abs(img[::256, ::256] - ref["image_probe"]).max())}
     else:
-        rng = np.random.default_rng(7)
-        img = rng.random((H, W, 3))
         res["reference"] = None
     for mode, name in ((0, "exact"), (1, "tcgen05_bf16x3")):
-        t0 = time.time()
-        r = sx.fit_image(img, cfg, sx.TrainConfig(batch_size=batch, steps=a.steps, record_every=1),
-                         sx.FitImageOptions(mlp_precision=mode))
-        dt = time.time() - t0
+        for attempt in range(2):  # the first call of the process carries one-time initialisation; report the second
+            t0 = time.time()
+            r = sx.fit_image(img, cfg, sx.TrainConfig(batch_size=batch, steps=a.steps, record_every=1),
+                             sx.FitImageOptions(mlp_precision=mode))
+            dt = time.time() - t0
         loss = [v for _, v in r.train.loss_curve]
         entry = {"seconds_incl_upload_and_final_render": dt, "loss_first": loss[0], "loss_last": loss[-1], "final_psnr": r.final_psnr}
-        if res.get("reference"):
-            lr = np.array(res["reference"]["loss"])
+        if ref is not None:
+            lr = np.array(ref["loss"])
             entry["max_rel_loss_diff_vs_reference"] = float(np.max(np.abs(np.array(loss) - lr) / lr))
-            entry["psnr_diff_vs_reference_db"] = r.final_psnr - res["reference"]["final_psnr"]
+            entry["psnr_diff_vs_reference_db"] = r.final_psnr - float(ref["final_psnr"])
         res[name] = entry
-    if res.get("reference"):
-        res["reference"].pop("loss")
     print(json.dumps(res), flush=True)
 
 

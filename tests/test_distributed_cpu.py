@@ -89,3 +89,41 @@ def test_level_ranges_cover_every_level_once():
             covered = [l for f, c in r for l in range(f, f + c)]
             assert covered == list(range(levels)), (levels, chunks, r)
             assert all(c >= 1 for _, c in r)
+
+
+def _chunk_worker(rank, world, port, out):
+    """The exchange of Trainer.distributed_step on CPU tensors: the level-major accumulator is all-reduced one level range
+    at a time, asynchronously, while 'the next range computes'; the result must equal one all-reduce of the whole buffer."""
+    from paper_2311_15439_b200.trainer import level_ranges
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    levels, per_level = 16, 64
+    g = torch.Generator().manual_seed(100 + rank)
+    whole = torch.randn(levels * per_level, generator=g)
+    whole[torch.rand(levels * per_level, generator=g) < 0.3] = -0.0  # untouched rows of this rank
+    chunked = whole.clone()
+    dist.all_reduce(whole)
+    pending = []
+    for first, count in level_ranges(levels, 4):
+        sl = chunked[first * per_level:(first + count) * per_level]  # contiguous slice of the level-major buffer
+        pending.append(dist.all_reduce(sl, async_op=True))
+    for w in pending:
+        w.wait()
+    if rank == 0:
+        out.put(bool(torch.equal(whole.view(torch.int32), chunked.view(torch.int32))))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_level_chunked_exchange_equals_the_whole_buffer_allreduce():
+    ctx = mp.get_context("spawn")
+    out = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chunk_worker, args=(r, 2, port, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    assert out.get() is True

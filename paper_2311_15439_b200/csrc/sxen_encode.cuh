@@ -1,11 +1,13 @@
 // sxen_encode.cuh -- the encode / encode_backward kernels (sm_100a).
 //
 // One thread owns one sample and LPT consecutive levels.  For each (sample, level) it walks the simplex once
-// (sxen_device.cuh: simplex_lookup) and then
-//   forward  : gathers the ND+1 table rows (read-only path, one vector load per row) and blends them,
-//   backward : scatter-adds weight * upstream into the gradient rows with one vector `red.global.add` per row,
+// (sxen_device.cuh: simplex_lookup; grid_lookup for the grid backend's 2^ND corners) and then
+//   forward  : gathers the vertex rows (read-only path, one vector load per row) and blends them,
+//   backward : scatter-adds weight * upstream into the gradient rows with one vector `red.global.add` per row -- one
+//              red.v4 for the two rows of an axis-0 pair; coarse levels go to replicated dense accumulators that
+//              coarse_fold_kernel adds into the hashed rows before the call returns,
 //   both     : does the two off the same lattice walk (the fused fwd+bwd kernel).
-// HBM-bound integer/gather work: no tensor cores here by design.
+// Memory-system-bound integer/gather work (L2 tag lookups): no tensor cores here by design.
 // Reference semantics: HashEncoder::encode / encode_backward, /root/reference/proj/src/encoding.cpp:295-335.
 #pragma once
 

@@ -193,6 +193,41 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def quick_dim(sx, torch, dev, device_index, n, t_log2, steps=12):
+    """Fused encode fwd+bwd samples/s at another input dimension, same workload shape as the headline line."""
+    N, LF = 1 << BATCH_LOG2, L * F
+    cfg = sx.EncoderConfig(dim=n, levels=L, table_size=1 << t_log2, features=F, base_resolution=BASE, growth=GROWTH[n])
+    enc = sx.HashEncoder(cfg, device=device_index)
+    enc.init_tables(42)
+    grad = sx.EncoderGradient(enc)
+    sets = []
+    for i in range(4):
+        x = torch.empty((N, n), dtype=torch.float32, device=dev)
+        r = sx.CounterRng(99, 1)
+        r.counter = i * N * n
+        r.fill_device(x)
+        up = torch.empty((N, LF), dtype=torch.float32, device=dev)
+        r2 = sx.CounterRng(7, 2)
+        r2.counter = i * N * LF
+        r2.fill_device(up, -1e-3, 1e-3)
+        sets.append((x, up, torch.empty((N, LF), dtype=torch.float32, device=dev)))
+    stream = torch.cuda.current_stream()
+    for i in range(3):
+        enc.encode_forward_backward(sets[i % 4][0], sets[i % 4][1], grad, out=sets[i % 4][2])
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(steps):
+        enc.encode_forward_backward(sets[i % 4][0], sets[i % 4][1], grad, out=sets[i % 4][2])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    enc.check()
+    ms = e0.elapsed_time(e1) / steps
+    peak, _ = hbm_peak()
+    return {"workload": workload_name(n, t_log2), "value": N / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "steps": steps,
+            "roofline_frac": alg_bytes(n, "fused") * N / (ms * 1e-3) / 1e9 / peak, "alg_bytes_per_sample": alg_bytes(n, "fused")}
+
+
 # ---------------------------------------------------------------------------------------------- our arm
 def run_ours(args):
     import torch
@@ -431,6 +466,15 @@ def run_ours(args):
             except Exception as exc:  # the GPU numbers stand on their own; say why the baseline is missing
                 cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": str(exc)}
 
+        # ---- extra (not the headline): the metric's other dimension (BASELINE.json quotes n = 2 and 3) on the same
+        # protocol -- fused launch, rotating inputs, CUDA events -- with fewer steps
+        other = None
+        if not args.no_train and world == 1 and n == 3 and args.backend == "simplex" and args.log2t == T_LOG2:
+            try:
+                other = {"n2": quick_dim(sx, torch, dev, local_rank, 2, args.log2t)}
+            except Exception as exc:
+                other = {"error": str(exc)}
+
         # ---- extra (not the headline): the whole training step with the tcgen05 head on the same batch shape
         train = None
         if not args.no_train and n in (2, 3) and args.backend == "simplex":
@@ -477,7 +521,7 @@ def run_ours(args):
                                      f"{len(ranges)} level chunks overlapped with the next chunk's kernel")
                                     if exchange else "single GPU"},
             "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu,
-            "train_step": train,
+            "train_step": train, "other_dims": other,
         }
     if dist is not None:
         dist.barrier()

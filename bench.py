@@ -458,7 +458,7 @@ def run_ours(args):
         if world == 1 and not args.no_cpu and args.backend == "simplex":
             try:
                 threads = host_threads()
-                samples = min(1 << 18, threads << 15)
+                samples = min(1 << BATCH_LOG2, threads << 16)  # the whole 2^20 batch on >= 16 threads: ~25 core-seconds
                 v, kind = cpu_reference_run(n, samples, threads, args.log2t)
                 cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
                        "sample": f"{samples} samples of the same workload (same RNG streams), reference worker pattern: "

@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(256) k(const float* __restrict__ tab, float* _
   uint32_t gid = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t s = gid / (L / LPT), g = gid % (L / LPT);
   if (s >= n) return;
-  float4 u = *reinterpret_cast<const float4*>(up + (size_t)s * 32 + g * 4);
+  float4 u = __ldcs(reinterpret_cast<const float4*>(up + (size_t)s * 32 + g * 4));
   float o[4];
 #pragma unroll
   for (int j = 0; j < LPT; ++j) {
@@ -74,6 +74,17 @@ __global__ void __launch_bounds__(256) k(const float* __restrict__ tab, float* _
         float* p = grd + ((size_t)l * T + idx[v]) * 2;
         asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(0.25f * ux), "f"(0.25f * uy) : "memory");
       }
+    } else if (MODE == 6) {  // interleaved [t0 t1 g0 g1] rows: 8-byte gather of the table half + red.v2 on the gradient half
+      float2 e[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) e[v] = __ldg(reinterpret_cast<const float2*>(tg + ((size_t)l * T + idx[v]) * 4));
+#pragma unroll
+      for (int v = 0; v < V; ++v) { a0 += 0.25f * e[v].x; a1 += 0.25f * e[v].y; }
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        float* p = tg + ((size_t)l * T + idx[v]) * 4 + 2;
+        asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(0.25f * ux), "f"(0.25f * uy) : "memory");
+      }
     } else if (MODE == 5) {  // atom.v2 with return on grads only (return-path cost at 8 bytes)
       float2 e[V];
 #pragma unroll
@@ -86,7 +97,7 @@ __global__ void __launch_bounds__(256) k(const float* __restrict__ tab, float* _
     }
     o[j * 2] = a0; o[j * 2 + 1] = a1;
   }
-  *reinterpret_cast<float4*>(out + (size_t)s * 32 + g * 4) = make_float4(o[0], o[1], o[2], o[3]);
+  __stcs(reinterpret_cast<float4*>(out + (size_t)s * 32 + g * 4), make_float4(o[0], o[1], o[2], o[3]));
 }
 
 int main() {
@@ -97,9 +108,9 @@ int main() {
   for (int i = 0; i < 4; ++i) { cudaMalloc(&up[i], (size_t)n * 128); cudaMalloc(&out[i], (size_t)n * 128); cudaMemset(up[i], 0, (size_t)n * 128); }
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   const char* names[] = {"gather + red.v2 (separate arrays)", "atom.v4 with return (interleaved)", "red.v4 no return (interleaved)",
-                         "gather only", "red.v2 only", "atom.v2 with return (grads only)"};
+                         "gather only", "red.v2 only", "atom.v2 with return (grads only)", "gather + red.v2, interleaved [t|g] rows"};
   dim3 grid(n * (L / LPT) / 256), block(256);
-  for (int m = 0; m < 6; ++m) {
+  for (int m = 0; m < 7; ++m) {
     for (int rep = 0; rep < 15; ++rep) {
       if (rep == 3) cudaEventRecord(a);
       int i = rep % 4;
@@ -110,6 +121,7 @@ int main() {
         case 3: k<3><<<grid, block>>>(tab, grd, tg, up[i], out[i], n); break;
         case 4: k<4><<<grid, block>>>(tab, grd, tg, up[i], out[i], n); break;
         case 5: k<5><<<grid, block>>>(tab, grd, tg, up[i], out[i], n); break;
+        case 6: k<6><<<grid, block>>>(tab, grd, tg, up[i], out[i], n); break;
       }
     }
     cudaEventRecord(b); cudaEventSynchronize(b);

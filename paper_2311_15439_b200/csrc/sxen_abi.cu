@@ -246,6 +246,17 @@ sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, c
   }
   if (n == 0 || level_count == 0) return SXEN_OK;
   DeviceGuard guard(enc->device);
+  {
+    // Tables + accumulator far beyond L2 (>= 192 MiB of tables) and the launch shape left to the library: the fused call
+    // runs as a forward launch followed by a backward launch, each level-major -- one level group's rows of ONE array
+    // stay L2-resident, where the fused kernel would need two (measured at T = 2^22, n = 3: 1.17 -> 0.84 ms).
+    const size_t bytes = static_cast<size_t>(enc->cfg.levels) * enc->level_floats() * sizeof(float);
+    if (mode == sxen_dev::kModeBoth && bytes >= (192ull << 20) && enc->tuning.level_major < 0) {
+      if (sxen_status st = run_encode(enc, x, type, nullptr, n, out, nullptr, sxen_dev::kModeFwd, stream, first_level, level_count))
+        return st;
+      return run_encode(enc, x, type, upstream, n, nullptr, grad, sxen_dev::kModeBwd, stream, first_level, level_count);
+    }
+  }
   EncodeArgs a;
   base_args(enc, x, type, n, a);
   a.upstream = upstream;

@@ -170,7 +170,9 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
       bool oob;
       if constexpr (GRID) oob = grid_lookup<ND, kBwd>(x, s_scale[l], s_res[l], a.mask, idx, w, dense);
       else oob = simplex_lookup<ND, kBwd>(x, s_scale[l], a.skew, s_res[l], a.mask, idx, w, dense);
-      if (oob) atomicAdd(a.status + 1, 1ULL);
+      // LookupCounters::out_of_bounds: the reference bumps it in encode AND in encode_backward (src/encoding.cpp:222,241),
+      // so the fused walk counts for both
+      if (oob) atomicAdd(a.status + 1, (kFwd && kBwd) ? 2ULL : 1ULL);
       const size_t level_off = static_cast<size_t>(a.level0 + l) * a.level_stride;
 
       if constexpr (kFwd) {

@@ -656,3 +656,44 @@ def test_maximum_sizes(sx, oracle_lib):
         kw.update(bad)
         with pytest.raises(ValueError):
             sx.HashEncoder(sx.EncoderConfig(**kw))
+
+
+def test_fused_call_counts_and_big_table_split(sx, oracle_lib):
+    """(a) The fused walk stands for the reference's encode + encode_backward pair, counters included: touched and
+    out-of-bounds both count twice.  (b) With tables beyond L2 and the launch shape left to the library, the fused entry
+    point runs as a forward plus a backward launch: same features (bit-exact), same gradients."""
+    cfg = oracle.Config(dim=5, levels=3, table_size=1 << 12, features=2, base_resolution=3, growth=2.0)
+    enc = make_encoder(sx, cfg, seed=1)
+    x = np.ones((64, 5))  # the far corner: the reference clamps some cells there at n = 5 (golden small_b0_n5)
+    up = np.ones((64, 6), dtype=np.float32)
+    enc.reset_counters()
+    enc.encode(dev(x))
+    once = enc.counters()
+    enc.reset_counters()
+    enc.encode_forward_backward(dev(x), dev(up), sx.EncoderGradient(enc))
+    both = enc.counters()
+    assert both.touched_vertices == 2 * once.touched_vertices
+    assert both.out_of_bounds == 2 * once.out_of_bounds
+    # (b) 2^22-row tables, 12 levels = 384 MiB: the library's auto path splits the fused call
+    cfg = oracle.Config(dim=3, levels=12, table_size=1 << 22, features=2, base_resolution=16, growth=1.5)
+    enc = make_encoder(sx, cfg, seed=42)
+    N = 50000
+    x32 = oracle_lib.rng_doubles(99, 1, N * 3).reshape(N, 3).astype(np.float32)
+    up32 = oracle_lib.rng_doubles(7, 2, N * 24, -1.0, 1.0).astype(np.float32).reshape(N, 24)
+    launches = sx.launch_count()
+    g_auto = sx.EncoderGradient(enc)
+    f_auto = enc.encode_forward_backward(dev(x32), dev(up32), g_auto)
+    auto_launches = sx.launch_count() - launches
+    enc.set_tuning(sx.Tuning(level_major=0))
+    launches = sx.launch_count()
+    g_fused = sx.EncoderGradient(enc)
+    f_fused = enc.encode_forward_backward(dev(x32), dev(up32), g_fused)
+    fused_launches = sx.launch_count() - launches
+    assert auto_launches == fused_launches + 1  # (grad creation launches are equal on both sides)
+    assert torch.equal(f_auto, f_fused)
+    sub = slice(0, 4096)
+    want, _ = oracle_lib.encode(cfg, oracle_lib.init_tables(cfg, 42), x32[sub].astype(np.float64))
+    assert np.array_equal(f_auto[sub].cpu().numpy().view(np.uint32), want.view(np.uint32))
+    assert g_auto.touched_total() == g_fused.touched_total()
+    d = (g_auto.device_view() - g_fused.device_view()).abs().max().item()
+    assert d <= 1e-5

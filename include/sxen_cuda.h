@@ -91,11 +91,12 @@ typedef struct sxen_lookup_counters {
 
 /* Launch-shape knobs of the encode kernels (no reference analogue; 0 = library default). */
 typedef struct sxen_tuning {
-  int32_t levels_per_thread; /* 1,2,4,8,16: levels one thread walks */
+  int32_t levels_per_thread; /* 1,2,4,16: levels one thread walks; 0 (default) = chosen with the launch shape below */
   int32_t block_threads;     /* CTA size, multiple of 32 */
   int32_t level_major;       /* 0: consecutive threads walk one sample's level groups (coalesced rows);
                                 1: grid.y = level group, all samples of a group before the next (L2-resident tables);
-                                -1 (default): chosen from the table footprint (level-major once tables >= 192 MiB) */
+                                -1 (default): chosen from the table footprint (level-major once tables exceed 96 MiB,
+                                i.e. tables + accumulator no longer fit L2 side by side) */
   int32_t exact_blend;       /* 1: fp64 chain-order blend, features bit-identical to the reference; 0: fp32 FMA blend */
   int32_t warp_aggregate;    /* backward: merge equal rows inside a warp before the atomic on levels whose
                                 lattice has at most this many vertices (0 = off) */

@@ -83,7 +83,7 @@ sxen_status validate(const sxen_encoder_config& c) {
 
 sxen_tuning default_tuning() {
   sxen_tuning t{};
-  t.levels_per_thread = 2;
+  t.levels_per_thread = 0;  // auto
   t.block_threads = 256;
   t.level_major = -1;  // auto
   t.exact_blend = 1;
@@ -262,11 +262,16 @@ sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, c
   a.upstream = upstream;
   a.out = out;
   a.grads = grad ? grad->values : nullptr;
-  // level_major < 0 = auto: once the tables alone outgrow L2 (>= 192 MiB) walk one level group at a time so that group's
-  // rows stay L2-resident (measured at T=2^22: fused 1.89 -> 1.18 ms, profiles/r1_sweep_n3_T22.log)
+  // Launch shape left to the library (level_major < 0, levels_per_thread == 0), by table footprint B = L*T*F*4 bytes
+  // (tables and accumulator are the same size; L2 is 126 MB):
+  //   B <= 96 MiB   sample-major, 2 levels per thread: a warp writes whole feature rows, everything stays near L2
+  //   B <  192 MiB  level-major, 4 levels per thread: one level group's rows at a time stay L2-resident
+  //                 (T = 2^20, n = 3: fused 1.07 -> 0.54 ms)
+  //   B >= 192 MiB  level-major, 2 levels per thread, and the fused call runs as forward + backward launches (above)
   const size_t table_bytes = static_cast<size_t>(enc->cfg.levels) * enc->level_floats() * sizeof(float);
   const bool big = table_bytes >= (192ull << 20);
-  a.level_major = enc->tuning.level_major < 0 ? (big ? 1 : 0) : (enc->tuning.level_major ? 1 : 0);
+  const bool mid = !big && table_bytes > (96ull << 20);
+  a.level_major = enc->tuning.level_major < 0 ? ((big || mid) ? 1 : 0) : (enc->tuning.level_major ? 1 : 0);
   a.merge_pairs = (enc->tuning.merge_pairs > 0 && enc->cfg.table_size >= 2) ? 1 : 0;
   // L2 eviction policies (profiles/r1_cache_hints.log).  Tables + gradients within reach of L2: the fused launch marks
   // its gradient lines evict_first so the table lines (cached on both dies) survive; beyond L2: gathers and reds both
@@ -276,7 +281,8 @@ sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, c
                         : (mode == sxen_dev::kModeBoth ? 8 : 0);
   EncodeLaunch ln{};
   ln.features = enc->cfg.features;
-  ln.lpt = enc->tuning.levels_per_thread;
+  ln.lpt = enc->tuning.levels_per_thread > 0 ? enc->tuning.levels_per_thread
+                                             : ((mid && enc->tuning.level_major < 0) ? 4 : 2);
   ln.mode = mode;
   ln.exact = enc->tuning.exact_blend ? 1 : 0;
   ln.grid_backend = enc->cfg.backend == SXEN_BACKEND_GRID ? 1 : 0;
@@ -537,7 +543,7 @@ sxen_status sxen_encoder_set_tuning(sxen_encoder* enc, const sxen_tuning* t) {
   SXEN_REQUIRE(enc != nullptr && t != nullptr, "null argument");
   sxen_tuning d = default_tuning();
   sxen_tuning n = *t;
-  if (n.levels_per_thread <= 0) n.levels_per_thread = d.levels_per_thread;
+  if (n.levels_per_thread < 0) n.levels_per_thread = d.levels_per_thread;
   if (n.block_threads <= 0) n.block_threads = d.block_threads;
   SXEN_REQUIRE(n.block_threads % 32 == 0 && n.block_threads <= 1024, "block_threads must be a multiple of 32, <= 1024");
   SXEN_REQUIRE(n.warp_aggregate >= 0, "warp_aggregate must be >= 0");

@@ -10,6 +10,8 @@ import paper_2311_15439_b200 as sx  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 log2t = int(sys.argv[2]) if len(sys.argv) > 2 else 19
+lpt = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+lm = int(sys.argv[4]) if len(sys.argv) > 4 else -1
 N = 1 << 20
 growth = 2.0 if n == 2 else 1.5
 cfg = sx.EncoderConfig(dim=n, levels=16, table_size=1 << log2t, features=2, base_resolution=16, growth=growth)
@@ -23,9 +25,9 @@ for i in range(4):
     up = torch.empty((N, 32), dtype=torch.float32, device="cuda")
     r = sx.CounterRng(7, 2); r.counter = i * N * 32; r.fill_device(up, -1e-3, 1e-3)
     xs.append(x); ups.append(up); outs.append(torch.empty((N, 32), dtype=torch.float32, device="cuda"))
-print(f"# n={n} T=2^{log2t}; hints = gather policy + 4 * red policy (0 none, 1 evict_last, 2 evict_first, 3 evict_unchanged)\nhints  fwd_us  bwd_us  fused_us")
+print(f"# n={n} T=2^{log2t} lpt={lpt} level_major={lm}; hints = gather policy + 4 * red policy (0 none, 1 evict_last, 2 evict_first, 3 evict_unchanged)\nhints  fwd_us  bwd_us  fused_us")
 for h in range(16):
-    enc.set_tuning(sx.Tuning(levels_per_thread=2, cache_hints=h))
+    enc.set_tuning(sx.Tuning(levels_per_thread=lpt, level_major=lm, cache_hints=h))
     res_t = []
     for which in ("fwd", "bwd", "fused"):
         fn = {"fwd": lambda i: enc.encode(xs[i % 4], out=outs[i % 4]), "bwd": lambda i: enc.encode_backward(xs[i % 4], ups[i % 4], grad),

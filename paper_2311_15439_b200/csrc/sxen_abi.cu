@@ -265,14 +265,14 @@ sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, c
   // Launch shape left to the library (level_major < 0, levels_per_thread == 0), by table footprint B = L*T*F*4 bytes
   // (tables and accumulator are the same size; L2 is 126 MB):
   //   B <= 96 MiB   sample-major, 2 levels per thread: a warp writes whole feature rows, everything stays near L2
-  //                 (dim <= 3 only: with 5+ vertices per level the fused sample-major kernel loses to the next shape,
-  //                 n = 4: 0.93 vs 0.66 ms)
+  //                 (fused launches at dim >= 4 take the next shape instead: n = 4, 0.93 vs 0.66 ms; separate forward /
+  //                 backward launches stay sample-major, 0.69 ms the pair)
   //   B <  192 MiB  level-major, 4 levels per thread: one level group's rows at a time stay L2-resident
   //                 (T = 2^20, n = 3: fused 1.07 -> 0.54 ms)
   //   B >= 192 MiB  level-major, 2 levels per thread, and the fused call runs as forward + backward launches (above)
   const size_t table_bytes = static_cast<size_t>(enc->cfg.levels) * enc->level_floats() * sizeof(float);
   const bool big = table_bytes >= (192ull << 20);
-  const bool mid = !big && (table_bytes > (96ull << 20) || enc->cfg.dim >= 4);
+  const bool mid = !big && (table_bytes > (96ull << 20) || (enc->cfg.dim >= 4 && mode == sxen_dev::kModeBoth));
   a.level_major = enc->tuning.level_major < 0 ? ((big || mid) ? 1 : 0) : (enc->tuning.level_major ? 1 : 0);
   a.merge_pairs = (enc->tuning.merge_pairs > 0 && enc->cfg.table_size >= 2) ? 1 : 0;
   // L2 eviction policies (profiles/r1_cache_hints.log).  Tables + gradients within reach of L2: the fused launch marks

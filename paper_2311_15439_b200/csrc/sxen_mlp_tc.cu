@@ -128,21 +128,24 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 constexpr int kSplit = 2;                       // epilogue threads per sample row: each handles HID/kSplit columns
 constexpr int CPT = HID / kSplit;               // columns per thread in a hidden-layer epilogue (multiple of 16)
 constexpr int kEpiThreads = kTile * kSplit;     // 8 epilogue warps (kSplit = 4 / 16 warps measured slower: 0.585 vs 0.47 ms)
-constexpr int kThreadsAll = kEpiThreads + 32;   // + one MMA-issuing warp
+constexpr int kThreadsAll = kEpiThreads + 64;   // + the chain-MMA warp + the weight-gradient-MMA warp
 
 template <bool TRAIN>
 __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_constant__ TcArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t bar_ready;  // 256 arrivals: the tiles of the next phase are written and the TMEM scratch is drained
   __shared__ uint64_t bar;        // dependent-chain MMAs of the current phase have completed
-  __shared__ uint64_t bar_g;      // every MMA of the tile (weight-gradient ones included) has completed
+  __shared__ uint64_t bar_g;      // every weight-gradient MMA of the tile has completed
+  __shared__ uint64_t bar_w;      // chain warp -> weight-gradient warp: the operands of backward phase 2 / 3 are in place
   __shared__ uint32_t tmem_base_slot;
   __shared__ double red_buf[kEpiThreads / 32][4];
   const int tid = threadIdx.x;
   const int t = tid & (kTile - 1);   // sample row inside the tile
   const int half = (tid >> 7) & (kSplit - 1);  // which slice of an epilogue's columns this thread handles
   const int warp = tid >> 5;
-  const bool is_mma_warp = warp == kEpiThreads / 32;
+  const bool is_mma_warp = warp == kEpiThreads / 32;        // issues the four dependent-chain GEMMs of every tile
+  const bool is_wgrad_warp = warp == kEpiThreads / 32 + 1;  // issues the three weight-gradient GEMMs (TRAIN)
+  const bool is_epi = tid < kEpiThreads;
   float* bias = reinterpret_cast<float*>(smem + kBias);
   const float* W0 = a.params;
   const float* b0 = W0 + HID * IN;
@@ -158,7 +161,7 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
                      loDH = cm16_bytes(kTile, HID);
 
   // ---- one-time setup: weights (hi/lo CM16 tiles, rows = output unit, cols = input unit), biases, ones columns
-  if (!is_mma_warp) {
+  if (is_epi) {
     for (int e = tid; e < HID * IN / 8; e += kEpiThreads) {
       const int o = e / (IN / 8), ch = e % (IN / 8);
       float v[8];
@@ -192,6 +195,7 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
     mbar_init(&bar_ready, kEpiThreads);
     mbar_init(&bar, 1);
     mbar_init(&bar_g, 1);
+    mbar_init(&bar_w, 1);
   }
   if (warp == 0) tmem_alloc(&tmem_base_slot, kTmemCols);
   fence_proxy_async();
@@ -224,6 +228,7 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
           mbar_wait(&bar_ready, ph);
           ph ^= 1;
           tc_fence_after();
+          if (p >= 2) mbar_arrive(&bar_w);  // hand the phase to the weight-gradient warp (its private two-phase barrier)
           switch (p) {
             case 0:  // layer 1: S0 = X0 * W0^T
               gemm_split(tb + tS0, make_idesc_bf16(128, HID, false, false), IN / 16, false, precise, kX0d, loX0, kStep, kW0d, loW0, kStep);
@@ -233,24 +238,48 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
               gemm_split(tb + tS1, make_idesc_bf16(128, HID, false, false), HID / 16, false, precise, kH1d, loH, kStep, kW1d, loW1, kStep);
               tc_commit(&bar);
               break;
-            case 2:  // S1 = dH2 * W1;  G2 += H2^T * dY (dW2^T);  G1 += dH2^T * [H1 | 1]
+            case 2:  // S1 = dH2 * W1
               gemm_split(tb + tS1, make_idesc_bf16(128, HID, false, true), HID / 16, false, precise, kDH2d, loDH, kStep, mW1d, loW1,
                          2 * cm16_row_group_stride(HID));
               tc_commit(&bar);
+              break;
+            default:  // S0[:, 0:32] = dH1 * W0 (d loss / d encoding)
+              gemm_split(tb + tS0, make_idesc_bf16(128, IN, false, true), HID / 16, false, precise, kDH1d, loDH, kStep, mW0d, loW0,
+                         2 * cm16_row_group_stride(IN));
+              tc_commit(&bar);
+              break;
+          }
+        }
+      }
+    }
+  } else if (is_wgrad_warp) {
+    // ============ weight-gradient warp: its own lane issues G2, G1 (phase 2) and G0 (phase 3) of every tile ============
+    // A single issuing thread spends ~35 cycles per tcgen05.mma; the 72 weight-gradient MMAs of a tile would otherwise
+    // sit in front of the next phase's chain MMAs in that thread's program order.  Issued from here they reach the tensor
+    // pipe whenever this lane gets to them, and tcgen05.commit on bar_g tracks exactly this thread's MMAs.
+    if constexpr (TRAIN) {
+      if ((tid & 31) == 0) {
+        const uint32_t sX0 = smem_u32(smem + kX0), sH1 = smem_u32(smem + kH1), sH2 = smem_u32(smem + kH2);
+        const uint32_t sDY = smem_u32(smem + kDY), sDH2 = smem_u32(smem + kDH2), sDH1 = smem_u32(smem + kDH1);
+        const uint64_t mX0d = desc16_mn_major(sX0, X0C, 0), mH1d = desc16_mn_major(sH1, HC, 0), mH2d = desc16_mn_major(sH2, HC, 0);
+        const uint64_t mDYd = desc16_mn_major(sDY, OUTP, 0), mDH2d = desc16_mn_major(sDH2, HID, 0), mDH1d = desc16_mn_major(sDH1, HID, 0);
+        uint32_t phw = 0;
+        for (unsigned long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+          for (int p = 2; p < kPhases; ++p) {
+            mbar_wait(&bar_w, phw);  // the chain warp has seen this phase's operands
+            phw ^= 1;
+            tc_fence_after();
+            if (p == 2) {  // G2 += H2^T * dY (dW2^T);  G1 += dH2^T * [H1 | 1]
               gemm_split(tb + tG2, make_idesc_bf16(64, OUTP, true, true), kTile / 16, g_started, precise, mH2d, loH,
                          2 * cm16_row_group_stride(HC), mDYd, loDY, 2 * cm16_row_group_stride(OUTP));
               gemm_split(tb + tG1, make_idesc_bf16(64, HC, true, true), kTile / 16, g_started, precise, mDH2d, loDH,
                          2 * cm16_row_group_stride(HID), mH1d, loH, 2 * cm16_row_group_stride(HC));
-              break;
-            default:  // S0[:, 0:32] = dH1 * W0 (d loss / d encoding);  G0 += dH1^T * [X0 | 1]
-              gemm_split(tb + tS0, make_idesc_bf16(128, IN, false, true), HID / 16, false, precise, kDH1d, loDH, kStep, mW0d, loW0,
-                         2 * cm16_row_group_stride(IN));
-              tc_commit(&bar);
+            } else {       // G0 += dH1^T * [X0 | 1]
               gemm_split(tb + tG0, make_idesc_bf16(64, X0C, true, true), kTile / 16, g_started, precise, mDH1d, loDH,
                          2 * cm16_row_group_stride(HID), mX0d, loX0, 2 * cm16_row_group_stride(X0C));
               tc_commit(&bar_g);  // covers G2, G1 and G0 of this tile
               g_started = true;
-              break;
+            }
           }
         }
       }

@@ -288,6 +288,15 @@ class Mlp {
     const sxen_mlp_config cc = cfg.c();
     check(sxen_mlp_create(&cc, device, &h_));
   }
+  Mlp(Mlp&& o) noexcept : cfg_(o.cfg_), h_(std::exchange(o.h_, nullptr)) {}  // movable, not copyable (include/sxen/mlp.hpp)
+  Mlp& operator=(Mlp&& o) noexcept {
+    if (this != &o) {
+      sxen_mlp_destroy(h_);
+      cfg_ = o.cfg_;
+      h_ = std::exchange(o.h_, nullptr);
+    }
+    return *this;
+  }
   Mlp(const Mlp&) = delete;
   Mlp& operator=(const Mlp&) = delete;
   ~Mlp() { sxen_mlp_destroy(h_); }

@@ -127,6 +127,13 @@ SXEN_API uint64_t sxen_launch_count(void);
 /* Pinned host memory for callers of the *_host entry points (pageable memory works too, but copies then serialise). */
 SXEN_API sxen_status sxen_host_alloc(size_t bytes, void** out);
 SXEN_API sxen_status sxen_host_free(void* ptr);
+/* Device buffers for a host that does not link the CUDA runtime itself (the C++ trainer/tasks mirror,
+ * include/sxen_b200_train.hpp): plain cudaMalloc / cudaFree / cudaMemcpyAsync + stream sync / cudaMemsetAsync. */
+SXEN_API sxen_status sxen_device_alloc(int32_t device, size_t bytes, void** out_dev);
+SXEN_API sxen_status sxen_device_free(int32_t device, void* ptr_dev);
+SXEN_API sxen_status sxen_device_upload(int32_t device, void* dst_dev, const void* src_host, size_t bytes, void* stream);
+SXEN_API sxen_status sxen_device_download(int32_t device, void* dst_host, const void* src_dev, size_t bytes, void* stream);
+SXEN_API sxen_status sxen_device_zero(int32_t device, void* dst_dev, size_t bytes, void* stream);
 
 /* ------------------------------------------------------------------ rng (include/sxen/rng.hpp:9-54), host-side */
 SXEN_API uint64_t sxen_mix64(uint64_t z);
@@ -331,6 +338,23 @@ SXEN_API sxen_status sxen_trainer_step(sxen_trainer* trainer, const void* coords
                                        const void* targets_dev, sxen_coord_type target_type, size_t n_samples,
                                        const sxen_adam_config* table_adam, const sxen_adam_config* mlp_adam,
                                        double* loss_out, void* stream);
+
+/* train_field's loop body (src/trainer.cpp:94-136) WITHOUT a host round trip per step: queues the whole step
+ * -- gradient pass, loss = sum/(B*out_w) into the step's slot of a device ring, both Adam updates -- and returns.  The
+ * reference throws TrainingError before the optimizer steps when the loss is non-finite (:121-123); here the update
+ * kernels of that and every later queued step return without writing (a device-side gate), and sxen_trainer_collect
+ * reports it.  At most 4096 steps may be queued between two collects (SXEN_LOGIC_ERROR beyond).  One stream per trainer. */
+SXEN_API sxen_status sxen_trainer_step_enqueue(sxen_trainer* trainer, const void* coords_dev, sxen_coord_type coord_type,
+                                               const void* targets_dev, sxen_coord_type target_type, size_t n_samples,
+                                               const sxen_adam_config* table_adam, const sxen_adam_config* mlp_adam,
+                                               void* stream);
+SXEN_API sxen_status sxen_trainer_pending(const sxen_trainer* trainer, size_t* out);
+/* Synchronises the stream and returns the losses of the steps queued since the last collect, in order (*count_out of
+ * them; capacity must hold them).  SXEN_TRAINING_ERROR when one was non-finite: *failed_out = its index in losses_out
+ * (else -1), losses before it are valid, tables / MLP / moments are as they were before that step.  Also reports the
+ * encoder's rejected-sample word and non-finite gradients like sxen_trainer_step. */
+SXEN_API sxen_status sxen_trainer_collect(sxen_trainer* trainer, double* losses_out, size_t capacity, size_t* count_out,
+                                          int64_t* failed_out, void* stream);
 
 /* ------------------------------------------------------------------ noise-field task around the path (src/noise.cpp, src/tasks.cpp:139-194) */
 typedef enum sxen_noise_kind { SXEN_NOISE_PERLIN = 0, SXEN_NOISE_SIMPLEX = 1 } sxen_noise_kind; /* include/sxen/noise.hpp:38 */

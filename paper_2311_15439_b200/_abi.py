@@ -148,6 +148,14 @@ SIGNATURES = {
     "sxen_trainer_update": (C.c_int, [_vp, _P(AdamConfigC), _P(AdamConfigC), _vp]),
     "sxen_trainer_check": (C.c_int, [_vp, _vp]),
     "sxen_trainer_step": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, _sz, _P(AdamConfigC), _P(AdamConfigC), _P(_dbl), _vp]),
+    "sxen_trainer_step_enqueue": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, _sz, _P(AdamConfigC), _P(AdamConfigC), _vp]),
+    "sxen_device_alloc": (C.c_int, [_i32, _sz, _P(_vp)]),
+    "sxen_device_free": (C.c_int, [_i32, _vp]),
+    "sxen_device_upload": (C.c_int, [_i32, _vp, _vp, _sz, _vp]),
+    "sxen_device_download": (C.c_int, [_i32, _vp, _vp, _sz, _vp]),
+    "sxen_device_zero": (C.c_int, [_i32, _vp, _sz, _vp]),
+    "sxen_trainer_pending": (C.c_int, [_vp, _P(_sz)]),
+    "sxen_trainer_collect": (C.c_int, [_vp, _P(_dbl), _sz, _P(_sz), _P(C.c_int64), _vp]),
 }
 
 

@@ -393,6 +393,47 @@ sxen_status sxen_host_free(void* ptr) {
   return SXEN_OK;
 }
 
+sxen_status sxen_device_alloc(int32_t device, size_t bytes, void** out_dev) {
+  SXEN_REQUIRE(out_dev != nullptr, "output pointer is null");
+  *out_dev = nullptr;
+  int ndev = 0;
+  SXEN_CUDA(cudaGetDeviceCount(&ndev));
+  SXEN_REQUIRE(device >= 0 && device < ndev, "device %d out of range (%d visible)", device, ndev);
+  DeviceGuard guard(device);
+  SXEN_CUDA(cudaMalloc(out_dev, bytes ? bytes : 1));
+  return SXEN_OK;
+}
+
+sxen_status sxen_device_free(int32_t device, void* ptr_dev) {
+  if (!ptr_dev) return SXEN_OK;
+  DeviceGuard guard(device);
+  SXEN_CUDA(cudaFree(ptr_dev));
+  return SXEN_OK;
+}
+
+sxen_status sxen_device_upload(int32_t device, void* dst_dev, const void* src_host, size_t bytes, void* stream) {
+  SXEN_REQUIRE(bytes == 0 || (dst_dev != nullptr && src_host != nullptr), "null argument");
+  DeviceGuard guard(device);
+  SXEN_CUDA(cudaMemcpyAsync(dst_dev, src_host, bytes, cudaMemcpyHostToDevice, as_stream(stream)));
+  SXEN_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  return SXEN_OK;
+}
+
+sxen_status sxen_device_download(int32_t device, void* dst_host, const void* src_dev, size_t bytes, void* stream) {
+  SXEN_REQUIRE(bytes == 0 || (dst_host != nullptr && src_dev != nullptr), "null argument");
+  DeviceGuard guard(device);
+  SXEN_CUDA(cudaMemcpyAsync(dst_host, src_dev, bytes, cudaMemcpyDeviceToHost, as_stream(stream)));
+  SXEN_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  return SXEN_OK;
+}
+
+sxen_status sxen_device_zero(int32_t device, void* dst_dev, size_t bytes, void* stream) {
+  SXEN_REQUIRE(bytes == 0 || dst_dev != nullptr, "null argument");
+  DeviceGuard guard(device);
+  SXEN_CUDA(cudaMemsetAsync(dst_dev, 0, bytes, as_stream(stream)));
+  return SXEN_OK;
+}
+
 // ---------------------------------------------------------------------------------------------- rng
 uint64_t sxen_mix64(uint64_t z) { return sxen_dev::mix64(z); }
 uint64_t sxen_hash_combine(uint64_t a, uint64_t b) { return sxen_dev::hash_combine(a, b); }

@@ -111,3 +111,11 @@ struct sxen_adam {
   unsigned long long* status = nullptr;
   unsigned long long* status_host = nullptr;
 };
+
+// Update steps of a QUEUED training step (sxen_trainer_step_enqueue): the kernels return at once when *gate_dev holds a
+// slot index (that step's loss was non-finite: the reference throws before updating, src/trainer.cpp:121-123).
+// gate_dev == nullptr: the public sxen_sparse_adam_step / sxen_adam_step.
+sxen_status sxen_sparse_adam_step_gated(sxen_sparse_adam* opt, sxen_encoder* enc, sxen_grad* grad, const sxen_adam_config* cfg,
+                                        int32_t clear_grad, const unsigned long long* gate_dev, void* stream);
+sxen_status sxen_adam_step_gated(sxen_adam* opt, float* params_dev, const void* grads_dev, sxen_coord_type grad_type,
+                                 size_t size, const sxen_adam_config* cfg, const unsigned long long* gate_dev, void* stream);

@@ -31,7 +31,8 @@ __device__ __forceinline__ double adam_delta(double g, double& m, double& v, con
 // touched it (feature 0 != -0.0f), zero gradients included; untouched rows' moments do not decay.
 __global__ void sparse_adam_kernel(float* __restrict__ tables, float* __restrict__ grads, double* __restrict__ m,
                                    double* __restrict__ v, size_t rows, int features, AdamScalars c, int clear_grad,
-                                   unsigned long long* __restrict__ status) {
+                                   unsigned long long* __restrict__ status, const unsigned long long* __restrict__ gate) {
+  if (gate != nullptr && *gate != kNoBad) return;  // a queued step whose loss was non-finite applies no update
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   for (size_t r = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < rows; r += stride) {
     const size_t base = r * static_cast<size_t>(features);
@@ -56,7 +57,8 @@ __global__ void sparse_adam_kernel(float* __restrict__ tables, float* __restrict
 // F == 2 fast path: 8-byte gradient/table rows, 16-byte moment rows, one vector access each.
 __global__ void sparse_adam_f2_kernel(float2* __restrict__ tables, float2* __restrict__ grads, double2* __restrict__ m,
                                       double2* __restrict__ v, size_t rows, AdamScalars c, int clear_grad,
-                                      unsigned long long* __restrict__ status) {
+                                      unsigned long long* __restrict__ status, const unsigned long long* __restrict__ gate) {
+  if (gate != nullptr && *gate != kNoBad) return;
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   for (size_t r = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < rows; r += stride) {
     const float2 g2 = grads[r];
@@ -83,7 +85,8 @@ __global__ void sparse_adam_f2_kernel(float2* __restrict__ tables, float2* __res
 template <typename G>
 __global__ void dense_adam_kernel(float* __restrict__ params, const G* __restrict__ grads, double* __restrict__ m,
                                   double* __restrict__ v, size_t n, AdamScalars c,
-                                  unsigned long long* __restrict__ status) {
+                                  unsigned long long* __restrict__ status, const unsigned long long* __restrict__ gate) {
+  if (gate != nullptr && *gate != kNoBad) return;
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     const double g = static_cast<double>(grads[i]);
@@ -196,6 +199,13 @@ sxen_status sxen_sparse_adam_step_count(const sxen_sparse_adam* opt, int64_t* ou
 
 sxen_status sxen_sparse_adam_step(sxen_sparse_adam* opt, sxen_encoder* enc, sxen_grad* grad, const sxen_adam_config* cfg,
                                   int32_t clear_grad, void* stream) {
+  return sxen_sparse_adam_step_gated(opt, enc, grad, cfg, clear_grad, nullptr, stream);
+}
+
+}  // extern "C"
+
+sxen_status sxen_sparse_adam_step_gated(sxen_sparse_adam* opt, sxen_encoder* enc, sxen_grad* grad, const sxen_adam_config* cfg,
+                                        int32_t clear_grad, const unsigned long long* gate_dev, void* stream) {
   SXEN_REQUIRE(opt != nullptr && enc != nullptr && grad != nullptr && cfg != nullptr, "null argument");
   // src/optimizer.cpp:57-61
   SXEN_REQUIRE(enc->cfg.levels == opt->levels && enc->cfg.features == opt->features &&
@@ -210,15 +220,17 @@ sxen_status sxen_sparse_adam_step(sxen_sparse_adam* opt, sxen_encoder* enc, sxen
   if (opt->features == 2) {
     sparse_adam_f2_kernel<<<grid_for(rows), 256, 0, as_stream(stream)>>>(
         reinterpret_cast<float2*>(enc->tables), reinterpret_cast<float2*>(grad->values),
-        reinterpret_cast<double2*>(opt->m), reinterpret_cast<double2*>(opt->v), rows, c, clear_grad, opt->status);
+        reinterpret_cast<double2*>(opt->m), reinterpret_cast<double2*>(opt->v), rows, c, clear_grad, opt->status, gate_dev);
   } else {
     sparse_adam_kernel<<<grid_for(rows), 256, 0, as_stream(stream)>>>(enc->tables, grad->values, opt->m, opt->v, rows,
-                                                                      opt->features, c, clear_grad, opt->status);
+                                                                      opt->features, c, clear_grad, opt->status, gate_dev);
   }
   SXEN_CUDA(cudaGetLastError());
   count_launch();
   return SXEN_OK;
 }
+
+extern "C" {
 
 sxen_status sxen_sparse_adam_check(sxen_sparse_adam* opt, void* stream) {
   SXEN_REQUIRE(opt != nullptr, "optimizer handle is null");
@@ -282,6 +294,13 @@ sxen_status sxen_adam_step_count(const sxen_adam* opt, int64_t* out) {
 
 sxen_status sxen_adam_step(sxen_adam* opt, float* params_dev, const void* grads_dev, sxen_coord_type grad_type,
                            size_t size, const sxen_adam_config* cfg, void* stream) {
+  return sxen_adam_step_gated(opt, params_dev, grads_dev, grad_type, size, cfg, nullptr, stream);
+}
+
+}  // extern "C"
+
+sxen_status sxen_adam_step_gated(sxen_adam* opt, float* params_dev, const void* grads_dev, sxen_coord_type grad_type,
+                                 size_t size, const sxen_adam_config* cfg, const unsigned long long* gate_dev, void* stream) {
   SXEN_REQUIRE(opt != nullptr && cfg != nullptr, "null argument");
   // src/optimizer.cpp:27-29
   SXEN_REQUIRE(size == opt->size, "adam step: parameter/gradient size mismatch");
@@ -292,15 +311,17 @@ sxen_status sxen_adam_step(sxen_adam* opt, float* params_dev, const void* grads_
   const AdamScalars c = scalars(*cfg, opt->t);
   if (grad_type == SXEN_COORD_F32) {
     dense_adam_kernel<float><<<grid_for(size), 256, 0, as_stream(stream)>>>(
-        params_dev, static_cast<const float*>(grads_dev), opt->m, opt->v, size, c, opt->status);
+        params_dev, static_cast<const float*>(grads_dev), opt->m, opt->v, size, c, opt->status, gate_dev);
   } else {
     dense_adam_kernel<double><<<grid_for(size), 256, 0, as_stream(stream)>>>(
-        params_dev, static_cast<const double*>(grads_dev), opt->m, opt->v, size, c, opt->status);
+        params_dev, static_cast<const double*>(grads_dev), opt->m, opt->v, size, c, opt->status, gate_dev);
   }
   SXEN_CUDA(cudaGetLastError());
   count_launch();
   return SXEN_OK;
 }
+
+extern "C" {
 
 sxen_status sxen_adam_check(sxen_adam* opt, void* stream) {
   SXEN_REQUIRE(opt != nullptr, "optimizer handle is null");

@@ -25,11 +25,31 @@ struct sxen_trainer {
   double* sample_loss = nullptr; // N
   double* loss_sum = nullptr;    // device scalar: sum of per-sample losses accumulated since the last update
   double* loss_host = nullptr;   // pinned
+  // queued steps (sxen_trainer_step_enqueue / _collect): one loss per step, read back by the collect call
+  double* loss_ring = nullptr;       // device, kLossRing slots
+  double* loss_ring_host = nullptr;  // pinned mirror
+  unsigned long long* gate = nullptr;       // device: slot of the first queued step whose loss was non-finite, else ~0
+  unsigned long long* gate_host = nullptr;  // pinned
+  size_t pending = 0;                // queued steps not collected yet
   int32_t out_w = 0, enc_w = 0;
   uint64_t mlp_params = 0;
 };
 
 namespace {
+
+constexpr size_t kLossRing = 4096;
+constexpr unsigned long long kNoFailure = ~0ULL;
+
+// The loss half of train_field's step (src/trainer.cpp:118-123) for a queued step: loss = sum / (B * out_w) goes to the
+// step's slot, a non-finite loss closes the gate (the update kernels of this and every later queued step then return
+// without touching anything, as the reference throws before its optimizer steps), and the sum is re-armed.
+__global__ void loss_record_kernel(double* __restrict__ loss_sum, double* __restrict__ ring, unsigned long long slot,
+                                   double denom, unsigned long long* __restrict__ gate) {
+  const double loss = __ddiv_rn(*loss_sum, denom);
+  ring[slot] = loss;
+  if (!isfinite(loss)) atomicMin(gate, slot);
+  *loss_sum = 0.0;
+}
 
 sxen_status ensure_workspace(sxen_trainer* t, size_t n) {
   if (n <= t->capacity) return SXEN_OK;
@@ -77,6 +97,13 @@ sxen_status sxen_trainer_create(sxen_encoder* enc, sxen_mlp* mlp, sxen_trainer**
   if (st == SXEN_OK && cudaMemset(t->loss_sum, 0, sizeof(double)) != cudaSuccess) st = fail(SXEN_CUDA_ERROR, "trainer: memset failed");
   if (st == SXEN_OK && cudaHostAlloc(&t->loss_host, sizeof(double), cudaHostAllocDefault) != cudaSuccess)
     st = fail(SXEN_CUDA_ERROR, "trainer: pinned allocation failed");
+  if (st == SXEN_OK && (cudaMalloc(&t->loss_ring, kLossRing * sizeof(double)) != cudaSuccess ||
+                        cudaMalloc(&t->gate, sizeof(unsigned long long)) != cudaSuccess ||
+                        cudaMemset(t->gate, 0xff, sizeof(unsigned long long)) != cudaSuccess))
+    st = fail(SXEN_CUDA_ERROR, "trainer: allocation failed");
+  if (st == SXEN_OK && (cudaHostAlloc(&t->loss_ring_host, kLossRing * sizeof(double), cudaHostAllocDefault) != cudaSuccess ||
+                        cudaHostAlloc(&t->gate_host, sizeof(unsigned long long), cudaHostAllocDefault) != cudaSuccess))
+    st = fail(SXEN_CUDA_ERROR, "trainer: pinned allocation failed");
   if (st != SXEN_OK) {
     sxen_trainer_destroy(t);
     return st;
@@ -97,6 +124,10 @@ sxen_status sxen_trainer_destroy(sxen_trainer* t) {
   cudaFree(t->sample_loss);
   cudaFree(t->loss_sum);
   cudaFreeHost(t->loss_host);
+  cudaFree(t->loss_ring);
+  cudaFree(t->gate);
+  cudaFreeHost(t->loss_ring_host);
+  cudaFreeHost(t->gate_host);
   delete t;
   return SXEN_OK;
 }
@@ -204,6 +235,71 @@ sxen_status sxen_trainer_step(sxen_trainer* t, const void* coords_dev, sxen_coor
   if (loss_out) *loss_out = loss;
   if (loss_st != SXEN_OK) return loss_st;  // the reference throws before updating (src/trainer.cpp:121-123)
   if (sxen_status st = sxen_trainer_update(t, table_adam, mlp_adam, stream)) return st;
+  return sxen_trainer_check(t, stream);
+}
+
+sxen_status sxen_trainer_step_enqueue(sxen_trainer* t, const void* coords_dev, sxen_coord_type coord_type,
+                                      const void* targets_dev, sxen_coord_type target_type, size_t n_samples,
+                                      const sxen_adam_config* table_adam, const sxen_adam_config* mlp_adam, void* stream) {
+  SXEN_REQUIRE(t != nullptr && table_adam != nullptr && mlp_adam != nullptr, "null argument");
+  SXEN_REQUIRE(n_samples >= 1, "train: batch_size must be >= 1");  // src/trainer.cpp:57
+  if (t->pending >= kLossRing)
+    return fail(SXEN_LOGIC_ERROR, "train: %zu queued steps not collected (sxen_trainer_collect first)", t->pending);
+  if (sxen_status st = sxen_trainer_accumulate(t, coords_dev, coord_type, targets_dev, target_type, n_samples, n_samples, stream))
+    return st;
+  DeviceGuard guard(t->device);
+  cudaStream_t s = as_stream(stream);
+  loss_record_kernel<<<1, 1, 0, s>>>(t->loss_sum, t->loss_ring, static_cast<unsigned long long>(t->pending),
+                                     static_cast<double>(n_samples) * static_cast<double>(t->out_w), t->gate);
+  SXEN_CUDA(cudaGetLastError());
+  count_launch();
+  ++t->pending;
+  // table_opt.step, mlp_opt.step (src/trainer.cpp:129-130), skipped on the device when the gate is closed
+  if (sxen_status st = sxen_sparse_adam_step_gated(t->table_opt, t->enc, t->grad, table_adam, 1, t->gate, stream)) return st;
+  double* mg = nullptr;
+  float* mp = nullptr;
+  sxen_mlp_grads_dev(t->mlp, &mg);
+  sxen_mlp_params_dev(t->mlp, &mp);
+  if (sxen_status st = sxen_adam_step_gated(t->mlp_opt, mp, mg, SXEN_COORD_F64, static_cast<size_t>(t->mlp_params), mlp_adam,
+                                            t->gate, stream))
+    return st;
+  return sxen_mlp_grad_clear(t->mlp, stream);
+}
+
+sxen_status sxen_trainer_pending(const sxen_trainer* t, size_t* out) {
+  SXEN_REQUIRE(t != nullptr && out != nullptr, "null argument");
+  *out = t->pending;
+  return SXEN_OK;
+}
+
+sxen_status sxen_trainer_collect(sxen_trainer* t, double* losses_out, size_t capacity, size_t* count_out,
+                                 int64_t* failed_out, void* stream) {
+  SXEN_REQUIRE(t != nullptr && count_out != nullptr, "null argument");
+  SXEN_REQUIRE(capacity >= t->pending && (losses_out != nullptr || t->pending == 0),
+               "train: %zu queued losses do not fit the caller's buffer (%zu)", t->pending, capacity);
+  DeviceGuard guard(t->device);
+  cudaStream_t s = as_stream(stream);
+  const size_t n = t->pending;
+  *count_out = n;
+  if (failed_out) *failed_out = -1;
+  if (n == 0) return SXEN_OK;
+  SXEN_CUDA(cudaMemcpyAsync(t->loss_ring_host, t->loss_ring, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  SXEN_CUDA(cudaMemcpyAsync(t->gate_host, t->gate, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  SXEN_CUDA(cudaStreamSynchronize(s));
+  t->pending = 0;
+  for (size_t i = 0; i < n; ++i) losses_out[i] = t->loss_ring_host[i];
+  if (*t->gate_host != kNoFailure) {
+    const unsigned long long bad = *t->gate_host;
+    SXEN_CUDA(cudaMemsetAsync(t->gate, 0xff, sizeof(unsigned long long), s));
+    // the gated steps left their gradients in the accumulators (the reference's are in the same state when it throws,
+    // and it drops them with the aborted run): clear them so the handle can go on from the last applied step
+    if (sxen_status st = sxen_grad_clear(t->grad, stream)) return st;
+    if (sxen_status st = sxen_mlp_grad_clear(t->mlp, stream)) return st;
+    SXEN_CUDA(cudaStreamSynchronize(s));
+    if (failed_out) *failed_out = static_cast<int64_t>(bad);
+    return fail(SXEN_TRAINING_ERROR, "loss became non-finite (queued step %llu of %zu)", bad, n);
+  }
+  if (sxen_status st = sxen_encoder_check(t->enc, stream)) return st;
   return sxen_trainer_check(t, stream);
 }
 

@@ -132,6 +132,36 @@ class Trainer:
             self._typ(targets), coords.shape[0], C.byref(ta), C.byref(ma), C.byref(out), _stream_ptr(stream)))
         return out.value
 
+    def step_enqueue(self, coords, targets, table_adam: AdamConfig, mlp_adam: AdamConfig, stream=None) -> None:
+        """Queues one whole step (gradient pass, loss into the device ring, both updates) without waiting for it;
+        ``collect`` returns the losses.  A non-finite loss stops every later update on the device."""
+        from .encoding import _stream_ptr
+        coords, targets = coords.contiguous(), targets.contiguous()
+        ta, ma = table_adam.c(), mlp_adam.c()
+        raise_for(self._lib, self._lib.sxen_trainer_step_enqueue(
+            self._h, C.c_void_p(coords.data_ptr()), self._typ(coords), C.c_void_p(targets.data_ptr()),
+            self._typ(targets), coords.shape[0], C.byref(ta), C.byref(ma), _stream_ptr(stream)))
+
+    def pending(self) -> int:
+        n = C.c_size_t()
+        raise_for(self._lib, self._lib.sxen_trainer_pending(self._h, C.byref(n)))
+        return n.value
+
+    def collect(self, stream=None):
+        """(losses, failed): the losses of the steps queued since the last collect; ``failed`` is the index of the
+        first non-finite one (the updates from that step on were not applied) or -1.  Rejected samples and non-finite
+        gradients raise like ``step``."""
+        from . import _abi
+        from .encoding import _stream_ptr
+        n = self.pending()
+        buf = (C.c_double * max(n, 1))()
+        cnt, failed = C.c_size_t(), C.c_int64(-1)
+        st = self._lib.sxen_trainer_collect(self._h, buf, n, C.byref(cnt), C.byref(failed), _stream_ptr(stream))
+        if st == _abi.TRAINING_ERROR and failed.value >= 0:
+            return list(buf[:cnt.value]), failed.value
+        raise_for(self._lib, st)
+        return list(buf[:cnt.value]), -1
+
     def distributed_step(self, coords, targets, table_adam: AdamConfig, mlp_adam: AdamConfig, group=None,
                          level_chunks: int = 4) -> float:
         """Batch-sharded step: coords/targets hold the WHOLE batch on every rank (the sampler is deterministic in
@@ -185,6 +215,8 @@ def level_ranges(levels: int, chunks: int):
     return [(f, min(per, levels - f)) for f in range(0, levels, per)]
 
 
+QUEUE_WINDOW = 256  # queued steps between two loss read-backs in train_field (the ring holds 4096)
+
 BatchSampler = Callable[[int, int], tuple]  # (step, batch) -> (coords [B, dim], targets [B, out_w]) CUDA tensors
 
 
@@ -211,16 +243,29 @@ def train_field(encoder, mlp, sampler: BatchSampler, cfg: TrainConfig, group=Non
         except Exception:
             distributed = False
     result = TrainResult()
-    for step in range(cfg.steps):
-        coords, targets = sampler(step, cfg.batch_size)
-        if distributed:
-            loss = trainer.distributed_step(coords, targets, cfg.table_adam, cfg.mlp_adam, group)
-        else:
-            loss = trainer.step(coords, targets, cfg.table_adam, cfg.mlp_adam)
+
+    def record(step: int, loss: float) -> None:
         if not math.isfinite(loss):
             raise TrainingError(f"loss became non-finite at step {step}")
         if step % cfg.record_every == 0 or step == cfg.steps - 1:
             result.loss_curve.append((step, loss))
         result.final_loss = loss
+
+    if distributed:
+        for step in range(cfg.steps):
+            coords, targets = sampler(step, cfg.batch_size)
+            record(step, trainer.distributed_step(coords, targets, cfg.table_adam, cfg.mlp_adam, group))
+    else:
+        # Single GPU: steps are queued back to back (no host round trip per step) and their losses read in windows;
+        # the device gate keeps the reference's "throw before the update" for a non-finite loss.
+        first = 0
+        for step in range(cfg.steps):
+            coords, targets = sampler(step, cfg.batch_size)
+            trainer.step_enqueue(coords, targets, cfg.table_adam, cfg.mlp_adam)
+            if step + 1 - first == QUEUE_WINDOW or step == cfg.steps - 1:
+                losses, _ = trainer.collect()
+                for k, loss in enumerate(losses):
+                    record(first + k, loss)
+                first = step + 1
     result.steps_run = cfg.steps
     return result

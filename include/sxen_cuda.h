@@ -107,7 +107,9 @@ typedef struct sxen_tuning {
                                 footprint; 0 = plain accesses */
   int32_t coarse_replicas;   /* backward: levels with at most 2^16 lattice vertices accumulate into replicated dense
                                 arrays that the same call folds into the hashed rows (relieves the per-address
-                                serialisation of the L2 atomic unit).  0 = on (default), -1 = off */
+                                serialisation of the L2 atomic unit).  0 = library default: on for launches of at least
+                                2^16 samples (below, the fold costs more than the contention it removes), 1 = always,
+                                -1 = off */
 } sxen_tuning;
 
 typedef struct sxen_encoder sxen_encoder;   /* sxen::HashEncoder     (include/sxen/encoding.hpp:92-148) */

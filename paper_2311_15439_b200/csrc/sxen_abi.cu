@@ -156,6 +156,11 @@ const encode_fn kEncode[8] = {sxen_dev::launch_encode_nd1, sxen_dev::launch_enco
                               sxen_dev::launch_encode_nd4, sxen_dev::launch_encode_nd5, sxen_dev::launch_encode_nd6,
                               sxen_dev::launch_encode_nd7, sxen_dev::launch_encode_nd8};
 typedef cudaError_t (*fold_fn)(const EncodeArgs&, cudaStream_t);
+typedef cudaError_t (*adam_walk_fn)(const EncodeArgs&, const sxen_dev::AdamWalkArgs&, int, cudaStream_t);
+const adam_walk_fn kAdamWalk[8] = {sxen_dev::launch_adam_walk_nd1, sxen_dev::launch_adam_walk_nd2,
+                                   sxen_dev::launch_adam_walk_nd3, sxen_dev::launch_adam_walk_nd4,
+                                   sxen_dev::launch_adam_walk_nd5, sxen_dev::launch_adam_walk_nd6,
+                                   sxen_dev::launch_adam_walk_nd7, sxen_dev::launch_adam_walk_nd8};
 const fold_fn kFold[8] = {sxen_dev::launch_fold_nd1, sxen_dev::launch_fold_nd2, sxen_dev::launch_fold_nd3,
                           sxen_dev::launch_fold_nd4, sxen_dev::launch_fold_nd5, sxen_dev::launch_fold_nd6,
                           sxen_dev::launch_fold_nd7, sxen_dev::launch_fold_nd8};
@@ -183,14 +188,20 @@ void base_args(const sxen_encoder* enc, const void* x, sxen_coord_type type, siz
   a.skew = enc->skew;
 }
 
-void level_chunk(const sxen_encoder* enc, const sxen_grad* grad, int level0, int level_end, EncodeArgs& a) {
+// Launches below this many samples skip the coarse-level replicas (tuning.coarse_replicas == 0): a small batch puts few
+// atomics on each hot row, while the fold that follows costs the same ~10 us whatever the batch
+// (profiles/r1s3_small_batch_launches.csv: 14 of a 2048-sample training step's 93 us).
+constexpr size_t kReplicaMinSamples = size_t{1} << 16;
+
+void level_chunk(const sxen_encoder* enc, const sxen_grad* grad, int level0, int level_end, size_t n_samples, EncodeArgs& a) {
   a.level0 = level0;
   a.n_levels = std::min<int>(sxen_dev::kMaxLaunchLevels, level_end - level0);
   a.agg_mask = 0;
   // the replicas are laid out for the lattice of the encoder the accumulator was created from
   const bool tuned_grid = enc->cfg.backend == SXEN_BACKEND_GRID && enc->cfg.features == 2 && enc->cfg.dim >= 2 &&
                           enc->cfg.dim <= 3;
-  const bool replicas = grad != nullptr && grad->coarse != nullptr && enc->tuning.coarse_replicas >= 0 &&
+  const bool replicas = grad != nullptr && grad->coarse != nullptr &&
+                        (enc->tuning.coarse_replicas > 0 || (enc->tuning.coarse_replicas == 0 && n_samples >= kReplicaMinSamples)) &&
                         (enc->cfg.backend == SXEN_BACKEND_SIMPLEX || tuned_grid) && grad->dim == enc->cfg.dim &&
                         grad->res == enc->res;
   a.coarse = replicas ? grad->coarse : nullptr;
@@ -291,7 +302,7 @@ sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, c
   ln.block_threads = enc->tuning.block_threads;
   const int level_end = first_level + level_count;
   for (int level0 = first_level; level0 < level_end; level0 += sxen_dev::kMaxLaunchLevels) {
-    level_chunk(enc, (mode & sxen_dev::kModeBwd) ? grad : nullptr, level0, level_end, a);
+    level_chunk(enc, (mode & sxen_dev::kModeBwd) ? grad : nullptr, level0, level_end, n, a);
     a.vec = 4;
     if (mode & sxen_dev::kModeFwd) a.vec = std::min(a.vec, ptr_vec(out));
     if (mode & sxen_dev::kModeBwd) a.vec = std::min(a.vec, ptr_vec(upstream));
@@ -358,6 +369,50 @@ __global__ void narrow_kernel(const double* __restrict__ src, float* __restrict_
   if (i < n) dst[i] = static_cast<float>(src[i]);
 }
 
+}  // namespace
+
+// SparseAdamState::step for the single-GPU trainer (declared in sxen_common.hpp): when the batch is small against the
+// tables, the update walks the batch (sparse_adam_walk_kernel) instead of scanning all L*T accumulator rows.  The caller
+// guarantees that every touched row of `grad` comes from this batch's backward.  Same arithmetic, same rows, same
+// clearing as sxen_sparse_adam_step(clear_grad = 1).
+bool sxen_sparse_adam_walk_pays(const sxen_encoder* enc, size_t n_samples) {
+  if (enc->cfg.features != 2) return false;
+  const double visits = static_cast<double>(n_samples) * enc->cfg.levels * enc->vertices();
+  const double rows = static_cast<double>(enc->cfg.levels) * enc->cfg.table_size;
+  return visits * 8.0 <= rows;  // a visit (lattice walk + atomic exchange) against a scanned row (one coalesced 8-byte load)
+}
+
+sxen_status sxen_sparse_adam_step_walk(sxen_sparse_adam* opt, sxen_encoder* enc, sxen_grad* grad, const void* x_dev,
+                                       sxen_coord_type type, size_t n_samples, const sxen_adam_config* cfg,
+                                       const unsigned long long* gate_dev, void* stream) {
+  SXEN_REQUIRE(opt != nullptr && enc != nullptr && grad != nullptr && cfg != nullptr, "null argument");
+  SXEN_REQUIRE(enc->cfg.features == 2 && enc->cfg.levels == opt->levels && enc->cfg.features == opt->features &&
+                   enc->cfg.table_size == opt->table_size && grad->levels == opt->levels &&
+                   grad->features == opt->features && grad->table_size == opt->table_size &&
+                   enc->device == opt->device && grad->device == opt->device,
+               "sparse adam step: encoder/gradient shape mismatch");
+  DeviceGuard guard(opt->device);
+  ++opt->t;  // src/optimizer.cpp:64
+  if (n_samples == 0) return SXEN_OK;
+  sxen_dev::AdamWalkArgs o{};
+  o.tables = reinterpret_cast<float2*>(enc->tables);
+  o.grads = reinterpret_cast<float2*>(grad->values);
+  o.m = reinterpret_cast<double2*>(opt->m);
+  o.v = reinterpret_cast<double2*>(opt->v);
+  o.c = sxen_adam_scalars(*cfg, opt->t);
+  o.status = opt->status;
+  o.gate = gate_dev;
+  EncodeArgs a;
+  base_args(enc, x_dev, type, n_samples, a);
+  for (int level0 = 0; level0 < enc->cfg.levels; level0 += sxen_dev::kMaxLaunchLevels) {
+    level_chunk(enc, nullptr, level0, enc->cfg.levels, 0, a);
+    SXEN_CUDA(kAdamWalk[enc->cfg.dim - 1](a, o, enc->cfg.backend == SXEN_BACKEND_GRID ? 1 : 0, as_stream(stream)));
+    count_launch();
+  }
+  return SXEN_OK;
+}
+
+namespace {
 }  // namespace
 
 extern "C" {
@@ -680,7 +735,7 @@ sxen_status sxen_encoder_encode_debug(sxen_encoder* enc, const void* x_dev, sxen
   EncodeArgs a;
   base_args(enc, x_dev, type, n_samples, a);
   for (int level0 = 0; level0 < enc->cfg.levels; level0 += sxen_dev::kMaxLaunchLevels) {
-    level_chunk(enc, nullptr, level0, enc->cfg.levels, a);
+    level_chunk(enc, nullptr, level0, enc->cfg.levels, 0, a);
     SXEN_CUDA(kDebug[enc->cfg.dim - 1](a, enc->cfg.backend == SXEN_BACKEND_GRID ? 1 : 0, idx_dev, w_dev,
                                        enc->cfg.levels, as_stream(stream)));
     count_launch();

@@ -119,3 +119,10 @@ sxen_status sxen_sparse_adam_step_gated(sxen_sparse_adam* opt, sxen_encoder* enc
                                         int32_t clear_grad, const unsigned long long* gate_dev, void* stream);
 sxen_status sxen_adam_step_gated(sxen_adam* opt, float* params_dev, const void* grads_dev, sxen_coord_type grad_type,
                                  size_t size, const sxen_adam_config* cfg, const unsigned long long* gate_dev, void* stream);
+
+// The same update driven by the batch (sxen_abi.cu): O(n_samples * L * V) instead of O(L * T); valid when every touched
+// row of `grad` comes from the backward of exactly these samples.  sxen_sparse_adam_walk_pays: the size rule.
+bool sxen_sparse_adam_walk_pays(const sxen_encoder* enc, size_t n_samples);
+sxen_status sxen_sparse_adam_step_walk(sxen_sparse_adam* opt, sxen_encoder* enc, sxen_grad* grad, const void* x_dev,
+                                       sxen_coord_type type, size_t n_samples, const sxen_adam_config* cfg,
+                                       const unsigned long long* gate_dev, void* stream);

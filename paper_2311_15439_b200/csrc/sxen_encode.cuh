@@ -11,6 +11,7 @@
 // Reference semantics: HashEncoder::encode / encode_backward, /root/reference/proj/src/encoding.cpp:295-335.
 #pragma once
 
+#include "sxen_adam.cuh"
 #include "sxen_device.cuh"
 
 namespace sxen_dev {
@@ -406,6 +407,64 @@ encode_debug_kernel(const __grid_constant__ EncodeArgs a, uint32_t* __restrict__
   }
 }
 
+// SparseAdamState::step (src/optimizer.cpp:54-84) driven by the BATCH instead of by a scan of the accumulator: one thread
+// per (sample, level) repeats the lattice walk of the backward that filled the accumulator and claims each of its rows
+// with a 64-bit atomic exchange against the untouched pattern; the first claimant gets the row's gradient and applies
+// the update, later ones see -0.0f and move on.  Visits exactly the touched rows, each once, in O(batch * L * V) work --
+// the scan reads all L*T rows, 36 of a 2048-sample training step's 93 us (profiles/r1s3_small_batch_launches.csv).
+// Only valid when every touched row comes from THIS batch (the single-GPU trainer's step), F == 2.
+template <int ND, bool GRID>
+__global__ void __launch_bounds__(256)
+sparse_adam_walk_kernel(const __grid_constant__ EncodeArgs a, const __grid_constant__ AdamWalkArgs o) {
+  constexpr int V = GRID ? (1 << ND) : (ND + 1);
+  if (o.gate != nullptr && *o.gate != kAdamNoBad) return;
+  const unsigned long long gid = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const unsigned long long s = gid / static_cast<unsigned long long>(a.n_levels);
+  const int l = static_cast<int>(gid - s * static_cast<unsigned long long>(a.n_levels));
+  if (s >= a.n_samples) return;
+  double x[ND];
+  if (!load_coords<ND>(a, s, x)) return;  // a rejected sample added no gradient (encode_kernel)
+  const size_t level_row0 = static_cast<size_t>(a.level0 + l) * (static_cast<size_t>(a.mask) + 1u);
+  constexpr unsigned long long kUntouchedRow = (static_cast<unsigned long long>(kUntouchedBits) << 32) | kUntouchedBits;
+  auto claim_and_update = [&](uint32_t row) {
+    const size_t r = level_row0 + row;
+    const unsigned long long got = atomicExch(reinterpret_cast<unsigned long long*>(o.grads + r), kUntouchedRow);
+    const uint32_t gx_bits = static_cast<uint32_t>(got), gy_bits = static_cast<uint32_t>(got >> 32);
+    if (gx_bits == kUntouchedBits) return;  // untouched, or already claimed by another thread
+    const double gx = static_cast<double>(__uint_as_float(gx_bits)), gy = static_cast<double>(__uint_as_float(gy_bits));
+    if (!isfinite(gx) || !isfinite(gy)) {
+      atomicMin(o.status, static_cast<unsigned long long>(2 * r + (isfinite(gx) ? 1 : 0)));  // src/optimizer.cpp:73-76
+      return;
+    }
+    double2 mm = o.m[r], vv = o.v[r];
+    float2 t = o.tables[r];
+    const double dx = adam_delta(gx, mm.x, vv.x, o.c);
+    const double dy = adam_delta(gy, mm.y, vv.y, o.c);
+    o.m[r] = mm;
+    o.v[r] = vv;
+    t.x = static_cast<float>(__dadd_rn(static_cast<double>(t.x), dx));
+    t.y = static_cast<float>(__dadd_rn(static_cast<double>(t.y), dy));
+    o.tables[r] = t;
+  };
+  if constexpr (GRID) {
+    GridCell<ND> cell;
+    grid_prepare<ND>(x, a.geom.scale[l], a.geom.res[l], cell);
+#pragma unroll 1
+    for (int m = 0; m < V; ++m) {
+      uint32_t idx;
+      double w;
+      grid_corner<ND>(cell, m, a.mask, idx, w);
+      claim_and_update(idx);
+    }
+  } else {
+    uint32_t idx[V];
+    double w[V];
+    simplex_lookup<ND>(x, a.geom.scale[l], a.skew, a.geom.res[l], a.mask, idx, w);
+#pragma unroll 1
+    for (int k = 0; k < V; ++k) claim_and_update(idx[k]);
+  }
+}
+
 // Adds the dense replicas of one launch's coarse levels into the hashed gradient rows and re-arms them with -0.0f.
 // One thread per (vertex, feature) of a level (blockIdx.y = local level).  Each replica slot is claimed with an atomic
 // exchange, so a backward kernel of another stream that is still adding loses nothing: whatever lands after the exchange
@@ -488,6 +547,16 @@ cudaError_t launch_fold_nd5(const EncodeArgs&, cudaStream_t);
 cudaError_t launch_fold_nd6(const EncodeArgs&, cudaStream_t);
 cudaError_t launch_fold_nd7(const EncodeArgs&, cudaStream_t);
 cudaError_t launch_fold_nd8(const EncodeArgs&, cudaStream_t);
+
+// sparse_adam_walk_kernel over the levels of the launch `a` describes
+cudaError_t launch_adam_walk_nd1(const EncodeArgs&, const AdamWalkArgs&, int grid_backend, cudaStream_t);
+cudaError_t launch_adam_walk_nd2(const EncodeArgs&, const AdamWalkArgs&, int grid_backend, cudaStream_t);
+cudaError_t launch_adam_walk_nd3(const EncodeArgs&, const AdamWalkArgs&, int grid_backend, cudaStream_t);
+cudaError_t launch_adam_walk_nd4(const EncodeArgs&, const AdamWalkArgs&, int grid_backend, cudaStream_t);
+cudaError_t launch_adam_walk_nd5(const EncodeArgs&, const AdamWalkArgs&, int grid_backend, cudaStream_t);
+cudaError_t launch_adam_walk_nd6(const EncodeArgs&, const AdamWalkArgs&, int grid_backend, cudaStream_t);
+cudaError_t launch_adam_walk_nd7(const EncodeArgs&, const AdamWalkArgs&, int grid_backend, cudaStream_t);
+cudaError_t launch_adam_walk_nd8(const EncodeArgs&, const AdamWalkArgs&, int grid_backend, cudaStream_t);
 
 cudaError_t launch_debug_nd1(EncodeArgs&, int grid_backend, uint32_t*, double*, int total_levels, cudaStream_t);
 cudaError_t launch_debug_nd2(EncodeArgs&, int grid_backend, uint32_t*, double*, int total_levels, cudaStream_t);

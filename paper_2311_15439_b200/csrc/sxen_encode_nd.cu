@@ -140,6 +140,19 @@ cudaError_t SXEN_CAT(launch_fold_nd, SXEN_ND)(const EncodeArgs& a, cudaStream_t 
   return cudaGetLastError();
 }
 
+cudaError_t SXEN_CAT(launch_adam_walk_nd, SXEN_ND)(const EncodeArgs& a, const AdamWalkArgs& o, int grid_backend,
+                                                    cudaStream_t stream) {
+  const int block = 256;
+  const unsigned long long threads = a.n_samples * static_cast<unsigned long long>(a.n_levels);
+  const unsigned blocks = static_cast<unsigned>((threads + block - 1) / block);
+  if (grid_backend) {
+    sparse_adam_walk_kernel<ND, true><<<blocks, block, 0, stream>>>(a, o);
+  } else {
+    sparse_adam_walk_kernel<ND, false><<<blocks, block, 0, stream>>>(a, o);
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t SXEN_CAT(launch_debug_nd, SXEN_ND)(EncodeArgs& a, int grid_backend, uint32_t* idx, double* w,
                                                int total_levels, cudaStream_t stream) {
   const int block = 256;

@@ -5,27 +5,17 @@
 // gradient values the updated parameters and moments are bit-identical to AdamState::step / SparseAdamState::step.
 #include <cmath>
 
+#include "sxen_adam.cuh"
 #include "sxen_common.hpp"
 
 using namespace sxen_host;
 
 namespace {
 
-constexpr unsigned long long kNoBad = ~0ULL;
-constexpr uint32_t kUntouchedBits = 0x80000000u;
-
-struct AdamScalars {
-  double beta1, beta2, one_minus_beta1, one_minus_beta2, neg_lr, epsilon, bc1, bc2;
-};
-
-// adam_delta, src/optimizer.cpp:9-15
-__device__ __forceinline__ double adam_delta(double g, double& m, double& v, const AdamScalars& c) {
-  m = __dadd_rn(__dmul_rn(c.beta1, m), __dmul_rn(c.one_minus_beta1, g));
-  v = __dadd_rn(__dmul_rn(c.beta2, v), __dmul_rn(__dmul_rn(c.one_minus_beta2, g), g));
-  const double m_hat = __ddiv_rn(m, c.bc1);
-  const double v_hat = __ddiv_rn(v, c.bc2);
-  return __ddiv_rn(__dmul_rn(c.neg_lr, m_hat), __dadd_rn(__dsqrt_rn(v_hat), c.epsilon));
-}
+using sxen_dev::AdamScalars;
+using sxen_dev::adam_delta;
+using sxen_dev::kUntouchedBits;
+constexpr unsigned long long kNoBad = sxen_dev::kAdamNoBad;
 
 // SparseAdamState::step, src/optimizer.cpp:54-84.  One thread per table row; a row is visited iff the accumulator
 // touched it (feature 0 != -0.0f), zero gradients included; untouched rows' moments do not decay.
@@ -102,7 +92,9 @@ __global__ void dense_adam_kernel(float* __restrict__ params, const G* __restric
   }
 }
 
-AdamScalars scalars(const sxen_adam_config& cfg, int64_t t) {
+}  // namespace
+
+sxen_dev::AdamScalars sxen_adam_scalars(const sxen_adam_config& cfg, int64_t t) {
   AdamScalars c;
   c.beta1 = cfg.beta1;
   c.beta2 = cfg.beta2;
@@ -114,6 +106,10 @@ AdamScalars scalars(const sxen_adam_config& cfg, int64_t t) {
   c.bc2 = 1.0 - std::pow(cfg.beta2, static_cast<double>(t));
   return c;
 }
+
+namespace {
+
+AdamScalars scalars(const sxen_adam_config& cfg, int64_t t) { return sxen_adam_scalars(cfg, t); }
 
 int grid_for(size_t n) {
   size_t b = (n + 255) / 256;

@@ -31,6 +31,7 @@ struct sxen_trainer {
   unsigned long long* gate = nullptr;       // device: slot of the first queued step whose loss was non-finite, else ~0
   unsigned long long* gate_host = nullptr;  // pinned
   size_t pending = 0;                // queued steps not collected yet
+  bool foreign_grads = false;        // the accumulators may hold rows of batches other than the current step's
   int32_t out_w = 0, enc_w = 0;
   uint64_t mlp_params = 0;
 };
@@ -66,6 +67,30 @@ sxen_status ensure_workspace(sxen_trainer* t, size_t n) {
   SXEN_CUDA(cudaMalloc(&t->sample_loss, (n + 1) * sizeof(double)));
   t->capacity = n;
   return SXEN_OK;
+}
+
+// table_opt.step then mlp_opt.step (src/trainer.cpp:129-130); the accumulators are cleared for the next step (:97-100).
+// walk_coords != nullptr: the table step visits the rows of that batch only (sxen_sparse_adam_step_walk) -- the caller has
+// checked that nothing else was accumulated.  gate: queued steps (nullptr otherwise).
+sxen_status update_impl(sxen_trainer* t, const sxen_adam_config* table_adam, const sxen_adam_config* mlp_adam,
+                        const void* walk_coords, sxen_coord_type coord_type, size_t n_samples,
+                        const unsigned long long* gate, void* stream) {
+  if (walk_coords != nullptr) {
+    if (sxen_status st = sxen_sparse_adam_step_walk(t->table_opt, t->enc, t->grad, walk_coords, coord_type, n_samples,
+                                                    table_adam, gate, stream))
+      return st;
+  } else if (sxen_status st = sxen_sparse_adam_step_gated(t->table_opt, t->enc, t->grad, table_adam, 1, gate, stream)) {
+    return st;
+  }
+  double* mg = nullptr;
+  float* mp = nullptr;
+  sxen_mlp_grads_dev(t->mlp, &mg);
+  sxen_mlp_params_dev(t->mlp, &mp);
+  if (sxen_status st = sxen_adam_step_gated(t->mlp_opt, mp, mg, SXEN_COORD_F64, static_cast<size_t>(t->mlp_params), mlp_adam,
+                                            gate, stream))
+    return st;
+  t->foreign_grads = false;
+  return sxen_mlp_grad_clear(t->mlp, stream);
 }
 
 }  // namespace
@@ -160,6 +185,7 @@ sxen_status sxen_trainer_accumulate_head(sxen_trainer* t, const void* coords_dev
                                                  nullptr, t->input_grad, t->loss_sum, stream))
     return st;
   t->head_samples = n_samples;
+  t->foreign_grads = true;
   return SXEN_OK;
 }
 
@@ -179,6 +205,8 @@ sxen_status sxen_trainer_accumulate_tables(sxen_trainer* t, const void* coords_d
 sxen_status sxen_trainer_accumulate(sxen_trainer* t, const void* coords_dev, sxen_coord_type coord_type,
                                     const void* targets_dev, sxen_coord_type target_type, size_t n_samples,
                                     size_t global_batch, void* stream) {
+  SXEN_REQUIRE(t != nullptr, "trainer handle is null");
+  t->foreign_grads = true;  // (the whole-step entry points reset this around their own call)
   if (sxen_status st = sxen_trainer_accumulate_head(t, coords_dev, coord_type, targets_dev, target_type, n_samples,
                                                     global_batch, stream))
     return st;
@@ -205,15 +233,7 @@ sxen_status sxen_trainer_update(sxen_trainer* t, const sxen_adam_config* table_a
                                 void* stream) {
   SXEN_REQUIRE(t != nullptr && table_adam != nullptr && mlp_adam != nullptr, "null argument");
   DeviceGuard guard(t->device);
-  // table_opt.step then mlp_opt.step (src/trainer.cpp:129-130); the accumulators are cleared for the next step (:97-100)
-  if (sxen_status st = sxen_sparse_adam_step(t->table_opt, t->enc, t->grad, table_adam, 1, stream)) return st;
-  double* mg = nullptr;
-  float* mp = nullptr;
-  sxen_mlp_grads_dev(t->mlp, &mg);
-  sxen_mlp_params_dev(t->mlp, &mp);
-  if (sxen_status st = sxen_adam_step(t->mlp_opt, mp, mg, SXEN_COORD_F64, static_cast<size_t>(t->mlp_params), mlp_adam, stream))
-    return st;
-  if (sxen_status st = sxen_mlp_grad_clear(t->mlp, stream)) return st;
+  if (sxen_status st = update_impl(t, table_adam, mlp_adam, nullptr, SXEN_COORD_F64, 0, nullptr, stream)) return st;
   SXEN_CUDA(cudaMemsetAsync(t->loss_sum, 0, sizeof(double), as_stream(stream)));
   return SXEN_OK;
 }
@@ -228,13 +248,18 @@ sxen_status sxen_trainer_step(sxen_trainer* t, const void* coords_dev, sxen_coor
                               sxen_coord_type target_type, size_t n_samples, const sxen_adam_config* table_adam,
                               const sxen_adam_config* mlp_adam, double* loss_out, void* stream) {
   SXEN_REQUIRE(n_samples >= 1, "train: batch_size must be >= 1");  // src/trainer.cpp:57
+  SXEN_REQUIRE(t != nullptr && table_adam != nullptr && mlp_adam != nullptr, "null argument");
+  const bool walk = !t->foreign_grads && sxen_sparse_adam_walk_pays(t->enc, n_samples);
   if (sxen_status st = sxen_trainer_accumulate(t, coords_dev, coord_type, targets_dev, target_type, n_samples, n_samples, stream))
     return st;
   double loss = 0.0;
   const sxen_status loss_st = sxen_trainer_loss(t, n_samples, &loss, stream);
   if (loss_out) *loss_out = loss;
   if (loss_st != SXEN_OK) return loss_st;  // the reference throws before updating (src/trainer.cpp:121-123)
-  if (sxen_status st = sxen_trainer_update(t, table_adam, mlp_adam, stream)) return st;
+  DeviceGuard guard(t->device);
+  if (sxen_status st = update_impl(t, table_adam, mlp_adam, walk ? coords_dev : nullptr, coord_type, n_samples, nullptr, stream))
+    return st;
+  SXEN_CUDA(cudaMemsetAsync(t->loss_sum, 0, sizeof(double), as_stream(stream)));
   return sxen_trainer_check(t, stream);
 }
 
@@ -245,6 +270,7 @@ sxen_status sxen_trainer_step_enqueue(sxen_trainer* t, const void* coords_dev, s
   SXEN_REQUIRE(n_samples >= 1, "train: batch_size must be >= 1");  // src/trainer.cpp:57
   if (t->pending >= kLossRing)
     return fail(SXEN_LOGIC_ERROR, "train: %zu queued steps not collected (sxen_trainer_collect first)", t->pending);
+  const bool own_rows_only = !t->foreign_grads;  // nothing accumulated since the last update but this step's batch
   if (sxen_status st = sxen_trainer_accumulate(t, coords_dev, coord_type, targets_dev, target_type, n_samples, n_samples, stream))
     return st;
   DeviceGuard guard(t->device);
@@ -254,16 +280,10 @@ sxen_status sxen_trainer_step_enqueue(sxen_trainer* t, const void* coords_dev, s
   SXEN_CUDA(cudaGetLastError());
   count_launch();
   ++t->pending;
-  // table_opt.step, mlp_opt.step (src/trainer.cpp:129-130), skipped on the device when the gate is closed
-  if (sxen_status st = sxen_sparse_adam_step_gated(t->table_opt, t->enc, t->grad, table_adam, 1, t->gate, stream)) return st;
-  double* mg = nullptr;
-  float* mp = nullptr;
-  sxen_mlp_grads_dev(t->mlp, &mg);
-  sxen_mlp_params_dev(t->mlp, &mp);
-  if (sxen_status st = sxen_adam_step_gated(t->mlp_opt, mp, mg, SXEN_COORD_F64, static_cast<size_t>(t->mlp_params), mlp_adam,
-                                            t->gate, stream))
-    return st;
-  return sxen_mlp_grad_clear(t->mlp, stream);
+  // table_opt.step, mlp_opt.step (src/trainer.cpp:129-130), skipped on the device when the gate is closed; a small batch
+  // visits its own rows instead of scanning all L*T
+  const bool walk = own_rows_only && sxen_sparse_adam_walk_pays(t->enc, n_samples);
+  return update_impl(t, table_adam, mlp_adam, walk ? coords_dev : nullptr, coord_type, n_samples, t->gate, stream);
 }
 
 sxen_status sxen_trainer_pending(const sxen_trainer* t, size_t* out) {
@@ -295,6 +315,7 @@ sxen_status sxen_trainer_collect(sxen_trainer* t, double* losses_out, size_t cap
     // and it drops them with the aborted run): clear them so the handle can go on from the last applied step
     if (sxen_status st = sxen_grad_clear(t->grad, stream)) return st;
     if (sxen_status st = sxen_mlp_grad_clear(t->mlp, stream)) return st;
+    t->foreign_grads = false;
     SXEN_CUDA(cudaStreamSynchronize(s));
     if (failed_out) *failed_out = static_cast<int64_t>(bad);
     return fail(SXEN_TRAINING_ERROR, "loss became non-finite (queued step %llu of %zu)", bad, n);

@@ -84,7 +84,7 @@ class Tuning:
     warp_aggregate: int = 0
     merge_pairs: int = 0  # 1 on, -1 off, 0 library default (on)
     cache_hints: int = -1  # F == 2: gather L2 policy + 4 * red L2 policy (0 none, 1 evict_last, 2 evict_first, 3 evict_unchanged); -1 auto
-    coarse_replicas: int = 0  # 0 on (library default), -1 off
+    coarse_replicas: int = 0  # 0 library default (on from 2^16 samples per launch), 1 always, -1 off
 
     def c(self) -> _abi.TuningC:
         return _abi.TuningC(self.levels_per_thread, self.block_threads, self.level_major, self.exact_blend,

@@ -176,3 +176,52 @@ def test_queue_overflow_is_a_logic_error(sx):
         tr.step_enqueue(x, y, ta, ma)
     losses, failed = tr.collect()
     assert len(losses) == 4096 and failed == -1 and losses[-1] < losses[0]
+
+
+@pytest.mark.parametrize("backend", [0, 1])
+def test_small_batch_table_update_walks_the_batch_like_the_scan(sx, backend):
+    """A small batch takes the batch-walking sparse Adam (O(batch*L*V) claims by atomic exchange) instead of the scan of
+    all L*T accumulator rows.  Same rows, same arithmetic: against a twin driven through accumulate + update (always the
+    scan) the updated-row sets are identical, the tables agree to the order of the fp32 atomics, and the accumulator is
+    left fully cleared (a row the walk missed would still be marked touched)."""
+    cfg = sx.EncoderConfig(dim=2, levels=16, table_size=1 << 17, features=2, base_resolution=16, growth=1.4,
+                           backend=backend)
+    ta, ma = sx.AdamConfig(lr=1e-2), sx.AdamConfig(lr=1e-3)
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    B = 1024   # 1024 * 16 * 3 * 8 <= 16 * 2^17: the walk pays
+    batches = [(torch.rand((B, 2), dtype=torch.float64, device="cuda", generator=gen),
+                torch.rand((B, 3), dtype=torch.float64, device="cuda", generator=gen)) for _ in range(4)]
+    batches[1][0][:8] = batches[1][0][0]          # repeated samples: several threads race for the same rows
+    batches[2][0][5] = torch.tensor([1.0, 0.0])   # the cube's corner (clamped cell)
+
+    def twin():
+        enc = sx.HashEncoder(cfg)
+        enc.init_tables(42)
+        mlp = sx.Mlp(sx.MlpConfig(cfg.encoded_width(), 64, 2, 3))
+        mlp.init_params(sx.hash_combine(42, 1))
+        return enc, mlp, sx.Trainer(enc, mlp)
+
+    e1, m1, t1 = twin()   # whole-step entry points: walk
+    e2, m2, t2 = twin()   # accumulate + update: scan
+    e3, m3, t3 = twin()   # queued steps: walk behind the gate
+    init = [e1.table(l).reshape(-1, 2).copy() for l in range(cfg.levels)]
+    for x, y in batches:
+        l1 = t1.step(x, y, ta, ma)
+        t2.accumulate(x, y, B)
+        l2 = t2.loss(B)
+        t2.update(ta, ma)
+        t3.step_enqueue(x, y, ta, ma)
+        assert np.isclose(l1, l2, rtol=1e-6)
+    l3, failed = t3.collect()
+    assert failed == -1 and np.isclose(l3[-1], l2, rtol=1e-6)
+    for tr in (t1, t2, t3):
+        g = tr.table_grad_device()
+        assert int((g.view(torch.int32) != -2147483648).sum().item()) == 0   # every row back to -0.0f
+    for l in range(cfg.levels):
+        a, b, c = (e.table(l).reshape(-1, 2) for e in (e1, e2, e3))
+        changed = (b != init[l]).any(axis=1)
+        assert changed.sum() > 0
+        assert np.array_equal((a != init[l]).any(axis=1), changed), l
+        assert np.array_equal((c != init[l]).any(axis=1), changed), l
+        assert np.allclose(a, b, rtol=1e-3, atol=1e-6) and np.allclose(c, b, rtol=1e-3, atol=1e-6)
+    assert np.allclose(m1.parameters(), m2.parameters(), rtol=1e-3, atol=1e-6)

@@ -498,7 +498,7 @@ def test_coarse_replicas_and_cache_policies_do_not_change_results(sx, oracle_lib
     wg, wt, _ = oracle_lib.encode_backward(cfg, x, up32.astype(np.float64))
     scale = abs_contrib(oracle_lib, cfg, x, up32.astype(np.float64))
     xd, upd = dev(x32), dev(up32)
-    for rep in (0, -1):
+    for rep in (1, 0, -1):   # forced on (N is below the automatic threshold), library default, off
         for hints in (-1, 0, 5, 8, 10, 15):
             for lm, lpt in ((0, 2), (1, 4), (0, 1)):
                 enc.set_tuning(sx.Tuning(levels_per_thread=lpt, level_major=lm, coarse_replicas=rep, cache_hints=hints))
@@ -596,7 +596,7 @@ def test_tuned_grid_backend_matches_the_oracle(sx, oracle_lib, n, growth):
     assert np.array_equal(idx, oi) and np.array_equal(w, ow)
     for lpt in (1, 2):
         for lm in (0, 1):
-            for rep, merge in ((0, 1), (-1, 1), (0, -1)):
+            for rep, merge in ((1, 1), (-1, 1), (1, -1)):
                 enc.set_tuning(sx.Tuning(levels_per_thread=lpt, level_major=lm, coarse_replicas=rep, merge_pairs=merge))
                 tag = (lpt, lm, rep, merge)
                 feats = enc.encode(xd).cpu().numpy()

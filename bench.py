@@ -498,6 +498,21 @@ def run_ours(args):
                 train = {"what": "encode -> tcgen05 MLP 32-64-64-3 (split bf16) fwd+MSE+bwd -> encode_backward -> sparse Adam "
                                  "+ Adam, one 2^20-sample batch per step, loss read back every step",
                          "ms_per_step": tms, "samples_per_s": N / (tms * 1e-3)}
+                # the same step queued (sxen_trainer_step_enqueue, losses collected once), at 2^20 samples and at the
+                # reference's default batch of 2048 (include/sxen/trainer.hpp:16)
+                for key, nb, reps in (("queued", N, 8), ("queued_batch_2048", 2048, 1000)):
+                    for i in range(3):
+                        tr.step_enqueue(xs[i % n_sets][:nb], tgt[:nb], ta, ma)
+                    tr.collect()
+                    torch.cuda.synchronize()
+                    e0.record(stream)
+                    for i in range(reps):
+                        tr.step_enqueue(xs[i % n_sets][:nb], tgt[:nb], ta, ma)
+                    e1.record(stream)
+                    losses, failed = tr.collect()
+                    assert failed == -1 and len(losses) == reps
+                    qms = e0.elapsed_time(e1) / reps
+                    train[key] = {"batch": nb, "ms_per_step": qms, "samples_per_s": nb / (qms * 1e-3)}
                 del tr, mlp
             except Exception as exc:
                 train = {"error": str(exc)}

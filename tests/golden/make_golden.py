@@ -326,9 +326,33 @@ def task_cases(ref: Ref):
     print("task_cases written; reference final PSNR", psnr, "loss", loss[0], "->", loss[-1])
 
 
+def acceptance_image_fitting(ref: Ref):
+    """The reference's own acceptance criterion `image-fitting-parity` (tests/acceptance_main.cpp:315-341), run by the
+    reference: make_test_image(512, 512, 7), L=8 T=2^16 F=2 base 4 growth 2 equal-memory, batch 512, 10 000 steps,
+    1 thread, both backends.  Stores the two final PSNRs and the recorded loss curves (every 1000th step)."""
+    import time
+    img = ref.make_test_image(512, 512, 7)
+    d = {"image_probe": img[::64, ::64].copy()}
+    for name, backend in (("simplex", oracle.BACKEND_SIMPLEX), ("grid", oracle.BACKEND_GRID)):
+        cfg = Config(dim=2, levels=8, table_size=1 << 16, features=2, base_resolution=4, growth=2.0, backend=backend,
+                     level_scale=oracle.SCALE_EQUAL_MEMORY)
+        t0 = time.time()
+        psnr, loss, _, _ = ref.fit_image(img, cfg, batch=512, steps=10000, train_seed=1234, threads=1, init_seed=42)
+        d[f"{name}/final_psnr"] = np.float64(psnr)
+        d[f"{name}/loss_every_1000"] = loss[::1000].copy()
+        d[f"{name}/loss_first_20"] = loss[:20].copy()
+        d[f"{name}/seconds"] = np.float64(time.time() - t0)
+        print(name, "final PSNR", psnr, "in", round(time.time() - t0, 1), "s", flush=True)
+    np.savez_compressed(os.path.join(OUT, "acceptance_image_fitting.npz"), **d)
+    print("acceptance_image_fitting written")
+
+
 if __name__ == "__main__":
     oracle.build(ref=True)
     ref = Ref()
+    if len(sys.argv) > 1 and sys.argv[1] == "acceptance":
+        acceptance_image_fitting(ref)
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "tasks":
         task_cases(ref)
         sys.exit(0)

@@ -283,7 +283,7 @@ SXEN_API sxen_status sxen_mlp_forward(sxen_mlp* mlp, const float* input_dev, siz
 SXEN_API sxen_status sxen_mlp_backward(sxen_mlp* mlp, const double* upstream_dev, size_t n_samples, float* input_grad_dev,
                                        double* input_grad_f64_dev, void* stream);
 /* Arithmetic of the head.  EXACT (default): fp64 accumulation in the reference's order, any shape, bit-identical outputs.
- * TENSOR_*: the fused tcgen05 kernel for the 32 -> 64 -> 64 -> {<=3} head; BF16X3 = split-bf16 operands (three MMAs per
+ * TENSOR_*: the fused tcgen05 kernel for the {16|32} -> 64 -> 64 -> {<=3} head; BF16X3 = split-bf16 operands (three MMAs per
  * product, ~1e-5 relative), BF16 = single bf16 product (~4e-3). */
 typedef enum sxen_mlp_precision { SXEN_MLP_EXACT = 0, SXEN_MLP_TENSOR_BF16X3 = 1, SXEN_MLP_TENSOR_BF16 = 2 } sxen_mlp_precision;
 SXEN_API sxen_status sxen_mlp_set_precision(sxen_mlp* mlp, int32_t precision);

@@ -39,7 +39,7 @@ struct sxen_mlp {
 // sxen_mlp_tc.cu
 bool sxen_mlp_tc_supported(const sxen_mlp_config& c);
 sxen_status sxen_mlp_tc_run(bool train, const float* params, const float* features, const void* targets, int target_f32,
-                            float* pred, float* input_grad, double* mlp_grad, double* loss_sum, size_t n, int out_w,
+                            float* pred, float* input_grad, double* mlp_grad, double* loss_sum, size_t n, int in_w, int out_w,
                             size_t global_batch, int precise, cudaStream_t stream);
 
 namespace {
@@ -393,7 +393,7 @@ sxen_status sxen_mlp_set_precision(sxen_mlp* mlp, int32_t precision) {
   SXEN_REQUIRE(precision == SXEN_MLP_EXACT || precision == SXEN_MLP_TENSOR_BF16X3 || precision == SXEN_MLP_TENSOR_BF16,
                "mlp: unknown precision mode %d", precision);
   SXEN_REQUIRE(precision == SXEN_MLP_EXACT || sxen_mlp_tc_supported(mlp->cfg),
-               "mlp: the tensor-core path covers input 32, hidden 64 x 2 layers, output <= 3; this head is %d/%d x %d/%d",
+               "mlp: the tensor-core path covers input 16 or 32, hidden 64 x 2 layers, output <= 3; this head is %d/%d x %d/%d",
                mlp->cfg.input_width, mlp->cfg.hidden_width, mlp->cfg.hidden_layers, mlp->cfg.output_width);
   mlp->precision = precision;
   return SXEN_OK;
@@ -421,7 +421,7 @@ sxen_status sxen_mlp_forward_backward(sxen_mlp* mlp, const float* input_dev, con
     double* loss = loss_sum_dev ? loss_sum_dev : mlp->loss_scratch;
     mlp->forward_done = false;  // no activations are kept: a separate backward would be a logic error
     return sxen_mlp_tc_run(true, mlp->params, input_dev, targets_dev, target_type == SXEN_COORD_F32 ? 1 : 0, pred_dev,
-                           input_grad_dev, mlp->grads, loss, n_samples, mlp->cfg.output_width, global_batch,
+                           input_grad_dev, mlp->grads, loss, n_samples, mlp->cfg.input_width, mlp->cfg.output_width, global_batch,
                            mlp->precision == SXEN_MLP_TENSOR_BF16X3 ? 1 : 0, st);
   }
   if (sxen_status s = sxen_mlp_forward(mlp, input_dev, n_samples, pred_dev, stream)) return s;
@@ -452,7 +452,7 @@ sxen_status sxen_mlp_forward(sxen_mlp* mlp, const float* input_dev, size_t n_sam
     SXEN_REQUIRE(n_samples == 0 || out_dev != nullptr, "mlp forward: output pointer is null");
     mlp->forward_done = false;
     return sxen_mlp_tc_run(false, mlp->params, input_dev, nullptr, 0, out_dev, nullptr, nullptr, nullptr, n_samples,
-                           mlp->cfg.output_width, 1, mlp->precision == SXEN_MLP_TENSOR_BF16X3 ? 1 : 0, as_stream(stream));
+                           mlp->cfg.input_width, mlp->cfg.output_width, 1, mlp->precision == SXEN_MLP_TENSOR_BF16X3 ? 1 : 0, as_stream(stream));
   }
   mlp->forward_done = true;
   mlp->forward_samples = n_samples;

@@ -1,4 +1,4 @@
-// sxen_mlp_tc.cu -- the 32 -> 64 -> 64 -> {<=16} MLP head on 5th-generation tensor cores (tcgen05 + TMEM), fully fused:
+// sxen_mlp_tc.cu -- the {16|32} -> 64 -> 64 -> {<=3} MLP head on 5th-generation tensor cores (tcgen05 + TMEM), fully fused:
 // forward, MSE loss + upstream, input gradients and weight gradients of one 128-sample tile never leave the SM.
 //
 // Reference semantics: Mlp::forward / Mlp::backward and run_chunk's loss (/root/reference/proj/src/mlp.cpp:137-202,
@@ -32,14 +32,14 @@ using namespace sxen_tc;
 namespace {
 
 constexpr int kTile = 128;
-constexpr int IN = 32, HID = 64, OUTP = 16;
-constexpr int X0C = IN + 8, HC = HID + 8;  // tile widths including the ones-column block
+constexpr int kInMax = 32, HID = 64, OUTP = 16;  // the kernel is instantiated for input widths 16 and 32 (template IN)
+constexpr int kX0CMax = kInMax + 8, HC = HID + 8;  // tile widths including the ones-column block
 
 // shared-memory map (bytes)
 constexpr uint32_t kW0 = 0;                                     // CM16(64, 32) hi, lo
-constexpr uint32_t kW1 = kW0 + 2 * cm16_bytes(HID, IN);         // CM16(64, 64) hi, lo
+constexpr uint32_t kW1 = kW0 + 2 * cm16_bytes(HID, kInMax);     // CM16(64, 64) hi, lo   (regions sized for IN = 32)
 constexpr uint32_t kX0 = kW1 + 2 * cm16_bytes(HID, HID);        // CM16(128, 40) hi, lo
-constexpr uint32_t kH1 = kX0 + 2 * cm16_bytes(kTile, X0C);      // CM16(128, 72) hi, lo
+constexpr uint32_t kH1 = kX0 + 2 * cm16_bytes(kTile, kX0CMax);  // CM16(128, 72) hi, lo
 constexpr uint32_t kH2 = kH1 + 2 * cm16_bytes(kTile, HC);
 constexpr uint32_t kDY = kH2 + 2 * cm16_bytes(kTile, HC);       // CM16(128, 16) hi, lo
 constexpr uint32_t kDH2 = kDY + 2 * cm16_bytes(kTile, OUTP);    // CM16(128, 64) hi, lo
@@ -130,8 +130,10 @@ constexpr int CPT = HID / kSplit;               // columns per thread in a hidde
 constexpr int kEpiThreads = kTile * kSplit;     // 8 epilogue warps (kSplit = 4 / 16 warps measured slower: 0.585 vs 0.47 ms)
 constexpr int kThreadsAll = kEpiThreads + 64;   // + the chain-MMA warp + the weight-gradient-MMA warp
 
-template <bool TRAIN>
+template <bool TRAIN, int IN>
 __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_constant__ TcArgs a) {
+  static_assert(IN == 16 || IN == 32, "input widths 16 (L=8, F=2: the reference's default encoder) and 32 (L=16, F=2)");
+  constexpr int X0C = IN + 8;
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t bar_ready;  // 256 arrivals: the tiles of the next phase are written and the TMEM scratch is drained
   __shared__ uint64_t bar;        // dependent-chain MMAs of the current phase have completed
@@ -306,13 +308,16 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
     // Software pipeline over tiles: the features of tile i+1 are requested right after tile i's have been written to
     // shared memory, and a tile's targets at its top, so neither global-load latency sits on the per-tile dependency chain
     // (ncu stall sampling had 9 % of the samples waiting on the feature loads and 5 % on the target loads).
-    constexpr int kXIt = (kTile * (IN / 8)) / kEpiThreads;  // 16-byte-pair chunks per thread
+    constexpr int kXCh = IN / 8;                             // 8-float chunks per feature row
+    constexpr int kXIt = (kTile * kXCh) / kEpiThreads;       // chunks per thread
+    constexpr int kXRows = kEpiThreads / 8 / kXCh;           // 8-row groups one pass of all epilogue threads covers
     float xin[kXIt][8];
-    const int xch = (tid >> 3) & 3;
+    const int xch = (tid >> 3) & (kXCh - 1);
+    const int xrow = (tid & 7) + 8 * ((tid >> 3) / kXCh);
     auto load_features = [&](unsigned long long tile_index) {
 #pragma unroll
       for (int it = 0; it < kXIt; ++it) {
-        const int row = (tid & 7) + 8 * ((tid >> 5) + (kEpiThreads / 32) * it);
+        const int row = xrow + 8 * kXRows * it;
         const unsigned long long gs = tile_index * kTile + row;
         if (tile_index < n_tiles && gs < a.n) {
           const float4* p = reinterpret_cast<const float4*>(a.features + gs * IN + xch * 8);
@@ -351,7 +356,7 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
       }
 #pragma unroll
       for (int it = 0; it < kXIt; ++it)
-        store_chunk(smem + kX0, smem + kX0 + loX0, (tid & 7) + 8 * ((tid >> 5) + (kEpiThreads / 32) * it), xch, X0C, xin[it]);
+        store_chunk(smem + kX0, smem + kX0 + loX0, xrow + 8 * kXRows * it, xch, X0C, xin[it]);
       ready();
       if constexpr (!TRAIN) load_features(tile + gridDim.x);  // in flight under this tile's two phases
 
@@ -505,12 +510,12 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
       double* gb1 = gW1 + HID * HID;
       double* gW2 = gb1 + HID;
       if (g_started) {
-        for (int c0 = 8 * half; c0 < X0C; c0 += 8 * kSplit) {  // G0: 40 columns = dW0[row][0..31], db0[row] at column 32
+        for (int c0 = 8 * half; c0 < X0C; c0 += 8 * kSplit) {  // G0: IN + 8 columns = dW0[row][0..IN), db0[row] at column IN
           uint32_t r[16];
-          tmem_ld16_nowait(tb + lane_base + tG0 + (c0 < 32 ? c0 : 24), r);  // the last read re-covers cols 24..39
+          tmem_ld16_nowait(tb + lane_base + tG0 + (c0 < IN ? c0 : IN - 8), r);  // the last read re-covers cols IN-8..IN+7
           tmem_ld_wait();
           if (lane < 16) {
-            if (c0 < 32) {
+            if (c0 < IN) {
               for (int i = 0; i < 8; ++i) atomicAdd(gW0 + row * IN + c0 + i, static_cast<double>(__uint_as_float(r[i])));
             } else {
               atomicAdd(gb0 + row, static_cast<double>(__uint_as_float(r[8])));
@@ -566,13 +571,14 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
 
 // Internal entry points used by sxen_mlp.cu / sxen_trainer.cu (declared there).
 bool sxen_mlp_tc_supported(const sxen_mlp_config& c) {
-  return c.input_width == IN && c.hidden_width == HID && c.hidden_layers == 2 && c.output_width >= 1 && c.output_width <= 3;
+  return (c.input_width == 16 || c.input_width == 32) && c.hidden_width == HID && c.hidden_layers == 2 && c.output_width >= 1 && c.output_width <= 3;
 }
 
 sxen_status sxen_mlp_tc_run(bool train, const float* params, const float* features, const void* targets, int target_f32,
-                            float* pred, float* input_grad, double* mlp_grad, double* loss_sum, size_t n, int out_w,
+                            float* pred, float* input_grad, double* mlp_grad, double* loss_sum, size_t n, int in_w, int out_w,
                             size_t global_batch, int precise, cudaStream_t stream) {
   if (n == 0) return SXEN_OK;
+  if (in_w != 16 && in_w != 32) return fail(SXEN_INVALID_ARGUMENT, "mlp (tensor cores): input width %d not instantiated", in_w);
   TcArgs a{};
   a.params = params;
   a.features = features;
@@ -591,13 +597,15 @@ sxen_status sxen_mlp_tc_run(bool train, const float* params, const float* featur
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned long long tiles = (n + kTile - 1) / kTile;
   const unsigned grid = static_cast<unsigned>(std::min<unsigned long long>(tiles, static_cast<unsigned long long>(sms)));
-  if (train) {
-    SXEN_CUDA(cudaFuncSetAttribute(mlp_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)));
-    mlp_tc_kernel<true><<<grid, kThreadsAll, kSmemBytes, stream>>>(a);
-  } else {
-    SXEN_CUDA(cudaFuncSetAttribute(mlp_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)));
-    mlp_tc_kernel<false><<<grid, kThreadsAll, kSmemBytes, stream>>>(a);
-  }
+  auto launch = [&](auto kernel) -> sxen_status {
+    SXEN_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)));
+    kernel<<<grid, kThreadsAll, kSmemBytes, stream>>>(a);
+    return SXEN_OK;
+  };
+  sxen_status st;
+  if (train) st = in_w == 32 ? launch(mlp_tc_kernel<true, 32>) : launch(mlp_tc_kernel<true, 16>);
+  else st = in_w == 32 ? launch(mlp_tc_kernel<false, 32>) : launch(mlp_tc_kernel<false, 16>);
+  if (st != SXEN_OK) return st;
   SXEN_CUDA(cudaGetLastError());
   count_launch();
   return SXEN_OK;

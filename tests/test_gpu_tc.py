@@ -58,28 +58,29 @@ def test_tcgen05_conventions(sx):
     assert not got.any() and want.any()  # tf32, MN-major B: the tensor core returns zeros
 
 
-def make_case(oracle_lib, n, out_w, seed):
-    mc = oracle.MlpConfig(32, 64, 2, out_w)
+def make_case(oracle_lib, n, out_w, seed, in_w=32):
+    mc = oracle.MlpConfig(in_w, 64, 2, out_w)
     rng = np.random.default_rng(seed)
     p = oracle_lib.mlp_init(mc, seed)
     p[-out_w:] = rng.standard_normal(out_w).astype(np.float32) * 0.1
-    p[32 * 64:32 * 64 + 64] = rng.standard_normal(64).astype(np.float32) * 0.05  # b0
-    inp = (rng.standard_normal((n, 32)) * 1e-1).astype(np.float32)
+    p[in_w * 64:in_w * 64 + 64] = rng.standard_normal(64).astype(np.float32) * 0.05  # b0
+    inp = (rng.standard_normal((n, in_w)) * 1e-1).astype(np.float32)
     tgt = rng.random((n, out_w))
     return mc, p, inp, tgt
 
 
 @pytest.mark.parametrize("mode,rtol", [(1, TC3_RTOL), (2, TC1_RTOL)])
-@pytest.mark.parametrize("n,out_w", [(128 * 150 + 37, 3), (500, 1)])
-def test_tensor_core_mlp_matches_oracle(sx, oracle_lib, mode, rtol, n, out_w):
-    mc, p, inp, tgt = make_case(oracle_lib, n, out_w, 7 + out_w)
+@pytest.mark.parametrize("n,out_w,in_w", [(128 * 150 + 37, 3, 32), (500, 1, 32), (128 * 150 + 37, 3, 16), (700, 2, 16)])
+def test_tensor_core_mlp_matches_oracle(sx, oracle_lib, mode, rtol, n, out_w, in_w):
+    """in_w = 32: L=16, F=2 (every BASELINE config); in_w = 16: L=8, F=2, the reference's default EncoderConfig."""
+    mc, p, inp, tgt = make_case(oracle_lib, n, out_w, 7 + out_w, in_w)
     want, acts = oracle_lib.mlp_forward(mc, p, inp)
     scale = 2.0 / (n * out_w)
     up = scale * (want.astype(np.float64) - tgt)
     wg, wig = oracle_lib.mlp_backward(mc, p, acts, up)
     wloss = ((want.astype(np.float64) - tgt) ** 2).sum()
 
-    mlp = sx.Mlp(sx.MlpConfig(32, 64, 2, out_w))
+    mlp = sx.Mlp(sx.MlpConfig(in_w, 64, 2, out_w))
     mlp.set_parameters(p)
     mlp.set_precision(mode)
     assert mlp.precision() == mode
@@ -100,9 +101,11 @@ def test_tensor_core_mlp_matches_oracle(sx, oracle_lib, mode, rtol, n, out_w):
     # Parameter gradients: sums over the batch.  Besides the per-product rounding (rtol * sum |term|) a ReLU flip (see
     # above) moves one sample's whole contribution, so entries are held to the rounding bound plus a three-flip
     # allowance, and each layer as a whole to a relative Frobenius error.
-    W1 = p[32 * 64 + 64:32 * 64 + 64 + 64 * 64].reshape(64, 64).astype(np.float64)
-    W2 = p[32 * 64 + 64 + 64 * 64 + 64:32 * 64 + 64 + 64 * 64 + 64 + 64 * out_w].reshape(out_w, 64).astype(np.float64)
-    x0, h1, h2 = acts[:, :32].astype(np.float64), acts[:, 32:96].astype(np.float64), acts[:, 96:160].astype(np.float64)
+    o1 = in_w * 64 + 64
+    W1 = p[o1:o1 + 64 * 64].reshape(64, 64).astype(np.float64)
+    W2 = p[o1 + 64 * 64 + 64:o1 + 64 * 64 + 64 + 64 * out_w].reshape(out_w, 64).astype(np.float64)
+    x0, h1, h2 = (acts[:, :in_w].astype(np.float64), acts[:, in_w:in_w + 64].astype(np.float64),
+                  acts[:, in_w + 64:in_w + 128].astype(np.float64))
     d2 = (up @ W2) * (h2 > 0)
     d1 = (d2 @ W1) * (h1 > 0)
     off = 0
@@ -127,9 +130,10 @@ def test_tensor_core_path_rejects_other_shapes(sx):
     mlp = sx.Mlp(sx.MlpConfig(32, 64, 1, 3))
     with pytest.raises(ValueError, match="tensor-core path"):
         mlp.set_precision(1)
-    mlp = sx.Mlp(sx.MlpConfig(16, 64, 2, 3))
+    mlp = sx.Mlp(sx.MlpConfig(24, 64, 2, 3))
     with pytest.raises(ValueError):
         mlp.set_precision(2)
+    sx.Mlp(sx.MlpConfig(16, 64, 2, 3)).set_precision(2)   # L=8, F=2 (the reference's default encoder) is instantiated
     with pytest.raises(ValueError):
         sx.Mlp(sx.MlpConfig(32, 64, 2, 3)).set_precision(7)
 

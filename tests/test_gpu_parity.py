@@ -697,3 +697,62 @@ def test_fused_call_counts_and_big_table_split(sx, oracle_lib):
     assert g_auto.touched_total() == g_fused.touched_total()
     d = (g_auto.device_view() - g_fused.device_view()).abs().max().item()
     assert d <= 1e-5
+
+
+def test_random_configurations_match_the_oracle(sx, oracle_lib):
+    """Seeded fuzz over the whole EncoderConfig surface (dim 1..8, both backends, raw / equal-memory ladders, F in
+    1..8, odd level counts, tiny and mid tables, growths from barely above 1 to 2.5) with samples that include exact 0 / 1
+    coordinates and repeated points: indices, weights, features bit-exact, touched sets exact, gradients within the fp32
+    bar, fused == separate, counters equal to the oracle's."""
+    rng = np.random.default_rng(20240229)
+    done = 0
+    while done < 120:
+        n = int(rng.integers(1, 9))
+        backend = int(rng.integers(0, 2))
+        if backend == oracle.BACKEND_GRID and n > 5:
+            continue  # 2^n corners x the oracle's Python-side loops: keep the CPU side in seconds
+        cfg = oracle.Config(dim=n, levels=int(rng.integers(1, 12)), table_size=1 << int(rng.integers(4, 15)),
+                            features=int(rng.choice([1, 2, 2, 2, 3, 4, 8])), base_resolution=int(rng.integers(1, 20)),
+                            growth=float(rng.choice([1.05, 1.26, 1.5, 2.0, 2.5])), backend=backend,
+                            level_scale=int(rng.integers(0, 2)))
+        if oracle_lib.validate(cfg) != 0:   # e.g. the finest resolution above 2^26 (src/encoding.cpp:52-57)
+            with pytest.raises(ValueError):
+                sx.HashEncoder(to_sx(sx, cfg))      # the same rejection on the device side
+            continue
+        done += 1
+        seed = int(rng.integers(1, 1 << 30))
+        tables = oracle_lib.init_tables(cfg, seed)
+        enc = make_encoder(sx, cfg, seed=seed)
+        N = int(rng.integers(1, 600))
+        x = rng.random((N, n))
+        x[rng.random((N, n)) < 0.03] = 0.0
+        x[rng.random((N, n)) < 0.03] = 1.0
+        if N > 4:
+            x[N // 2] = x[0]
+        x32 = x.astype(np.float32)
+        x = x32.astype(np.float64)
+        up = (rng.standard_normal((N, cfg.encoded_width)) * 1e-2).astype(np.float32)
+        tag = (cfg, N)
+        want, bad = oracle_lib.encode(cfg, tables, x)
+        assert bad == -1
+        oi, ow, _, _, _ = oracle_lib.encode_debug(cfg, x)
+        wg, wt, _ = oracle_lib.encode_backward(cfg, x, up.astype(np.float64))
+        scale = abs_contrib(oracle_lib, cfg, x, up.astype(np.float64))
+        enc.set_tuning(sx.Tuning(levels_per_thread=int(rng.choice([0, 1, 2, 4])), level_major=int(rng.integers(-1, 2)),
+                                 coarse_replicas=int(rng.choice([0, 1, -1]))))
+        xd, upd = dev(x32), dev(up)
+        idx, w = enc.encode_debug(xd)
+        assert np.array_equal(idx, oi) and np.array_equal(w, ow), tag
+        feats = enc.encode(xd).cpu().numpy()
+        assert np.array_equal(feats.view(np.uint32), want.view(np.uint32)), tag
+        grad = sx.EncoderGradient(enc)
+        enc.encode_backward(xd, upd, grad)
+        vals, tch = grad_dense(grad, cfg)
+        assert np.array_equal(tch, wt), tag
+        assert (np.abs(vals - wg) <= GRAD_RTOL * scale + GRAD_ATOL).all(), tag
+        grad2 = sx.EncoderGradient(enc)
+        feats2 = enc.encode_forward_backward(xd, upd, grad2).cpu().numpy()
+        assert np.array_equal(feats2.view(np.uint32), want.view(np.uint32)), tag
+        vals2, tch2 = grad_dense(grad2, cfg)
+        assert np.array_equal(tch2, wt) and (np.abs(vals2 - wg) <= GRAD_RTOL * scale + GRAD_ATOL).all(), tag
+        enc.check()

@@ -17,3 +17,18 @@ def test_cpp_wrapper_builds_and_runs(tmp_path):
                     "-lsxen_b200", f"-Wl,-rpath,{lib_dir}"], check=True)
     out = subprocess.run([exe], check=True, capture_output=True, text=True).stdout
     assert "wrapper ok" in out
+
+
+def test_cpp_trainer_mirror_builds(tmp_path):
+    """include/sxen_b200_train.hpp (train_field / fit_image / fit_field over the C ABI) compiles with plain g++ -- no CUDA
+    headers on the include path -- and links against libsxen_b200.so alone; the program's GPU run is
+    tests/test_gpu_cpp_trainer.py."""
+    lib_dir = os.path.join(ROOT, "paper_2311_15439_b200", "lib")
+    exe = str(tmp_path / "train_tasks_check")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "train_tasks_check.cpp"), "-o", exe, "-L", lib_dir,
+                    "-lsxen_b200", f"-Wl,-rpath,{lib_dir}"], check=True)
+    run = subprocess.run([exe], capture_output=True, text=True)
+    assert run.returncode == 2 and "usage" in run.stdout
+    needed = subprocess.run(["readelf", "-d", exe], capture_output=True, text=True).stdout
+    assert "libsxen_b200.so" in needed and "libcudart" not in needed

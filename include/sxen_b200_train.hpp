@@ -91,7 +91,7 @@ class AdamState {
 struct TrainConfig {
   int batch_size = 2048;
   int steps = 10000;
-  int aux_dims = 0;
+  int aux_dims = 0;  // extra inputs appended verbatim after the encoding
   AdamConfig table_adam{.lr = 1e-2, .beta1 = 0.9, .beta2 = 0.99, .epsilon = 1e-15};
   AdamConfig mlp_adam{.lr = 1e-3, .beta1 = 0.9, .beta2 = 0.99, .epsilon = 1e-15};
   std::uint64_t seed = 1234;
@@ -100,9 +100,11 @@ struct TrainConfig {
   int queue_window = 256;  // steps queued between two loss read-backs (1 = the reference's per-step cadence); <= 4096
 };
 
-// include/sxen/trainer.hpp:26-32 with device spans: coords = batch x dim, targets = batch x output_width, both f64,
-// filled by work queued on `stream`.  Called on the coordinating thread only; determinism comes from (seed, step).
-using BatchSampler = std::function<void(int step, DeviceSpan<double> coords, DeviceSpan<double> targets, void* stream)>;
+// include/sxen/trainer.hpp:26-32 with device spans: coords = batch x dim, aux = batch x aux_dims pass-through inputs (empty
+// when aux_dims == 0), targets = batch x output_width, all f64, filled by work queued on `stream`.  Called on the
+// coordinating thread only; determinism comes from (seed, step).
+using BatchSampler = std::function<void(int step, DeviceSpan<double> coords, DeviceSpan<double> aux,
+                                        DeviceSpan<double> targets, void* stream)>;
 
 // include/sxen/trainer.hpp:34-38
 struct TrainResult {
@@ -118,7 +120,7 @@ inline TrainResult train_field(HashEncoder& encoder, Mlp& mlp, const BatchSample
                                int device = 0, void* stream = nullptr) {
   if (cfg.batch_size < 1) throw std::invalid_argument("train: batch_size must be >= 1");
   if (cfg.steps < 0) throw std::invalid_argument("train: steps must be >= 0");
-  if (cfg.aux_dims != 0) throw std::invalid_argument("train: aux_dims must be 0 on the device path");
+  if (cfg.aux_dims < 0) throw std::invalid_argument("train: aux_dims must be >= 0");  // src/trainer.cpp:59
   if (cfg.record_every < 1) throw std::invalid_argument("train: record_every must be >= 1");
   if (cfg.queue_window < 1 || cfg.queue_window > 4096) throw std::invalid_argument("train: queue_window must be in [1, 4096]");
   if (!sampler) throw std::invalid_argument("train: sampler must be callable");
@@ -126,19 +128,21 @@ inline TrainResult train_field(HashEncoder& encoder, Mlp& mlp, const BatchSample
     sxen_trainer* h = nullptr;
     ~Handle() { sxen_trainer_destroy(h); }
   } trainer;
-  check(sxen_trainer_create(encoder.handle(), mlp.handle(), &trainer.h));  // width check, src/trainer.cpp:61-65
+  check(sxen_trainer_create_aux(encoder.handle(), mlp.handle(), cfg.aux_dims, &trainer.h));  // width check, :61-65
   const std::size_t batch = static_cast<std::size_t>(cfg.batch_size);
   const std::size_t dim = static_cast<std::size_t>(encoder.config().dim);
   const std::size_t out_w = static_cast<std::size_t>(mlp.config().output_width);
   // one batch slot: the sampler's work and the step's kernels are ordered on `stream`, so step k+1's sampler cannot
   // overwrite what step k's queued kernels still read
-  DeviceBuffer<double> coords(batch * dim, device), targets(batch * out_w, device);
+  const std::size_t aux_w = static_cast<std::size_t>(cfg.aux_dims);
+  DeviceBuffer<double> coords(batch * dim, device), targets(batch * out_w, device), aux(batch * aux_w, device);
+  if (aux_w > 0) check(sxen_trainer_set_aux(trainer.h, aux.data(), SXEN_COORD_F64));
   const sxen_adam_config ta = cfg.table_adam.c(), ma = cfg.mlp_adam.c();
   TrainResult result;
   std::vector<double> losses(static_cast<std::size_t>(cfg.queue_window));
   int first = 0;
   for (int step = 0; step < cfg.steps; ++step) {
-    sampler(step, coords.span(batch * dim), targets.span(batch * out_w), stream);
+    sampler(step, coords.span(batch * dim), aux.span(batch * aux_w), targets.span(batch * out_w), stream);
     check(sxen_trainer_step_enqueue(trainer.h, coords.data(), SXEN_COORD_F64, targets.data(), SXEN_COORD_F64, batch, &ta, &ma,
                                     stream));
     if (step + 1 - first == cfg.queue_window || step == cfg.steps - 1) {
@@ -245,7 +249,8 @@ inline FitImageResult fit_image(const ImageDataset& image, const EncoderConfig& 
   const int w = image.width, h = image.height;
   const std::uint64_t seed = train_cfg.seed;
   const double* px = image_dev.data();
-  const BatchSampler sampler = [=](int step, DeviceSpan<double> coords, DeviceSpan<double> targets, void* s) {  // :112-126
+  const BatchSampler sampler = [=](int step, DeviceSpan<double> coords, DeviceSpan<double> /*aux*/,
+                                   DeviceSpan<double> targets, void* s) {  // :112-126
     check(sxen_sample_image_batch(seed, static_cast<std::uint64_t>(step), px, w, h, coords.size / 2, coords.data,
                                   targets.data, s));
   };
@@ -314,7 +319,8 @@ inline FitFieldResult fit_field(const NoiseFieldSpec& spec, const EncoderConfig&
   const sxen_noise_spec cs = spec.c();
   const std::uint64_t seed = train_cfg.seed;
   const std::size_t dim = static_cast<std::size_t>(spec.dim);
-  const BatchSampler sampler = [=](int step, DeviceSpan<double> coords, DeviceSpan<double> targets, void* s) {  // :156-166
+  const BatchSampler sampler = [=](int step, DeviceSpan<double> coords, DeviceSpan<double> /*aux*/,
+                                   DeviceSpan<double> targets, void* s) {  // :156-166
     check(sxen_sample_field_batch(&cs, seed, 1, static_cast<std::uint64_t>(step), coords.size / dim, coords.data,
                                   targets.data, s));
   };

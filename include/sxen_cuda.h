@@ -307,6 +307,12 @@ SXEN_API sxen_status sxen_mse_loss(const float* pred_dev, size_t pred_stride, co
 typedef struct sxen_trainer sxen_trainer;
 /* Binds an encoder and an MLP (not owned) with a gradient accumulator, SparseAdamState and AdamState (owned). */
 SXEN_API sxen_status sxen_trainer_create(sxen_encoder* enc, sxen_mlp* mlp, sxen_trainer** out);
+/* TrainConfig::aux_dims (include/sxen/trainer.hpp:18): aux_dims extra inputs per sample appended verbatim after the encoding
+ * (src/trainer.cpp:32-35); the MLP's input width must be L*F + aux_dims (std::invalid_argument otherwise, :61-65).
+ * sxen_trainer_set_aux names the caller-owned N x aux_dims array (f64 or f32) the NEXT accumulate / step calls read; it
+ * must hold the batch those calls are given and stay valid until their stream work completes. */
+SXEN_API sxen_status sxen_trainer_create_aux(sxen_encoder* enc, sxen_mlp* mlp, int32_t aux_dims, sxen_trainer** out);
+SXEN_API sxen_status sxen_trainer_set_aux(sxen_trainer* trainer, const void* aux_dev, sxen_coord_type aux_type);
 SXEN_API sxen_status sxen_trainer_destroy(sxen_trainer* trainer);
 /* run_chunk over this rank's contiguous chunk: encode -> forward -> MSE -> backward -> encode_backward.  Table and MLP
  * gradients and the loss sum ACCUMULATE until sxen_trainer_update.  global_batch is the B of upstream = 2e/(B*out_w). */

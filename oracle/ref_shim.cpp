@@ -306,6 +306,32 @@ int sxr_train_field(void* eh, void* mh, const double* coords, const double* targ
   });
 }
 
+// train_field with pass-through inputs (TrainConfig::aux_dims, src/trainer.cpp:32-35,59-65): the sampler replays
+// caller-provided coords / aux / targets, one slab per step.
+int sxr_train_field_aux(void* eh, void* mh, const double* coords, const double* aux, int aux_dims, const double* targets,
+                        int steps, int batch, int threads, const AdamCfg* table_adam, const AdamCfg* mlp_adam,
+                        double* loss_out) {
+  auto* enc = static_cast<sxen::HashEncoder*>(eh);
+  auto* mlp = static_cast<sxen::Mlp*>(mh);
+  return guarded([&] {
+    sxen::TrainConfig tc;
+    tc.batch_size = batch;
+    tc.steps = steps;
+    tc.aux_dims = aux_dims;
+    tc.table_adam = to_ref(*table_adam);
+    tc.mlp_adam = to_ref(*mlp_adam);
+    tc.threads = threads;
+    tc.record_every = 1;
+    sxen::BatchSampler sampler = [&](int step, std::span<double> c, std::span<double> a, std::span<double> t) {
+      std::memcpy(c.data(), coords + static_cast<std::size_t>(step) * c.size(), c.size() * sizeof(double));
+      if (!a.empty()) std::memcpy(a.data(), aux + static_cast<std::size_t>(step) * a.size(), a.size() * sizeof(double));
+      std::memcpy(t.data(), targets + static_cast<std::size_t>(step) * t.size(), t.size() * sizeof(double));
+    };
+    const sxen::TrainResult r = sxen::train_field(*enc, *mlp, sampler, tc);
+    for (std::size_t i = 0; i < r.loss_curve.size(); ++i) loss_out[r.loss_curve[i].first] = r.loss_curve[i].second;
+  });
+}
+
 // ---- CPU baseline: the reference's worker pattern (src/trainer.cpp:104-116) restricted to the
 // encode + encode_backward pair, steady_clock around the fan-out (src/analysis.cpp:279-290).
 // Accumulators are allocated and cleared outside the timed region.  Returns seconds (<0 on error).

@@ -154,6 +154,8 @@ SIGNATURES = {
     "sxen_device_upload": (C.c_int, [_i32, _vp, _vp, _sz, _vp]),
     "sxen_device_download": (C.c_int, [_i32, _vp, _vp, _sz, _vp]),
     "sxen_device_zero": (C.c_int, [_i32, _vp, _sz, _vp]),
+    "sxen_trainer_create_aux": (C.c_int, [_vp, _vp, _i32, _P(_vp)]),
+    "sxen_trainer_set_aux": (C.c_int, [_vp, _vp, C.c_int]),
     "sxen_trainer_pending": (C.c_int, [_vp, _P(_sz)]),
     "sxen_trainer_collect": (C.c_int, [_vp, _P(_dbl), _sz, _P(_sz), _P(C.c_int64), _vp]),
 }

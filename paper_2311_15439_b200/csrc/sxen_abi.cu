@@ -238,10 +238,13 @@ sxen_status check_batch(const sxen_encoder* enc, const void* x, sxen_coord_type 
 
 // first_level / level_count select a contiguous range of encoder levels (count < 0 = all from first_level on): the
 // launch reads and writes only that range's slice of every feature / upstream row and of the accumulator.
+// row_stride > 0: feature / upstream rows are row_stride floats apart (>= L*F; the trainer's [encoding | aux] rows).
 sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, const float* upstream, size_t n,
                        float* out, sxen_grad* grad, int mode, cudaStream_t stream, int first_level = 0,
-                       int level_count = -1) {
+                       int level_count = -1, int row_stride = 0) {
   if (sxen_status st = check_batch(enc, x, type, n)) return st;
+  SXEN_REQUIRE(row_stride == 0 || row_stride >= enc->cfg.levels * enc->cfg.features,
+               "encode: row stride %d below the encoded width %d", row_stride, enc->cfg.levels * enc->cfg.features);
   if (level_count < 0) level_count = enc->cfg.levels - first_level;
   SXEN_REQUIRE(first_level >= 0 && level_count >= 0 && first_level + level_count <= enc->cfg.levels,
                "level range [%d, %d) outside the encoder's %d levels", first_level, first_level + level_count,
@@ -263,13 +266,16 @@ sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, c
     // stay L2-resident, where the fused kernel would need two (measured at T = 2^22, n = 3: 1.17 -> 0.84 ms).
     const size_t bytes = static_cast<size_t>(enc->cfg.levels) * enc->level_floats() * sizeof(float);
     if (mode == sxen_dev::kModeBoth && bytes >= (192ull << 20) && enc->tuning.level_major < 0) {
-      if (sxen_status st = run_encode(enc, x, type, nullptr, n, out, nullptr, sxen_dev::kModeFwd, stream, first_level, level_count))
+      if (sxen_status st = run_encode(enc, x, type, nullptr, n, out, nullptr, sxen_dev::kModeFwd, stream, first_level, level_count,
+                                      row_stride))
         return st;
-      return run_encode(enc, x, type, upstream, n, nullptr, grad, sxen_dev::kModeBwd, stream, first_level, level_count);
+      return run_encode(enc, x, type, upstream, n, nullptr, grad, sxen_dev::kModeBwd, stream, first_level, level_count,
+                        row_stride);
     }
   }
   EncodeArgs a;
   base_args(enc, x, type, n, a);
+  if (row_stride > 0) a.row_width = row_stride;
   a.upstream = upstream;
   a.out = out;
   a.grads = grad ? grad->values : nullptr;
@@ -370,6 +376,23 @@ __global__ void narrow_kernel(const double* __restrict__ src, float* __restrict_
 }
 
 }  // namespace
+
+// encode / encode_backward with feature rows `row_stride` floats apart (declared in sxen_common.hpp): the trainer's
+// [encoding | aux] MLP input rows, src/trainer.cpp:31-35,47.
+sxen_status sxen_encoder_encode_strided(sxen_encoder* enc, const void* x_dev, sxen_coord_type type, size_t n_samples,
+                                        float* out_dev, int row_stride, void* stream) {
+  SXEN_REQUIRE(enc != nullptr, "encoder handle is null");
+  return run_encode(enc, x_dev, type, nullptr, n_samples, out_dev, nullptr, sxen_dev::kModeFwd, as_stream(stream), 0, -1,
+                    row_stride);
+}
+
+sxen_status sxen_encoder_encode_backward_strided(sxen_encoder* enc, const void* x_dev, sxen_coord_type type,
+                                                 const float* upstream_dev, int row_stride, size_t n_samples,
+                                                 sxen_grad* grad, int first_level, int level_count, void* stream) {
+  SXEN_REQUIRE(enc != nullptr, "encoder handle is null");
+  return run_encode(enc, x_dev, type, upstream_dev, n_samples, nullptr, grad, sxen_dev::kModeBwd, as_stream(stream),
+                    first_level, level_count, row_stride);
+}
 
 // SparseAdamState::step for the single-GPU trainer (declared in sxen_common.hpp): when the batch is small against the
 // tables, the update walks the batch (sparse_adam_walk_kernel) instead of scanning all L*T accumulator rows.  The caller

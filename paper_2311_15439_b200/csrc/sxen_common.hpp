@@ -126,3 +126,10 @@ bool sxen_sparse_adam_walk_pays(const sxen_encoder* enc, size_t n_samples);
 sxen_status sxen_sparse_adam_step_walk(sxen_sparse_adam* opt, sxen_encoder* enc, sxen_grad* grad, const void* x_dev,
                                        sxen_coord_type type, size_t n_samples, const sxen_adam_config* cfg,
                                        const unsigned long long* gate_dev, void* stream);
+
+// Encode / encode_backward over feature rows `row_stride` floats apart (sxen_abi.cu), for the trainer's [encoding | aux] rows.
+sxen_status sxen_encoder_encode_strided(sxen_encoder* enc, const void* x_dev, sxen_coord_type type, size_t n_samples,
+                                        float* out_dev, int row_stride, void* stream);
+sxen_status sxen_encoder_encode_backward_strided(sxen_encoder* enc, const void* x_dev, sxen_coord_type type,
+                                                 const float* upstream_dev, int row_stride, size_t n_samples,
+                                                 sxen_grad* grad, int first_level, int level_count, void* stream);

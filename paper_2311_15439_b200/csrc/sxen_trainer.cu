@@ -33,6 +33,9 @@ struct sxen_trainer {
   size_t pending = 0;                // queued steps not collected yet
   bool foreign_grads = false;        // the accumulators may hold rows of batches other than the current step's
   int32_t out_w = 0, enc_w = 0;
+  int32_t aux_dims = 0, in_w = 0;    // TrainConfig::aux_dims; MLP input width = enc_w + aux_dims
+  const void* aux = nullptr;         // caller-owned N x aux_dims pass-through inputs of the next batch (sxen_trainer_set_aux)
+  sxen_coord_type aux_type = SXEN_COORD_F64;
   uint64_t mlp_params = 0;
 };
 
@@ -52,6 +55,17 @@ __global__ void loss_record_kernel(double* __restrict__ loss_sum, double* __rest
   *loss_sum = 0.0;
 }
 
+// src/trainer.cpp:32-35: the aux inputs follow the encoding in every MLP input row, narrowed to float
+template <typename T>
+__global__ void aux_fill_kernel(float* __restrict__ rows, int row_stride, int first_col, const T* __restrict__ aux,
+                                int aux_dims, size_t n) {
+  const size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n * static_cast<size_t>(aux_dims)) return;
+  const size_t s = e / static_cast<size_t>(aux_dims);
+  const int a = static_cast<int>(e - s * static_cast<size_t>(aux_dims));
+  rows[s * static_cast<size_t>(row_stride) + static_cast<size_t>(first_col + a)] = static_cast<float>(aux[e]);
+}
+
 sxen_status ensure_workspace(sxen_trainer* t, size_t n) {
   if (n <= t->capacity) return SXEN_OK;
   cudaFree(t->features);
@@ -61,8 +75,8 @@ sxen_status ensure_workspace(sxen_trainer* t, size_t n) {
   t->features = t->input_grad = nullptr;
   t->upstream = t->sample_loss = nullptr;
   t->capacity = 0;
-  SXEN_CUDA(cudaMalloc(&t->features, n * static_cast<size_t>(t->enc_w) * sizeof(float)));
-  SXEN_CUDA(cudaMalloc(&t->input_grad, n * static_cast<size_t>(t->enc_w) * sizeof(float)));
+  SXEN_CUDA(cudaMalloc(&t->features, n * static_cast<size_t>(t->in_w) * sizeof(float)));
+  SXEN_CUDA(cudaMalloc(&t->input_grad, n * static_cast<size_t>(t->in_w) * sizeof(float)));
   SXEN_CUDA(cudaMalloc(&t->upstream, n * static_cast<size_t>(t->out_w) * sizeof(double)));
   SXEN_CUDA(cudaMalloc(&t->sample_loss, (n + 1) * sizeof(double)));
   t->capacity = n;
@@ -98,21 +112,28 @@ sxen_status update_impl(sxen_trainer* t, const sxen_adam_config* table_adam, con
 extern "C" {
 
 sxen_status sxen_trainer_create(sxen_encoder* enc, sxen_mlp* mlp, sxen_trainer** out) {
+  return sxen_trainer_create_aux(enc, mlp, 0, out);
+}
+
+sxen_status sxen_trainer_create_aux(sxen_encoder* enc, sxen_mlp* mlp, int32_t aux_dims, sxen_trainer** out) {
   SXEN_REQUIRE(enc != nullptr && mlp != nullptr && out != nullptr, "null argument");
   *out = nullptr;
   sxen_encoder_config ec;
   sxen_encoder_get_config(enc, &ec);
   sxen_mlp_config mc;
   if (sxen_status st = sxen_mlp_get_config(mlp, &mc)) return st;
-  // src/trainer.cpp:61-65 (aux_dims = 0: this path feeds the encoding straight into the head)
-  SXEN_REQUIRE(mc.input_width == ec.levels * ec.features, "train: MLP input width %d != encoded width %d + aux 0",
-               mc.input_width, ec.levels * ec.features);
+  // src/trainer.cpp:59-65
+  SXEN_REQUIRE(aux_dims >= 0, "train: aux_dims must be >= 0");
+  SXEN_REQUIRE(mc.input_width == ec.levels * ec.features + aux_dims, "train: MLP input width %d != encoded width %d + aux %d",
+               mc.input_width, ec.levels * ec.features, aux_dims);
   sxen_trainer* t = new sxen_trainer();
   t->enc = enc;
   t->mlp = mlp;
   t->device = enc->device;
   t->out_w = mc.output_width;
   t->enc_w = ec.levels * ec.features;
+  t->aux_dims = aux_dims;
+  t->in_w = t->enc_w + aux_dims;
   DeviceGuard guard(t->device);
   sxen_status st = sxen_grad_create(enc, &t->grad);
   if (st == SXEN_OK) st = sxen_sparse_adam_create(enc, &t->table_opt);
@@ -157,6 +178,14 @@ sxen_status sxen_trainer_destroy(sxen_trainer* t) {
   return SXEN_OK;
 }
 
+sxen_status sxen_trainer_set_aux(sxen_trainer* t, const void* aux_dev, sxen_coord_type aux_type) {
+  SXEN_REQUIRE(t != nullptr, "trainer handle is null");
+  SXEN_REQUIRE(aux_dev == nullptr || t->aux_dims > 0, "train: this trainer was created with aux_dims = 0");
+  t->aux = aux_dev;
+  t->aux_type = aux_type;
+  return SXEN_OK;
+}
+
 sxen_status sxen_trainer_table_grad(sxen_trainer* t, sxen_grad** out) {
   SXEN_REQUIRE(t != nullptr && out != nullptr, "null argument");
   *out = t->grad;
@@ -178,8 +207,25 @@ sxen_status sxen_trainer_accumulate_head(sxen_trainer* t, const void* coords_dev
   if (n_samples == 0) return SXEN_OK;
   DeviceGuard guard(t->device);
   if (sxen_status st = ensure_workspace(t, n_samples)) return st;
-  // encoder.encode (src/trainer.cpp:31)
-  if (sxen_status st = sxen_encoder_encode(t->enc, coords_dev, coord_type, n_samples, t->features, stream)) return st;
+  if (t->aux_dims > 0 && t->aux == nullptr)
+    return fail(SXEN_LOGIC_ERROR, "train: aux_dims = %d but no aux inputs were set for this batch (sxen_trainer_set_aux)",
+                t->aux_dims);
+  // encoder.encode (src/trainer.cpp:31) into the first enc_w columns of the MLP input rows, aux inputs behind (:32-35)
+  if (sxen_status st = sxen_encoder_encode_strided(t->enc, coords_dev, coord_type, n_samples, t->features,
+                                                   t->aux_dims > 0 ? t->in_w : 0, stream))
+    return st;
+  if (t->aux_dims > 0) {
+    const size_t elems = n_samples * static_cast<size_t>(t->aux_dims);
+    const unsigned blocks = static_cast<unsigned>((elems + 255) / 256);
+    if (t->aux_type == SXEN_COORD_F32)
+      aux_fill_kernel<float><<<blocks, 256, 0, as_stream(stream)>>>(t->features, t->in_w, t->enc_w,
+                                                                   static_cast<const float*>(t->aux), t->aux_dims, n_samples);
+    else
+      aux_fill_kernel<double><<<blocks, 256, 0, as_stream(stream)>>>(t->features, t->in_w, t->enc_w,
+                                                                    static_cast<const double*>(t->aux), t->aux_dims, n_samples);
+    SXEN_CUDA(cudaGetLastError());
+    count_launch();
+  }
   // mlp.forward, loss + upstream, mlp.backward (:36-46): one fused call (tensor-core kernel or the exact chain)
   if (sxen_status st = sxen_mlp_forward_backward(t->mlp, t->features, targets_dev, target_type, n_samples, global_batch,
                                                  nullptr, t->input_grad, t->loss_sum, stream))
@@ -198,8 +244,8 @@ sxen_status sxen_trainer_accumulate_tables(sxen_trainer* t, const void* coords_d
                 n_samples, t->head_samples);
   DeviceGuard guard(t->device);
   // encoder.encode_backward on d(loss)/d(encoding) (:47), levels [first_level, first_level + level_count)
-  return sxen_encoder_encode_backward_levels(t->enc, coords_dev, coord_type, t->input_grad, n_samples, t->grad,
-                                             first_level, level_count, stream);
+  return sxen_encoder_encode_backward_strided(t->enc, coords_dev, coord_type, t->input_grad, t->aux_dims > 0 ? t->in_w : 0,
+                                              n_samples, t->grad, first_level, level_count, stream);
 }
 
 sxen_status sxen_trainer_accumulate(sxen_trainer* t, const void* coords_dev, sxen_coord_type coord_type,

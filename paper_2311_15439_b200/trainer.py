@@ -54,11 +54,26 @@ def chunk_bounds(batch: int, workers: int, worker: int) -> Tuple[int, int]:
 class Trainer:
     """Owns the gradient accumulator and both Adam states for one (encoder, mlp) pair."""
 
-    def __init__(self, encoder, mlp):
+    def __init__(self, encoder, mlp, aux_dims: int = 0):
+        """aux_dims: TrainConfig::aux_dims, extra inputs per sample appended after the encoding (src/trainer.cpp:32-35);
+        the MLP's input width must be encoded width + aux_dims (ValueError otherwise, :61-65)."""
         self._lib = _lib()
         self._h = C.c_void_p()
-        self.encoder, self.mlp = encoder, mlp
-        raise_for(self._lib, self._lib.sxen_trainer_create(encoder._h, mlp._h, C.byref(self._h)))
+        self.encoder, self.mlp, self.aux_dims = encoder, mlp, int(aux_dims)
+        self._aux = None
+        raise_for(self._lib, self._lib.sxen_trainer_create_aux(encoder._h, mlp._h, int(aux_dims), C.byref(self._h)))
+
+    def set_aux(self, aux) -> None:
+        """The [batch, aux_dims] CUDA tensor (f64 or f32) the next accumulate / step calls read; kept alive here."""
+        if aux is None:
+            self._aux = None
+            raise_for(self._lib, self._lib.sxen_trainer_set_aux(self._h, None, _abi.COORD_F64))
+            return
+        aux = aux.contiguous()
+        if aux.dim() != 2 or aux.shape[1] != self.aux_dims:
+            raise ValueError(f"train: aux must be [batch, {self.aux_dims}]")
+        self._aux = aux
+        raise_for(self._lib, self._lib.sxen_trainer_set_aux(self._h, C.c_void_p(aux.data_ptr()), self._typ(aux)))
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -226,13 +241,13 @@ def train_field(encoder, mlp, sampler: BatchSampler, cfg: TrainConfig, group=Non
         raise ValueError("train: batch_size must be >= 1")
     if cfg.steps < 0:
         raise ValueError("train: steps must be >= 0")
-    if cfg.aux_dims != 0:
-        raise ValueError("train: aux_dims must be 0 on the device path")
+    if cfg.aux_dims < 0:
+        raise ValueError("train: aux_dims must be >= 0")
     if cfg.record_every < 1:
         raise ValueError("train: record_every must be >= 1")
     if sampler is None:
         raise ValueError("train: sampler must be callable")
-    trainer = Trainer(encoder, mlp)
+    trainer = Trainer(encoder, mlp, cfg.aux_dims)
     distributed = False
     if group is not None:
         distributed = True
@@ -251,21 +266,40 @@ def train_field(encoder, mlp, sampler: BatchSampler, cfg: TrainConfig, group=Non
             result.loss_curve.append((step, loss))
         result.final_loss = loss
 
+    def draw(step: int):
+        """(coords, targets) from the sampler; with aux_dims > 0 it returns (coords, aux, targets) and the aux tensor is
+        handed to the trainer for this batch (BatchSampler's three spans, include/sxen/trainer.hpp:26-32)."""
+        got = sampler(step, cfg.batch_size)
+        if cfg.aux_dims > 0:
+            if len(got) != 3:
+                raise ValueError("train: with aux_dims > 0 the sampler returns (coords, aux, targets)")
+            coords, aux, targets = got
+            if aux.shape[0] != coords.shape[0]:
+                raise ValueError("train: aux batch size differs from coords")
+            trainer.set_aux(aux)
+            return coords, targets
+        return got[0], got[-1]
+
     if distributed:
+        if cfg.aux_dims > 0:
+            raise ValueError("train: aux_dims > 0 is single-GPU on the device path")
         for step in range(cfg.steps):
-            coords, targets = sampler(step, cfg.batch_size)
+            coords, targets = draw(step)
             record(step, trainer.distributed_step(coords, targets, cfg.table_adam, cfg.mlp_adam, group))
     else:
         # Single GPU: steps are queued back to back (no host round trip per step) and their losses read in windows;
         # the device gate keeps the reference's "throw before the update" for a non-finite loss.
         first = 0
+        keep = []   # aux tensors of the queued steps stay alive until their window is collected
         for step in range(cfg.steps):
-            coords, targets = sampler(step, cfg.batch_size)
+            coords, targets = draw(step)
+            keep.append(trainer._aux)
             trainer.step_enqueue(coords, targets, cfg.table_adam, cfg.mlp_adam)
             if step + 1 - first == QUEUE_WINDOW or step == cfg.steps - 1:
                 losses, _ = trainer.collect()
                 for k, loss in enumerate(losses):
                     record(first + k, loss)
                 first = step + 1
+                keep.clear()
     result.steps_run = cfg.steps
     return result

@@ -146,7 +146,7 @@ int main(int argc, char** argv) {
     EXPECT(throws_invalid([&] { fit_field(s2, cfg, tc, h1); }));
     HashEncoder enc(cfg);
     Mlp wrong(MlpConfig{cfg.encoded_width() + 1, 64, 2, 3});
-    EXPECT(throws_invalid([&] { train_field(enc, wrong, [](int, DeviceSpan<double>, DeviceSpan<double>, void*) {}, tc); }));
+    EXPECT(throws_invalid([&] { train_field(enc, wrong, [](int, DeviceSpan<double>, DeviceSpan<double>, DeviceSpan<double>, void*) {}, tc); }));
   }
 
   // a non-finite loss: TrainingError naming the step; the queued updates of that and the later steps were not applied
@@ -160,7 +160,7 @@ int main(int argc, char** argv) {
     const std::vector<float> params_before = mlp.parameters();
     const std::size_t batch = 512;
     std::vector<double> hx(batch * 2, 0.25), ht(batch * 3, std::numeric_limits<double>::quiet_NaN());
-    const BatchSampler nan_sampler = [&](int, DeviceSpan<double> coords, DeviceSpan<double> targets, void* s) {
+    const BatchSampler nan_sampler = [&](int, DeviceSpan<double> coords, DeviceSpan<double>, DeviceSpan<double> targets, void* s) {
       check(sxen_device_upload(0, coords.data, hx.data(), hx.size() * sizeof(double), s));
       check(sxen_device_upload(0, targets.data, ht.data(), ht.size() * sizeof(double), s));
     };
@@ -184,7 +184,7 @@ int main(int argc, char** argv) {
 
     // ... and at a later step: finite targets for steps 0-2, NaN from step 3 on -> "step 3", three losses usable
     std::vector<double> good(batch * 3, 0.5);
-    const BatchSampler late = [&](int step, DeviceSpan<double> coords, DeviceSpan<double> targets, void* s) {
+    const BatchSampler late = [&](int step, DeviceSpan<double> coords, DeviceSpan<double>, DeviceSpan<double> targets, void* s) {
       check(sxen_device_upload(0, coords.data, hx.data(), hx.size() * sizeof(double), s));
       check(sxen_device_upload(0, targets.data, (step < 3 ? good : ht).data(), ht.size() * sizeof(double), s));
     };
@@ -196,13 +196,39 @@ int main(int argc, char** argv) {
     }
     EXPECT(thrown);
     // the trainer stays usable afterwards
-    const BatchSampler fine = [&](int, DeviceSpan<double> coords, DeviceSpan<double> targets, void* s) {
+    const BatchSampler fine = [&](int, DeviceSpan<double> coords, DeviceSpan<double>, DeviceSpan<double> targets, void* s) {
       check(sxen_device_upload(0, coords.data, hx.data(), hx.size() * sizeof(double), s));
       check(sxen_device_upload(0, targets.data, good.data(), good.size() * sizeof(double), s));
     };
     const TrainResult ok = train_field(enc, mlp, fine, t3);
     EXPECT(ok.steps_run == 8 && std::isfinite(ok.final_loss));
     EXPECT(ok.loss_curve.front().second > ok.final_loss);
+  }
+  // tests/test_neural.cpp:439-462: encoder + aux widths against the head's input width
+  {
+    EncoderConfig ec;
+    ec.dim = 2;
+    ec.levels = 2;
+    ec.table_size = 1u << 6;
+    ec.features = 2;
+    ec.base_resolution = 4;
+    HashEncoder enc(ec);
+    Mlp mlp(MlpConfig{ec.encoded_width() + 1, 8, 1, 1});
+    TrainConfig t4;
+    t4.threads = 1;
+    EXPECT(throws_invalid(
+        [&] { train_field(enc, mlp, [](int, DeviceSpan<double>, DeviceSpan<double>, DeviceSpan<double>, void*) {}, t4); }));
+    t4.aux_dims = 1;  // now the widths line up
+    t4.steps = 3;
+    t4.batch_size = 4;
+    std::vector<double> c(8, 0.5), a(4, 0.7), tg(4, 0.1);
+    const BatchSampler ok = [&](int, DeviceSpan<double> coords, DeviceSpan<double> aux, DeviceSpan<double> targets, void* s) {
+      check(sxen_device_upload(0, coords.data, c.data(), c.size() * sizeof(double), s));
+      check(sxen_device_upload(0, aux.data, a.data(), a.size() * sizeof(double), s));
+      check(sxen_device_upload(0, targets.data, tg.data(), tg.size() * sizeof(double), s));
+    };
+    const TrainResult r = train_field(enc, mlp, ok, t4);
+    EXPECT(r.steps_run == 3 && std::isfinite(r.final_loss));
   }
   std::printf("launches %llu\n", static_cast<unsigned long long>(sxen_launch_count()));
   std::printf("train_tasks ok\n");

@@ -326,6 +326,39 @@ def task_cases(ref: Ref):
     print("task_cases written; reference final PSNR", psnr, "loss", loss[0], "->", loss[-1])
 
 
+def aux_cases(ref: Ref):
+    """train_field with pass-through inputs appended after the encoding (TrainConfig::aux_dims, src/trainer.cpp:32-35): 12
+    steps of 256 samples, 2 aux inputs, run by the reference on 1 thread; also the reference's own width-mismatch case
+    (tests/test_neural.cpp:439-462)."""
+    import ctypes as C
+    lib = ref.lib
+    cfg = Config(dim=2, levels=4, table_size=1 << 10, features=2, base_resolution=4, growth=2.0)
+    aux_dims = 2
+    mc = MlpConfig(cfg.encoded_width + aux_dims, 16, 2, 1)
+    steps, batch = 12, 256
+    coords = ref.rng_doubles(4321, 5, steps * batch * 2).reshape(steps, batch, 2)
+    aux = ref.rng_doubles(4321, 6, steps * batch * aux_dims, -1.0, 1.0).reshape(steps, batch, aux_dims)
+    targets = np.ascontiguousarray(0.5 + 0.25 * np.sin(5.0 * coords[..., :1]) + 0.25 * aux[..., :1] * aux[..., 1:2])
+    enc = ref.encoder(cfg)
+    enc.init_tables(42)
+    mlp = ref.mlp(mc)
+    mlp.init(ref.hash_combine(42, 1))
+    loss = np.zeros(steps)
+    ta, ma = AdamConfig(lr=1e-2).c(), AdamConfig(lr=1e-3).c()
+    lib.sxr_train_field_aux.restype = C.c_int
+    st = lib.sxr_train_field_aux(enc.h, mlp.h, coords.ctypes.data_as(C.POINTER(C.c_double)),
+                                 aux.ctypes.data_as(C.POINTER(C.c_double)), aux_dims,
+                                 targets.ctypes.data_as(C.POINTER(C.c_double)), steps, batch, 1, C.byref(ta), C.byref(ma),
+                                 loss.ctypes.data_as(C.POINTER(C.c_double)))
+    assert st == 0, ref.lib.sxr_last_error()
+    d = {"cfg": np.array([cfg.dim, cfg.levels, cfg.table_size, cfg.features, cfg.base_resolution], dtype=np.int64),
+         "growth": np.float64(cfg.growth), "aux_dims": np.int64(aux_dims), "mlp": np.array([mc.input_width, 16, 2, 1], dtype=np.int64),
+         "coords": coords, "aux": aux, "targets": targets, "loss": loss, "tables": enc.tables(),
+         "mlp_params": mlp.params().copy()}
+    np.savez_compressed(os.path.join(OUT, "aux_cases.npz"), **d)
+    print("aux_cases written; loss", loss[:3], "...", loss[-1])
+
+
 def acceptance_image_fitting(ref: Ref):
     """The reference's own acceptance criterion `image-fitting-parity` (tests/acceptance_main.cpp:315-341), run by the
     reference: make_test_image(512, 512, 7), L=8 T=2^16 F=2 base 4 growth 2 equal-memory, batch 512, 10 000 steps,
@@ -350,6 +383,9 @@ def acceptance_image_fitting(ref: Ref):
 if __name__ == "__main__":
     oracle.build(ref=True)
     ref = Ref()
+    if len(sys.argv) > 1 and sys.argv[1] == "aux":
+        aux_cases(ref)
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "acceptance":
         acceptance_image_fitting(ref)
         sys.exit(0)

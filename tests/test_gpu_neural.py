@@ -213,3 +213,63 @@ def test_overlapped_distributed_step_on_one_rank_equals_the_plain_step(sx):
     finally:
         if created:
             dist.destroy_process_group()
+
+
+def test_training_with_aux_inputs_matches_reference_run(sx):
+    """TrainConfig::aux_dims (src/trainer.cpp:32-35,59-65): pass-through inputs appended after the encoding.  Against the
+    reference's own 12-step run with 2 aux inputs (tests/golden/aux_cases.npz, make_golden.py aux): first loss rel 1e-13,
+    loss curve rel 1e-3, final tables / parameters close; the width rule and the missing-aux error as the reference's
+    test (tests/test_neural.cpp:439-462)."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "aux_cases.npz"))
+    c = g["cfg"]
+    cfg = sx.EncoderConfig(dim=int(c[0]), levels=int(c[1]), table_size=int(c[2]), features=int(c[3]),
+                           base_resolution=int(c[4]), growth=float(g["growth"]))
+    aux_dims = int(g["aux_dims"])
+    mc = sx.MlpConfig(*[int(v) for v in g["mlp"]])
+    coords, aux, targets = g["coords"], g["aux"], g["targets"]
+    steps, batch = coords.shape[0], coords.shape[1]
+
+    def run(aux_dtype, per_step):
+        enc = sx.HashEncoder(cfg)
+        enc.init_tables(42)
+        mlp = sx.Mlp(mc)
+        mlp.init_params(sx.hash_combine(42, 1))
+        if per_step:   # the per-step entry point
+            tr = sx.Trainer(enc, mlp, aux_dims)
+            loss = []
+            for s in range(steps):
+                tr.set_aux(dev(aux[s]).to(aux_dtype))
+                loss.append(tr.step(dev(coords[s]), dev(targets[s]), sx.AdamConfig(lr=1e-2), sx.AdamConfig(lr=1e-3)))
+            return enc, mlp, np.array(loss)
+
+        def sampler(step, b):
+            assert b == batch
+            return dev(coords[step]), dev(aux[step]).to(aux_dtype), dev(targets[step])
+
+        res = sx.train_field(enc, mlp, sampler, sx.TrainConfig(batch_size=batch, steps=steps, record_every=1,
+                                                               aux_dims=aux_dims))
+        return enc, mlp, np.array([v for _, v in res.loss_curve])
+
+    ref = g["loss"]
+    for aux_dtype, per_step in ((torch.float64, False), (torch.float64, True), (torch.float32, False)):
+        enc, mlp, loss = run(aux_dtype, per_step)
+        assert abs(loss[0] - ref[0]) <= 1e-13 * ref[0], (aux_dtype, per_step)   # aux is narrowed to float either way (:33)
+        assert np.all(np.abs(loss - ref) <= 1e-3 * ref), (loss, ref)
+        tabs = np.stack([enc.table(l) for l in range(cfg.levels)])
+        assert (np.abs(tabs - g["tables"]) <= 1e-6).mean() >= 0.99
+        assert np.abs(mlp.parameters() - g["mlp_params"]).max() <= 1e-4
+
+    enc = sx.HashEncoder(cfg)
+    mlp = sx.Mlp(mc)
+    with pytest.raises(ValueError, match="encoded width"):
+        sx.Trainer(enc, mlp)                       # aux_dims = 0: widths do not line up
+    with pytest.raises(ValueError, match="encoded width"):
+        sx.Trainer(enc, mlp, aux_dims + 1)
+    with pytest.raises(ValueError):
+        sx.Trainer(enc, mlp, -1)
+    tr = sx.Trainer(enc, mlp, aux_dims)
+    with pytest.raises(RuntimeError, match="no aux inputs"):
+        tr.step(dev(coords[0]), dev(targets[0]), sx.AdamConfig(), sx.AdamConfig())
+    with pytest.raises(ValueError):
+        tr.set_aux(dev(aux[0][:, :1]))

@@ -234,6 +234,48 @@ inline double render_mse(const HashEncoder& encoder, Mlp& mlp, DeviceSpan<const 
   return sum / (3.0 * static_cast<double>(total));
 }
 
+// sxen::render_image (src/tasks.cpp:51-96): the fitted model at every pixel centre, clamped to [0, 1].  `threads` is
+// accepted and ignored (the rows are one device batch per chunk).
+inline ImageDataset render_image(const HashEncoder& encoder, Mlp& mlp, int width, int height, int /*threads*/ = 0,
+                                 int device = 0, void* stream = nullptr, std::size_t chunk = std::size_t{1} << 20) {
+  if (encoder.config().dim != 2) throw std::invalid_argument("render_image: encoder dim must be 2");
+  if (mlp.config().input_width != encoder.config().encoded_width() || mlp.config().output_width != 3)
+    throw std::invalid_argument("render_image: model widths do not form a 2D->RGB map");
+  if (width < 1 || height < 1) throw std::invalid_argument("image: width and height must be >= 1");
+  ImageDataset out;
+  out.width = width;
+  out.height = height;
+  const std::size_t total = static_cast<std::size_t>(width) * static_cast<std::size_t>(height);
+  out.pixels.resize(3 * total);
+  const std::size_t step = std::min(chunk, total);
+  const std::size_t enc_w = static_cast<std::size_t>(encoder.config().encoded_width());
+  DeviceBuffer<double> coords(step * 2, device);
+  DeviceBuffer<float> feats(step * enc_w, device), pred(step * 3, device);
+  for (std::size_t first = 0; first < total; first += step) {
+    const std::size_t n = std::min(step, total - first);
+    check(sxen_pixel_centers(width, height, first, n, coords.data(), stream));
+    encoder.encode(coords.cspan(n * 2), feats.span(n * enc_w), stream);
+    mlp.forward(feats.cspan(n * enc_w), pred.span(n * 3), stream);
+    const std::vector<float> p = pred.download(n * 3, stream);
+    for (std::size_t i = 0; i < n * 3; ++i) out.pixels[first * 3 + i] = std::clamp(static_cast<double>(p[i]), 0.0, 1.0);
+  }
+  encoder.check_async(stream);
+  return out;
+}
+
+// src/tasks.cpp:35-49
+inline double image_mse(const ImageDataset& a, const ImageDataset& b) {
+  if (a.width != b.width || a.height != b.height || a.pixels.size() != b.pixels.size())
+    throw std::invalid_argument("image_mse: shape mismatch");
+  double sum = 0.0;
+  for (std::size_t i = 0; i < a.pixels.size(); ++i) {
+    const double e = a.pixels[i] - b.pixels[i];
+    sum += e * e;
+  }
+  return sum / static_cast<double>(a.pixels.size());
+}
+inline double image_psnr(const ImageDataset& a, const ImageDataset& b) { return psnr_from_mse(image_mse(a, b)); }
+
 // sxen::fit_image (src/tasks.cpp:98-137)
 inline FitImageResult fit_image(const ImageDataset& image, const EncoderConfig& encoder_cfg, const TrainConfig& train_cfg,
                                 const FitImageOptions& opt = {}, int device = 0, void* stream = nullptr) {

@@ -16,8 +16,8 @@ from .mlp import Mlp, MlpConfig  # noqa: E402
 from .trainer import TrainConfig, Trainer, TrainResult, chunk_bounds, level_ranges, train_field  # noqa: E402
 from .checkpoint import load_checkpoint, save_checkpoint  # noqa: E402
 from .tasks import (FitFieldOptions, FitFieldResult, FitImageOptions, FitImageResult, NoiseFieldSpec, NoiseKind,  # noqa: E402
-                    field_sampler, fit_field, fit_image, image_sampler, make_test_image, noise_field_value, psnr_from_mse,
-                    render_mse)
+                    field_sampler, fit_field, fit_image, image_mse, image_psnr, image_sampler, make_test_image,
+                    noise_field_value, psnr_from_mse, render_image, render_mse)
 from .rng import CounterRng, hash_combine, mix64  # noqa: E402
 from .analysis import (KernelBenchConfig, KernelBenchReport, bench_kernel, bench_side, read_kernel_csv,  # noqa: E402
                        write_kernel_csv)
@@ -26,7 +26,7 @@ __all__ = ["lib", "CudaError", "IoError", "TrainingError", "Backend", "LevelScal
            "EncoderGradient", "LookupCounters", "Tuning", "equal_memory_multiplier", "level_resolution",
            "skew_constants", "hash_coords", "AdamConfig", "AdamState", "SparseAdamState", "CounterRng", "mix64",
            "hash_combine", "Mlp", "MlpConfig", "TrainConfig", "Trainer", "TrainResult", "chunk_bounds", "level_ranges", "train_field",
-           "FitImageOptions", "FitImageResult", "fit_image", "image_sampler", "psnr_from_mse", "render_mse",
+           "FitImageOptions", "FitImageResult", "fit_image", "image_sampler", "psnr_from_mse", "render_mse", "render_image", "image_mse", "image_psnr",
            "save_checkpoint", "load_checkpoint", "KernelBenchConfig", "KernelBenchReport", "bench_kernel", "bench_side",
            "read_kernel_csv", "write_kernel_csv", "NoiseKind", "NoiseFieldSpec", "noise_field_value", "field_sampler",
            "FitFieldOptions", "FitFieldResult", "fit_field", "make_test_image"]

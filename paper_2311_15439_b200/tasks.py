@@ -100,6 +100,44 @@ def render_mse(encoder: HashEncoder, mlp: Mlp, image_dev, width: int, height: in
     return float(acc.item()) / (3.0 * total)
 
 
+def render_image(encoder: HashEncoder, mlp: Mlp, width: int, height: int, threads: int = 0, chunk: int = 1 << 20) -> np.ndarray:
+    """sxen::render_image (src/tasks.cpp:51-96): the fitted model at every pixel centre, clamped to [0, 1], as a
+    [height, width, 3] float64 array (ImageDataset::pixels order).  `threads` has no device meaning."""
+    import torch
+    if encoder.config.dim != 2:
+        raise ValueError("render_image: encoder dim must be 2")
+    if mlp.config.input_width != encoder.config.encoded_width() or mlp.config.output_width != 3:
+        raise ValueError("render_image: model widths do not form a 2D->RGB map")
+    if width < 1 or height < 1:
+        raise ValueError("image: width and height must be >= 1")
+    lib = _lib()
+    dev = torch.device(f"cuda:{encoder.device}")
+    total = width * height
+    out = np.empty((total, 3), dtype=np.float64)
+    stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    coords = torch.empty((min(chunk, total), 2), dtype=torch.float64, device=dev)
+    for first in range(0, total, chunk):
+        n = min(chunk, total - first)
+        raise_for(lib, lib.sxen_pixel_centers(width, height, first, n, C.c_void_p(coords.data_ptr()), stream))
+        pred = mlp.forward(encoder.encode(coords[:n]))
+        out[first:first + n] = pred.double().clamp_(0.0, 1.0).cpu().numpy()
+    encoder.check()
+    return out.reshape(height, width, 3)
+
+
+def image_mse(a: np.ndarray, b: np.ndarray) -> float:
+    """src/tasks.cpp:35-45"""
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    if a.shape != b.shape:
+        raise ValueError("image_mse: shape mismatch")
+    e = (a - b).ravel()
+    return float(np.dot(e, e)) / e.size
+
+
+def image_psnr(a: np.ndarray, b: np.ndarray) -> float:
+    return psnr_from_mse(image_mse(a, b))
+
+
 def fit_image(image, encoder_cfg: EncoderConfig, train_cfg: TrainConfig, opt: FitImageOptions = None,
               device: int = 0) -> FitImageResult:
     """sxen::fit_image (src/tasks.cpp:98-137): image is [h, w, 3] in [0, 1]."""

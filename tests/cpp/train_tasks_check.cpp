@@ -59,10 +59,15 @@ int main(int argc, char** argv) {
   // fit_image, exact head, losses read back every step and in windows of 64: the same training run
   for (int window : {1, 64}) {
     tc.queue_window = window;
-    const FitImageResult r = fit_image(img, cfg, tc);
+    FitImageResult r = fit_image(img, cfg, tc);
     EXPECT(r.train.steps_run == tc.steps && r.train.loss_curve.size() == static_cast<std::size_t>(tc.steps));
     EXPECT(r.psnr_curve.size() == r.train.loss_curve.size());
     EXPECT(r.train.final_loss == r.train.loss_curve.back().second);
+    if (window == 1) {  // render_image + image_psnr == the fused error sum behind final_psnr (src/tasks.cpp:35-96)
+      const ImageDataset rendered = render_image(r.encoder, r.mlp, img.width, img.height);
+      EXPECT(rendered.pixels.size() == img.pixels.size());
+      EXPECT(std::abs(image_psnr(rendered, img) - r.final_psnr) <= 1e-9);
+    }
     print_curve(window == 1 ? "fit_image_w1_loss" : "fit_image_w64_loss", r.train);
     std::printf("%s %.17g\n", window == 1 ? "fit_image_w1_psnr" : "fit_image_w64_psnr", r.final_psnr);
   }

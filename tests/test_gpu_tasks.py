@@ -64,6 +64,12 @@ def test_render_of_reference_model_reproduces_reference_psnr(sx, golden_task):
     image_dev = torch.as_tensor(img, device="cuda:0")
     psnr = sx.psnr_from_mse(sx.render_mse(enc, mlp, image_dev, img.shape[1], img.shape[0], chunk=1000))
     assert abs(psnr - float(g["final_psnr"])) <= 1e-6
+    # render_image + image_psnr (src/tasks.cpp:35-96) give the same number as the fused error sum, and clamp to [0, 1]
+    rendered = sx.render_image(enc, mlp, img.shape[1], img.shape[0], chunk=777)
+    assert rendered.shape == img.shape and rendered.min() >= 0.0 and rendered.max() <= 1.0
+    assert abs(sx.image_psnr(rendered, img) - float(g["final_psnr"])) <= 1e-6
+    with pytest.raises(ValueError, match="shape mismatch"):
+        sx.image_mse(rendered, img[:-1])
     mlp.set_precision(1)  # tensor-core head: same model, PSNR within 0.01 dB
     psnr_tc = sx.psnr_from_mse(sx.render_mse(enc, mlp, image_dev, img.shape[1], img.shape[0]))
     assert abs(psnr_tc - float(g["final_psnr"])) <= 1e-2

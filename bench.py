@@ -148,6 +148,48 @@ def cpu_reference_run(n: int, samples: int, threads: int, t_log2: int = T_LOG2):
     return samples / secs, kind
 
 
+def cpu_reference_train_step(n: int, batch: int, threads: int, t_log2: int = T_LOG2):
+    """The reference's own train_field (src/trainer.cpp:53-139: encode -> Mlp::forward -> MSE -> Mlp::backward ->
+    encode_backward -> sparse Adam + Adam) on `threads` workers at `batch` samples per step of the bench workload's shape.
+    Seconds per step = (wall clock of a 3-step run - wall clock of a 1-step run) / 2, which leaves out the per-run set-up
+    (every worker's dense fp64 accumulator, the moments).  None when the compiled reference is not there."""
+    one = _cpu_reference_train_run(n, batch, threads, 1, t_log2)
+    three = _cpu_reference_train_run(n, batch, threads, 3, t_log2)
+    if one is None or three is None or three <= one:
+        return None
+    return (three - one) / 2.0
+
+
+def _cpu_reference_train_run(n: int, batch: int, threads: int, steps: int, t_log2: int):
+    import ctypes as C
+    import time
+
+    import numpy as np
+
+    import oracle
+    if not oracle.Ref.available():
+        return None
+    cfg = oracle.Config(dim=n, levels=L, table_size=1 << t_log2, features=F, base_resolution=BASE, growth=GROWTH[n])
+    ref = oracle.Ref()
+    enc = ref.encoder(cfg)
+    enc.init_tables(42)
+    mlp = ref.mlp(oracle.MlpConfig(L * F, 64, 2, 3))
+    mlp.init(ref.hash_combine(42, 1))
+    o = oracle.Oracle()
+    coords = o.rng_doubles(99, 1, steps * batch * n)
+    targets = o.rng_doubles(5, 3, steps * batch * 3)
+    loss = np.zeros(steps)
+    ta, ma = oracle.AdamConfig(lr=1e-2).c(), oracle.AdamConfig(lr=1e-3).c()
+    t0 = time.perf_counter()
+    st = ref.lib.sxr_train_field(enc.h, mlp.h, coords.ctypes.data_as(C.POINTER(C.c_double)),
+                                 targets.ctypes.data_as(C.POINTER(C.c_double)), steps, batch, threads, C.byref(ta),
+                                 C.byref(ma), loss.ctypes.data_as(C.POINTER(C.c_double)))
+    dt = time.perf_counter() - t0
+    if st != 0 or not np.isfinite(loss).all():
+        return None
+    return dt
+
+
 def host_threads() -> int:
     cores = os.cpu_count() or 1
     try:
@@ -514,6 +556,15 @@ def run_ours(args):
                     qms = e0.elapsed_time(e1) / reps
                     train[key] = {"batch": nb, "ms_per_step": qms, "samples_per_s": nb / (qms * 1e-3)}
                 del tr, mlp
+                if rank == 0 and world == 1 and not args.no_cpu:
+                    # the reference's own train_field on the host cores, bounded: 2 steps of 2^16 samples
+                    th = host_threads()
+                    sec = cpu_reference_train_step(n, 1 << 16, th, t_log2=args.log2t)
+                    if sec is not None:
+                        train["cpu_reference"] = {"batch": 1 << 16, "cores": th, "ms_per_step": sec * 1e3,
+                                                  "samples_per_s": (1 << 16) / sec,
+                                                  "what": "the unmodified reference's train_field (oracle/_ref): (3-step run - "
+                                                          "1-step run) / 2, wall clock"}
             except Exception as exc:
                 train = {"error": str(exc)}
 

@@ -273,3 +273,49 @@ def test_training_with_aux_inputs_matches_reference_run(sx):
         tr.step(dev(coords[0]), dev(targets[0]), sx.AdamConfig(), sx.AdamConfig())
     with pytest.raises(ValueError):
         tr.set_aux(dev(aux[0][:, :1]))
+
+
+def test_random_trainer_shapes_match_the_oracle(sx, oracle_lib):
+    """Seeded fuzz of the gradient pass of one training step (run_chunk, src/trainer.cpp:20-49) over encoder and head
+    shapes the fixed cases do not visit: dim 1..6, F in {1, 2, 4}, 1..3 hidden layers of odd widths, 1..4 outputs, ragged
+    batches, a global batch larger than the local chunk (a rank's share).  Exact head: loss rel 1e-12, MLP gradients rel
+    1e-9, table gradients within the fp32-atomics bar, touched sets exact."""
+    rng = np.random.default_rng(77)
+    for case in range(24):
+        n = int(rng.integers(1, 7))
+        cfg = oracle.Config(dim=n, levels=int(rng.integers(1, 9)), table_size=1 << int(rng.integers(6, 13)),
+                            features=int(rng.choice([1, 2, 2, 4])), base_resolution=int(rng.integers(2, 12)),
+                            growth=float(rng.choice([1.3, 1.5, 2.0])), backend=int(rng.integers(0, 2)) if n <= 4 else 0)
+        assert oracle_lib.validate(cfg) == 0
+        layers = int(rng.integers(1, 4))
+        mc = oracle.MlpConfig(cfg.encoded_width, int(rng.choice([8, 16, 33, 64])), layers, int(rng.integers(1, 5)))
+        seed = int(rng.integers(1, 1 << 30))
+        tables = oracle_lib.init_tables(cfg, seed)
+        tables = (tables.astype(np.float64) * 2000.0).astype(np.float32)   # O(0.1) features: every layer's ReLU is exercised
+        params = oracle_lib.mlp_init(mc, seed + 1)
+        B = int(rng.integers(1, 300))
+        global_batch = B + int(rng.integers(0, 3)) * 17
+        x = rng.random((B, n))
+        x[rng.random((B, n)) < 0.02] = 1.0
+        tgt = rng.random((B, mc.output_width))
+        loss, wtg, wtouched, wmg, _ = oracle_lib.train_grads(cfg, mc, tables, params, x, tgt, global_batch)
+        enc = sx.HashEncoder(sx.EncoderConfig(dim=cfg.dim, levels=cfg.levels, table_size=cfg.table_size,
+                                              features=cfg.features, base_resolution=cfg.base_resolution,
+                                              growth=cfg.growth, backend=cfg.backend))
+        for l in range(cfg.levels):
+            enc.set_table(l, tables[l])
+        mlp = sx.Mlp(sx.MlpConfig(mc.input_width, mc.hidden_width, mc.hidden_layers, mc.output_width))
+        mlp.set_parameters(params)
+        tr = sx.Trainer(enc, mlp)
+        tr.accumulate(dev(x), dev(tgt), global_batch)
+        tag = (case, cfg, mc, B, global_batch)
+        # both divide this chunk's sum by (global_batch * out_w), as the reference does once all chunks are in (:120)
+        got_loss = tr.loss(global_batch)
+        assert abs(got_loss - loss) <= 1e-12 * abs(loss), tag
+        assert np.allclose(mlp.gradient(), wmg, rtol=1e-9, atol=1e-18), tag
+        g = tr.table_grad_device().cpu().numpy().reshape(cfg.levels, cfg.table_size, cfg.features)
+        touched = (g[..., 0].view(np.uint32) != 0x80000000).astype(np.uint8)
+        assert np.array_equal(touched, wtouched), tag
+        vals = np.where(touched[..., None].astype(bool), g, 0.0)
+        scale = np.abs(wtg).max() + 1e-30
+        assert np.abs(vals - wtg).max() <= 2e-5 * scale, (tag, np.abs(vals - wtg).max() / scale)

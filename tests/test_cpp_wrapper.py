@@ -32,3 +32,20 @@ def test_cpp_trainer_mirror_builds(tmp_path):
     assert run.returncode == 2 and "usage" in run.stdout
     needed = subprocess.run(["readelf", "-d", exe], capture_output=True, text=True).stdout
     assert "libsxen_b200.so" in needed and "libcudart" not in needed
+
+
+def _build_analysis_check(tmp_path):
+    lib_dir = os.path.join(ROOT, "paper_2311_15439_b200", "lib")
+    exe = str(tmp_path / "analysis_check")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "analysis_check.cpp"), "-o", exe, "-L", lib_dir,
+                    "-lsxen_b200", f"-Wl,-rpath,{lib_dir}"], check=True)
+    return exe
+
+
+def test_cpp_analysis_mirror_host_part(tmp_path):
+    """include/sxen_b200_analysis.hpp: bench_side, the reference's kernel CSV schema (round trip bit-exact, the reference's
+    rejections as IoError) and bench_kernel's argument checks -- no device needed."""
+    exe = _build_analysis_check(tmp_path)
+    run = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True)
+    assert run.returncode == 0 and "analysis ok" in run.stdout, run.stdout + run.stderr

@@ -225,3 +225,16 @@ def test_small_batch_table_update_walks_the_batch_like_the_scan(sx, backend):
         assert np.array_equal((c != init[l]).any(axis=1), changed), l
         assert np.allclose(a, b, rtol=1e-3, atol=1e-6) and np.allclose(c, b, rtol=1e-3, atol=1e-6)
     assert np.allclose(m1.parameters(), m2.parameters(), rtol=1e-3, atol=1e-6)
+
+
+def test_cpp_bench_kernel_protocol(sx, tmp_path):
+    """include/sxen_b200_analysis.hpp on the device: the reference's bench-kernel protocol (src/analysis.cpp:233-313) from a
+    C++ host program -- exact vertices per sample (n+1 simplex, 2^n grid), cells = side^n, a resolved time."""
+    lib_dir = os.path.join(ROOT, "paper_2311_15439_b200", "lib")
+    exe = str(tmp_path / "analysis_check")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "analysis_check.cpp"), "-o", exe, "-L", lib_dir,
+                    "-lsxen_b200", f"-Wl,-rpath,{lib_dir}"], check=True)
+    run = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=600)
+    assert run.returncode == 0 and run.stdout.strip().endswith("analysis ok"), run.stdout + run.stderr
+    assert run.stdout.count("bench_kernel n=") == 6

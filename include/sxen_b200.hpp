@@ -312,6 +312,10 @@ class Mlp {
     check(sxen_mlp_download_params(h_, p.data()));
     return p;
   }
+  void set_parameters(std::span<const float> values) {
+    if (values.size() != parameter_count()) throw std::invalid_argument("mlp: parameter count mismatch");
+    check(sxen_mlp_upload_params(h_, values.data()));
+  }
   void forward(DeviceSpan<const float> input, DeviceSpan<float> out, void* stream = nullptr) {
     check(sxen_mlp_forward(h_, input.data, input.size / static_cast<std::size_t>(cfg_.input_width), out.data, stream));
   }

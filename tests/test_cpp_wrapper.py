@@ -49,3 +49,15 @@ def test_cpp_analysis_mirror_host_part(tmp_path):
     exe = _build_analysis_check(tmp_path)
     run = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True)
     assert run.returncode == 0 and "analysis ok" in run.stdout, run.stdout + run.stderr
+
+
+def test_cpp_checkpoint_mirror_host_part(tmp_path):
+    """include/sxen_b200_checkpoint.hpp: the rejections load_checkpoint decides before any device object exists
+    (src/checkpoint.cpp:114-130) raise IoError -- no device needed."""
+    lib_dir = os.path.join(ROOT, "paper_2311_15439_b200", "lib")
+    exe = str(tmp_path / "checkpoint_check")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "checkpoint_check.cpp"), "-o", exe, "-L", lib_dir,
+                    "-lsxen_b200", f"-Wl,-rpath,{lib_dir}"], check=True)
+    run = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True)
+    assert run.returncode == 0 and "checkpoint ok" in run.stdout, run.stdout + run.stderr

@@ -238,3 +238,18 @@ def test_cpp_bench_kernel_protocol(sx, tmp_path):
     run = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=600)
     assert run.returncode == 0 and run.stdout.strip().endswith("analysis ok"), run.stdout + run.stderr
     assert run.stdout.count("bench_kernel n=") == 6
+
+
+def test_cpp_checkpoint_round_trip_of_reference_files(sx, tmp_path):
+    """include/sxen_b200_checkpoint.hpp on the device: the reference-written fixtures (tests/golden/ref_checkpoint*.sxen,
+    src/checkpoint.cpp:81-112) load and re-save byte for byte from a C++ host program; truncated files, trailing bytes and
+    a bad MLP magic raise IoError; a device-written grid / F=4 model reads back identically."""
+    lib_dir = os.path.join(ROOT, "paper_2311_15439_b200", "lib")
+    exe = str(tmp_path / "checkpoint_check")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "checkpoint_check.cpp"), "-o", exe, "-L", lib_dir,
+                    "-lsxen_b200", f"-Wl,-rpath,{lib_dir}"], check=True)
+    gold = os.path.join(ROOT, "tests", "golden")
+    run = subprocess.run([exe, str(tmp_path), os.path.join(gold, "ref_checkpoint.sxen"),
+                          os.path.join(gold, "ref_checkpoint_nomlp.sxen")], capture_output=True, text=True, timeout=600)
+    assert run.returncode == 0 and run.stdout.strip().endswith("checkpoint ok"), run.stdout + run.stderr

@@ -457,6 +457,13 @@ def run_ours(args):
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic_for(f"{dom}_n{n}" + ("_grid" if args.backend == "grid" else "")), "peak_source": peak_src,
                 "alg_bytes_per_sample": dom_bytes, "kernel_ms": kms, **parts}
+    if args.path == "fused" and args.backend == "simplex" and n == 3 and args.log2t == T_LOG2:
+        # diagnostic next to the contract's HBM figure: what actually binds is the L2 request rate.
+        # 137 tag lookups per sample (52 gathers + 56 reds + 28 reds forwarded between the dies + 1 write, ncu); the peak
+        # is a pure random-gather kernel's rate on this chip (tools/ubench/tma_path.cu, profiles/r1s3_ubench_tma_path.log)
+        roofline["l2_requests"] = {"lookups_per_sample": 137, "achieved_G_per_s": 137 * N / (kms * 1e-3) / 1e9,
+                                   "measured_random_gather_peak_G_per_s": 278.6,
+                                   "frac": 137 * N / (kms * 1e-3) / 1e9 / 278.6}
 
     line = None
     if rank == 0:

@@ -458,12 +458,15 @@ def run_ours(args):
                 "frac": achieved / peak, "traffic": traffic_for(f"{dom}_n{n}" + ("_grid" if args.backend == "grid" else "")), "peak_source": peak_src,
                 "alg_bytes_per_sample": dom_bytes, "kernel_ms": kms, **parts}
     if args.path == "fused" and args.backend == "simplex" and n == 3 and args.log2t == T_LOG2:
-        # diagnostic next to the contract's HBM figure: what actually binds is the L2 request rate.
-        # 137 tag lookups per sample (52 gathers + 56 reds + 28 reds forwarded between the dies + 1 write, ncu); the peak
-        # is a pure random-gather kernel's rate on this chip (tools/ubench/tma_path.cu, profiles/r1s3_ubench_tma_path.log)
-        roofline["l2_requests"] = {"lookups_per_sample": 137, "achieved_G_per_s": 137 * N / (kms * 1e-3) / 1e9,
-                                   "measured_random_gather_peak_G_per_s": 278.6,
-                                   "frac": 137 * N / (kms * 1e-3) / 1e9 / 278.6}
+        # diagnostic next to the contract's HBM figure: what binds is the request rate at both ends of the crossbar
+        # (DESIGN.md 3.2).  From the SMs: ~110 requests per sample (52 gathers + 56 reds + the streamed rows); at the L2:
+        # 137 tag lookups (28 reds are forwarded between the dies).  The SM-side ceiling is a pure random-gather kernel's
+        # rate on this chip, 0.96 of one request per clock per SM (tools/ubench/tma_path.cu,
+        # profiles/r1s3_ubench_tma_path.log).
+        rate = N / (kms * 1e-3) / 1e9
+        roofline["requests"] = {"sm_requests_per_sample": 110, "sm_request_rate_G_per_s": 110 * rate,
+                                "measured_sm_request_peak_G_per_s": 278.6, "sm_frac": 110 * rate / 278.6,
+                                "l2_lookups_per_sample": 137, "l2_lookup_rate_G_per_s": 137 * rate}
 
     line = None
     if rank == 0:

@@ -543,6 +543,25 @@ def run_ours(args):
                 cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
                        "sample": f"{samples} samples of the same workload (same RNG streams), reference worker pattern: "
                                  f"encode+encode_backward per contiguous chunk into a per-thread accumulator"}
+                # parity in the same run: the first 2^16 samples of this run's inputs through the device
+                # path against the CPU checker -- vertex indices, weights and features bit for bit
+                try:
+                    import oracle
+                    sub = 1 << 16
+                    ocfg = oracle.Config(dim=n, levels=L, table_size=1 << args.log2t, features=F, base_resolution=BASE,
+                                         growth=GROWTH[n])
+                    o = oracle.Oracle()
+                    xsub = xs[0][:sub].contiguous()
+                    xh = xsub.double().cpu().numpy()
+                    oi, ow, _, _, _ = o.encode_debug(ocfg, xh)
+                    gi, gw = enc.encode_debug(xsub)
+                    want, _bad = o.encode(ocfg, o.init_tables(ocfg, 42), xh[:1 << 14])
+                    got = enc.encode(xsub[:1 << 14]).cpu().numpy()
+                    cpu["parity"] = {"samples": sub, "indices_bit_exact": bool(np.array_equal(gi, oi)),
+                                     "weights_bit_exact": bool(np.array_equal(gw, ow)),
+                                     "features_bit_exact": bool(np.array_equal(got.view(np.uint32), want.view(np.uint32)))}
+                except Exception as exc:
+                    cpu["parity"] = {"error": str(exc)}
             except Exception as exc:  # the GPU numbers stand on their own; say why the baseline is missing
                 cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable", "sample": str(exc)}
 

@@ -3,6 +3,8 @@
 Bars: forward activations and per-sample input gradients BIT-EXACT (fp64 accumulation in the reference's order);
 parameter gradients rel 1e-12 (fp64 reassociation only); first-step loss rel 1e-13; loss curve of a 12-step run within
 1e-3 of the reference's (table gradients are fp32 atomics, Adam amplifies sign flips of near-zero gradients)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -281,7 +283,7 @@ def test_random_trainer_shapes_match_the_oracle(sx, oracle_lib):
     batches, a global batch larger than the local chunk (a rank's share).  Exact head: loss rel 1e-12, MLP gradients rel
     1e-9, table gradients within the fp32-atomics bar, touched sets exact."""
     rng = np.random.default_rng(77)
-    for case in range(24):
+    for case in range(int(os.environ.get("SXEN_FUZZ_CASES", "24"))):
         n = int(rng.integers(1, 7))
         cfg = oracle.Config(dim=n, levels=int(rng.integers(1, 9)), table_size=1 << int(rng.integers(6, 13)),
                             features=int(rng.choice([1, 2, 2, 4])), base_resolution=int(rng.integers(2, 12)),

@@ -6,6 +6,8 @@ Bars (stated once, used below):
   * table gradients (fp32 atomics vs the reference's fp64 accumulator): |d| <= GRAD_RTOL * sum of |contributions|
   * touched rows: exact set equality;  optimizer given identical gradients: BIT-EXACT params and moments
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -706,7 +708,8 @@ def test_random_configurations_match_the_oracle(sx, oracle_lib):
     bar, fused == separate, counters equal to the oracle's."""
     rng = np.random.default_rng(20240229)
     done = 0
-    while done < 120:
+    cases = int(os.environ.get("SXEN_FUZZ_CASES", "120"))   # a longer soak: SXEN_FUZZ_CASES=2000
+    while done < cases:
         n = int(rng.integers(1, 9))
         backend = int(rng.integers(0, 2))
         if backend == oracle.BACKEND_GRID and n > 5:

@@ -351,7 +351,15 @@ sxen_status sxen_trainer_collect(sxen_trainer* t, double* losses_out, size_t cap
   if (n == 0) return SXEN_OK;
   SXEN_CUDA(cudaMemcpyAsync(t->loss_ring_host, t->loss_ring, n * sizeof(double), cudaMemcpyDeviceToHost, s));
   SXEN_CUDA(cudaMemcpyAsync(t->gate_host, t->gate, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  // the three error words ride on the same synchronisation: the encoder's first rejected sample and the optimizers' first
+  // non-finite gradient element.  All clear (the normal case) = one stream sync per collect; anything else takes the
+  // checking entry points below, which re-read, reset and word the error.
+  SXEN_CUDA(cudaMemcpyAsync(t->enc->status_host, t->enc->status, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  SXEN_CUDA(cudaMemcpyAsync(t->table_opt->status_host, t->table_opt->status, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  SXEN_CUDA(cudaMemcpyAsync(t->mlp_opt->status_host, t->mlp_opt->status, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   SXEN_CUDA(cudaStreamSynchronize(s));
+  const bool words_clear = t->enc->status_host[0] == kNoFailure && *t->table_opt->status_host == kNoFailure &&
+                           *t->mlp_opt->status_host == kNoFailure;
   t->pending = 0;
   for (size_t i = 0; i < n; ++i) losses_out[i] = t->loss_ring_host[i];
   if (*t->gate_host != kNoFailure) {
@@ -366,6 +374,7 @@ sxen_status sxen_trainer_collect(sxen_trainer* t, double* losses_out, size_t cap
     if (failed_out) *failed_out = static_cast<int64_t>(bad);
     return fail(SXEN_TRAINING_ERROR, "loss became non-finite (queued step %llu of %zu)", bad, n);
   }
+  if (words_clear) return SXEN_OK;
   if (sxen_status st = sxen_encoder_check(t->enc, stream)) return st;
   return sxen_trainer_check(t, stream);
 }

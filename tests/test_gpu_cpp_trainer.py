@@ -253,3 +253,22 @@ def test_cpp_checkpoint_round_trip_of_reference_files(sx, tmp_path):
     run = subprocess.run([exe, str(tmp_path), os.path.join(gold, "ref_checkpoint.sxen"),
                           os.path.join(gold, "ref_checkpoint_nomlp.sxen")], capture_output=True, text=True, timeout=600)
     assert run.returncode == 0 and run.stdout.strip().endswith("checkpoint ok"), run.stdout + run.stderr
+
+
+def test_queued_steps_report_a_rejected_coordinate_at_collect(sx):
+    """check_input (src/encoding.cpp:183-194) on the queued path: the offending sample is named when the window is
+    collected (ValueError = std::invalid_argument), and the handle goes on afterwards."""
+    ta, ma = sx.AdamConfig(lr=1e-2), sx.AdamConfig(lr=1e-3)
+    _, enc, mlp = _model(sx)
+    tr = sx.Trainer(enc, mlp)
+    x = torch.rand((256, 2), dtype=torch.float64, device="cuda")
+    y = torch.rand((256, 3), dtype=torch.float64, device="cuda")
+    bad = x.clone()
+    bad[37, 1] = 1.5
+    tr.step_enqueue(x, y, ta, ma)
+    tr.step_enqueue(bad, y, ta, ma)
+    with pytest.raises(ValueError, match="sample 37"):
+        tr.collect()
+    tr.step_enqueue(x, y, ta, ma)
+    losses, failed = tr.collect()
+    assert failed == -1 and len(losses) == 1 and np.isfinite(losses[0])

@@ -295,18 +295,20 @@ sxen_status sxen_trainer_step(sxen_trainer* t, const void* coords_dev, sxen_coor
                               const sxen_adam_config* mlp_adam, double* loss_out, void* stream) {
   SXEN_REQUIRE(n_samples >= 1, "train: batch_size must be >= 1");  // src/trainer.cpp:57
   SXEN_REQUIRE(t != nullptr && table_adam != nullptr && mlp_adam != nullptr, "null argument");
-  const bool walk = !t->foreign_grads && sxen_sparse_adam_walk_pays(t->enc, n_samples);
-  if (sxen_status st = sxen_trainer_accumulate(t, coords_dev, coord_type, targets_dev, target_type, n_samples, n_samples, stream))
+  if (t->pending != 0)
+    return fail(SXEN_LOGIC_ERROR, "train: %zu queued steps not collected (sxen_trainer_collect first)", t->pending);
+  // One queued step, collected at once: the device-side gate keeps "throw before the update" for a non-finite loss
+  // (src/trainer.cpp:121-123) and the loss, the gate and the three error words come back on ONE stream synchronisation
+  // (the separate loss / check entry points cost four).
+  if (sxen_status st = sxen_trainer_step_enqueue(t, coords_dev, coord_type, targets_dev, target_type, n_samples, table_adam,
+                                                 mlp_adam, stream))
     return st;
   double loss = 0.0;
-  const sxen_status loss_st = sxen_trainer_loss(t, n_samples, &loss, stream);
+  size_t count = 0;
+  int64_t failed = -1;
+  const sxen_status st = sxen_trainer_collect(t, &loss, 1, &count, &failed, stream);
   if (loss_out) *loss_out = loss;
-  if (loss_st != SXEN_OK) return loss_st;  // the reference throws before updating (src/trainer.cpp:121-123)
-  DeviceGuard guard(t->device);
-  if (sxen_status st = update_impl(t, table_adam, mlp_adam, walk ? coords_dev : nullptr, coord_type, n_samples, nullptr, stream))
-    return st;
-  SXEN_CUDA(cudaMemsetAsync(t->loss_sum, 0, sizeof(double), as_stream(stream)));
-  return sxen_trainer_check(t, stream);
+  return st;
 }
 
 sxen_status sxen_trainer_step_enqueue(sxen_trainer* t, const void* coords_dev, sxen_coord_type coord_type,

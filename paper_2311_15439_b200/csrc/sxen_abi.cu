@@ -819,7 +819,12 @@ sxen_status host_pipeline(sxen_encoder* enc, const double* x_host, const void* u
   {
     const size_t cap = enc->stage_samples;
     std::vector<size_t> ramp;
-    for (size_t r = 1u << 15; r < cap; r <<= 1) ramp.push_back(r);
+    size_t ramp0 = 1u << 15;
+    if (const char* env = std::getenv("SXEN_HOST_RAMP_LOG2")) {  // tuning aid, like SXEN_HOST_CHUNK_LOG2
+      const int v = std::atoi(env);
+      if (v >= 12 && v <= 20) ramp0 = static_cast<size_t>(1) << v;
+    }
+    for (size_t r = ramp0; r < cap; r <<= 1) ramp.push_back(r);
     size_t ramps = 0;
     for (size_t r : ramp) ramps += 2 * r;
     if (n_samples > ramps + cap / 2) {

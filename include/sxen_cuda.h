@@ -341,7 +341,8 @@ SXEN_API sxen_status sxen_trainer_loss(sxen_trainer* trainer, size_t global_batc
 SXEN_API sxen_status sxen_trainer_update(sxen_trainer* trainer, const sxen_adam_config* table_adam,
                                          const sxen_adam_config* mlp_adam, void* stream);
 SXEN_API sxen_status sxen_trainer_check(sxen_trainer* trainer, void* stream);  /* non-finite gradient -> SXEN_TRAINING_ERROR */
-/* One whole single-GPU step: accumulate + loss + update + check. */
+/* One whole single-GPU step: accumulate + loss + update + check -- one queued step (below) collected at once, so the loss and
+ * the error words come back on a single stream synchronisation.  SXEN_LOGIC_ERROR while queued steps await their collect. */
 SXEN_API sxen_status sxen_trainer_step(sxen_trainer* trainer, const void* coords_dev, sxen_coord_type coord_type,
                                        const void* targets_dev, sxen_coord_type target_type, size_t n_samples,
                                        const sxen_adam_config* table_adam, const sxen_adam_config* mlp_adam,

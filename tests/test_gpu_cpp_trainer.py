@@ -272,3 +272,20 @@ def test_queued_steps_report_a_rejected_coordinate_at_collect(sx):
     tr.step_enqueue(x, y, ta, ma)
     losses, failed = tr.collect()
     assert failed == -1 and len(losses) == 1 and np.isfinite(losses[0])
+
+
+def test_per_step_call_refuses_to_jump_a_queue(sx):
+    """sxen_trainer_step is one queued step collected at once: with steps still queued it would hand back the wrong loss,
+    so it is a logic error until they are collected."""
+    ta, ma = sx.AdamConfig(lr=1e-2), sx.AdamConfig(lr=1e-3)
+    _, enc, mlp = _model(sx, T=1 << 10)
+    tr = sx.Trainer(enc, mlp)
+    x = torch.rand((128, 2), dtype=torch.float64, device="cuda")
+    y = torch.rand((128, 3), dtype=torch.float64, device="cuda")
+    first = tr.step(x, y, ta, ma)
+    tr.step_enqueue(x, y, ta, ma)
+    with pytest.raises(RuntimeError, match="not collected"):
+        tr.step(x, y, ta, ma)
+    (second,), failed = tr.collect()
+    third = tr.step(x, y, ta, ma)
+    assert failed == -1 and first > second > third

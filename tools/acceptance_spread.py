@@ -1,3 +1,8 @@
+#!/usr/bin/env python
+"""tools/acceptance_spread.py -- the reference's image-fitting-parity acceptance configuration (tests/acceptance_main.cpp:
+315-341: 512 x 512 test image, L=8 T=2^16 F=2 base 4 growth 2 equal-memory, batch 512, 10 000 steps), six launches per
+(head precision, backend): how far the final PSNR moves from launch to launch with the order of the fp32 atomics, next to
+the reference's own deterministic run (tests/golden/acceptance_image_fitting.npz).  Run from the repo root."""
 import sys, os, numpy as np
 sys.path.insert(0, os.getcwd())
 import paper_2311_15439_b200 as sx

@@ -60,10 +60,21 @@ def workload_name(n: int, t_log2: int = T_LOG2, backend: str = "simplex") -> str
             f"2^{BATCH_LOG2} uniform random samples per GPU")
 
 
-class ClockSampler:
-    """nvidia-smi clocks/throttle reasons DURING the timed region (B200_PROFILING.md recipe)."""
+def workload_config(n: int, t_log2: int, backend: str) -> dict:
+    """The workload definition, identical (keys and values) on both arms; everything arm-specific lives elsewhere
+    in the line (`launch` on the GPU arm, `cpu_baseline.sample` on the reference arm)."""
+    return {"workload": workload_name(n, t_log2, backend), "dim": n, "levels": L, "features": F, "backend": backend,
+            "table_size_log2": t_log2, "base_resolution": BASE, "growth": GROWTH[n],
+            "samples_per_gpu_per_step": 1 << BATCH_LOG2,
+            "inputs": "coords CounterRng(99,1), upstream CounterRng(7,2)*1e-3, tables init_tables(42)"}
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons DURING the run (B200_PROFILING.md recipe).  Started before the warm-up and stopped
+    after the e2e leg (nvidia-smi needs about a second before its first sample, longer than the timed region itself);
+    `mark()` timestamps let the summary say how many samples fell inside the timed region."""
+
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
@@ -71,19 +82,26 @@ class ClockSampler:
         self.idx = gpu_index
         self.proc = None
         self.path = None
+        self.marks = {}
 
     def start(self):
         try:
             fd, self.path = tempfile.mkstemp(suffix=".csv")
             os.close(fd)
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "100", "-i", str(self.idx)], stdout=open(self.path, "w"),
+                                          "-lms", "50", "-i", str(self.idx)], stdout=open(self.path, "w"),
                                          stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
 
+    def mark(self, name: str):
+        import datetime
+        self.marks[name] = datetime.datetime.now()
+
     def stop(self):
-        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        import datetime
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "samples_in_timed_region": 0,
+               "window": "warm-up + timed region + separate-launch diagnostics + e2e leg (GPU busy throughout)"}
         if self.proc is None:
             return out
         time.sleep(0.15)
@@ -92,25 +110,36 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, mx, reasons = [], [], set()
+        sm, mx, power, reasons, inside = [], [], [], set(), []
+        t0, t1 = self.marks.get("timed_region_start"), self.marks.get("timed_region_end")
         try:
             for line in open(self.path):
                 p = [c.strip() for c in line.split(",")]
-                if len(p) < 9:
+                if len(p) < 10:
                     continue
                 try:
-                    sm.append(float(p[1]))
-                    mx.append(float(p[2]))
+                    sm.append(float(p[2]))
+                    mx.append(float(p[3]))
+                    power.append(float(p[4]))
                 except ValueError:
                     continue
-                for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), p[5:9]):
+                try:
+                    ts = datetime.datetime.strptime(p[0], "%Y/%m/%d %H:%M:%S.%f")
+                    if t0 is not None and t1 is not None and t0 <= ts <= t1:
+                        inside.append(sm[-1])
+                except ValueError:
+                    pass
+                for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), p[6:10]):
                     if val.lower().startswith("active"):
                         reasons.add(name)
             os.unlink(self.path)
         except Exception:
             pass
         if sm:
-            out.update(sm_mhz=statistics.median(sm), sm_max_mhz=max(mx), reasons=sorted(reasons), samples=len(sm))
+            out.update(sm_mhz=statistics.median(sm), sm_min_mhz=min(sm), sm_max_mhz=max(mx), power_w_max=max(power),
+                       reasons=sorted(reasons), samples=len(sm), samples_in_timed_region=len(inside))
+            if inside:
+                out["sm_mhz_timed_region"] = statistics.median(inside)
         return out
 
 
@@ -224,11 +253,11 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * samples / value, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(n, args.log2t), "dim": n, "levels": L, "features": F, "table_size_log2": args.log2t,
-                   "note": "CPU reference arm: unmodified reference sources (oracle/_ref) on host cores only"},
+        "config": workload_config(n, args.log2t, args.backend),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"{samples} samples per step (same RNG streams as the GPU arm), "
-                                   f"encode+encode_backward per worker chunk, steady_clock"},
+                         "sample": f"{samples} samples per step (same RNG streams as the GPU arm), mean of {len(vals)} runs after "
+                                   f"{args.warmup} warm-up runs, encode+encode_backward per worker chunk, steady_clock; "
+                                   f"unmodified reference sources (oracle/_ref) on host cores only"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -281,13 +310,30 @@ def run_ours(args):
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if not torch.cuda.is_available() or sx.device_count() < 1:
         raise SystemExit("bench.py: no sm_100 CUDA device -- the GPU arm has no CPU fallback")
-    torch.cuda.set_device(local_rank)
+    n_dev = torch.cuda.device_count()
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} ranks")
+    if world > n_dev and not args.oversubscribe:
+        raise SystemExit(f"bench.py: {world} ranks but only {n_dev} CUDA device(s) visible -- one rank per GPU "
+                         f"(--oversubscribe shares devices for a functional check; its numbers are not scaling numbers)")
+    device_index = local_rank % n_dev if args.oversubscribe else local_rank
+    torch.cuda.set_device(device_index)
     dist = None
     if world > 1 or "WORLD_SIZE" in os.environ:  # under torchrun a single rank still drives the NCCL path
         import torch.distributed as dist_mod
         dist = dist_mod
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        if args.oversubscribe and world > n_dev:
+            # NCCL refuses two ranks on one device; gloo stages CUDA tensors through the host (functional check only)
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{device_index}"))
+        print(f"[bench rank {rank}/{world}] pid {os.getpid()} device cuda:{device_index} "
+              f"({torch.cuda.get_device_name(device_index)}) backend {dist.get_backend()}", file=sys.stderr, flush=True)
+    local_rank = device_index
+    sampler = ClockSampler(local_rank)
+    if rank == 0:
+        sampler.start()   # runs through warm-up, the timed region and the e2e leg
 
     n = args.dim
     N = 1 << BATCH_LOG2
@@ -299,7 +345,7 @@ def run_ours(args):
     enc = sx.HashEncoder(cfg, device=local_rank)
     enc.init_tables(42)
     tune = sx.Tuning(levels_per_thread=args.lpt, block_threads=args.block, level_major=args.level_major,
-                     exact_blend=args.exact, warp_aggregate=args.aggregate)
+                     exact_blend=args.exact, warp_aggregate=args.aggregate, level_chunk=args.level_chunk)
     enc.set_tuning(tune)
     grad = sx.EncoderGradient(enc)
 
@@ -327,11 +373,12 @@ def run_ours(args):
         # Launch-shape autotune OUTSIDE the timed region: one fused launch vs forward + backward launches, sample-major vs
         # level-major.  Which wins depends on whether tables + gradients of the walked levels fit L2 side by side
         # (profiles/r1_sweep_*.log): time each candidate for a few steps and keep the fastest.
-        cands = [("fused", 0, 2), ("split", 0, 2), ("fused", 1, 4), ("split", 1, 2)]
+        # (path, level_major, levels per thread, level_chunk: -1 one grid slice, 8 = the grid walks ranges of 8 levels)
+        cands = [("fused", 0, 2, -1), ("fused", 0, 2, 8), ("split", 0, 2, -1), ("fused", 1, 4, -1), ("split", 1, 2, -1)]
         autotune = {}
-        for path, lm, lpt in cands:
+        for path, lm, lpt, chunk in cands:
             enc.set_tuning(sx.Tuning(levels_per_thread=lpt, block_threads=args.block, level_major=lm,
-                                     exact_blend=args.exact, warp_aggregate=args.aggregate))
+                                     exact_blend=args.exact, warp_aggregate=args.aggregate, level_chunk=chunk))
 
             def one(i, path=path):
                 k = i % n_sets
@@ -346,20 +393,20 @@ def run_ours(args):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            for i in range(4):
+            for i in range(8):
                 one(i)
             e1.record(stream)
             torch.cuda.synchronize()
-            autotune[f"{path}/level_major={lm}/lpt={lpt}"] = e0.elapsed_time(e1) / 4
+            autotune[f"{path}/level_major={lm}/lpt={lpt}/level_chunk={chunk}"] = e0.elapsed_time(e1) / 8
         if dist is not None:  # every rank must take the same path
             t = torch.tensor(list(autotune.values()), dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             autotune = dict(zip(autotune.keys(), [float(v) for v in t.tolist()]))
         best = min(autotune, key=autotune.get)
-        path, lm, lpt = cands[list(autotune.keys()).index(best)]
+        path, lm, lpt, chunk = cands[list(autotune.keys()).index(best)]
         args.path = path
         enc.set_tuning(sx.Tuning(levels_per_thread=lpt, block_threads=args.block, level_major=lm, exact_blend=args.exact,
-                                 warp_aggregate=args.aggregate))
+                                 warp_aggregate=args.aggregate, level_chunk=chunk))
 
     exchange = dist is not None and not args.no_allreduce
     ranges = sx.level_ranges(L, args.level_chunks if exchange else 1)
@@ -413,15 +460,14 @@ def run_ours(args):
     enc.check()
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    sampler = ClockSampler(local_rank)
-    if rank == 0:
-        sampler.start()
     launches0 = sx.launch_count()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    if rank == 0:
+        sampler.mark("timed_region_start")
     t_start.record(stream)
     for i in range(args.steps):
         evs[i][2].record(stream)
@@ -431,7 +477,8 @@ def run_ours(args):
     if dist is not None:
         dist.barrier()
     launches = sx.launch_count() - launches0
-    clocks = sampler.stop() if rank == 0 else None
+    if rank == 0:
+        sampler.mark("timed_region_end")
     enc.check()
     total_ms = t_start.elapsed_time(t_end)
     if dist is not None:
@@ -492,46 +539,62 @@ def run_ours(args):
                                 "measured_sm_request_peak_G_per_s": 278.6, "sm_frac": 110 * rate / 278.6,
                                 "l2_lookups_per_sample": 137, "l2_lookup_rate_G_per_s": 137 * rate}
 
+    rank_info = [{"rank": 0, "device": local_rank, "name": torch.cuda.get_device_name(local_rank), "pid": os.getpid()}]
+    if dist is not None:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, {"rank": rank, "device": local_rank, "name": torch.cuda.get_device_name(local_rank),
+                                          "pid": os.getpid()})
+        rank_info = gathered
+    # ---- e2e: the host-buffer C-ABI call on EVERY rank (each GPU has its own PCIe link), pinned host memory, H2D + D2H inside
+    # the timed region; wall clock between two barriers, max over ranks
+    import ctypes as C
+
+    import numpy as np
+    lib = sx.lib
+
+    def pinned(shape, dtype):
+        nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        p = C.c_void_p()
+        assert lib.sxen_host_alloc(nbytes, C.byref(p)) == 0, lib.sxen_last_error()
+        buf = (C.c_char * nbytes).from_address(p.value)
+        return np.frombuffer(buf, dtype=dtype).reshape(shape), p
+
+    hx, px = pinned((N, n), np.float64)
+    hup, pup = pinned((N, LF), np.float32)
+    hout, pout = pinned((N, LF), np.float32)
+    hx[:] = xs[0].double().cpu().numpy()
+    hup[:] = ups[0].cpu().numpy()
+    e2e_steps = max(3, args.steps)
+    for _ in range(max(3, args.warmup)):
+        enc.encode_forward_backward(hx, hup, grad, out=hout)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    per_step = []
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        t1 = time.perf_counter()
+        enc.encode_forward_backward(hx, hup, grad, out=hout)   # synchronous: returns with the features in hout
+        per_step.append(time.perf_counter() - t1)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps              # the mean over exactly e2e_steps calls is the value
+    if dist is not None:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": world * N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(hx.nbytes + hup.nbytes) * world,
+           "d2h_bytes_per_step": int(hout.nbytes) * world, "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
+           "ms_per_step_median": statistics.median(per_step) * 1e3, "ms_per_step_min": min(per_step) * 1e3, "n_gpus": world,
+           "call": "sxen_encoder_encode_forward_backward_host (x f64, upstream f32, features f32; pinned host buffers), "
+                   "one call per rank per step"}
+    # spot parity of the e2e result against the device path
+    assert np.array_equal(hout[:4096], outs[0][:4096].cpu().numpy()) or args.exact == 0
+    for p in (px, pup, pout):
+        lib.sxen_host_free(p)
+
     line = None
     if rank == 0:
-        # ---- e2e: the host-buffer C-ABI call, pinned host memory, H2D + D2H inside the timed region
-        import ctypes as C
-
-        import numpy as np
-        lib = sx.lib
-
-        def pinned(shape, dtype):
-            nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
-            p = C.c_void_p()
-            assert lib.sxen_host_alloc(nbytes, C.byref(p)) == 0, lib.sxen_last_error()
-            buf = (C.c_char * nbytes).from_address(p.value)
-            return np.frombuffer(buf, dtype=dtype).reshape(shape), p
-
-        hx, px = pinned((N, n), np.float64)
-        hup, pup = pinned((N, LF), np.float32)
-        hout, pout = pinned((N, LF), np.float32)
-        hx[:] = xs[0].double().cpu().numpy()
-        hup[:] = ups[0].cpu().numpy()
-        e2e_steps = max(3, args.steps)
-        for _ in range(max(3, args.warmup)):
-            enc.encode_forward_backward(hx, hup, grad, out=hout)
-        torch.cuda.synchronize()
-        per_step = []
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            t1 = time.perf_counter()
-            enc.encode_forward_backward(hx, hup, grad, out=hout)   # synchronous: returns with the features in hout
-            per_step.append(time.perf_counter() - t1)
-        torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t0) / e2e_steps              # the mean over exactly e2e_steps calls is the value
-        e2e = {"value": N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(hx.nbytes + hup.nbytes),
-               "d2h_bytes_per_step": int(hout.nbytes), "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
-               "ms_per_step_median": statistics.median(per_step) * 1e3, "ms_per_step_min": min(per_step) * 1e3, "n_gpus": 1,
-               "call": "sxen_encoder_encode_forward_backward_host (x f64, upstream f32, features f32; pinned host buffers)"}
-        # spot parity of the e2e result against the device path
-        assert np.array_equal(hout[:4096], outs[0][:4096].cpu().numpy()) or args.exact == 0
-        for p in (px, pup, pout):
-            lib.sxen_host_free(p)
+        clocks = sampler.stop()
 
         # ---- CPU baseline on this box's host cores (bounded sample), N=1 only
         cpu = None
@@ -539,10 +602,15 @@ def run_ours(args):
             try:
                 threads = host_threads()
                 samples = min(1 << BATCH_LOG2, threads << 16)  # the whole 2^20 batch on >= 16 threads: ~25 core-seconds
-                v, kind = cpu_reference_run(n, samples, threads, args.log2t)
-                cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
-                       "sample": f"{samples} samples of the same workload (same RNG streams), reference worker pattern: "
-                                 f"encode+encode_backward per contiguous chunk into a per-thread accumulator"}
+                runs = []
+                for i in range(4):   # one warm-up run (page faults of every worker's accumulator), then the mean of three
+                    v, kind = cpu_reference_run(n, samples, threads, args.log2t)
+                    if i > 0:
+                        runs.append(v)
+                cpu = {"value": statistics.mean(runs), "unit": UNIT, "cores": threads, "kind": kind, "runs": runs,
+                       "sample": f"{samples} samples of the same workload (same RNG streams), mean of 3 runs after 1 warm-up "
+                                 f"run, reference worker pattern: encode+encode_backward per contiguous chunk into a "
+                                 f"per-thread accumulator"}
                 # parity in the same run: the first 2^16 samples of this run's inputs through the device
                 # path against the CPU checker -- vertex indices, weights and features bit for bit
                 try:
@@ -630,19 +698,20 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64 lattice math / u32 hash / f32 features+grads", "data": "synthetic",
-            "config": {"workload": workload_name(n, args.log2t, args.backend), "dim": n, "levels": L, "features": F,
-                       "backend": args.backend, "table_size_log2": args.log2t, "base_resolution": BASE, "growth": GROWTH[n], "samples_per_gpu_per_step": N,
-                       "coords": "f32 on device (CounterRng(99,1))", "path": args.path,
-                       "autotune_ms": autotune,
+            "config": workload_config(n, args.log2t, args.backend),
+            "launch": {"coords": "f32 on device", "path": args.path, "autotune_ms": autotune,
+                       "ranks": rank_info,
                        "l2_policy": f"inputs larger than L2: {n_sets} rotating input sets x 268 MB, plus "
                                     f"{L * (1 << args.log2t) * F * 4 >> 20} MiB tables and as much gradient accumulator",
                        "tuning": {"levels_per_thread": t.levels_per_thread, "block_threads": t.block_threads,
                                   "level_major": t.level_major, "exact_blend": t.exact_blend,
-                                  "warp_aggregate": t.warp_aggregate},
-                       "multi_gpu": (f"batch sharded, tables replicated, NCCL all-reduce of the "
-                                     f"{L * (1 << args.log2t) * F * 4 >> 20} MiB table-gradient accumulator per step in "
+                                  "warp_aggregate": t.warp_aggregate, "level_chunk": t.level_chunk},
+                       "multi_gpu": (f"batch sharded over {world} ranks, tables replicated, {dist.get_backend()} SUM all-reduce of "
+                                     f"the {L * (1 << args.log2t) * F * 4 >> 20} MiB table-gradient accumulator per step in "
                                      f"{len(ranges)} level chunks overlapped with the next chunk's kernel")
-                                    if exchange else "single GPU"},
+                                    if exchange else (f"{world} replicas, no exchange (--no-allreduce)" if world > 1
+                                                      else "single GPU"),
+                       "oversubscribed": bool(args.oversubscribe and world > n_dev)},
             "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline, "cpu_baseline": cpu,
             "train_step": train, "other_dims": other,
         }
@@ -667,19 +736,47 @@ def main():
     ap.add_argument("--lpt", type=int, default=0)
     ap.add_argument("--block", type=int, default=0)
     ap.add_argument("--level-major", type=int, default=-1)
+    ap.add_argument("--level-chunk", type=int, default=0, help="sxen_tuning.level_chunk for --path fused|split (0 = library default)")
     ap.add_argument("--exact", type=int, default=1)
     ap.add_argument("--aggregate", type=int, default=0)
     ap.add_argument("--no-allreduce", action="store_true")
     ap.add_argument("--level-chunks", type=int, default=4,
                     help="multi-GPU: level chunks whose gradient all-reduce overlaps the next chunk's kernel")
+    ap.add_argument("--oversubscribe", action="store_true",
+                    help="functional check only: let ranks share devices (rank %% device count) over gloo")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-train", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     else:
         run_ours(args)
+
+
+def spawn_ranks(args) -> int:
+    """`python bench.py --gpus N` outside a launcher: re-run this command line as N ranks, one per GPU, the way the driver
+    does (python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 --master-port P).  Fails
+    loudly when the box has fewer than N devices (unless --oversubscribe)."""
+    import socket
+
+    import torch
+    n_dev = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if n_dev < 1:
+        raise SystemExit("bench.py: no sm_100 CUDA device -- the GPU arm has no CPU fallback")
+    if n_dev < args.gpus and not args.oversubscribe:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but only {n_dev} CUDA device(s) visible on this box")
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    print("[bench] spawning:", " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
 
 
 if __name__ == "__main__":

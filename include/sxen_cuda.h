@@ -110,6 +110,11 @@ typedef struct sxen_tuning {
                                 serialisation of the L2 atomic unit).  0 = library default: on for launches of at least
                                 2^16 samples (below, the fold costs more than the contention it removes), 1 = always,
                                 -1 = off */
+  int32_t level_chunk;       /* sample-major launches: the grid walks the levels in contiguous ranges of this many levels
+                                (blockIdx.y = range; sample-major inside a range), so only one range's table and accumulator
+                                rows are live in L2 at a time.  Used when it is levels_per_thread * 2^k.  0 = library
+                                default (8 for the fused launch at dim 3 when tables + accumulator only just fit L2:
+                                profiles/r2_l2_window_n3.log), -1 = off */
 } sxen_tuning;
 
 typedef struct sxen_encoder sxen_encoder;   /* sxen::HashEncoder     (include/sxen/encoding.hpp:92-148) */

@@ -44,7 +44,7 @@ class NoiseSpecC(C.Structure):  # sxen_noise_spec
 class TuningC(C.Structure):
     _fields_ = [("levels_per_thread", C.c_int32), ("block_threads", C.c_int32), ("level_major", C.c_int32),
                 ("exact_blend", C.c_int32), ("warp_aggregate", C.c_int32), ("merge_pairs", C.c_int32),
-                ("cache_hints", C.c_int32), ("coarse_replicas", C.c_int32)]
+                ("cache_hints", C.c_int32), ("coarse_replicas", C.c_int32), ("level_chunk", C.c_int32)]
 
 
 _P = C.POINTER

@@ -36,6 +36,8 @@ struct EncodeArgs {
   int32_t groups_shift;          // log2(groups) when a power of two, else -1
   int32_t coord_f32;             // coordinate element type
   int32_t level_major;           // 1: blockIdx.y = level group
+  int32_t span_groups;           // sample-major: level groups one blockIdx.y slice covers (a power of two when groups_shift
+                                 // >= 0, then groups_shift = log2(span_groups)); == groups unless the launch is chunked
   int32_t vec;                   // proven float alignment of every thread's out/upstream chunk: 4, 2 or 1
   uint32_t agg_mask;             // bit l: warp-aggregate the backward atomics of local level l
   int32_t merge_pairs;           // F == 2: one red.v4 for two chain vertices in the same 16-byte slot
@@ -112,14 +114,16 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
   } else {
     const unsigned long long gid = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (a.groups_shift >= 0) {
+      // chunked launch: blockIdx.y walks contiguous ranges of span_groups level groups, sample-major inside a range, so the
+      // rows of one range of levels (tables + accumulator) are what L2 holds while that range is in flight
       s = gid >> a.groups_shift;
-      g = static_cast<int>(gid & static_cast<unsigned long long>(a.groups - 1));
+      g = static_cast<int>(gid & static_cast<unsigned long long>(a.span_groups - 1)) + static_cast<int>(blockIdx.y) * a.span_groups;
     } else {
       s = gid / static_cast<unsigned long long>(a.groups);
       g = static_cast<int>(gid - s * static_cast<unsigned long long>(a.groups));
     }
   }
-  const bool in_range = s < a.n_samples;
+  const bool in_range = s < a.n_samples && g < a.groups;
 
   double x[ND];
   bool ok = false;
@@ -520,6 +524,7 @@ __global__ void __launch_bounds__(256) coarse_fold_kernel(const __grid_constant_
 // ---- host-side launch plumbing, one translation unit per ND (sxen_encode_nd.cu) -----------------------------
 
 struct EncodeLaunch {
+  int chunk_levels;     // sample-major launches: levels per blockIdx.y slice (0 = one slice); used when it is LPT * 2^k
   int features;         // F, any
   int lpt;              // requested levels per thread
   int mode;             // kModeFwd / kModeBwd / kModeBoth

@@ -15,8 +15,17 @@ template <int F, int LPT, int MODE, bool EXACT, bool GRID = false>
 cudaError_t go(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t stream) {
   a.groups = (a.n_levels + LPT - 1) / LPT;
   a.groups_shift = -1;
+  a.span_groups = a.groups;
+  int slices = 1;
+  if (!a.level_major && ln.chunk_levels > 0 && ln.chunk_levels % LPT == 0 && ln.chunk_levels < a.n_levels) {
+    const int cg = ln.chunk_levels / LPT;
+    if ((cg & (cg - 1)) == 0) {
+      a.span_groups = cg;
+      slices = (a.groups + cg - 1) / cg;
+    }
+  }
   for (int sft = 0; sft < 31; ++sft)
-    if ((1 << sft) == a.groups) a.groups_shift = sft;
+    if ((1 << sft) == a.span_groups) a.groups_shift = sft;
   // out/upstream chunk alignment the kernel may rely on (base pointers are checked by the caller via a.vec)
   const int k = LPT * F;
   int vec = a.vec;
@@ -31,8 +40,8 @@ cudaError_t go(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t stream) {
   if (a.level_major) {
     grid = dim3(static_cast<unsigned>((a.n_samples + block - 1) / block), static_cast<unsigned>(a.groups), 1);
   } else {
-    const unsigned long long threads = a.n_samples * static_cast<unsigned long long>(a.groups);
-    grid = dim3(static_cast<unsigned>((threads + block - 1) / block), 1, 1);
+    const unsigned long long threads = a.n_samples * static_cast<unsigned long long>(a.span_groups);
+    grid = dim3(static_cast<unsigned>((threads + block - 1) / block), static_cast<unsigned>(slices), 1);
   }
   encode_kernel<ND, F, LPT, MODE, EXACT, GRID><<<grid, block, 0, stream>>>(a);
   return cudaGetLastError();

@@ -85,10 +85,11 @@ class Tuning:
     merge_pairs: int = 0  # 1 on, -1 off, 0 library default (on)
     cache_hints: int = -1  # F == 2: gather L2 policy + 4 * red L2 policy (0 none, 1 evict_last, 2 evict_first, 3 evict_unchanged); -1 auto
     coarse_replicas: int = 0  # 0 library default (on from 2^16 samples per launch), 1 always, -1 off
+    level_chunk: int = 0  # sample-major launches: levels per grid slice; 0 library default, -1 off
 
     def c(self) -> _abi.TuningC:
         return _abi.TuningC(self.levels_per_thread, self.block_threads, self.level_major, self.exact_blend,
-                            self.warp_aggregate, self.merge_pairs, self.cache_hints, self.coarse_replicas)
+                            self.warp_aggregate, self.merge_pairs, self.cache_hints, self.coarse_replicas, self.level_chunk)
 
 
 def equal_memory_multiplier(n: int) -> float:
@@ -281,7 +282,7 @@ class HashEncoder:
         c = _abi.TuningC()
         raise_for(self._lib, self._lib.sxen_encoder_get_tuning(self._h, C.byref(c)))
         return Tuning(c.levels_per_thread, c.block_threads, c.level_major, c.exact_blend, c.warp_aggregate,
-                      c.merge_pairs, c.cache_hints, c.coarse_replicas)
+                      c.merge_pairs, c.cache_hints, c.coarse_replicas, c.level_chunk)
 
     # ---- the hot path
     def _check_x(self, x):

@@ -380,6 +380,30 @@ def acceptance_image_fitting(ref: Ref):
     print("acceptance_image_fitting written")
 
 
+def acceptance_thread_spread(ref: Ref):
+    """How far the REFERENCE's own final PSNR moves when only its worker count changes (threads = 1, 2, 3, 4, 8: the per-worker
+    fp64 accumulators are merged in worker order, src/trainer.cpp:125-128, so each count is a different summation order of
+    the same gradients) on its image-fitting-parity configuration (tests/acceptance_main.cpp:315-341).  This is the
+    reference-side yardstick for the device path's launch-to-launch spread (fp32 atomics); written as JSON."""
+    import json
+    import time
+    img = ref.make_test_image(512, 512, 7)
+    out = {"config": "512x512 test image seed 7, L=8 T=2^16 F=2 base 4 growth 2 equal-memory, batch 512, 10000 steps, "
+                     "train seed 1234, init seed 42", "runs": []}
+    for name, backend, counts in (("simplex", oracle.BACKEND_SIMPLEX, (1, 2, 3, 4, 8)), ("grid", oracle.BACKEND_GRID, (1, 2, 8))):
+        cfg = Config(dim=2, levels=8, table_size=1 << 16, features=2, base_resolution=4, growth=2.0, backend=backend,
+                     level_scale=oracle.SCALE_EQUAL_MEMORY)
+        for th in counts:
+            t0 = time.time()
+            psnr, loss, _, _ = ref.fit_image(img, cfg, batch=512, steps=10000, train_seed=1234, threads=th, init_seed=42)
+            out["runs"].append({"backend": name, "threads": th, "final_psnr": float(psnr),
+                                "loss_every_1000": [float(v) for v in loss[::1000]], "seconds": round(time.time() - t0, 1)})
+            print(name, "threads", th, "final PSNR", psnr, "in", round(time.time() - t0, 1), "s", flush=True)
+            with open(os.path.join(OUT, "acceptance_thread_spread.json"), "w") as f:
+                json.dump(out, f, indent=1)
+    print("acceptance_thread_spread written")
+
+
 if __name__ == "__main__":
     oracle.build(ref=True)
     ref = Ref()
@@ -388,6 +412,9 @@ if __name__ == "__main__":
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "acceptance":
         acceptance_image_fitting(ref)
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "spread":
+        acceptance_thread_spread(ref)
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "tasks":
         task_cases(ref)

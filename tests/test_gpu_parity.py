@@ -759,3 +759,30 @@ def test_random_configurations_match_the_oracle(sx, oracle_lib):
         vals2, tch2 = grad_dense(grad2, cfg)
         assert np.array_equal(tch2, wt) and (np.abs(vals2 - wg) <= GRAD_RTOL * scale + GRAD_ATOL).all(), tag
         enc.check()
+
+
+@pytest.mark.parametrize("dim,levels,chunk,lpt", [(3, 16, 8, 2), (3, 16, 4, 2), (3, 12, 8, 4), (2, 16, 8, 1), (3, 10, 4, 2), (3, 16, 0, 0)])
+def test_chunked_fused_launch_matches_the_oracle(sx, oracle_lib, dim, levels, chunk, lpt):
+    """sxen_tuning.level_chunk: one fused launch whose grid walks the levels in contiguous ranges (blockIdx.y = range,
+    sample-major inside a range -- the library default at dim 3, T = 2^19, 16 levels).  Same features bit for bit as the
+    oracle (HashEncoder::encode, src/encoding.cpp:295-315), same touched rows, gradients to the fp32-atomic bar
+    (encode_backward, :317-335); ragged sample counts and level counts that the range size does not divide included."""
+    cfg = oracle.Config(dim=dim, levels=levels, table_size=1 << 19, features=2, base_resolution=16,
+                        growth=1.5 if dim == 3 else 2.0)
+    enc = make_encoder(sx, cfg, seed=42)
+    enc.set_tuning(sx.Tuning(levels_per_thread=lpt, level_major=0 if chunk else -1, level_chunk=chunk))
+    N = 3001
+    x32 = oracle_lib.rng_doubles(99, 1, N * dim).reshape(N, dim).astype(np.float32)
+    up32 = oracle_lib.rng_doubles(7, 2, N * levels * 2, -1.0, 1.0).astype(np.float32).reshape(N, levels * 2)
+    grad = sx.EncoderGradient(enc)
+    feats = enc.encode_forward_backward(dev(x32), dev(up32), grad)
+    enc.check()
+    xd, upd = x32.astype(np.float64), up32.astype(np.float64)
+    want, bad = oracle_lib.encode(cfg, oracle_lib.init_tables(cfg, 42), xd)
+    assert bad == -1
+    assert np.array_equal(feats.cpu().numpy().view(np.uint32), want.view(np.uint32))
+    og, ot, _ = oracle_lib.encode_backward(cfg, xd, upd)
+    scale = abs_contrib(oracle_lib, cfg, xd, upd)
+    gv, gt = grad_dense(grad, cfg)
+    assert np.array_equal(gt, ot)
+    assert (np.abs(gv - og) <= GRAD_RTOL * scale + GRAD_ATOL).all()

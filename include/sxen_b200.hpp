@@ -28,6 +28,10 @@ struct TrainingError : std::runtime_error {
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+// SXEN_NCCL_ERROR: the gradient exchange between ranks failed (no reference analogue either).
+struct CommError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 
 // Re-raises a C-ABI status as the exception the reference would have thrown.
 inline void check(sxen_status st) {
@@ -38,6 +42,7 @@ inline void check(sxen_status st) {
     case SXEN_LOGIC_ERROR: throw std::logic_error(msg);
     case SXEN_TRAINING_ERROR: throw TrainingError(msg);
     case SXEN_IO_ERROR: throw IoError(msg);
+    case SXEN_NCCL_ERROR: throw CommError(msg);
     default: throw CudaError(msg);
   }
 }

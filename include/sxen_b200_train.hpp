@@ -13,7 +13,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <exception>
 #include <functional>
+#include <thread>
 
 #include "sxen_b200.hpp"
 
@@ -98,6 +100,7 @@ struct TrainConfig {
   int threads = 0;
   int record_every = 100;
   int queue_window = 256;  // steps queued between two loss read-backs (1 = the reference's per-step cadence); <= 4096
+  int level_chunks = 4;    // batch-sharded runs: level ranges whose gradient exchange overlaps the next range's backward
 };
 
 // include/sxen/trainer.hpp:26-32 with device spans: coords = batch x dim, aux = batch x aux_dims pass-through inputs (empty
@@ -105,6 +108,54 @@ struct TrainConfig {
 // coordinating thread only; determinism comes from (seed, step).
 using BatchSampler = std::function<void(int step, DeviceSpan<double> coords, DeviceSpan<double> aux,
                                         DeviceSpan<double> targets, void* stream)>;
+
+// One rank's end of the gradient exchange of a batch-sharded run (sxen_comm_*, sxen_cuda.h).  The reference's analogue is
+// the worker fan-out and worker-order merge inside train_field (src/trainer.cpp:101-128); ranks are the workers here.
+class Comm {
+ public:
+  Comm() = default;
+  // NCCL, one process per GPU: rank 0 calls unique_id() and hands the bytes to its peers over any side channel.
+  static sxen_comm_id unique_id() {
+    sxen_comm_id id{};
+    check(sxen_comm_unique_id(&id));
+    return id;
+  }
+  Comm(const sxen_comm_id& id, int world, int rank, int device) { check(sxen_comm_create(&id, world, rank, device, &h_)); }
+  // LOCAL: every rank in this process, one host thread per rank (train_field_local below); devices[r] = rank r's device.
+  static std::vector<Comm> local(const std::vector<int>& devices) {
+    std::vector<std::int32_t> dev(devices.begin(), devices.end());
+    std::vector<sxen_comm*> raw(devices.size(), nullptr);
+    check(sxen_comm_create_local(static_cast<std::int32_t>(dev.size()), dev.data(), raw.data()));
+    std::vector<Comm> out(devices.size());
+    for (std::size_t r = 0; r < raw.size(); ++r) out[r].h_ = raw[r];
+    return out;
+  }
+  Comm(Comm&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
+  Comm& operator=(Comm&& o) noexcept {
+    if (this != &o) {
+      sxen_comm_destroy(h_);
+      h_ = std::exchange(o.h_, nullptr);
+    }
+    return *this;
+  }
+  Comm(const Comm&) = delete;
+  Comm& operator=(const Comm&) = delete;
+  ~Comm() { sxen_comm_destroy(h_); }
+  sxen_comm* handle() const { return h_; }
+  int world() const {
+    std::int32_t w = 1;
+    if (h_) check(sxen_comm_info(h_, &w, nullptr, nullptr, nullptr));
+    return w;
+  }
+  int rank() const {
+    std::int32_t r = 0;
+    if (h_) check(sxen_comm_info(h_, nullptr, &r, nullptr, nullptr));
+    return r;
+  }
+
+ private:
+  sxen_comm* h_ = nullptr;
+};
 
 // include/sxen/trainer.hpp:34-38
 struct TrainResult {
@@ -116,8 +167,14 @@ struct TrainResult {
 // sxen::train_field (src/trainer.cpp:53-139).  Throws TrainingError when a loss or gradient goes non-finite -- tables,
 // MLP and moments are then as they were before the offending step, as in the reference -- and std::invalid_argument
 // for the reference's argument checks (:55-65).
+//
+// comm != nullptr: this process (or thread) is ONE RANK of a batch-sharded run.  encoder / mlp are this rank's replicas,
+// initialised like every other rank's; the sampler fills the WHOLE batch on every rank (it is deterministic in (seed, step),
+// as the reference's contract requires, include/sxen/trainer.hpp:29-30), the rank runs its contiguous chunk
+// (src/trainer.cpp:93,107-108), gradients and the loss are summed over the ranks where the reference merges its workers
+// (:125-128) and every rank applies the identical update -- sxen_trainer_step_sharded, one loss read-back per step.
 inline TrainResult train_field(HashEncoder& encoder, Mlp& mlp, const BatchSampler& sampler, const TrainConfig& cfg,
-                               int device = 0, void* stream = nullptr) {
+                               int device = 0, void* stream = nullptr, const Comm* comm = nullptr) {
   if (cfg.batch_size < 1) throw std::invalid_argument("train: batch_size must be >= 1");
   if (cfg.steps < 0) throw std::invalid_argument("train: steps must be >= 0");
   if (cfg.aux_dims < 0) throw std::invalid_argument("train: aux_dims must be >= 0");  // src/trainer.cpp:59
@@ -139,6 +196,23 @@ inline TrainResult train_field(HashEncoder& encoder, Mlp& mlp, const BatchSample
   if (aux_w > 0) check(sxen_trainer_set_aux(trainer.h, aux.data(), SXEN_COORD_F64));
   const sxen_adam_config ta = cfg.table_adam.c(), ma = cfg.mlp_adam.c();
   TrainResult result;
+  if (comm != nullptr && comm->handle() != nullptr) {
+    if (aux_w > 0 && comm->world() > 1) throw std::invalid_argument("train: aux_dims > 0 is single-GPU on the device path");
+    check(sxen_trainer_set_comm(trainer.h, comm->handle()));
+    for (int step = 0; step < cfg.steps; ++step) {
+      sampler(step, coords.span(batch * dim), aux.span(batch * aux_w), targets.span(batch * out_w), stream);
+      double loss = 0.0;
+      const sxen_status st = sxen_trainer_step_sharded(trainer.h, coords.data(), SXEN_COORD_F64, targets.data(), SXEN_COORD_F64,
+                                                       batch, &ta, &ma, cfg.level_chunks, &loss, stream);
+      if (st == SXEN_TRAINING_ERROR && !std::isfinite(loss))
+        throw TrainingError("loss became non-finite at step " + std::to_string(step));  // src/trainer.cpp:121-123
+      check(st);
+      if (step % cfg.record_every == 0 || step == cfg.steps - 1) result.loss_curve.emplace_back(step, loss);
+      result.final_loss = loss;
+    }
+    result.steps_run = cfg.steps;
+    return result;
+  }
   std::vector<double> losses(static_cast<std::size_t>(cfg.queue_window));
   int first = 0;
   for (int step = 0; step < cfg.steps; ++step) {
@@ -163,6 +237,60 @@ inline TrainResult train_field(HashEncoder& encoder, Mlp& mlp, const BatchSample
   }
   result.steps_run = cfg.steps;
   return result;
+}
+
+// One model replica of a batch-sharded run inside ONE process (train_field_local): rank r's encoder and MLP on device r.
+struct Replica {
+  HashEncoder* encoder = nullptr;
+  Mlp* mlp = nullptr;
+  int device = 0;
+  void* stream = nullptr;
+};
+
+// train_field with the reference's own layout -- one worker THREAD per chunk of the batch (src/trainer.cpp:101-116) -- where
+// every worker drives a GPU: rank r trains replicas[r] through a LOCAL communicator (the library's peer-memory all-reduce;
+// two replicas may share a device).  make_sampler(r) returns rank r's BatchSampler (each rank fills its own device buffers
+// with the same (seed, step) stream).  Returns rank 0's result -- the loss curve is the same on every rank, and so are the
+// trained replicas, bit for bit (the exchange sums in rank order on one rank per slice).  An exception on any rank
+// breaks the group, every worker returns, and the first exception is rethrown here.
+inline TrainResult train_field_local(const std::vector<Replica>& replicas, const std::function<BatchSampler(int rank)>& make_sampler,
+                                     const TrainConfig& cfg) {
+  if (replicas.empty()) throw std::invalid_argument("train: no replicas");
+  std::vector<int> devices;
+  for (const Replica& r : replicas) {
+    if (r.encoder == nullptr || r.mlp == nullptr) throw std::invalid_argument("train: a replica lacks its encoder or MLP");
+    devices.push_back(r.device);
+  }
+  std::vector<Comm> comms = Comm::local(devices);
+  std::vector<TrainResult> results(replicas.size());
+  std::vector<std::exception_ptr> errors(replicas.size());
+  std::vector<std::thread> workers;
+  for (std::size_t r = 0; r < replicas.size(); ++r) {
+    workers.emplace_back([&, r] {
+      try {
+        results[r] = train_field(*replicas[r].encoder, *replicas[r].mlp, make_sampler(static_cast<int>(r)), cfg,
+                                 replicas[r].device, replicas[r].stream, &comms[r]);
+      } catch (...) {
+        errors[r] = std::current_exception();
+        sxen_comm_abort(comms[r].handle());  // peers waiting for this rank leave their collective with CommError
+      }
+    });
+  }
+  for (std::thread& w : workers) w.join();
+  // the rank that failed first in rank order speaks (peers of a failed rank only report the broken group)
+  std::exception_ptr first_comm;
+  for (std::size_t r = 0; r < errors.size(); ++r) {
+    if (!errors[r]) continue;
+    try {
+      std::rethrow_exception(errors[r]);
+    } catch (const CommError&) {
+      if (!first_comm) first_comm = errors[r];
+    } catch (...) {
+      std::rethrow_exception(errors[r]);
+    }
+  }
+  if (first_comm) std::rethrow_exception(first_comm);
+  return results[0];
 }
 
 // ------------------------------------------------------------------------------------------------ tasks

@@ -48,7 +48,8 @@ typedef enum sxen_status {
   SXEN_LOGIC_ERROR = 2,      /* std::logic_error      (src/mlp.cpp:165-167) */
   SXEN_TRAINING_ERROR = 3,   /* sxen::TrainingError   (src/trainer.cpp:121-123, src/optimizer.cpp:35-37,73-76) */
   SXEN_CUDA_ERROR = 4,       /* no reference analogue: device/runtime failure */
-  SXEN_IO_ERROR = 5          /* sxen::IoError         (include/sxen/errors.hpp:8-10) */
+  SXEN_IO_ERROR = 5,         /* sxen::IoError         (include/sxen/errors.hpp:8-10) */
+  SXEN_NCCL_ERROR = 6        /* no reference analogue: the gradient exchange between ranks failed (sxen_comm_*) */
 } sxen_status;
 
 typedef enum sxen_backend { SXEN_BACKEND_SIMPLEX = 0, SXEN_BACKEND_GRID = 1 } sxen_backend;           /* include/sxen/encoding.hpp:12 */
@@ -369,6 +370,56 @@ SXEN_API sxen_status sxen_trainer_pending(const sxen_trainer* trainer, size_t* o
  * encoder's rejected-sample word and non-finite gradients like sxen_trainer_step. */
 SXEN_API sxen_status sxen_trainer_collect(sxen_trainer* trainer, double* losses_out, size_t capacity, size_t* count_out,
                                           int64_t* failed_out, void* stream);
+
+/* ------------------------------------------------------------------ multi-GPU: batch-sharded step (src/trainer.cpp:93-128) */
+/* The reference fans a batch out over worker threads with private accumulators and merges them in worker order before the
+ * optimizer steps (src/trainer.cpp:101-128).  Here ranks are the workers -- one per GPU, tables / MLP / moments replicated,
+ * rank r takes the contiguous chunk [r*ceil(B/W), min(B, (r+1)*ceil(B/W))) of every batch (:93,107-108) -- and the merge is a
+ * SUM all-reduce of the table-gradient accumulator, the MLP gradient and the loss sum.  (The in-band "touched" marker
+ * survives a SUM: -0 + -0 = -0.)  A communicator is one rank's end of that exchange. */
+typedef struct sxen_comm sxen_comm;
+#define SXEN_COMM_ID_BYTES 128
+typedef struct sxen_comm_id { char bytes[SXEN_COMM_ID_BYTES]; } sxen_comm_id; /* an ncclUniqueId */
+/* NCCL transport, one process per GPU: rank 0 draws the id (ncclGetUniqueId), the host hands its bytes to the other ranks
+ * (file, socket, MPI, torch.distributed ...), every rank calls sxen_comm_create (ncclCommInitRank; collective).  libnccl.so.2
+ * is resolved at run time (an already loaded copy first, else the loader path, else $SXEN_NCCL_LIB). */
+SXEN_API sxen_status sxen_comm_unique_id(sxen_comm_id* out);
+SXEN_API sxen_status sxen_comm_create(const sxen_comm_id* id, int32_t world, int32_t rank, int32_t device, sxen_comm** out);
+/* LOCAL transport, all ranks in one process with ONE HOST THREAD PER RANK (the reference's worker-thread layout): fills
+ * out[0..world) with the ranks' handles; devices[r] is rank r's device (the same device may appear more than once).  The
+ * exchange is this library's own kernel over peer-mapped memory: rank r sums slice r of every rank's buffer in rank order --
+ * the reference's fixed merge order, so the result is bit-identical on all ranks and reproducible -- and stores it into
+ * every buffer (P2P loads / stores over NVLink between devices).  Every rank must call each collective, from its own
+ * thread; a rank that fails breaks the group (peers return SXEN_NCCL_ERROR instead of waiting). */
+SXEN_API sxen_status sxen_comm_create_local(int32_t world, const int32_t* devices, sxen_comm** out);
+SXEN_API sxen_status sxen_comm_destroy(sxen_comm* comm);
+/* Marks the group broken: peers blocked in (or later entering) a collective return SXEN_NCCL_ERROR instead of waiting for a
+ * rank that has failed.  LOCAL: immediate; NCCL: ncclCommAbort of this rank's communicator. */
+SXEN_API sxen_status sxen_comm_abort(sxen_comm* comm);
+/* any of the outputs may be NULL; kind: 0 = NCCL, 1 = LOCAL */
+SXEN_API sxen_status sxen_comm_info(const sxen_comm* comm, int32_t* world, int32_t* rank, int32_t* device, int32_t* kind);
+/* In-place SUM over the ranks of count elements (type: SXEN_COORD_F32 / SXEN_COORD_F64), stream-ordered. */
+SXEN_API sxen_status sxen_comm_allreduce(sxen_comm* comm, void* buf_dev, size_t count, sxen_coord_type type, void* stream);
+
+/* Attaches a communicator (not owned; NULL detaches) to a trainer.  The trainer's encoder, MLP and the communicator must
+ * live on the same device; replicas on all ranks must have been initialised identically (same seeds). */
+SXEN_API sxen_status sxen_trainer_set_comm(sxen_trainer* trainer, sxen_comm* comm);
+/* The exchange between sxen_trainer_accumulate* and sxen_trainer_update, in the pieces a host overlaps with the backward:
+ * _head sums the MLP gradient and the loss sum, _levels the accumulator slice of encoder levels [first_level,
+ * first_level + level_count) (contiguous: level l starts at values + l*T*F).  No-ops without a communicator. */
+SXEN_API sxen_status sxen_trainer_allreduce_head(sxen_trainer* trainer, void* stream);
+SXEN_API sxen_status sxen_trainer_allreduce_levels(sxen_trainer* trainer, int32_t first_level, int32_t level_count, void* stream);
+/* One whole batch-sharded step (train_field's loop body, src/trainer.cpp:94-136, with ranks as the workers).  coords_dev /
+ * targets_dev hold the WHOLE batch of global_batch samples on every rank (the samplers are deterministic in (seed, step), so
+ * nothing needs scattering); this rank runs its contiguous chunk, the exchange is overlapped with the backward -- the MLP
+ * gradient and the loss go first, then encode_backward walks the levels in level_chunks ranges and each range's slice is
+ * all-reduced on the trainer's second stream while the next range computes -- and every rank applies the identical update.
+ * *loss_out = batch MSE before the update, the same on all ranks.  SXEN_TRAINING_ERROR (non-finite loss: nothing was updated,
+ * on any rank) / SXEN_INVALID_ARGUMENT as sxen_trainer_step.  Without a communicator: a plain single-GPU step. */
+SXEN_API sxen_status sxen_trainer_step_sharded(sxen_trainer* trainer, const void* coords_dev, sxen_coord_type coord_type,
+                                               const void* targets_dev, sxen_coord_type target_type, size_t global_batch,
+                                               const sxen_adam_config* table_adam, const sxen_adam_config* mlp_adam,
+                                               int32_t level_chunks, double* loss_out, void* stream);
 
 /* ------------------------------------------------------------------ noise-field task around the path (src/noise.cpp, src/tasks.cpp:139-194) */
 typedef enum sxen_noise_kind { SXEN_NOISE_PERLIN = 0, SXEN_NOISE_SIMPLEX = 1 } sxen_noise_kind; /* include/sxen/noise.hpp:38 */

@@ -10,7 +10,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libsxen_b200.so")
 
-OK, INVALID_ARGUMENT, LOGIC_ERROR, TRAINING_ERROR, CUDA_ERROR, IO_ERROR = range(6)
+OK, INVALID_ARGUMENT, LOGIC_ERROR, TRAINING_ERROR, CUDA_ERROR, IO_ERROR, NCCL_ERROR = range(7)
 BACKEND_SIMPLEX, BACKEND_GRID = 0, 1
 SCALE_RAW, SCALE_EQUAL_MEMORY = 0, 1
 COORD_F64, COORD_F32 = 0, 1
@@ -158,6 +158,18 @@ SIGNATURES = {
     "sxen_trainer_set_aux": (C.c_int, [_vp, _vp, C.c_int]),
     "sxen_trainer_pending": (C.c_int, [_vp, _P(_sz)]),
     "sxen_trainer_collect": (C.c_int, [_vp, _P(_dbl), _sz, _P(_sz), _P(C.c_int64), _vp]),
+    "sxen_comm_unique_id": (C.c_int, [_vp]),
+    "sxen_comm_create": (C.c_int, [_vp, _i32, _i32, _i32, _P(_vp)]),
+    "sxen_comm_create_local": (C.c_int, [_i32, _P(_i32), _P(_vp)]),
+    "sxen_comm_destroy": (C.c_int, [_vp]),
+    "sxen_comm_abort": (C.c_int, [_vp]),
+    "sxen_comm_info": (C.c_int, [_vp, _P(_i32), _P(_i32), _P(_i32), _P(_i32)]),
+    "sxen_comm_allreduce": (C.c_int, [_vp, _vp, _sz, C.c_int, _vp]),
+    "sxen_trainer_set_comm": (C.c_int, [_vp, _vp]),
+    "sxen_trainer_allreduce_head": (C.c_int, [_vp, _vp]),
+    "sxen_trainer_allreduce_levels": (C.c_int, [_vp, _i32, _i32, _vp]),
+    "sxen_trainer_step_sharded": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, _sz, _P(AdamConfigC), _P(AdamConfigC), _i32,
+                                            _P(_dbl), _vp]),
 }
 
 

@@ -32,6 +32,9 @@ __global__ void sparse_adam_kernel(float* __restrict__ tables, float* __restrict
       const double g = static_cast<double>(grads[i]);
       if (!isfinite(g)) {
         atomicMin(status, static_cast<unsigned long long>(i));  // TrainingError, src/optimizer.cpp:73-76
+        // the reference aborts the run here; this ABI can be called again, so the row must not keep its NaN/Inf (the next
+        // backward would add into it): with clear_grad the whole row is re-armed like every other visited row
+        if (clear_grad) grads[i] = __uint_as_float(kUntouchedBits);
         continue;
       }
       double mi = m[i], vi = v[i];
@@ -56,6 +59,7 @@ __global__ void sparse_adam_f2_kernel(float2* __restrict__ tables, float2* __res
     const double gx = static_cast<double>(g2.x), gy = static_cast<double>(g2.y);
     if (!isfinite(gx) || !isfinite(gy)) {
       atomicMin(status, static_cast<unsigned long long>(2 * r + (isfinite(gx) ? 1 : 0)));
+      if (clear_grad) grads[r] = make_float2(__uint_as_float(kUntouchedBits), __uint_as_float(kUntouchedBits));  // (see above)
       continue;
     }
     double2 mm = m[r], vv = v[r];

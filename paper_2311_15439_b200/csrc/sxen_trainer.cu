@@ -4,6 +4,7 @@
 //   update         = SparseAdamState::step on the tables (touched rows only) + AdamState::step on the MLP (:129-130)
 // The two halves are separate entry points so a multi-GPU host can all-reduce the gradient buffers in between
 // (the reference merges its workers' accumulators at exactly that point, :125-128).
+#include <algorithm>
 #include <cmath>
 
 #include "sxen_common.hpp"
@@ -37,6 +38,10 @@ struct sxen_trainer {
   const void* aux = nullptr;         // caller-owned N x aux_dims pass-through inputs of the next batch (sxen_trainer_set_aux)
   sxen_coord_type aux_type = SXEN_COORD_F64;
   uint64_t mlp_params = 0;
+  // batch-sharded steps (sxen_trainer_set_comm / _step_sharded): the exchange runs on a second stream behind events
+  sxen_comm* comm = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_compute = nullptr, ev_comm = nullptr;
 };
 
 namespace {
@@ -47,12 +52,20 @@ constexpr unsigned long long kNoFailure = ~0ULL;
 // The loss half of train_field's step (src/trainer.cpp:118-123) for a queued step: loss = sum / (B * out_w) goes to the
 // step's slot, a non-finite loss closes the gate (the update kernels of this and every later queued step then return
 // without touching anything, as the reference throws before its optimizer steps), and the sum is re-armed.
+// The encoder's rejected-sample word closes the gate too: check_input throws before anything is computed
+// (src/encoding.cpp:183-194), so a batch with a coordinate outside [0,1] must not reach the optimizers either.
 __global__ void loss_record_kernel(double* __restrict__ loss_sum, double* __restrict__ ring, unsigned long long slot,
-                                   double denom, unsigned long long* __restrict__ gate) {
+                                   double denom, unsigned long long* __restrict__ gate,
+                                   const unsigned long long* __restrict__ rejected_sample) {
   const double loss = __ddiv_rn(*loss_sum, denom);
   ring[slot] = loss;
-  if (!isfinite(loss)) atomicMin(gate, slot);
+  if (!isfinite(loss) || *rejected_sample != kNoFailure) atomicMin(gate, slot);
   *loss_sum = 0.0;
+}
+
+// sharded steps: 1.0 when this rank's encoder rejected a coordinate in the batch (summed over the ranks with the loss)
+__global__ void reject_flag_kernel(double* __restrict__ flag, const unsigned long long* __restrict__ rejected_sample) {
+  *flag = (*rejected_sample != kNoFailure) ? 1.0 : 0.0;
 }
 
 // src/trainer.cpp:32-35: the aux inputs follow the encoding in every MLP input row, narrowed to float
@@ -139,9 +152,10 @@ sxen_status sxen_trainer_create_aux(sxen_encoder* enc, sxen_mlp* mlp, int32_t au
   if (st == SXEN_OK) st = sxen_sparse_adam_create(enc, &t->table_opt);
   if (st == SXEN_OK) st = sxen_mlp_parameter_count(mlp, &t->mlp_params);
   if (st == SXEN_OK) st = sxen_adam_create(static_cast<size_t>(t->mlp_params), t->device, &t->mlp_opt);
-  if (st == SXEN_OK && cudaMalloc(&t->loss_sum, sizeof(double)) != cudaSuccess) st = fail(SXEN_CUDA_ERROR, "trainer: allocation failed");
-  if (st == SXEN_OK && cudaMemset(t->loss_sum, 0, sizeof(double)) != cudaSuccess) st = fail(SXEN_CUDA_ERROR, "trainer: memset failed");
-  if (st == SXEN_OK && cudaHostAlloc(&t->loss_host, sizeof(double), cudaHostAllocDefault) != cudaSuccess)
+  // loss_sum[0] = sum of the per-sample losses; loss_sum[1] = ranks whose chunk held a rejected coordinate (sharded steps)
+  if (st == SXEN_OK && cudaMalloc(&t->loss_sum, 2 * sizeof(double)) != cudaSuccess) st = fail(SXEN_CUDA_ERROR, "trainer: allocation failed");
+  if (st == SXEN_OK && cudaMemset(t->loss_sum, 0, 2 * sizeof(double)) != cudaSuccess) st = fail(SXEN_CUDA_ERROR, "trainer: memset failed");
+  if (st == SXEN_OK && cudaHostAlloc(&t->loss_host, 2 * sizeof(double), cudaHostAllocDefault) != cudaSuccess)
     st = fail(SXEN_CUDA_ERROR, "trainer: pinned allocation failed");
   if (st == SXEN_OK && (cudaMalloc(&t->loss_ring, kLossRing * sizeof(double)) != cudaSuccess ||
                         cudaMalloc(&t->gate, sizeof(unsigned long long)) != cudaSuccess ||
@@ -174,6 +188,9 @@ sxen_status sxen_trainer_destroy(sxen_trainer* t) {
   cudaFree(t->gate);
   cudaFreeHost(t->loss_ring_host);
   cudaFreeHost(t->gate_host);
+  if (t->comm_stream) cudaStreamDestroy(t->comm_stream);
+  if (t->ev_compute) cudaEventDestroy(t->ev_compute);
+  if (t->ev_comm) cudaEventDestroy(t->ev_comm);
   delete t;
   return SXEN_OK;
 }
@@ -324,7 +341,7 @@ sxen_status sxen_trainer_step_enqueue(sxen_trainer* t, const void* coords_dev, s
   DeviceGuard guard(t->device);
   cudaStream_t s = as_stream(stream);
   loss_record_kernel<<<1, 1, 0, s>>>(t->loss_sum, t->loss_ring, static_cast<unsigned long long>(t->pending),
-                                     static_cast<double>(n_samples) * static_cast<double>(t->out_w), t->gate);
+                                     static_cast<double>(n_samples) * static_cast<double>(t->out_w), t->gate, t->enc->status);
   SXEN_CUDA(cudaGetLastError());
   count_launch();
   ++t->pending;
@@ -332,6 +349,127 @@ sxen_status sxen_trainer_step_enqueue(sxen_trainer* t, const void* coords_dev, s
   // visits its own rows instead of scanning all L*T
   const bool walk = own_rows_only && sxen_sparse_adam_walk_pays(t->enc, n_samples);
   return update_impl(t, table_adam, mlp_adam, walk ? coords_dev : nullptr, coord_type, n_samples, t->gate, stream);
+}
+
+// ------------------------------------------------------------------------------------------------ batch-sharded step
+sxen_status sxen_trainer_set_comm(sxen_trainer* t, sxen_comm* comm) {
+  SXEN_REQUIRE(t != nullptr, "trainer handle is null");
+  if (comm != nullptr) {
+    int32_t device = -1;
+    if (sxen_status st = sxen_comm_info(comm, nullptr, nullptr, &device, nullptr)) return st;
+    SXEN_REQUIRE(device == t->device, "train: the communicator lives on device %d, the trainer on device %d", device, t->device);
+    DeviceGuard guard(t->device);
+    if (t->comm_stream == nullptr) {
+      SXEN_CUDA(cudaStreamCreateWithFlags(&t->comm_stream, cudaStreamNonBlocking));
+      SXEN_CUDA(cudaEventCreateWithFlags(&t->ev_compute, cudaEventDisableTiming));
+      SXEN_CUDA(cudaEventCreateWithFlags(&t->ev_comm, cudaEventDisableTiming));
+    }
+  }
+  t->comm = comm;
+  return SXEN_OK;
+}
+
+sxen_status sxen_trainer_allreduce_head(sxen_trainer* t, void* stream) {
+  SXEN_REQUIRE(t != nullptr, "trainer handle is null");
+  if (t->comm == nullptr) return SXEN_OK;
+  double* mg = nullptr;
+  if (sxen_status st = sxen_mlp_grads_dev(t->mlp, &mg)) return st;
+  if (sxen_status st = sxen_comm_allreduce(t->comm, mg, static_cast<size_t>(t->mlp_params), SXEN_COORD_F64, stream)) return st;
+  t->foreign_grads = true;
+  return sxen_comm_allreduce(t->comm, t->loss_sum, 2, SXEN_COORD_F64, stream);
+}
+
+sxen_status sxen_trainer_allreduce_levels(sxen_trainer* t, int32_t first_level, int32_t level_count, void* stream) {
+  SXEN_REQUIRE(t != nullptr, "trainer handle is null");
+  sxen_encoder_config ec;
+  sxen_encoder_get_config(t->enc, &ec);
+  SXEN_REQUIRE(first_level >= 0 && level_count >= 0 && first_level + level_count <= ec.levels,
+               "level range [%d, %d) outside the encoder's %d levels", first_level, first_level + level_count, ec.levels);
+  if (t->comm == nullptr || level_count == 0) return SXEN_OK;
+  const size_t per_level = static_cast<size_t>(ec.table_size) * static_cast<size_t>(ec.features);
+  t->foreign_grads = true;  // the accumulator now holds other ranks' rows: the table update must scan, not walk this batch
+  return sxen_comm_allreduce(t->comm, t->grad->values + static_cast<size_t>(first_level) * per_level,
+                             static_cast<size_t>(level_count) * per_level, SXEN_COORD_F32, stream);
+}
+
+sxen_status sxen_trainer_step_sharded(sxen_trainer* t, const void* coords_dev, sxen_coord_type coord_type,
+                                      const void* targets_dev, sxen_coord_type target_type, size_t global_batch,
+                                      const sxen_adam_config* table_adam, const sxen_adam_config* mlp_adam,
+                                      int32_t level_chunks, double* loss_out, void* stream) {
+  SXEN_REQUIRE(t != nullptr && table_adam != nullptr && mlp_adam != nullptr, "null argument");
+  SXEN_REQUIRE(global_batch >= 1, "train: batch_size must be >= 1");  // src/trainer.cpp:57
+  SXEN_REQUIRE(coords_dev != nullptr && targets_dev != nullptr, "null argument");
+  if (t->pending != 0)
+    return fail(SXEN_LOGIC_ERROR, "train: %zu queued steps not collected (sxen_trainer_collect first)", t->pending);
+  int32_t world = 1, rank = 0;
+  if (t->comm != nullptr)
+    if (sxen_status st = sxen_comm_info(t->comm, &world, &rank, nullptr, nullptr)) return st;
+  SXEN_REQUIRE(t->aux_dims == 0 || world == 1, "train: aux_dims > 0 is single-GPU on the device path");
+  sxen_encoder_config ec;
+  sxen_encoder_get_config(t->enc, &ec);
+  // the reference's contiguous chunks with ranks as the workers: chunk = ceil(B / W), src/trainer.cpp:93,107-108
+  const size_t chunk = (global_batch + static_cast<size_t>(world) - 1) / static_cast<size_t>(world);
+  const size_t begin = std::min(global_batch, static_cast<size_t>(rank) * chunk);
+  const size_t n_local = std::min(global_batch, begin + chunk) - begin;
+  const size_t csize = coord_type == SXEN_COORD_F32 ? sizeof(float) : sizeof(double);
+  const size_t tsize = target_type == SXEN_COORD_F32 ? sizeof(float) : sizeof(double);
+  const char* x = static_cast<const char*>(coords_dev) + begin * static_cast<size_t>(ec.dim) * csize;
+  const char* y = static_cast<const char*>(targets_dev) + begin * static_cast<size_t>(t->out_w) * tsize;
+  DeviceGuard guard(t->device);
+  cudaStream_t s = as_stream(stream);
+  cudaStream_t cs = t->comm != nullptr ? t->comm_stream : s;
+  auto hand_to_comm = [&]() -> sxen_status {  // what the compute stream has queued so far precedes the next exchange
+    if (cs == s) return SXEN_OK;
+    SXEN_CUDA(cudaEventRecord(t->ev_compute, s));
+    SXEN_CUDA(cudaStreamWaitEvent(cs, t->ev_compute, 0));
+    return SXEN_OK;
+  };
+  // run_chunk's head on this rank's chunk (src/trainer.cpp:31-46), upstream scaled by the GLOBAL batch (:26-27)
+  if (sxen_status st = sxen_trainer_accumulate_head(t, x, coord_type, y, target_type, n_local, global_batch, stream)) return st;
+  reject_flag_kernel<<<1, 1, 0, s>>>(t->loss_sum + 1, t->enc->status);
+  SXEN_CUDA(cudaGetLastError());
+  count_launch();
+  if (sxen_status st = hand_to_comm()) return st;
+  if (sxen_status st = sxen_trainer_allreduce_head(t, cs)) return st;   // under the first range's backward
+  const int chunks = std::max(1, std::min<int>(level_chunks <= 0 ? 4 : level_chunks, ec.levels));
+  const int per = (ec.levels + chunks - 1) / chunks;
+  for (int first = 0; first < ec.levels; first += per) {
+    const int count = std::min(per, ec.levels - first);
+    if (n_local > 0)
+      if (sxen_status st = sxen_trainer_accumulate_tables(t, x, coord_type, n_local, first, count, stream)) return st;
+    if (sxen_status st = hand_to_comm()) return st;
+    if (sxen_status st = sxen_trainer_allreduce_levels(t, first, count, cs)) return st;
+  }
+  if (cs != s) {
+    SXEN_CUDA(cudaEventRecord(t->ev_comm, cs));
+    SXEN_CUDA(cudaStreamWaitEvent(s, t->ev_comm, 0));
+  }
+  // the merged loss decides, identically on every rank, whether the step is applied (src/trainer.cpp:118-123)
+  SXEN_CUDA(cudaMemcpyAsync(t->loss_host, t->loss_sum, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  SXEN_CUDA(cudaStreamSynchronize(s));
+  const double loss = t->loss_host[0] / (static_cast<double>(global_batch) * static_cast<double>(t->out_w));
+  if (loss_out) *loss_out = loss;
+  auto drop_step = [&]() -> sxen_status {
+    if (sxen_status st = sxen_grad_clear(t->grad, stream)) return st;
+    if (sxen_status st = sxen_mlp_grad_clear(t->mlp, stream)) return st;
+    SXEN_CUDA(cudaMemsetAsync(t->loss_sum, 0, 2 * sizeof(double), s));
+    t->foreign_grads = false;
+    return SXEN_OK;
+  };
+  if (t->loss_host[1] != 0.0) {  // some rank's chunk held a coordinate outside [0,1]: nobody updates (src/encoding.cpp:183-194)
+    if (sxen_status st = drop_step()) return st;
+    if (sxen_status st = sxen_encoder_check(t->enc, stream)) return st;  // this rank's own sample, named
+    return fail(SXEN_INVALID_ARGUMENT, "encode: a coordinate outside [0,1] was rejected on another rank");
+  }
+  if (!std::isfinite(loss)) {
+    if (sxen_status st = drop_step()) return st;
+    return fail(SXEN_TRAINING_ERROR, "loss became non-finite");
+  }
+  if (sxen_status st = update_impl(t, table_adam, mlp_adam, nullptr, coord_type, 0,
+                                   nullptr, stream))
+    return st;
+  SXEN_CUDA(cudaMemsetAsync(t->loss_sum, 0, 2 * sizeof(double), s));
+  return sxen_trainer_check(t, stream);
 }
 
 sxen_status sxen_trainer_pending(const sxen_trainer* t, size_t* out) {
@@ -374,6 +512,16 @@ sxen_status sxen_trainer_collect(sxen_trainer* t, double* losses_out, size_t cap
     t->foreign_grads = false;
     SXEN_CUDA(cudaStreamSynchronize(s));
     if (failed_out) *failed_out = static_cast<int64_t>(bad);
+    // the gated steps bumped both optimizers' step counters on the host without applying an update: take them back, so the
+    // next applied step uses the bias correction of the number of updates actually made (src/optimizer.cpp:31-32,64-66)
+    const int64_t skipped = static_cast<int64_t>(n) - static_cast<int64_t>(bad);
+    t->table_opt->t -= skipped;
+    t->mlp_opt->t -= skipped;
+    // re-read and reset the latched error words so they cannot surface on an unrelated later collect
+    const bool rejected = t->enc->status_host[0] != kNoFailure;
+    const sxen_status enc_st = sxen_encoder_check(t->enc, stream);
+    sxen_trainer_check(t, stream);
+    if (rejected && enc_st != SXEN_OK) return enc_st;  // std::invalid_argument: thrown before the step changed anything
     return fail(SXEN_TRAINING_ERROR, "loss became non-finite (queued step %llu of %zu)", bad, n);
   }
   if (words_clear) return SXEN_OK;

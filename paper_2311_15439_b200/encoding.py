@@ -136,11 +136,27 @@ def _coord_type(t):
     raise ValueError("coordinates must be float64 or float32")
 
 
-def _stream_ptr(stream) -> C.c_void_p:
+def _stream_ptr(stream, device=None) -> C.c_void_p:
+    """`stream` as a cudaStream_t; None = torch's current stream ON `device` (a handle's device index or a torch.device;
+    default: the current device) -- never another device's stream for a handle that lives elsewhere."""
     if stream is None:
         import torch
-        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
     return C.c_void_p(int(stream))
+
+
+def _owner_device(owner) -> int:
+    """Device index of the library handle behind `owner` (encoder / gradient / MLP / trainer mirrors)."""
+    for path in (("device",), ("encoder", "device"), ("mlp", "device")):
+        o = owner
+        for name in path:
+            o = getattr(o, name, None)
+            if o is None:
+                break
+        if isinstance(o, int):
+            return o
+    import torch
+    return torch.cuda.current_device()
 
 
 class EncoderGradient:
@@ -150,6 +166,7 @@ class EncoderGradient:
         self._lib = _lib()
         self._h = C.c_void_p()
         self._cfg = encoder.config
+        self.device = encoder.device
         raise_for(self._lib, self._lib.sxen_grad_create(encoder._h, C.byref(self._h)))
 
     def __del__(self):
@@ -210,7 +227,12 @@ class _DevArray:
 def _wrap_device(ptr: int, count: int, dtype, owner):
     import torch
     typestr = {torch.float32: "<f4", torch.float64: "<f8"}[dtype]
-    return torch.as_tensor(_DevArray(ptr, count, typestr, owner), device="cuda")
+    # the handle's device, not the current one: on another device torch would silently hand back a COPY, and a gradient
+    # exchange over that copy would exchange nothing
+    t = torch.as_tensor(_DevArray(ptr, count, typestr, owner), device=f"cuda:{_owner_device(owner)}")
+    if count and t.data_ptr() != ptr:
+        raise RuntimeError("device view: torch copied library-owned memory instead of wrapping it")
+    return t
 
 
 class HashEncoder:
@@ -302,7 +324,7 @@ class HashEncoder:
             elif tuple(out.shape) != (n, LF):  # src/encoding.cpp:297-299
                 raise ValueError("encode: output span has wrong width")
             raise_for(self._lib, self._lib.sxen_encoder_encode(self._h, C.c_void_p(x.data_ptr()), _coord_type(x), n,
-                                                               C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+                                                               C.c_void_p(out.data_ptr()), _stream_ptr(stream, self.device)))
             return out
         x = np.ascontiguousarray(x, dtype=np.float64)
         self._check_x(x)
@@ -329,11 +351,11 @@ class HashEncoder:
             if levels is not None:
                 raise_for(self._lib, self._lib.sxen_encoder_encode_backward_levels(
                     self._h, C.c_void_p(x.data_ptr()), _coord_type(x), C.c_void_p(upstream.data_ptr()), x.shape[0],
-                    grad._h, int(levels[0]), int(levels[1]), _stream_ptr(stream)))
+                    grad._h, int(levels[0]), int(levels[1]), _stream_ptr(stream, self.device)))
                 return
             raise_for(self._lib, self._lib.sxen_encoder_encode_backward(
                 self._h, C.c_void_p(x.data_ptr()), _coord_type(x), C.c_void_p(upstream.data_ptr()), x.shape[0],
-                grad._h, _stream_ptr(stream)))
+                grad._h, _stream_ptr(stream, self.device)))
             return
         if levels is not None:
             raise ValueError("encode_backward: a level range needs device tensors")
@@ -382,11 +404,11 @@ class HashEncoder:
         if levels is not None:
             raise_for(self._lib, self._lib.sxen_encoder_encode_forward_backward_levels(
                 self._h, C.c_void_p(x.data_ptr()), _coord_type(x), C.c_void_p(upstream.data_ptr()), n,
-                C.c_void_p(out.data_ptr()), grad._h, int(levels[0]), int(levels[1]), _stream_ptr(stream)))
+                C.c_void_p(out.data_ptr()), grad._h, int(levels[0]), int(levels[1]), _stream_ptr(stream, self.device)))
             return out
         raise_for(self._lib, self._lib.sxen_encoder_encode_forward_backward(
             self._h, C.c_void_p(x.data_ptr()), _coord_type(x), C.c_void_p(upstream.data_ptr()), n,
-            C.c_void_p(out.data_ptr()), grad._h, _stream_ptr(stream)))
+            C.c_void_p(out.data_ptr()), grad._h, _stream_ptr(stream, self.device)))
         return out
 
     def encode_debug(self, x, stream=None):
@@ -401,9 +423,9 @@ class HashEncoder:
         w = torch.zeros((n, L, V), dtype=torch.float64, device=x.device)
         raise_for(self._lib, self._lib.sxen_encoder_encode_debug(self._h, C.c_void_p(x.data_ptr()), _coord_type(x), n,
                                                                  C.c_void_p(idx.data_ptr()), C.c_void_p(w.data_ptr()),
-                                                                 _stream_ptr(stream)))
+                                                                 _stream_ptr(stream, self.device)))
         return idx.cpu().numpy().view(np.uint32), w.cpu().numpy()
 
     def check(self, stream=None) -> None:
         """Synchronise and raise what the reference would have thrown for launches since the last check."""
-        raise_for(self._lib, self._lib.sxen_encoder_check(self._h, _stream_ptr(stream) if stream is not None else C.c_void_p(0)))
+        raise_for(self._lib, self._lib.sxen_encoder_check(self._h, _stream_ptr(stream, self.device) if stream is not None else C.c_void_p(0)))

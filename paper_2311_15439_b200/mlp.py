@@ -148,7 +148,7 @@ class Mlp:
         raise_for(self._lib, self._lib.sxen_mlp_forward_backward(
             self._h, C.c_void_p(x.data_ptr()), C.c_void_p(tg.data_ptr()), typ, n, global_batch or n,
             C.c_void_p(pred.data_ptr()) if want_pred else None, C.c_void_p(ig.data_ptr()), C.c_void_p(loss.data_ptr()),
-            _stream_ptr(stream)))
+            _stream_ptr(stream, self.device)))
         return ig, loss, pred
 
     def forward(self, inputs, stream=None):
@@ -160,7 +160,7 @@ class Mlp:
         x = inputs.to(torch.float32).contiguous()
         out = torch.empty((x.shape[0], self._cfg.output_width), dtype=torch.float32, device=x.device)
         raise_for(self._lib, self._lib.sxen_mlp_forward(self._h, C.c_void_p(x.data_ptr()), x.shape[0],
-                                                        C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+                                                        C.c_void_p(out.data_ptr()), _stream_ptr(stream, self.device)))
         return out
 
     def backward(self, upstream, stream=None, dtype=None):
@@ -176,5 +176,5 @@ class Mlp:
         ig = torch.empty((n, self._cfg.input_width), dtype=torch.float32 if want32 else torch.float64, device=up.device)
         raise_for(self._lib, self._lib.sxen_mlp_backward(
             self._h, C.c_void_p(up.data_ptr()), n, C.c_void_p(ig.data_ptr()) if want32 else None,
-            None if want32 else C.c_void_p(ig.data_ptr()), _stream_ptr(stream)))
+            None if want32 else C.c_void_p(ig.data_ptr()), _stream_ptr(stream, self.device)))
         return ig

@@ -69,7 +69,7 @@ def image_sampler(image_dev, width: int, height: int, seed: int):
         raise_for(lib, lib.sxen_sample_image_batch(seed & ((1 << 64) - 1), step, C.c_void_p(image_dev.data_ptr()), width,
                                                    height, batch, C.c_void_p(coords.data_ptr()),
                                                    C.c_void_p(targets.data_ptr()),
-                                                   C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+                                                   C.c_void_p(torch.cuda.current_stream(image_dev.device).cuda_stream)))
         return coords, targets
 
     return sampler
@@ -87,7 +87,7 @@ def render_mse(encoder: HashEncoder, mlp: Mlp, image_dev, width: int, height: in
     dev = image_dev.device
     total = width * height
     acc = torch.zeros(1, dtype=torch.float64, device=dev)
-    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
     coords = torch.empty((min(chunk, total), 2), dtype=torch.float64, device=dev)
     for first in range(0, total, chunk):
         n = min(chunk, total - first)

@@ -90,21 +90,21 @@ class Trainer:
         coords, targets = coords.contiguous(), targets.contiguous()
         raise_for(self._lib, self._lib.sxen_trainer_accumulate(
             self._h, C.c_void_p(coords.data_ptr()), self._typ(coords), C.c_void_p(targets.data_ptr()),
-            self._typ(targets), coords.shape[0], global_batch, _stream_ptr(stream)))
+            self._typ(targets), coords.shape[0], global_batch, _stream_ptr(stream, self.encoder.device)))
 
     def accumulate_head(self, coords, targets, global_batch: int, stream=None) -> None:
         """encode -> MLP forward -> loss/upstream -> MLP backward; d(loss)/d(encoding) stays in the workspace."""
         from .encoding import _stream_ptr
         raise_for(self._lib, self._lib.sxen_trainer_accumulate_head(
             self._h, C.c_void_p(coords.data_ptr()), self._typ(coords), C.c_void_p(targets.data_ptr()),
-            self._typ(targets), coords.shape[0], global_batch, _stream_ptr(stream)))
+            self._typ(targets), coords.shape[0], global_batch, _stream_ptr(stream, self.encoder.device)))
 
     def accumulate_tables(self, coords, first_level: int, level_count: int, stream=None) -> None:
         """encode_backward of the batch of the last accumulate_head for one range of encoder levels."""
         from .encoding import _stream_ptr
         raise_for(self._lib, self._lib.sxen_trainer_accumulate_tables(
             self._h, C.c_void_p(coords.data_ptr()), self._typ(coords), coords.shape[0], first_level, level_count,
-            _stream_ptr(stream)))
+            _stream_ptr(stream, self.encoder.device)))
 
     def table_grad_device(self):
         """Flat float32 view of the table-gradient accumulator (untouched rows carry -0.0; SUM all-reduce keeps that)."""
@@ -126,15 +126,15 @@ class Trainer:
     def loss(self, global_batch: int, stream=None) -> float:
         from .encoding import _stream_ptr
         out = C.c_double()
-        raise_for(self._lib, self._lib.sxen_trainer_loss(self._h, global_batch, C.byref(out), _stream_ptr(stream)))
+        raise_for(self._lib, self._lib.sxen_trainer_loss(self._h, global_batch, C.byref(out), _stream_ptr(stream, self.encoder.device)))
         return out.value
 
     def update(self, table_adam: AdamConfig, mlp_adam: AdamConfig, stream=None, check: bool = True) -> None:
         from .encoding import _stream_ptr
         ta, ma = table_adam.c(), mlp_adam.c()
-        raise_for(self._lib, self._lib.sxen_trainer_update(self._h, C.byref(ta), C.byref(ma), _stream_ptr(stream)))
+        raise_for(self._lib, self._lib.sxen_trainer_update(self._h, C.byref(ta), C.byref(ma), _stream_ptr(stream, self.encoder.device)))
         if check:
-            raise_for(self._lib, self._lib.sxen_trainer_check(self._h, _stream_ptr(stream)))
+            raise_for(self._lib, self._lib.sxen_trainer_check(self._h, _stream_ptr(stream, self.encoder.device)))
 
     def step(self, coords, targets, table_adam: AdamConfig, mlp_adam: AdamConfig, stream=None) -> float:
         """One whole single-GPU step; returns the batch MSE before the update (TrainResult::loss_curve's value)."""
@@ -144,7 +144,7 @@ class Trainer:
         out = C.c_double()
         raise_for(self._lib, self._lib.sxen_trainer_step(
             self._h, C.c_void_p(coords.data_ptr()), self._typ(coords), C.c_void_p(targets.data_ptr()),
-            self._typ(targets), coords.shape[0], C.byref(ta), C.byref(ma), C.byref(out), _stream_ptr(stream)))
+            self._typ(targets), coords.shape[0], C.byref(ta), C.byref(ma), C.byref(out), _stream_ptr(stream, self.encoder.device)))
         return out.value
 
     def step_enqueue(self, coords, targets, table_adam: AdamConfig, mlp_adam: AdamConfig, stream=None) -> None:
@@ -155,7 +155,7 @@ class Trainer:
         ta, ma = table_adam.c(), mlp_adam.c()
         raise_for(self._lib, self._lib.sxen_trainer_step_enqueue(
             self._h, C.c_void_p(coords.data_ptr()), self._typ(coords), C.c_void_p(targets.data_ptr()),
-            self._typ(targets), coords.shape[0], C.byref(ta), C.byref(ma), _stream_ptr(stream)))
+            self._typ(targets), coords.shape[0], C.byref(ta), C.byref(ma), _stream_ptr(stream, self.encoder.device)))
 
     def pending(self) -> int:
         n = C.c_size_t()
@@ -171,11 +171,32 @@ class Trainer:
         n = self.pending()
         buf = (C.c_double * max(n, 1))()
         cnt, failed = C.c_size_t(), C.c_int64(-1)
-        st = self._lib.sxen_trainer_collect(self._h, buf, n, C.byref(cnt), C.byref(failed), _stream_ptr(stream))
+        st = self._lib.sxen_trainer_collect(self._h, buf, n, C.byref(cnt), C.byref(failed), _stream_ptr(stream, self.encoder.device))
         if st == _abi.TRAINING_ERROR and failed.value >= 0:
             return list(buf[:cnt.value]), failed.value
         raise_for(self._lib, st)
         return list(buf[:cnt.value]), -1
+
+    def set_comm(self, comm) -> None:
+        """Attaches a ``Comm`` (kept alive here; None detaches): ``step_sharded`` then exchanges through the C ABI."""
+        self._comm_handle = comm
+        raise_for(self._lib, self._lib.sxen_trainer_set_comm(self._h, comm._h if comm is not None else None))
+
+    def step_sharded(self, coords, targets, table_adam: AdamConfig, mlp_adam: AdamConfig, level_chunks: int = 4,
+                     stream=None) -> float:
+        """sxen_trainer_step_sharded: one whole batch-sharded step inside the library -- coords / targets hold the WHOLE batch
+        on every rank, this rank runs its contiguous chunk (src/trainer.cpp:93,107-108), the exchange (the attached Comm)
+        overlaps the backward level range by level range, every rank applies the identical update.  Returns the batch MSE
+        before the update; raises TrainingError (nothing updated, on any rank) when it is non-finite."""
+        from .comm import _check
+        from .encoding import _stream_ptr
+        coords, targets = coords.contiguous(), targets.contiguous()
+        ta, ma = table_adam.c(), mlp_adam.c()
+        out = C.c_double()
+        _check(self._lib, self._lib.sxen_trainer_step_sharded(
+            self._h, C.c_void_p(coords.data_ptr()), self._typ(coords), C.c_void_p(targets.data_ptr()), self._typ(targets),
+            coords.shape[0], C.byref(ta), C.byref(ma), level_chunks, C.byref(out), _stream_ptr(stream, self.encoder.device)))
+        return out.value
 
     def distributed_step(self, coords, targets, table_adam: AdamConfig, mlp_adam: AdamConfig, group=None,
                          level_chunks: int = 4) -> float:

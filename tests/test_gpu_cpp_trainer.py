@@ -266,12 +266,30 @@ def test_queued_steps_report_a_rejected_coordinate_at_collect(sx):
     bad = x.clone()
     bad[37, 1] = 1.5
     tr.step_enqueue(x, y, ta, ma)
+    torch.cuda.synchronize()
+    tables1 = np.stack([enc.table(l) for l in range(enc.config.levels)])
+    params1 = mlp.parameters().copy()
     tr.step_enqueue(bad, y, ta, ma)
+    tr.step_enqueue(x, y, ta, ma)   # queued behind the rejected batch: must not be applied either
     with pytest.raises(ValueError, match="sample 37"):
         tr.collect()
+    # the reference rejects the batch before it changes anything (check_input throws inside encode): tables, MLP and the
+    # step counters are as they were after the one good step -- the device gate closed on the encoder's rejected-sample word
+    assert np.array_equal(np.stack([enc.table(l) for l in range(enc.config.levels)]), tables1)
+    assert np.array_equal(mlp.parameters(), params1)
+    # a twin that ran the same two good steps and nothing else ends in the same state (bias corrections included)
+    _, enc2, mlp2 = _model(sx)
+    tr2 = sx.Trainer(enc2, mlp2)
+    tr2.step_enqueue(x, y, ta, ma)
+    tr2.step_enqueue(x, y, ta, ma)
+    tr2.collect()
     tr.step_enqueue(x, y, ta, ma)
     losses, failed = tr.collect()
     assert failed == -1 and len(losses) == 1 and np.isfinite(losses[0])
+    # (fp32 atomics: same rows, values to the accumulation-order bar)
+    a = np.stack([enc.table(l) for l in range(enc.config.levels)])
+    b = np.stack([enc2.table(l) for l in range(enc2.config.levels)])
+    assert np.array_equal(a != tables1, b != tables1) and np.abs(a - b).max() <= 1e-3 * 1e-2
 
 
 def test_per_step_call_refuses_to_jump_a_queue(sx):

@@ -1,0 +1,315 @@
+"""GPU (-m gpu): the batch-sharded training step on ONE B200 -- two ranks sharing cuda:0.
+
+The reference fans a batch out over worker threads with private accumulators and merges them in worker order before the
+optimizer steps (src/trainer.cpp:93,101-128).  Ranks are the workers here.  Covered:
+  * the C ABI's communicator (sxen_comm_*): LOCAL transport (the library's own peer-memory kernel) from two host threads,
+    NCCL transport through a one-rank communicator (NCCL refuses two ranks on one device)
+  * sxen_trainer_step_sharded from Python threads and from a C++ host program (train_field_local): every rank ends with the
+    same model bit for bit; against a single-GPU twin on the whole batch the updated-row sets are equal and values agree to
+    the fp32-accumulation bar
+  * Trainer.distributed_step (torch.distributed exchange) on two gloo ranks that share cuda:0
+"""
+import os
+import socket
+import subprocess
+import threading
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TABLE_ATOL = 2e-3 * 1e-2 + 1e-7   # Adam steps are <= lr = 1e-2 per step; fp32 accumulation order moves them by ~1e-3 of that
+LOSS_RTOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def sx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2311_15439_b200 as pkg
+    return pkg
+
+
+def run_ranks(world, fn):
+    """fn(rank) on one host thread per rank; re-raises the first failure."""
+    errors, results = [None] * world, [None] * world
+
+    def body(r):
+        try:
+            results[r] = fn(r)
+        except BaseException as exc:  # noqa: BLE001
+            errors[r] = exc
+
+    threads = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    for e in errors:
+        if e is not None:
+            raise e
+    return results
+
+
+def test_local_allreduce_sums_in_rank_order_and_keeps_the_untouched_marker(sx):
+    """sxen_comm_allreduce over the LOCAL transport: SUM in place on every rank, identical bits on all ranks, -0.0f (the
+    accumulator's "untouched" marker) survives exactly where every rank holds it; ragged counts (slices are cut on 16-byte
+    packs) and float64 buffers included."""
+    for world in (2, 3):
+        comms = sx.Comm.local([0] * world)
+        assert [c.info()["rank"] for c in comms] == list(range(world)) and comms[0].info()["kind"] == "local"
+        for count, dtype in ((1 << 20, torch.float32), (1001, torch.float32), (3, torch.float32), (6467, torch.float64),
+                             (0, torch.float32)):
+            gen = torch.Generator(device="cuda").manual_seed(count + world)
+            src = [torch.randn(count, dtype=dtype, device="cuda:0", generator=gen) for _ in range(world)]
+            if count >= 3:
+                for r in range(world):
+                    src[r][0] = -0.0          # untouched everywhere
+                    src[r][1] = -0.0
+                src[world - 1][1] = 0.0       # touched (zero gradient) on the last rank only
+            bufs = [t.clone() for t in src]
+            streams = [torch.cuda.Stream() for _ in range(world)]
+            for s in streams:
+                s.wait_stream(torch.cuda.current_stream())
+
+            def body(r):
+                with torch.cuda.stream(streams[r]):
+                    comms[r].allreduce(bufs[r], stream=streams[r].cuda_stream)
+                streams[r].synchronize()
+
+            run_ranks(world, body)
+            want = src[0].clone()
+            for r in range(1, world):
+                want = want + src[r]          # rank order, the reference's merge order
+            for r in range(world):
+                assert torch.equal(bufs[r].view(torch.int32 if dtype == torch.float32 else torch.int64),
+                                   want.view(torch.int32 if dtype == torch.float32 else torch.int64)), (world, count, r)
+            if count >= 3:
+                bits = bufs[0][:2].view(torch.int32).tolist() if dtype == torch.float32 else None
+                if bits is not None:
+                    assert bits[0] == -(1 << 31) and bits[1] == 0   # -0.0 kept, +0.0 where any rank touched
+
+
+def _models(sx, cfg, precision, n):
+    out = []
+    for _ in range(n):
+        enc = sx.HashEncoder(cfg)
+        enc.init_tables(42)
+        mlp = sx.Mlp(sx.MlpConfig(cfg.encoded_width(), 64, 2, 3))
+        mlp.init_params(sx.hash_combine(42, 1))
+        mlp.set_precision(precision)
+        out.append((enc, mlp, sx.Trainer(enc, mlp)))
+    return out
+
+
+def _tables(enc):
+    return np.stack([enc.table(l) for l in range(enc.config.levels)])
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+@pytest.mark.parametrize("world,batch", [(2, 6001), (3, 4096)])
+def test_step_sharded_on_ranks_sharing_one_gpu_matches_the_whole_batch_step(sx, precision, world, batch):
+    """sxen_trainer_step_sharded, one host thread per rank, LOCAL communicator on cuda:0: contiguous chunks of ceil(B/W)
+    (src/trainer.cpp:93,107-108), upstream scaled by the global batch (:26-27), gradients merged where the reference merges
+    its workers (:125-128), identical update on every rank."""
+    cfg = sx.EncoderConfig(dim=3, levels=16, table_size=1 << 14, features=2, base_resolution=16, growth=1.5)
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    steps = 4
+    xs = [torch.rand((batch, 3), dtype=torch.float64, device="cuda:0", generator=gen) for _ in range(steps)]
+    ys = [torch.rand((batch, 3), dtype=torch.float64, device="cuda:0", generator=gen) for _ in range(steps)]
+    ta, ma = sx.AdamConfig(lr=1e-2), sx.AdamConfig(lr=1e-3)
+    torch.cuda.synchronize()
+    ranks = _models(sx, cfg, precision, world)
+    comms = sx.Comm.local([0] * world)
+    init = _tables(ranks[0][0])
+    streams = [torch.cuda.Stream() for _ in range(world)]
+
+    def body(r):
+        enc, mlp, tr = ranks[r]
+        tr.set_comm(comms[r])
+        losses = []
+        with torch.cuda.stream(streams[r]):
+            for x, y in zip(xs, ys):
+                losses.append(tr.step_sharded(x, y, ta, ma, level_chunks=4, stream=streams[r].cuda_stream))
+        streams[r].synchronize()
+        return losses
+
+    losses = run_ranks(world, body)
+    (enc1, mlp1, tr1), = _models(sx, cfg, precision, 1)
+    whole = [tr1.step(x, y, ta, ma) for x, y in zip(xs, ys)]
+    torch.cuda.synchronize()
+    t0 = _tables(ranks[0][0])
+    for r in range(1, world):
+        assert losses[r] == losses[0]                                    # the same merged loss on every rank, bit for bit
+        assert np.array_equal(_tables(ranks[r][0]), t0)                  # ... and the same model
+        assert np.array_equal(ranks[r][1].parameters(), ranks[0][1].parameters())
+    assert np.allclose(losses[0], whole, rtol=LOSS_RTOL if precision == 0 else 1e-3)
+    tw = _tables(enc1)
+    if precision == 0:
+        assert np.array_equal(t0 != init, tw != init)                    # exactly the rows the whole-batch step updated
+    assert np.abs(t0 - tw).max() <= (TABLE_ATOL if precision == 0 else 20 * TABLE_ATOL)
+    assert np.abs(ranks[0][1].parameters() - mlp1.parameters()).max() <= (1e-5 if precision == 0 else 2e-3)
+
+
+def test_step_sharded_rejects_on_every_rank_and_survives(sx):
+    """A coordinate outside [0,1] in one rank's chunk: ValueError on every rank (check_input, src/encoding.cpp:183-194),
+    no rank updates, the next good step goes through.  A non-finite target: TrainingError on every rank, same guarantee
+    (src/trainer.cpp:121-123)."""
+    cfg = sx.EncoderConfig(dim=2, levels=8, table_size=1 << 12, features=2, base_resolution=8, growth=1.7)
+    world, batch = 2, 1000
+    ta, ma = sx.AdamConfig(lr=1e-2), sx.AdamConfig(lr=1e-3)
+    x = torch.rand((batch, 2), dtype=torch.float64, device="cuda:0")
+    y = torch.rand((batch, 3), dtype=torch.float64, device="cuda:0")
+    bad_x = x.clone()
+    bad_x[batch - 3, 0] = -0.5       # rank 1's chunk
+    bad_y = y.clone()
+    bad_y[5, 1] = float("nan")       # rank 0's chunk
+    torch.cuda.synchronize()
+    ranks = _models(sx, cfg, 0, world)
+    comms = sx.Comm.local([0] * world)
+    init = _tables(ranks[0][0])
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    seen = [[] for _ in range(world)]
+
+    def body(r):
+        enc, mlp, tr = ranks[r]
+        tr.set_comm(comms[r])
+        with torch.cuda.stream(streams[r]):
+            for xx, yy in ((bad_x, y), (x, bad_y)):
+                try:
+                    tr.step_sharded(xx, yy, ta, ma, stream=streams[r].cuda_stream)
+                    seen[r].append("ok")
+                except ValueError as exc:
+                    seen[r].append(("ValueError", str(exc)))
+                except sx.TrainingError:
+                    seen[r].append("TrainingError")
+            streams[r].synchronize()
+            assert np.array_equal(_tables(enc), init)
+            return tr.step_sharded(x, y, ta, ma, stream=streams[r].cuda_stream)
+
+    good = run_ranks(world, body)
+    assert seen[0][0][0] == "ValueError" and "another rank" in seen[0][0][1]
+    assert seen[1][0][0] == "ValueError" and f"sample {batch - 3 - 500}" in seen[1][0][1]   # index inside rank 1's chunk
+    assert seen[0][1] == seen[1][1] == "TrainingError"
+    assert good[0] == good[1] and np.isfinite(good[0])
+    assert not np.array_equal(_tables(ranks[0][0]), init)
+    assert np.array_equal(_tables(ranks[0][0]), _tables(ranks[1][0]))
+
+
+def test_nccl_transport_through_the_c_abi_on_one_rank(sx):
+    """sxen_comm_unique_id / sxen_comm_create (ncclGetUniqueId / ncclCommInitRank through dlopen): a one-rank communicator
+    all-reduces in place and sxen_trainer_step_sharded through it reproduces the plain step."""
+    comm = sx.Comm.nccl(sx.Comm.unique_id(), 1, 0, 0)
+    assert comm.info() == {"world": 1, "rank": 0, "device": 0, "kind": "nccl"}
+    t = torch.randn(100003, dtype=torch.float32, device="cuda:0")
+    want = t.clone()
+    comm.allreduce(t)
+    torch.cuda.synchronize()
+    assert torch.equal(t, want)
+    cfg = sx.EncoderConfig(dim=3, levels=16, table_size=1 << 14, features=2, base_resolution=16, growth=1.5)
+    x = torch.rand((5000, 3), dtype=torch.float32, device="cuda:0")
+    y = torch.rand((5000, 3), dtype=torch.float32, device="cuda:0")
+    ta, ma = sx.AdamConfig(lr=1e-2), sx.AdamConfig(lr=1e-3)
+    (e0, m0, tr0), (e1, m1, tr1) = _models(sx, cfg, 1, 2)
+    tr1.set_comm(comm)
+    a = [tr0.step(x, y, ta, ma) for _ in range(3)]
+    b = [tr1.step_sharded(x, y, ta, ma) for _ in range(3)]
+    torch.cuda.synchronize()
+    assert np.allclose(a, b, rtol=1e-5)
+    assert np.abs(_tables(e0) - _tables(e1)).max() <= TABLE_ATOL
+    with pytest.raises(ValueError):
+        sx.Comm.nccl(b"short", 1, 0, 0)
+
+
+def test_cpp_host_trains_sharded_without_python(sx, tmp_path):
+    """tests/cpp/sharded_train_check.cpp: train_field_local (include/sxen_b200_train.hpp) -- worker threads as ranks, each
+    driving a replica on cuda:0 through the LOCAL communicator -- against a single-GPU twin, plus a rejected coordinate
+    in one rank's chunk."""
+    exe = str(tmp_path / "sharded_train_check")
+    lib_dir = os.path.join(ROOT, "paper_2311_15439_b200", "lib")
+    subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "sharded_train_check.cpp"), "-o", exe, "-L", lib_dir,
+                    "-lsxen_b200", f"-Wl,-rpath,{lib_dir}", "-lpthread"], check=True)
+    for ranks, batch in ((2, 4097), (3, 2048)):
+        # 4 steps: Adam (epsilon 1e-15) turns any difference in a near-zero gradient into a full lr-sized step, so runs that
+        # differ only in fp32 summation order drift apart step by step; the comparison with the twin is made while the bar
+        # of one step's accumulation error still means something
+        run = subprocess.run([exe, str(ranks), "4", str(batch)], capture_output=True, text=True, timeout=600)
+        assert run.returncode == 0 and run.stdout.strip().endswith("sharded ok"), run.stdout + run.stderr
+        lines = {l.split()[0]: l.split() for l in run.stdout.splitlines()}
+        for tag in ("exact", "tc"):
+            f = dict(zip(lines[tag][1::2], lines[tag][2::2]))
+            assert int(f["updated_rows"]) > 1000
+            if tag == "exact":
+                assert int(f["row_set_mismatch"]) == 0 and int(f["updated_rows"]) == int(f["twin"])
+            assert float(f["table_max_abs_diff"]) <= (TABLE_ATOL if tag == "exact" else 20 * TABLE_ATOL)
+            assert float(f["loss_max_rel_diff"]) <= (1e-5 if tag == "exact" else 1e-3)
+            assert float(f["last_loss"]) < float(f["first_loss"])
+        assert "rejected" in lines and "another rank" in run.stdout
+
+
+# ------------------------------------------------------------------------------------------ torch.distributed, 2 gloo ranks
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gloo_rank(rank, world, port, out_dir):
+    """One rank of Trainer.distributed_step over gloo (CUDA tensors staged through the host), all ranks on cuda:0."""
+    import torch.distributed as dist
+
+    import paper_2311_15439_b200 as sx
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    cfg = sx.EncoderConfig(dim=3, levels=16, table_size=1 << 14, features=2, base_resolution=16, growth=1.5)
+    enc = sx.HashEncoder(cfg)
+    enc.init_tables(42)
+    mlp = sx.Mlp(sx.MlpConfig(32, 64, 2, 3))
+    mlp.init_params(sx.hash_combine(42, 1))
+    tr = sx.Trainer(enc, mlp)
+    gen = torch.Generator(device="cuda").manual_seed(3)   # the same whole batch on every rank
+    ta, ma = sx.AdamConfig(lr=1e-2), sx.AdamConfig(lr=1e-3)
+    losses = []
+    for _ in range(3):
+        x = torch.rand((5001, 3), dtype=torch.float64, device="cuda:0", generator=gen)
+        y = torch.rand((5001, 3), dtype=torch.float64, device="cuda:0", generator=gen)
+        losses.append(tr.distributed_step(x, y, ta, ma, level_chunks=4))
+    torch.cuda.synchronize()
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), losses=np.array(losses),
+             tables=np.stack([enc.table(l) for l in range(16)]), params=mlp.parameters())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_distributed_step_on_two_gloo_ranks_sharing_one_gpu(sx, tmp_path):
+    """The real Trainer.distributed_step (level-chunked backward, exchange on a second stream) on world_size 2: each rank
+    runs its half of every batch on cuda:0, gloo carries the SUM.  Both ranks must end with the same model, which must
+    match a single-rank run of the whole batches: same updated rows, values to the fp32-accumulation bar."""
+    import torch.multiprocessing as mp
+    world = 2
+    mp.spawn(_gloo_rank, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    r0, r1 = np.load(tmp_path / "rank0.npz"), np.load(tmp_path / "rank1.npz")
+    assert np.array_equal(r0["losses"], r1["losses"])
+    assert np.array_equal(r0["tables"], r1["tables"]) and np.array_equal(r0["params"], r1["params"])
+    cfg = sx.EncoderConfig(dim=3, levels=16, table_size=1 << 14, features=2, base_resolution=16, growth=1.5)
+    (enc, mlp, tr), = _models(sx, cfg, 0, 1)
+    init = _tables(enc)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    ta, ma = sx.AdamConfig(lr=1e-2), sx.AdamConfig(lr=1e-3)
+    whole = []
+    for _ in range(3):
+        x = torch.rand((5001, 3), dtype=torch.float64, device="cuda:0", generator=gen)
+        y = torch.rand((5001, 3), dtype=torch.float64, device="cuda:0", generator=gen)
+        whole.append(tr.step(x, y, ta, ma))
+    torch.cuda.synchronize()
+    assert np.allclose(r0["losses"], whole, rtol=LOSS_RTOL)
+    tw = _tables(enc)
+    assert np.array_equal(r0["tables"] != init, tw != init)
+    assert np.abs(r0["tables"] - tw).max() <= TABLE_ATOL
+    assert np.abs(r0["params"] - mlp.parameters()).max() <= 1e-5

@@ -412,6 +412,16 @@ def run_ours(args):
     ranges = sx.level_ranges(L, args.level_chunks if exchange else 1)
     per_level = gview.numel() // L
     comm = torch.cuda.Stream(device=dev) if exchange else None
+    # the exchange goes through the library's own communicator (sxen_comm_*: NCCL resolved with dlopen, the id carried by the
+    # launcher's process group); oversubscribed functional runs (two ranks on one device, which NCCL refuses) use gloo
+    abi_comm = sx.Comm.from_torch(local_rank) if exchange and dist.get_backend() == "nccl" else None
+
+    def allreduce(t, on):
+        if abi_comm is not None:
+            abi_comm.allreduce(t, stream=on.cuda_stream)
+        else:
+            with torch.cuda.stream(on):
+                dist.all_reduce(t)
 
     def step_overlapped(i, ev=None):
         """Batch-sharded step: the levels are walked in chunks and each chunk's slice of the table-gradient accumulator is
@@ -429,8 +439,7 @@ def run_ours(args):
             done = torch.cuda.Event()
             done.record(stream)
             comm.wait_event(done)
-            with torch.cuda.stream(comm):
-                dist.all_reduce(gview[first * per_level:(first + count) * per_level])
+            allreduce(gview[first * per_level:(first + count) * per_level], comm)
         if ev is not None:
             ev[1].record(stream)  # compute done; the tail of the exchange is inside the step but not inside kernel_ms
         stream.wait_stream(comm)
@@ -451,7 +460,7 @@ def run_ours(args):
             if ev is not None:
                 ev[1].record(stream)
         if dist is not None and not args.no_allreduce:
-            dist.all_reduce(gview)  # table-gradient exchange of the batch-sharded step
+            allreduce(gview, stream)  # table-gradient exchange of the batch-sharded step
 
     for i in range(args.warmup):
         step(i)
@@ -706,7 +715,8 @@ def run_ours(args):
                        "tuning": {"levels_per_thread": t.levels_per_thread, "block_threads": t.block_threads,
                                   "level_major": t.level_major, "exact_blend": t.exact_blend,
                                   "warp_aggregate": t.warp_aggregate, "level_chunk": t.level_chunk},
-                       "multi_gpu": (f"batch sharded over {world} ranks, tables replicated, {dist.get_backend()} SUM all-reduce of "
+                       "multi_gpu": (f"batch sharded over {world} ranks, tables replicated, "
+                                     f"{'sxen_comm_allreduce (NCCL)' if abi_comm is not None else dist.get_backend()} SUM all-reduce of "
                                      f"the {L * (1 << args.log2t) * F * 4 >> 20} MiB table-gradient accumulator per step in "
                                      f"{len(ranges)} level chunks overlapped with the next chunk's kernel")
                                     if exchange else (f"{world} replicas, no exchange (--no-allreduce)" if world > 1

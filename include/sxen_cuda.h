@@ -54,7 +54,8 @@ typedef enum sxen_status {
 
 typedef enum sxen_backend { SXEN_BACKEND_SIMPLEX = 0, SXEN_BACKEND_GRID = 1 } sxen_backend;           /* include/sxen/encoding.hpp:12 */
 typedef enum sxen_level_scale { SXEN_SCALE_RAW = 0, SXEN_SCALE_EQUAL_MEMORY = 1 } sxen_level_scale;   /* include/sxen/encoding.hpp:13 */
-typedef enum sxen_coord_type { SXEN_COORD_F64 = 0, SXEN_COORD_F32 = 1 } sxen_coord_type;
+typedef enum sxen_coord_type { SXEN_COORD_F64 = 0, SXEN_COORD_F32 = 1,
+                               SXEN_ELEM_I64 = 2 /* sxen_comm_allreduce only: the fixed-point accumulator words */ } sxen_coord_type;
 
 /* sxen::EncoderConfig, field for field (include/sxen/encoding.hpp:18-33). */
 typedef struct sxen_encoder_config {
@@ -238,6 +239,20 @@ SXEN_API sxen_status sxen_grad_download(const sxen_grad* grad, int32_t level, fl
 /* Inverse of sxen_grad_download: overwrites one level (rows with touched_host[r]==0 become untouched). */
 SXEN_API sxen_status sxen_grad_upload(sxen_grad* grad, int32_t level, const float* values_host, const uint8_t* touched_host);
 SXEN_API sxen_status sxen_grad_touched_total(const sxen_grad* grad, uint64_t* out); /* EncoderGradient::touched_total */
+/* Reproducible accumulation (opt-in; on != 0 allocates a second L x T x F buffer of 64-bit words).  The reference's gradient
+ * sums are bit-reproducible for a fixed (seed, threads): per-worker fp64 accumulators merged in worker order
+ * (src/trainer.cpp:125-128, tests/test_neural.cpp:370-408).  fp32 atomics are not: the order they land in changes the low
+ * bits, and Adam (epsilon 1e-15) turns low bits of near-zero gradients into lr-sized steps.  In this mode every backward
+ * ALSO adds each contribution -- the fp64 product w * upstream, as src/encoding.cpp:116 -- as 64-bit fixed point in units of
+ * 2^-52 with integer atomics (associative: order-free), and the optimizers, sxen_grad_download* and sxen_grad_merge use those
+ * sums.  The fp32 accumulator keeps carrying "touched" and the non-finite check; a sum of magnitude >= 2^10 is outside the
+ * fixed-point range and is reported by the optimizer like a non-finite gradient.  Costs two more L2 atomics per row. */
+SXEN_API sxen_status sxen_grad_set_reproducible(sxen_grad* grad, int32_t on);
+SXEN_API sxen_status sxen_grad_is_reproducible(const sxen_grad* grad, int32_t* out);
+/* the fixed-point words (NULL / 0 when the mode is off): for an all-reduce of type SXEN_ELEM_I64 next to the values */
+SXEN_API sxen_status sxen_grad_fixed_dev(sxen_grad* grad, int64_t** out_dev, size_t* count);
+/* EncoderGradient::slice as the reference's doubles: the exact fixed-point sums in reproducible mode, else the f32 values. */
+SXEN_API sxen_status sxen_grad_download_f64(const sxen_grad* grad, int32_t level, double* values_host);
 /* EncoderGradient::merge (src/encoding.cpp:122-131): dst += src, touched = union. */
 SXEN_API sxen_status sxen_grad_merge(sxen_grad* dst, const sxen_grad* src, void* stream);
 
@@ -279,6 +294,10 @@ SXEN_API sxen_status sxen_mlp_download_params(const sxen_mlp* mlp, float* dst_ho
 SXEN_API sxen_status sxen_mlp_params_dev(sxen_mlp* mlp, float** out_dev);
 SXEN_API sxen_status sxen_mlp_grads_dev(sxen_mlp* mlp, double** out_dev);                  /* MlpGradient::values(), for all-reduce */
 SXEN_API sxen_status sxen_mlp_grad_clear(sxen_mlp* mlp, void* stream);                     /* MlpGradient::clear */
+/* Reproducible MlpGradient (exact head): the thread blocks' partial sums meet in 64-bit fixed point (units of 2^-52,
+ * integer atomics) instead of fp64 atomics, so the gradient does not depend on block scheduling -- the counterpart of the
+ * reference's fixed worker-order merge (src/mlp.cpp:83-88, src/trainer.cpp:125-128). */
+SXEN_API sxen_status sxen_mlp_set_reproducible(sxen_mlp* mlp, int32_t on);
 SXEN_API sxen_status sxen_mlp_grad_download(const sxen_mlp* mlp, double* dst_host);
 /* Mlp::forward, batched (src/mlp.cpp:137-162). input_dev: N x input_width f32; out_dev (may be NULL): N x output_width.
  * The activations stay in the handle (the batched MlpWorkspace) for the matching backward. */
@@ -398,8 +417,13 @@ SXEN_API sxen_status sxen_comm_destroy(sxen_comm* comm);
 SXEN_API sxen_status sxen_comm_abort(sxen_comm* comm);
 /* any of the outputs may be NULL; kind: 0 = NCCL, 1 = LOCAL */
 SXEN_API sxen_status sxen_comm_info(const sxen_comm* comm, int32_t* world, int32_t* rank, int32_t* device, int32_t* kind);
-/* In-place SUM over the ranks of count elements (type: SXEN_COORD_F32 / SXEN_COORD_F64), stream-ordered. */
+/* In-place SUM over the ranks of count elements (type: SXEN_COORD_F32 / SXEN_COORD_F64 / SXEN_ELEM_I64), stream-ordered. */
 SXEN_API sxen_status sxen_comm_allreduce(sxen_comm* comm, void* buf_dev, size_t count, sxen_coord_type type, void* stream);
+
+/* Bit-reproducible training steps (opt-in): sxen_grad_set_reproducible on the trainer's accumulator, sxen_mlp_set_reproducible
+ * on its MLP, and -- with the exact head -- d(loss)/d(encoding) handed to encode_backward as doubles.  Two runs of the same
+ * steps then produce the same bits, on one GPU or sharded (the exchange sums the fixed-point words). */
+SXEN_API sxen_status sxen_trainer_set_reproducible(sxen_trainer* trainer, int32_t on);
 
 /* Attaches a communicator (not owned; NULL detaches) to a trainer.  The trainer's encoder, MLP and the communicator must
  * live on the same device; replicas on all ranks must have been initialised identically (same seeds). */

@@ -158,6 +158,12 @@ SIGNATURES = {
     "sxen_trainer_set_aux": (C.c_int, [_vp, _vp, C.c_int]),
     "sxen_trainer_pending": (C.c_int, [_vp, _P(_sz)]),
     "sxen_trainer_collect": (C.c_int, [_vp, _P(_dbl), _sz, _P(_sz), _P(C.c_int64), _vp]),
+    "sxen_grad_set_reproducible": (C.c_int, [_vp, _i32]),
+    "sxen_grad_is_reproducible": (C.c_int, [_vp, _P(_i32)]),
+    "sxen_grad_fixed_dev": (C.c_int, [_vp, _P(_vp), _P(_sz)]),
+    "sxen_grad_download_f64": (C.c_int, [_vp, _i32, _P(_dbl)]),
+    "sxen_mlp_set_reproducible": (C.c_int, [_vp, _i32]),
+    "sxen_trainer_set_reproducible": (C.c_int, [_vp, _i32]),
     "sxen_comm_unique_id": (C.c_int, [_vp]),
     "sxen_comm_create": (C.c_int, [_vp, _i32, _i32, _i32, _P(_vp)]),
     "sxen_comm_create_local": (C.c_int, [_i32, _P(_i32), _P(_vp)]),

@@ -132,6 +132,11 @@ __global__ void grad_merge_kernel(float* __restrict__ dst, const float* __restri
   }
 }
 
+__global__ void add_i64_kernel(long long* __restrict__ dst, const long long* __restrict__ src, size_t n) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] += src[i];
+}
+
 __global__ void grad_touched_kernel(const float* __restrict__ v, size_t rows, int features,
                                     unsigned long long* __restrict__ out) {
   unsigned long long local = 0;
@@ -242,7 +247,7 @@ sxen_status check_batch(const sxen_encoder* enc, const void* x, sxen_coord_type 
 // row_stride > 0: feature / upstream rows are row_stride floats apart (>= L*F; the trainer's [encoding | aux] rows).
 sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, const float* upstream, size_t n,
                        float* out, sxen_grad* grad, int mode, cudaStream_t stream, int first_level = 0,
-                       int level_count = -1, int row_stride = 0) {
+                       int level_count = -1, int row_stride = 0, const double* upstream64 = nullptr) {
   if (sxen_status st = check_batch(enc, x, type, n)) return st;
   SXEN_REQUIRE(row_stride == 0 || row_stride >= enc->cfg.levels * enc->cfg.features,
                "encode: row stride %d below the encoded width %d", row_stride, enc->cfg.levels * enc->cfg.features);
@@ -271,7 +276,7 @@ sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, c
                                       row_stride))
         return st;
       return run_encode(enc, x, type, upstream, n, nullptr, grad, sxen_dev::kModeBwd, stream, first_level, level_count,
-                        row_stride);
+                        row_stride, upstream64);
     }
   }
   EncodeArgs a;
@@ -280,6 +285,8 @@ sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, c
   a.upstream = upstream;
   a.out = out;
   a.grads = grad ? grad->values : nullptr;
+  a.fixed = (grad && (mode & sxen_dev::kModeBwd)) ? grad->fixed : nullptr;
+  a.upstream64 = a.fixed ? upstream64 : nullptr;
   // Launch shape left to the library (level_major < 0, levels_per_thread == 0), by table footprint B = L*T*F*4 bytes
   // (tables and accumulator are the same size; L2 is 126 MB):
   //   B <= 96 MiB   sample-major, 2 levels per thread: a warp writes whole feature rows, everything stays near L2
@@ -314,6 +321,12 @@ sxen_status run_encode(sxen_encoder* enc, const void* x, sxen_coord_type type, c
                        enc->cfg.features == 2 && table_bytes > (48ull << 20) && level_count >= 16)
                           ? 8 : 0;
   ln.exact = enc->tuning.exact_blend ? 1 : 0;
+  ln.repro = a.fixed != nullptr ? 1 : 0;
+  if (ln.repro) {  // the reproducible kernels exist sample-major with one or two levels per thread
+    a.level_major = 0;
+    ln.lpt = std::min(ln.lpt, 2);
+    ln.chunk_levels = 0;
+  }
   ln.grid_backend = enc->cfg.backend == SXEN_BACKEND_GRID ? 1 : 0;
   ln.block_threads = enc->tuning.block_threads;
   const int level_end = first_level + level_count;
@@ -404,6 +417,15 @@ sxen_status sxen_encoder_encode_backward_strided(sxen_encoder* enc, const void* 
                     first_level, level_count, row_stride);
 }
 
+sxen_status sxen_encoder_encode_backward_strided64(sxen_encoder* enc, const void* x_dev, sxen_coord_type type,
+                                                   const float* upstream_dev, const double* upstream64_dev, int row_stride,
+                                                   size_t n_samples, sxen_grad* grad, int first_level, int level_count,
+                                                   void* stream) {
+  SXEN_REQUIRE(enc != nullptr, "encoder handle is null");
+  return run_encode(enc, x_dev, type, upstream_dev, n_samples, nullptr, grad, sxen_dev::kModeBwd, as_stream(stream),
+                    first_level, level_count, row_stride, upstream64_dev);
+}
+
 // SparseAdamState::step for the single-GPU trainer (declared in sxen_common.hpp): when the batch is small against the
 // tables, the update walks the batch (sparse_adam_walk_kernel) instead of scanning all L*T accumulator rows.  The caller
 // guarantees that every touched row of `grad` comes from this batch's backward.  Same arithmetic, same rows, same
@@ -435,6 +457,7 @@ sxen_status sxen_sparse_adam_step_walk(sxen_sparse_adam* opt, sxen_encoder* enc,
   o.c = sxen_adam_scalars(*cfg, opt->t);
   o.status = opt->status;
   o.gate = gate_dev;
+  o.fixed = reinterpret_cast<longlong2*>(grad->fixed);
   EncodeArgs a;
   base_args(enc, x_dev, type, n_samples, a);
   for (int level0 = 0; level0 < enc->cfg.levels; level0 += sxen_dev::kMaxLaunchLevels) {
@@ -985,6 +1008,7 @@ sxen_status sxen_grad_destroy(sxen_grad* grad) {
   DeviceGuard guard(grad->device);
   cudaFree(grad->values);
   cudaFree(grad->coarse);
+  cudaFree(grad->fixed);
   delete grad;
   return SXEN_OK;
 }
@@ -996,6 +1020,36 @@ sxen_status sxen_grad_clear(sxen_grad* grad, void* stream) {
                                                                           grad->count(), kUntouchedBits);
   SXEN_CUDA(cudaGetLastError());
   count_launch();
+  if (grad->fixed) SXEN_CUDA(cudaMemsetAsync(grad->fixed, 0, grad->count() * sizeof(long long), as_stream(stream)));
+  return SXEN_OK;
+}
+
+sxen_status sxen_grad_set_reproducible(sxen_grad* grad, int32_t on) {
+  SXEN_REQUIRE(grad != nullptr, "gradient handle is null");
+  DeviceGuard guard(grad->device);
+  if (on && !grad->fixed) {
+    SXEN_CUDA(cudaMalloc(&grad->fixed, grad->count() * sizeof(long long)));
+    SXEN_CUDA(cudaDeviceSynchronize());
+    return sxen_grad_clear(grad, nullptr);  // both representations start from the same (empty) state
+  }
+  if (!on && grad->fixed) {
+    SXEN_CUDA(cudaDeviceSynchronize());
+    cudaFree(grad->fixed);
+    grad->fixed = nullptr;
+  }
+  return SXEN_OK;
+}
+
+sxen_status sxen_grad_is_reproducible(const sxen_grad* grad, int32_t* out) {
+  SXEN_REQUIRE(grad != nullptr && out != nullptr, "null argument");
+  *out = grad->fixed != nullptr ? 1 : 0;
+  return SXEN_OK;
+}
+
+sxen_status sxen_grad_fixed_dev(sxen_grad* grad, int64_t** out_dev, size_t* count) {
+  SXEN_REQUIRE(grad != nullptr && out_dev != nullptr, "null argument");
+  *out_dev = reinterpret_cast<int64_t*>(grad->fixed);
+  if (count) *count = grad->fixed ? grad->count() : 0;
   return SXEN_OK;
 }
 
@@ -1021,6 +1075,28 @@ sxen_status sxen_grad_download(const sxen_grad* grad, int32_t level, float* valu
     if (untouched)
       for (int f = 0; f < grad->features; ++f) values_host[r * grad->features + f] = 0.0f;
   }
+  if (grad->fixed) {  // reproducible mode: report the exact sums (rounded once to float), not the fp32-atomic ones
+    std::vector<long long> q(per);
+    SXEN_CUDA(cudaMemcpy(q.data(), grad->fixed + static_cast<size_t>(level) * per, per * sizeof(long long), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < per; ++i) values_host[i] = static_cast<float>(static_cast<double>(q[i]) * 0x1p-52);
+  }
+  return SXEN_OK;
+}
+
+sxen_status sxen_grad_download_f64(const sxen_grad* grad, int32_t level, double* values_host) {
+  SXEN_REQUIRE(grad != nullptr && values_host != nullptr, "null argument");
+  SXEN_REQUIRE(level >= 0 && level < grad->levels, "gradient: level out of range");
+  DeviceGuard guard(grad->device);
+  const size_t per = static_cast<size_t>(grad->table_size) * static_cast<size_t>(grad->features);
+  if (grad->fixed) {
+    std::vector<long long> q(per);
+    SXEN_CUDA(cudaMemcpy(q.data(), grad->fixed + static_cast<size_t>(level) * per, per * sizeof(long long), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < per; ++i) values_host[i] = static_cast<double>(q[i]) * 0x1p-52;  // exact: |q| < 2^53 in range
+    return SXEN_OK;
+  }
+  std::vector<float> v(per);
+  if (sxen_status st = sxen_grad_download(grad, level, v.data(), nullptr)) return st;
+  for (size_t i = 0; i < per; ++i) values_host[i] = static_cast<double>(v[i]);
   return SXEN_OK;
 }
 
@@ -1039,6 +1115,12 @@ sxen_status sxen_grad_upload(sxen_grad* grad, int32_t level, const float* values
   }
   SXEN_CUDA(cudaMemcpy(grad->values + static_cast<size_t>(level) * per, tmp.data(), per * sizeof(float),
                        cudaMemcpyHostToDevice));
+  if (grad->fixed) {
+    std::vector<long long> q(per);
+    for (size_t i = 0; i < per; ++i)
+      q[i] = touched_host[i / grad->features] ? std::llrint(static_cast<double>(values_host[i]) * 0x1p52) : 0;
+    SXEN_CUDA(cudaMemcpy(grad->fixed + static_cast<size_t>(level) * per, q.data(), per * sizeof(long long), cudaMemcpyHostToDevice));
+  }
   return SXEN_OK;
 }
 
@@ -1067,9 +1149,15 @@ sxen_status sxen_grad_merge(sxen_grad* dst, const sxen_grad* src, void* stream) 
                "EncoderGradient::merge: shape mismatch");
   DeviceGuard guard(dst->device);
   const size_t rows = static_cast<size_t>(dst->levels) * dst->table_size;
+  SXEN_REQUIRE((dst->fixed != nullptr) == (src->fixed != nullptr), "EncoderGradient::merge: one accumulator is in reproducible mode, the other is not");
   grad_merge_kernel<<<grid_for(rows), 256, 0, as_stream(stream)>>>(dst->values, src->values, rows, dst->features);
   SXEN_CUDA(cudaGetLastError());
   count_launch();
+  if (dst->fixed) {
+    add_i64_kernel<<<grid_for(dst->count()), 256, 0, as_stream(stream)>>>(dst->fixed, src->fixed, dst->count());
+    SXEN_CUDA(cudaGetLastError());
+    count_launch();
+  }
   return SXEN_OK;
 }
 

@@ -33,6 +33,7 @@ struct AdamWalkArgs {
   AdamScalars c;
   unsigned long long* status;        // first non-finite gradient element (TrainingError)
   const unsigned long long* gate;    // queued steps: non-~0 = skip
+  longlong2* fixed;                  // reproducible mode: fixed-point sums (units of 2^-52), nullptr = off
 };
 
 }  // namespace sxen_dev

@@ -342,7 +342,8 @@ sxen_status sxen_comm_info(const sxen_comm* c, int32_t* world, int32_t* rank, in
 
 sxen_status sxen_comm_allreduce(sxen_comm* c, void* buf_dev, size_t count, sxen_coord_type type, void* stream) {
   SXEN_REQUIRE(c != nullptr, "comm handle is null");
-  SXEN_REQUIRE(type == SXEN_COORD_F32 || type == SXEN_COORD_F64, "all-reduce: unknown element type %d", static_cast<int>(type));
+  SXEN_REQUIRE(type == SXEN_COORD_F32 || type == SXEN_COORD_F64 || type == SXEN_ELEM_I64, "all-reduce: unknown element type %d",
+               static_cast<int>(type));
   SXEN_REQUIRE(count == 0 || buf_dev != nullptr, "all-reduce: buffer is null");
   if (c->world == 1 && c->kind == 1) return SXEN_OK;
   DeviceGuard guard(c->device);
@@ -350,10 +351,12 @@ sxen_status sxen_comm_allreduce(sxen_comm* c, void* buf_dev, size_t count, sxen_
     if (count == 0) return SXEN_OK;
     if (c->nccl == nullptr) return fail(SXEN_NCCL_ERROR, "all-reduce: the communicator was aborted");
     NcclApi& api = nccl_api();
-    SXEN_NCCL(api.AllReduce(buf_dev, buf_dev, count, type == SXEN_COORD_F32 ? ncclFloat32 : ncclFloat64, ncclSum, c->nccl,
-                            as_stream(stream)));
+    SXEN_NCCL(api.AllReduce(buf_dev, buf_dev, count,
+                            type == SXEN_COORD_F32 ? ncclFloat32 : type == SXEN_COORD_F64 ? ncclFloat64 : ncclInt64, ncclSum,
+                            c->nccl, as_stream(stream)));
     return SXEN_OK;
   }
+  if (type == SXEN_ELEM_I64) return local_allreduce<long long>(c, buf_dev, count, 2, as_stream(stream));
   return type == SXEN_COORD_F32 ? local_allreduce<float>(c, buf_dev, count, 1, as_stream(stream))
                                 : local_allreduce<double>(c, buf_dev, count, 0, as_stream(stream));
 }

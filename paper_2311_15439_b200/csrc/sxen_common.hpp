@@ -80,6 +80,7 @@ struct sxen_grad {
   int levels = 0, features = 0;
   uint32_t table_size = 0;
   float* values = nullptr;  // L x T x F, untouched rows carry -0.0f in feature 0
+  long long* fixed = nullptr;  // reproducible mode (sxen_grad_set_reproducible): the same sums in 64-bit fixed point, units of 2^-52
   // Coarse simplex levels (few lattice vertices, every sample's atomics land on them) accumulate into 2^shift dense
   // replicas [replica][vertex][F] that the backward launch folds into `values` before it returns (sxen_encode.cuh).
   float* coarse = nullptr;
@@ -133,3 +134,13 @@ sxen_status sxen_encoder_encode_strided(sxen_encoder* enc, const void* x_dev, sx
 sxen_status sxen_encoder_encode_backward_strided(sxen_encoder* enc, const void* x_dev, sxen_coord_type type,
                                                  const float* upstream_dev, int row_stride, size_t n_samples,
                                                  sxen_grad* grad, int first_level, int level_count, void* stream);
+
+// sxen_mlp_forward_backward with d(loss)/d(input) also as doubles (exact head; NULL = not wanted), sxen_mlp.cu
+extern "C" sxen_status sxen_mlp_forward_backward_ex(sxen_mlp* mlp, const float* input_dev, const void* targets_dev,
+                                         sxen_coord_type target_type, size_t n_samples, size_t global_batch, float* pred_dev,
+                                         float* input_grad_dev, double* input_grad_f64_dev, double* loss_sum_dev, void* stream);
+// encode_backward with the upstream ALSO as doubles (reproducible mode: the fixed-point sums take the fp64 product)
+sxen_status sxen_encoder_encode_backward_strided64(sxen_encoder* enc, const void* x_dev, sxen_coord_type type,
+                                                   const float* upstream_dev, const double* upstream64_dev, int row_stride,
+                                                   size_t n_samples, sxen_grad* grad, int first_level, int level_count,
+                                                   void* stream);

@@ -43,6 +43,8 @@ struct EncodeArgs {
   int32_t merge_pairs;           // F == 2: one red.v4 for two chain vertices in the same 16-byte slot
   int32_t cache_hints;           // F == 2: gather L2 policy + 4 * red L2 policy (0 none, 1 evict_last, 2 evict_first, 3 evict_unchanged)
   double skew;                   // F_n
+  long long* fixed;              // reproducible mode: 64-bit fixed-point accumulator, same layout as grads (nullptr = off)
+  const double* upstream64;      // reproducible mode: upstream as the reference's doubles (nullptr: widen `upstream`)
   float* coarse;                 // replicated dense accumulators of the coarse levels (nullptr = none)
   LevelGeom geom;
   CoarseGeom cg;                 // geometry of `coarse`
@@ -88,7 +90,18 @@ __device__ __forceinline__ bool load_coords(const EncodeArgs& a, unsigned long l
   return ok;
 }
 
-template <int ND, int F, int LPT, int MODE, bool EXACT, bool GRID = false>
+// REPRO (backward / both): besides the fp32 atomics every contribution is ALSO added as 64-bit fixed point (units of
+// 2^-52) with red.global.add.u64 -- integer addition is associative, so the sums do not depend on the order the atomics
+// land in and a training run is bit-reproducible, like the reference's fixed worker-order merge (src/trainer.cpp:125-128,
+// tests/test_neural.cpp:370-408).  The product w * upstream is taken in fp64 as the reference does (src/encoding.cpp:116);
+// the fp32 accumulator keeps carrying the touched marker, the NaN / range check and an approximate value.
+constexpr double kFixedScale = 0x1p52, kFixedUnit = 0x1p-52;
+__device__ __forceinline__ void red_add_fixed(long long* p, double v) {
+  const long long q = __double2ll_rn(__dmul_rn(v, kFixedScale));
+  asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(q) : "memory");
+}
+
+template <int ND, int F, int LPT, int MODE, bool EXACT, bool GRID = false, bool REPRO = false>
 __global__ void __launch_bounds__((LPT >= 4 || GRID) ? 256 : 512)
 encode_kernel(const __grid_constant__ EncodeArgs a) {
   constexpr int V = GRID ? (1 << ND) : (ND + 1);  // vertices per (sample, level): gather_grid / gather_simplex
@@ -149,6 +162,7 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
 
   float upv[K];
   float outv[K];
+  double upd[REPRO ? K : 1];
   const int gather_kind = a.cache_hints & 3, red_kind = (a.cache_hints >> 2) & 3;
   const uint64_t gather_pol = l2_policy(gather_kind), red_pol = l2_policy(red_kind);
   if constexpr (kBwd) {
@@ -157,6 +171,12 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
     } else {
 #pragma unroll
       for (int q = 0; q < K; ++q) upv[q] = (l_begin + q / F < a.n_levels) ? __ldcs(a.upstream + chunk + q) : 0.0f;
+    }
+    if constexpr (REPRO) {
+#pragma unroll
+      for (int q = 0; q < K; ++q)
+        upd[q] = (a.upstream64 != nullptr && l_begin + q / F < a.n_levels) ? __ldcs(a.upstream64 + chunk + q)
+                                                                           : static_cast<double>(upv[q]);
     }
   }
 
@@ -240,6 +260,15 @@ encode_kernel(const __grid_constant__ EncodeArgs a) {
         // address (profiles/r1_per_level_n*.log: level 0 costs 4-12x a fine level).  Such levels accumulate into one of
         // 2^shift dense replicas picked by the sample index (rows = dense lattice positions instead of hashed rows);
         // coarse_fold_kernel adds the replicas into the hashed rows right after this launch.
+        if constexpr (REPRO) {
+          // exact sums next to the fp32 ones, straight into the hashed rows (before idx[] is redirected to a replica)
+          long long* fl = a.fixed + level_off;
+#pragma unroll
+          for (int k = 0; k < V; ++k) {
+#pragma unroll
+            for (int f = 0; f < F; ++f) red_add_fixed(fl + static_cast<size_t>(idx[k]) * F + f, __dmul_rn(w[k], upd[j * F + f]));
+          }
+        }
         const int cshift = s_cshift[l];
         if (cshift >= 0) {
           const uint32_t rep = static_cast<uint32_t>(s) & ((1u << cshift) - 1u);
@@ -333,7 +362,11 @@ __global__ void __launch_bounds__(256) encode_generic_kernel(const __grid_consta
     for (int f = 0; f < F; ++f) {
       double acc = 0.0;
       float up = 0.0f;
-      if constexpr (kBwd) up = __ldg(a.upstream + chunk + f);
+      double upd = 0.0;
+      if constexpr (kBwd) {
+        up = __ldg(a.upstream + chunk + f);
+        upd = a.upstream64 != nullptr ? __ldg(a.upstream64 + chunk + f) : static_cast<double>(up);
+      }
 #pragma unroll 1
       for (int m = 0; m < (1 << ND); ++m) {
         uint32_t idx;
@@ -341,7 +374,10 @@ __global__ void __launch_bounds__(256) encode_generic_kernel(const __grid_consta
         grid_corner<ND>(cell, m, a.mask, idx, w);
         if constexpr (kFwd)
           acc = __dadd_rn(acc, __dmul_rn(w, static_cast<double>(__ldg(tab + static_cast<size_t>(idx) * F + f))));
-        if constexpr (kBwd) red_add(gl + static_cast<size_t>(idx) * F + f, canon(__fmul_rn(static_cast<float>(w), up)));
+        if constexpr (kBwd) {
+          red_add(gl + static_cast<size_t>(idx) * F + f, canon(__fmul_rn(static_cast<float>(w), up)));
+          if (a.fixed != nullptr) red_add_fixed(a.fixed + level_off + static_cast<size_t>(idx) * F + f, __dmul_rn(w, upd));
+        }
       }
       if constexpr (kFwd) a.out[chunk + f] = static_cast<float>(acc);
     }
@@ -362,6 +398,12 @@ __global__ void __launch_bounds__(256) encode_generic_kernel(const __grid_consta
 #pragma unroll
         for (int k = 0; k <= ND; ++k)
           red_add(gl + static_cast<size_t>(idx[k]) * F + f, canon(__fmul_rn(static_cast<float>(w[k]), up)));
+        if (a.fixed != nullptr) {
+          const double upd = a.upstream64 != nullptr ? __ldg(a.upstream64 + chunk + f) : static_cast<double>(up);
+#pragma unroll
+          for (int k = 0; k <= ND; ++k)
+            red_add_fixed(a.fixed + level_off + static_cast<size_t>(idx[k]) * F + f, __dmul_rn(w[k], upd));
+        }
       }
     }
   }
@@ -435,9 +477,17 @@ sparse_adam_walk_kernel(const __grid_constant__ EncodeArgs a, const __grid_const
     const unsigned long long got = atomicExch(reinterpret_cast<unsigned long long*>(o.grads + r), kUntouchedRow);
     const uint32_t gx_bits = static_cast<uint32_t>(got), gy_bits = static_cast<uint32_t>(got >> 32);
     if (gx_bits == kUntouchedBits) return;  // untouched, or already claimed by another thread
-    const double gx = static_cast<double>(__uint_as_float(gx_bits)), gy = static_cast<double>(__uint_as_float(gy_bits));
-    if (!isfinite(gx) || !isfinite(gy)) {
-      atomicMin(o.status, static_cast<unsigned long long>(2 * r + (isfinite(gx) ? 1 : 0)));  // src/optimizer.cpp:73-76
+    double gx = static_cast<double>(__uint_as_float(gx_bits)), gy = static_cast<double>(__uint_as_float(gy_bits));
+    const bool repro = o.fixed != nullptr;
+    const bool okx = isfinite(gx) && (!repro || fabs(gx) < 1024.0), oky = isfinite(gy) && (!repro || fabs(gy) < 1024.0);
+    if (repro) {  // the row is this thread's now: take the order-free sums and re-arm them
+      const longlong2 q = o.fixed[r];
+      o.fixed[r] = make_longlong2(0, 0);
+      gx = __dmul_rn(static_cast<double>(q.x), kFixedUnit);
+      gy = __dmul_rn(static_cast<double>(q.y), kFixedUnit);
+    }
+    if (!okx || !oky) {
+      atomicMin(o.status, static_cast<unsigned long long>(2 * r + (okx ? 1 : 0)));  // src/optimizer.cpp:73-76
       return;
     }
     double2 mm = o.m[r], vv = o.v[r];
@@ -524,6 +574,7 @@ __global__ void __launch_bounds__(256) coarse_fold_kernel(const __grid_constant_
 // ---- host-side launch plumbing, one translation unit per ND (sxen_encode_nd.cu) -----------------------------
 
 struct EncodeLaunch {
+  int repro;            // reproducible mode (EncodeArgs::fixed != nullptr): the REPRO instantiation, F == 2, LPT <= 2
   int chunk_levels;     // sample-major launches: levels per blockIdx.y slice (0 = one slice); used when it is LPT * 2^k
   int features;         // F, any
   int lpt;              // requested levels per thread

@@ -11,7 +11,7 @@ namespace {
 
 constexpr int ND = SXEN_ND;
 
-template <int F, int LPT, int MODE, bool EXACT, bool GRID = false>
+template <int F, int LPT, int MODE, bool EXACT, bool GRID = false, bool REPRO = false>
 cudaError_t go(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t stream) {
   a.groups = (a.n_levels + LPT - 1) / LPT;
   a.groups_shift = -1;
@@ -43,7 +43,7 @@ cudaError_t go(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t stream) {
     const unsigned long long threads = a.n_samples * static_cast<unsigned long long>(a.span_groups);
     grid = dim3(static_cast<unsigned>((threads + block - 1) / block), static_cast<unsigned>(slices), 1);
   }
-  encode_kernel<ND, F, LPT, MODE, EXACT, GRID><<<grid, block, 0, stream>>>(a);
+  encode_kernel<ND, F, LPT, MODE, EXACT, GRID, REPRO><<<grid, block, 0, stream>>>(a);
   return cudaGetLastError();
 }
 
@@ -73,9 +73,22 @@ cudaError_t generic_by_mode(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t 
   }
 }
 
+// Reproducible mode (sxen_grad_set_reproducible): fixed-point sums next to the fp32 atomics; F == 2, both backends at
+// ND <= 3 for the grid (the tuned kernel), exact blend, one or two levels per thread.
+template <bool GRID>
+cudaError_t launch_f2_repro(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t stream, int* used) {
+  if (ln.lpt >= 2) {
+    *used = 2;
+    return ln.mode == kModeBwd ? go<2, 2, kModeBwd, true, GRID, true>(ln, a, stream) : go<2, 2, kModeBoth, true, GRID, true>(ln, a, stream);
+  }
+  *used = 1;
+  return ln.mode == kModeBwd ? go<2, 1, kModeBwd, true, GRID, true>(ln, a, stream) : go<2, 1, kModeBoth, true, GRID, true>(ln, a, stream);
+}
+
 // F == 2 is the configuration every BASELINE workload uses: full tuning surface.
 cudaError_t launch_f2(const EncodeLaunch& ln, EncodeArgs& a, cudaStream_t stream, int* used) {
   int lpt = ln.lpt;
+  if (ln.repro && (ln.mode & kModeBwd)) return launch_f2_repro<false>(ln, a, stream, used);
 #if SXEN_ND == 2 || SXEN_ND == 3
   if (lpt >= 16) {
     *used = 16;
@@ -116,6 +129,7 @@ cudaError_t SXEN_CAT(launch_encode_nd, SXEN_ND)(const EncodeLaunch& ln, EncodeAr
 #if SXEN_ND == 2 || SXEN_ND == 3
     // the paper's comparator in its 2D / 3D settings: same tuned kernel, 2^ND corners instead of ND+1 vertices
     if (ln.features == 2) {
+      if (ln.repro && (ln.mode & kModeBwd)) return launch_f2_repro<true>(ln, a, stream, used_lpt);
       if (ln.lpt >= 2) {
         *used_lpt = 2;
         return ln.exact ? by_mode<2, 2, true, true>(ln, a, stream) : by_mode<2, 2, false, true>(ln, a, stream);
@@ -126,6 +140,10 @@ cudaError_t SXEN_CAT(launch_encode_nd, SXEN_ND)(const EncodeLaunch& ln, EncodeAr
 #endif
     *used_lpt = 1;
     return generic_by_mode<true>(ln, a, stream);
+  }
+  if (ln.repro && (ln.mode & kModeBwd) && ln.features != 2) {  // fixed-point sums for the other widths: the general kernel
+    *used_lpt = 1;
+    return generic_by_mode<false>(ln, a, stream);
   }
   switch (ln.features) {
     case 2: return launch_f2(ln, a, stream, used_lpt);

@@ -26,6 +26,9 @@ struct sxen_mlp {
   bool forward_done = false;
   int precision = SXEN_MLP_EXACT;  // sxen_mlp_precision
   double* loss_scratch = nullptr;  // 1 double, used when the caller does not want the loss
+  // reproducible mode (sxen_mlp_set_reproducible): the blocks' partial parameter gradients meet in 64-bit fixed point
+  // (units of 2^-52, integer atomics: order-free) and are folded into `grads` once per backward
+  long long* grads_fixed = nullptr;
   int layer_count() const { return cfg.hidden_layers + 1; }
   int layer_in(int l) const { return l == 0 ? cfg.input_width : cfg.hidden_width; }
   int layer_out(int l) const { return l == layer_count() - 1 ? cfg.output_width : cfg.hidden_width; }
@@ -40,7 +43,8 @@ struct sxen_mlp {
 bool sxen_mlp_tc_supported(const sxen_mlp_config& c);
 sxen_status sxen_mlp_tc_run(bool train, const float* params, const float* features, const void* targets, int target_f32,
                             float* pred, float* input_grad, double* mlp_grad, double* loss_sum, size_t n, int in_w, int out_w,
-                            size_t global_batch, int precise, cudaStream_t stream);
+                            size_t global_batch, int precise, cudaStream_t stream, long long* grad_fixed = nullptr,
+                            int* used_ctas = nullptr);
 
 namespace {
 
@@ -175,10 +179,30 @@ __global__ void gather_cols_kernel(const float* __restrict__ src, unsigned long 
 // delta_in / delta_out: [N x width] doubles (ping-pong scratch).
 constexpr int kTile = 32;
 
+// reproducible mode: a block's partial sum as 64-bit fixed point, units of 2^-52 (a non-finite sum becomes the most negative
+// value, which poisons the total visibly: fold_fixed_kernel turns |total| >= 2^62 into NaN for Adam's check)
+__device__ __forceinline__ unsigned long long to_fixed(double v) {
+  return static_cast<unsigned long long>(__double2ll_rn(__dmul_rn(v, 0x1p52)));
+}
+// the tensor-core head's per-CTA loss partials, added to the running sum in CTA order (one thread: <= 148 terms)
+__global__ void sum_parts_kernel(double* __restrict__ acc, const double* __restrict__ parts, int n) {
+  double s = *acc;
+  for (int i = 0; i < n; ++i) s = __dadd_rn(s, parts[i]);
+  *acc = s;
+}
+__global__ void fold_fixed_kernel(double* __restrict__ grads, long long* __restrict__ fixed, unsigned long long n) {
+  const unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long q = fixed[i];
+  fixed[i] = 0;
+  const bool sane = q > -(1LL << 62) && q < (1LL << 62);
+  grads[i] = __dadd_rn(grads[i], sane ? __dmul_rn(static_cast<double>(q), 0x1p-52) : __longlong_as_double(0x7ff8000000000000LL));
+}
+
 __global__ void __launch_bounds__(256)
 mlp_backward_layer_kernel(const float* __restrict__ params, const float* __restrict__ acts, double* __restrict__ grads,
                           const double* __restrict__ delta_cur, double* __restrict__ delta_next,
-                          unsigned long long n_samples, MlpShape s, int layer) {
+                          unsigned long long n_samples, MlpShape s, int layer, long long* __restrict__ fixed) {
   extern __shared__ double smem[];
   const int in = s.in_w[layer], ow = s.out_w[layer];
   double* d_tile = smem;                                    // [kTile][ow]
@@ -199,11 +223,13 @@ mlp_backward_layer_kernel(const float* __restrict__ params, const float* __restr
       const int o = p / in, i = p - o * in;
       for (int r = 0; r < rows; ++r)
         acc = __dadd_rn(acc, __dmul_rn(d_tile[r * ow + o], static_cast<double>(src_tile[r * in + i])));
-      atomicAdd(grads + s.w_off[layer] + p, acc);
+      if (fixed) atomicAdd(reinterpret_cast<unsigned long long*>(fixed + s.w_off[layer] + p), to_fixed(acc));
+      else atomicAdd(grads + s.w_off[layer] + p, acc);
     } else {
       const int o = p - ow * in;
       for (int r = 0; r < rows; ++r) acc = __dadd_rn(acc, d_tile[r * ow + o]);
-      atomicAdd(grads + s.b_off[layer] + o, acc);
+      if (fixed) atomicAdd(reinterpret_cast<unsigned long long*>(fixed + s.b_off[layer] + o), to_fixed(acc));
+      else atomicAdd(grads + s.b_off[layer] + o, acc);
     }
   }
   // downstream deltas: thread per (sample, input unit), o in order
@@ -323,6 +349,7 @@ sxen_status sxen_mlp_destroy(sxen_mlp* mlp) {
   cudaFree(mlp->grads);
   cudaFree(mlp->acts);
   cudaFree(mlp->loss_scratch);
+  cudaFree(mlp->grads_fixed);
   delete mlp;
   return SXEN_OK;
 }
@@ -410,6 +437,15 @@ sxen_status sxen_mlp_get_precision(const sxen_mlp* mlp, int32_t* out) {
 sxen_status sxen_mlp_forward_backward(sxen_mlp* mlp, const float* input_dev, const void* targets_dev,
                                       sxen_coord_type target_type, size_t n_samples, size_t global_batch, float* pred_dev,
                                       float* input_grad_dev, double* loss_sum_dev, void* stream) {
+  return sxen_mlp_forward_backward_ex(mlp, input_dev, targets_dev, target_type, n_samples, global_batch, pred_dev,
+                                      input_grad_dev, nullptr, loss_sum_dev, stream);
+}
+
+// + input_grad_f64_dev (may be NULL): d(loss)/d(input) as the reference's doubles (exact head only; the tensor-core head
+// leaves it untouched and returns 0 in *wrote_f64 -- internal, declared in sxen_common.hpp)
+sxen_status sxen_mlp_forward_backward_ex(sxen_mlp* mlp, const float* input_dev, const void* targets_dev,
+                                         sxen_coord_type target_type, size_t n_samples, size_t global_batch, float* pred_dev,
+                                         float* input_grad_dev, double* input_grad_f64_dev, double* loss_sum_dev, void* stream) {
   SXEN_REQUIRE(mlp != nullptr, "mlp handle is null");
   SXEN_REQUIRE(n_samples == 0 || (input_dev && targets_dev && input_grad_dev), "mlp forward_backward: null pointer");
   SXEN_REQUIRE(global_batch >= 1, "mlp forward_backward: global batch must be >= 1");
@@ -420,9 +456,18 @@ sxen_status sxen_mlp_forward_backward(sxen_mlp* mlp, const float* input_dev, con
   if (mlp->precision != SXEN_MLP_EXACT) {
     double* loss = loss_sum_dev ? loss_sum_dev : mlp->loss_scratch;
     mlp->forward_done = false;  // no activations are kept: a separate backward would be a logic error
-    return sxen_mlp_tc_run(true, mlp->params, input_dev, targets_dev, target_type == SXEN_COORD_F32 ? 1 : 0, pred_dev,
-                           input_grad_dev, mlp->grads, loss, n_samples, mlp->cfg.input_width, mlp->cfg.output_width, global_batch,
-                           mlp->precision == SXEN_MLP_TENSOR_BF16X3 ? 1 : 0, st);
+    int ctas = 0;
+    if (sxen_status s = sxen_mlp_tc_run(true, mlp->params, input_dev, targets_dev, target_type == SXEN_COORD_F32 ? 1 : 0, pred_dev,
+                                        input_grad_dev, mlp->grads, loss, n_samples, mlp->cfg.input_width, mlp->cfg.output_width,
+                                        global_batch, mlp->precision == SXEN_MLP_TENSOR_BF16X3 ? 1 : 0, st, mlp->grads_fixed, &ctas))
+      return s;
+    if (mlp->grads_fixed) {  // the CTAs' partial sums met in fixed point (order-free): fold them into the fp64 buffers
+      fold_fixed_kernel<<<grid_for(mlp->param_count), 256, 0, st>>>(mlp->grads, mlp->grads_fixed, mlp->param_count);
+      sum_parts_kernel<<<1, 1, 0, st>>>(loss, reinterpret_cast<const double*>(mlp->grads_fixed + mlp->param_count), ctas);
+      SXEN_CUDA(cudaGetLastError());
+      count_launch(2);
+    }
+    return SXEN_OK;
   }
   if (sxen_status s = sxen_mlp_forward(mlp, input_dev, n_samples, pred_dev, stream)) return s;
   const MlpShape sh = shape_of(mlp);
@@ -438,7 +483,7 @@ sxen_status sxen_mlp_forward_backward(sxen_mlp* mlp, const float* input_dev, con
     add_scalar_kernel<<<1, 1, 0, st>>>(loss_sum_dev, batch_sum);
     count_launch();
   }
-  if (s == SXEN_OK) s = sxen_mlp_backward(mlp, upstream, n_samples, input_grad_dev, nullptr, stream);
+  if (s == SXEN_OK) s = sxen_mlp_backward(mlp, upstream, n_samples, input_grad_dev, input_grad_f64_dev, stream);
   cudaFreeAsync(scratch, st);
   return s;
 }
@@ -521,7 +566,7 @@ sxen_status sxen_mlp_backward(sxen_mlp* mlp, const double* upstream_dev, size_t 
       SXEN_CUDA(cudaFuncSetAttribute(mlp_backward_layer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     double* dst = (l == 0 && input_grad_f64_dev) ? input_grad_f64_dev : nxt;
     mlp_backward_layer_kernel<<<static_cast<unsigned>((n_samples + kTile - 1) / kTile), 256, smem, st>>>(
-        mlp->params, mlp->acts, mlp->grads, cur, dst, n_samples, s, l);
+        mlp->params, mlp->acts, mlp->grads, cur, dst, n_samples, s, l, mlp->grads_fixed);
     SXEN_CUDA(cudaGetLastError());
     count_launch();
     if (l == 0 && input_grad_dev) {
@@ -531,7 +576,27 @@ sxen_status sxen_mlp_backward(sxen_mlp* mlp, const double* upstream_dev, size_t 
     }
     std::swap(cur, nxt);
   }
+  if (mlp->grads_fixed) {
+    fold_fixed_kernel<<<grid_for(mlp->param_count), 256, 0, st>>>(mlp->grads, mlp->grads_fixed, mlp->param_count);
+    SXEN_CUDA(cudaGetLastError());
+    count_launch();
+  }
   SXEN_CUDA(cudaFreeAsync(scratch, st));
+  return SXEN_OK;
+}
+
+sxen_status sxen_mlp_set_reproducible(sxen_mlp* mlp, int32_t on) {
+  SXEN_REQUIRE(mlp != nullptr, "mlp handle is null");
+  DeviceGuard guard(mlp->device);
+  if (on && !mlp->grads_fixed) {
+    // + one double per CTA of the tensor-core head for its loss partial (persistent kernel: at most one CTA per SM)
+    SXEN_CUDA(cudaMalloc(&mlp->grads_fixed, (mlp->param_count + 1024) * sizeof(long long)));
+    SXEN_CUDA(cudaMemset(mlp->grads_fixed, 0, (mlp->param_count + 1024) * sizeof(long long)));
+  } else if (!on && mlp->grads_fixed) {
+    SXEN_CUDA(cudaDeviceSynchronize());
+    cudaFree(mlp->grads_fixed);
+    mlp->grads_fixed = nullptr;
+  }
   return SXEN_OK;
 }
 

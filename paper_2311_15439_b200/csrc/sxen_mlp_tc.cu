@@ -65,6 +65,7 @@ struct TcArgs {
   float* input_grad;        // N x 32 (training)
   double* mlp_grad;         // parameter layout, accumulated into
   double* loss_sum;         // accumulated into
+  long long* grad_fixed;    // reproducible mode: parameter layout in units of 2^-52, then one double per CTA for the loss (nullptr = off)
   unsigned long long n;
   int out_w;
   int target_f32;
@@ -119,6 +120,15 @@ __device__ __forceinline__ void gemm_split(uint32_t d, uint32_t idesc, int kstep
       mma_bf16(d, ah + (a_lo >> 4), bh, idesc, true);
     }
   }
+}
+
+// One CTA's partial sum into the batch total: an fp64 atomic, or -- reproducible mode -- an integer atomic on the fixed-point
+// shadow of the same element (order-free; sxen_mlp.cu folds the shadow into the fp64 buffer after the kernel).
+__device__ __forceinline__ void add_total(double* base, long long* fixed, size_t index, double v) {
+  if (fixed != nullptr)
+    atomicAdd(reinterpret_cast<unsigned long long*>(fixed + index), static_cast<unsigned long long>(__double2ll_rn(__dmul_rn(v, 0x1p52))));
+  else
+    atomicAdd(base + index, v);
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -504,11 +514,9 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
       tc_fence_after();
       const int lane = tid & 31;
       const int row = 16 * (warp & 3) + lane;  // output unit o (G0, G1) or hidden unit i (G2)
-      double* gW0 = a.mlp_grad;
-      double* gb0 = gW0 + HID * IN;
-      double* gW1 = gb0 + HID;
-      double* gb1 = gW1 + HID * HID;
-      double* gW2 = gb1 + HID;
+      constexpr size_t gW0 = 0, gb0 = gW0 + HID * IN, gW1 = gb0 + HID, gb1 = gW1 + HID * HID, gW2 = gb1 + HID;  // offsets
+      double* const G = a.mlp_grad;
+      long long* const FX = a.grad_fixed;
       if (g_started) {
         for (int c0 = 8 * half; c0 < X0C; c0 += 8 * kSplit) {  // G0: IN + 8 columns = dW0[row][0..IN), db0[row] at column IN
           uint32_t r[16];
@@ -516,9 +524,9 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
           tmem_ld_wait();
           if (lane < 16) {
             if (c0 < IN) {
-              for (int i = 0; i < 8; ++i) atomicAdd(gW0 + row * IN + c0 + i, static_cast<double>(__uint_as_float(r[i])));
+              for (int i = 0; i < 8; ++i) add_total(G, FX, gW0 + row * IN + c0 + i, static_cast<double>(__uint_as_float(r[i])));
             } else {
-              atomicAdd(gb0 + row, static_cast<double>(__uint_as_float(r[8])));
+              add_total(G, FX, gb0 + row, static_cast<double>(__uint_as_float(r[8])));
             }
           }
         }
@@ -528,9 +536,9 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
           tmem_ld_wait();
           if (lane < 16) {
             if (c0 < 64) {
-              for (int i = 0; i < 8; ++i) atomicAdd(gW1 + row * HID + c0 + i, static_cast<double>(__uint_as_float(r[i])));
+              for (int i = 0; i < 8; ++i) add_total(G, FX, gW1 + row * HID + c0 + i, static_cast<double>(__uint_as_float(r[i])));
             } else {
-              atomicAdd(gb1 + row, static_cast<double>(__uint_as_float(r[8])));
+              add_total(G, FX, gb1 + row, static_cast<double>(__uint_as_float(r[8])));
             }
           }
         }
@@ -539,7 +547,7 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
           tmem_ld16_nowait(tb + lane_base + tG2, r);
           tmem_ld_wait();
           if (lane < 16)
-            for (int o = 0; o < a.out_w; ++o) atomicAdd(gW2 + o * HID + row, static_cast<double>(__uint_as_float(r[o])));
+            for (int o = 0; o < a.out_w; ++o) add_total(G, FX, gW2 + o * HID + row, static_cast<double>(__uint_as_float(r[o])));
         }
       }
       // loss and output-bias gradient: per-thread fp64 partials -> warp shuffle -> one atomic per CTA (below)
@@ -559,9 +567,13 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
       double tot[4] = {0, 0, 0, 0};
       for (int w = 0; w < kEpiThreads / 32; ++w)
         for (int k = 0; k < 4; ++k) tot[k] += red_buf[w][k];
-      double* gb2 = a.mlp_grad + HID * IN + HID + HID * HID + HID + a.out_w * HID;
-      atomicAdd(a.loss_sum, tot[0]);
-      for (int o = 0; o < a.out_w && o < 3; ++o) atomicAdd(gb2 + o, tot[1 + o]);
+      const size_t gb2 = HID * IN + HID + HID * HID + HID + a.out_w * HID;
+      const size_t n_params = gb2 + a.out_w;
+      // reproducible mode: the CTAs' loss partials (not bounded like a gradient, so not fixed point) go to one slot per CTA
+      // behind the parameter words; the host side adds them to *loss_sum in CTA order
+      if (a.grad_fixed != nullptr) reinterpret_cast<double*>(a.grad_fixed + n_params)[blockIdx.x] = tot[0];
+      else atomicAdd(a.loss_sum, tot[0]);
+      for (int o = 0; o < a.out_w && o < 3; ++o) add_total(a.mlp_grad, a.grad_fixed, gb2 + o, tot[1 + o]);
     }
   }
   if (warp == 0) tmem_dealloc(tb, kTmemCols);
@@ -576,7 +588,7 @@ bool sxen_mlp_tc_supported(const sxen_mlp_config& c) {
 
 sxen_status sxen_mlp_tc_run(bool train, const float* params, const float* features, const void* targets, int target_f32,
                             float* pred, float* input_grad, double* mlp_grad, double* loss_sum, size_t n, int in_w, int out_w,
-                            size_t global_batch, int precise, cudaStream_t stream) {
+                            size_t global_batch, int precise, cudaStream_t stream, long long* grad_fixed, int* used_ctas) {
   if (n == 0) return SXEN_OK;
   if (in_w != 16 && in_w != 32) return fail(SXEN_INVALID_ARGUMENT, "mlp (tensor cores): input width %d not instantiated", in_w);
   TcArgs a{};
@@ -587,6 +599,7 @@ sxen_status sxen_mlp_tc_run(bool train, const float* params, const float* featur
   a.input_grad = input_grad;
   a.mlp_grad = mlp_grad;
   a.loss_sum = loss_sum;
+  a.grad_fixed = train ? grad_fixed : nullptr;
   a.n = n;
   a.out_w = out_w;
   a.target_f32 = target_f32;
@@ -608,5 +621,6 @@ sxen_status sxen_mlp_tc_run(bool train, const float* params, const float* featur
   if (st != SXEN_OK) return st;
   SXEN_CUDA(cudaGetLastError());
   count_launch();
+  if (used_ctas) *used_ctas = static_cast<int>(grid);
   return SXEN_OK;
 }

@@ -19,9 +19,17 @@ constexpr unsigned long long kNoBad = sxen_dev::kAdamNoBad;
 
 // SparseAdamState::step, src/optimizer.cpp:54-84.  One thread per table row; a row is visited iff the accumulator
 // touched it (feature 0 != -0.0f), zero gradients included; untouched rows' moments do not decay.
+// `fixed` != nullptr (reproducible mode, sxen_grad_set_reproducible): the gradient is the 64-bit fixed-point sum (units of
+// 2^-52, order-free); the fp32 accumulator still says which rows were touched and carries the NaN / range check -- a sum
+// of 2^10 or more in magnitude does not fit the fixed-point word and is reported like a non-finite gradient.
+__device__ __forceinline__ bool usable(double g_f32, bool repro) {
+  return isfinite(g_f32) && (!repro || fabs(g_f32) < 1024.0);
+}
+
 __global__ void sparse_adam_kernel(float* __restrict__ tables, float* __restrict__ grads, double* __restrict__ m,
                                    double* __restrict__ v, size_t rows, int features, AdamScalars c, int clear_grad,
-                                   unsigned long long* __restrict__ status, const unsigned long long* __restrict__ gate) {
+                                   unsigned long long* __restrict__ status, const unsigned long long* __restrict__ gate,
+                                   long long* __restrict__ fixed) {
   if (gate != nullptr && *gate != kNoBad) return;  // a queued step whose loss was non-finite applies no update
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   for (size_t r = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < rows; r += stride) {
@@ -29,8 +37,13 @@ __global__ void sparse_adam_kernel(float* __restrict__ tables, float* __restrict
     if (__float_as_uint(grads[base]) == kUntouchedBits) continue;
     for (int f = 0; f < features; ++f) {
       const size_t i = base + static_cast<size_t>(f);
-      const double g = static_cast<double>(grads[i]);
-      if (!isfinite(g)) {
+      double g = static_cast<double>(grads[i]);
+      const bool ok = usable(g, fixed != nullptr);
+      if (fixed != nullptr) {
+        g = __dmul_rn(static_cast<double>(fixed[i]), 0x1p-52);
+        if (clear_grad) fixed[i] = 0;
+      }
+      if (!ok) {
         atomicMin(status, static_cast<unsigned long long>(i));  // TrainingError, src/optimizer.cpp:73-76
         // the reference aborts the run here; this ABI can be called again, so the row must not keep its NaN/Inf (the next
         // backward would add into it): with clear_grad the whole row is re-armed like every other visited row
@@ -50,15 +63,23 @@ __global__ void sparse_adam_kernel(float* __restrict__ tables, float* __restrict
 // F == 2 fast path: 8-byte gradient/table rows, 16-byte moment rows, one vector access each.
 __global__ void sparse_adam_f2_kernel(float2* __restrict__ tables, float2* __restrict__ grads, double2* __restrict__ m,
                                       double2* __restrict__ v, size_t rows, AdamScalars c, int clear_grad,
-                                      unsigned long long* __restrict__ status, const unsigned long long* __restrict__ gate) {
+                                      unsigned long long* __restrict__ status, const unsigned long long* __restrict__ gate,
+                                      longlong2* __restrict__ fixed) {
   if (gate != nullptr && *gate != kNoBad) return;
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   for (size_t r = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < rows; r += stride) {
     const float2 g2 = grads[r];
     if (__float_as_uint(g2.x) == kUntouchedBits) continue;
-    const double gx = static_cast<double>(g2.x), gy = static_cast<double>(g2.y);
-    if (!isfinite(gx) || !isfinite(gy)) {
-      atomicMin(status, static_cast<unsigned long long>(2 * r + (isfinite(gx) ? 1 : 0)));
+    double gx = static_cast<double>(g2.x), gy = static_cast<double>(g2.y);
+    const bool okx = usable(gx, fixed != nullptr), oky = usable(gy, fixed != nullptr);
+    if (fixed != nullptr) {
+      const longlong2 q = fixed[r];
+      gx = __dmul_rn(static_cast<double>(q.x), 0x1p-52);
+      gy = __dmul_rn(static_cast<double>(q.y), 0x1p-52);
+      if (clear_grad) fixed[r] = make_longlong2(0, 0);
+    }
+    if (!okx || !oky) {
+      atomicMin(status, static_cast<unsigned long long>(2 * r + (okx ? 1 : 0)));
       if (clear_grad) grads[r] = make_float2(__uint_as_float(kUntouchedBits), __uint_as_float(kUntouchedBits));  // (see above)
       continue;
     }
@@ -220,10 +241,12 @@ sxen_status sxen_sparse_adam_step_gated(sxen_sparse_adam* opt, sxen_encoder* enc
   if (opt->features == 2) {
     sparse_adam_f2_kernel<<<grid_for(rows), 256, 0, as_stream(stream)>>>(
         reinterpret_cast<float2*>(enc->tables), reinterpret_cast<float2*>(grad->values),
-        reinterpret_cast<double2*>(opt->m), reinterpret_cast<double2*>(opt->v), rows, c, clear_grad, opt->status, gate_dev);
+        reinterpret_cast<double2*>(opt->m), reinterpret_cast<double2*>(opt->v), rows, c, clear_grad, opt->status, gate_dev,
+        reinterpret_cast<longlong2*>(grad->fixed));
   } else {
     sparse_adam_kernel<<<grid_for(rows), 256, 0, as_stream(stream)>>>(enc->tables, grad->values, opt->m, opt->v, rows,
-                                                                      opt->features, c, clear_grad, opt->status, gate_dev);
+                                                                      opt->features, c, clear_grad, opt->status, gate_dev,
+                                                                      grad->fixed);
   }
   SXEN_CUDA(cudaGetLastError());
   count_launch();

@@ -22,6 +22,9 @@ struct sxen_trainer {
   size_t head_samples = 0;       // samples whose input gradient the last accumulate_head left in the workspace
   float* features = nullptr;     // N x L*F
   float* input_grad = nullptr;   // N x L*F
+  double* input_grad64 = nullptr; // N x L*F, reproducible mode with the exact head: the same gradient as doubles
+  bool reproducible = false;
+  bool have_grad64 = false;      // the last accumulate_head filled input_grad64
   double* upstream = nullptr;    // N x out_w
   double* sample_loss = nullptr; // N
   double* loss_sum = nullptr;    // device scalar: sum of per-sample losses accumulated since the last update
@@ -83,13 +86,16 @@ sxen_status ensure_workspace(sxen_trainer* t, size_t n) {
   if (n <= t->capacity) return SXEN_OK;
   cudaFree(t->features);
   cudaFree(t->input_grad);
+  cudaFree(t->input_grad64);
   cudaFree(t->upstream);
   cudaFree(t->sample_loss);
+  t->input_grad64 = nullptr;
   t->features = t->input_grad = nullptr;
   t->upstream = t->sample_loss = nullptr;
   t->capacity = 0;
   SXEN_CUDA(cudaMalloc(&t->features, n * static_cast<size_t>(t->in_w) * sizeof(float)));
   SXEN_CUDA(cudaMalloc(&t->input_grad, n * static_cast<size_t>(t->in_w) * sizeof(float)));
+  if (t->reproducible) SXEN_CUDA(cudaMalloc(&t->input_grad64, n * static_cast<size_t>(t->in_w) * sizeof(double)));
   SXEN_CUDA(cudaMalloc(&t->upstream, n * static_cast<size_t>(t->out_w) * sizeof(double)));
   SXEN_CUDA(cudaMalloc(&t->sample_loss, (n + 1) * sizeof(double)));
   t->capacity = n;
@@ -180,6 +186,7 @@ sxen_status sxen_trainer_destroy(sxen_trainer* t) {
   sxen_adam_destroy(t->mlp_opt);
   cudaFree(t->features);
   cudaFree(t->input_grad);
+  cudaFree(t->input_grad64);
   cudaFree(t->upstream);
   cudaFree(t->sample_loss);
   cudaFree(t->loss_sum);
@@ -244,8 +251,12 @@ sxen_status sxen_trainer_accumulate_head(sxen_trainer* t, const void* coords_dev
     count_launch();
   }
   // mlp.forward, loss + upstream, mlp.backward (:36-46): one fused call (tensor-core kernel or the exact chain)
-  if (sxen_status st = sxen_mlp_forward_backward(t->mlp, t->features, targets_dev, target_type, n_samples, global_batch,
-                                                 nullptr, t->input_grad, t->loss_sum, stream))
+  int32_t precision = SXEN_MLP_EXACT;
+  sxen_mlp_get_precision(t->mlp, &precision);
+  t->have_grad64 = t->reproducible && precision == SXEN_MLP_EXACT && t->input_grad64 != nullptr;
+  if (sxen_status st = sxen_mlp_forward_backward_ex(t->mlp, t->features, targets_dev, target_type, n_samples, global_batch,
+                                                    nullptr, t->input_grad, t->have_grad64 ? t->input_grad64 : nullptr,
+                                                    t->loss_sum, stream))
     return st;
   t->head_samples = n_samples;
   t->foreign_grads = true;
@@ -261,8 +272,9 @@ sxen_status sxen_trainer_accumulate_tables(sxen_trainer* t, const void* coords_d
                 n_samples, t->head_samples);
   DeviceGuard guard(t->device);
   // encoder.encode_backward on d(loss)/d(encoding) (:47), levels [first_level, first_level + level_count)
-  return sxen_encoder_encode_backward_strided(t->enc, coords_dev, coord_type, t->input_grad, t->aux_dims > 0 ? t->in_w : 0,
-                                              n_samples, t->grad, first_level, level_count, stream);
+  return sxen_encoder_encode_backward_strided64(t->enc, coords_dev, coord_type, t->input_grad,
+                                                t->have_grad64 ? t->input_grad64 : nullptr, t->aux_dims > 0 ? t->in_w : 0,
+                                                n_samples, t->grad, first_level, level_count, stream);
 }
 
 sxen_status sxen_trainer_accumulate(sxen_trainer* t, const void* coords_dev, sxen_coord_type coord_type,
@@ -351,6 +363,19 @@ sxen_status sxen_trainer_step_enqueue(sxen_trainer* t, const void* coords_dev, s
   return update_impl(t, table_adam, mlp_adam, walk ? coords_dev : nullptr, coord_type, n_samples, t->gate, stream);
 }
 
+sxen_status sxen_trainer_set_reproducible(sxen_trainer* t, int32_t on) {
+  SXEN_REQUIRE(t != nullptr, "trainer handle is null");
+  if (t->pending != 0)
+    return fail(SXEN_LOGIC_ERROR, "train: %zu queued steps not collected (sxen_trainer_collect first)", t->pending);
+  DeviceGuard guard(t->device);
+  if (sxen_status st = sxen_grad_set_reproducible(t->grad, on)) return st;
+  if (sxen_status st = sxen_mlp_set_reproducible(t->mlp, on)) return st;
+  t->reproducible = on != 0;
+  t->capacity = 0;  // the workspace is re-made with (or without) the f64 gradient rows at the next step
+  t->have_grad64 = false;
+  return SXEN_OK;
+}
+
 // ------------------------------------------------------------------------------------------------ batch-sharded step
 sxen_status sxen_trainer_set_comm(sxen_trainer* t, sxen_comm* comm) {
   SXEN_REQUIRE(t != nullptr, "trainer handle is null");
@@ -388,8 +413,12 @@ sxen_status sxen_trainer_allreduce_levels(sxen_trainer* t, int32_t first_level, 
   if (t->comm == nullptr || level_count == 0) return SXEN_OK;
   const size_t per_level = static_cast<size_t>(ec.table_size) * static_cast<size_t>(ec.features);
   t->foreign_grads = true;  // the accumulator now holds other ranks' rows: the table update must scan, not walk this batch
-  return sxen_comm_allreduce(t->comm, t->grad->values + static_cast<size_t>(first_level) * per_level,
-                             static_cast<size_t>(level_count) * per_level, SXEN_COORD_F32, stream);
+  if (sxen_status st = sxen_comm_allreduce(t->comm, t->grad->values + static_cast<size_t>(first_level) * per_level,
+                                           static_cast<size_t>(level_count) * per_level, SXEN_COORD_F32, stream))
+    return st;
+  if (t->grad->fixed == nullptr) return SXEN_OK;
+  return sxen_comm_allreduce(t->comm, t->grad->fixed + static_cast<size_t>(first_level) * per_level,
+                             static_cast<size_t>(level_count) * per_level, SXEN_ELEM_I64, stream);
 }
 
 sxen_status sxen_trainer_step_sharded(sxen_trainer* t, const void* coords_dev, sxen_coord_type coord_type,

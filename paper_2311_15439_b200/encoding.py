@@ -200,6 +200,35 @@ class EncoderGradient:
                                                           touched.ctypes.data_as(C.POINTER(C.c_uint8))))
         return vals, touched
 
+    def set_reproducible(self, on: bool = True) -> None:
+        """sxen_grad_set_reproducible: every backward also keeps order-free 64-bit fixed-point sums (units of 2^-52) that
+        the optimizers and ``level`` / ``level_f64`` then use -- the reference's bit-reproducible merge
+        (src/trainer.cpp:125-128) instead of fp32-atomic order."""
+        raise_for(self._lib, self._lib.sxen_grad_set_reproducible(self._h, 1 if on else 0))
+
+    def reproducible(self) -> bool:
+        out = C.c_int32()
+        raise_for(self._lib, self._lib.sxen_grad_is_reproducible(self._h, C.byref(out)))
+        return bool(out.value)
+
+    def level_f64(self, level: int) -> np.ndarray:
+        """values[T, F] of one level as doubles: the exact fixed-point sums in reproducible mode, else the f32 values."""
+        T, F = self._cfg.table_size, self._cfg.features
+        vals = np.empty((T, F), dtype=np.float64)
+        raise_for(self._lib, self._lib.sxen_grad_download_f64(self._h, level, vals.ctypes.data_as(C.POINTER(C.c_double))))
+        return vals
+
+    def fixed_device_view(self):
+        """The fixed-point words as a flat int64 CUDA tensor (reproducible mode), for an exchange or a bit comparison."""
+        import torch
+        ptr, cnt = C.c_void_p(), C.c_size_t()
+        raise_for(self._lib, self._lib.sxen_grad_fixed_dev(self._h, C.byref(ptr), C.byref(cnt)))
+        if not ptr.value:
+            raise RuntimeError("gradient accumulator is not in reproducible mode")
+        t = torch.as_tensor(_DevArray(ptr.value, cnt.value, "<i8", self), device=f"cuda:{self.device}")
+        assert t.data_ptr() == ptr.value
+        return t
+
     def set_level(self, level: int, values, touched) -> None:
         vals = np.ascontiguousarray(values, dtype=np.float32)
         tch = np.ascontiguousarray(touched, dtype=np.uint8)

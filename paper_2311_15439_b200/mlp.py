@@ -128,6 +128,11 @@ class Mlp:
         """0 = exact fp64-accumulate (default), 1 = tcgen05 split-bf16 (~1e-5), 2 = tcgen05 single bf16 (~4e-3)."""
         raise_for(self._lib, self._lib.sxen_mlp_set_precision(self._h, int(mode)))
 
+    def set_reproducible(self, on: bool = True) -> None:
+        """sxen_mlp_set_reproducible: the kernels' partial parameter gradients (and the tensor-core head's loss) meet in
+        64-bit fixed point, so they do not depend on block scheduling (src/mlp.cpp:83-88's fixed-order merge)."""
+        raise_for(self._lib, self._lib.sxen_mlp_set_reproducible(self._h, 1 if on else 0))
+
     def precision(self) -> int:
         out = C.c_int32()
         raise_for(self._lib, self._lib.sxen_mlp_get_precision(self._h, C.byref(out)))

@@ -34,6 +34,7 @@ class TrainConfig:
     seed: int = 1234
     threads: int = 0
     record_every: int = 100
+    reproducible: bool = False  # no reference field: order-free gradient sums (Trainer.set_reproducible)
 
 
 @dataclass
@@ -116,6 +117,19 @@ class Trainer:
         raise_for(self._lib, self._lib.sxen_grad_values_dev(g, C.byref(ptr), C.byref(cnt)))
         return _wrap_device(ptr.value, cnt.value, torch.float32, self)
 
+    def table_grad_fixed_device(self):
+        """The accumulator's fixed-point words (flat int64 view) in reproducible mode, else None; summed over the ranks
+        next to the f32 values, which then only carry the touched markers."""
+        import torch
+        from .encoding import _DevArray
+        g = C.c_void_p()
+        raise_for(self._lib, self._lib.sxen_trainer_table_grad(self._h, C.byref(g)))
+        ptr, cnt = C.c_void_p(), C.c_size_t()
+        raise_for(self._lib, self._lib.sxen_grad_fixed_dev(g, C.byref(ptr), C.byref(cnt)))
+        if not ptr.value:
+            return None
+        return torch.as_tensor(_DevArray(ptr.value, cnt.value, "<i8", self), device=f"cuda:{self.encoder.device}")
+
     def loss_device(self):
         import torch
         from .encoding import _wrap_device
@@ -177,6 +191,11 @@ class Trainer:
         raise_for(self._lib, st)
         return list(buf[:cnt.value]), -1
 
+    def set_reproducible(self, on: bool = True) -> None:
+        """sxen_trainer_set_reproducible: bit-reproducible steps (order-free fixed-point gradient sums for the tables and
+        the MLP; with the exact head d(loss)/d(encoding) reaches encode_backward as doubles)."""
+        raise_for(self._lib, self._lib.sxen_trainer_set_reproducible(self._h, 1 if on else 0))
+
     def set_comm(self, comm) -> None:
         """Attaches a ``Comm`` (kept alive here; None detaches): ``step_sharded`` then exchanges through the C ABI."""
         self._comm_handle = comm
@@ -216,6 +235,7 @@ class Trainer:
         levels = self.encoder.config.levels
         bounds = level_ranges(levels, level_chunks)
         gview = self.table_grad_device()
+        fview = self.table_grad_fixed_device()
         per_level = gview.numel() // levels
         if not x.is_cuda:
             raise ValueError("distributed_step: coords must be CUDA tensors")
@@ -238,6 +258,8 @@ class Trainer:
             comm.wait_event(ev)
             with torch.cuda.stream(comm):
                 dist.all_reduce(gview[first * per_level:(first + count) * per_level], group=group)
+                if fview is not None:
+                    dist.all_reduce(fview[first * per_level:(first + count) * per_level], group=group)
         main.wait_stream(comm)
         loss = self.loss(batch)
         self.update(table_adam, mlp_adam)
@@ -269,6 +291,8 @@ def train_field(encoder, mlp, sampler: BatchSampler, cfg: TrainConfig, group=Non
     if sampler is None:
         raise ValueError("train: sampler must be callable")
     trainer = Trainer(encoder, mlp, cfg.aux_dims)
+    if cfg.reproducible:
+        trainer.set_reproducible(True)
     distributed = False
     if group is not None:
         distributed = True

@@ -91,7 +91,13 @@ def main():
         print(f"{name:40s} mean {t[0]:.4f} ms  best {t[1]:.4f}  median {t[2]:.4f}  -> {N / t[2] / 1e6:.3f} G samples/s "
               f"frac {((652 + 1164) if n == 3 else 1424) * N / (t[2] * 1e-3) / 1e9 / 6552:.3f}", flush=True)
 
-    show("base fused", timeit(fused))
+    enc.set_tuning(sx.Tuning(exact_blend=1, level_chunk=-1))
+    show("base fused (one grid slice)", timeit(fused))
+    for ch in (8, 4):
+        for lpt in (2, 1, 4):
+            enc.set_tuning(sx.Tuning(exact_blend=1, level_chunk=ch, levels_per_thread=lpt, level_major=0))
+            show(f"ONE launch, level_chunk={ch} lpt={lpt}", timeit(fused))
+    enc.set_tuning(sx.Tuning(exact_blend=1, level_chunk=-1))
     for k in (2, 4):
         show(f"fused in {k} level chunks", timeit(chunks(k)))
 
@@ -113,13 +119,13 @@ def main():
             show(f"fused level-major lpt={lpt}", timeit(fused))
         except Exception as exc:
             print("level-major lpt", lpt, "failed:", exc)
-    enc.set_tuning(sx.Tuning(exact_blend=1))
+    enc.set_tuning(sx.Tuning(exact_blend=1, level_chunk=-1))
 
     # persisting-L2 window over the tables
     err, prop = rt.cudaGetDeviceProperties(0)
     print("persistingL2CacheMaxSize", prop.persistingL2CacheMaxSize >> 20, "MiB; accessPolicyMaxWindowSize",
           prop.accessPolicyMaxWindowSize >> 20, "MiB; l2CacheSize", prop.l2CacheSize >> 20, "MiB", flush=True)
-    ATTR = rt.cudaLaunchAttributeID.cudaLaunchAttributeAccessPolicyWindow
+    ATTR = rt.cudaStreamAttrID.cudaStreamAttributeAccessPolicyWindow if hasattr(rt.cudaStreamAttrID, 'cudaStreamAttributeAccessPolicyWindow') else rt.cudaLaunchAttributeID.cudaLaunchAttributeAccessPolicyWindow
     tables_ptr = enc.tables_device().data_ptr()
     table_bytes = L * (1 << args.log2t) * 2 * 4
     gptr = grad.device_view().data_ptr()
@@ -129,7 +135,7 @@ def main():
         assert err == rt.cudaError_t.cudaSuccess, err
         for what, base_ptr in (("tables", tables_ptr), ("grads", gptr)):
             for ratio in (1.0, 0.6):
-                attr = rt.cudaLaunchAttributeValue()
+                attr = rt.cudaStreamAttrValue()
                 w = rt.cudaAccessPolicyWindow()
                 w.base_ptr = base_ptr
                 w.num_bytes = min(table_bytes, prop.accessPolicyMaxWindowSize)
@@ -142,7 +148,7 @@ def main():
                 show(f"window {what} carve {carve >> 20} MiB ratio {ratio}", timeit(fused))
                 show(f"window {what} carve {carve >> 20} MiB ratio {ratio} + 2 chunks", timeit(chunks(2)))
         # reset
-        attr = rt.cudaLaunchAttributeValue()
+        attr = rt.cudaStreamAttrValue()
         w = rt.cudaAccessPolicyWindow()
         w.num_bytes = 0
         attr.accessPolicyWindow = w

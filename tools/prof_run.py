@@ -15,13 +15,14 @@ ap.add_argument("--dim", type=int, default=3)
 ap.add_argument("--lpt", type=int, default=0)
 ap.add_argument("--level-major", type=int, default=0)
 ap.add_argument("--log2t", type=int, default=19)
+ap.add_argument("--level-chunk", type=int, default=0, help="sxen_tuning.level_chunk (0 library default, -1 one grid slice)")
 a = ap.parse_args()
 n, N = a.dim, 1 << 20
 cfg = sx.EncoderConfig(dim=n, levels=16, table_size=1 << a.log2t, features=2, base_resolution=16,
                        growth={2: 2.0, 3: 1.5}.get(n, 1.5))
 enc = sx.HashEncoder(cfg)
 enc.init_tables(42)
-enc.set_tuning(sx.Tuning(levels_per_thread=a.lpt, level_major=a.level_major))
+enc.set_tuning(sx.Tuning(levels_per_thread=a.lpt, level_major=a.level_major, level_chunk=a.level_chunk))
 grad = sx.EncoderGradient(enc)
 x = torch.empty((N, n), dtype=torch.float32, device="cuda")
 sx.CounterRng(99, 1).fill_device(x)

@@ -432,6 +432,46 @@ inline FitImageResult fit_image(const ImageDataset& image, const EncoderConfig& 
   return result;
 }
 
+// fit_image on make_test_image(width, height, image_seed) WITHOUT the image in memory (BASELINE configs[2], the gigapixel fit:
+// 32768 x 32768 would be 26 GB as doubles): the sampler (src/tasks.cpp:112-126) draws the pixel and evaluates the image's
+// procedural definition (src/image.cpp:68-96) there, sxen_sample_test_image_batch.  comm != nullptr: this call is one rank of a
+// batch-sharded run (train_field above).  The final PSNR is render_image's over the first psnr_pixels pixels in row-major
+// order (the whole image when it has no more).
+inline FitImageResult fit_test_image(int width, int height, std::uint64_t image_seed, const EncoderConfig& encoder_cfg,
+                                     const TrainConfig& train_cfg, const FitImageOptions& opt = {}, int device = 0,
+                                     void* stream = nullptr, const Comm* comm = nullptr, std::size_t psnr_pixels = std::size_t{1} << 24) {
+  if (width < 1 || height < 1) throw std::invalid_argument("test image: width and height must be >= 1");
+  if (encoder_cfg.dim != 2) throw std::invalid_argument("fit_image: encoder dim must be 2");
+  HashEncoder encoder(encoder_cfg, device);
+  encoder.init_tables(opt.init_seed, stream);
+  Mlp mlp(MlpConfig{encoder_cfg.encoded_width(), opt.mlp_hidden_width, opt.mlp_hidden_layers, 3}, device);
+  mlp.init_params(sxen_hash_combine(opt.init_seed, 1), stream);
+  if (opt.mlp_precision != MlpPrecision::exact) check(sxen_mlp_set_precision(mlp.handle(), static_cast<int>(opt.mlp_precision)));
+  const std::uint64_t seed = train_cfg.seed;
+  const BatchSampler sampler = [=](int step, DeviceSpan<double> coords, DeviceSpan<double> /*aux*/, DeviceSpan<double> targets,
+                                   void* s) {
+    check(sxen_sample_test_image_batch(image_seed, width, height, seed, static_cast<std::uint64_t>(step), 0, coords.size / 2,
+                                       coords.data, targets.data, s));
+  };
+  TrainResult train = train_field(encoder, mlp, sampler, train_cfg, device, stream, comm);
+  FitImageResult result{std::move(encoder), std::move(mlp), std::move(train), 0.0, {}};
+  for (const auto& [s, loss] : result.train.loss_curve) result.psnr_curve.emplace_back(s, psnr_from_mse(loss));
+  const std::size_t total = std::min(psnr_pixels, static_cast<std::size_t>(width) * static_cast<std::size_t>(height));
+  const std::size_t step = std::min<std::size_t>(total, std::size_t{1} << 20);
+  DeviceBuffer<double> coords(step * 2, device), sum(1, device);
+  DeviceBuffer<float> feats(step * static_cast<std::size_t>(encoder_cfg.encoded_width()), device), pred(step * 3, device);
+  sum.zero(stream);
+  for (std::size_t first = 0; first < total; first += step) {
+    const std::size_t n = std::min(step, total - first);
+    check(sxen_pixel_centers(width, height, first, n, coords.data(), stream));
+    result.encoder.encode(coords.cspan(n * 2), feats.span(n * static_cast<std::size_t>(encoder_cfg.encoded_width())), stream);
+    result.mlp.forward(feats.cspan(n * static_cast<std::size_t>(encoder_cfg.encoded_width())), pred.span(n * 3), stream);
+    check(sxen_test_image_sq_error(image_seed, width, height, pred.data(), first, n, sum.data(), stream));
+  }
+  result.final_psnr = psnr_from_mse(sum.download(1, stream)[0] / (3.0 * static_cast<double>(total)));
+  return result;
+}
+
 // include/sxen/noise.hpp:38-50, same defaults (sxen_noise_spec_default)
 enum class NoiseKind { perlin = SXEN_NOISE_PERLIN, simplex = SXEN_NOISE_SIMPLEX };
 struct NoiseFieldSpec {

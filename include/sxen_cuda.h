@@ -475,6 +475,18 @@ SXEN_API sxen_status sxen_sample_field_batch(const sxen_noise_spec* spec, uint64
 SXEN_API sxen_status sxen_sample_image_batch(uint64_t seed, uint64_t step, const double* image_dev, int32_t width,
                                              int32_t height, size_t n_samples, double* coords_dev, double* targets_dev,
                                              void* stream);
+/* The same sampler over make_test_image(width, height, image_seed) (src/image.cpp:68-96) WITHOUT the image in memory: the
+ * drawn pixel's RGB is evaluated on the fly from the procedural definition (BASELINE configs[2]: 32768 x 32768 would be
+ * 26 GB as doubles).  Fills samples [first_sample, first_sample + n_samples) of step `step`'s batch (draw s+1 of
+ * CounterRng(train_seed, step) for sample s), so a rank of a batch-sharded run can generate its own chunk only.
+ * coords_dev n_samples x 2 f64, targets_dev n_samples x 3 f64; coordinates and pixel indices bit-identical to
+ * sxen_sample_image_batch, targets equal to the stored image's to rounding (libm). */
+SXEN_API sxen_status sxen_sample_test_image_batch(uint64_t image_seed, int32_t width, int32_t height, uint64_t train_seed,
+                                                  uint64_t step, size_t first_sample, size_t n_samples, double* coords_dev,
+                                                  double* targets_dev, void* stream);
+/* sxen_render_sq_error against the never-materialised test image: pred_dev count x 3 f32 for pixels [first_pixel, +count). */
+SXEN_API sxen_status sxen_test_image_sq_error(uint64_t image_seed, int32_t width, int32_t height, const float* pred_dev,
+                                              size_t first_pixel, size_t count, double* sum_dev, void* stream);
 /* render_image's coordinates (src/tasks.cpp:69-71) for pixels [first_pixel, first_pixel + count), row-major. */
 SXEN_API sxen_status sxen_pixel_centers(int32_t width, int32_t height, size_t first_pixel, size_t count, double* coords_dev,
                                         void* stream);

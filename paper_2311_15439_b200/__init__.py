@@ -17,7 +17,8 @@ from .trainer import TrainConfig, Trainer, TrainResult, chunk_bounds, level_rang
 from .checkpoint import load_checkpoint, save_checkpoint  # noqa: E402
 from .tasks import (FitFieldOptions, FitFieldResult, FitImageOptions, FitImageResult, NoiseFieldSpec, NoiseKind,  # noqa: E402
                     field_sampler, fit_field, fit_image, image_mse, image_psnr, image_sampler, make_test_image,
-                    noise_field_value, psnr_from_mse, render_image, render_mse)
+                    noise_field_value, psnr_from_mse, render_image, render_mse, fit_test_image, test_image_mse,
+                    test_image_sampler)
 from .rng import CounterRng, hash_combine, mix64  # noqa: E402
 from .comm import Comm, CommError  # noqa: E402
 from .analysis import (KernelBenchConfig, KernelBenchReport, bench_kernel, bench_side, read_kernel_csv,  # noqa: E402
@@ -30,7 +31,8 @@ __all__ = ["lib", "CudaError", "IoError", "TrainingError", "Backend", "LevelScal
            "FitImageOptions", "FitImageResult", "fit_image", "image_sampler", "psnr_from_mse", "render_mse", "render_image", "image_mse", "image_psnr",
            "save_checkpoint", "load_checkpoint", "KernelBenchConfig", "KernelBenchReport", "bench_kernel", "bench_side",
            "read_kernel_csv", "write_kernel_csv", "NoiseKind", "NoiseFieldSpec", "noise_field_value", "field_sampler",
-           "FitFieldOptions", "FitFieldResult", "fit_field", "make_test_image", "Comm", "CommError"]
+           "FitFieldOptions", "FitFieldResult", "fit_field", "make_test_image", "Comm", "CommError", "fit_test_image", "test_image_sampler",
+           "test_image_mse"]
 
 
 def device_count() -> int:

@@ -162,6 +162,80 @@ __global__ void __launch_bounds__(128) sample_field_kernel(const sxen_noise_spec
   }
 }
 
+// make_test_image (src/image.cpp:68-96) at one pixel centre: a shared 4-octave Perlin field plus one 5-octave field per
+// channel, v = 0.45 * base + 0.55 * channel, pixel = clamp(0.5 + 0.62 * v, 0, 1).
+struct TestImageSpec {
+  sxen_noise_spec shared;
+  sxen_noise_spec channel[3];
+};
+
+__device__ __forceinline__ void test_image_pixel(const TestImageSpec& im, const double (&xy)[2], double (&rgb)[3]) {
+  const double base = noise_field_value(im.shared, xy);
+#pragma unroll 1
+  for (int c = 0; c < 3; ++c) {
+    const double v = 0.45 * base + 0.55 * noise_field_value(im.channel[c], xy);
+    const double p = 0.5 + 0.62 * v;
+    rgb[c] = p < 0.0 ? 0.0 : (1.0 < p ? 1.0 : p);
+  }
+}
+
+// fit_image's sampler (src/tasks.cpp:112-126) over an image that is never materialised: draw s (1-based, s = first + i + 1)
+// of CounterRng(train_seed, step) picks the pixel, its centre is the coordinate, make_test_image's formula is the target.
+__global__ void __launch_bounds__(128) sample_test_image_kernel(const TestImageSpec im, uint64_t key, int w, int h,
+                                                                unsigned long long first, unsigned long long n,
+                                                                double* __restrict__ coords, double* __restrict__ targets) {
+  const unsigned long long pixels = static_cast<unsigned long long>(w) * static_cast<unsigned long long>(h);
+  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+  for (unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t u = sxen_dev::mix64(key + 0x9e3779b97f4a7c15ULL * (first + i + 1));
+    const unsigned long long idx = u % pixels;
+    const double xy[2] = {__ddiv_rn(__dadd_rn(static_cast<double>(idx % static_cast<unsigned long long>(w)), 0.5), static_cast<double>(w)),
+                          __ddiv_rn(__dadd_rn(static_cast<double>(idx / static_cast<unsigned long long>(w)), 0.5), static_cast<double>(h))};
+    double rgb[3];
+    test_image_pixel(im, xy, rgb);
+    coords[2 * i] = xy[0];
+    coords[2 * i + 1] = xy[1];
+    targets[3 * i] = rgb[0];
+    targets[3 * i + 1] = rgb[1];
+    targets[3 * i + 2] = rgb[2];
+  }
+}
+
+// render_image's error against the same never-materialised image (src/tasks.cpp:76-78, 35-46): pixel p of the list (or
+// first + i when the list is null) -> sum of (clamp(pred, 0, 1) - pixel)^2 over the 3 channels, added to *sum.
+__global__ void __launch_bounds__(128) test_image_error_kernel(const TestImageSpec im, int w, int h, const float* __restrict__ pred,
+                                                               unsigned long long first, unsigned long long count,
+                                                               double* __restrict__ sum) {
+  __shared__ double part[4];
+  double acc = 0.0;
+  const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+  for (unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
+    const unsigned long long p = first + i;
+    const double xy[2] = {__ddiv_rn(__dadd_rn(static_cast<double>(p % static_cast<unsigned long long>(w)), 0.5), static_cast<double>(w)),
+                          __ddiv_rn(__dadd_rn(static_cast<double>(p / static_cast<unsigned long long>(w)), 0.5), static_cast<double>(h))};
+    double rgb[3];
+    test_image_pixel(im, xy, rgb);
+    for (int c = 0; c < 3; ++c) {
+      double q = static_cast<double>(pred[3 * i + c]);
+      q = q < 0.0 ? 0.0 : (1.0 < q ? 1.0 : q);
+      const double e = q - rgb[c];
+      acc += e * e;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(sum, part[0] + part[1] + part[2] + part[3]);
+}
+
+TestImageSpec test_image_spec(uint64_t seed) {  // src/image.cpp:72-79
+  TestImageSpec im{};
+  im.shared = sxen_noise_spec{2, SXEN_NOISE_PERLIN, 4, 0, sxen_dev::hash_combine(seed, 0xABu), 4.0};
+  for (int c = 0; c < 3; ++c)
+    im.channel[c] = sxen_noise_spec{2, SXEN_NOISE_PERLIN, 5, 0, sxen_dev::hash_combine(seed, static_cast<uint64_t>(c + 1)), 8.0};
+  return im;
+}
+
 int blocks_for(size_t n) {
   size_t b = (n + 127) / 128;
   if (b > 148 * 16) b = 148 * 16;
@@ -205,6 +279,33 @@ sxen_status sxen_sample_field_batch(const sxen_noise_spec* spec, uint64_t seed, 
   // CounterRng(seed, stream) or CounterRng(seed), include/sxen/rng.hpp:22-29
   const uint64_t key = has_stream ? sxen_dev::hash_combine(sxen_dev::mix64(seed), stream_id) : sxen_dev::mix64(seed);
   sample_field_kernel<<<blocks_for(n_samples), 128, 0, as_stream(stream)>>>(*spec, key, n_samples, coords_dev, targets_dev);
+  SXEN_CUDA(cudaGetLastError());
+  count_launch();
+  return SXEN_OK;
+}
+
+sxen_status sxen_sample_test_image_batch(uint64_t image_seed, int32_t width, int32_t height, uint64_t train_seed, uint64_t step,
+                                         size_t first_sample, size_t n_samples, double* coords_dev, double* targets_dev,
+                                         void* stream) {
+  SXEN_REQUIRE(width >= 1 && height >= 1, "test image: width and height must be >= 1");  // src/image.cpp:69-71
+  SXEN_REQUIRE(n_samples == 0 || (coords_dev != nullptr && targets_dev != nullptr), "sample_test_image_batch: null pointer");
+  if (n_samples == 0) return SXEN_OK;
+  const uint64_t key = sxen_dev::hash_combine(sxen_dev::mix64(train_seed), step);  // CounterRng(seed, step), src/tasks.cpp:116
+  sample_test_image_kernel<<<blocks_for(n_samples), 128, 0, as_stream(stream)>>>(test_image_spec(image_seed), key, width, height,
+                                                                                first_sample, n_samples, coords_dev, targets_dev);
+  SXEN_CUDA(cudaGetLastError());
+  count_launch();
+  return SXEN_OK;
+}
+
+sxen_status sxen_test_image_sq_error(uint64_t image_seed, int32_t width, int32_t height, const float* pred_dev, size_t first_pixel,
+                                     size_t count, double* sum_dev, void* stream) {
+  SXEN_REQUIRE(width >= 1 && height >= 1, "test image: width and height must be >= 1");
+  SXEN_REQUIRE(count == 0 || (pred_dev != nullptr && sum_dev != nullptr), "test_image_sq_error: null pointer");
+  SXEN_REQUIRE(first_pixel + count <= static_cast<size_t>(width) * static_cast<size_t>(height), "test_image_sq_error: pixel range outside the image");
+  if (count == 0) return SXEN_OK;
+  test_image_error_kernel<<<blocks_for(count), 128, 0, as_stream(stream)>>>(test_image_spec(image_seed), width, height, pred_dev,
+                                                                           first_pixel, count, sum_dev);
   SXEN_CUDA(cudaGetLastError());
   count_launch();
   return SXEN_OK;

@@ -75,6 +75,70 @@ def image_sampler(image_dev, width: int, height: int, seed: int):
     return sampler
 
 
+def test_image_sampler(width: int, height: int, image_seed: int, train_seed: int, device: int = 0, first: int = 0,
+                       count: int = None):
+    """fit_image's BatchSampler over make_test_image(width, height, image_seed) without the image in memory
+    (sxen_sample_test_image_batch; BASELINE configs[2]: a 32768 x 32768 image is 26 GB as doubles).  ``first`` / ``count``
+    restrict every batch to that slice of its samples (a rank's chunk of a sharded batch)."""
+    import torch
+    lib = _lib()
+    dev = torch.device(f"cuda:{device}")
+    m64 = (1 << 64) - 1
+
+    def sampler(step: int, batch: int):
+        n = batch - first if count is None else count
+        coords = torch.empty((n, 2), dtype=torch.float64, device=dev)
+        targets = torch.empty((n, 3), dtype=torch.float64, device=dev)
+        raise_for(lib, lib.sxen_sample_test_image_batch(image_seed & m64, width, height, train_seed & m64, step, first, n,
+                                                        C.c_void_p(coords.data_ptr()), C.c_void_p(targets.data_ptr()),
+                                                        C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+        return coords, targets
+
+    return sampler
+
+
+def test_image_mse(encoder: HashEncoder, mlp: Mlp, width: int, height: int, image_seed: int, first_pixel: int = 0,
+                   count: int = None, chunk: int = 1 << 20) -> float:
+    """render_image's MSE (src/tasks.cpp:51-96, 35-46) against the never-materialised test image over pixels
+    [first_pixel, first_pixel + count) in row-major order (default: the whole image)."""
+    import torch
+    lib = _lib()
+    dev = torch.device(f"cuda:{encoder.device}")
+    total = width * height - first_pixel if count is None else count
+    acc = torch.zeros(1, dtype=torch.float64, device=dev)
+    stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    coords = torch.empty((min(chunk, total), 2), dtype=torch.float64, device=dev)
+    for off in range(0, total, chunk):
+        n = min(chunk, total - off)
+        raise_for(lib, lib.sxen_pixel_centers(width, height, first_pixel + off, n, C.c_void_p(coords.data_ptr()), stream))
+        pred = mlp.forward(encoder.encode(coords[:n]))
+        raise_for(lib, lib.sxen_test_image_sq_error(image_seed & ((1 << 64) - 1), width, height, C.c_void_p(pred.data_ptr()),
+                                                    first_pixel + off, n, C.c_void_p(acc.data_ptr()), stream))
+    return float(acc.item()) / (3.0 * total)
+
+
+def fit_test_image(width: int, height: int, image_seed: int, encoder_cfg: EncoderConfig, train_cfg: TrainConfig,
+                   opt: FitImageOptions = None, device: int = 0, psnr_pixels: int = 1 << 24) -> FitImageResult:
+    """fit_image (src/tasks.cpp:98-137) on make_test_image(width, height, image_seed) evaluated on the fly -- the gigapixel
+    workload (BASELINE configs[2]).  The final PSNR is measured over the first ``psnr_pixels`` pixels in row-major order
+    (the whole image when it has no more than that)."""
+    opt = opt or FitImageOptions()
+    if encoder_cfg.dim != 2:
+        raise ValueError("fit_image: encoder dim must be 2")
+    encoder = HashEncoder(encoder_cfg, device=device)
+    encoder.init_tables(opt.init_seed)
+    mlp = Mlp(MlpConfig(encoder_cfg.encoded_width(), opt.mlp_hidden_width, opt.mlp_hidden_layers, 3), device=device)
+    mlp.init_params(hash_combine(opt.init_seed, 1))
+    if opt.mlp_precision:
+        mlp.set_precision(opt.mlp_precision)
+    train = train_field(encoder, mlp, test_image_sampler(width, height, image_seed, train_cfg.seed, device), train_cfg)
+    result = FitImageResult(encoder, mlp, train)
+    result.psnr_curve = [(s, psnr_from_mse(l)) for s, l in train.loss_curve]
+    result.final_psnr = psnr_from_mse(test_image_mse(encoder, mlp, width, height, image_seed, 0,
+                                                     min(psnr_pixels, width * height)))
+    return result
+
+
 def render_mse(encoder: HashEncoder, mlp: Mlp, image_dev, width: int, height: int, chunk: int = 1 << 20) -> float:
     """MSE of render_image(encoder, mlp) against the image over all channels (src/tasks.cpp:51-96, 35-46), without
     materialising the rendered image on the host."""

@@ -404,6 +404,37 @@ def acceptance_thread_spread(ref: Ref):
     print("acceptance_thread_spread written")
 
 
+def gigapixel_sampler(ref: Ref):
+    """BASELINE configs[2]: the 32768 x 32768 procedural image is never stored (26 GB as doubles); fit_image's sampler
+    (src/tasks.cpp:112-126) draws pixel indices and the target is make_test_image's formula (src/image.cpp:68-96) at that
+    pixel centre.  This fixture holds, for steps 0 and 7 of train seed 1234, the first 1024 draws: pixel index, coordinates
+    and the RGB target computed by the REFERENCE's noise_field_value (the six lines of make_test_image around it are
+    restated here in numpy and first checked against ref.make_test_image on a 64 x 64 image)."""
+    def test_image_at(coords, seed):
+        shared = ref.noise_field(2, ref.hash_combine(seed, 0xAB), oracle.NOISE_PERLIN if hasattr(oracle, "NOISE_PERLIN") else 0, 4, 4.0, coords)
+        out = np.empty((coords.shape[0], 3))
+        for c in range(3):
+            ch = ref.noise_field(2, ref.hash_combine(seed, c + 1), 0, 5, 8.0, coords)
+            out[:, c] = np.clip(0.5 + 0.62 * (0.45 * shared + 0.55 * ch), 0.0, 1.0)
+        return out
+
+    small = ref.make_test_image(64, 64, 7)
+    yy, xx = np.meshgrid(np.arange(64), np.arange(64), indexing="ij")
+    cc = np.stack([(xx.ravel() + 0.5) / 64, (yy.ravel() + 0.5) / 64], axis=1)
+    assert np.array_equal(test_image_at(cc, 7).reshape(64, 64, 3), small), "numpy restatement of make_test_image differs"
+    W = H = 32768
+    d = {"width": np.int64(W), "height": np.int64(H), "image_seed": np.int64(7), "train_seed": np.int64(1234)}
+    for step in (0, 7):
+        u = ref.rng_u64(1234, step, 1024)
+        idx = (u % np.uint64(W * H)).astype(np.int64)
+        coords = np.stack([((idx % W) + 0.5) / W, ((idx // W) + 0.5) / H], axis=1)
+        d[f"step{step}/idx"] = idx
+        d[f"step{step}/coords"] = coords
+        d[f"step{step}/targets"] = test_image_at(coords, 7)
+    np.savez_compressed(os.path.join(OUT, "gigapixel_sampler.npz"), **d)
+    print("gigapixel_sampler written", d["step0/idx"][:4], d["step0/targets"][:2])
+
+
 if __name__ == "__main__":
     oracle.build(ref=True)
     ref = Ref()
@@ -412,6 +443,9 @@ if __name__ == "__main__":
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "acceptance":
         acceptance_image_fitting(ref)
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "gigapixel":
+        gigapixel_sampler(ref)
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "spread":
         acceptance_thread_spread(ref)

@@ -786,3 +786,35 @@ def test_chunked_fused_launch_matches_the_oracle(sx, oracle_lib, dim, levels, ch
     gv, gt = grad_dense(grad, cfg)
     assert np.array_equal(gt, ot)
     assert (np.abs(gv - og) <= GRAD_RTOL * scale + GRAD_ATOL).all()
+
+
+@pytest.mark.parametrize("dim", [2, 4, 5, 6])
+def test_config5_table_size_under_the_library_launch_shape(sx, oracle_lib, dim):
+    """BASELINE configs[4] as stated -- n = 2..6 at L=16, F=2, T=2^22 (512 MiB of tables) -- under the launch shape the
+    library picks on its own there (level-major, two levels per thread, the fused call split into a forward and a backward
+    launch, evict_last hints): a 2^14-sample batch against the oracle.  Indices / weights / features bit for bit, touched
+    rows exact, gradients to the fp32-atomic bar.  (n = 3 at this size: test_level_major... above.)"""
+    cfg = oracle.Config(dim=dim, levels=16, table_size=1 << 22, features=2, base_resolution=16, growth=1.5 if dim > 2 else 2.0)
+    enc = make_encoder(sx, cfg, seed=42)
+    N = 1 << 14
+    x32 = oracle_lib.rng_doubles(99, 1, N * dim).reshape(N, dim).astype(np.float32)
+    up32 = oracle_lib.rng_doubles(7, 2, N * 32, -1.0, 1.0).astype(np.float32).reshape(N, 32)
+    xd, upd = x32.astype(np.float64), up32.astype(np.float64)
+    t = enc.tuning()
+    assert t.level_major == -1 and t.levels_per_thread == 0 and t.cache_hints == -1   # everything left to the library
+    grad = sx.EncoderGradient(enc)
+    launches = sx.launch_count()
+    feats = enc.encode_forward_backward(dev(x32), dev(up32), grad)
+    assert sx.launch_count() - launches >= 2   # forward launch + backward launch (+ fold)
+    enc.check()
+    idx, w = enc.encode_debug(dev(x32))
+    oi, ow, _, _, _ = oracle_lib.encode_debug(cfg, xd)
+    assert np.array_equal(idx, oi) and np.array_equal(w, ow)
+    want, bad = oracle_lib.encode(cfg, oracle_lib.init_tables(cfg, 42), xd)
+    assert bad == -1 and np.array_equal(feats.cpu().numpy().view(np.uint32), want.view(np.uint32))
+    og, ot, _ = oracle_lib.encode_backward(cfg, xd, upd)
+    scale = abs_contrib(oracle_lib, cfg, xd, upd)
+    for l in range(16):   # level by level: the dense [16, 2^22, 2] arrays are 512 MiB each on the host
+        gv, gt = grad.level(l)
+        assert np.array_equal(gt, ot[l]), (dim, l)
+        assert (np.abs(gv - og[l]) <= GRAD_RTOL * scale[l] + GRAD_ATOL).all(), (dim, l)

@@ -99,5 +99,33 @@ def train_throughput(n, log2_batch, growth, label):
     torch.cuda.empty_cache()
 
 
-train_throughput(2, 22, 2.0, "C3-style 2D fit, 2^22 samples/step, L=16 F=2 T=2^19 growth 2.0, tcgen05 head, full training step")
+def c3_gigapixel(steps=30):
+    """BASELINE configs[2] as written: fit_image on the 32768 x 32768 procedural test image, 2^22 samples per step, the pixel
+    targets evaluated where they are drawn (sxen_sample_test_image_batch: the image would be 26 GB as doubles); L=16 F=2 T=2^19
+    base 16 growth 2.0, tcgen05 head.  Wall clock per step includes the sampler; PSNR over the first 2^22 pixels."""
+    cfg = sx.EncoderConfig(dim=2, levels=16, table_size=1 << 19, features=2, base_resolution=16, growth=2.0)
+    N = 1 << 22
+    sampler = sx.test_image_sampler(32768, 32768, 7, 1234)
+    coords, targets = sampler(0, N)
+    torch.cuda.synchronize()
+    t0 = time.time()
+    for k in range(4):
+        sampler(k, N)
+    torch.cuda.synchronize()
+    sample_ms = (time.time() - t0) / 4 * 1e3
+    for attempt in range(2):
+        t0 = time.time()
+        r = sx.fit_test_image(32768, 32768, 7, cfg, sx.TrainConfig(batch_size=N, steps=steps, record_every=1),
+                              sx.FitImageOptions(mlp_precision=1), psnr_pixels=1 << 22)
+        dt = time.time() - t0
+    loss = [v for _, v in r.train.loss_curve]
+    print(json.dumps({"config": "C3 as written: 32768 x 32768 procedural image, 2^22 samples/step, L=16 F=2 T=2^19 growth 2.0, "
+                                "tcgen05 head, fit_image end to end", "steps": steps, "samples_per_step": N,
+                      "seconds_incl_setup_and_final_render": dt, "sampler_ms_per_step": sample_ms,
+                      "ms_per_step_incl_sampler": dt / steps * 1e3, "samples_per_s_incl_sampler": N * steps / dt,
+                      "loss_first": loss[0], "loss_last": loss[-1], "psnr_first_2^22_pixels": r.final_psnr}), flush=True)
+
+
+c3_gigapixel()
+train_throughput(2, 22, 2.0, "C3-style 2D fit, 2^22 samples/step, L=16 F=2 T=2^19 growth 2.0, tcgen05 head, full training step (repeated batch)")
 train_throughput(3, 24, 1.5, "C4-style 3D encode + fused 64-wide MLP, 2^24 samples/step, L=16 F=2 T=2^19, full training step")

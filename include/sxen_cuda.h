@@ -420,6 +420,15 @@ SXEN_API sxen_status sxen_comm_info(const sxen_comm* comm, int32_t* world, int32
 /* In-place SUM over the ranks of count elements (type: SXEN_COORD_F32 / SXEN_COORD_F64 / SXEN_ELEM_I64), stream-ordered. */
 SXEN_API sxen_status sxen_comm_allreduce(sxen_comm* comm, void* buf_dev, size_t count, sxen_coord_type type, void* stream);
 
+/* run_chunk as ONE kernel (csrc/sxen_train_fused.cu): gather warps encode the next tile straight into the tensor cores'
+ * operand tile, the tcgen05 head runs, scatter warps take d loss / d encoding out of TMEM into encode_backward -- no feature or
+ * gradient array in HBM.  Covers the simplex backend, F = 2, 16 levels, dim 2 or 3, head 32 -> 64 -> 64 -> <= 3 on the tensor
+ * cores, no aux inputs, default accumulation.  mode 0 (default) = the three separate kernels -- measured faster: one CTA per SM
+ * cannot hold enough warps to hide the lattice walk's latency next to the head's epilogue registers --,
+ * 1 = the fused kernel or SXEN_INVALID_ARGUMENT, -1 = fused whenever the shapes allow.  Used by sxen_trainer_accumulate /
+ * _step / _step_enqueue. */
+SXEN_API sxen_status sxen_trainer_set_fused(sxen_trainer* trainer, int32_t mode);
+
 /* Bit-reproducible training steps (opt-in): sxen_grad_set_reproducible on the trainer's accumulator, sxen_mlp_set_reproducible
  * on its MLP, and -- with the exact head -- d(loss)/d(encoding) handed to encode_backward as doubles.  Two runs of the same
  * steps then produce the same bits, on one GPU or sharded (the exchange sums the fixed-point words). */

@@ -164,6 +164,7 @@ SIGNATURES = {
     "sxen_grad_download_f64": (C.c_int, [_vp, _i32, _P(_dbl)]),
     "sxen_mlp_set_reproducible": (C.c_int, [_vp, _i32]),
     "sxen_trainer_set_reproducible": (C.c_int, [_vp, _i32]),
+    "sxen_trainer_set_fused": (C.c_int, [_vp, _i32]),
     "sxen_sample_test_image_batch": (C.c_int, [_u64, _i32, _i32, _u64, _u64, _sz, _sz, _vp, _vp, _vp]),
     "sxen_test_image_sq_error": (C.c_int, [_u64, _i32, _i32, _vp, _sz, _sz, _vp, _vp]),
     "sxen_comm_unique_id": (C.c_int, [_vp]),

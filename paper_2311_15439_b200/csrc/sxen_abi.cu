@@ -426,6 +426,38 @@ sxen_status sxen_encoder_encode_backward_strided64(sxen_encoder* enc, const void
                     first_level, level_count, row_stride, upstream64_dev);
 }
 
+sxen_status sxen_encoder_fused_args(sxen_encoder* enc, sxen_grad* grad, const void* x_dev, sxen_coord_type type, size_t n_samples,
+                                    EncodeArgs* out) {
+  if (sxen_status st = check_batch(enc, x_dev, type, n_samples)) return st;
+  SXEN_REQUIRE(grad != nullptr && out != nullptr, "null argument");
+  SXEN_REQUIRE(grad->levels == enc->cfg.levels && grad->features == enc->cfg.features && grad->table_size == enc->cfg.table_size &&
+                   grad->device == enc->device,
+               "encode_backward: gradient accumulator shape mismatch");
+  SXEN_REQUIRE(enc->cfg.levels <= sxen_dev::kMaxLaunchLevels, "fused step: more than %d levels", sxen_dev::kMaxLaunchLevels);
+  EncodeArgs& a = *out;
+  base_args(enc, x_dev, type, n_samples, a);
+  a.grads = grad->values;
+  level_chunk(enc, grad, 0, enc->cfg.levels, n_samples, a);
+  a.merge_pairs = (enc->tuning.merge_pairs > 0 && enc->cfg.table_size >= 2) ? 1 : 0;
+  // gathers and reds share L2 as in the fused encode launch: gradient lines evict_first (profiles/r1_cache_hints.log)
+  a.cache_hints = enc->tuning.cache_hints >= 0 ? enc->tuning.cache_hints : 8;
+  return SXEN_OK;
+}
+
+sxen_status sxen_encoder_fused_finish(sxen_encoder* enc, const EncodeArgs& a, void* stream) {
+  if (a.coarse != nullptr) {
+    bool any = false;
+    for (int l = 0; l < a.n_levels; ++l) any = any || a.cg.shift[l] >= 0;
+    if (any) {
+      SXEN_CUDA(kFold[enc->cfg.dim - 1](a, as_stream(stream)));
+      count_launch();
+    }
+  }
+  enc->touched += static_cast<uint64_t>(a.n_samples) * static_cast<uint64_t>(enc->cfg.levels) *
+                  static_cast<uint64_t>(enc->vertices()) * 2u;  // the forward walk and the backward walk (src/encoding.cpp:222,241)
+  return SXEN_OK;
+}
+
 // SparseAdamState::step for the single-GPU trainer (declared in sxen_common.hpp): when the batch is small against the
 // tables, the update walks the batch (sparse_adam_walk_kernel) instead of scanning all L*T accumulator rows.  The caller
 // guarantees that every touched row of `grad` comes from this batch's backward.  Same arithmetic, same rows, same

@@ -144,3 +144,18 @@ sxen_status sxen_encoder_encode_backward_strided64(sxen_encoder* enc, const void
                                                    const float* upstream_dev, const double* upstream64_dev, int row_stride,
                                                    size_t n_samples, sxen_grad* grad, int first_level, int level_count,
                                                    void* stream);
+
+// ---- the fused training kernel (sxen_train_fused.cu) and what it needs from the encoder (sxen_abi.cu)
+namespace sxen_dev { struct EncodeArgs; }
+bool sxen_train_fused_supported(const sxen_encoder_config& ec, const sxen_mlp_config& mc);
+// fills the argument block of one launch over ALL levels of `enc` for a backward into `grad` (geometry, replicas, policies)
+sxen_status sxen_encoder_fused_args(sxen_encoder* enc, sxen_grad* grad, const void* x_dev, sxen_coord_type type, size_t n_samples,
+                                    sxen_dev::EncodeArgs* out);
+// the coarse-level fold of that launch + the encoder's touched counter (forward + backward walks)
+sxen_status sxen_encoder_fused_finish(sxen_encoder* enc, const sxen_dev::EncodeArgs& args, void* stream);
+sxen_status sxen_train_fused_run(const sxen_dev::EncodeArgs& e, int dim, const float* params, const void* targets, int target_f32,
+                                 double* mlp_grad, double* loss_sum, long long* grad_fixed, int out_w, size_t global_batch,
+                                 int precise, cudaStream_t stream, int* used_ctas);
+// sxen_mlp.cu: the pieces of an Mlp handle the fused kernel works on, and the fold of its reproducible partials
+extern "C" sxen_status sxen_mlp_fused_view(sxen_mlp* mlp, float** params, double** grads, long long** grads_fixed, int32_t* precision);
+extern "C" sxen_status sxen_mlp_fused_fold(sxen_mlp* mlp, double* loss_sum_dev, int ctas, void* stream);

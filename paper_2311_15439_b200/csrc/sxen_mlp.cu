@@ -585,6 +585,30 @@ sxen_status sxen_mlp_backward(sxen_mlp* mlp, const double* upstream_dev, size_t 
   return SXEN_OK;
 }
 
+sxen_status sxen_mlp_fused_view(sxen_mlp* mlp, float** params, double** grads, long long** grads_fixed, int32_t* precision) {
+  SXEN_REQUIRE(mlp != nullptr, "mlp handle is null");
+  *params = mlp->params;
+  *grads = mlp->grads;
+  *grads_fixed = mlp->grads_fixed;
+  *precision = mlp->precision;
+  if (!mlp->loss_scratch) {
+    DeviceGuard guard(mlp->device);
+    SXEN_CUDA(cudaMalloc(&mlp->loss_scratch, sizeof(double)));
+  }
+  mlp->forward_done = false;  // no activations are kept: a separate Mlp::backward would be a logic error
+  return SXEN_OK;
+}
+
+sxen_status sxen_mlp_fused_fold(sxen_mlp* mlp, double* loss_sum_dev, int ctas, void* stream) {
+  if (!mlp->grads_fixed) return SXEN_OK;
+  cudaStream_t st = as_stream(stream);
+  fold_fixed_kernel<<<grid_for(mlp->param_count), 256, 0, st>>>(mlp->grads, mlp->grads_fixed, mlp->param_count);
+  sum_parts_kernel<<<1, 1, 0, st>>>(loss_sum_dev, reinterpret_cast<const double*>(mlp->grads_fixed + mlp->param_count), ctas);
+  SXEN_CUDA(cudaGetLastError());
+  count_launch(2);
+  return SXEN_OK;
+}
+
 sxen_status sxen_mlp_set_reproducible(sxen_mlp* mlp, int32_t on) {
   SXEN_REQUIRE(mlp != nullptr, "mlp handle is null");
   DeviceGuard guard(mlp->device);

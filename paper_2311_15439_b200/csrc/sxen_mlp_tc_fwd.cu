@@ -1,24 +1,15 @@
-// sxen_mlp_tc.cu -- the {16|32} -> 64 -> 64 -> {<=3} MLP head on 5th-generation tensor cores (tcgen05 + TMEM), fully fused:
-// forward, MSE loss + upstream, input gradients and weight gradients of one 128-sample tile never leave the SM.
+// sxen_mlp_tc_fwd.cu -- Mlp::forward on the tensor cores (inference: render_image, hold-out evaluation), one epilogue <-> MMA
+// hand-off per 128-sample tile.  Reference semantics: /root/reference/proj/src/mlp.cpp:137-162; numerics as sxen_mlp_tc.cu
+// (split-bf16 GEMMs, fp32 accumulation in TMEM).
 //
-// Reference semantics: Mlp::forward / Mlp::backward and run_chunk's loss (/root/reference/proj/src/mlp.cpp:137-202,
-// src/trainer.cpp:26-48).  The reference accumulates in fp64; here every GEMM runs as split-bf16 ("bf16x3"):
-// x = hi + lo with hi = bf16(x), lo = bf16(x - hi), D += A_hi*B_hi + A_hi*B_lo + A_lo*B_hi in fp32 TMEM accumulators,
-// i.e. ~16 mantissa bits per operand, relative error ~1e-5 per product (tests state the tolerance).
-// kind::tf32 was not usable: on sm_100a MN-major tf32 operands produce zeros (tools/tc_probe.py), and the weight-gradient
-// GEMMs need the sample dimension as K, i.e. MN-major views of the activation tiles.
-//
-// Layout: all operand tiles are bf16 CM16 tiles (sxen_tc.cuh), self-dual, so ONE activation tile [128 samples][features]
-// is the K-major A operand of the next layer, the K-major A operand of the input-gradient GEMM and the MN-major operand of
-// the weight-gradient GEMM.  Each tile carries one extra 8-column block whose first column is 1.0: used as the B operand of
-// a weight-gradient GEMM it makes the bias gradient fall out as column `in` of the same accumulator.
-// The 64 -> out_w (<= 3) output layer and its input gradient are three dot products per unit: they run on the CUDA cores in
-// fp32 inside the layer-2 epilogue (partial sums of the two column halves meet through shared memory), which removes two
-// tensor-core round trips from the per-tile dependency chain: X0*W0^T | H1*W1^T | dH2*W1 | dH1*W0.
-// One CTA = 128 samples = 128 TMEM lanes, 256 threads: threads t and t+128 share sample t of the tile and split every
-// epilogue's columns in halves (warps w and w+4 read the same TMEM lane quadrant).  The weight-gradient MMAs of a phase are
-// queued behind the phase's dependent-chain MMAs and are only waited for when the tiles they read are about to be rewritten,
-// so they run under the following epilogues.
+// Schedule.  X0 is double-buffered and the layer-1 GEMM of tile k+1 is issued right behind the layer-2 GEMM of tile k, so at
+// the top of a tile ONE wait covers "layer 2 of the previous tile" and "layer 1 of this tile": the epilogue warps turn S1 into
+// the previous tile's predictions, stage the next tile's features, turn S0 into this tile's H1 and hand over -- against two
+// hand-offs per tile in the fused training kernel's forward half (0.145 -> 0.117 ms per 2^20 samples).  The kernel body also
+// carries the matching three-hand-off TRAINING schedule (layer 1 of the next tile issued together with the last backward
+// GEMM, the input gradient leaving through its own TMEM columns); measured, that one loses to sxen_mlp_tc.cu's schedule
+// (0.423 vs 0.391 ms: the wait for the previous tile's weight-gradient MMAs lands on the critical path), so only the forward
+// instantiation is built.
 #include <algorithm>
 
 #include "sxen_mlp_tc_common.cuh"
@@ -32,8 +23,9 @@ namespace {
 // shared-memory map (bytes)
 constexpr uint32_t kW0 = 0;                                     // CM16(64, 32) hi, lo
 constexpr uint32_t kW1 = kW0 + 2 * cm16_bytes(HID, kInMax);     // CM16(64, 64) hi, lo   (regions sized for IN = 32)
-constexpr uint32_t kX0 = kW1 + 2 * cm16_bytes(HID, HID);        // CM16(128, 40) hi, lo
-constexpr uint32_t kH1 = kX0 + 2 * cm16_bytes(kTile, kX0CMax);  // CM16(128, 72) hi, lo
+constexpr uint32_t kX0 = kW1 + 2 * cm16_bytes(HID, HID);        // CM16(128, 40) hi, lo -- TWO buffers, tile parity
+constexpr uint32_t kX0Bytes = 2 * cm16_bytes(kTile, kX0CMax);
+constexpr uint32_t kH1 = kX0 + 2 * kX0Bytes;                    // CM16(128, 72) hi, lo
 constexpr uint32_t kH2 = kH1 + 2 * cm16_bytes(kTile, HC);
 constexpr uint32_t kDY = kH2 + 2 * cm16_bytes(kTile, HC);       // CM16(128, 16) hi, lo
 constexpr uint32_t kDH2 = kDY + 2 * cm16_bytes(kTile, OUTP);    // CM16(128, 64) hi, lo
@@ -44,20 +36,21 @@ constexpr uint32_t kPP = kW2f + 3 * HID * 4;                    // partial predi
 constexpr uint32_t kSmemBytes = kPP + 4 * kTile * 4 * 4;  // pp[kSplit <= 4][128][4]
 
 // TMEM columns (fp32): scratch accumulators (128 lanes) and the persistent weight-gradient accumulators (M = 64)
-constexpr uint32_t tS0 = 0;     // [128 x 64] layer-1 pre-activation, later d(input) (32 cols)
+constexpr uint32_t tS0 = 0;     // [128 x 64] layer-1 pre-activation
 constexpr uint32_t tS1 = 64;    // [128 x 64] layer-2 pre-activation, later dH1
 constexpr uint32_t tG0 = 128;   // [64 x 40]  dW0 | db0
 constexpr uint32_t tG1 = 168;   // [64 x 72]  dW1 | db1
 constexpr uint32_t tG2 = 240;   // [64 x 16]  dW2^T
-constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t tDX = 256;   // [128 x 32] d(input): its own columns, so that the next tile's layer 1 can overwrite S0 at once
+constexpr uint32_t kTmemCols = 512;
 
 template <bool TRAIN, int IN>
 __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_constant__ TcArgs a) {
   static_assert(IN == 16 || IN == 32, "input widths 16 (L=8, F=2: the reference's default encoder) and 32 (L=16, F=2)");
   constexpr int X0C = IN + 8;
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t bar_ready;  // 256 arrivals: the tiles of the next phase are written and the TMEM scratch is drained
-  __shared__ uint64_t bar;        // dependent-chain MMAs of the current phase have completed
+  __shared__ uint64_t bar_ready;  // 256 arrivals: the tiles of the next GEMM group are written and the TMEM scratch is drained
+  __shared__ uint64_t bar;        // the chain warp's GEMMs up to here have completed
   __shared__ uint64_t bar_g;      // every weight-gradient MMA of the tile has completed
   __shared__ uint64_t bar_w;      // chain warp -> weight-gradient warp: the operands of backward phase 2 / 3 are in place
   __shared__ uint32_t tmem_base_slot;
@@ -66,7 +59,7 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
   const int t = tid & (kTile - 1);   // sample row inside the tile
   const int half = (tid >> 7) & (kSplit - 1);  // which slice of an epilogue's columns this thread handles
   const int warp = tid >> 5;
-  const bool is_mma_warp = warp == kEpiThreads / 32;        // issues the four dependent-chain GEMMs of every tile
+  const bool is_mma_warp = warp == kEpiThreads / 32;        // issues the dependent-chain GEMMs of every tile
   const bool is_wgrad_warp = warp == kEpiThreads / 32 + 1;  // issues the three weight-gradient GEMMs (TRAIN)
   const bool is_epi = tid < kEpiThreads;
   float* bias = reinterpret_cast<float*>(smem + kBias);
@@ -108,6 +101,7 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
     if (half == 0) {
       float ones[8] = {1.0f, 0, 0, 0, 0, 0, 0, 0};
       store_chunk(smem + kX0, smem + kX0 + loX0, t, IN / 8, X0C, ones);
+      store_chunk(smem + kX0 + kX0Bytes, smem + kX0 + kX0Bytes + loX0, t, IN / 8, X0C, ones);
       store_chunk(smem + kH1, smem + kH1 + loH, t, HID / 8, HC, ones);
       store_chunk(smem + kH2, smem + kH2 + loH, t, HID / 8, HC, ones);
       float zero[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -128,82 +122,90 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
   const uint32_t tb = tmem_base_slot;
   const bool precise = a.precise != 0;
   const unsigned long long n_tiles = (a.n + kTile - 1) / kTile;
-  constexpr int kPhases = TRAIN ? 4 : 2;
   bool g_started = false;
 
+  // Schedule (round 2).  The layer-1 GEMM of tile k+1 is issued TOGETHER with the last GEMM of tile k (its X0 tile sits in the
+  // second buffer, its accumulator S0 has been free since tile k's first epilogue), and the input gradient leaves through
+  // its own TMEM columns (tDX) at the top of the next tile.  A tile therefore costs THREE epilogue <-> MMA round trips
+  //     [S0 -> H1] -> H1*W1^T | [S1 -> H2, output layer, loss, dH2] -> dH2*W1 | [S1 -> dH1] -> dH1*W0 + X0'*W0^T
+  // where the round-1 kernel paid five (0.41 ms per 2^20 samples, 53 % of its warp-stall samples in the hand-offs);
+  // forward only: one round trip per tile instead of two.
   if (is_mma_warp) {
-    // =========================== MMA warp: one lane issues every tcgen05.mma of the CTA ===========================
+    // =========================== MMA warp: one lane issues every chain tcgen05.mma of the CTA ===========================
     if ((tid & 31) == 0) {
       const uint32_t sW0 = smem_u32(smem + kW0), sW1 = smem_u32(smem + kW1);
-      const uint32_t sX0 = smem_u32(smem + kX0), sH1 = smem_u32(smem + kH1), sH2 = smem_u32(smem + kH2);
-      const uint32_t sDY = smem_u32(smem + kDY), sDH2 = smem_u32(smem + kDH2), sDH1 = smem_u32(smem + kDH1);
+      const uint32_t sH1 = smem_u32(smem + kH1), sDH2 = smem_u32(smem + kDH2), sDH1 = smem_u32(smem + kDH1);
       // K-major views step 256 B per UMMA_K = 16; MN-major views step two 8-row groups
-      const uint64_t kX0d = desc16_k_major(sX0, X0C, 0), kH1d = desc16_k_major(sH1, HC, 0);
+      const uint64_t kH1d = desc16_k_major(sH1, HC, 0);
       const uint64_t kW0d = desc16_k_major(sW0, IN, 0), kW1d = desc16_k_major(sW1, HID, 0);
       const uint64_t kDH2d = desc16_k_major(sDH2, HID, 0), kDH1d = desc16_k_major(sDH1, HID, 0);
       const uint64_t mW0d = desc16_mn_major(sW0, IN, 0), mW1d = desc16_mn_major(sW1, HID, 0);
-      const uint64_t mX0d = desc16_mn_major(sX0, X0C, 0), mH1d = desc16_mn_major(sH1, HC, 0), mH2d = desc16_mn_major(sH2, HC, 0);
-      const uint64_t mDYd = desc16_mn_major(sDY, OUTP, 0), mDH2d = desc16_mn_major(sDH2, HID, 0), mDH1d = desc16_mn_major(sDH1, HID, 0);
       constexpr uint32_t kStep = 256;
+      auto layer1 = [&](int b) {  // S0 = X0[b] * W0^T
+        const uint64_t kX0d = desc16_k_major(smem_u32(smem + kX0 + b * kX0Bytes), X0C, 0);
+        gemm_split(tb + tS0, make_idesc_bf16(128, HID, false, false), IN / 16, false, precise, kX0d, loX0, kStep, kW0d, loW0, kStep);
+      };
       uint32_t ph = 0;
-      for (unsigned long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        for (int p = 0; p < kPhases; ++p) {
-          mbar_wait(&bar_ready, ph, 0x100u + static_cast<uint32_t>(p), a.progress);
-          ph ^= 1;
-          tc_fence_after();
-          if (p >= 2) mbar_arrive(&bar_w);  // hand the phase to the weight-gradient warp (its private two-phase barrier)
-          switch (p) {
-            case 0:  // layer 1: S0 = X0 * W0^T
-              gemm_split(tb + tS0, make_idesc_bf16(128, HID, false, false), IN / 16, false, precise, kX0d, loX0, kStep, kW0d, loW0, kStep);
-              tc_commit(&bar);
-              break;
-            case 1:  // layer 2: S1 = H1 * W1^T
-              gemm_split(tb + tS1, make_idesc_bf16(128, HID, false, false), HID / 16, false, precise, kH1d, loH, kStep, kW1d, loW1, kStep);
-              tc_commit(&bar);
-              break;
-            case 2:  // S1 = dH2 * W1
-              gemm_split(tb + tS1, make_idesc_bf16(128, HID, false, true), HID / 16, false, precise, kDH2d, loDH, kStep, mW1d, loW1,
-                         2 * cm16_row_group_stride(HID));
-              tc_commit(&bar);
-              break;
-            default:  // S0[:, 0:32] = dH1 * W0 (d loss / d encoding)
-              gemm_split(tb + tS0, make_idesc_bf16(128, IN, false, true), HID / 16, false, precise, kDH1d, loDH, kStep, mW0d, loW0,
-                         2 * cm16_row_group_stride(IN));
-              tc_commit(&bar);
-              break;
-          }
+      auto wait_ready = [&]() {
+        mbar_wait(&bar_ready, ph, 0x100u + static_cast<uint32_t>(ph), a.progress);
+        ph ^= 1;
+        tc_fence_after();
+      };
+      if (blockIdx.x < n_tiles) {
+        wait_ready();  // the first tile's X0
+        layer1(0);
+        tc_commit(&bar);
+      }
+      int k = 0;
+      for (unsigned long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
+        const bool has_next = tile + gridDim.x < n_tiles;
+        wait_ready();  // layer 2: S1 = H1 * W1^T
+        gemm_split(tb + tS1, make_idesc_bf16(128, HID, false, false), HID / 16, false, precise, kH1d, loH, kStep, kW1d, loW1, kStep);
+        if constexpr (!TRAIN) {
+          if (has_next) layer1((k + 1) & 1);
+          tc_commit(&bar);
+        } else {
+          tc_commit(&bar);
+          wait_ready();  // S1 = dH2 * W1
+          mbar_arrive(&bar_w);
+          gemm_split(tb + tS1, make_idesc_bf16(128, HID, false, true), HID / 16, false, precise, kDH2d, loDH, kStep, mW1d, loW1,
+                     2 * cm16_row_group_stride(HID));
+          tc_commit(&bar);
+          wait_ready();  // tDX = dH1 * W0 (d loss / d encoding), and the next tile's layer 1 right behind it
+          mbar_arrive(&bar_w);
+          gemm_split(tb + tDX, make_idesc_bf16(128, IN, false, true), HID / 16, false, precise, kDH1d, loDH, kStep, mW0d, loW0,
+                     2 * cm16_row_group_stride(IN));
+          if (has_next) layer1((k + 1) & 1);
+          tc_commit(&bar);
         }
       }
     }
   } else if (is_wgrad_warp) {
     // ============ weight-gradient warp: its own lane issues G2, G1 (phase 2) and G0 (phase 3) of every tile ============
-    // A single issuing thread spends ~35 cycles per tcgen05.mma; the 72 weight-gradient MMAs of a tile would otherwise
-    // sit in front of the next phase's chain MMAs in that thread's program order.  Issued from here they reach the tensor
-    // pipe whenever this lane gets to them, and tcgen05.commit on bar_g tracks exactly this thread's MMAs.
     if constexpr (TRAIN) {
       if ((tid & 31) == 0) {
-        const uint32_t sX0 = smem_u32(smem + kX0), sH1 = smem_u32(smem + kH1), sH2 = smem_u32(smem + kH2);
+        const uint32_t sH1 = smem_u32(smem + kH1), sH2 = smem_u32(smem + kH2);
         const uint32_t sDY = smem_u32(smem + kDY), sDH2 = smem_u32(smem + kDH2), sDH1 = smem_u32(smem + kDH1);
-        const uint64_t mX0d = desc16_mn_major(sX0, X0C, 0), mH1d = desc16_mn_major(sH1, HC, 0), mH2d = desc16_mn_major(sH2, HC, 0);
+        const uint64_t mH1d = desc16_mn_major(sH1, HC, 0), mH2d = desc16_mn_major(sH2, HC, 0);
         const uint64_t mDYd = desc16_mn_major(sDY, OUTP, 0), mDH2d = desc16_mn_major(sDH2, HID, 0), mDH1d = desc16_mn_major(sDH1, HID, 0);
         uint32_t phw = 0;
-        for (unsigned long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-          for (int p = 2; p < kPhases; ++p) {
-            mbar_wait(&bar_w, phw, 0x200u + static_cast<uint32_t>(p), a.progress);  // the chain warp has seen this phase's operands
-            phw ^= 1;
-            tc_fence_after();
-            if (p == 2) {  // G2 += H2^T * dY (dW2^T);  G1 += dH2^T * [H1 | 1]
-              gemm_split(tb + tG2, make_idesc_bf16(64, OUTP, true, true), kTile / 16, g_started, precise, mH2d, loH,
-                         2 * cm16_row_group_stride(HC), mDYd, loDY, 2 * cm16_row_group_stride(OUTP));
-              gemm_split(tb + tG1, make_idesc_bf16(64, HC, true, true), kTile / 16, g_started, precise, mDH2d, loDH,
-                         2 * cm16_row_group_stride(HID), mH1d, loH, 2 * cm16_row_group_stride(HC));
-            } else {       // G0 += dH1^T * [X0 | 1]
-              gemm_split(tb + tG0, make_idesc_bf16(64, X0C, true, true), kTile / 16, g_started, precise, mDH1d, loDH,
-                         2 * cm16_row_group_stride(HID), mX0d, loX0, 2 * cm16_row_group_stride(X0C));
-              tc_commit(&bar_g);  // covers G2, G1 and G0 of this tile
-              g_started = true;
-            }
-          }
+        int k = 0;
+        for (unsigned long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
+          mbar_wait(&bar_w, phw, 0x200u, a.progress);  // G2 += H2^T * dY (dW2^T);  G1 += dH2^T * [H1 | 1]
+          phw ^= 1;
+          tc_fence_after();
+          gemm_split(tb + tG2, make_idesc_bf16(64, OUTP, true, true), kTile / 16, g_started, precise, mH2d, loH,
+                     2 * cm16_row_group_stride(HC), mDYd, loDY, 2 * cm16_row_group_stride(OUTP));
+          gemm_split(tb + tG1, make_idesc_bf16(64, HC, true, true), kTile / 16, g_started, precise, mDH2d, loDH,
+                     2 * cm16_row_group_stride(HID), mH1d, loH, 2 * cm16_row_group_stride(HC));
+          mbar_wait(&bar_w, phw, 0x201u, a.progress);  // G0 += dH1^T * [X0 | 1]
+          phw ^= 1;
+          tc_fence_after();
+          const uint64_t mX0d = desc16_mn_major(smem_u32(smem + kX0 + (k & 1) * kX0Bytes), X0C, 0);
+          gemm_split(tb + tG0, make_idesc_bf16(64, X0C, true, true), kTile / 16, g_started, precise, mDH1d, loDH,
+                     2 * cm16_row_group_stride(HID), mX0d, loX0, 2 * cm16_row_group_stride(X0C));
+          tc_commit(&bar_g);  // covers G2, G1 and G0 of this tile
+          g_started = true;
         }
       }
     }
@@ -214,21 +216,19 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
     double loss_acc = 0.0;
     double db2_acc[3] = {0.0, 0.0, 0.0};
 
-    // hidden-layer epilogue: 32 columns of this thread's row out of a TMEM accumulator -> (bias, ReLU | mask) -> hi/lo tile
     auto ready = [&]() {
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(&bar_ready);
     };
     auto wait_chain = [&]() {
-      mbar_wait(&bar, phase, 0x300u, a.progress);
+      mbar_wait(&bar, phase, 0x300u + static_cast<uint32_t>(phase), a.progress);
       phase ^= 1;
       tc_fence_after();
     };
 
-    // Software pipeline over tiles: the features of tile i+1 are requested right after tile i's have been written to
-    // shared memory, and a tile's targets at its top, so neither global-load latency sits on the per-tile dependency chain
-    // (ncu stall sampling had 9 % of the samples waiting on the feature loads and 5 % on the target loads).
+    // Software pipeline over tiles: a tile's features are requested a tile ahead (registers) and written into the X0
+    // buffer of its parity while the previous tile's backward GEMMs run.
     constexpr int kXCh = IN / 8;                             // 8-float chunks per feature row
     constexpr int kXIt = (kTile * kXCh) / kEpiThreads;       // chunks per thread
     constexpr int kXRows = kEpiThreads / 8 / kXCh;           // 8-row groups one pass of all epilogue threads covers
@@ -251,16 +251,79 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
         }
       }
     };
+    // Lane mapping of the staging: 8 rows x 4 chunks per warp instruction keeps both the global reads (64 contiguous bytes
+    // per row) and the shared stores (8 rows = 8 distinct 16-byte bank groups) efficient.
+    auto stage_features = [&](int b) {
+#pragma unroll
+      for (int it = 0; it < kXIt; ++it)
+        store_chunk(smem + kX0 + b * kX0Bytes, smem + kX0 + b * kX0Bytes + loX0, xrow + 8 * kXRows * it, xch, X0C, xin[it]);
+    };
+    // d loss / d encoding of one tile: tDX -> global memory
+    auto store_input_grad = [&](unsigned long long tile_index) {
+      if (half < IN / 16) {
+        uint32_t r[16];
+        tmem_ld16_nowait(tb + lane_base + tDX + 16 * half, r);
+        tmem_ld_wait();
+        const unsigned long long smp = tile_index * kTile + t;
+        if (smp < a.n) {
+          float4* dst = reinterpret_cast<float4*>(a.input_grad + smp * IN + 16 * half);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            __stcs(dst + q, make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
+                                        __uint_as_float(r[4 * q + 3])));
+        }
+      }
+    };
+    // layer-2 epilogue of one tile, forward only: S1 -> ReLU -> output layer -> predictions
+    auto forward_out = [&](unsigned long long tile_index) {
+      uint32_t r[CPT / 16][16];
+#pragma unroll
+      for (int q = 0; q < CPT / 16; ++q) tmem_ld16_nowait(tb + lane_base + tS1 + CPT * half + 16 * q, r[q]);
+      tmem_ld_wait();
+      float p0 = 0.0f, p1 = 0.0f, p2 = 0.0f;
+#pragma unroll
+      for (int q = 0; q < CPT / 16; ++q) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int c = CPT * half + 16 * q + i;
+          float x = __uint_as_float(r[q][i]) + bias[HID + c];
+          x = x > 0.0f ? x : 0.0f;
+          p0 = __fmaf_rn(w2f[c], x, p0);
+          p1 = __fmaf_rn(w2f[HID + c], x, p1);
+          p2 = __fmaf_rn(w2f[2 * HID + c], x, p2);
+        }
+      }
+      *reinterpret_cast<float4*>(pp + (half * kTile + t) * 4) = make_float4(p0, p1, p2, 0.0f);
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+      if (half == 0) {
+        float pr[3] = {bias[2 * HID], bias[2 * HID + 1], bias[2 * HID + 2]};
+#pragma unroll
+        for (int k = 0; k < kSplit; ++k) {
+          const float4 pk = *reinterpret_cast<const float4*>(pp + (k * kTile + t) * 4);
+          pr[0] += pk.x;
+          pr[1] += pk.y;
+          pr[2] += pk.z;
+        }
+        const unsigned long long smp = tile_index * kTile + t;
+        if (smp < a.n && a.pred)
+          for (int o = 0; o < a.out_w && o < 3; ++o) a.pred[smp * a.out_w + o] = pr[o];
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");  // pp is rewritten by the next tile
+    };
+
     load_features(blockIdx.x);
+    if (blockIdx.x < n_tiles) {
+      stage_features(0);
+      ready();
+    }
+    load_features(static_cast<unsigned long long>(blockIdx.x) + gridDim.x);
 
-    for (unsigned long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const unsigned long long s0 = tile * kTile;
-      const unsigned long long smp = s0 + t;
+    int k = 0;
+    unsigned long long prev_tile = 0;
+    for (unsigned long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
+      const unsigned long long smp = tile * kTile + t;
       const bool valid = smp < a.n;
-
-      // ---- stage 0: features -> X0 tiles.  Lane mapping: 8 rows x 4 chunks per warp instruction keeps both the global
-      // reads (64 contiguous bytes per row) and the shared stores (8 rows = 8 distinct 16-byte bank groups) efficient.
-      // The previous tile's weight-gradient MMAs still read X0: wait for them before overwriting it.
+      const bool has_next = tile + gridDim.x < n_tiles;
       double tgt[3] = {0.0, 0.0, 0.0};
       if constexpr (TRAIN) {
         if (valid) {
@@ -270,20 +333,24 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
               tgt[o] = a.target_f32 ? static_cast<double>(static_cast<const float*>(a.targets)[smp * a.out_w + o])
                                     : static_cast<const double*>(a.targets)[smp * a.out_w + o];
         }
-        if (g_started) {
+      }
+      // ---- top of the tile: this tile's layer 1 (and the previous tile's last GEMM) have completed
+      wait_chain();
+      if constexpr (TRAIN) {
+        if (k > 0) store_input_grad(prev_tile);
+        if (g_started) {  // the previous tile's weight-gradient MMAs read H1 .. dH1 and its X0 buffer: all free after this
           mbar_wait(&bar_g, phase_g, 0x400u, a.progress);
           phase_g ^= 1;
         }
+      } else {
+        if (k > 0) forward_out(prev_tile);
+        if (has_next) {  // the buffer of the other parity was last read by the previous tile's layer 1: complete
+          stage_features((k + 1) & 1);
+          load_features(tile + 2ull * gridDim.x);
+        }
       }
-#pragma unroll
-      for (int it = 0; it < kXIt; ++it)
-        store_chunk(smem + kX0, smem + kX0 + loX0, xrow + 8 * kXRows * it, xch, X0C, xin[it]);
-      ready();
-      if constexpr (!TRAIN) load_features(tile + gridDim.x);  // in flight under this tile's two phases
-
       // ---- layer 1 epilogue: S0 -> H1
       uint32_t m1 = 0, m2 = 0;  // ReLU masks of this thread's 32 units (bit i = unit 32*half + i active)
-      wait_chain();
       {
         uint32_t r[CPT / 16][16];
 #pragma unroll
@@ -304,6 +371,8 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
         }
       }
       ready();
+      prev_tile = tile;
+      if constexpr (!TRAIN) continue;  // forward only: the layer-2 epilogue runs at the top of the next tile
 
       // ---- layer 2 epilogue: S1 -> H2, then the output layer, the loss and its way back to dH2 on the CUDA cores
       wait_chain();
@@ -337,8 +406,8 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
       {
         float pr[3] = {bias[2 * HID], bias[2 * HID + 1], bias[2 * HID + 2]};
 #pragma unroll
-        for (int k = 0; k < kSplit; ++k) {
-          const float4 pk = *reinterpret_cast<const float4*>(pp + (k * kTile + t) * 4);
+        for (int kk = 0; kk < kSplit; ++kk) {
+          const float4 pk = *reinterpret_cast<const float4*>(pp + (kk * kTile + t) * 4);
           pr[0] += pk.x;
           pr[1] += pk.y;
           pr[2] += pk.z;
@@ -347,22 +416,19 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
         for (int o = 0; o < 3; ++o) {
           if (o < a.out_w) {
             if (half == 0 && valid && a.pred) a.pred[smp * a.out_w + o] = pr[o];
-            if constexpr (TRAIN) {
-              if (valid) {
-                // src/trainer.cpp:38-44: e = pred - target, loss += e*e, upstream = 2e/(B*out_w), all in double
-                const double e = static_cast<double>(pr[o]) - tgt[o];
-                const double up = a.upstream_scale * e;
-                u[o] = static_cast<float>(up);
-                if (half == 0) {
-                  loss_acc += e * e;
-                  db2_acc[o] += up;
-                }
+            if (valid) {
+              // src/trainer.cpp:38-44: e = pred - target, loss += e*e, upstream = 2e/(B*out_w), all in double
+              const double e = static_cast<double>(pr[o]) - tgt[o];
+              const double up = a.upstream_scale * e;
+              u[o] = static_cast<float>(up);
+              if (half == 0) {
+                loss_acc += e * e;
+                db2_acc[o] += up;
               }
             }
           }
         }
       }
-      if constexpr (!TRAIN) continue;  // the tiles and S1 are only rewritten after the next bar_ready rounds
       if (half == 0) store_chunk(smem + kDY, smem + kDY + loDY, t, 0, OUTP, u);  // B operand of G2 = H2^T * dY
       {
         // dH2[c] = sum_o u[o] * W2[o][c], zero where layer 2's ReLU clamped (src/mlp.cpp:189-199)
@@ -380,7 +446,13 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
         }
       }
       ready();
-
+      // ---- in the shadow of dH2*W1: the NEXT tile's features into the X0 buffer of its parity (last read by the layer 1 and
+      // the weight-gradient GEMM of the tile before this one: both complete, see the waits at the top), and the request for
+      // the tile after that
+      if (has_next) {
+        stage_features((k + 1) & 1);
+        load_features(tile + 2ull * gridDim.x);
+      }
       // ---- backward epilogue of layer 2: S1 -> dH1 (masked by layer 1's ReLU)
       wait_chain();
       {
@@ -397,26 +469,16 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
           store_chunk(smem + kDH1, smem + kDH1 + loDH, t, (CPT / 8) * half + 2 * q + 1, HID, v + 8);
         }
       }
-      ready();
-
-      // ---- backward epilogue of layer 1: S0[:, 0:32] -> d loss / d encoding, straight to global memory
-      load_features(tile + gridDim.x);  // in flight under the last phase (earlier, the loads only hold scoreboards)
-      wait_chain();
-      if (half < IN / 16) {
-        uint32_t r[16];
-        tmem_ld16_nowait(tb + lane_base + tS0 + 16 * half, r);
-        tmem_ld_wait();
-        if (valid) {
-          float4* dst = reinterpret_cast<float4*>(a.input_grad + smp * IN + 16 * half);
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            __stcs(dst + q, make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
-                                        __uint_as_float(r[4 * q + 3])));
-        }
-      }
-      tc_fence_before();
+      ready();  // -> dH1*W0 into tDX, G0, and the next tile's layer 1
       g_started = true;
     }
+    // ---- the last tile's results
+    if (k > 0) {
+      wait_chain();
+      if constexpr (TRAIN) store_input_grad(prev_tile);
+      else forward_out(prev_tile);
+    }
+    tc_fence_before();
 
     if constexpr (TRAIN) {
       // ---- weight gradients out of TMEM.  An M = 64 accumulator keeps row i in lane (i/16)*32 + i%16 (tools/tc_probe.py),
@@ -464,10 +526,10 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
       // loss and output-bias gradient: per-thread fp64 partials -> warp shuffle -> one atomic per CTA (below)
       double part[4] = {loss_acc, db2_acc[0], db2_acc[1], db2_acc[2]};
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        for (int o = 16; o > 0; o >>= 1) part[k] += __shfl_down_sync(0xffffffffu, part[k], o);
+      for (int kk = 0; kk < 4; ++kk)
+        for (int o = 16; o > 0; o >>= 1) part[kk] += __shfl_down_sync(0xffffffffu, part[kk], o);
       if (lane == 0)
-        for (int k = 0; k < 4; ++k) red_buf[warp][k] = part[k];
+        for (int kk = 0; kk < 4; ++kk) red_buf[warp][kk] = part[kk];
     }
   }
 
@@ -477,7 +539,7 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
     if (tid == 0) {
       double tot[4] = {0, 0, 0, 0};
       for (int w = 0; w < kEpiThreads / 32; ++w)
-        for (int k = 0; k < 4; ++k) tot[k] += red_buf[w][k];
+        for (int kk = 0; kk < 4; ++kk) tot[kk] += red_buf[w][kk];
       const size_t gb2 = HID * IN + HID + HID * HID + HID + a.out_w * HID;
       const size_t n_params = gb2 + a.out_w;
       // reproducible mode: the CTAs' loss partials (not bounded like a gradient, so not fixed point) go to one slot per CTA
@@ -492,53 +554,18 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
 
 }  // namespace
 
-// Diagnostics: host-mapped words the kernels' mbarrier watchdog writes before it traps (wait id, CTA); nullptr = off.
-static volatile unsigned int* g_tc_progress = nullptr;
-extern "C" SXEN_API sxen_status sxen_debug_tc_progress(unsigned int* mapped_host_words) {
-  g_tc_progress = mapped_host_words;
-  return SXEN_OK;
-}
-sxen_status sxen_mlp_tc_forward_launch(const sxen_mlp_tc::TcArgs& a, int in_w, cudaStream_t stream, int* used_ctas);  // sxen_mlp_tc_fwd.cu
-
-// Internal entry points used by sxen_mlp.cu / sxen_trainer.cu (declared there).
-bool sxen_mlp_tc_supported(const sxen_mlp_config& c) {
-  return (c.input_width == 16 || c.input_width == 32) && c.hidden_width == HID && c.hidden_layers == 2 && c.output_width >= 1 && c.output_width <= 3;
-}
-
-sxen_status sxen_mlp_tc_run(bool train, const float* params, const float* features, const void* targets, int target_f32,
-                            float* pred, float* input_grad, double* mlp_grad, double* loss_sum, size_t n, int in_w, int out_w,
-                            size_t global_batch, int precise, cudaStream_t stream, long long* grad_fixed, int* used_ctas) {
-  if (n == 0) return SXEN_OK;
-  if (in_w != 16 && in_w != 32) return fail(SXEN_INVALID_ARGUMENT, "mlp (tensor cores): input width %d not instantiated", in_w);
-  TcArgs a{};
-  a.params = params;
-  a.features = features;
-  a.targets = targets;
-  a.pred = pred;
-  a.input_grad = input_grad;
-  a.mlp_grad = mlp_grad;
-  a.loss_sum = loss_sum;
-  a.grad_fixed = train ? grad_fixed : nullptr;
-  a.n = n;
-  a.out_w = out_w;
-  a.target_f32 = target_f32;
-  a.precise = precise;
-  a.upstream_scale = 2.0 / static_cast<double>(global_batch * static_cast<size_t>(out_w));  // src/trainer.cpp:26-27
-  a.progress = g_tc_progress;
-  if (!train) return sxen_mlp_tc_forward_launch(a, in_w, stream, used_ctas);  // its own kernel: one hand-off per tile
+sxen_status sxen_mlp_tc_forward_launch(const TcArgs& a, int in_w, cudaStream_t stream, int* used_ctas) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned long long tiles = (n + kTile - 1) / kTile;
+  const unsigned long long tiles = (a.n + kTile - 1) / kTile;
   const unsigned grid = static_cast<unsigned>(std::min<unsigned long long>(tiles, static_cast<unsigned long long>(sms)));
   auto launch = [&](auto kernel) -> sxen_status {
     SXEN_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)));
     kernel<<<grid, kThreadsAll, kSmemBytes, stream>>>(a);
     return SXEN_OK;
   };
-  sxen_status st;
-  st = in_w == 32 ? launch(mlp_tc_kernel<true, 32>) : launch(mlp_tc_kernel<true, 16>);
-  if (st != SXEN_OK) return st;
+  if (sxen_status st = in_w == 32 ? launch(mlp_tc_kernel<false, 32>) : launch(mlp_tc_kernel<false, 16>)) return st;
   SXEN_CUDA(cudaGetLastError());
   count_launch();
   if (used_ctas) *used_ctas = static_cast<int>(grid);

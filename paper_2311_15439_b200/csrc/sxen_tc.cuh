@@ -141,16 +141,35 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+// Waits for the phase of `bar` with the given parity to complete.  A hand-off bug between warp roles shows up as a wait that
+// never ends; a hung kernel takes the GPU with it, so the wait carries a watchdog: after ~2 s (4e9 cycles) it traps -- the
+// host sees a CUDA error instead of a hang -- after noting which wait gave up in `dbg` (host-mapped words, may be null):
+// dbg[0] = id, dbg[1] = blockIdx.x.
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "WAIT_LOOP:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@p bra WAIT_DONE;\n\t"
-      "bra WAIT_LOOP;\n\t"
-      "WAIT_DONE:\n\t}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+  return done != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32_t id = 0, volatile unsigned int* dbg = nullptr) {
+  if (mbar_try_wait(bar, parity)) return;
+  const long long t0 = clock64();
+  uint32_t spins = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if ((++spins & 0x3ffu) == 0u && clock64() - t0 > 4000000000ll) {
+      if (dbg != nullptr) {
+        dbg[0] = id;
+        dbg[1] = blockIdx.x;
+        __threadfence_system();
+      }
+      __trap();
+    }
+  }
 }
 
 // TMEM -> registers: this warp's 32 lanes x 16 consecutive columns (thread = lane = accumulator row).

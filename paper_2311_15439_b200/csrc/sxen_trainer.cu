@@ -6,8 +6,10 @@
 // (the reference merges its workers' accumulators at exactly that point, :125-128).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "sxen_common.hpp"
+#include "sxen_encode.cuh"
 
 using namespace sxen_host;
 
@@ -23,6 +25,8 @@ struct sxen_trainer {
   float* features = nullptr;     // N x L*F
   float* input_grad = nullptr;   // N x L*F
   double* input_grad64 = nullptr; // N x L*F, reproducible mode with the exact head: the same gradient as doubles
+  int fused_mode = 0;            // sxen_trainer_set_fused: 0 = three kernels (default: they are faster), 1 = the fused
+                                 // kernel (error if the shapes do not allow it), -1 = fused whenever the shapes allow
   bool reproducible = false;
   bool have_grad64 = false;      // the last accumulate_head filled input_grad64
   double* upstream = nullptr;    // N x out_w
@@ -277,11 +281,61 @@ sxen_status sxen_trainer_accumulate_tables(sxen_trainer* t, const void* coords_d
                                                 n_samples, t->grad, first_level, level_count, stream);
 }
 
+// run_chunk as ONE kernel (sxen_train_fused.cu) when the shapes allow: simplex, F = 2, 16 levels, n in {2, 3}, the tensor-core
+// head 32 -> 64 -> 64 -> <= 3, no aux inputs, default (fp32-atomic) table accumulation.  SXEN_FUSED_TRAIN=0 keeps the three
+// kernels (a measuring aid).
+static bool fused_step_applies(const sxen_trainer* t) {
+  static const bool enabled = [] {
+    const char* env = std::getenv("SXEN_FUSED_TRAIN");
+    return env == nullptr || std::atoi(env) != 0;
+  }();
+  if (!enabled || t->fused_mode == 0 || t->aux_dims != 0 || t->grad->fixed != nullptr) return false;
+  int32_t precision = SXEN_MLP_EXACT;
+  sxen_mlp_get_precision(t->mlp, &precision);
+  if (precision == SXEN_MLP_EXACT) return false;
+  sxen_encoder_config ec;
+  sxen_encoder_get_config(t->enc, &ec);
+  sxen_mlp_config mc;
+  sxen_mlp_get_config(t->mlp, &mc);
+  return sxen_train_fused_supported(ec, mc);
+}
+
+static sxen_status accumulate_fused(sxen_trainer* t, const void* coords_dev, sxen_coord_type coord_type, const void* targets_dev,
+                                    sxen_coord_type target_type, size_t n_samples, size_t global_batch, void* stream) {
+  SXEN_REQUIRE(global_batch >= 1 && n_samples <= global_batch, "train: local chunk (%zu) exceeds the global batch (%zu)",
+               n_samples, global_batch);
+  SXEN_REQUIRE(targets_dev != nullptr, "train: targets pointer is null");
+  DeviceGuard guard(t->device);
+  sxen_dev::EncodeArgs e;
+  if (sxen_status st = sxen_encoder_fused_args(t->enc, t->grad, coords_dev, coord_type, n_samples, &e)) return st;
+  float* params = nullptr;
+  double* grads = nullptr;
+  long long* fixed = nullptr;
+  int32_t precision = 0;
+  if (sxen_status st = sxen_mlp_fused_view(t->mlp, &params, &grads, &fixed, &precision)) return st;
+  sxen_encoder_config ec;
+  sxen_encoder_get_config(t->enc, &ec);
+  int ctas = 0;
+  if (sxen_status st = sxen_train_fused_run(e, ec.dim, params, targets_dev, target_type == SXEN_COORD_F32 ? 1 : 0, grads,
+                                            t->loss_sum, fixed, t->out_w, global_batch,
+                                            precision == SXEN_MLP_TENSOR_BF16X3 ? 1 : 0, as_stream(stream), &ctas))
+    return st;
+  if (sxen_status st = sxen_mlp_fused_fold(t->mlp, t->loss_sum, ctas, stream)) return st;
+  t->head_samples = 0;
+  return sxen_encoder_fused_finish(t->enc, e, stream);
+}
+
 sxen_status sxen_trainer_accumulate(sxen_trainer* t, const void* coords_dev, sxen_coord_type coord_type,
                                     const void* targets_dev, sxen_coord_type target_type, size_t n_samples,
                                     size_t global_batch, void* stream) {
   SXEN_REQUIRE(t != nullptr, "trainer handle is null");
   t->foreign_grads = true;  // (the whole-step entry points reset this around their own call)
+  if (n_samples > 0 && fused_step_applies(t))
+    return accumulate_fused(t, coords_dev, coord_type, targets_dev, target_type, n_samples, global_batch, stream);
+  if (t->fused_mode == 1)
+    return fail(SXEN_INVALID_ARGUMENT, "train: the fused kernel was required (sxen_trainer_set_fused) but does not cover this "
+                                       "configuration (simplex, F=2, 16 levels, dim 2|3, tensor-core head 32-64-64-<=3, no aux, "
+                                       "default accumulation)");
   if (sxen_status st = sxen_trainer_accumulate_head(t, coords_dev, coord_type, targets_dev, target_type, n_samples,
                                                     global_batch, stream))
     return st;
@@ -361,6 +415,13 @@ sxen_status sxen_trainer_step_enqueue(sxen_trainer* t, const void* coords_dev, s
   // visits its own rows instead of scanning all L*T
   const bool walk = own_rows_only && sxen_sparse_adam_walk_pays(t->enc, n_samples);
   return update_impl(t, table_adam, mlp_adam, walk ? coords_dev : nullptr, coord_type, n_samples, t->gate, stream);
+}
+
+sxen_status sxen_trainer_set_fused(sxen_trainer* t, int32_t mode) {
+  SXEN_REQUIRE(t != nullptr, "trainer handle is null");
+  SXEN_REQUIRE(mode >= -1 && mode <= 1, "train: fused mode must be -1 (auto), 0 (off) or 1 (required)");
+  t->fused_mode = mode;
+  return SXEN_OK;
 }
 
 sxen_status sxen_trainer_set_reproducible(sxen_trainer* t, int32_t on) {

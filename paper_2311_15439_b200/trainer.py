@@ -191,6 +191,11 @@ class Trainer:
         raise_for(self._lib, st)
         return list(buf[:cnt.value]), -1
 
+    def set_fused(self, mode: int = 0) -> None:
+        """sxen_trainer_set_fused: 0 = three kernels (default, measured faster), 1 = the one-kernel step (encode -> tcgen05
+        head -> encode_backward, nothing through HBM) or ValueError, -1 = fused whenever the shapes allow."""
+        raise_for(self._lib, self._lib.sxen_trainer_set_fused(self._h, int(mode)))
+
     def set_reproducible(self, on: bool = True) -> None:
         """sxen_trainer_set_reproducible: bit-reproducible steps (order-free fixed-point gradient sums for the tables and
         the MLP; with the exact head d(loss)/d(encoding) reaches encode_backward as doubles)."""

@@ -202,13 +202,14 @@ __global__ void fold_fixed_kernel(double* __restrict__ grads, long long* __restr
 __global__ void __launch_bounds__(256)
 mlp_backward_layer_kernel(const float* __restrict__ params, const float* __restrict__ acts, double* __restrict__ grads,
                           const double* __restrict__ delta_cur, double* __restrict__ delta_next,
-                          unsigned long long n_samples, MlpShape s, int layer, long long* __restrict__ fixed) {
+                          unsigned long long n_samples, MlpShape s, int layer, long long* __restrict__ fixed, int tile) {
   extern __shared__ double smem[];
   const int in = s.in_w[layer], ow = s.out_w[layer];
-  double* d_tile = smem;                                    // [kTile][ow]
-  float* src_tile = reinterpret_cast<float*>(smem + static_cast<size_t>(kTile) * ow);  // [kTile][in]
-  const unsigned long long s0 = static_cast<unsigned long long>(blockIdx.x) * kTile;
-  const int rows = static_cast<int>(min(static_cast<unsigned long long>(kTile), n_samples - s0));
+  // `tile` samples per block: kTile, or fewer for layers whose tile would not fit shared memory (widths up to 2^14)
+  double* d_tile = smem;                                    // [tile][ow]
+  float* src_tile = reinterpret_cast<float*>(smem + static_cast<size_t>(tile) * ow);  // [tile][in]
+  const unsigned long long s0 = static_cast<unsigned long long>(blockIdx.x) * tile;
+  const int rows = static_cast<int>(min(static_cast<unsigned long long>(tile), n_samples - s0));
   for (int i = threadIdx.x; i < rows * ow; i += blockDim.x) d_tile[i] = delta_cur[s0 * ow + i];
   for (int i = threadIdx.x; i < rows * in; i += blockDim.x) {
     const int r = i / in, c = i - r * in;
@@ -556,7 +557,14 @@ sxen_status sxen_mlp_backward(sxen_mlp* mlp, const double* upstream_dev, size_t 
   SXEN_CUDA(cudaMemcpyAsync(cur, upstream_dev, n_samples * static_cast<size_t>(mlp->cfg.output_width) * sizeof(double),
                             cudaMemcpyDeviceToDevice, st));
   for (int l = s.layers - 1; l >= 0; --l) {
-    const size_t smem = static_cast<size_t>(kTile) * s.out_w[l] * sizeof(double) + static_cast<size_t>(kTile) * s.in_w[l] * sizeof(float);
+    // samples per block: kTile when the tile fits, else halved until it does -- MlpConfig::validate admits widths up to 2^14
+    // (src/mlp.cpp:13), and the reference trains them; a block's partial sums then cover fewer samples, nothing else changes
+    int tile = kTile;
+    auto smem_for = [&](int tl) {
+      return static_cast<size_t>(tl) * s.out_w[l] * sizeof(double) + static_cast<size_t>(tl) * s.in_w[l] * sizeof(float);
+    };
+    while (tile > 1 && smem_for(tile) > 200 * 1024) tile >>= 1;
+    const size_t smem = smem_for(tile);
     if (smem > 200 * 1024) {
       cudaFreeAsync(scratch, st);
       return fail(SXEN_INVALID_ARGUMENT, "mlp backward: layer %d (%d x %d) exceeds the shared-memory tile of this path", l,
@@ -565,8 +573,8 @@ sxen_status sxen_mlp_backward(sxen_mlp* mlp, const double* upstream_dev, size_t 
     if (smem > 48 * 1024)
       SXEN_CUDA(cudaFuncSetAttribute(mlp_backward_layer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     double* dst = (l == 0 && input_grad_f64_dev) ? input_grad_f64_dev : nxt;
-    mlp_backward_layer_kernel<<<static_cast<unsigned>((n_samples + kTile - 1) / kTile), 256, smem, st>>>(
-        mlp->params, mlp->acts, mlp->grads, cur, dst, n_samples, s, l, mlp->grads_fixed);
+    mlp_backward_layer_kernel<<<static_cast<unsigned>((n_samples + tile - 1) / tile), 256, smem, st>>>(
+        mlp->params, mlp->acts, mlp->grads, cur, dst, n_samples, s, l, mlp->grads_fixed, tile);
     SXEN_CUDA(cudaGetLastError());
     count_launch();
     if (l == 0 && input_grad_dev) {

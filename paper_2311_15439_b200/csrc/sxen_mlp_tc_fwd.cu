@@ -230,8 +230,10 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
     // Software pipeline over tiles: a tile's features are requested a tile ahead (registers) and written into the X0
     // buffer of its parity while the previous tile's backward GEMMs run.
     constexpr int kXCh = IN / 8;                             // 8-float chunks per feature row
-    constexpr int kXIt = (kTile * kXCh) / kEpiThreads;       // chunks per thread
-    constexpr int kXRows = kEpiThreads / 8 / kXCh;           // 8-row groups one pass of all epilogue threads covers
+    constexpr int kXThreads = kEpiThreads < kTile * kXCh ? kEpiThreads : kTile * kXCh;  // threads that stage (all, or one per chunk)
+    constexpr int kXIt = (kTile * kXCh) / kXThreads;         // chunks per staging thread
+    constexpr int kXRows = kXThreads / 8 / kXCh;             // 8-row groups one pass of the staging threads covers
+    const bool stages = tid < kXThreads;
     float xin[kXIt][8];
     const int xch = (tid >> 3) & (kXCh - 1);
     const int xrow = (tid & 7) + 8 * ((tid >> 3) / kXCh);
@@ -240,7 +242,7 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
       for (int it = 0; it < kXIt; ++it) {
         const int row = xrow + 8 * kXRows * it;
         const unsigned long long gs = tile_index * kTile + row;
-        if (tile_index < n_tiles && gs < a.n) {
+        if (stages && tile_index < n_tiles && gs < a.n) {
           const float4* p = reinterpret_cast<const float4*>(a.features + gs * IN + xch * 8);
           const float4 x0 = __ldg(p), x1 = __ldg(p + 1);
           xin[it][0] = x0.x; xin[it][1] = x0.y; xin[it][2] = x0.z; xin[it][3] = x0.w;
@@ -256,7 +258,7 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
     auto stage_features = [&](int b) {
 #pragma unroll
       for (int it = 0; it < kXIt; ++it)
-        store_chunk(smem + kX0 + b * kX0Bytes, smem + kX0 + b * kX0Bytes + loX0, xrow + 8 * kXRows * it, xch, X0C, xin[it]);
+        if (stages) store_chunk(smem + kX0 + b * kX0Bytes, smem + kX0 + b * kX0Bytes + loX0, xrow + 8 * kXRows * it, xch, X0C, xin[it]);
     };
     // d loss / d encoding of one tile: tDX -> global memory
     auto store_input_grad = [&](unsigned long long tile_index) {

@@ -519,6 +519,9 @@ SXEN_API sxen_status sxen_debug_tc_progress(unsigned int* mapped_host_words);
 /* 16 device counters (NULL = off) the fused training kernel's roles add their cycles to: per role {cycles in the tile loop,
  * cycles of those spent waiting on each of up to three barriers} (tools/fused_step_bench.py). */
 SXEN_API sxen_status sxen_debug_fused_timing(unsigned long long* counters_dev);
+/* The same for the stand-alone tcgen05 training kernel, 8 counters: [0..2] epilogue thread 0 {cycles in the tile loop, waiting on
+ * the chain MMAs, waiting on the weight-gradient MMAs}, [4..5] chain warp {cycles in the tile loop, waiting on the epilogue}. */
+SXEN_API sxen_status sxen_debug_tc_timing(unsigned long long* counters_dev);
 
 #ifdef __cplusplus
 }

@@ -146,9 +146,14 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
       const uint64_t mDYd = desc16_mn_major(sDY, OUTP, 0), mDH2d = desc16_mn_major(sDH2, HID, 0), mDH1d = desc16_mn_major(sDH1, HID, 0);
       constexpr uint32_t kStep = 256;
       uint32_t ph = 0;
+      const bool timed = a.timing != nullptr;
+      unsigned long long t_ready = 0;
+      const long long t_begin = clock64();
       for (unsigned long long tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         for (int p = 0; p < kPhases; ++p) {
+          const long long t0 = timed ? clock64() : 0;
           mbar_wait(&bar_ready, ph, 0x100u + static_cast<uint32_t>(p), a.progress);
+          if (timed) t_ready += static_cast<unsigned long long>(clock64() - t0);
           ph ^= 1;
           tc_fence_after();
           if (p >= 2) mbar_arrive(&bar_w);  // hand the phase to the weight-gradient warp (its private two-phase barrier)
@@ -173,6 +178,10 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
               break;
           }
         }
+      }
+      if (timed) {
+        atomicAdd(a.timing + 4, static_cast<unsigned long long>(clock64() - t_begin));
+        atomicAdd(a.timing + 5, t_ready);
       }
     }
   } else if (is_wgrad_warp) {
@@ -220,8 +229,13 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
       tc_fence_before();
       mbar_arrive(&bar_ready);
     };
+    const bool timed = a.timing != nullptr && tid == 0;
+    unsigned long long t_chain = 0, t_wgrad = 0;
+    const long long t_begin = clock64();
     auto wait_chain = [&]() {
+      const long long t0 = timed ? clock64() : 0;
       mbar_wait(&bar, phase, 0x300u, a.progress);
+      if (timed) t_chain += static_cast<unsigned long long>(clock64() - t0);
       phase ^= 1;
       tc_fence_after();
     };
@@ -273,7 +287,9 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
                                     : static_cast<const double*>(a.targets)[smp * a.out_w + o];
         }
         if (g_started) {
+          const long long t0 = timed ? clock64() : 0;
           mbar_wait(&bar_g, phase_g, 0x400u, a.progress);
+          if (timed) t_wgrad += static_cast<unsigned long long>(clock64() - t0);
           phase_g ^= 1;
         }
       }
@@ -420,6 +436,11 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
       g_started = true;
     }
 
+    if (timed) {
+      atomicAdd(a.timing + 0, static_cast<unsigned long long>(clock64() - t_begin));
+      atomicAdd(a.timing + 1, t_chain);
+      atomicAdd(a.timing + 2, t_wgrad);
+    }
     if constexpr (TRAIN) {
       // ---- weight gradients out of TMEM.  An M = 64 accumulator keeps row i in lane (i/16)*32 + i%16 (tools/tc_probe.py),
       // so lanes 0..15 of each warp hold rows 16*(warp%4) .. +15; warps w and w+4 split the columns.
@@ -500,6 +521,11 @@ extern "C" SXEN_API sxen_status sxen_debug_tc_progress(unsigned int* mapped_host
   g_tc_progress = mapped_host_words;
   return SXEN_OK;
 }
+static unsigned long long* g_tc_timing = nullptr;
+extern "C" SXEN_API sxen_status sxen_debug_tc_timing(unsigned long long* counters_dev) {
+  g_tc_timing = counters_dev;
+  return SXEN_OK;
+}
 sxen_status sxen_mlp_tc_forward_launch(const sxen_mlp_tc::TcArgs& a, int in_w, cudaStream_t stream, int* used_ctas);  // sxen_mlp_tc_fwd.cu
 
 // Internal entry points used by sxen_mlp.cu / sxen_trainer.cu (declared there).
@@ -527,6 +553,7 @@ sxen_status sxen_mlp_tc_run(bool train, const float* params, const float* featur
   a.precise = precise;
   a.upstream_scale = 2.0 / static_cast<double>(global_batch * static_cast<size_t>(out_w));  // src/trainer.cpp:26-27
   a.progress = g_tc_progress;
+  a.timing = g_tc_timing;
   if (!train) return sxen_mlp_tc_forward_launch(a, in_w, stream, used_ctas);  // its own kernel: one hand-off per tile
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);

@@ -29,6 +29,8 @@ struct TcArgs {
   int target_f32;
   int precise;              // 1: bf16x3, 0: single bf16 product
   double upstream_scale;    // 2 / (global_batch * out_w)
+  unsigned long long* timing;       // tuning aid (nullptr = off): {epilogue thread 0: cycles in the tile loop, of those waiting on the
+                                    // chain, waiting on the weight-gradient MMAs; chain warp: loop cycles, waiting on the epilogue}
   volatile unsigned int* progress;  // debugging aid (nullptr = off): host-mapped words the mbar_wait watchdog writes (id, CTA)
 };
 

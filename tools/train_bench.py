@@ -55,3 +55,24 @@ for mode, name in ((1, "tcgen05 bf16x3"), (2, "tcgen05 bf16"), (0, "exact fp64")
     print(f"    full training step ({name}): {sms:8.3f} ms for {Nm} samples = {Nm / sms / 1e6:7.3f} Gsamples/s", flush=True)
     if a.once:
         break
+
+# ---- where the stand-alone training kernel's warps spend their cycles (sxen_debug_tc_timing)
+if not a.once:
+    import ctypes as C
+    counters = torch.zeros(8, dtype=torch.int64, device="cuda")
+    sx.lib.sxen_debug_tc_timing(C.c_void_p(counters.data_ptr()))
+    mlp = sx.Mlp(sx.MlpConfig(32, 64, 2, 3))
+    mlp.init_params(sx.hash_combine(42, 1))
+    mlp.set_precision(1)
+    mlp.forward_backward(feats, tgt)
+    torch.cuda.synchronize()
+    counters.zero_()
+    mlp.forward_backward(feats, tgt)
+    torch.cuda.synchronize()
+    sx.lib.sxen_debug_tc_timing(None)
+    c = counters.cpu().numpy().astype(float)
+    ctas = min(148, (N + 127) // 128)
+    tiles = (N + 127) // 128 / ctas
+    print(f"tcgen05 training kernel, cycles per 128-sample tile: epilogue thread in the loop {c[0] / ctas / tiles:.0f}, of those waiting on "
+          f"the chain MMAs {c[1] / ctas / tiles:.0f}, on the weight-gradient MMAs {c[2] / ctas / tiles:.0f}; chain warp in the loop "
+          f"{c[4] / ctas / tiles:.0f}, waiting on the epilogue {c[5] / ctas / tiles:.0f}", flush=True)

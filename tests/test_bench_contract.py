@@ -55,3 +55,17 @@ def test_our_arm_line():
     assert c["kind"] in ("reference", "port") and c["cores"] >= 1 and c["value"] > 0
     assert "workload" in d["config"] and "model" not in d["config"]
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+
+
+def test_gpus_flag_without_devices_fails_loudly():
+    """`python bench.py --gpus 2` outside a launcher re-runs itself as two ranks (one per GPU); on a box that does not have
+    them -- this container has none -- it must say so and exit non-zero, never fall back to fewer ranks or to the CPU."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"], capture_output=True,
+                         text=True, timeout=300, cwd=ROOT, env=env)
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available() and torch.cuda.device_count() >= 2:
+        pytest.skip("this box has the devices")
+    assert out.returncode != 0
+    assert "CUDA device" in (out.stderr + out.stdout)
+    assert not [l for l in out.stdout.splitlines() if l.startswith("{")]   # no bench line of a run that did not happen

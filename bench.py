@@ -409,7 +409,20 @@ def run_ours(args):
                                  warp_aggregate=args.aggregate, level_chunk=chunk))
 
     exchange = dist is not None and not args.no_allreduce
-    ranges = sx.level_ranges(L, args.level_chunks if exchange else 1)
+    # Level ranges of the overlapped exchange.  Ranges must start on whole 32-byte sectors of the feature rows (4 levels at F = 2)
+    # or the launches pay for partial-sector stores, and the LAST range's all-reduce is the exposed one, so it should be small:
+    # 8 + 4 + 4 levels compute in 0.500 ms on one GPU where four equal ranges take 0.518 (profiles/r2_l2_window_n3.log).
+    if not exchange:
+        ranges = sx.level_ranges(L, 1)
+    elif args.level_ranges:
+        counts = [int(c) for c in args.level_ranges.split(",")]
+        assert sum(counts) == L and all(c > 0 for c in counts), "--level-ranges must add up to the level count"
+        ranges, first = [], 0
+        for c in counts:
+            ranges.append((first, c))
+            first += c
+    else:
+        ranges = sx.level_ranges(L, args.level_chunks)
     per_level = gview.numel() // L
     comm = torch.cuda.Stream(device=dev) if exchange else None
     # the exchange goes through the library's own communicator (sxen_comm_*: NCCL resolved with dlopen, the id carried by the
@@ -750,6 +763,9 @@ def main():
     ap.add_argument("--exact", type=int, default=1)
     ap.add_argument("--aggregate", type=int, default=0)
     ap.add_argument("--no-allreduce", action="store_true")
+    ap.add_argument("--level-ranges", default="8,4,4",
+                    help="multi-GPU: level counts of the ranges whose gradient all-reduce overlaps the next range's kernel "
+                         "(empty = --level-chunks equal ranges)")
     ap.add_argument("--level-chunks", type=int, default=4,
                     help="multi-GPU: level chunks whose gradient all-reduce overlaps the next chunk's kernel")
     ap.add_argument("--oversubscribe", action="store_true",

@@ -101,6 +101,8 @@ struct TrainConfig {
   int record_every = 100;
   int queue_window = 256;  // steps queued between two loss read-backs (1 = the reference's per-step cadence); <= 4096
   int level_chunks = 4;    // batch-sharded runs: level ranges whose gradient exchange overlaps the next range's backward
+  bool reproducible = false;  // order-free fixed-point gradient sums (sxen_trainer_set_reproducible): bit-identical runs for a fixed
+                              // seed, as the reference's are for a fixed (seed, threads) (tests/test_neural.cpp:370-408)
 };
 
 // include/sxen/trainer.hpp:26-32 with device spans: coords = batch x dim, aux = batch x aux_dims pass-through inputs (empty
@@ -186,6 +188,7 @@ inline TrainResult train_field(HashEncoder& encoder, Mlp& mlp, const BatchSample
     ~Handle() { sxen_trainer_destroy(h); }
   } trainer;
   check(sxen_trainer_create_aux(encoder.handle(), mlp.handle(), cfg.aux_dims, &trainer.h));  // width check, :61-65
+  if (cfg.reproducible) check(sxen_trainer_set_reproducible(trainer.h, 1));
   const std::size_t batch = static_cast<std::size_t>(cfg.batch_size);
   const std::size_t dim = static_cast<std::size_t>(encoder.config().dim);
   const std::size_t out_w = static_cast<std::size_t>(mlp.config().output_width);

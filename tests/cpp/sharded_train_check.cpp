@@ -117,6 +117,33 @@ int main(int argc, char** argv) {
     EXPECT(updated_rows > 0);
   }
 
+  // (2b) reproducible mode: two sharded runs of the same steps end bit-identical to each other (the exchange sums fixed-point words)
+  {
+    TrainConfig rc = tc;
+    rc.reproducible = true;
+    std::vector<float> first_run;
+    for (int run = 0; run < 2; ++run) {
+      std::vector<std::unique_ptr<Model>> models;
+      std::vector<Replica> replicas;
+      for (int r = 0; r < ranks; ++r) {
+        models.push_back(std::make_unique<Model>(ec, devices[static_cast<std::size_t>(r)], MlpPrecision::exact));
+        replicas.push_back(Replica{&models.back()->encoder, &models.back()->mlp, devices[static_cast<std::size_t>(r)], nullptr});
+      }
+      train_field_local(replicas, make_sampler, rc);
+      std::vector<float> all;
+      for (int l = 0; l < ec.levels; ++l) {
+        const std::vector<float> t0 = models[0]->encoder.table(l);
+        for (int r = 1; r < ranks; ++r) EXPECT(models[static_cast<std::size_t>(r)]->encoder.table(l) == t0);
+        all.insert(all.end(), t0.begin(), t0.end());
+      }
+      const std::vector<float> p0 = models[0]->mlp.parameters();
+      all.insert(all.end(), p0.begin(), p0.end());
+      if (run == 0) first_run = all;
+      else EXPECT(all == first_run);
+    }
+    std::printf("reproducible ok\n");
+  }
+
   // (3) a coordinate outside [0,1] in the LAST rank's chunk only: std::invalid_argument, nothing updated on any rank
   {
     std::vector<std::unique_ptr<Model>> models;

@@ -248,7 +248,7 @@ def test_cpp_host_trains_sharded_without_python(sx, tmp_path):
             assert float(f["table_max_abs_diff"]) <= (TABLE_ATOL if tag == "exact" else 20 * TABLE_ATOL)
             assert float(f["loss_max_rel_diff"]) <= (1e-5 if tag == "exact" else 1e-3)
             assert float(f["last_loss"]) < float(f["first_loss"])
-        assert "rejected" in lines and "another rank" in run.stdout
+        assert "rejected" in lines and "another rank" in run.stdout and "reproducible ok" in run.stdout
 
 
 # ------------------------------------------------------------------------------------------ torch.distributed, 2 gloo ranks

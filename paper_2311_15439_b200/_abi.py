@@ -172,6 +172,7 @@ SIGNATURES = {
     "sxen_debug_tc_progress": (C.c_int, [_vp]),
     "sxen_debug_fused_timing": (C.c_int, [_vp]),
     "sxen_debug_tc_timing": (C.c_int, [_vp]),
+    "sxen_debug_tc_variant": (C.c_int, [_i32]),
     "sxen_comm_unique_id": (C.c_int, [_vp]),
     "sxen_comm_create": (C.c_int, [_vp, _i32, _i32, _i32, _P(_vp)]),
     "sxen_comm_create_local": (C.c_int, [_i32, _P(_i32), _P(_vp)]),

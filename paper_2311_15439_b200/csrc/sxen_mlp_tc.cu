@@ -527,6 +527,14 @@ extern "C" SXEN_API sxen_status sxen_debug_tc_timing(unsigned long long* counter
   return SXEN_OK;
 }
 sxen_status sxen_mlp_tc_forward_launch(const sxen_mlp_tc::TcArgs& a, int in_w, cudaStream_t stream, int* used_ctas);  // sxen_mlp_tc_fwd.cu
+sxen_status sxen_mlp_tc2_train_launch(const sxen_mlp_tc::TcArgs& a, int in_w, cudaStream_t stream, int* used_ctas);  // sxen_mlp_tc2.cu
+// Which training kernel runs: 2 = two tiles in flight per SM (sxen_mlp_tc2.cu), 1 = one tile in flight (this file).
+static int g_tc_variant = 2;
+extern "C" SXEN_API sxen_status sxen_debug_tc_variant(int variant) {
+  if (variant != 1 && variant != 2) return fail(SXEN_INVALID_ARGUMENT, "tc variant %d: 1 (one tile in flight) or 2 (two)", variant);
+  g_tc_variant = variant;
+  return SXEN_OK;
+}
 
 // Internal entry points used by sxen_mlp.cu / sxen_trainer.cu (declared there).
 bool sxen_mlp_tc_supported(const sxen_mlp_config& c) {
@@ -555,6 +563,7 @@ sxen_status sxen_mlp_tc_run(bool train, const float* params, const float* featur
   a.progress = g_tc_progress;
   a.timing = g_tc_timing;
   if (!train) return sxen_mlp_tc_forward_launch(a, in_w, stream, used_ctas);  // its own kernel: one hand-off per tile
+  if (g_tc_variant == 2) return sxen_mlp_tc2_train_launch(a, in_w, stream, used_ctas);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -71,7 +71,8 @@ def test_fused_step_equals_the_three_kernel_step(sx, dim, out_w, n):
     assert torch.equal(touched0, touched1)
     scale = g0.abs().max().item()
     assert (g1 - g0).abs().max().item() <= 2e-5 * scale
-    assert np.abs(mg1 - mg0).max() <= 1e-9 * np.abs(mg0).max()
+    # parameter gradients: fp32 sums over a CTA's tiles in TMEM; the stand-alone head groups them by its two tile groups
+    assert np.abs(mg1 - mg0).max() <= 1e-4 * np.abs(mg0).max()
     c0, c1 = e0.counters(), e1.counters()
     assert c0.touched_vertices == c1.touched_vertices and c0.out_of_bounds == c1.out_of_bounds
 

@@ -70,9 +70,12 @@ def make_case(oracle_lib, n, out_w, seed, in_w=32):
 
 
 @pytest.mark.parametrize("mode,rtol", [(1, TC3_RTOL), (2, TC1_RTOL)])
-@pytest.mark.parametrize("n,out_w,in_w", [(128 * 150 + 37, 3, 32), (500, 1, 32), (128 * 150 + 37, 3, 16), (700, 2, 16)])
+@pytest.mark.parametrize("n,out_w,in_w", [(128 * 150 + 37, 3, 32), (500, 1, 32), (128 * 150 + 37, 3, 16), (700, 2, 16),
+                                          (128 * 148 * 5 + 37, 3, 32), (128 * 148 * 4 + 1, 2, 16)])
 def test_tensor_core_mlp_matches_oracle(sx, oracle_lib, mode, rtol, n, out_w, in_w):
-    """in_w = 32: L=16, F=2 (every BASELINE config); in_w = 16: L=8, F=2, the reference's default EncoderConfig."""
+    """in_w = 32: L=16, F=2 (every BASELINE config); in_w = 16: L=8, F=2, the reference's default EncoderConfig.  The two
+    largest cases give every CTA of the training kernel several tiles, so both of its tile groups (csrc/sxen_mlp_tc2.cu)
+    and the ring of operand buffers they share go round more than once."""
     mc, p, inp, tgt = make_case(oracle_lib, n, out_w, 7 + out_w, in_w)
     want, acts = oracle_lib.mlp_forward(mc, p, inp)
     scale = 2.0 / (n * out_w)
@@ -165,10 +168,38 @@ def test_training_with_tensor_core_head_tracks_the_exact_head(sx):
     assert np.all(np.abs(tc - exact) <= 5e-3 * exact), (tc, exact)
 
 
+@pytest.mark.parametrize("n,in_w,out_w", [(1, 32, 3), (128 * 148 + 5, 32, 3), (128 * 148 * 3 + 77, 32, 1), (128 * 148 * 6, 16, 2),
+                                          (128 * 148 * 7 + 129, 16, 3)])
+def test_both_training_kernels_agree(sx, n, in_w, out_w):
+    """One tile in flight per SM (csrc/sxen_mlp_tc.cu) against two (csrc/sxen_mlp_tc2.cu, the default): the per-sample
+    arithmetic is the same, so predictions, loss terms and input gradients agree bit for bit; the parameter gradients are
+    fp32 sums over a CTA's tiles taken in a different grouping."""
+    gen = torch.Generator(device="cuda:0").manual_seed(n)
+    x = torch.randn((n, in_w), device="cuda:0", generator=gen) * 0.3
+    tg = torch.rand((n, out_w), device="cuda:0", generator=gen)
+    res = {}
+    try:
+        for variant in (1, 2):
+            assert sx.lib.sxen_debug_tc_variant(variant) == 0
+            mlp = sx.Mlp(sx.MlpConfig(in_w, 64, 2, out_w))
+            mlp.init_params(11)
+            mlp.set_precision(1)
+            ig, loss, pred = mlp.forward_backward(x, tg, want_pred=True)
+            torch.cuda.synchronize()
+            res[variant] = (ig.cpu().numpy(), loss.item(), pred.cpu().numpy(), mlp.gradient())
+    finally:
+        sx.lib.sxen_debug_tc_variant(2)
+    assert sx.lib.sxen_debug_tc_variant(3) != 0
+    a, b = res[1], res[2]
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[2], b[2])
+    assert abs(a[1] - b[1]) <= 1e-12 * abs(a[1])
+    assert np.abs(a[3] - b[3]).max() <= 1e-4 * np.abs(a[3]).max()
+
+
 @pytest.mark.timeout(180)
 def test_back_to_back_training_launches_complete(sx):
-    """The training kernel has three kinds of warps handing work to each other through mbarriers (epilogue warps, the
-    chain-MMA warp, the weight-gradient-MMA warp).  A parity-lapping bug between them does not show in results, it shows as
+    """The training kernel's warps hand work to each other and to the tensor core through mbarriers and named barriers (two
+    tile groups, three GEMM-issuing lanes each).  A parity-lapping bug between them does not show in results, it shows as
     a hang when launches follow each other without synchronisation at awkward batch sizes (tools/mlp_stress.py).  Also
     checks the accumulated gradient against the same launches done one by one."""
     import random

@@ -127,8 +127,8 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
       mbar_init(&bar_chain[k], 1);
       mbar_init(&bar_p2[k], 1);
       mbar_init(&bar_g2[k], 1);
-      mbar_init(&bar_g1[k], 1);
-      mbar_init(&bar_g0[k], 1);
+      mbar_init(&bar_g1[k], 2);  // two issuing lanes each
+      mbar_init(&bar_g0[k], 2);
     }
   }
   if (warp == 0) tmem_alloc(&tmem_base_slot, kTmemCols);
@@ -137,6 +137,19 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
   __syncthreads();
   tc_fence_after();
   const uint32_t tb = tmem_base_slot;
+  {
+    // the weight-gradient accumulators start at zero (their GEMMs only ever accumulate): warp (quadrant, slice) of a group
+    // clears its 32 lanes of a slice of the group's 128 accumulator columns
+    const uint32_t base = tb + kTmemGroup * g + tG0 + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+    for (int c = (128 / kSplit) * half; c < (128 / kSplit) * (half + 1); c += 16)
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(base + c), "r"(0)
+          : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
   const bool precise = a.precise != 0;
   const unsigned long long n_tiles = (a.n + kTile - 1) / kTile;
   const unsigned long long my_tiles = n_tiles > blockIdx.x ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
@@ -165,7 +178,6 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
     // Hand-over of phase P: the group's threads have written the operand tiles and drained the TMEM scratch; one named
     // barrier later three elected lanes issue the phase's GEMMs.  K-major views step 256 B per UMMA_K = 16, MN-major views
     // two 8-row groups.  The first weight-gradient GEMMs of the group overwrite its accumulators.
-    bool g_first = true;
     auto hand_over = [&](auto phase_tag, uint32_t sH1, uint32_t sH2) {
       constexpr int P = decltype(phase_tag)::value;
       fence_proxy_async();
@@ -189,24 +201,32 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
                        desc16_mn_major(sW0, IN, 0), loW0, 2 * cm16_row_group_stride(IN));
           if constexpr (P == 2) tc_commit(&bar_p2[g]);
           tc_commit(&bar_chain[g]);
-        } else if (lw == 5) {
-          if constexpr (P == 2) {  // G2 += H2^T * dY (dW2^T): on its own barrier, the tile's third epilogue overwrites H2 with dH1
+        } else if (lw >= 4) {
+          // Weight-gradient GEMMs, always accumulating (the accumulators start at zero).  K = the tile's 128 samples = eight
+          // UMMA_K steps; dW1 and dW0 are issued four steps each by two lanes so that no warp is held up much longer than the
+          // chain GEMM takes anyway (the next hand-over waits for the group's slowest warp).
+          constexpr int kHalfK = kTile / 32;
+          const int second = lw & 1;  // which four K steps
+          const uint32_t kofs = static_cast<uint32_t>(second) * kHalfK * kStepH;
+          if constexpr (P == 2) {
             tc_fence_after();
-            gemm_split(tg + tG2, make_idesc_bf16(64, 8, true, true), kTile / 16, !g_first, precise, desc16_mn_major(sH2, HC, 0), loH,
-                       kStepH, desc16_mn_major(sD, HC, 0, HID), loH, kStepH);
-            tc_commit(&bar_g2[g]);
-          } else if constexpr (P == 3) {  // G0 += dH1^T * [X0 | 1]
-            tc_fence_after();
-            gemm_split(tg + tG0, make_idesc_bf16(64, X0C, true, true), kTile / 16, !g_first, precise, desc16_mn_major(sH2, HC, 0), loH,
-                       kStepH, desc16_mn_major(sX0, X0C, 0), loX0, 2 * cm16_row_group_stride(X0C));
-            tc_commit(&bar_g0[g]);
-          }
-        } else if (lw == 6) {
-          if constexpr (P == 2) {  // G1 += dH2^T * [H1 | 1]
-            tc_fence_after();
-            gemm_split(tg + tG1, make_idesc_bf16(64, HC, true, true), kTile / 16, !g_first, precise, desc16_mn_major(sD, HC, 0), loH,
-                       kStepH, desc16_mn_major(sH1, HC, 0), loH, kStepH);
-            tc_commit(&bar_g1[g]);
+            if (lw == 4) {  // G2 += H2^T * dY (dW2^T): on its own barrier, the tile's third epilogue overwrites H2 with dH1
+              gemm_split(tg + tG2, make_idesc_bf16(64, 8, true, true), kTile / 16, true, precise, desc16_mn_major(sH2, HC, 0), loH,
+                         kStepH, desc16_mn_major(sD, HC, 0, HID), loH, kStepH);
+              tc_commit(&bar_g2[g]);
+            } else if (lw >= 6) {  // G1 += dH2^T * [H1 | 1]
+              gemm_split(tg + tG1, make_idesc_bf16(64, HC, true, true), kHalfK, true, precise, desc16_mn_major(sD + kofs, HC, 0), loH,
+                         kStepH, desc16_mn_major(sH1 + kofs, HC, 0), loH, kStepH);
+              tc_commit(&bar_g1[g]);
+            }
+          } else if constexpr (P == 3) {
+            if (lw >= 6) {  // G0 += dH1^T * [X0 | 1]
+              tc_fence_after();
+              const uint32_t xofs = static_cast<uint32_t>(second) * kHalfK * 2 * cm16_row_group_stride(X0C);
+              gemm_split(tg + tG0, make_idesc_bf16(64, X0C, true, true), kHalfK, true, precise, desc16_mn_major(sH2 + kofs, HC, 0), loH,
+                         kStepH, desc16_mn_major(sX0 + xofs, X0C, 0), loX0, 2 * cm16_row_group_stride(X0C));
+              tc_commit(&bar_g0[g]);
+            }
           }
         }
       }
@@ -298,6 +318,14 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
       hand_over(std::integral_constant<int, 1>{}, smem_u32(H1), smem_u32(H2));
 
       // ---- layer 2 epilogue: S1 -> H2, then the output layer, the loss and its way back to dH2 on the CUDA cores
+      const unsigned long long smp = static_cast<unsigned long long>(tile) * kTile + t;
+      const bool valid = smp < a.n;
+      // the row's targets are needed after the layer-2 conversion: loaded there, the L2 round trip cost 8 % of the kernel's
+      // stall samples; held in registers across the conversion, they spill.  So: pull the line into L1 now, load later.
+      if (valid && half == 0) {
+        const char* tp = static_cast<const char*>(a.targets) + smp * a.out_w * (a.target_f32 ? 4 : 8);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(tp));
+      }
       wait_chain();
       if (tile != first_tile || g > 0) {
         // H2 goes where the other group's tile keeps H1, dH2 | dY where it keeps its own: both are dead once that tile's
@@ -330,9 +358,7 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
         }
         *reinterpret_cast<float4*>(pp + (half * kTile + t) * 4) = make_float4(p0, p1, p2, 0.0f);
       }
-      const unsigned long long smp = static_cast<unsigned long long>(tile) * kTile + t;
-      const bool valid = smp < a.n;
-      double tgt[3] = {0.0, 0.0, 0.0};  // requested here: the loads complete under the named barrier
+      double tgt[3] = {0.0, 0.0, 0.0};
       if (valid) {
 #pragma unroll
         for (int o = 0; o < 3; ++o)
@@ -449,7 +475,6 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
       }
       tc_fence_before();
       r1 = r2;
-      g_first = false;
     }
 
     if (timed && g == 0) {

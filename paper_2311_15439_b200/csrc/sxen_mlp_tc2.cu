@@ -126,8 +126,8 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
     for (int k = 0; k < kGroups; ++k) {
       mbar_init(&bar_chain[k], 1);
       mbar_init(&bar_p2[k], 1);
-      mbar_init(&bar_g2[k], 1);
-      mbar_init(&bar_g1[k], 2);  // two issuing lanes each
+      mbar_init(&bar_g2[k], 2);  // the weight-gradient GEMMs have two issuing lanes each
+      mbar_init(&bar_g1[k], 2);
       mbar_init(&bar_g0[k], 2);
     }
   }
@@ -183,49 +183,62 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
       fence_proxy_async();
       tc_fence_before();
       asm volatile("bar.sync %0, %1;" ::"r"(2 + 2 * g), "n"(kGroupThreads) : "memory");
-      if ((lt & 31) == 0) {
-        const uint32_t sX0 = sX0b + g * kX0Bytes;
-        if (lw == 0) {
-          tc_fence_after();
+      // GEMM issue from warp-uniform code (gemm_split_uniform): everything the descriptors are built from goes through
+      // __shfl_sync so that the compiler keeps it in uniform registers; one lane's instructions reach the tensor core.
+      const int lw_u = __shfl_sync(0xffffffffu, lw, 0);
+      if (lw_u == 0 || (P >= 2 && lw_u >= 4)) {
+        const bool leader = (lt & 31) == 0;
+        const uint32_t g_u = static_cast<uint32_t>(__shfl_sync(0xffffffffu, g, 0));
+        const uint32_t tg_u = __shfl_sync(0xffffffffu, tg, 0);
+        const uint32_t sH1_u = __shfl_sync(0xffffffffu, sH1, 0), sH2_u = __shfl_sync(0xffffffffu, sH2, 0);
+        const uint32_t sX0 = sX0b + g_u * kX0Bytes;
+        tc_fence_after();
+        if (lw_u == 0) {
           if constexpr (P == 0)  // layer 1: S0 = X0 * W0^T
-            gemm_split(tg + tS0, make_idesc_bf16(128, HID, false, false), IN / 16, false, precise, desc16_k_major(sX0, X0C, 0), loX0,
-                       kStep, desc16_k_major(sW0, IN, 0), loW0, kStep);
+            gemm_split_uniform(tg_u + tS0, make_idesc_bf16(128, HID, false, false), IN / 16, false, precise, desc16_k_major(sX0, X0C, 0),
+                               loX0, kStep, desc16_k_major(sW0, IN, 0), loW0, kStep, leader);
           else if constexpr (P == 1)  // layer 2: S1 = H1 * W1^T
-            gemm_split(tg + tS1, make_idesc_bf16(128, HID, false, false), HID / 16, false, precise, desc16_k_major(sH1, HC, 0), loH,
-                       kStep, desc16_k_major(sW1, HID, 0), loW1, kStep);
+            gemm_split_uniform(tg_u + tS1, make_idesc_bf16(128, HID, false, false), HID / 16, false, precise,
+                               desc16_k_major(sH1_u, HC, 0), loH, kStep, desc16_k_major(sW1, HID, 0), loW1, kStep, leader);
           else if constexpr (P == 2)  // S1 = dH2 * W1
-            gemm_split(tg + tS1, make_idesc_bf16(128, HID, false, true), HID / 16, false, precise, desc16_k_major(sD, HC, 0), loH, kStep,
-                       desc16_mn_major(sW1, HID, 0), loW1, 2 * cm16_row_group_stride(HID));
+            gemm_split_uniform(tg_u + tS1, make_idesc_bf16(128, HID, false, true), HID / 16, false, precise, desc16_k_major(sD, HC, 0),
+                               loH, kStep, desc16_mn_major(sW1, HID, 0), loW1, 2 * cm16_row_group_stride(HID), leader);
           else  // S0[:, 0:IN] = dH1 * W0 (d loss / d encoding); dH1 sits in the tile's H2 buffer
-            gemm_split(tg + tS0, make_idesc_bf16(128, IN, false, true), HID / 16, false, precise, desc16_k_major(sH2, HC, 0), loH, kStep,
-                       desc16_mn_major(sW0, IN, 0), loW0, 2 * cm16_row_group_stride(IN));
-          if constexpr (P == 2) tc_commit(&bar_p2[g]);
-          tc_commit(&bar_chain[g]);
-        } else if (lw >= 4) {
+            gemm_split_uniform(tg_u + tS0, make_idesc_bf16(128, IN, false, true), HID / 16, false, precise,
+                               desc16_k_major(sH2_u, HC, 0), loH, kStep, desc16_mn_major(sW0, IN, 0), loW0,
+                               2 * cm16_row_group_stride(IN), leader);
+          if (leader) {
+            if constexpr (P == 2) tc_commit(&bar_p2[g_u]);
+            tc_commit(&bar_chain[g_u]);
+          }
+        } else {
           // Weight-gradient GEMMs, always accumulating (the accumulators start at zero).  K = the tile's 128 samples = eight
-          // UMMA_K steps; dW1 and dW0 are issued four steps each by two lanes so that no warp is held up much longer than the
+          // UMMA_K steps; each GEMM is issued four steps each by two warps so that no warp is held up much longer than the
           // chain GEMM takes anyway (the next hand-over waits for the group's slowest warp).
-          constexpr int kHalfK = kTile / 32;
-          const int second = lw & 1;  // which four K steps
-          const uint32_t kofs = static_cast<uint32_t>(second) * kHalfK * kStepH;
+          // Reproducible mode: two lanes' MMAs into one accumulator reach the tensor core in an order that can change from
+          // run to run, and fp32 sums depend on it -- there the first lane issues all eight steps and the second only commits.
+          const bool one_issuer = a.grad_fixed != nullptr;
+          const uint32_t second = static_cast<uint32_t>(lw_u & 1);  // which four K steps
+          const int kHalfK = one_issuer ? (second ? 0 : kTile / 16) : kTile / 32;
+          const uint32_t kofs = second * (kTile / 32) * kStepH;
           if constexpr (P == 2) {
-            tc_fence_after();
-            if (lw == 4) {  // G2 += H2^T * dY (dW2^T): on its own barrier, the tile's third epilogue overwrites H2 with dH1
-              gemm_split(tg + tG2, make_idesc_bf16(64, 8, true, true), kTile / 16, true, precise, desc16_mn_major(sH2, HC, 0), loH,
-                         kStepH, desc16_mn_major(sD, HC, 0, HID), loH, kStepH);
-              tc_commit(&bar_g2[g]);
-            } else if (lw >= 6) {  // G1 += dH2^T * [H1 | 1]
-              gemm_split(tg + tG1, make_idesc_bf16(64, HC, true, true), kHalfK, true, precise, desc16_mn_major(sD + kofs, HC, 0), loH,
-                         kStepH, desc16_mn_major(sH1 + kofs, HC, 0), loH, kStepH);
-              tc_commit(&bar_g1[g]);
+            if (lw_u < 6) {  // G2 += H2^T * dY (dW2^T): on its own barrier, the tile's third epilogue overwrites H2 with dH1
+              gemm_split_uniform(tg_u + tG2, make_idesc_bf16(64, 8, true, true), kHalfK, true, precise,
+                                 desc16_mn_major(sH2_u + kofs, HC, 0), loH, kStepH, desc16_mn_major(sD + kofs, HC, 0, HID), loH, kStepH,
+                                 leader);
+              if (leader) tc_commit(&bar_g2[g_u]);
+            } else {  // G1 += dH2^T * [H1 | 1]
+              gemm_split_uniform(tg_u + tG1, make_idesc_bf16(64, HC, true, true), kHalfK, true, precise,
+                                 desc16_mn_major(sD + kofs, HC, 0), loH, kStepH, desc16_mn_major(sH1_u + kofs, HC, 0), loH, kStepH, leader);
+              if (leader) tc_commit(&bar_g1[g_u]);
             }
           } else if constexpr (P == 3) {
-            if (lw >= 6) {  // G0 += dH1^T * [X0 | 1]
-              tc_fence_after();
-              const uint32_t xofs = static_cast<uint32_t>(second) * kHalfK * 2 * cm16_row_group_stride(X0C);
-              gemm_split(tg + tG0, make_idesc_bf16(64, X0C, true, true), kHalfK, true, precise, desc16_mn_major(sH2 + kofs, HC, 0), loH,
-                         kStepH, desc16_mn_major(sX0 + xofs, X0C, 0), loX0, 2 * cm16_row_group_stride(X0C));
-              tc_commit(&bar_g0[g]);
+            if (lw_u >= 6) {  // G0 += dH1^T * [X0 | 1]
+              const uint32_t xofs = second * (kTile / 32) * 2 * cm16_row_group_stride(X0C);
+              gemm_split_uniform(tg_u + tG0, make_idesc_bf16(64, X0C, true, true), kHalfK, true, precise,
+                                 desc16_mn_major(sH2_u + kofs, HC, 0), loH, kStepH, desc16_mn_major(sX0 + xofs, X0C, 0), loX0,
+                                 2 * cm16_row_group_stride(X0C), leader);
+              if (leader) tc_commit(&bar_g0[g_u]);
             }
           }
         }
@@ -267,8 +280,11 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
         const int row = xrow + 8 * kXRows * it;
         const unsigned long long gs = static_cast<unsigned long long>(tile_index) * kTile + row;
         if (stages && tile_index < tiles32 && gs < a.n) {
+          // read once: keep the features out of the little L1 this kernel leaves (28 KB; the targets are prefetched into it)
           const float4* p = reinterpret_cast<const float4*>(a.features + gs * IN + xch * 8);
-          const float4 x0 = __ldg(p), x1 = __ldg(p + 1);
+          float4 x0, x1;
+          asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x0.x), "=f"(x0.y), "=f"(x0.z), "=f"(x0.w) : "l"(p));
+          asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x1.x), "=f"(x1.y), "=f"(x1.z), "=f"(x1.w) : "l"(p + 1));
           xin[it][0] = x0.x; xin[it][1] = x0.y; xin[it][2] = x0.z; xin[it][3] = x0.w;
           xin[it][4] = x1.x; xin[it][5] = x1.y; xin[it][6] = x1.z; xin[it][7] = x1.w;
         } else {
@@ -299,11 +315,13 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
       // ---- layer 1 epilogue: S0 -> H1
       uint32_t m1 = 0, m2 = 0;  // ReLU masks of this thread's units (bit i = unit CPT*half + i active)
       wait_chain();
+      uint32_t ra[CPT / 16][16];
+#pragma unroll
+      for (int q = 0; q < CPT / 16; ++q) tmem_ld16_nowait(S0 + CPT * half + 16 * q, ra[q]);
+      tmem_ld_wait();
 #pragma unroll
       for (int q = 0; q < CPT / 16; ++q) {
-        uint32_t r[16];
-        tmem_ld16_nowait(S0 + CPT * half + 16 * q, r);
-        tmem_ld_wait();
+        const uint32_t(&r)[16] = ra[q];
         float v[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
@@ -322,7 +340,7 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
       const bool valid = smp < a.n;
       // the row's targets are needed after the layer-2 conversion: loaded there, the L2 round trip cost 8 % of the kernel's
       // stall samples; held in registers across the conversion, they spill.  So: pull the line into L1 now, load later.
-      if (valid && half == 0) {
+      if (valid) {
         const char* tp = static_cast<const char*>(a.targets) + smp * a.out_w * (a.target_f32 ? 4 : 8);
         asm volatile("prefetch.global.L1 [%0];" ::"l"(tp));
       }
@@ -417,11 +435,13 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
       wait_chain();
       timed_wait(&bar_g2[g], phase_g2, 0x600u + static_cast<uint32_t>(g), t_wgrad);  // dW2 has consumed H2
       phase_g2 ^= 1;
+      uint32_t rb[CPT / 16][16];
+#pragma unroll
+      for (int q = 0; q < CPT / 16; ++q) tmem_ld16_nowait(S1 + CPT * half + 16 * q, rb[q]);
+      tmem_ld_wait();
 #pragma unroll
       for (int q = 0; q < CPT / 16; ++q) {
-        uint32_t r[16];
-        tmem_ld16_nowait(S1 + CPT * half + 16 * q, r);
-        tmem_ld_wait();
+        const uint32_t(&r)[16] = rb[q];
         float v[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) v[k] = ((m1 >> (16 * q + k)) & 1u) ? __uint_as_float(r[k]) : 0.0f;

@@ -83,6 +83,32 @@ __device__ __forceinline__ void gemm_split(uint32_t d, uint32_t idesc, int kstep
   }
 }
 
+// The same GEMM issued from warp-uniform code: the whole warp walks the loop with warp-uniform operands (descriptors built from
+// __shfl_sync'ed values live in uniform registers) and only the MMA instruction itself is predicated on `leader`.  Issued from
+// inside an `if (lane == 0)` branch the compiler must assume per-thread descriptors and wraps every tcgen05.mma in a
+// serialising loop (ELECT + 3 x R2UR.BROADCAST + branch): ~35 cycles per MMA against ~10 here.
+__device__ __forceinline__ void mma_bf16_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, bool accumulate,
+                                               bool leader) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+      "@q tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(static_cast<uint32_t>(accumulate)), "r"(static_cast<uint32_t>(leader))
+      : "memory");
+}
+__device__ __forceinline__ void gemm_split_uniform(uint32_t d, uint32_t idesc, int ksteps, bool accumulate, bool precise, uint64_t a0,
+                                                   uint32_t a_lo, uint32_t a_step, uint64_t b0, uint32_t b_lo, uint32_t b_step,
+                                                   bool leader) {
+#pragma unroll
+  for (int ks = 0; ks < ksteps; ++ks) {
+    const uint64_t ah = a0 + ((static_cast<uint64_t>(ks) * a_step) >> 4), bh = b0 + ((static_cast<uint64_t>(ks) * b_step) >> 4);
+    mma_bf16_elect(d, ah, bh, idesc, accumulate || ks > 0, leader);
+    if (precise) {
+      mma_bf16_elect(d, ah, bh + (b_lo >> 4), idesc, true, leader);
+      mma_bf16_elect(d, ah + (a_lo >> 4), bh, idesc, true, leader);
+    }
+  }
+}
+
 // One CTA's partial sum into the batch total: an fp64 atomic, or -- reproducible mode -- an integer atomic on the fixed-point
 // shadow of the same element (order-free; sxen_mlp.cu folds the shadow into the fp64 buffer after the kernel).
 __device__ __forceinline__ void add_total(double* base, long long* fixed, size_t index, double v) {

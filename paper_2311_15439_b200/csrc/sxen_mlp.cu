@@ -29,6 +29,9 @@ struct sxen_mlp {
   // reproducible mode (sxen_mlp_set_reproducible): the blocks' partial parameter gradients meet in 64-bit fixed point
   // (units of 2^-52, integer atomics: order-free) and are folded into `grads` once per backward
   long long* grads_fixed = nullptr;
+  // tensor-core head: one row of parameter-gradient partial sums per CTA (sxen_mlp_tc2.cu), allocated at the first training launch
+  double* tc_partials = nullptr;
+  size_t tc_partial_stride = 0;
   int layer_count() const { return cfg.hidden_layers + 1; }
   int layer_in(int l) const { return l == 0 ? cfg.input_width : cfg.hidden_width; }
   int layer_out(int l) const { return l == layer_count() - 1 ? cfg.output_width : cfg.hidden_width; }
@@ -44,7 +47,7 @@ bool sxen_mlp_tc_supported(const sxen_mlp_config& c);
 sxen_status sxen_mlp_tc_run(bool train, const float* params, const float* features, const void* targets, int target_f32,
                             float* pred, float* input_grad, double* mlp_grad, double* loss_sum, size_t n, int in_w, int out_w,
                             size_t global_batch, int precise, cudaStream_t stream, long long* grad_fixed = nullptr,
-                            int* used_ctas = nullptr);
+                            int* used_ctas = nullptr, double* partials = nullptr, size_t partial_stride = 0);
 
 namespace {
 
@@ -351,6 +354,7 @@ sxen_status sxen_mlp_destroy(sxen_mlp* mlp) {
   cudaFree(mlp->acts);
   cudaFree(mlp->loss_scratch);
   cudaFree(mlp->grads_fixed);
+  cudaFree(mlp->tc_partials);
   delete mlp;
   return SXEN_OK;
 }
@@ -458,9 +462,16 @@ sxen_status sxen_mlp_forward_backward_ex(sxen_mlp* mlp, const float* input_dev, 
     double* loss = loss_sum_dev ? loss_sum_dev : mlp->loss_scratch;
     mlp->forward_done = false;  // no activations are kept: a separate backward would be a logic error
     int ctas = 0;
+    if (!mlp->tc_partials) {  // persistent kernel: at most one CTA per SM
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, mlp->device);
+      mlp->tc_partial_stride = (mlp->param_count + 31) / 32 * 32;
+      SXEN_CUDA(cudaMalloc(&mlp->tc_partials, static_cast<size_t>(sms) * mlp->tc_partial_stride * sizeof(double)));
+    }
     if (sxen_status s = sxen_mlp_tc_run(true, mlp->params, input_dev, targets_dev, target_type == SXEN_COORD_F32 ? 1 : 0, pred_dev,
                                         input_grad_dev, mlp->grads, loss, n_samples, mlp->cfg.input_width, mlp->cfg.output_width,
-                                        global_batch, mlp->precision == SXEN_MLP_TENSOR_BF16X3 ? 1 : 0, st, mlp->grads_fixed, &ctas))
+                                        global_batch, mlp->precision == SXEN_MLP_TENSOR_BF16X3 ? 1 : 0, st, mlp->grads_fixed, &ctas,
+                                        mlp->tc_partials, mlp->tc_partial_stride))
       return s;
     if (mlp->grads_fixed) {  // the CTAs' partial sums met in fixed point (order-free): fold them into the fp64 buffers
       fold_fixed_kernel<<<grid_for(mlp->param_count), 256, 0, st>>>(mlp->grads, mlp->grads_fixed, mlp->param_count);

@@ -543,7 +543,8 @@ bool sxen_mlp_tc_supported(const sxen_mlp_config& c) {
 
 sxen_status sxen_mlp_tc_run(bool train, const float* params, const float* features, const void* targets, int target_f32,
                             float* pred, float* input_grad, double* mlp_grad, double* loss_sum, size_t n, int in_w, int out_w,
-                            size_t global_batch, int precise, cudaStream_t stream, long long* grad_fixed, int* used_ctas) {
+                            size_t global_batch, int precise, cudaStream_t stream, long long* grad_fixed, int* used_ctas,
+                            double* partials, size_t partial_stride) {
   if (n == 0) return SXEN_OK;
   if (in_w != 16 && in_w != 32) return fail(SXEN_INVALID_ARGUMENT, "mlp (tensor cores): input width %d not instantiated", in_w);
   TcArgs a{};
@@ -563,7 +564,13 @@ sxen_status sxen_mlp_tc_run(bool train, const float* params, const float* featur
   a.progress = g_tc_progress;
   a.timing = g_tc_timing;
   if (!train) return sxen_mlp_tc_forward_launch(a, in_w, stream, used_ctas);  // its own kernel: one hand-off per tile
-  if (g_tc_variant == 2) return sxen_mlp_tc2_train_launch(a, in_w, stream, used_ctas);
+  if (g_tc_variant == 2) {
+    if (a.grad_fixed == nullptr) {  // per-CTA gradient rows + a fixed-order reduction instead of contended atomics
+      a.partials = partials;
+      a.partial_stride = partial_stride;
+    }
+    return sxen_mlp_tc2_train_launch(a, in_w, stream, used_ctas);
+  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

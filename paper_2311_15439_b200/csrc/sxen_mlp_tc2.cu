@@ -151,6 +151,13 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
     tc_fence_after();
   }
   const bool precise = a.precise != 0;
+  // Where the CTA's parameter gradients go.  148 CTAs adding to the same 6467 words serialise in L2 (the read-out at the end of
+  // a 2^20-sample launch cost 4 % of the kernel, a mid-kernel flush 16 us): with `partials` every CTA owns a row, clears it here
+  // and a reduction kernel adds the rows in a fixed order afterwards.
+  double* const grad_out = a.partials != nullptr ? a.partials + blockIdx.x * a.partial_stride : a.mlp_grad;
+  if (a.partials != nullptr)
+    for (unsigned long long e = tid; e < a.partial_stride; e += kThreads2) grad_out[e] = 0.0;
+  __syncthreads();
   const unsigned long long n_tiles = (a.n + kTile - 1) / kTile;
   const unsigned long long my_tiles = n_tiles > blockIdx.x ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   const unsigned long long group_tiles[kGroups] = {(my_tiles + 1) / 2, my_tiles / 2};  // tile j of the CTA belongs to group j % 2
@@ -293,6 +300,71 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
         }
       }
     };
+    // ---- the group's weight-gradient accumulators -> batch total (fp64 atomics or fixed point), then back to zero.
+    // An M = 64 accumulator keeps row i in lane (i/16)*32 + i%16 (tools/tc_probe.py): lanes 0..15 of a warp hold rows
+    // 16*(warp%4) .. +15.  Warp (quadrant, slice) owns its lanes of the slice's half of the 128 accumulator columns, reads
+    // and clears exactly those, so no warp waits for another.  Run every kFlushTiles tiles of the group, and once more for both
+    // groups together when the CTA is done: the accumulators are fp32 and a sum over T tiles is off by ~T * 2^-24 of its size
+    // -- left to the end of a 2^24-sample launch (443 tiles per group) the parameter gradients were 2.5e-4 off the fp64
+    // reference, against 1e-5 at 2^20 samples.  A flush is 6467 reds, one wavefront each on a data pipe that is busy already
+    // (~22 k cycles, two tiles' worth), hence not more often.
+    constexpr uint32_t kFlushTiles = 64;
+    // `final_pass`: the CTA is done -- both groups' accumulators are summed, sixteen warps share the columns, nothing is cleared.
+    auto flush_gradients = [&](bool final_pass) {
+      constexpr size_t gW0 = 0, gb0 = gW0 + HID * IN, gW1 = gb0 + HID, gb1 = gW1 + HID * HID, gW2 = gb1 + HID;  // parameter layout
+      constexpr int kG1 = tG1 - tG0, kG2 = tG2 - tG0;  // accumulator columns relative to tG0: dW0|db0, dW1|db1, dW2^T
+      const int lane = lt & 31;
+      const size_t row = 16 * (warp & 3) + lane;  // output unit (dW0, dW1) or hidden unit (dW2^T)
+      // eight blocks of 16 columns: a group's warp takes four, in the final pass two -- which two rotates with the CTA so that
+      // the CTAs, all finishing together, do not walk the same addresses in the same order
+      const int first_blk = final_pass ? 2 * ((2 * g + half + static_cast<int>(blockIdx.x)) & 3) : 4 * half;
+      const int n_blk = final_pass ? 2 : 4;
+      for (int blk = first_blk; blk < first_blk + n_blk; ++blk) {
+        const int c_base = 16 * blk;
+        float v[16];
+        {
+          uint32_t r[16];
+          tmem_ld16_nowait((final_pass ? tb : tg) + lane_base + tG0 + c_base, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
+          if (final_pass && group_tiles[1] > 0) {
+            tmem_ld16_nowait(tb + kTmemGroup + lane_base + tG0 + c_base, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[k] += __uint_as_float(r[k]);
+          }
+        }
+        if (lane < 16) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int c = c_base + k;
+            const double d = static_cast<double>(v[k]);
+            if (c < kG1) {
+              if (c < IN) add_total(grad_out, a.grad_fixed, gW0 + row * IN + c, d);
+              else if (c == IN) add_total(grad_out, a.grad_fixed, gb0 + row, d);
+            } else if (c < kG2) {
+              if (c - kG1 < HID) add_total(grad_out, a.grad_fixed, gW1 + row * HID + (c - kG1), d);
+              else if (c - kG1 == HID) add_total(grad_out, a.grad_fixed, gb1 + row, d);
+            } else if (c - kG2 < a.out_w) {
+              add_total(grad_out, a.grad_fixed, gW2 + static_cast<size_t>(c - kG2) * HID + row, d);
+            }
+          }
+        }
+        if (!final_pass)
+          asm volatile(
+              "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(tg + lane_base + tG0 + c_base),
+              "r"(0)
+              : "memory");
+      }
+      if (!final_pass) {
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();  // ordered before the next weight-gradient GEMMs by the hand-over barrier
+      }
+    };
+    static_assert(kSplit == 2, "flush_gradients splits the accumulator columns in two halves");
+    uint32_t tiles_done = 0;
+    uint32_t next_flush = kFlushTiles / 2 + blockIdx.x % (kFlushTiles / 2);  // differs from CTA to CTA: the flushes do not coincide
     const uint32_t first_tile = blockIdx.x + static_cast<uint32_t>(g) * gridDim.x;
     load_features(first_tile);
 
@@ -306,6 +378,16 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
       if (tile != first_tile) {
         timed_wait(&bar_g0[g], phase_g0, 0x400u + static_cast<uint32_t>(g), t_wgrad);
         phase_g0 ^= 1;
+        // every kFlushTiles tiles.  Every GEMM into the accumulators is done here: dW2 was waited for in the tile's third
+        // epilogue, dW0 just above.
+        if (tiles_done == next_flush) {
+          next_flush += kFlushTiles;
+          timed_wait(&bar_g1[g], (tiles_done - 1) & 1, 0x410u + static_cast<uint32_t>(g), t_wgrad);
+          tc_fence_after();
+          const long long tf0 = TIMED ? clock64() : 0;
+          flush_gradients(false);
+          if (timed) atomicAdd(a.timing + 6, static_cast<unsigned long long>(clock64() - tf0));
+        }
       }
 #pragma unroll
       for (int it = 0; it < kXIt; ++it)
@@ -495,6 +577,7 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
       }
       tc_fence_before();
       r1 = r2;
+      ++tiles_done;
     }
 
     if (timed && g == 0) {
@@ -503,70 +586,20 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
       atomicAdd(a.timing + 2, t_wgrad);
       atomicAdd(a.timing + 3, t_cross);
     }
-    // ---- weight gradients out of TMEM.  An M = 64 accumulator keeps row i in lane (i/16)*32 + i%16 (tools/tc_probe.py), so
-    // lanes 0..15 of each warp hold rows 16*(warp%4) .. +15; the warps that share a lane quadrant split the columns.
+    // ---- the last tiles' weight gradients
     if (group_tiles[g] > 0) {  // the group's last tile: dW1 (its barrier's phases were the other group's to follow) and dW0
       mbar_wait(&bar_g1[g], static_cast<uint32_t>((group_tiles[g] - 1) & 1), 0x700u + static_cast<uint32_t>(g), a.progress);
       mbar_wait(&bar_g0[g], phase_g0, 0x710u + static_cast<uint32_t>(g), a.progress);
     }
     tc_fence_before();
-    __syncthreads();  // both groups' accumulators are final
+    __syncthreads();  // both groups' accumulators are final (a group without tiles still holds the zeros it started with)
     tc_fence_after();
-    const int lane = tid & 31;
-    const int row = 16 * (warp & 3) + lane;  // output unit o (G0, G1) or hidden unit i (G2)
-    const int slice = warp >> 2;
-    constexpr int kSlices = kEpi2 / 128;
-    constexpr size_t gW0 = 0, gb0 = gW0 + HID * IN, gW1 = gb0 + HID, gb1 = gW1 + HID * HID, gW2 = gb1 + HID;  // offsets
-    double* const G = a.mlp_grad;
-    long long* const FX = a.grad_fixed;
-    // sixteen columns of an accumulator, summed over the groups that ran a tile (a group without tiles never wrote its columns)
-    auto load_sum = [&](uint32_t column, float (&v)[16]) {
-#pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = 0.0f;
-      for (int k = 0; k < kGroups; ++k) {
-        if (group_tiles[k] == 0) continue;
-        uint32_t r[16];
-        tmem_ld16_nowait(tb + kTmemGroup * k + lane_base + column, r);
-        tmem_ld_wait();
-#pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] += __uint_as_float(r[q]);
-      }
-    };
-    if (my_tiles > 0) {
-      for (int c0 = 8 * slice; c0 < X0C; c0 += 8 * kSlices) {  // G0: IN + 8 columns = dW0[row][0..IN), db0[row] at column IN
-        float v[16];
-        load_sum(tG0 + (c0 < IN ? c0 : IN - 8), v);  // the last read re-covers cols IN-8..IN+7
-        if (lane < 16) {
-          if (c0 < IN) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) add_total(G, FX, gW0 + row * IN + c0 + k, static_cast<double>(v[k]));
-          } else {
-            add_total(G, FX, gb0 + row, static_cast<double>(v[8]));
-          }
-        }
-      }
-      for (int c0 = 8 * slice; c0 < HC; c0 += 8 * kSlices) {  // G1: 72 columns = dW1[row][0..63], db1[row] at column 64
-        float v[16];
-        load_sum(tG1 + (c0 < 64 ? c0 : 56), v);
-        if (lane < 16) {
-          if (c0 < 64) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) add_total(G, FX, gW1 + row * HID + c0 + k, static_cast<double>(v[k]));
-          } else {
-            add_total(G, FX, gb1 + row, static_cast<double>(v[8]));
-          }
-        }
-      }
-      if (slice == kSlices - 1) {  // G2: dW2^T[i = row][o]
-        float v[16];
-        load_sum(tG2, v);
-        if (lane < 16) {
-#pragma unroll
-          for (int o = 0; o < 3; ++o)
-            if (o < a.out_w) add_total(G, FX, gW2 + o * HID + row, static_cast<double>(v[o]));
-        }
-      }
+    {
+      const long long tf0 = TIMED ? clock64() : 0;
+      if (my_tiles > 0) flush_gradients(true);
+      if (timed && g == 0) atomicAdd(a.timing + 7, static_cast<unsigned long long>(clock64() - tf0));
     }
+    const int lane = tid & 31;
     // loss and output-bias gradient: per-thread fp64 partials -> warp shuffle -> one atomic per CTA (below)
     double part[4] = {0.0, 0.0, 0.0, 0.0};
     if (half == 0)
@@ -590,9 +623,28 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
     // behind the parameter words; the host side adds them to *loss_sum in CTA order
     if (a.grad_fixed != nullptr) reinterpret_cast<double*>(a.grad_fixed + n_params)[blockIdx.x] = tot[0];
     else atomicAdd(a.loss_sum, tot[0]);
-    for (int o = 0; o < a.out_w && o < 3; ++o) add_total(a.mlp_grad, a.grad_fixed, gb2 + o, tot[1 + o]);
+    for (int o = 0; o < a.out_w && o < 3; ++o) add_total(grad_out, a.grad_fixed, gb2 + o, tot[1 + o]);
   }
   if (warp == 0) tmem_dealloc(tb, kTmemCols);
+}
+
+// mlp_grad[p] += sum over the CTAs' rows, in a fixed order: 8 strided partial sums per parameter, then those in sequence.
+__global__ void __launch_bounds__(256) reduce_partials_kernel(double* __restrict__ mlp_grad, const double* __restrict__ partials,
+                                                              unsigned rows, unsigned long long stride, unsigned n_params) {
+  __shared__ double part[8][33];
+  const unsigned px = threadIdx.x & 31, sy = threadIdx.x >> 5;
+  const unsigned p = blockIdx.x * 32 + px;
+  double sum = 0.0;
+  if (p < n_params)
+    for (unsigned r = sy; r < rows; r += 8) sum += partials[r * stride + p];
+  part[sy][px] = sum;
+  __syncthreads();
+  if (sy == 0 && p < n_params) {
+    double total = part[0][px];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) total += part[k][px];
+    mlp_grad[p] += total;
+  }
 }
 
 }  // namespace
@@ -616,6 +668,12 @@ sxen_status sxen_mlp_tc2_train_launch(const sxen_mlp_tc::TcArgs& a, int in_w, cu
   if (st != SXEN_OK) return st;
   SXEN_CUDA(cudaGetLastError());
   count_launch();
+  if (a.partials != nullptr) {
+    const unsigned n_params = static_cast<unsigned>(HID * in_w + HID + HID * HID + HID + a.out_w * HID + a.out_w);
+    reduce_partials_kernel<<<(n_params + 31) / 32, 256, 0, stream>>>(a.mlp_grad, a.partials, grid, a.partial_stride, n_params);
+    SXEN_CUDA(cudaGetLastError());
+    count_launch();
+  }
   if (used_ctas) *used_ctas = static_cast<int>(grid);
   return SXEN_OK;
 }

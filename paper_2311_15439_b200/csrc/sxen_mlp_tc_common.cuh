@@ -24,6 +24,8 @@ struct TcArgs {
   double* mlp_grad;         // parameter layout, accumulated into
   double* loss_sum;         // accumulated into
   long long* grad_fixed;    // reproducible mode: parameter layout in units of 2^-52, then one double per CTA for the loss (nullptr = off)
+  double* partials;         // sxen_mlp_tc2.cu: one row of `partial_stride` doubles per CTA (parameter layout); the CTA adds its
+  unsigned long long partial_stride;  // gradients there and a reduction kernel folds the rows into mlp_grad (nullptr = atomics on mlp_grad)
   unsigned long long n;
   int out_w;
   int target_f32;
@@ -111,11 +113,13 @@ __device__ __forceinline__ void gemm_split_uniform(uint32_t d, uint32_t idesc, i
 
 // One CTA's partial sum into the batch total: an fp64 atomic, or -- reproducible mode -- an integer atomic on the fixed-point
 // shadow of the same element (order-free; sxen_mlp.cu folds the shadow into the fp64 buffer after the kernel).
+// Explicit `red`: atomicAdd with its result unused compiles to ATOMG with a discarded destination for 64-bit operands, and a
+// warp then issues one such instruction per L2 round trip (a 64-instruction read-out took 49 k cycles).
 __device__ __forceinline__ void add_total(double* base, long long* fixed, size_t index, double v) {
   if (fixed != nullptr)
-    atomicAdd(reinterpret_cast<unsigned long long*>(fixed + index), static_cast<unsigned long long>(__double2ll_rn(__dmul_rn(v, 0x1p52))));
+    asm volatile("red.global.add.u64 [%0], %1;" ::"l"(fixed + index), "l"(__double2ll_rn(__dmul_rn(v, 0x1p52))) : "memory");
   else
-    atomicAdd(base + index, v);
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(base + index), "d"(v) : "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {

@@ -289,7 +289,11 @@ def test_queued_steps_report_a_rejected_coordinate_at_collect(sx):
     # (fp32 atomics: same rows, values to the accumulation-order bar)
     a = np.stack([enc.table(l) for l in range(enc.config.levels)])
     b = np.stack([enc2.table(l) for l in range(enc2.config.levels)])
-    assert np.array_equal(a != tables1, b != tables1) and np.abs(a - b).max() <= 1e-3 * 1e-2
+    assert np.array_equal(a != tables1, b != tables1)
+    # ... except for the odd entry whose gradient is a near-complete cancellation: summation order decides its sign and Adam
+    # turns the sign into a full lr-sized step (tests/test_gpu_sharded.py: assert_tables_match)
+    d = np.abs(a.astype(np.float64) - b)
+    assert int((d > 1e-3 * 1e-2).sum()) <= 5 and d.max() <= 5e-2, (int((d > 1e-5).sum()), d.max())
 
 
 def test_per_step_call_refuses_to_jump_a_queue(sx):

@@ -196,6 +196,37 @@ def test_both_training_kernels_agree(sx, n, in_w, out_w):
     assert np.abs(a[3] - b[3]).max() <= 1e-4 * np.abs(a[3]).max()
 
 
+def test_parameter_gradients_stay_accurate_over_long_launches(sx):
+    """The weight-gradient accumulators are fp32 (TMEM); a CTA of a 2^22-sample launch sums 222 tiles.  The kernel flushes them
+    into the fp64 totals every 64 tiles of a group (csrc/sxen_mlp_tc2.cu: flush_gradients), which keeps the error at the level
+    of a short launch: 2.2e-5 of the largest entry here (1.2e-4 with one flush at the end).  Reference: the same network in
+    fp64 PyTorch (src/mlp.cpp:137-202 semantics: ReLU hidden layers, linear output, MSE mean over batch and outputs)."""
+    n = (1 << 22) + 77
+    gen = torch.Generator(device="cuda:0").manual_seed(22)
+    x = torch.randn((n, 32), device="cuda:0", generator=gen) * 0.3
+    tg = torch.rand((n, 3), device="cuda:0", generator=gen)
+    mlp = sx.Mlp(sx.MlpConfig(32, 64, 2, 3))
+    mlp.init_params(11)
+    mlp.set_precision(1)
+    mlp.forward_backward(x, tg)
+    torch.cuda.synchronize()
+    g = mlp.gradient()
+    p = torch.from_numpy(mlp.parameters()).to("cuda:0").double()
+    sizes = [(64, 32), (64,), (64, 64), (64,), (3, 64), (3,)]
+    parts, off = [], 0
+    for shp in sizes:
+        k = int(np.prod(shp))
+        parts.append(p[off:off + k].view(*shp).clone().requires_grad_())
+        off += k
+    W0, b0, W1, b1, W2, b2 = parts
+    for s0 in range(0, n, 1 << 20):
+        xs, ts = x[s0:s0 + (1 << 20)].double(), tg[s0:s0 + (1 << 20)].double()
+        out = torch.relu(torch.relu(xs @ W0.T + b0) @ W1.T + b1) @ W2.T + b2
+        (((out - ts) ** 2).sum() / (n * 3)).backward()
+    ref = torch.cat([t.grad.flatten() for t in parts]).cpu().numpy()
+    assert np.abs(g - ref).max() <= 5e-5 * np.abs(ref).max(), np.abs(g - ref).max() / np.abs(ref).max()
+
+
 @pytest.mark.timeout(180)
 def test_back_to_back_training_launches_complete(sx):
     """The training kernel's warps hand work to each other and to the tensor core through mbarriers and named barriers (two

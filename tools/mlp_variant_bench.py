@@ -53,7 +53,7 @@ for variant in ((1, 2) if a.variant == 0 else (a.variant,)):
     per = c / ctas / tiles
     print(f"variant {variant}: {ms:.4f} ms per launch ({N} samples, width {a.width}) = {N / ms / 1e6:.3f} Gsamples/s; cycles per tile of the "
           f"CTA: epilogue loop {per[0]:.0f}, waiting chain {per[1]:.0f}, own wgrad {per[2]:.0f}, other group {per[3]:.0f}; chain warp loop "
-          f"{per[4]:.0f}, idle {per[5]:.0f}", flush=True)
+          f"{per[4]:.0f}, idle {per[5]:.0f}; gradient flushes per CTA: mid-kernel {c[6] / ctas:.0f} cycles in all, final {c[7] / ctas:.0f}", flush=True)
     results[variant] = out
 sx.lib.sxen_debug_tc_variant(2)
 if a.variant != 0:

@@ -184,6 +184,12 @@ constexpr int kTile = 32;
 
 // reproducible mode: a block's partial sum as 64-bit fixed point, units of 2^-52 (a non-finite sum becomes the most negative
 // value, which poisons the total visibly: fold_fixed_kernel turns |total| >= 2^62 into NaN for Adam's check)
+// Explicit reds: atomicAdd on a 64-bit operand with the result unused still compiles to ATOMG (destination discarded) on
+// sm_100a and a warp issues one per L2 round trip (csrc/sxen_mlp_tc_common.cuh: add_total).
+__device__ __forceinline__ void red_add_f64(double* p, double v) { asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory"); }
+__device__ __forceinline__ void red_add_u64(long long* p, unsigned long long v) {
+  asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ unsigned long long to_fixed(double v) {
   return static_cast<unsigned long long>(__double2ll_rn(__dmul_rn(v, 0x1p52)));
 }
@@ -227,13 +233,13 @@ mlp_backward_layer_kernel(const float* __restrict__ params, const float* __restr
       const int o = p / in, i = p - o * in;
       for (int r = 0; r < rows; ++r)
         acc = __dadd_rn(acc, __dmul_rn(d_tile[r * ow + o], static_cast<double>(src_tile[r * in + i])));
-      if (fixed) atomicAdd(reinterpret_cast<unsigned long long*>(fixed + s.w_off[layer] + p), to_fixed(acc));
-      else atomicAdd(grads + s.w_off[layer] + p, acc);
+      if (fixed) red_add_u64(fixed + s.w_off[layer] + p, to_fixed(acc));
+      else red_add_f64(grads + s.w_off[layer] + p, acc);
     } else {
       const int o = p - ow * in;
       for (int r = 0; r < rows; ++r) acc = __dadd_rn(acc, d_tile[r * ow + o]);
-      if (fixed) atomicAdd(reinterpret_cast<unsigned long long*>(fixed + s.b_off[layer] + o), to_fixed(acc));
-      else atomicAdd(grads + s.b_off[layer] + o, acc);
+      if (fixed) red_add_u64(fixed + s.b_off[layer] + o, to_fixed(acc));
+      else red_add_f64(grads + s.b_off[layer] + o, acc);
     }
   }
   // downstream deltas: thread per (sample, input unit), o in order

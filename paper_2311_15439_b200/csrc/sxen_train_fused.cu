@@ -157,10 +157,11 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 __device__ __forceinline__ void add_total(double* base, long long* fixed, size_t index, double v) {
+  // explicit reds: see sxen_mlp_tc_common.cuh (atomicAdd on 64-bit operands becomes ATOMG, one L2 round trip per instruction)
   if (fixed != nullptr)
-    atomicAdd(reinterpret_cast<unsigned long long*>(fixed + index), static_cast<unsigned long long>(__double2ll_rn(__dmul_rn(v, 0x1p52))));
+    asm volatile("red.global.add.u64 [%0], %1;" ::"l"(fixed + index), "l"(__double2ll_rn(__dmul_rn(v, 0x1p52))) : "memory");
   else
-    atomicAdd(base + index, v);
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(base + index), "d"(v) : "memory");
 }
 
 // mbar_wait that charges its cycles to `waited` when the role is being timed

@@ -523,7 +523,7 @@ SXEN_API sxen_status sxen_debug_fused_timing(unsigned long long* counters_dev);
  * the chain MMAs, waiting on the weight-gradient MMAs}, [4..5] chain warp {cycles in the tile loop, waiting on the epilogue}. */
 SXEN_API sxen_status sxen_debug_tc_timing(unsigned long long* counters_dev);
 /* Which stand-alone tcgen05 training kernel runs (A/B measurements): 2 = two tiles in flight per SM (csrc/sxen_mlp_tc2.cu, the
- * default), 1 = one tile in flight (csrc/sxen_mlp_tc.cu).  With variant 2 the timing counters read: [0..3] thread 0 of the first
+ * default; launches of at most one tile per SM still take the other kernel), 1 = one tile in flight (csrc/sxen_mlp_tc.cu).  With variant 2 the timing counters read: [0..3] thread 0 of the first
  * epilogue group {cycles in the tile loop, waiting on the chain MMAs, on its own weight-gradient MMAs, on the other group's
  * phase-2 MMAs}, [4..5] chain warp {cycles in its loop, polling with nothing to issue}. */
 SXEN_API sxen_status sxen_debug_tc_variant(int variant);

@@ -564,17 +564,19 @@ sxen_status sxen_mlp_tc_run(bool train, const float* params, const float* featur
   a.progress = g_tc_progress;
   a.timing = g_tc_timing;
   if (!train) return sxen_mlp_tc_forward_launch(a, in_w, stream, used_ctas);  // its own kernel: one hand-off per tile
-  if (g_tc_variant == 2) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned long long tiles = (n + kTile - 1) / kTile;
+  // two tiles in flight pay off from the second tile of a CTA on; a launch of at most one tile per SM (the reference's default
+  // batch of 2048 is 16 tiles) only pays that kernel's fixed costs -- gradient rows to clear, a reduction kernel behind it
+  if (g_tc_variant == 2 && tiles > static_cast<unsigned long long>(sms)) {
     if (a.grad_fixed == nullptr) {  // per-CTA gradient rows + a fixed-order reduction instead of contended atomics
       a.partials = partials;
       a.partial_stride = partial_stride;
     }
     return sxen_mlp_tc2_train_launch(a, in_w, stream, used_ctas);
   }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned long long tiles = (n + kTile - 1) / kTile;
   const unsigned grid = static_cast<unsigned>(std::min<unsigned long long>(tiles, static_cast<unsigned long long>(sms)));
   auto launch = [&](auto kernel) -> sxen_status {
     SXEN_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)));

@@ -15,7 +15,8 @@ import oracle
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-TC3_RTOL = 3e-5   # ~2^-16 per operand, three layers deep
+TC3_RTOL = 1.5e-5   # measured: predictions 6.2e-6 .. 1.1e-5 of the largest, input gradients 8e-6 at the 99.9th percentile (1e-5)
+TC3_SUM_RTOL = 3e-5   # parameter gradients: batch sums with cancellation, plus the odd ReLU flip (see the test)
 TC1_RTOL = 3e-2   # bf16: 2^-8 per operand
 
 
@@ -111,17 +112,18 @@ def test_tensor_core_mlp_matches_oracle(sx, oracle_lib, mode, rtol, n, out_w, in
                   acts[:, in_w + 64:in_w + 128].astype(np.float64))
     d2 = (up @ W2) * (h2 > 0)
     d1 = (d2 @ W1) * (h1 > 0)
+    srtol = TC3_SUM_RTOL if mode == 1 else rtol
     off = 0
     for l, (delta, src) in enumerate([(d1, x0), (d2, h1), (up, h2)]):
         o_w, i_w = delta.shape[1], src.shape[1]
         wscale = np.abs(delta).T @ np.abs(src)
         flip = 3 * np.abs(up).max() * np.abs(W2).max() * 64 * np.abs(W1).max() * np.abs(src).max() if mode == 1 else np.inf
         blk, ref = g[off:off + o_w * i_w].reshape(o_w, i_w), wg[off:off + o_w * i_w].reshape(o_w, i_w)
-        assert (np.abs(blk - ref) <= 2 * rtol * wscale + flip).all(), (l, "weights", np.abs(blk - ref).max())
-        assert np.linalg.norm(blk - ref) <= 10 * rtol * np.linalg.norm(ref), (l, np.linalg.norm(blk - ref) / np.linalg.norm(ref))
+        assert (np.abs(blk - ref) <= 2 * srtol * wscale + flip).all(), (l, "weights", np.abs(blk - ref).max())
+        assert np.linalg.norm(blk - ref) <= 10 * srtol * np.linalg.norm(ref), (l, np.linalg.norm(blk - ref) / np.linalg.norm(ref))
         off += o_w * i_w
         bref = wg[off:off + o_w]
-        assert np.linalg.norm(g[off:off + o_w] - bref) <= 10 * rtol * np.linalg.norm(bref) + 1e-12, (l, "biases")
+        assert np.linalg.norm(g[off:off + o_w] - bref) <= 10 * srtol * np.linalg.norm(bref) + 1e-12, (l, "biases")
         off += o_w
     # f32 targets take the same path
     mlp.clear_gradient()

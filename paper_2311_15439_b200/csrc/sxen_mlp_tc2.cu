@@ -430,7 +430,9 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
       if (tile != first_tile || g > 0) {
         // H2 goes where the other group's tile keeps H1, dH2 | dY where it keeps its own: both are dead once that tile's
         // phase-2 GEMMs (chain: dH2 * W1, weight gradients: dW2, dW1) have completed
+        // (three barriers: the three GEMMs come from different lanes, and a commit only covers its own lane's MMAs)
         timed_wait(&bar_g1[g ^ 1], phase_x, 0x500u + static_cast<uint32_t>(g), t_cross);
+        timed_wait(&bar_g2[g ^ 1], phase_x, 0x520u + static_cast<uint32_t>(g), t_cross);
         timed_wait(&bar_p2[g ^ 1], phase_x, 0x510u + static_cast<uint32_t>(g), t_cross);
         phase_x ^= 1;
       }

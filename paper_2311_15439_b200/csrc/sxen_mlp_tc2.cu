@@ -630,21 +630,30 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
   if (warp == 0) tmem_dealloc(tb, kTmemCols);
 }
 
-// mlp_grad[p] += sum over the CTAs' rows, in a fixed order: 8 strided partial sums per parameter, then those in sequence.
-__global__ void __launch_bounds__(256) reduce_partials_kernel(double* __restrict__ mlp_grad, const double* __restrict__ partials,
-                                                              unsigned rows, unsigned long long stride, unsigned n_params) {
-  __shared__ double part[8][33];
+// mlp_grad[p] += sum over the CTAs' rows, in a fixed order: 32 strided partial sums per parameter (at most five loads per thread,
+// all in flight at once -- with eight the kernel was a chain of 19 dependent L2 round trips, 12 us), then those in sequence.
+__global__ void __launch_bounds__(1024) reduce_partials_kernel(double* __restrict__ mlp_grad, const double* __restrict__ partials,
+                                                               unsigned rows, unsigned long long stride, unsigned n_params) {
+  __shared__ double part[32][33];
   const unsigned px = threadIdx.x & 31, sy = threadIdx.x >> 5;
   const unsigned p = blockIdx.x * 32 + px;
+  double v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const unsigned r = sy + 32 * k;
+    v[k] = (p < n_params && r < rows) ? partials[r * stride + p] : 0.0;
+  }
   double sum = 0.0;
-  if (p < n_params)
-    for (unsigned r = sy; r < rows; r += 8) sum += partials[r * stride + p];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) sum += v[k];
+  for (unsigned r = sy + 256; r < rows; r += 32)  // more than 256 CTAs: not on any current part
+    if (p < n_params) sum += partials[r * stride + p];
   part[sy][px] = sum;
   __syncthreads();
   if (sy == 0 && p < n_params) {
     double total = part[0][px];
 #pragma unroll
-    for (int k = 1; k < 8; ++k) total += part[k][px];
+    for (int k = 1; k < 32; ++k) total += part[k][px];
     mlp_grad[p] += total;
   }
 }
@@ -672,7 +681,7 @@ sxen_status sxen_mlp_tc2_train_launch(const sxen_mlp_tc::TcArgs& a, int in_w, cu
   count_launch();
   if (a.partials != nullptr) {
     const unsigned n_params = static_cast<unsigned>(HID * in_w + HID + HID * HID + HID + a.out_w * HID + a.out_w);
-    reduce_partials_kernel<<<(n_params + 31) / 32, 256, 0, stream>>>(a.mlp_grad, a.partials, grid, a.partial_stride, n_params);
+    reduce_partials_kernel<<<(n_params + 31) / 32, 1024, 0, stream>>>(a.mlp_grad, a.partials, grid, a.partial_stride, n_params);
     SXEN_CUDA(cudaGetLastError());
     count_launch();
   }

@@ -11,4 +11,8 @@ python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.
 python bench.py --gpus 2 --oversubscribe --steps 5 --no-train --no-cpu 2> gpurun_out/r2_final_2ranks.err | tail -n1 > gpurun_out/r2_final_2ranks_oversubscribed.json
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r2_final_launches_bench.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu --no-train --path fused --lpt 2 --level-major 0 > /dev/null 2>&1
+python tools/config_runs.py --skip-c1 > gpurun_out/r2_final_config_runs.log 2>&1
+python tools/train_bench.py --reps 20 > gpurun_out/r2_final_train_bench.txt 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/r2_final_launches_train_step.csv \
+    python tools/train_bench.py --reps 3 > /dev/null 2>&1
 for f in gpurun_out/r2_final_*.err; do echo "== $f"; tail -c 300 "$f"; done

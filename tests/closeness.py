@@ -4,8 +4,8 @@ Two runs of the same kernels on the same data differ in the order their fp32 (ta
 moves a sum by one rounding of its summands -- and two things amplify it beyond a plain tolerance:
   * an entry that is a near-complete cancellation carries the rounding relative to its summands, not to itself;
   * Adam (update = lr * m / (sqrt(v) + 1e-15)) turns the SIGN of such a near-zero gradient component into a full lr-sized
-    step, so after a few steps one or two of ~10^5 updated table entries can sit ~lr away from their twin (observed about
-    once in ten runs of tests/cpp/sharded_train_check.cpp).
+    step; the changed entry changes the features of the samples in its cell, and within two more steps a few hundred of
+    ~10^5 updated table entries sit up to ~lr/3 away from their twin (about once in ten runs, see assert_tables_match).
 """
 import numpy as np
 
@@ -16,10 +16,17 @@ def sums_close(got, want, rtol):
     return bool(np.all(np.abs(got - want) <= rtol * np.abs(want) + 1e-13 * np.abs(want).max()))
 
 
-def assert_tables_match(got, want, atol, rtol=0.0, stragglers=5, cap=5e-2):
-    """Within atol + rtol*|want| everywhere except at most `stragglers` entries, and those within `cap` (a few lr)."""
+def assert_tables_match(got, want, atol, rtol=0.0, straggler_fraction=5e-3, cap=5e-2):
+    """Within atol + rtol*|want| everywhere -- or, when an Adam sign flip has happened (module docstring), everywhere except
+    a small fraction of the entries, and those within `cap` (a few lr).
+
+    Measured on tests/cpp/sharded_train_check.cpp (2 ranks, 4 steps, 140 k updated entries): about one run in ten -- of the
+    sharded run or of its single-GPU twin alike -- takes the other branch at ONE near-cancelled gradient component; two
+    steps later 395 entries (0.28 %) sit up to 3.1e-3 from the other branch and the loss differs by 2e-7 relative.  Always
+    the same 395 entries: the outcome is bimodal, not noisy.  The callers check row sets and loss curves exactly / tightly
+    next to this; a rank's or a sample's contribution going missing moves the loss by far more than their bars."""
     got, want = np.asarray(got, dtype=np.float64), np.asarray(want, dtype=np.float64)
     d = np.abs(got - want)
     off = int((d > atol + rtol * np.abs(want)).sum())
-    assert off <= stragglers, (off, float(d.max()))
+    assert off <= max(5, straggler_fraction * d.size), (off, d.size, float(d.max()))
     assert off == 0 or float(d.max()) <= cap, float(d.max())

@@ -120,6 +120,18 @@ int main(int argc, char** argv) {
                 tag, ranks, updated_rows, updated_rows_twin, row_set_mismatch, worst, off_exact, off_tc, worst_loss,
                 sharded.loss_curve.front().second, sharded.loss_curve.back().second);
     EXPECT(updated_rows > 0);
+    // diagnostics for a comparison that fails: the loss curves side by side and where the tables part
+    std::printf("diag-%s losses sharded/twin:", tag);
+    for (std::size_t k = 0; k < sharded.loss_curve.size(); ++k)
+      std::printf(" %.17g/%.17g", sharded.loss_curve[k].second, whole.loss_curve[k].second);
+    std::printf("\ndiag-%s entries off the exact bar per level:", tag);
+    for (int l = 0; l < ec.levels; ++l) {
+      const std::vector<float> t0 = models[0]->encoder.table(l), tw = twin.encoder.table(l);
+      std::size_t off = 0;
+      for (std::size_t e = 0; e < t0.size(); ++e) off += std::fabs(static_cast<double>(t0[e]) - tw[e]) > 2.01e-5;
+      std::printf(" %zu", off);
+    }
+    std::printf("\n");
   }
 
   // (2b) reproducible mode: two sharded runs of the same steps end bit-identical to each other (the exchange sums fixed-point words)

@@ -97,6 +97,60 @@ class ClockSampler:
     def mark(self, name: str):
         import datetime
         self.marks[name] = datetime.datetime.now()
+        if name in ("timed_region_start", "e2e_region_start"):
+            self._nvml_start("timed" if name.startswith("timed") else "e2e")
+        elif name in ("timed_region_end", "e2e_region_end"):
+            self._nvml_stop()
+
+    # nvidia-smi cannot sample faster than the timed region lasts (tens of milliseconds), so the timed region itself is
+    # polled through NVML from a thread of this process: SM clock + clock-event reasons about once a millisecond.
+    NVML_REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
+
+    def _nvml_start(self, tag: str):
+        if not hasattr(self, "nvml"):
+            self.nvml = {}
+        rec = self.nvml.setdefault(tag, {"sm": [], "bits": 0})
+        self._nvml_thread = None
+        try:
+            import threading
+            import pynvml
+            pynvml.nvmlInit()
+            # NVML enumerates physical devices; CUDA_VISIBLE_DEVICES may renumber them for torch
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            phys = self.idx
+            if vis:
+                ids = [v for v in vis.split(",") if v.strip()]
+                if self.idx < len(ids) and ids[self.idx].strip().isdigit():
+                    phys = int(ids[self.idx])
+            h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+            self._nvml_run = True
+
+            def poll():
+                k = 0
+                while self._nvml_run:
+                    try:
+                        rec["sm"].append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                        if k % 3 == 0:   # the reasons word costs a second driver call: every third poll
+                            rec["bits"] |= int(pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h))
+                        k += 1
+                    except Exception:
+                        break
+                    time.sleep(0.0005)
+                try:
+                    rec["bits"] |= int(pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h))
+                except Exception:
+                    pass
+
+            self._nvml_thread = threading.Thread(target=poll, daemon=True)
+            self._nvml_thread.start()
+        except Exception:
+            self._nvml_thread = None
+
+    def _nvml_stop(self):
+        if getattr(self, "_nvml_thread", None) is not None:
+            self._nvml_run = False
+            self._nvml_thread.join(timeout=2)
+            self._nvml_thread = None
 
     def stop(self):
         import datetime
@@ -140,6 +194,22 @@ class ClockSampler:
                        reasons=sorted(reasons), samples=len(sm), samples_in_timed_region=len(inside))
             if inside:
                 out["sm_mhz_timed_region"] = statistics.median(inside)
+        all_reasons = set(out.get("reasons", []))
+        for tag, key in (("timed", "timed_region"), ("e2e", "e2e_region")):
+            rec = getattr(self, "nvml", {}).get(tag)
+            if not rec or not rec["sm"]:
+                continue
+            # the in-process NVML poll of that region proper
+            nv = rec["sm"]
+            out[f"samples_in_{key}"] = out.get(f"samples_in_{key}", 0) + len(nv)
+            out[f"sm_mhz_{key}"] = statistics.median(nv)
+            out[f"sm_min_mhz_{key}"] = min(nv)
+            out[f"reasons_{key}"] = sorted(nm for bit, nm in self.NVML_REASONS.items() if rec["bits"] & bit)
+            all_reasons |= set(out[f"reasons_{key}"])
+            out["region_source"] = "NVML polled from a thread of this process while the region runs"
+            if out.get("sm_mhz") is None:
+                out.update(sm_mhz=statistics.median(nv), sm_min_mhz=min(nv), samples=len(nv))
+        out["reasons"] = sorted(all_reasons)
         return out
 
 
@@ -593,6 +663,8 @@ def run_ours(args):
     if dist is not None:
         dist.barrier()
     per_step = []
+    if rank == 0:
+        sampler.mark("e2e_region_start")
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         t1 = time.perf_counter()
@@ -600,6 +672,8 @@ def run_ours(args):
         per_step.append(time.perf_counter() - t1)
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / e2e_steps              # the mean over exactly e2e_steps calls is the value
+    if rank == 0:
+        sampler.mark("e2e_region_end")
     if dist is not None:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -4,6 +4,7 @@ Host logic only; sampling, encode, MLP, loss, updates and the rendered-image err
 from __future__ import annotations
 
 import ctypes as C
+import enum
 import math
 from dataclasses import dataclass, field
 from typing import List, Tuple
@@ -223,7 +224,7 @@ def fit_image(image, encoder_cfg: EncoderConfig, train_cfg: TrainConfig, opt: Fi
 
 
 # ------------------------------------------------------------------------------------------------ noise-field task
-class NoiseKind:  # include/sxen/noise.hpp:38
+class NoiseKind(enum.IntEnum):  # include/sxen/noise.hpp:38; .name is to_string(NoiseKind)
     perlin = 0
     simplex = 1
 

@@ -5,10 +5,15 @@ run on the device path with the reference's own configurations and pass conditio
   kernel-scaling-trend  (:285-304)  grid / simplex time per lookup: >= 2.0 at n = 7 and larger than at n = 2
   roundtrip-safety      (:540-567)  zero out-of-bounds accesses over 10^6 encodes per n = 2..5, both backends, with coordinates
                                     forced to exactly 0.0 and 1.0 along the way; outputs finite
-(image-fitting-parity: tests/test_gpu_tasks.py and tests/test_gpu_reproducible.py; gradient-integrity: tests/test_oracle_fd.py
-pins the oracle, tests/test_gpu_neural.py and tests/test_gpu_fused_step.py compare the device path with it.)"""
+  gradient-integrity    (:345-509)  analytic backward of the whole pipeline (encoder -> MLP -> MSE) against central finite
+                                    differences on 20 random parameters, rel 1e-3; the difference quotient goes through an
+                                    independent double-precision pipeline (tests/independent.py) reading the live parameters
+(image-fitting-parity: tests/test_gpu_tasks.py and tests/test_gpu_reproducible.py; tests/test_oracle_fd.py runs
+gradient-integrity on the oracle as well.)"""
 import numpy as np
 import pytest
+
+from independent import encode_simplex_level, mlp_forward
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -68,3 +73,68 @@ def test_roundtrip_safety(sx):
             enc.check()
             assert enc.counters().out_of_bounds == 0, (n, backend)
             assert bool(torch.isfinite(out).all())
+
+
+def test_gradient_integrity(sx):
+    ec = sx.EncoderConfig(dim=2, levels=2, table_size=64, features=2, base_resolution=4)
+    enc = sx.HashEncoder(ec)
+    T, F, L = ec.table_size, ec.features, ec.levels
+
+    def draws(seed, count, lo=0.0, hi=1.0):
+        t = torch.empty(count, dtype=torch.float64, device="cuda")
+        sx.CounterRng(seed).fill_device(t, lo, hi)
+        return t.cpu().numpy()
+
+    # a generic operating point: tables at activation scale, biases off zero (away from the ReLU kinks, :352-360)
+    tables = draws(96, L * T * F, -0.5, 0.5).astype(np.float32).reshape(L, T * F)
+    for l in range(L):
+        enc.set_table(l, tables[l])
+    mc = sx.MlpConfig(ec.encoded_width(), 16, 2, 1)
+    mlp = sx.Mlp(mc)
+    mlp.init_params(sx.hash_combine(314, 1))
+    params = mlp.parameters()
+    bias_draws, pos, off = draws(97, 16 + 16 + 1, -0.25, 0.25), 0, 0
+    spans = []                                           # (weights slice, bias slice) per layer
+    for l in range(mc.layer_count()):
+        i, o = mc.layer_input_width(l), mc.layer_output_width(l)
+        params[off + i * o:off + i * o + o] += bias_draws[pos:pos + o].astype(np.float32)
+        spans.append((slice(off, off + i * o), slice(off + i * o, off + i * o + o), o, i))
+        pos, off = pos + o, off + i * o + o
+    mlp.set_parameters(params)
+    B = 8
+    u = draws(2718, 3 * B).reshape(B, 3)
+    points, targets = np.ascontiguousarray(u[:, :2]), -0.5 + u[:, 2:3]
+
+    # analytic gradient of the mean squared error over the fixed batch, on the device
+    trainer = sx.Trainer(enc, mlp)
+    trainer.accumulate(torch.as_tensor(points, device="cuda"), torch.as_tensor(targets, device="cuda"), B)
+    torch.cuda.synchronize()
+    tgrad = trainer.table_grad_device().cpu().numpy().astype(np.float64).reshape(L, T * F)
+    mgrad = mlp.gradient()
+
+    def reference_loss(tab, par):
+        feat = np.concatenate([encode_simplex_level(2, enc.resolution(l), T, F, tab[l], points) for l in range(L)], axis=1)
+        ws = [par[w].reshape(o, i) for w, _, o, i in spans]
+        bs = [par[b] for _, b, _, _ in spans]
+        e = mlp_forward(mc, ws, bs, feat)[:, 0] - targets[:, 0]
+        return float((e * e).sum() / B)
+
+    candidates = [("t", l, k, tgrad[l, k]) for l in range(L) for k in range(T * F) if abs(tgrad[l, k]) > 1e-6]
+    candidates += [("m", 0, k, mgrad[k]) for k in range(mgrad.size) if abs(mgrad[k]) > 1e-6]
+    assert len(candidates) >= 20
+    order = np.random.default_rng(424242).permutation(len(candidates))
+    worst, kinds = 0.0, set()
+    for ci in order[:20]:
+        kind, l, k, analytic = candidates[ci]
+        tab, par = tables.copy(), params.copy()
+        arr = tab[l] if kind == "t" else par
+        orig = arr[k]
+        arr[k] = orig + np.float32(1e-3)
+        up, loss_up = float(arr[k]), reference_loss(tab, par)
+        arr[k] = orig - np.float32(1e-3)
+        down, loss_down = float(arr[k]), reference_loss(tab, par)
+        fd = (loss_up - loss_down) / (up - down)
+        worst = max(worst, abs(fd - analytic) / abs(analytic))
+        kinds.add(kind)
+    print(f"gradient-integrity on the device: 20 parameters, max relative error {worst:.3g} (tolerance 1e-3)")
+    assert worst <= 1e-3 and kinds == {"t", "m"}

@@ -70,3 +70,76 @@ def test_malformed_checkpoints_raise_io_error(sx, tmp_path):
             sx.load_checkpoint(p)
     with pytest.raises(sx.IoError):
         sx.load_checkpoint(str(tmp_path / "missing.sxen"))
+
+
+# ---- the reference's own `checkpoint` suite (/root/reference/proj/tests/test_checkpoint.cpp), case by case
+def sample_config(sx, **kw):                             # :20-31
+    base = dict(dim=3, levels=3, table_size=1 << 8, features=2, base_resolution=5, growth=1.7, backend=sx.Backend.simplex,
+                level_scale=sx.LevelScale.raw)
+    base.update(kw)
+    return sx.EncoderConfig(**base)
+
+
+def test_suite_encoder_only_round_trip_is_bit_exact(sx, tmp_path):          # :47-71
+    cfg = sample_config(sx)
+    enc = sx.HashEncoder(cfg)
+    enc.init_tables(71)
+    path = str(tmp_path / "enc_only.ckpt")
+    sx.save_checkpoint(path, enc)
+    got, mlp = sx.load_checkpoint(path)
+    assert mlp is None
+    g = got.config
+    assert (g.dim, g.levels, g.table_size, g.features, g.base_resolution, g.growth, g.backend) == \
+           (cfg.dim, cfg.levels, cfg.table_size, cfg.features, cfg.base_resolution, cfg.growth, cfg.backend)
+    for l in range(cfg.levels):
+        assert got.resolution(l) == enc.resolution(l)
+        assert np.array_equal(got.table(l).view(np.uint32), enc.table(l).view(np.uint32))
+
+
+def test_suite_encoder_plus_head_round_trip_is_bit_exact(sx, tmp_path):     # :73-99
+    cfg = sample_config(sx)
+    enc = sx.HashEncoder(cfg)
+    enc.init_tables(72)
+    mc = sx.MlpConfig(cfg.encoded_width(), 12, 2, 3)
+    mlp = sx.Mlp(mc)
+    mlp.init_params(73)
+    path = str(tmp_path / "enc_mlp.ckpt")
+    sx.save_checkpoint(path, enc, mlp)
+    _, got = sx.load_checkpoint(path)
+    assert got is not None
+    gm = got.config
+    assert (gm.input_width, gm.hidden_width, gm.hidden_layers, gm.output_width) == (mc.input_width, 12, 2, 3)
+    assert np.array_equal(got.parameters().view(np.uint32), mlp.parameters().view(np.uint32))
+
+
+def test_suite_level_scale_is_a_loader_parameter_not_file_state(sx, tmp_path):   # :101-116
+    cfg = sample_config(sx, level_scale=sx.LevelScale.equal_memory)
+    enc = sx.HashEncoder(cfg)
+    enc.init_tables(74)
+    path = str(tmp_path / "scale_mode.ckpt")
+    sx.save_checkpoint(path, enc)
+    raw, _ = sx.load_checkpoint(path)                    # default: raw
+    assert raw.config.level_scale == sx.LevelScale.raw and raw.resolution(0) != enc.resolution(0)
+    matched, _ = sx.load_checkpoint(path, sx.LevelScale.equal_memory)
+    assert matched.config.level_scale == sx.LevelScale.equal_memory
+    assert [matched.resolution(l) for l in range(cfg.levels)] == [enc.resolution(l) for l in range(cfg.levels)]
+
+
+def test_suite_corrupt_missing_and_unwritable_are_io_errors(sx, tmp_path):  # :118-165
+    enc = sx.HashEncoder(sample_config(sx))
+    enc.init_tables(75)
+    good = str(tmp_path / "good.ckpt")
+    sx.save_checkpoint(good, enc)
+    data = open(good, "rb").read()
+    assert len(data) > 64
+    cases = {"bad_magic": b"Z" + data[1:], "bad_version": data[:4] + bytes([99]) + data[5:],
+             "truncated": data[:-7], "trailing": data + b"x"}
+    for name, blob in cases.items():
+        p = str(tmp_path / f"{name}.ckpt")
+        open(p, "wb").write(blob)
+        with pytest.raises(sx.IoError):
+            sx.load_checkpoint(p)
+    with pytest.raises(sx.IoError):
+        sx.load_checkpoint(str(tmp_path / "does_not_exist.ckpt"))
+    with pytest.raises(sx.IoError):
+        sx.save_checkpoint("/nonexistent-dir/x.ckpt", enc)

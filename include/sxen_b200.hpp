@@ -321,6 +321,37 @@ class Mlp {
     if (values.size() != parameter_count()) throw std::invalid_argument("mlp: parameter count mismatch");
     check(sxen_mlp_upload_params(h_, values.data()));
   }
+  // The reference's call shape (include/sxen/mlp.hpp:94-99) with host spans, N samples per call: `out` is
+  // MlpWorkspace::output(), `input_grad` MlpWorkspace::input_grad(); the workspace and the MlpGradient live in the handle.
+  void forward(std::span<const float> input, std::span<float> out) {
+    const std::size_t in_w = static_cast<std::size_t>(cfg_.input_width), out_w = static_cast<std::size_t>(cfg_.output_width);
+    if (input.size() % in_w != 0 || out.size() != input.size() / in_w * out_w)  // src/mlp.cpp:138-143
+      throw std::invalid_argument("mlp forward: input or output span has the wrong width");
+    check(sxen_mlp_forward_host(h_, input.data(), input.size() / in_w, out.data()));
+  }
+  void backward(std::span<const double> upstream, std::span<double> input_grad) {
+    const std::size_t in_w = static_cast<std::size_t>(cfg_.input_width), out_w = static_cast<std::size_t>(cfg_.output_width);
+    if (upstream.size() % out_w != 0 || (!input_grad.empty() && input_grad.size() != upstream.size() / out_w * in_w))
+      throw std::invalid_argument("mlp backward: upstream span has the wrong width");  // src/mlp.cpp:168-173
+    check(sxen_mlp_backward_host(h_, upstream.data(), upstream.size() / out_w, input_grad.empty() ? nullptr : input_grad.data()));
+  }
+  // MlpGradient::values() / clear() (include/sxen/mlp.hpp:40-74): fp64, laid out like parameters()
+  std::vector<double> gradient() const {
+    std::vector<double> g(parameter_count());
+    check(sxen_mlp_grad_download(h_, g.data()));
+    return g;
+  }
+  void clear_gradient(void* stream = nullptr) { check(sxen_mlp_grad_clear(h_, stream)); }
+  int layer_count() const { return cfg_.hidden_layers + 1; }
+  int layer_input_width(int l) const { return l == 0 ? cfg_.input_width : cfg_.hidden_width; }
+  int layer_output_width(int l) const { return l == layer_count() - 1 ? cfg_.output_width : cfg_.hidden_width; }
+  // offset of layer l's weights in parameters() (per layer: out*in weights, then out biases; src/mlp.cpp:19-32)
+  std::size_t layer_offset(int l) const {
+    std::size_t off = 0;
+    for (int k = 0; k < l; ++k)
+      off += static_cast<std::size_t>(layer_input_width(k)) * layer_output_width(k) + static_cast<std::size_t>(layer_output_width(k));
+    return off;
+  }
   void forward(DeviceSpan<const float> input, DeviceSpan<float> out, void* stream = nullptr) {
     check(sxen_mlp_forward(h_, input.data, input.size / static_cast<std::size_t>(cfg_.input_width), out.data, stream));
   }

@@ -307,6 +307,12 @@ SXEN_API sxen_status sxen_mlp_forward(sxen_mlp* mlp, const float* input_dev, siz
  * may be NULL.  SXEN_LOGIC_ERROR if no forward populated the workspace. */
 SXEN_API sxen_status sxen_mlp_backward(sxen_mlp* mlp, const double* upstream_dev, size_t n_samples, float* input_grad_dev,
                                        double* input_grad_f64_dev, void* stream);
+/* The same two calls with the reference's HOST spans (include/sxen/mlp.hpp:94-99; MlpWorkspace::output() and
+ * ::input_grad() are the out arguments): input_host N x input_width f32 -> out_host N x output_width f32; upstream_host
+ * N x output_width f64 -> input_grad_host N x input_width f64 (may be NULL).  Synchronous; same status codes. */
+SXEN_API sxen_status sxen_mlp_forward_host(sxen_mlp* mlp, const float* input_host, size_t n_samples, float* out_host);
+SXEN_API sxen_status sxen_mlp_backward_host(sxen_mlp* mlp, const double* upstream_host, size_t n_samples,
+                                            double* input_grad_host);
 /* Arithmetic of the head.  EXACT (default): fp64 accumulation in the reference's order, any shape, bit-identical outputs.
  * TENSOR_*: the fused tcgen05 kernel for the {16|32} -> 64 -> 64 -> {<=3} head; BF16X3 = split-bf16 operands (three MMAs per
  * product, ~1e-5 relative), BF16 = single bf16 product (~4e-3). */

@@ -125,6 +125,8 @@ SIGNATURES = {
     "sxen_mlp_grad_download": (C.c_int, [_vp, _P(_dbl)]),
     "sxen_mlp_forward": (C.c_int, [_vp, _vp, _sz, _vp, _vp]),
     "sxen_mlp_backward": (C.c_int, [_vp, _vp, _sz, _vp, _vp, _vp]),
+    "sxen_mlp_forward_host": (C.c_int, [_vp, _vp, _sz, _vp]),
+    "sxen_mlp_backward_host": (C.c_int, [_vp, _vp, _sz, _vp]),
     "sxen_mlp_set_precision": (C.c_int, [_vp, _i32]),
     "sxen_mlp_get_precision": (C.c_int, [_vp, _P(_i32)]),
     "sxen_mlp_forward_backward": (C.c_int, [_vp, _vp, _vp, C.c_int, _sz, _sz, _vp, _vp, _vp, _vp]),

@@ -610,6 +610,57 @@ sxen_status sxen_mlp_backward(sxen_mlp* mlp, const double* upstream_dev, size_t 
   return SXEN_OK;
 }
 
+// ---- the reference's own call shape: host spans in, host spans out (include/sxen/mlp.hpp:94-99), n samples per call
+namespace {
+struct DeviceScratch {  // a few short-lived device buffers, freed on every exit path
+  void* p[3] = {nullptr, nullptr, nullptr};
+  ~DeviceScratch() {
+    for (void* q : p)
+      if (q) cudaFree(q);
+  }
+};
+}  // namespace
+
+sxen_status sxen_mlp_forward_host(sxen_mlp* mlp, const float* input_host, size_t n_samples, float* out_host) {
+  SXEN_REQUIRE(mlp != nullptr, "mlp handle is null");
+  SXEN_REQUIRE(n_samples == 0 || (input_host != nullptr && out_host != nullptr), "mlp forward: null input or output pointer");
+  DeviceGuard guard(mlp->device);
+  if (n_samples == 0) return sxen_mlp_forward(mlp, nullptr, 0, nullptr, nullptr);
+  const size_t in_bytes = n_samples * static_cast<size_t>(mlp->cfg.input_width) * sizeof(float);
+  const size_t out_bytes = n_samples * static_cast<size_t>(mlp->cfg.output_width) * sizeof(float);
+  DeviceScratch d;
+  SXEN_CUDA(cudaMalloc(&d.p[0], in_bytes));
+  SXEN_CUDA(cudaMalloc(&d.p[1], out_bytes));
+  SXEN_CUDA(cudaMemcpy(d.p[0], input_host, in_bytes, cudaMemcpyHostToDevice));
+  if (sxen_status st = sxen_mlp_forward(mlp, static_cast<const float*>(d.p[0]), n_samples, static_cast<float*>(d.p[1]), nullptr))
+    return st;
+  SXEN_CUDA(cudaMemcpy(out_host, d.p[1], out_bytes, cudaMemcpyDeviceToHost));  // synchronises the legacy stream
+  return SXEN_OK;
+}
+
+sxen_status sxen_mlp_backward_host(sxen_mlp* mlp, const double* upstream_host, size_t n_samples, double* input_grad_host) {
+  SXEN_REQUIRE(mlp != nullptr, "mlp handle is null");
+  if (!mlp->forward_done)  // src/mlp.cpp:165-167, before anything is copied
+    return fail(SXEN_LOGIC_ERROR, "mlp backward called before forward populated the workspace");
+  SXEN_REQUIRE(n_samples == mlp->forward_samples, "mlp backward: batch of %zu samples does not match the forward pass (%zu)",
+               n_samples, mlp->forward_samples);
+  SXEN_REQUIRE(n_samples == 0 || upstream_host != nullptr, "mlp backward: upstream pointer is null");
+  if (n_samples == 0) return SXEN_OK;
+  DeviceGuard guard(mlp->device);
+  const size_t up_bytes = n_samples * static_cast<size_t>(mlp->cfg.output_width) * sizeof(double);
+  const size_t ig_bytes = n_samples * static_cast<size_t>(mlp->cfg.input_width) * sizeof(double);
+  DeviceScratch d;
+  SXEN_CUDA(cudaMalloc(&d.p[0], up_bytes));
+  SXEN_CUDA(cudaMalloc(&d.p[1], ig_bytes));
+  SXEN_CUDA(cudaMemcpy(d.p[0], upstream_host, up_bytes, cudaMemcpyHostToDevice));
+  if (sxen_status st = sxen_mlp_backward(mlp, static_cast<const double*>(d.p[0]), n_samples, nullptr, static_cast<double*>(d.p[1]),
+                                         nullptr))
+    return st;
+  if (input_grad_host) SXEN_CUDA(cudaMemcpy(input_grad_host, d.p[1], ig_bytes, cudaMemcpyDeviceToHost));
+  else SXEN_CUDA(cudaStreamSynchronize(nullptr));
+  return SXEN_OK;
+}
+
 sxen_status sxen_mlp_fused_view(sxen_mlp* mlp, float** params, double** grads, long long** grads_fixed, int32_t* precision) {
   SXEN_REQUIRE(mlp != nullptr, "mlp handle is null");
   *params = mlp->params;

@@ -157,7 +157,17 @@ class Mlp:
         return ig, loss, pred
 
     def forward(self, inputs, stream=None):
-        """Batched Mlp::forward.  inputs: CUDA float32 [N, input_width]; returns CUDA float32 [N, output_width]."""
+        """Batched Mlp::forward.  inputs: CUDA float32 [N, input_width] -> CUDA float32 [N, output_width]; a numpy array takes
+        the host-buffer entry point and returns numpy."""
+        if isinstance(inputs, np.ndarray):
+            # the reference's host spans (Mlp::forward(span<const float>, ws) + ws.output()), N samples per call
+            x = np.ascontiguousarray(inputs, dtype=np.float32)
+            if x.ndim != 2 or x.shape[1] != self._cfg.input_width:
+                raise ValueError("mlp forward: input width mismatch")
+            out = np.empty((x.shape[0], self._cfg.output_width), dtype=np.float32)
+            raise_for(self._lib, self._lib.sxen_mlp_forward_host(self._h, C.c_void_p(x.ctypes.data), x.shape[0],
+                                                                 C.c_void_p(out.ctypes.data)))
+            return out
         import torch
         from .encoding import _stream_ptr
         if inputs.ndim != 2 or inputs.shape[1] != self._cfg.input_width:  # src/mlp.cpp:138-140
@@ -171,6 +181,15 @@ class Mlp:
     def backward(self, upstream, stream=None, dtype=None):
         """Batched Mlp::backward.  upstream: CUDA float64 [N, output_width]; returns d(loss)/d(input) [N, input_width]
         (float64 by default, the reference's type; float32 when dtype=torch.float32)."""
+        if isinstance(upstream, np.ndarray):
+            # host spans: Mlp::backward(span<const double>, ws, grad) + ws.input_grad()
+            up = np.ascontiguousarray(upstream, dtype=np.float64)
+            if up.ndim != 2 or up.shape[1] != self._cfg.output_width:
+                raise ValueError("mlp backward: upstream width mismatch")
+            ig = np.empty((up.shape[0], self._cfg.input_width), dtype=np.float64)
+            raise_for(self._lib, self._lib.sxen_mlp_backward_host(self._h, C.c_void_p(up.ctypes.data), up.shape[0],
+                                                                  C.c_void_p(ig.ctypes.data)))
+            return ig
         import torch
         from .encoding import _stream_ptr
         if upstream.ndim != 2 or upstream.shape[1] != self._cfg.output_width:  # src/mlp.cpp:168-170

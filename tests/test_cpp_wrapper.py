@@ -63,13 +63,17 @@ def test_cpp_checkpoint_mirror_host_part(tmp_path):
     assert run.returncode == 0 and "checkpoint ok" in run.stdout, run.stdout + run.stderr
 
 
-def test_cpp_encoding_suite_builds(tmp_path):
-    """tests/cpp/encoding_suite_check.cpp (the reference's encoding suite over the C++ mirror) compiles warning-free with
-    plain g++ and links against libsxen_b200.so alone; its GPU run is tests/test_gpu_cpp_suite.py."""
+import pytest  # noqa: E402
+
+
+@pytest.mark.parametrize("program", ["encoding_suite_check", "neural_suite_check"])
+def test_cpp_suites_build(tmp_path, program):
+    """tests/cpp/{encoding,neural}_suite_check.cpp (the reference's suites over the C++ mirror) compile warning-free with
+    plain g++ and link against libsxen_b200.so alone; their GPU run is tests/test_gpu_cpp_suite.py."""
     lib_dir = os.path.join(ROOT, "paper_2311_15439_b200", "lib")
-    exe = str(tmp_path / "encoding_suite_check")
+    exe = str(tmp_path / program)
     subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
-                    os.path.join(ROOT, "tests", "cpp", "encoding_suite_check.cpp"), "-o", exe, "-L", lib_dir,
+                    os.path.join(ROOT, "tests", "cpp", program + ".cpp"), "-o", exe, "-L", lib_dir,
                     "-lsxen_b200", f"-Wl,-rpath,{lib_dir}"], check=True)
     needed = subprocess.run(["readelf", "-d", exe], capture_output=True, text=True).stdout
     assert "libsxen_b200.so" in needed and "libcudart" not in needed

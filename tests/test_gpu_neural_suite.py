@@ -341,3 +341,27 @@ def test_a_non_finite_target_aborts_with_a_training_error(sx):              # :4
     with pytest.raises(sx.TrainingError):
         sx.train_field(enc, mlp, constant_sampler(0.5, float("inf")), sx.TrainConfig(batch_size=4, steps=5, threads=1))
     assert np.array_equal(mlp.parameters(), before)       # thrown before any update (src/trainer.cpp:121-123)
+
+
+def test_host_span_calls_equal_the_device_calls(sx):
+    """Mlp::forward / backward through the host-buffer entry points (sxen_mlp_forward_host / _backward_host: the
+    reference's span signatures, include/sxen/mlp.hpp:94-99) against the device-pointer calls: same bits."""
+    mlp_h, mlp_d = sx.Mlp(tiny_mlp(sx, 8, 16, 2, 3)), sx.Mlp(tiny_mlp(sx, 8, 16, 2, 3))
+    mlp_h.init_params(41)
+    mlp_d.init_params(41)
+    x = torch.cat([random_input(sx, 8, 2000 + it) for it in range(37)])
+    up = np.linspace(-1.0, 1.0, 37 * 3).reshape(37, 3)
+    with pytest.raises(RuntimeError):                    # std::logic_error, before anything is copied
+        mlp_h.backward(up)
+    out_h = mlp_h.forward(x.cpu().numpy())
+    assert isinstance(out_h, np.ndarray) and np.array_equal(out_h.view(np.uint32), mlp_d.forward(x).cpu().numpy().view(np.uint32))
+    ig_h = mlp_h.backward(up)
+    ig_d = mlp_d.backward(dev(up)).cpu().numpy()
+    assert ig_h.dtype == np.float64 and np.array_equal(ig_h, ig_d)
+    gh, gd = mlp_h.gradient(), mlp_d.gradient()
+    assert (np.abs(gh - gd) <= 1e-12 * np.abs(gd) + 1e-300).all()
+    with pytest.raises(ValueError):
+        mlp_h.forward(np.zeros((2, 7), dtype=np.float32))
+    with pytest.raises(ValueError):
+        mlp_h.backward(np.zeros((36, 3)))                 # batch differs from the forward's
+    assert mlp_h.forward(np.zeros((0, 8), dtype=np.float32)).shape == (0, 3)

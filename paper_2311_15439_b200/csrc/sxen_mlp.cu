@@ -32,6 +32,9 @@ struct sxen_mlp {
   // tensor-core head: one row of parameter-gradient partial sums per CTA (sxen_mlp_tc2.cu), allocated at the first training launch
   double* tc_partials = nullptr;
   size_t tc_partial_stride = 0;
+  // host-span entry points (sxen_mlp_forward_host / _backward_host): grow-only staging, [0] = in, [1] = out
+  void* host_stage[2] = {nullptr, nullptr};
+  size_t host_stage_bytes[2] = {0, 0};
   int layer_count() const { return cfg.hidden_layers + 1; }
   int layer_in(int l) const { return l == 0 ? cfg.input_width : cfg.hidden_width; }
   int layer_out(int l) const { return l == layer_count() - 1 ? cfg.output_width : cfg.hidden_width; }
@@ -361,6 +364,8 @@ sxen_status sxen_mlp_destroy(sxen_mlp* mlp) {
   cudaFree(mlp->loss_scratch);
   cudaFree(mlp->grads_fixed);
   cudaFree(mlp->tc_partials);
+  cudaFree(mlp->host_stage[0]);
+  cudaFree(mlp->host_stage[1]);
   delete mlp;
   return SXEN_OK;
 }
@@ -612,13 +617,17 @@ sxen_status sxen_mlp_backward(sxen_mlp* mlp, const double* upstream_dev, size_t 
 
 // ---- the reference's own call shape: host spans in, host spans out (include/sxen/mlp.hpp:94-99), n samples per call
 namespace {
-struct DeviceScratch {  // a few short-lived device buffers, freed on every exit path
-  void* p[3] = {nullptr, nullptr, nullptr};
-  ~DeviceScratch() {
-    for (void* q : p)
-      if (q) cudaFree(q);
-  }
-};
+// grow-only device staging of the host-span calls (a per-sample caller would otherwise pay cudaMalloc + cudaFree per call)
+sxen_status host_stage(sxen_mlp* mlp, int which, size_t bytes) {
+  if (mlp->host_stage_bytes[which] >= bytes) return SXEN_OK;
+  cudaFree(mlp->host_stage[which]);
+  mlp->host_stage[which] = nullptr;
+  mlp->host_stage_bytes[which] = 0;
+  const size_t want = std::max<size_t>(bytes, 4096);
+  SXEN_CUDA(cudaMalloc(&mlp->host_stage[which], want));
+  mlp->host_stage_bytes[which] = want;
+  return SXEN_OK;
+}
 }  // namespace
 
 sxen_status sxen_mlp_forward_host(sxen_mlp* mlp, const float* input_host, size_t n_samples, float* out_host) {
@@ -628,13 +637,13 @@ sxen_status sxen_mlp_forward_host(sxen_mlp* mlp, const float* input_host, size_t
   if (n_samples == 0) return sxen_mlp_forward(mlp, nullptr, 0, nullptr, nullptr);
   const size_t in_bytes = n_samples * static_cast<size_t>(mlp->cfg.input_width) * sizeof(float);
   const size_t out_bytes = n_samples * static_cast<size_t>(mlp->cfg.output_width) * sizeof(float);
-  DeviceScratch d;
-  SXEN_CUDA(cudaMalloc(&d.p[0], in_bytes));
-  SXEN_CUDA(cudaMalloc(&d.p[1], out_bytes));
-  SXEN_CUDA(cudaMemcpy(d.p[0], input_host, in_bytes, cudaMemcpyHostToDevice));
-  if (sxen_status st = sxen_mlp_forward(mlp, static_cast<const float*>(d.p[0]), n_samples, static_cast<float*>(d.p[1]), nullptr))
+  if (sxen_status st = host_stage(mlp, 0, in_bytes)) return st;
+  if (sxen_status st = host_stage(mlp, 1, out_bytes)) return st;
+  SXEN_CUDA(cudaMemcpy(mlp->host_stage[0], input_host, in_bytes, cudaMemcpyHostToDevice));
+  if (sxen_status st = sxen_mlp_forward(mlp, static_cast<const float*>(mlp->host_stage[0]), n_samples,
+                                        static_cast<float*>(mlp->host_stage[1]), nullptr))
     return st;
-  SXEN_CUDA(cudaMemcpy(out_host, d.p[1], out_bytes, cudaMemcpyDeviceToHost));  // synchronises the legacy stream
+  SXEN_CUDA(cudaMemcpy(out_host, mlp->host_stage[1], out_bytes, cudaMemcpyDeviceToHost));  // synchronises the legacy stream
   return SXEN_OK;
 }
 
@@ -649,14 +658,13 @@ sxen_status sxen_mlp_backward_host(sxen_mlp* mlp, const double* upstream_host, s
   DeviceGuard guard(mlp->device);
   const size_t up_bytes = n_samples * static_cast<size_t>(mlp->cfg.output_width) * sizeof(double);
   const size_t ig_bytes = n_samples * static_cast<size_t>(mlp->cfg.input_width) * sizeof(double);
-  DeviceScratch d;
-  SXEN_CUDA(cudaMalloc(&d.p[0], up_bytes));
-  SXEN_CUDA(cudaMalloc(&d.p[1], ig_bytes));
-  SXEN_CUDA(cudaMemcpy(d.p[0], upstream_host, up_bytes, cudaMemcpyHostToDevice));
-  if (sxen_status st = sxen_mlp_backward(mlp, static_cast<const double*>(d.p[0]), n_samples, nullptr, static_cast<double*>(d.p[1]),
-                                         nullptr))
+  if (sxen_status st = host_stage(mlp, 0, up_bytes)) return st;
+  if (sxen_status st = host_stage(mlp, 1, ig_bytes)) return st;
+  SXEN_CUDA(cudaMemcpy(mlp->host_stage[0], upstream_host, up_bytes, cudaMemcpyHostToDevice));
+  if (sxen_status st = sxen_mlp_backward(mlp, static_cast<const double*>(mlp->host_stage[0]), n_samples, nullptr,
+                                         static_cast<double*>(mlp->host_stage[1]), nullptr))
     return st;
-  if (input_grad_host) SXEN_CUDA(cudaMemcpy(input_grad_host, d.p[1], ig_bytes, cudaMemcpyDeviceToHost));
+  if (input_grad_host) SXEN_CUDA(cudaMemcpy(input_grad_host, mlp->host_stage[1], ig_bytes, cudaMemcpyDeviceToHost));
   else SXEN_CUDA(cudaStreamSynchronize(nullptr));
   return SXEN_OK;
 }

@@ -511,14 +511,8 @@ SXEN_API sxen_status sxen_render_sq_error(const float* pred_dev, const double* i
                                           double* sum_dev, void* stream);
 
 /* ------------------------------------------------------------------ diagnostics (not part of the drop-in surface) */
-/* Hardware-convention probes behind tests/test_gpu_tc.py: ONE tcgen05.mma tile D[m x n] = A[m x k] * B[n x k]^T with bf16
- * (kind::f16) or tf32 operands staged in the kernels' own shared-memory layouts, the raw 128 TMEM lanes x n columns written to
- * raw_dev.  They pin what the tensor-core kernels rely on (self-dual CM16 tiles K-major and MN-major, the lane map of M = 64
- * accumulators, kind::tf32 returning zeros for MN-major operands on sm_100a). */
-SXEN_API sxen_status sxen_debug_tc_probe_bf16(const float* a_dev, const float* b_dev, int32_t m, int32_t n, int32_t k,
-                                              int32_t a_mn_major, int32_t b_mn_major, float* raw_dev);
-SXEN_API sxen_status sxen_debug_tc_probe(const float* a_dev, const float* b_dev, int32_t m, int32_t n, int32_t k,
-                                         int32_t a_mn_major, int32_t b_mn_major, int32_t swizzle128, float* raw_dev);
+/* (The tcgen05 hardware-convention probes of tests/test_gpu_tc.py are a test-only library, tests/cuda/sxen_tc_probe.cu; what
+ * stays here are hooks INSIDE the product kernels: watchdog words, cycle counters, the A/B switch of the two training kernels.) */
 /* The mbarrier waits of the tensor-core kernels trap after ~2 s instead of hanging the GPU; with two host-MAPPED words
  * registered here (NULL = off) the wait that gave up first notes its id and CTA in them (tools/mlp_watchdog_probe.py). */
 SXEN_API sxen_status sxen_debug_tc_progress(unsigned int* mapped_host_words);

@@ -169,8 +169,6 @@ SIGNATURES = {
     "sxen_trainer_set_fused": (C.c_int, [_vp, _i32]),
     "sxen_sample_test_image_batch": (C.c_int, [_u64, _i32, _i32, _u64, _u64, _sz, _sz, _vp, _vp, _vp]),
     "sxen_test_image_sq_error": (C.c_int, [_u64, _i32, _i32, _vp, _sz, _sz, _vp, _vp]),
-    "sxen_debug_tc_probe_bf16": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]),
-    "sxen_debug_tc_probe": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp]),
     "sxen_debug_tc_progress": (C.c_int, [_vp]),
     "sxen_debug_fused_timing": (C.c_int, [_vp]),
     "sxen_debug_tc_timing": (C.c_int, [_vp]),

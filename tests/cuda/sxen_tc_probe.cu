@@ -1,14 +1,22 @@
 // sxen_tc_probe.cu -- one tcgen05.mma on caller-supplied operands, raw TMEM dumped to global memory.
-// Test infrastructure for the tensor-core path (tests/test_gpu_tc.py): pins the shared-memory descriptor conventions of
+// Test infrastructure for the tensor-core path (tests/test_gpu_tc.py), built into its own library
+// (tests/cuda/_build/libsxen_tc_probe.so, `make -C paper_2311_15439_b200/csrc probe`), NOT into libsxen_b200.so: pins the shared-memory descriptor conventions of
 // sxen_tc.cuh (K-major and MN-major views of a core-matrix tile) and the TMEM lane mapping of M=128 and M=64
 // accumulators on real hardware before the MLP kernels rely on them.
 #include <cuda_bf16.h>
 
-#include "sxen_common.hpp"
-#include "sxen_tc.cuh"
+#include <cuda_runtime.h>
 
-using namespace sxen_host;
+#include <cstdint>
+
+#include "../../paper_2311_15439_b200/csrc/sxen_tc.cuh"
+
 using namespace sxen_tc;
+
+// 0 = ok, 1 = unsupported arguments, 2 = CUDA error (cudaGetErrorString(cudaGetLastError()) has the text).
+#define PROBE_API extern "C" __attribute__((visibility("default")))
+#define PROBE_CUDA(call) do { if ((call) != cudaSuccess) return 2; } while (0)
+#define PROBE_REQUIRE(cond, what) do { if (!(cond)) return 1; } while (0)
 
 namespace {
 
@@ -121,34 +129,32 @@ __global__ void __launch_bounds__(128) tc_probe_bf16_kernel(const float* __restr
 
 }  // namespace
 
-extern "C" SXEN_API sxen_status sxen_debug_tc_probe_bf16(const float* a_dev, const float* b_dev, int32_t m, int32_t n,
+PROBE_API int sxen_tc_probe_bf16(const float* a_dev, const float* b_dev, int32_t m, int32_t n,
                                                          int32_t k, int32_t a_mn_major, int32_t b_mn_major, float* raw_dev) {
-  SXEN_REQUIRE((m == 64 || m == 128) && n >= 8 && n <= 256 && n % 8 == 0 && k >= 16 && k % 16 == 0, "tc probe: unsupported shape");
+  PROBE_REQUIRE((m == 64 || m == 128) && n >= 8 && n <= 256 && n % 8 == 0 && k >= 16 && k % 16 == 0, "tc probe: unsupported shape");
   const size_t smem = ((static_cast<size_t>(m) * k * 2 + 1023) / 1024) * 1024 + static_cast<size_t>(n) * k * 2 + 1024;
-  SXEN_CUDA(cudaFuncSetAttribute(tc_probe_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  SXEN_CUDA(cudaMemset(raw_dev, 0, sizeof(float) * 128 * static_cast<size_t>(n)));
+  PROBE_CUDA(cudaFuncSetAttribute(tc_probe_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  PROBE_CUDA(cudaMemset(raw_dev, 0, sizeof(float) * 128 * static_cast<size_t>(n)));
   tc_probe_bf16_kernel<<<1, 128, smem>>>(a_dev, b_dev, m, n, k, a_mn_major, b_mn_major, raw_dev);
-  SXEN_CUDA(cudaGetLastError());
-  count_launch();
-  SXEN_CUDA(cudaDeviceSynchronize());
-  return SXEN_OK;
+  PROBE_CUDA(cudaGetLastError());
+  PROBE_CUDA(cudaDeviceSynchronize());
+  return 0;
 }
 
-extern "C" SXEN_API sxen_status sxen_debug_tc_probe(const float* a_dev, const float* b_dev, int32_t m, int32_t n, int32_t k,
+PROBE_API int sxen_tc_probe(const float* a_dev, const float* b_dev, int32_t m, int32_t n, int32_t k,
                                                     int32_t a_mn_major, int32_t b_mn_major, int32_t swizzle128, float* raw_dev) {
-  SXEN_REQUIRE((m == 64 || m == 128) && n >= 8 && n <= 256 && n % 8 == 0 && k >= 8 && k % 8 == 0, "tc probe: unsupported shape");
-  SXEN_REQUIRE(m % 8 == 0 && (m == 128 ? n % 16 == 0 : true), "tc probe: N must be a multiple of 16 for M=128");
+  PROBE_REQUIRE((m == 64 || m == 128) && n >= 8 && n <= 256 && n % 8 == 0 && k >= 8 && k % 8 == 0, "tc probe: unsupported shape");
+  PROBE_REQUIRE(m % 8 == 0 && (m == 128 ? n % 16 == 0 : true), "tc probe: N must be a multiple of 16 for M=128");
   const size_t smem = ((static_cast<size_t>(m) * k * 4 + 1023) / 1024) * 1024 + static_cast<size_t>(n) * k * 4 + 1024;
   if (swizzle128) {
     const int a_cols = a_mn_major ? m : k, b_cols = b_mn_major ? n : k;
-    SXEN_REQUIRE(a_cols % 32 == 0 && b_cols % 32 == 0, "tc probe: swizzled tiles need 32-element column blocks");
+    PROBE_REQUIRE(a_cols % 32 == 0 && b_cols % 32 == 0, "tc probe: swizzled tiles need 32-element column blocks");
   }
-  SXEN_REQUIRE(smem <= 200 * 1024, "tc probe: operands exceed shared memory");
-  SXEN_CUDA(cudaFuncSetAttribute(tc_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  SXEN_CUDA(cudaMemset(raw_dev, 0, sizeof(float) * 128 * static_cast<size_t>(n)));
+  PROBE_REQUIRE(smem <= 200 * 1024, "tc probe: operands exceed shared memory");
+  PROBE_CUDA(cudaFuncSetAttribute(tc_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  PROBE_CUDA(cudaMemset(raw_dev, 0, sizeof(float) * 128 * static_cast<size_t>(n)));
   tc_probe_kernel<<<1, 128, smem>>>(a_dev, b_dev, m, n, k, a_mn_major, b_mn_major, swizzle128, raw_dev);
-  SXEN_CUDA(cudaGetLastError());
-  count_launch();
-  SXEN_CUDA(cudaDeviceSynchronize());
-  return SXEN_OK;
+  PROBE_CUDA(cudaGetLastError());
+  PROBE_CUDA(cudaDeviceSynchronize());
+  return 0;
 }

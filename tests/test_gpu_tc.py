@@ -1,11 +1,12 @@
 """GPU (-m gpu): the tcgen05 tensor-core MLP head.
 
-1. Hardware conventions the kernel relies on, pinned with sxen_debug_tc_probe*: bf16 operands in the self-dual CM16 tile
+1. Hardware conventions the kernel relies on, pinned with tests/cuda/sxen_tc_probe.cu: bf16 operands in the self-dual CM16 tile
    work K-major and MN-major, M=64 accumulators keep row i in TMEM lane (i/16)*32 + i%16, and kind::tf32 accepts K-major
    operands only (MN-major silently yields zeros -- why the head runs on split bf16).
 2. Parity of the fused kernel against the oracle's fp64 MLP: split-bf16 (bf16x3) within TC3_RTOL of the largest magnitude
    in the compared array, single bf16 within TC1_RTOL."""
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -32,8 +33,13 @@ def dev(a):
     return torch.as_tensor(np.ascontiguousarray(a), device="cuda:0")
 
 
+PROBE_LIB = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cuda", "_build", "libsxen_tc_probe.so")
+
+
 def probe(sx, name, M, N, K, a_mn, b_mn, extra=()):
-    fn = getattr(sx.lib, name)
+    # test-only library (tests/cuda/sxen_tc_probe.cu, built by __graft_entry__.build()); not part of libsxen_b200.so
+    assert os.path.exists(PROBE_LIB), "run __graft_entry__.build() (make -C paper_2311_15439_b200/csrc probe)"
+    fn = getattr(C.CDLL(PROBE_LIB), name)
     fn.restype = C.c_int
     rng = np.random.default_rng(M * 1000 + N * 10 + K + a_mn * 2 + b_mn)
     A = rng.integers(-3, 4, size=(M, K)).astype(np.float32)
@@ -42,7 +48,7 @@ def probe(sx, name, M, N, K, a_mn, b_mn, extra=()):
     raw = torch.zeros((128, N), dtype=torch.float32, device="cuda:0")
     args = [C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()), C.c_int32(M), C.c_int32(N), C.c_int32(K), C.c_int32(a_mn),
             C.c_int32(b_mn)] + [C.c_int32(e) for e in extra] + [C.c_void_p(raw.data_ptr())]
-    assert fn(*args) == 0, sx.lib.sxen_last_error()
+    assert fn(*args) == 0, (name, M, N, K)
     R = raw.cpu().numpy()
     lanes = list(range(128)) if M == 128 else [(i // 16) * 32 + i % 16 for i in range(64)]
     return R[lanes], A @ B.T
@@ -51,11 +57,11 @@ def probe(sx, name, M, N, K, a_mn, b_mn, extra=()):
 def test_tcgen05_conventions(sx):
     for M, N, K, a_mn, b_mn in [(128, 64, 32, 0, 0), (128, 16, 64, 0, 0), (128, 64, 16, 0, 1), (128, 32, 64, 0, 1),
                                 (64, 16, 128, 1, 1), (64, 72, 128, 1, 1), (64, 40, 128, 1, 1)]:
-        got, want = probe(sx, "sxen_debug_tc_probe_bf16", M, N, K, a_mn, b_mn)
+        got, want = probe(sx, "sxen_tc_probe_bf16", M, N, K, a_mn, b_mn)
         assert np.array_equal(got, want), (M, N, K, a_mn, b_mn)
-    got, want = probe(sx, "sxen_debug_tc_probe", 128, 64, 32, 0, 0, extra=(0,))
+    got, want = probe(sx, "sxen_tc_probe", 128, 64, 32, 0, 0, extra=(0,))
     assert np.array_equal(got, want)  # tf32, K-major: fine
-    got, want = probe(sx, "sxen_debug_tc_probe", 128, 64, 16, 0, 1, extra=(0,))
+    got, want = probe(sx, "sxen_tc_probe", 128, 64, 16, 0, 1, extra=(0,))
     assert not got.any() and want.any()  # tf32, MN-major B: the tensor core returns zeros
 
 

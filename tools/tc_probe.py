@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""tools/tc_probe.py -- pin tcgen05 descriptor conventions and TMEM lane mapping on hardware (sxen_debug_tc_probe)."""
+"""tools/tc_probe.py -- pin tcgen05 descriptor conventions and TMEM lane mapping on hardware (tests/cuda/sxen_tc_probe.cu, the test-only probe library)."""
 import ctypes as C
 import os
 import sys
@@ -11,9 +11,9 @@ import torch  # noqa: E402
 
 import paper_2311_15439_b200 as sx  # noqa: E402
 
-lib = sx.lib
-lib.sxen_debug_tc_probe.restype = C.c_int
-lib.sxen_debug_tc_probe.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]
+lib = C.CDLL(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "cuda", "_build", "libsxen_tc_probe.so"))
+lib.sxen_tc_probe.restype = C.c_int
+lib.sxen_tc_probe.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]
 rng = np.random.default_rng(0)
 ok_all = True
 cases = [(128, 64, 32, 0, 0, 0), (128, 64, 16, 0, 1, 0), (64, 64, 128, 1, 1, 0), (64, 64, 32, 0, 0, 0),
@@ -25,9 +25,9 @@ for M, N, K, a_mn, b_mn, swz in cases:
     D = A @ B.T
     a, b = torch.as_tensor(A, device="cuda"), torch.as_tensor(B, device="cuda")
     raw = torch.zeros((128, N), dtype=torch.float32, device="cuda")
-    st = lib.sxen_debug_tc_probe(a.data_ptr(), b.data_ptr(), M, N, K, a_mn, b_mn, swz, raw.data_ptr())
+    st = lib.sxen_tc_probe(a.data_ptr(), b.data_ptr(), M, N, K, a_mn, b_mn, swz, raw.data_ptr())
     if st != 0:
-        print("probe failed:", lib.sxen_last_error().decode())
+        print("probe failed: status", st)
         ok_all = False
         continue
     R = raw.cpu().numpy()
@@ -51,8 +51,8 @@ for M, N, K, a_mn, b_mn, swz in cases:
         bad = np.argwhere(R != D)
         print("   first mismatches:", bad[:5].tolist(), R[tuple(bad[0])] if len(bad) else None, D[tuple(bad[0])] if len(bad) else None)
 print("---- bf16 (kind::f16), CM16 no-swizzle tiles")
-lib.sxen_debug_tc_probe_bf16.restype = C.c_int
-lib.sxen_debug_tc_probe_bf16.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]
+lib.sxen_tc_probe_bf16.restype = C.c_int
+lib.sxen_tc_probe_bf16.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]
 for M, N, K, a_mn, b_mn in [(128, 64, 32, 0, 0), (128, 64, 64, 0, 0), (128, 16, 64, 0, 0), (128, 64, 16, 0, 1), (128, 32, 64, 0, 1),
                             (128, 64, 128, 1, 1), (64, 64, 128, 1, 1), (64, 40, 128, 1, 1), (64, 16, 128, 1, 1), (64, 72, 128, 1, 1),
                             (64, 64, 32, 0, 0), (128, 64, 64, 1, 0)]:
@@ -61,9 +61,9 @@ for M, N, K, a_mn, b_mn in [(128, 64, 32, 0, 0), (128, 64, 64, 0, 0), (128, 16, 
     D = A @ B.T
     a, b = torch.as_tensor(A, device="cuda"), torch.as_tensor(B, device="cuda")
     raw = torch.zeros((128, N), dtype=torch.float32, device="cuda")
-    st = lib.sxen_debug_tc_probe_bf16(a.data_ptr(), b.data_ptr(), M, N, K, a_mn, b_mn, raw.data_ptr())
+    st = lib.sxen_tc_probe_bf16(a.data_ptr(), b.data_ptr(), M, N, K, a_mn, b_mn, raw.data_ptr())
     if st != 0:
-        print("probe failed:", lib.sxen_last_error().decode())
+        print("probe failed: status", st)
         continue
     R = raw.cpu().numpy()
     if M == 128:

@@ -319,7 +319,10 @@ struct ImageDataset {
 };
 
 // Head arithmetic of the fitted model; no reference analogue (the reference has one, fp64-accumulated path = exact).
-enum class MlpPrecision { exact = SXEN_MLP_EXACT, tensor_bf16x3 = SXEN_MLP_TENSOR_BF16X3, tensor_bf16 = SXEN_MLP_TENSOR_BF16 };
+enum class MlpPrecision {
+  exact = SXEN_MLP_EXACT, tensor_bf16x3 = SXEN_MLP_TENSOR_BF16X3, tensor_bf16 = SXEN_MLP_TENSOR_BF16,
+  tensor_bf16x4 = SXEN_MLP_TENSOR_BF16X4
+};
 
 // include/sxen/tasks.hpp:30-34
 struct FitImageOptions {

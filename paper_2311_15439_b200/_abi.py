@@ -14,7 +14,7 @@ OK, INVALID_ARGUMENT, LOGIC_ERROR, TRAINING_ERROR, CUDA_ERROR, IO_ERROR, NCCL_ER
 BACKEND_SIMPLEX, BACKEND_GRID = 0, 1
 SCALE_RAW, SCALE_EQUAL_MEMORY = 0, 1
 COORD_F64, COORD_F32 = 0, 1
-MLP_EXACT, MLP_TENSOR_BF16X3, MLP_TENSOR_BF16 = 0, 1, 2
+MLP_EXACT, MLP_TENSOR_BF16X3, MLP_TENSOR_BF16, MLP_TENSOR_BF16X4 = 0, 1, 2, 3
 
 
 class EncoderConfigC(C.Structure):

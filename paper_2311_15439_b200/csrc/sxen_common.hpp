@@ -46,6 +46,11 @@ struct DeviceGuard {
 
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+// sxen_mlp_precision -> the tensor-core kernels' `precise` argument (products per operand pair: 0 one, 1 three, 2 four)
+inline int sxen_tc_products(int precision) {
+  return precision == SXEN_MLP_TENSOR_BF16X3 ? 1 : precision == SXEN_MLP_TENSOR_BF16X4 ? 2 : 0;
+}
+
 }  // namespace sxen_host
 
 struct sxen_encoder {

@@ -433,7 +433,8 @@ sxen_status sxen_mlp_grad_download(const sxen_mlp* mlp, double* dst_host) {
 
 sxen_status sxen_mlp_set_precision(sxen_mlp* mlp, int32_t precision) {
   SXEN_REQUIRE(mlp != nullptr, "mlp handle is null");
-  SXEN_REQUIRE(precision == SXEN_MLP_EXACT || precision == SXEN_MLP_TENSOR_BF16X3 || precision == SXEN_MLP_TENSOR_BF16,
+  SXEN_REQUIRE(precision == SXEN_MLP_EXACT || precision == SXEN_MLP_TENSOR_BF16X3 || precision == SXEN_MLP_TENSOR_BF16 ||
+                   precision == SXEN_MLP_TENSOR_BF16X4,
                "mlp: unknown precision mode %d", precision);
   SXEN_REQUIRE(precision == SXEN_MLP_EXACT || sxen_mlp_tc_supported(mlp->cfg),
                "mlp: the tensor-core path covers input 16 or 32, hidden 64 x 2 layers, output <= 3; this head is %d/%d x %d/%d",
@@ -481,7 +482,7 @@ sxen_status sxen_mlp_forward_backward_ex(sxen_mlp* mlp, const float* input_dev, 
     }
     if (sxen_status s = sxen_mlp_tc_run(true, mlp->params, input_dev, targets_dev, target_type == SXEN_COORD_F32 ? 1 : 0, pred_dev,
                                         input_grad_dev, mlp->grads, loss, n_samples, mlp->cfg.input_width, mlp->cfg.output_width,
-                                        global_batch, mlp->precision == SXEN_MLP_TENSOR_BF16X3 ? 1 : 0, st, mlp->grads_fixed, &ctas,
+                                        global_batch, sxen_tc_products(mlp->precision), st, mlp->grads_fixed, &ctas,
                                         mlp->tc_partials, mlp->tc_partial_stride))
       return s;
     if (mlp->grads_fixed) {  // the CTAs' partial sums met in fixed point (order-free): fold them into the fp64 buffers
@@ -520,7 +521,7 @@ sxen_status sxen_mlp_forward(sxen_mlp* mlp, const float* input_dev, size_t n_sam
     SXEN_REQUIRE(n_samples == 0 || out_dev != nullptr, "mlp forward: output pointer is null");
     mlp->forward_done = false;
     return sxen_mlp_tc_run(false, mlp->params, input_dev, nullptr, 0, out_dev, nullptr, nullptr, nullptr, n_samples,
-                           mlp->cfg.input_width, mlp->cfg.output_width, 1, mlp->precision == SXEN_MLP_TENSOR_BF16X3 ? 1 : 0, as_stream(stream));
+                           mlp->cfg.input_width, mlp->cfg.output_width, 1, sxen_tc_products(mlp->precision), as_stream(stream));
   }
   mlp->forward_done = true;
   mlp->forward_samples = n_samples;

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
   __syncthreads();
   tc_fence_after();
   const uint32_t tb = tmem_base_slot;
-  const bool precise = a.precise != 0;
+  const int precise = a.precise;
   const unsigned long long n_tiles = (a.n + kTile - 1) / kTile;
   constexpr int kPhases = TRAIN ? 4 : 2;
   bool g_started = false;

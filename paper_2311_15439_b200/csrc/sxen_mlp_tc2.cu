@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp_tc2_kernel(const __grid_cons
     __syncthreads();
     tc_fence_after();
   }
-  const bool precise = a.precise != 0;
+  const int precise = a.precise;
   // Where the CTA's parameter gradients go.  148 CTAs adding to the same 6467 words serialise in L2 (the read-out at the end of
   // a 2^20-sample launch cost 4 % of the kernel, a mid-kernel flush 16 us): with `partials` every CTA owns a row, clears it here
   // and a reduction kernel adds the rows in a fixed order afterwards.

@@ -29,7 +29,7 @@ struct TcArgs {
   unsigned long long n;
   int out_w;
   int target_f32;
-  int precise;              // 1: bf16x3, 0: single bf16 product
+  int precise;              // 0: single bf16 product, 1: bf16x3, 2: bf16x4 (gemm_split)
   double upstream_scale;    // 2 / (global_batch * out_w)
   unsigned long long* timing;       // tuning aid (nullptr = off): {epilogue thread 0: cycles in the tile loop, of those waiting on the
                                     // chain, waiting on the weight-gradient MMAs; chain warp: loop cycles, waiting on the epilogue}
@@ -73,16 +73,29 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 
 // D += A*B over `ksteps` UMMA_K=16 steps with split operands.  a0/b0 are the descriptors of the hi tiles at k step 0;
 // the lo tile sits `a_lo`/`b_lo` bytes further and one k step adds `a_step`/`b_step` bytes (address field = bytes >> 4).
-__device__ __forceinline__ void gemm_split(uint32_t d, uint32_t idesc, int ksteps, bool accumulate, bool precise, uint64_t a0,
-                                           uint32_t a_lo, uint32_t a_step, uint64_t b0, uint32_t b_lo, uint32_t b_step) {
+// precise: 0 = one bf16 product; 1 = split operands, three products (hi*hi + hi*lo + lo*hi); 2 = the fourth product too
+// (lo*lo, <= 2^-18 of a term: SXEN_MLP_TENSOR_BF16X4 -- predictions and input gradients within 1e-5 of the largest magnitude at
+// +13 % kernel time, tools/tc_accuracy.py, profiles/r2s4_tc_lolo.log).
+// The product count is dispatched ONCE per GEMM (PRODUCTS is a template argument of the issue loop): a per-k-step test of a
+// run-time `precise` for the fourth product cost the default mode 5 % (0.303 -> 0.318 ms per 2^20 samples).
+template <int PRODUCTS>
+__device__ __forceinline__ void gemm_split_p(uint32_t d, uint32_t idesc, int ksteps, bool accumulate, uint64_t a0, uint32_t a_lo,
+                                             uint32_t a_step, uint64_t b0, uint32_t b_lo, uint32_t b_step) {
   for (int ks = 0; ks < ksteps; ++ks) {
     const uint64_t ah = a0 + ((static_cast<uint64_t>(ks) * a_step) >> 4), bh = b0 + ((static_cast<uint64_t>(ks) * b_step) >> 4);
     mma_bf16(d, ah, bh, idesc, accumulate || ks > 0);
-    if (precise) {
+    if constexpr (PRODUCTS >= 3) {
       mma_bf16(d, ah, bh + (b_lo >> 4), idesc, true);
       mma_bf16(d, ah + (a_lo >> 4), bh, idesc, true);
     }
+    if constexpr (PRODUCTS >= 4) mma_bf16(d, ah + (a_lo >> 4), bh + (b_lo >> 4), idesc, true);
   }
+}
+__device__ __forceinline__ void gemm_split(uint32_t d, uint32_t idesc, int ksteps, bool accumulate, int precise, uint64_t a0,
+                                           uint32_t a_lo, uint32_t a_step, uint64_t b0, uint32_t b_lo, uint32_t b_step) {
+  if (precise == 1) gemm_split_p<3>(d, idesc, ksteps, accumulate, a0, a_lo, a_step, b0, b_lo, b_step);
+  else if (precise == 0) gemm_split_p<1>(d, idesc, ksteps, accumulate, a0, a_lo, a_step, b0, b_lo, b_step);
+  else gemm_split_p<4>(d, idesc, ksteps, accumulate, a0, a_lo, a_step, b0, b_lo, b_step);
 }
 
 // The same GEMM issued from warp-uniform code: the whole warp walks the loop with warp-uniform operands (descriptors built from
@@ -97,18 +110,27 @@ __device__ __forceinline__ void mma_bf16_elect(uint32_t d_tmem, uint64_t a_desc,
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(static_cast<uint32_t>(accumulate)), "r"(static_cast<uint32_t>(leader))
       : "memory");
 }
-__device__ __forceinline__ void gemm_split_uniform(uint32_t d, uint32_t idesc, int ksteps, bool accumulate, bool precise, uint64_t a0,
-                                                   uint32_t a_lo, uint32_t a_step, uint64_t b0, uint32_t b_lo, uint32_t b_step,
-                                                   bool leader) {
+template <int PRODUCTS>
+__device__ __forceinline__ void gemm_split_uniform_p(uint32_t d, uint32_t idesc, int ksteps, bool accumulate, uint64_t a0,
+                                                     uint32_t a_lo, uint32_t a_step, uint64_t b0, uint32_t b_lo, uint32_t b_step,
+                                                     bool leader) {
 #pragma unroll
   for (int ks = 0; ks < ksteps; ++ks) {
     const uint64_t ah = a0 + ((static_cast<uint64_t>(ks) * a_step) >> 4), bh = b0 + ((static_cast<uint64_t>(ks) * b_step) >> 4);
     mma_bf16_elect(d, ah, bh, idesc, accumulate || ks > 0, leader);
-    if (precise) {
+    if constexpr (PRODUCTS >= 3) {
       mma_bf16_elect(d, ah, bh + (b_lo >> 4), idesc, true, leader);
       mma_bf16_elect(d, ah + (a_lo >> 4), bh, idesc, true, leader);
     }
+    if constexpr (PRODUCTS >= 4) mma_bf16_elect(d, ah + (a_lo >> 4), bh + (b_lo >> 4), idesc, true, leader);
   }
+}
+__device__ __forceinline__ void gemm_split_uniform(uint32_t d, uint32_t idesc, int ksteps, bool accumulate, int precise, uint64_t a0,
+                                                   uint32_t a_lo, uint32_t a_step, uint64_t b0, uint32_t b_lo, uint32_t b_step,
+                                                   bool leader) {
+  if (precise == 1) gemm_split_uniform_p<3>(d, idesc, ksteps, accumulate, a0, a_lo, a_step, b0, b_lo, b_step, leader);
+  else if (precise == 0) gemm_split_uniform_p<1>(d, idesc, ksteps, accumulate, a0, a_lo, a_step, b0, b_lo, b_step, leader);
+  else gemm_split_uniform_p<4>(d, idesc, ksteps, accumulate, a0, a_lo, a_step, b0, b_lo, b_step, leader);
 }
 
 // One CTA's partial sum into the batch total: an fp64 atomic, or -- reproducible mode -- an integer atomic on the fixed-point

@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
   __syncthreads();
   tc_fence_after();
   const uint32_t tb = tmem_base_slot;
-  const bool precise = a.precise != 0;
+  const int precise = a.precise;
   const unsigned long long n_tiles = (a.n + kTile - 1) / kTile;
   bool g_started = false;
 
@@ -141,6 +141,8 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
       const uint64_t kDH2d = desc16_k_major(sDH2, HID, 0), kDH1d = desc16_k_major(sDH1, HID, 0);
       const uint64_t mW0d = desc16_mn_major(sW0, IN, 0), mW1d = desc16_mn_major(sW1, HID, 0);
       constexpr uint32_t kStep = 256;
+      // (called with a CONSTANT parity only: with a run-time b and four products the second tile of a CTA came out at
+      // single-bf16 accuracy on hardware -- not root-caused, profiles/r2s4_tc_lolo.log)
       auto layer1 = [&](int b) {  // S0 = X0[b] * W0^T
         const uint64_t kX0d = desc16_k_major(smem_u32(smem + kX0 + b * kX0Bytes), X0C, 0);
         gemm_split(tb + tS0, make_idesc_bf16(128, HID, false, false), IN / 16, false, precise, kX0d, loX0, kStep, kW0d, loW0, kStep);
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
         wait_ready();  // layer 2: S1 = H1 * W1^T
         gemm_split(tb + tS1, make_idesc_bf16(128, HID, false, false), HID / 16, false, precise, kH1d, loH, kStep, kW1d, loW1, kStep);
         if constexpr (!TRAIN) {
-          if (has_next) layer1((k + 1) & 1);
+          if (has_next) { if ((k + 1) & 1) layer1(1); else layer1(0); }  // constant parities: see layer1
           tc_commit(&bar);
         } else {
           tc_commit(&bar);
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
           mbar_arrive(&bar_w);
           gemm_split(tb + tDX, make_idesc_bf16(128, IN, false, true), HID / 16, false, precise, kDH1d, loDH, kStep, mW0d, loW0,
                      2 * cm16_row_group_stride(IN));
-          if (has_next) layer1((k + 1) & 1);
+          if (has_next) { if ((k + 1) & 1) layer1(1); else layer1(0); }  // constant parities: see layer1
           tc_commit(&bar);
         }
       }

@@ -84,7 +84,7 @@ struct FusedArgs {
   long long* grad_fixed;    // reproducible MLP gradient: parameter layout in units of 2^-52, then one double per CTA (nullptr = off)
   int out_w;
   int target_f32;
-  int precise;              // 1: bf16x3, 0: single bf16 product
+  int precise;              // 0: single bf16 product, otherwise bf16x3
   double upstream_scale;    // 2 / (global_batch * out_w)
   unsigned long long* timing;  // nullptr, or 16 counters: per role {cycles in the tile loop, cycles of those spent waiting} (a tuning aid)
 };
@@ -140,7 +140,7 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[1
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-__device__ __forceinline__ void gemm_split(uint32_t d, uint32_t idesc, int ksteps, bool accumulate, bool precise, uint64_t a0,
+__device__ __forceinline__ void gemm_split(uint32_t d, uint32_t idesc, int ksteps, bool accumulate, int precise, uint64_t a0,
                                            uint32_t a_lo, uint32_t a_step, uint64_t b0, uint32_t b_lo, uint32_t b_step) {
   for (int ks = 0; ks < ksteps; ++ks) {
     const uint64_t ah = a0 + ((static_cast<uint64_t>(ks) * a_step) >> 4), bh = b0 + ((static_cast<uint64_t>(ks) * b_step) >> 4);
@@ -273,7 +273,7 @@ train_fused_kernel(const __grid_constant__ EncodeArgs e, const __grid_constant__
   __syncthreads();
   tc_fence_after();
   const uint32_t tb = tmem_base_slot;
-  const bool precise = a.precise != 0;
+  const int precise = a.precise != 0;  // this kernel issues three products in either split mode (BF16X4 = BF16X3 here)
   const unsigned long long n = e.n_samples;
   const unsigned long long n_tiles = (n + kTile - 1) / kTile;
   // tiles of this CTA: blockIdx.x, blockIdx.x + gridDim.x, ...; `k` counts them (buffer = k & 1)

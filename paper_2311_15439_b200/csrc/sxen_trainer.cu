@@ -318,7 +318,7 @@ static sxen_status accumulate_fused(sxen_trainer* t, const void* coords_dev, sxe
   int ctas = 0;
   if (sxen_status st = sxen_train_fused_run(e, ec.dim, params, targets_dev, target_type == SXEN_COORD_F32 ? 1 : 0, grads,
                                             t->loss_sum, fixed, t->out_w, global_batch,
-                                            precision == SXEN_MLP_TENSOR_BF16X3 ? 1 : 0, as_stream(stream), &ctas))
+                                            sxen_tc_products(precision), as_stream(stream), &ctas))
     return st;
   if (sxen_status st = sxen_mlp_fused_fold(t->mlp, t->loss_sum, ctas, stream)) return st;
   t->head_samples = 0;

@@ -4,7 +4,7 @@
    work K-major and MN-major, M=64 accumulators keep row i in TMEM lane (i/16)*32 + i%16, and kind::tf32 accepts K-major
    operands only (MN-major silently yields zeros -- why the head runs on split bf16).
 2. Parity of the fused kernel against the oracle's fp64 MLP: split-bf16 (bf16x3) within TC3_RTOL of the largest magnitude
-   in the compared array, single bf16 within TC1_RTOL."""
+   in the compared array, with the fourth product (bf16x4) within TC4_RTOL = 1e-5, single bf16 within TC1_RTOL."""
 import ctypes as C
 import os
 
@@ -17,6 +17,8 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 TC3_RTOL = 1.5e-5   # measured: predictions 6.2e-6 .. 1.1e-5 of the largest, input gradients 8e-6 at the 99.9th percentile (1e-5)
+TC4_RTOL = 1e-5     # SXEN_MLP_TENSOR_BF16X4 (fourth product): SURVEY 8c's bar; measured predictions 4.6e-6 .. 7.3e-6, input gradients
+                    # 4.3e-6 at the 99.9th percentile (profiles/r2s4_tc_lolo.log)
 TC3_SUM_RTOL = 3e-5   # parameter gradients: batch sums with cancellation, plus the odd ReLU flip (see the test)
 TC1_RTOL = 3e-2   # bf16: 2^-8 per operand
 
@@ -76,7 +78,7 @@ def make_case(oracle_lib, n, out_w, seed, in_w=32):
     return mc, p, inp, tgt
 
 
-@pytest.mark.parametrize("mode,rtol", [(1, TC3_RTOL), (2, TC1_RTOL)])
+@pytest.mark.parametrize("mode,rtol", [(1, TC3_RTOL), (2, TC1_RTOL), (3, TC4_RTOL)])
 @pytest.mark.parametrize("n,out_w,in_w", [(128 * 150 + 37, 3, 32), (500, 1, 32), (128 * 150 + 37, 3, 16), (700, 2, 16),
                                           (128 * 148 * 5 + 37, 3, 32), (128 * 148 * 4 + 1, 2, 16)])
 def test_tensor_core_mlp_matches_oracle(sx, oracle_lib, mode, rtol, n, out_w, in_w):
@@ -106,7 +108,7 @@ def test_tensor_core_mlp_matches_oracle(sx, oracle_lib, mode, rtol, n, out_w, in
     # ReLU than in fp64 (src/mlp.cpp:197 masks on the stored activation); that changes the sample's input gradient by a
     # whole weight column.  Such samples are rare: bound their share, and hold every other sample to the tolerance.
     bad = (np.abs(ig - wig) > 4 * rtol * np.abs(wig).max()).any(axis=1)
-    assert bad.mean() <= (2e-3 if mode == 1 else 0.25), bad.mean()
+    assert bad.mean() <= (2e-3 if mode != 2 else 0.25), bad.mean()
     g = mlp.gradient()
     # Parameter gradients: sums over the batch.  Besides the per-product rounding (rtol * sum |term|) a ReLU flip (see
     # above) moves one sample's whole contribution, so entries are held to the rounding bound plus a three-flip
@@ -118,12 +120,12 @@ def test_tensor_core_mlp_matches_oracle(sx, oracle_lib, mode, rtol, n, out_w, in
                   acts[:, in_w + 64:in_w + 128].astype(np.float64))
     d2 = (up @ W2) * (h2 > 0)
     d1 = (d2 @ W1) * (h1 > 0)
-    srtol = TC3_SUM_RTOL if mode == 1 else rtol
+    srtol = TC3_SUM_RTOL if mode != 2 else rtol
     off = 0
     for l, (delta, src) in enumerate([(d1, x0), (d2, h1), (up, h2)]):
         o_w, i_w = delta.shape[1], src.shape[1]
         wscale = np.abs(delta).T @ np.abs(src)
-        flip = 3 * np.abs(up).max() * np.abs(W2).max() * 64 * np.abs(W1).max() * np.abs(src).max() if mode == 1 else np.inf
+        flip = 3 * np.abs(up).max() * np.abs(W2).max() * 64 * np.abs(W1).max() * np.abs(src).max() if mode != 2 else np.inf
         blk, ref = g[off:off + o_w * i_w].reshape(o_w, i_w), wg[off:off + o_w * i_w].reshape(o_w, i_w)
         assert (np.abs(blk - ref) <= 2 * srtol * wscale + flip).all(), (l, "weights", np.abs(blk - ref).max())
         assert np.linalg.norm(blk - ref) <= 10 * srtol * np.linalg.norm(ref), (l, np.linalg.norm(blk - ref) / np.linalg.norm(ref))
@@ -178,7 +180,8 @@ def test_training_with_tensor_core_head_tracks_the_exact_head(sx):
 
 @pytest.mark.parametrize("n,in_w,out_w", [(1, 32, 3), (128 * 148 + 5, 32, 3), (128 * 148 * 3 + 77, 32, 1), (128 * 148 * 6, 16, 2),
                                           (128 * 148 * 7 + 129, 16, 3)])
-def test_both_training_kernels_agree(sx, n, in_w, out_w):
+@pytest.mark.parametrize("mode", [1, 3])
+def test_both_training_kernels_agree(sx, n, in_w, out_w, mode):
     """One tile in flight per SM (csrc/sxen_mlp_tc.cu) against two (csrc/sxen_mlp_tc2.cu, the default): the per-sample
     arithmetic is the same, so predictions, loss terms and input gradients agree bit for bit; the parameter gradients are
     fp32 sums over a CTA's tiles taken in a different grouping."""
@@ -191,7 +194,7 @@ def test_both_training_kernels_agree(sx, n, in_w, out_w):
             assert sx.lib.sxen_debug_tc_variant(variant) == 0
             mlp = sx.Mlp(sx.MlpConfig(in_w, 64, 2, out_w))
             mlp.init_params(11)
-            mlp.set_precision(1)
+            mlp.set_precision(mode)
             ig, loss, pred = mlp.forward_backward(x, tg, want_pred=True)
             torch.cuda.synchronize()
             res[variant] = (ig.cpu().numpy(), loss.item(), pred.cpu().numpy(), mlp.gradient())

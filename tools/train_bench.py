@@ -39,7 +39,7 @@ def timeit(fn, reps):
     return e0.elapsed_time(e1) / reps
 
 
-for mode, name in ((1, "tcgen05 bf16x3"), (2, "tcgen05 bf16"), (0, "exact fp64")):
+for mode, name in ((1, "tcgen05 bf16x3"), (3, "tcgen05 bf16x4"), (2, "tcgen05 bf16"), (0, "exact fp64")):
     mlp = sx.Mlp(sx.MlpConfig(32, 64, 2, 3))
     mlp.init_params(sx.hash_combine(42, 1))
     mlp.set_precision(mode)

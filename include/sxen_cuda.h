@@ -316,7 +316,7 @@ SXEN_API sxen_status sxen_mlp_backward_host(sxen_mlp* mlp, const double* upstrea
 /* Arithmetic of the head.  EXACT (default): fp64 accumulation in the reference's order, any shape, bit-identical outputs.
  * TENSOR_*: the fused tcgen05 kernel for the {16|32} -> 64 -> 64 -> {<=3} head; BF16X3 = split-bf16 operands (three MMAs per
  * product: predictions within 1.5e-5 of their largest magnitude, measured 6e-6 .. 1.1e-5), BF16X4 = the same with the fourth
- * (lo x lo) product: within 1e-5 (measured 4.6e-6 .. 7.3e-6) at +13 % kernel time, BF16 = single bf16 product (~4e-3). */
+ * (lo x lo) product: within 1e-5 (measured 4.6e-6 .. 7.3e-6) at +15 % kernel time, BF16 = single bf16 product (~4e-3). */
 typedef enum sxen_mlp_precision {
   SXEN_MLP_EXACT = 0, SXEN_MLP_TENSOR_BF16X3 = 1, SXEN_MLP_TENSOR_BF16 = 2, SXEN_MLP_TENSOR_BF16X4 = 3
 } sxen_mlp_precision;

@@ -75,7 +75,7 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 // the lo tile sits `a_lo`/`b_lo` bytes further and one k step adds `a_step`/`b_step` bytes (address field = bytes >> 4).
 // precise: 0 = one bf16 product; 1 = split operands, three products (hi*hi + hi*lo + lo*hi); 2 = the fourth product too
 // (lo*lo, <= 2^-18 of a term: SXEN_MLP_TENSOR_BF16X4 -- predictions and input gradients within 1e-5 of the largest magnitude at
-// +13 % kernel time, tools/tc_accuracy.py, profiles/r2s4_tc_lolo.log).
+// +15 % kernel time, tools/tc_accuracy.py, profiles/r2s4_tc_lolo.log).
 // The product count is dispatched ONCE per GEMM (PRODUCTS is a template argument of the issue loop): a per-k-step test of a
 // run-time `precise` for the fourth product cost the default mode 5 % (0.303 -> 0.318 ms per 2^20 samples).
 template <int PRODUCTS>

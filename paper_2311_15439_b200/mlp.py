@@ -126,7 +126,7 @@ class Mlp:
 
     def set_precision(self, mode: int) -> None:
         """0 = exact fp64-accumulate (default), 1 = tcgen05 split-bf16, three products (within 1.5e-5), 2 = tcgen05 single bf16
-        (~4e-3), 3 = split-bf16 with the fourth (lo x lo) product (within 1e-5, +13 % kernel time)."""
+        (~4e-3), 3 = split-bf16 with the fourth (lo x lo) product (within 1e-5, +15 % kernel time)."""
         raise_for(self._lib, self._lib.sxen_mlp_set_precision(self._h, int(mode)))
 
     def set_reproducible(self, on: bool = True) -> None:

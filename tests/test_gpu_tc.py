@@ -152,11 +152,11 @@ def test_tensor_core_path_rejects_other_shapes(sx):
 
 
 def test_training_with_tensor_core_head_tracks_the_exact_head(sx):
-    """Same seeds, same batches: loss curves of the bf16x3 head and of the exact head agree to 5e-3 over 40 steps
-    (1e-9 on the first step; Adam amplifies the 1e-5 arithmetic difference as training proceeds)."""
+    """Same seeds, same batches: loss curves of the bf16x3 / bf16x4 heads and of the exact head agree to 5e-3 over 40 steps
+    (1e-7 on the first step; Adam amplifies the 1e-5 arithmetic difference as training proceeds)."""
     cfg = sx.EncoderConfig(dim=2, levels=16, table_size=1 << 14, features=2, base_resolution=16, growth=1.3)
     curves = []
-    for mode in (0, 1):
+    for mode in (0, 1, 3):
         enc = sx.HashEncoder(cfg)
         enc.init_tables(42)
         mlp = sx.Mlp(sx.MlpConfig(32, 64, 2, 3))
@@ -172,10 +172,11 @@ def test_training_with_tensor_core_head_tracks_the_exact_head(sx):
 
         res = sx.train_field(enc, mlp, sampler, sx.TrainConfig(batch_size=4096, steps=40, record_every=1))
         curves.append(np.array([v for _, v in res.loss_curve]))
-    exact, tc = curves
+    exact = curves[0]
     assert exact[-1] < 0.5 * exact[0]
-    assert abs(tc[0] - exact[0]) <= 1e-7 * exact[0]
-    assert np.all(np.abs(tc - exact) <= 5e-3 * exact), (tc, exact)
+    for tc in curves[1:]:
+        assert abs(tc[0] - exact[0]) <= 1e-7 * exact[0]
+        assert np.all(np.abs(tc - exact) <= 5e-3 * exact), (tc, exact)
 
 
 @pytest.mark.parametrize("n,in_w,out_w", [(1, 32, 3), (128 * 148 + 5, 32, 3), (128 * 148 * 3 + 77, 32, 1), (128 * 148 * 6, 16, 2),

@@ -141,8 +141,9 @@ __global__ void __launch_bounds__(kThreadsAll, 1) mlp_tc_kernel(const __grid_con
       const uint64_t kDH2d = desc16_k_major(sDH2, HID, 0), kDH1d = desc16_k_major(sDH1, HID, 0);
       const uint64_t mW0d = desc16_mn_major(sW0, IN, 0), mW1d = desc16_mn_major(sW1, HID, 0);
       constexpr uint32_t kStep = 256;
-      // (called with a CONSTANT parity only: with a run-time b and four products the second tile of a CTA came out at
-      // single-bf16 accuracy on hardware -- not root-caused, profiles/r2s4_tc_lolo.log)
+      // (called with a CONSTANT parity only: with a run-time b and four products nvcc 12.9 loads the fourth MMA's B descriptor
+      // under a predicate that is not set on this path, the instruction repeats product three and the second tile of a CTA
+      // comes out 2^-9 off -- DESIGN.md 3.4)
       auto layer1 = [&](int b) {  // S0 = X0[b] * W0^T
         const uint64_t kX0d = desc16_k_major(smem_u32(smem + kX0 + b * kX0Bytes), X0C, 0);
         gemm_split(tb + tS0, make_idesc_bf16(128, HID, false, false), IN / 16, false, precise, kX0d, loX0, kStep, kW0d, loW0, kStep);
